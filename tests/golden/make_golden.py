@@ -1,0 +1,197 @@
+"""Generate the golden fixtures in tests/golden/ from the REFERENCE itself.
+
+Run in the build container (needs /root/reference):
+
+    python tests/golden/make_golden.py
+
+It imports the reference package from /root/reference/pkg/src and routes its
+max-flow seam to the reference's own compiled core (oracle/_ref, built from
+_core.pyx by oracle/build_oracle.py) exactly as the reference's benchmark
+swaps backends (pkg/benchmarks/bench_backends.py:42-44).  Outputs are small
+.npz files committed to the repo; nothing at test time reads /root/reference.
+
+Fixtures
+  bk_graphs.npz   random single graphs (test_backends.py:12-25 and
+                  test_maxflow.py:65-76 styles, plus integer lattices) with the
+                  reference's labels and flow values.
+  run_<case>.npz  full admm.run traces: per-iteration mu, energy, residual_sq,
+                  max_block_residual, clamped, block labels (packed bits), plus
+                  the final state.y, labels, multipliers, converged, iterations,
+                  best_iteration.  Config mapping of SURVEY.md §8(a):
+                  AdmmConfig(mu0=rho, mu_fact=1, eps=0, max_iters=N).
+"""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import dope  # noqa: E402  (the reference)
+import dope.admm as ref_admm  # noqa: E402
+import dope.maxflow as ref_maxflow  # noqa: E402
+from dope.energy import EnergyModel, SparseWeights  # noqa: E402
+from dope.grid import GridShape  # noqa: E402
+from dope.partition import make_partition  # noqa: E402
+
+import build_oracle  # noqa: E402
+from paper_1704_03116_b200 import workloads as W  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+def ref_core():
+    build_oracle.build_reference_core()
+    import oracle as orc  # noqa
+    core = orc.reference_core()
+    assert core is not None and core.BACKEND == "compiled"
+    return core
+
+
+def gen_bk(core):
+    rng = np.random.default_rng(20261019)
+    graphs = []
+    # test_backends.py:12-25 style (float caps, directed asymmetric)
+    for _ in range(150):
+        m = int(rng.integers(1, 40))
+        pairs = [(i, j) for i in range(m) for j in range(i + 1, m) if rng.random() < 0.25]
+        pi = np.array([p[0] for p in pairs], dtype=np.int32)
+        pj = np.array([p[1] for p in pairs], dtype=np.int32)
+        cij = rng.random(pi.size) * 3
+        cji = rng.random(pi.size) * 3
+        tcap = rng.uniform(-4, 4, m)
+        if rng.random() < 0.3:
+            tcap = np.round(tcap)
+        graphs.append((tcap, pi, pj, cij, cji))
+    # integer instances with many exact ties (tie-break pinning)
+    for _ in range(150):
+        m = int(rng.integers(1, 64))
+        pairs = [(i, j) for i in range(m) for j in range(i + 1, m) if rng.random() < 0.15]
+        pi = np.array([p[0] for p in pairs], dtype=np.int32)
+        pj = np.array([p[1] for p in pairs], dtype=np.int32)
+        c = rng.integers(0, 4, pi.size).astype(np.float64)
+        asym = rng.random() < 0.3
+        cji = rng.integers(0, 4, pi.size).astype(np.float64) if asym else c.copy()
+        tcap = rng.integers(-3, 4, m).astype(np.float64)
+        graphs.append((tcap, pi, pj, c, cji))
+    # small integer lattices (the block problems' shape)
+    for _ in range(40):
+        h, w = int(rng.integers(1, 12)), int(rng.integers(1, 12))
+        idx = np.arange(h * w).reshape(h, w)
+        pi = np.concatenate([idx[:, :-1].ravel(), idx[:-1, :].ravel()]).astype(np.int32)
+        pj = np.concatenate([idx[:, 1:].ravel(), idx[1:, :].ravel()]).astype(np.int32)
+        c = np.full(pi.size, float(rng.integers(1, 5)))
+        tcap = rng.integers(-8, 9, h * w).astype(np.float64)
+        graphs.append((tcap, pi, pj, c, c.copy()))
+    # empty graph and isolated nodes
+    graphs.append((np.zeros(0), np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0), np.zeros(0)))
+    graphs.append((np.array([0.0, -1.0, 2.0, 0.0]), np.zeros(0, np.int32), np.zeros(0, np.int32),
+                   np.zeros(0), np.zeros(0)))
+    labels, flows = [], []
+    for g in graphs:
+        lab, fl = core.bk_maxflow(g[0].copy(), *g[1:])
+        labels.append(np.asarray(lab, dtype=np.uint8))
+        flows.append(fl)
+    m_off = np.cumsum([0] + [g[0].size for g in graphs])
+    p_off = np.cumsum([0] + [g[1].size for g in graphs])
+    np.savez_compressed(
+        OUT / "bk_graphs.npz",
+        m_off=m_off, p_off=p_off,
+        tcap=np.concatenate([g[0] for g in graphs]),
+        pi=np.concatenate([g[1] for g in graphs]).astype(np.int32),
+        pj=np.concatenate([g[2] for g in graphs]).astype(np.int32),
+        cij=np.concatenate([g[3] for g in graphs]),
+        cji=np.concatenate([g[4] for g in graphs]),
+        labels=np.concatenate(labels), flows=np.array(flows))
+    print("bk_graphs:", len(graphs))
+
+
+def ref_run(wl: W.Workload, iters: int | None = None):
+    rows, cols, vals = wl.pair_arrays()
+    shape = GridShape(wl.dims)
+    model = EnergyModel(wl.u.astype(np.float64), SparseWeights(wl.n, rows, cols, vals), wl.lam)
+    part = make_partition(shape, wl.kpa, 0)
+    cfg = ref_admm.AdmmConfig(mu0=wl.rho, mu_fact=1.0, eps=0.0,
+                              max_iters=iters if iters else wl.iters)
+    hist = []
+    orig = ref_admm.update_blocks
+
+    def recording(state, problems, lam, config):
+        out = orig(state, problems, lam, config)
+        g = np.zeros(wl.n, dtype=np.uint8)
+        for b, lab in zip(part.blocks, state.block_labels):
+            g[b.pixels] = lab
+        hist.append(g)
+        return out
+
+    ref_admm.update_blocks = recording
+    try:
+        labels, state = ref_admm.run(model, part, cfg)
+    finally:
+        ref_admm.update_blocks = orig
+    a = np.zeros(wl.n)
+    for b, m in zip(part.blocks, state.multipliers):
+        a[b.pixels] = m
+    tr = state.trace
+    return dict(
+        mu=np.array([t.mu for t in tr]), energy=np.array([t.energy for t in tr]),
+        residual_sq=np.array([t.residual_sq for t in tr]),
+        max_block_residual=np.array([t.max_block_residual for t in tr]),
+        clamped=np.array([t.clamped for t in tr]),
+        yhat_bits=np.packbits(np.array(hist, dtype=np.uint8), axis=1),
+        y=state.y, labels=np.asarray(labels, dtype=np.int8), a=a,
+        converged=state.converged, iterations=state.iteration,
+        best_iteration=state.best_iteration)
+
+
+def save_run(case: str, wl: W.Workload, iters: int | None = None, store_u: bool = True):
+    r = ref_run(wl, iters)
+    meta = dict(dims=np.array(wl.dims), block=np.array(wl.block), conn=wl.conn, lam=wl.lam,
+                rho=wl.rho, max_iters=iters if iters else wl.iters, name=wl.name)
+    if store_u:
+        meta["u"] = wl.u
+    np.savez_compressed(OUT / f"run_{case}.npz", **r, **meta)
+    print(f"run_{case}: iters={r['iterations']} converged={r['converged']} "
+          f"best={r['best_iteration']} E_last={r['energy'][-1]}")
+
+
+class _RaggedWL(W.Workload):
+    @property
+    def kpa(self):
+        return self.meta["kpa"]
+
+
+def main():
+    core = ref_core()
+    ref_maxflow.bk_maxflow = core.bk_maxflow     # the reference's own seam swap
+    gen_bk(core)
+    save_run("c1", W.c1())
+    save_run("mini256", W.mini_disks(256, 64, 8, 2, 25, seed=1))
+    save_run("mini128_b16", W.mini_disks(128, 16, 6, 2, 20, seed=2, rmax=40.0))
+    save_run("mini256_b128", W.mini_disks(256, 128, 6, 2, 15, seed=3))
+    save_run("mini3d", W.c4(seed=4, size=64, block=32, iters=12))
+    rng = np.random.default_rng(7)
+    rag = _RaggedWL("ragged70x53", (70, 53), (0, 0), 4,
+                    rng.integers(-6, 7, (70, 53)).astype(np.int32).ravel(), [1, 1], 2.0, 1.0,
+                    12, True, meta={"kpa": (3, 4)})
+    r = ref_run(rag)
+    np.savez_compressed(OUT / "run_ragged.npz", **r, dims=np.array(rag.dims),
+                        kpa=np.array((3, 4)), conn=4, lam=2.0, rho=1.0, max_iters=12,
+                        name=rag.name, u=rag.u)
+    print("run_ragged:", r["iterations"], r["energy"][-1])
+    # early convergence (stop rule admm.py:305-307): one block converges at it 1
+    one = W.mini_disks(64, 64, 2, 1, 10, seed=5, rmax=20.0)
+    save_run("single_block", one)
+    # rho = 2 with lam*w = 2: lam/mu = 1 stays integral
+    r2 = W.mini_disks(128, 32, 4, 2, 15, seed=6, rmax=40.0)
+    r2.rho = 2.0
+    save_run("rho2", r2)
+
+
+if __name__ == "__main__":
+    main()
