@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark of the DOPE hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl b200|reference]
+
+A "step" is one complete ADMM run of the workload from init_state (C3: the
+4096^2 4-connected grid, 4096 sub-regions of 64^2, 100 iterations -- the grid
+BASELINE.json's north star targets), inputs resident in HBM.  value =
+ADMM iterations/s over the whole job; pixel-edges/s = E * iterations/s.
+Prints ONE JSON line on rank 0.
+
+--impl reference times the reference algorithm's CPU implementation (the
+oracle's C port of the reference loop, all host threads) on a bounded sample
+of the same workload -- the reference's own Python loop cannot leave the build
+container (it is reported in DESIGN.md instead).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BYTES_PER_PIXEL_ITER = 21      # read u,a,y (int32), write a,y, yhat (1 B)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default="C3")
+    p.add_argument("--iters", type=int, default=None, help="override ADMM iterations per run")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-iters", type=int, default=2)
+    p.add_argument("--no-graph", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self._proc = None
+            return
+        threading.Thread(target=self._read, daemon=True).start()
+
+    def _read(self):
+        for line in self._proc.stdout:
+            if self._stop.is_set():
+                break
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        self._stop.set()
+        if self._proc:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 7:
+                for nm, v in zip(names, r[3:7]):
+                    if v.strip().lower() in ("active", "1"):
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def build_problem(wl, device):
+    """Lower the workload (validation happens once, outside timing)."""
+    import paper_1704_03116_b200 as dope
+    rows, cols, vals = wl.pair_arrays()
+    model = dope.EnergyModel(wl.u.astype(np.float64), dope.SparseWeights(wl.n, rows, cols, vals),
+                             wl.lam)
+    del rows, cols, vals
+    part = dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0, materialize=False)
+    problems = dope.assemble_block_problems(model, part)
+    return model, part, problems
+
+
+def cpu_baseline(wl, iters: int):
+    """Oracle C port of the reference loop on the host cores (bounded sample)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as orc
+    threads = os.cpu_count() or 1
+    spec = orc.LatticeSpec(wl.dims, wl.kpa, wl.offsets, wl.weights, wl.u.astype(np.float64), wl.lam)
+    t0 = time.perf_counter()
+    out = orc.run(spec, wl.rho, 1.0, 0.0, iters, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": out["iterations"] / dt, "unit": "iterations/s", "cores": threads,
+            "kind": "port",
+            "sample": f"{wl.name}: first {out['iterations']} ADMM iterations from init_state "
+                      f"(oracle C port of admm.run + BK, {threads} threads), {dt:.1f} s"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1704_03116_b200 import workloads as W
+    wl = W.by_name(args.config)
+    iters = max(1, args.cpu_sample_iters)
+    vals = []
+    for s in range(args.warmup + args.steps):
+        r = cpu_baseline(wl, iters)
+        if s >= args.warmup:
+            vals.append(r["value"])
+    v = statistics.mean(vals)
+    line = {"metric": "ADMM iterations/s", "value": v, "unit": "iterations/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * iters / v,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{wl.name} {wl.dims[0]}x{wl.dims[1]} 4-conn, "
+                                   f"{wl.num_blocks} sub-regions of {wl.block[0]}x{wl.block[1]}; "
+                                   f"each step = first {iters} iterations",
+                       "pixel_edges_per_s": v * wl.num_pairs},
+            "cpu_baseline": {**r, "value": v},
+            "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    from paper_1704_03116_b200 import workloads as W
+    from paper_1704_03116_b200.admm import _DeviceState
+    wl = W.by_name(args.config, seed=rank if ws > 1 else 0)
+    iters = args.iters or wl.iters
+    model, part, problems = build_problem(wl, torch.device("cuda", local))
+    dev = _DeviceState(problems, int(wl.rho), 0.0, iters, True, True)
+    use_graph = int(not args.no_graph)
+
+    def step():
+        dev.call("dope_admm_init")
+        dev.call("dope_admm_run", iters, use_graph, fuse=1)
+        dev.call("dope_finish_run")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    rs = dev.raise_on_error()
+    iters_done = rs.iteration
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    for _ in range(args.steps):
+        step()
+    t_end.record()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    sampler.stop()
+    ms = t_start.elapsed_time(t_end)
+    rs = dev.raise_on_error()
+    assert rs.iteration == iters_done
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_iters = iters_done * args.steps * ws
+    value = total_iters / (ms / 1e3)
+    solves_per_run = rs.solves
+    sweeps_per_run = rs.sweeps
+
+    # ---- per-kernel timing pass (CUDA events on the launching stream) ----
+    evs = {"K1_block_mincut": [], "K2_consensus": [], "K3_finalize": []}
+    dev.call("dope_admm_init")
+    stream = torch.cuda.current_stream()
+    for it in range(iters_done):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e[0].record(stream)
+        dev.call("dope_update_blocks")
+        e[1].record(stream)
+        dev.call("dope_update_global", fuse=1)
+        e[2].record(stream)
+        dev.call("dope_reduce_finalize")
+        e[3].record(stream)
+        evs["K1_block_mincut"].append((e[0], e[1]))
+        evs["K2_consensus"].append((e[1], e[2]))
+        evs["K3_finalize"].append((e[2], e[3]))
+    torch.cuda.synchronize()
+    kern = {k: [a.elapsed_time(b) for a, b in v] for k, v in evs.items()}
+    kstat = {k: {"total_ms": sum(v), "avg_ms": sum(v) / len(v), "launches": len(v)}
+             for k, v in kern.items()}
+    dom = max(kstat, key=lambda k: kstat[k]["total_ms"])
+    peak, peak_kind = measured_peaks()
+    n = wl.n
+    if dom == "K2_consensus":
+        alg_bytes = BYTES_PER_PIXEL_ITER * n
+    elif dom == "K1_block_mincut":
+        # per solved block: read u,a,y (12 B/px), write yhat (1), residual graph r/w (8)
+        alg_bytes = (12 + 1 + 8) * (n / wl.num_blocks) * (solves_per_run / iters_done)
+    else:
+        alg_bytes = 20.0 * wl.num_blocks
+    achieved = alg_bytes / (kstat[dom]["avg_ms"] / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "kernel": dom,
+            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+            "algorithmic_bytes_per_launch": alg_bytes}
+    iter_bytes = BYTES_PER_PIXEL_ITER * n
+    iter_roof = {"bytes_per_iteration": iter_bytes,
+                 "achieved_GBps": iter_bytes * (value / ws) / 1e9,
+                 "frac_of_measured_hbm": iter_bytes * (value / ws) / 1e9 / peak}
+
+    # ---- e2e through the C ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        u_host = torch.from_numpy(wl.u.astype(np.int32)).pin_memory()
+        lab_host = torch.empty(n, dtype=torch.int8).pin_memory()
+        tr_host = torch.empty(iters, dtype=torch.int64).pin_memory()
+        for s in range(args.warmup + args.steps):
+            if s == args.warmup:
+                torch.cuda.synchronize()
+                if ws > 1:
+                    dist.barrier()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+            problems.u.copy_(u_host, non_blocking=True)
+            step()
+            lab_host.copy_((dev.y2 >= 1).to(torch.int8), non_blocking=True)
+            tr_host.copy_(dev.tr_e, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ms_e2e = e0.elapsed_time(e1)
+        if ws > 1:
+            t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        e2e = {"value": iters_done * args.steps * ws / (ms_e2e / 1e3), "unit": "iterations/s",
+               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": n + 8 * iters}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, args.cpu_sample_iters)
+
+    if rank == 0:
+        line = {
+            "metric": "ADMM iterations/s", "value": value, "unit": "iterations/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"{wl.name}: {wl.dims[0]}x{wl.dims[1]} 4-connected Potts, "
+                                   f"{wl.num_blocks} sub-regions of {wl.block[0]}x{wl.block[1]}, "
+                                   f"{iters_done} ADMM iterations per step (full run from init)",
+                       "pixel_edges_per_s": value * wl.num_pairs,
+                       "l2": "state ~0.4 GB > 126 MB L2 (inputs larger than L2)",
+                       "parallelism": f"{ws} replica(s)" if ws > 1 else "1 GPU",
+                       "block_solves_per_run": solves_per_run,
+                       "push_relabel_sweeps_per_run": sweeps_per_run,
+                       "kernels": kstat},
+            "roofline": roof, "iteration_roofline": iter_roof,
+            "clocks": sampler.summary(), "gpu_launches": 3 * iters * args.steps + 2 * args.steps,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,161 @@
+/*
+ * dope_b200.h -- C ABI of the B200-native DOPE hot path.
+ *
+ * Drop-in boundary for the reference's two seams:
+ *
+ *   Seam 1 (per graph) replaces the kernel-backend function
+ *     bk_maxflow(tcap, pair_i, pair_j, cap_ij, cap_ji) -> (labels, flow)
+ *     /root/reference/pkg/src/dope/_core.pyx:263-333 (contract
+ *     _core_py.py:25-35; bound by name at maxflow.py:14 via _kernels.py:19-21)
+ *     -> dope_bk_maxflow().
+ *
+ *   Seam 2 (batched, one CTA per sub-region) replaces the per-iteration step
+ *   functions of admm.py:
+ *     update_blocks      admm.py:171-191  (+ blockform.block_objective
+ *                        blockform.py:257-273, maxflow.solve_binary
+ *                        maxflow.py:423-425)            -> dope_update_blocks()
+ *     update_global      admm.py:230-238  (solve_global admm.py:194-209)
+ *     update_multipliers admm.py:241-248
+ *     block_residuals    admm.py:251-257
+ *     evaluate_energy    energy.py:187-194              -> dope_update_global()
+ *     run bookkeeping    admm.py:283-310 (trace, best, stop)
+ *                                                       -> dope_reduce_finalize()
+ *     run                admm.py:265-310                -> dope_admm_run()
+ *
+ * Conventions
+ *   - Plain pointers and sizes; no framework types.  Device pointers are
+ *     caller-owned (the Python host allocates them with torch); the library
+ *     allocates nothing persistent.  `stream` is a cudaStream_t passed as
+ *     void*; every call is asynchronous on it.
+ *   - Return codes: 0 ok; < 0 invalid arguments / unsupported geometry
+ *     (see DOPE_E_*); > 0 never returned by launch calls -- solver failures
+ *     are reported on the device in dope_run_state.error as 1 + block id
+ *     (the reference's BlockSolveError(block_id), admm.py:85-90).
+ *   - Integer lattice path: grid coordinates row-major (GridShape.strides,
+ *     grid.py:46-52), block ids row-major over the block lattice
+ *     (partition.py:103), non-overlapping near-equal box tiling
+ *     (partition.py:62-77 with overlap 0).  All per-pixel arrays are global
+ *     row-major so they compare elementwise with the reference's vectors.
+ */
+#ifndef DOPE_B200_H
+#define DOPE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DOPE_ABI_VERSION 1
+
+#define DOPE_OK 0
+#define DOPE_E_ARGS (-1)        /* null pointer / bad size */
+#define DOPE_E_GEOMETRY (-2)    /* no kernel variant for this block box */
+#define DOPE_E_CAPACITY (-3)    /* capacities exceed the int8 residual range */
+#define DOPE_E_CUDA (-4)        /* a CUDA launch failed (see dope_last_cuda_error) */
+#define DOPE_E_NONSUBMODULAR (-5)
+
+/* Device-resident run bookkeeping (one per run; caller allocates
+ * sizeof(dope_run_state) bytes of device memory, 8-byte aligned). */
+typedef struct dope_run_state {
+    int64_t best_energy;        /* scaled energy of the best iterate so far   */
+    int32_t iteration;          /* iterations completed                        */
+    int32_t best_iteration;     /* admm.py:300-303 (strict <)                  */
+    int32_t converged;          /* admm.py:305-307                             */
+    int32_t stop;               /* converged or error: later launches no-op    */
+    int32_t copy_best_pending;  /* last iteration set a new best; the next
+                                   consensus pass copies y into ybest          */
+    int32_t parity;             /* which multiplier buffer is current          */
+    int32_t error;              /* 0 or 1 + first failing block id             */
+    int32_t max_rounds_seen;    /* diagnostics: max global-relabel rounds      */
+    int64_t solves;             /* diagnostics: block solves performed         */
+    int64_t sweeps;             /* diagnostics: push/relabel sweeps            */
+} dope_run_state;
+
+/* Integer lattice problem (C1, C3, C4, C5 of BASELINE.json).
+ * Scaling: all quantities that are half-integers in the reference are held
+ * doubled: y2 = 2*y (y = 1/2 at init, {0,1} afterwards), block terminal
+ * capacity 2*linear, pair capacity 2*lambda*w.  Energies are exact integers. */
+typedef struct dope_lattice {
+    int32_t ndim;               /* 2 or 3                                     */
+    int32_t conn;               /* 4 (2D) or 6 (3D)                           */
+    int64_t dims[3];            /* row-major grid extents (unused axes = 1)   */
+    int32_t kpa[3];             /* blocks per axis (make_partition)           */
+    int32_t lamw;               /* lambda * w, integer, constant over pairs   */
+    int32_t mu;                 /* ADMM penalty, integer; lamw % mu == 0      */
+    double eps;                 /* stop when max block residual <= eps        */
+    int32_t max_iters;          /* trace capacity                             */
+    int32_t warm_start;         /* 1: reuse each block's residual graph       */
+    int32_t skip_clean;         /* 1: re-solve only blocks whose linear term
+                                   may have changed (exact)    */
+    int32_t fuse_multipliers;   /* 1: dope_update_global also does
+                                   update_multipliers (the run loop)          */
+    /* caller-owned device buffers */
+    const int32_t *u;           /* n   unary                                  */
+    int32_t *a[2];              /* n   multipliers, ping-pong by state.parity */
+    int32_t *y2;                /* n   2*y                                    */
+    int32_t *ybest;             /* n   2*y of the best iterate                */
+    uint8_t *yhat;              /* n   block labels (global layout)           */
+    uint8_t *resid;             /* K * resid_stride bytes: residual graphs    */
+    uint32_t *dirty;            /* K   block needs a re-solve                 */
+    int64_t *part_energy;       /* K   per-block energy partials              */
+    int64_t *part_ressq;        /* K   per-block sum (yhat - y)^2             */
+    int32_t *part_flags;        /* K   bit0: clamped                          */
+    dope_run_state *state;      /* 1                                          */
+    int64_t *trace_energy;      /* max_iters                                  */
+    double *trace_residual_sq;  /* max_iters                                  */
+    double *trace_max_residual; /* max_iters                                  */
+    int32_t *trace_clamped;     /* max_iters                                  */
+} dope_lattice;
+
+/* Library / ABI identification; "b200-sm100a". */
+const char *dope_backend_name(void);
+int dope_abi_version(void);
+const char *dope_last_cuda_error(void);
+
+/* Bytes of residual state per block for this geometry (0 if unsupported). */
+int64_t dope_resid_stride(const dope_lattice *L);
+/* Validate geometry / capacities; 0 or DOPE_E_*. */
+int dope_lattice_check(const dope_lattice *L);
+
+/* init_state (admm.py:160-168): y = 1/2, a = 0, yhat = 0, every block dirty,
+ * cold residual graphs, run state reset. */
+int dope_admm_init(const dope_lattice *L, void *stream);
+/* update_blocks: one CTA per sub-region computes 2*linear from (u, a, y,
+ * y-halo) and solves the block min cut on the GPU; yhat = sink side. */
+int dope_update_blocks(const dope_lattice *L, void *stream);
+/* update_global + block_residuals + energy partials (+ update_multipliers
+ * when fuse_multipliers); marks next iteration's dirty blocks. */
+int dope_update_global(const dope_lattice *L, void *stream);
+/* update_multipliers alone (a += yhat - y) for the step-level API. */
+int dope_update_multipliers(const dope_lattice *L, void *stream);
+/* Reduce partials, append the trace entry, track the best iterate, test
+ * convergence, advance the iteration counter. */
+int dope_reduce_finalize(const dope_lattice *L, void *stream);
+/* `iters` iterations of blocks -> global -> reduce (no host sync); launches
+ * become no-ops once converged.  use_graph: capture one iteration in a CUDA
+ * graph and replay it. */
+int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void *stream);
+/* End of run (admm.py:308-310): if not converged, y2 <- ybest. */
+int dope_finish_run(const dope_lattice *L, void *stream);
+/* evaluate_energy of an arbitrary doubled labeling y2 (int path):
+ * out[0] = sum u*y2 * 2 + lamw * sum (y2_i - y2_j)^2, i.e. 4*E (exact). */
+int dope_energy4(const dope_lattice *L, const int32_t *y2, int64_t *out, void *stream);
+
+/* Seam 1: general two-terminal graph, float64 capacities with the
+ * reference's EPS = 1e-12 saturation rule (_core.pyx:13).  Device pointers;
+ * m nodes, npairs pairs (arc 2p: i->j with cap_ij[p], arc 2p+1: j->i with
+ * cap_ji[p], _core.pyx:293-297).  labels[i] = 1 iff node i reaches the sink
+ * in the final residual graph (== the reference's sink tree); flow[0]
+ * receives the max-flow value.  Inputs are not modified (_core.pyx:269).
+ * `workspace` must hold dope_bk_workspace_bytes(m, npairs) bytes. */
+int dope_bk_maxflow(int32_t m, const double *tcap, int64_t npairs, const int32_t *pair_i,
+                    const int32_t *pair_j, const double *cap_ij, const double *cap_ji,
+                    uint8_t *labels, double *flow, void *workspace, int64_t workspace_bytes,
+                    void *stream);
+int64_t dope_bk_workspace_bytes(int32_t m, int64_t npairs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DOPE_B200_H */

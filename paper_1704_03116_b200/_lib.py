@@ -1,0 +1,132 @@
+"""ctypes binding of include/dope_b200.h (the C ABI of libdope_b200.so).
+
+The library is REQUIRED: there is no CPU fallback.  Loading fails loudly when
+the .so is missing or was built against a different ABI version.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libdope_b200.so"
+ABI_VERSION = 1
+
+DOPE_OK = 0
+DOPE_E_ARGS = -1
+DOPE_E_GEOMETRY = -2
+DOPE_E_CAPACITY = -3
+DOPE_E_CUDA = -4
+DOPE_E_NONSUBMODULAR = -5
+
+
+class RunState(C.Structure):
+    """Mirror of dope_run_state."""
+    _fields_ = [
+        ("best_energy", C.c_int64),
+        ("iteration", C.c_int32),
+        ("best_iteration", C.c_int32),
+        ("converged", C.c_int32),
+        ("stop", C.c_int32),
+        ("copy_best_pending", C.c_int32),
+        ("parity", C.c_int32),
+        ("error", C.c_int32),
+        ("max_rounds_seen", C.c_int32),
+        ("solves", C.c_int64),
+        ("sweeps", C.c_int64),
+    ]
+
+
+class Lattice(C.Structure):
+    """Mirror of dope_lattice."""
+    _fields_ = [
+        ("ndim", C.c_int32),
+        ("conn", C.c_int32),
+        ("dims", C.c_int64 * 3),
+        ("kpa", C.c_int32 * 3),
+        ("lamw", C.c_int32),
+        ("mu", C.c_int32),
+        ("eps", C.c_double),
+        ("max_iters", C.c_int32),
+        ("warm_start", C.c_int32),
+        ("skip_clean", C.c_int32),
+        ("fuse_multipliers", C.c_int32),
+        ("u", C.c_void_p),
+        ("a", C.c_void_p * 2),
+        ("y2", C.c_void_p),
+        ("ybest", C.c_void_p),
+        ("yhat", C.c_void_p),
+        ("resid", C.c_void_p),
+        ("dirty", C.c_void_p),
+        ("part_energy", C.c_void_p),
+        ("part_ressq", C.c_void_p),
+        ("part_flags", C.c_void_p),
+        ("state", C.c_void_p),
+        ("trace_energy", C.c_void_p),
+        ("trace_residual_sq", C.c_void_p),
+        ("trace_max_residual", C.c_void_p),
+        ("trace_clamped", C.c_void_p),
+    ]
+
+
+class DopeError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    """Load libdope_b200.so (raises if absent -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise DopeError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_1704_03116_b200.build` "
+            "(the DOPE B200 path has no CPU fallback)")
+    lb = C.CDLL(str(LIB_PATH))
+    lb.dope_backend_name.restype = C.c_char_p
+    lb.dope_abi_version.restype = C.c_int
+    lb.dope_last_cuda_error.restype = C.c_char_p
+    P = C.POINTER(Lattice)
+    lb.dope_resid_stride.restype = C.c_int64
+    lb.dope_resid_stride.argtypes = [P]
+    lb.dope_lattice_check.restype = C.c_int
+    lb.dope_lattice_check.argtypes = [P]
+    for name in ("dope_admm_init", "dope_update_blocks", "dope_update_global",
+                 "dope_update_multipliers", "dope_reduce_finalize", "dope_finish_run"):
+        f = getattr(lb, name)
+        f.restype = C.c_int
+        f.argtypes = [P, C.c_void_p]
+    lb.dope_admm_run.restype = C.c_int
+    lb.dope_admm_run.argtypes = [P, C.c_int32, C.c_int32, C.c_void_p]
+    lb.dope_energy4.restype = C.c_int
+    lb.dope_energy4.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p]
+    lb.dope_bk_maxflow.restype = C.c_int
+    lb.dope_bk_maxflow.argtypes = [C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_int64, C.c_void_p]
+    lb.dope_bk_workspace_bytes.restype = C.c_int64
+    lb.dope_bk_workspace_bytes.argtypes = [C.c_int32, C.c_int64]
+    if lb.dope_abi_version() != ABI_VERSION:
+        raise DopeError(f"libdope_b200 ABI {lb.dope_abi_version()} != {ABI_VERSION}")
+    _lib = lb
+    return lb
+
+
+def check(rc: int, what: str) -> None:
+    if rc == DOPE_OK:
+        return
+    msg = {DOPE_E_ARGS: "invalid arguments", DOPE_E_GEOMETRY: "unsupported block geometry",
+           DOPE_E_CAPACITY: "capacities exceed the int8 residual range",
+           DOPE_E_NONSUBMODULAR: "negative pairwise weights"}.get(rc)
+    if rc == DOPE_E_CUDA:
+        msg = "CUDA error: " + lib().dope_last_cuda_error().decode()
+    raise DopeError(f"{what} failed ({rc}): {msg}")
+
+
+def exported_symbols() -> list[str]:
+    return ["dope_backend_name", "dope_abi_version", "dope_last_cuda_error", "dope_resid_stride",
+            "dope_lattice_check", "dope_admm_init", "dope_update_blocks", "dope_update_global",
+            "dope_update_multipliers", "dope_reduce_finalize", "dope_admm_run",
+            "dope_finish_run", "dope_energy4", "dope_bk_maxflow", "dope_bk_workspace_bytes"]

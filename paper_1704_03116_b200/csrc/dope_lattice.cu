@@ -1,0 +1,992 @@
+// dope_lattice.cu -- B200 (sm_100a) kernels for DOPE's ADMM hot path on
+// integer lattice models, behind the C ABI of include/dope_b200.h.
+//
+//   K1 k_block_mincut   one CTA per sub-region.  Prologue computes the block
+//                       objective (blockform.py:257-273 collapsed to the q==1
+//                       stencil) straight from u, a, y and the y-halo; the
+//                       block's residual graph lives in shared memory; exact
+//                       integer push-relabel with a warp-level bit-parallel
+//                       global relabel (ballot-built masks, shfl word shifts);
+//                       labels = nodes that reach the sink in the final
+//                       residual graph (= the reference's sink tree,
+//                       _core.pyx:257-259; see DESIGN.md for the proof that
+//                       this set is unique, hence bit-exact).
+//   K2 k_consensus      one CTA per sub-region: solve_global + clamp
+//                       (admm.py:194-238), update_multipliers (admm.py:241-248),
+//                       block residual partials (admm.py:251-257), energy
+//                       partials (energy.py:187-194), next-iteration dirty
+//                       blocks, best-iterate copy.
+//   K3 k_finalize       one CTA: deterministic reduction of the partials, trace
+//                       record, best iterate (strict <), stop rule
+//                       (admm.py:283-307).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "dope_b200.h"
+
+#define FULLMASK 0xffffffffu
+
+namespace dope {
+
+constexpr uint16_t HINF = 0xFFFF;
+
+static thread_local char g_last_err[256] = "";
+
+static int cuda_check(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return DOPE_OK;
+    snprintf(g_last_err, sizeof(g_last_err), "%s: %s", what, cudaGetErrorString(e));
+    return DOPE_E_CUDA;
+}
+
+// ---------------------------------------------------------------------------
+// Geometry helpers (partition.py:62-77 with overlap 0)
+// ---------------------------------------------------------------------------
+
+struct Axis {
+    int32_t dim, k, base, rem;
+    __host__ __device__ void range(int32_t r, int32_t &lo, int32_t &len) const {
+        lo = r * base + (r < rem ? r : rem);
+        len = base + (r < rem ? 1 : 0);
+    }
+    __host__ __device__ int32_t owner(int32_t c) const {
+        int32_t big = rem * (base + 1);
+        return c < big ? c / (base + 1) : rem + (c - big) / base;
+    }
+};
+
+__host__ __device__ inline Axis make_axis(int64_t dim, int32_t k) {
+    Axis a;
+    a.dim = (int32_t)dim;
+    a.k = k;
+    a.base = (int32_t)(dim / k);
+    a.rem = (int32_t)(dim % k);
+    return a;
+}
+
+struct Lat2 {
+    Axis ay, ax;            // rows, cols
+    int32_t W;              // grid width (row stride)
+    int32_t lamw, mu, q;    // q = lamw / mu
+    int32_t cap;            // pair capacity per direction = 2*lamw
+    int32_t warm, skip_clean, fuse;
+    double eps;
+    const int32_t *u;
+    int32_t *a0, *a1, *y2, *ybest;
+    uint8_t *yhat, *resid;
+    uint32_t *dirty;
+    int64_t *pe, *pr;
+    int32_t *pf;
+    dope_run_state *st;
+    int64_t *tr_e;
+    double *tr_rs, *tr_mr;
+    int32_t *tr_cl;
+    int32_t max_iters;
+    int32_t K;
+    int32_t boxh, boxw;     // padded box used for the block layout
+};
+
+// ---------------------------------------------------------------------------
+// Bit-parallel BFS helpers (one warp).  The block's nodes are numbered
+// v = r*BW + c over the padded box; bit v of the 64-bit word array is node v.
+// Lane `l` owns words [l*WPL, (l+1)*WPL).
+// ---------------------------------------------------------------------------
+
+template <int WPL, int LANES, int T>
+__device__ __forceinline__ uint64_t fetch_word(const uint64_t (&R)[WPL], int lane) {
+    // word index lane*WPL + T  (T compile-time, may be negative)
+    constexpr int DL = (T >= 0) ? (T / WPL) : -((-T + WPL - 1) / WPL);
+    constexpr int SLOT = T - DL * WPL;
+    uint64_t v = R[SLOT];
+    if constexpr (DL > 0) {
+        v = __shfl_down_sync(FULLMASK, v, DL);
+        if (lane + DL >= LANES) v = 0;
+    } else if constexpr (DL < 0) {
+        v = __shfl_up_sync(FULLMASK, v, -DL);
+        if (lane + DL < 0) v = 0;
+    }
+    return v;
+}
+
+// out[k] = bits of R shifted so that bit x holds R[x + S]  (S != 0)
+template <int WPL, int LANES, int S, int K>
+__device__ __forceinline__ uint64_t shifted(const uint64_t (&R)[WPL], int lane) {
+    if constexpr (S > 0) {
+        constexpr int Q = S / 64, REM = S % 64;
+        uint64_t lo = fetch_word<WPL, LANES, K + Q>(R, lane);
+        if constexpr (REM == 0) {
+            return lo;
+        } else {
+            uint64_t hi = fetch_word<WPL, LANES, K + Q + 1>(R, lane);
+            return (lo >> REM) | (hi << (64 - REM));
+        }
+    } else {
+        constexpr int T = -S;
+        constexpr int Q = T / 64, REM = T % 64;
+        uint64_t hi = fetch_word<WPL, LANES, K - Q>(R, lane);
+        if constexpr (REM == 0) {
+            return hi;
+        } else {
+            uint64_t lo = fetch_word<WPL, LANES, K - Q - 1>(R, lane);
+            return (hi << REM) | (lo >> (64 - REM));
+        }
+    }
+}
+
+template <int WPL, int LANES, int BW, int K>
+__device__ __forceinline__ uint64_t expand_word(const uint64_t (&R)[WPL], uint64_t mE, uint64_t mW,
+                                                uint64_t mS, uint64_t mN, int lane) {
+    // node v joins when it has a residual arc to an already reached node
+    return (mE & shifted<WPL, LANES, 1, K>(R, lane)) | (mW & shifted<WPL, LANES, -1, K>(R, lane)) |
+           (mS & shifted<WPL, LANES, BW, K>(R, lane)) | (mN & shifted<WPL, LANES, -BW, K>(R, lane));
+}
+
+template <int WPL, int LANES, int BW, int K>
+struct Expand {
+    __device__ __forceinline__ static void run(const uint64_t (&R)[WPL], uint64_t (&NEW)[WPL],
+                                               const uint64_t *mE, const uint64_t *mW,
+                                               const uint64_t *mS, const uint64_t *mN, int lane) {
+        Expand<WPL, LANES, BW, K - 1>::run(R, NEW, mE, mW, mS, mN, lane);
+        const int idx = lane * WPL + (K - 1);
+        const bool on = lane < LANES;
+        uint64_t e = on ? mE[idx] : 0, w = on ? mW[idx] : 0, s = on ? mS[idx] : 0,
+                 n = on ? mN[idx] : 0;
+        NEW[K - 1] = expand_word<WPL, LANES, BW, K - 1>(R, e, w, s, n, lane) & ~R[K - 1];
+    }
+};
+template <int WPL, int LANES, int BW>
+struct Expand<WPL, LANES, BW, 0> {
+    __device__ __forceinline__ static void run(const uint64_t (&)[WPL], uint64_t (&)[WPL],
+                                               const uint64_t *, const uint64_t *,
+                                               const uint64_t *, const uint64_t *, int) {}
+};
+
+// Global relabel: exact BFS distances to the sink set (g < 0) over residual
+// arcs, written to h[] (HINF = unreached).  Returns (on lane 0..31 of warp 0)
+// whether any active node (g > 0) is reached; `reach` receives the reached
+// set.  Early exit once every active node has a level, except when there is
+// none (then the BFS runs to completion and `reach` is the exact sink side).
+template <int NW, int BW>
+__device__ int bfs_relabel(const uint64_t *__restrict__ mE, const uint64_t *__restrict__ mW,
+                           const uint64_t *__restrict__ mS, const uint64_t *__restrict__ mN,
+                           const uint64_t *__restrict__ mSink, const uint64_t *__restrict__ mAct,
+                           uint64_t *__restrict__ reach, uint16_t *__restrict__ h, int lane,
+                           int *levels_out) {
+    constexpr int LANES = NW < 32 ? NW : 32;
+    constexpr int WPL = NW < 32 ? 1 : NW / 32;
+    static_assert(NW % LANES == 0, "word layout");
+    const bool on = lane < LANES;
+    uint64_t R[WPL], A[WPL], NEW[WPL];
+    bool any_act = false;
+#pragma unroll
+    for (int k = 0; k < WPL; ++k) {
+        const int idx = lane * WPL + k;
+        R[k] = on ? mSink[idx] : 0;
+        A[k] = on ? mAct[idx] : 0;
+        any_act |= (A[k] != 0);
+        uint64_t nb = R[k];
+        while (nb) {
+            const int b = __ffsll((long long)nb) - 1;
+            nb &= nb - 1;
+            h[idx * 64 + b] = 0;
+        }
+    }
+    const bool have_active = __any_sync(FULLMASK, any_act);
+    int level = 0;
+    for (;;) {
+        if (have_active) {
+            bool missing = false;
+#pragma unroll
+            for (int k = 0; k < WPL; ++k) missing |= (A[k] & ~R[k]) != 0;
+            if (!__any_sync(FULLMASK, missing)) break;
+        }
+        Expand<WPL, LANES, BW, WPL>::run(R, NEW, mE, mW, mS, mN, lane);
+        bool grew = false;
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) grew |= (NEW[k] != 0);
+        if (!__any_sync(FULLMASK, grew)) break;
+        ++level;
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) {
+            R[k] |= NEW[k];
+            uint64_t nb = NEW[k];
+            const int base = (lane * WPL + k) * 64;
+            while (nb) {
+                const int b = __ffsll((long long)nb) - 1;
+                nb &= nb - 1;
+                h[base + b] = (uint16_t)level;
+            }
+        }
+    }
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < WPL; ++k) {
+        if (on) reach[lane * WPL + k] = R[k];
+        hit |= (A[k] & R[k]) != 0;
+    }
+    *levels_out = level;
+    return __any_sync(FULLMASK, hit);
+}
+
+// ---------------------------------------------------------------------------
+// K1: block min-cut (2D, 4-connected)
+// ---------------------------------------------------------------------------
+
+template <int BH, int BW, int NT>
+struct K1Cfg {
+    static constexpr int M = BH * BW;
+    static_assert(M % NT == 0, "nodes per thread");
+    static_assert(M % 64 == 0, "bit words");
+    static constexpr int NPT = M / NT;
+    static constexpr int NW = M / 64;
+    static constexpr size_t OFF_G = 0;                       // int32[M]
+    static constexpr size_t OFF_R = OFF_G + 4 * (size_t)M;   // uint8[4][M]  (E,W,S,N)
+    static constexpr size_t OFF_H = OFF_R + 4 * (size_t)M;   // uint16[M]
+    static constexpr size_t OFF_MASK = OFF_H + 2 * (size_t)M;  // uint64[6][NW]
+    static constexpr size_t OFF_REACH = OFF_MASK + 6 * 8 * (size_t)NW;
+    static constexpr size_t OFF_MISC = OFF_REACH + 8 * (size_t)NW;
+    static constexpr size_t SMEM = OFF_MISC + 64;
+};
+
+struct K1Tune {
+    int32_t sweep_min, sweep_mul;   // sweeps per round = sweep_min + sweep_mul*levels
+    int32_t max_rounds;
+};
+
+template <int BH, int BW, int NT>
+__global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
+    using C = K1Cfg<BH, BW, NT>;
+    constexpr int M = C::M, NPT = C::NPT, NW = C::NW;
+    extern __shared__ __align__(16) uint8_t smem[];
+    int32_t *g = reinterpret_cast<int32_t *>(smem + C::OFF_G);
+    uint8_t *rr = smem + C::OFF_R;
+    uint16_t *h = reinterpret_cast<uint16_t *>(smem + C::OFF_H);
+    uint64_t *masks = reinterpret_cast<uint64_t *>(smem + C::OFF_MASK);
+    uint64_t *reach = reinterpret_cast<uint64_t *>(smem + C::OFF_REACH);
+    int *misc = reinterpret_cast<int *>(smem + C::OFF_MISC);
+    uint32_t *masks32 = reinterpret_cast<uint32_t *>(masks);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int k = blockIdx.x;
+    if (L.st->stop) return;
+    if (L.skip_clean) {
+        if (L.dirty[k] == 0) return;
+    }
+    __syncthreads();
+    if (tid == 0) L.dirty[k] = 0;
+
+    const int by = k / L.ax.k, bx = k % L.ax.k;
+    int32_t lo_r, hr, lo_c, wc;
+    L.ay.range(by, lo_r, hr);
+    L.ax.range(bx, lo_c, wc);
+    const int32_t Wg = L.W;
+    const int32_t cap = L.cap;
+    const int32_t *__restrict__ a_cur = L.st->parity ? L.a1 : L.a0;
+    uint8_t *gres = L.resid + (size_t)k * 4 * M;
+
+    // ---- prologue: 2*linear (blockform.py:271-272 on the q==1 stencil) ----
+    // lin2 = 2u + lamw * sum_cross (y2_g - y2_j) + mu*(2a - y2_g) + mu
+    if (L.warm) {
+        // residual planes are stored block-major, 4*M bytes, 16-byte chunks
+        const uint4 *src = reinterpret_cast<const uint4 *>(gres);
+        uint4 *dst = reinterpret_cast<uint4 *>(rr);
+        for (int i = tid; i < M * 4 / 16; i += NT) dst[i] = src[i];
+        __syncthreads();
+    }
+#pragma unroll 4
+    for (int i = 0; i < NPT; ++i) {
+        const int v = tid + i * NT;
+        const int r = v / BW, c = v % BW;
+        const bool valid = (r < hr) && (c < wc);
+        int32_t gv = 0;
+        uint8_t re = 0, rw = 0, rs = 0, rn = 0;
+        if (valid) {
+            const int64_t G = (int64_t)(lo_r + r) * Wg + lo_c + c;
+            const int32_t yg = L.y2[G];
+            int32_t s = 0;
+            if (c == 0 && lo_c > 0) s += yg - L.y2[G - 1];
+            if (c == wc - 1 && lo_c + wc < Wg) s += yg - L.y2[G + 1];
+            if (r == 0 && lo_r > 0) s += yg - L.y2[G - Wg];
+            if (r == hr - 1 && lo_r + hr < L.ay.dim) s += yg - L.y2[G + Wg];
+            const int32_t lin2 = 2 * L.u[G] + L.lamw * s + L.mu * (2 * a_cur[G] - yg) + L.mu;
+            const bool hasE = c + 1 < wc, hasW = c > 0, hasS = r + 1 < hr, hasN = r > 0;
+            if (L.warm) {
+                re = rr[0 * M + v]; rw = rr[1 * M + v]; rs = rr[2 * M + v]; rn = rr[3 * M + v];
+                // net inflow of the stored flow: sum_d (r_d - cap)
+                int32_t f = 0;
+                if (hasE) f += (int32_t)re - cap;
+                if (hasW) f += (int32_t)rw - cap;
+                if (hasS) f += (int32_t)rs - cap;
+                if (hasN) f += (int32_t)rn - cap;
+                gv = lin2 + f;
+            } else {
+                re = hasE ? cap : 0; rw = hasW ? cap : 0; rs = hasS ? cap : 0; rn = hasN ? cap : 0;
+                gv = lin2;
+            }
+        }
+        g[v] = gv;
+        if (!L.warm) {
+            rr[0 * M + v] = re; rr[1 * M + v] = rw; rr[2 * M + v] = rs; rr[3 * M + v] = rn;
+        }
+    }
+    __syncthreads();
+
+    // ---- solve: rounds of (global relabel BFS, push/relabel sweeps) ----
+    uint64_t *mE = masks, *mW = masks + NW, *mS = masks + 2 * NW, *mN = masks + 3 * NW;
+    uint64_t *mSink = masks + 4 * NW, *mAct = masks + 5 * NW;
+    int rounds = 0;
+    long long sweeps_done = 0;
+    for (;;) {
+        // masks via ballots: warp covers 32 consecutive nodes per step
+#pragma unroll 2
+        for (int i = 0; i < NPT; ++i) {
+            const int v = tid + i * NT;
+            const int32_t gv = g[v];
+            const uint32_t bE = __ballot_sync(FULLMASK, rr[0 * M + v] != 0);
+            const uint32_t bW = __ballot_sync(FULLMASK, rr[1 * M + v] != 0);
+            const uint32_t bS = __ballot_sync(FULLMASK, rr[2 * M + v] != 0);
+            const uint32_t bN = __ballot_sync(FULLMASK, rr[3 * M + v] != 0);
+            const uint32_t bK = __ballot_sync(FULLMASK, gv < 0);
+            const uint32_t bA = __ballot_sync(FULLMASK, gv > 0);
+            h[v] = HINF;
+            if (lane == 0) {
+                const int w32 = (i * NT + warp * 32) >> 5;
+                masks32[0 * 2 * NW + w32] = bE;
+                masks32[1 * 2 * NW + w32] = bW;
+                masks32[2 * 2 * NW + w32] = bS;
+                masks32[3 * 2 * NW + w32] = bN;
+                masks32[4 * 2 * NW + w32] = bK;
+                masks32[5 * 2 * NW + w32] = bA;
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            int levels = 0;
+            const int hit = bfs_relabel<NW, BW>(mE, mW, mS, mN, mSink, mAct, reach, h, lane, &levels);
+            if (lane == 0) { misc[0] = hit; misc[1] = levels; }
+        }
+        __syncthreads();
+        const int hit = misc[0];
+        const int levels = misc[1];
+        if (!hit) break;
+        if (++rounds > T.max_rounds) {
+            if (tid == 0) atomicCAS(&L.st->error, 0, k + 1);
+            break;
+        }
+        const int cap_sweeps = T.sweep_min + T.sweep_mul * levels;
+        for (int sw = 0; sw < cap_sweeps; ++sw) {
+            ++sweeps_done;
+            // push phase: admissible arcs h(w) == h(v) - 1
+#pragma unroll 2
+            for (int i = 0; i < NPT; ++i) {
+                const int v = tid + i * NT;
+                const int32_t e = g[v];
+                if (e <= 0) continue;
+                const uint16_t hv = h[v];
+                if (hv == HINF || hv == 0) continue;
+                const uint16_t ht = hv - 1;
+                int32_t left = e;
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    const int off = (d == 0) ? 1 : (d == 1) ? -1 : (d == 2) ? BW : -BW;
+                    const int32_t rv = rr[d * M + v];
+                    if (rv == 0) continue;
+                    const int w = v + off;
+                    if (h[w] != ht) continue;
+                    const int32_t delta = left < rv ? left : rv;
+                    rr[d * M + v] = (uint8_t)(rv - delta);
+                    rr[(d ^ 1) * M + w] = (uint8_t)(rr[(d ^ 1) * M + w] + delta);
+                    atomicAdd(&g[w], delta);
+                    left -= delta;
+                    if (left == 0) break;
+                }
+                if (left != e) atomicSub(&g[v], e - left);
+            }
+            __syncthreads();
+            // relabel phase: h(v) = 1 + min over residual arcs (monotone)
+            int act = 0;
+#pragma unroll 2
+            for (int i = 0; i < NPT; ++i) {
+                const int v = tid + i * NT;
+                if (g[v] <= 0) continue;
+                const uint16_t hv = h[v];
+                if (hv == HINF) continue;
+                uint32_t mn = HINF;
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    const int off = (d == 0) ? 1 : (d == 1) ? -1 : (d == 2) ? BW : -BW;
+                    if (rr[d * M + v] == 0) continue;
+                    const uint32_t hw = h[v + off];
+                    mn = hw < mn ? hw : mn;
+                }
+                const uint32_t nh = (mn + 1 >= (uint32_t)M) ? HINF : mn + 1;
+                if (nh != hv) h[v] = (uint16_t)nh;
+                act |= (nh != HINF);
+            }
+            if (!__syncthreads_or(act)) break;
+        }
+    }
+
+    // ---- epilogue: labels (sink side), residual graph, stats ----
+    for (int i = 0; i < NPT; ++i) {
+        const int v = tid + i * NT;
+        const int r = v / BW, c = v % BW;
+        if (r < hr && c < wc) {
+            const int64_t G = (int64_t)(lo_r + r) * Wg + lo_c + c;
+            L.yhat[G] = (uint8_t)((reach[v >> 6] >> (v & 63)) & 1ull);
+        }
+    }
+    if (L.warm) {
+        uint4 *dst = reinterpret_cast<uint4 *>(gres);
+        const uint4 *src = reinterpret_cast<const uint4 *>(rr);
+        for (int i = tid; i < M * 4 / 16; i += NT) dst[i] = src[i];
+    }
+    if (tid == 0) {
+        atomicAdd((unsigned long long *)&L.st->solves, 1ull);
+        atomicAdd((unsigned long long *)&L.st->sweeps, (unsigned long long)sweeps_done);
+        atomicMax(&L.st->max_rounds_seen, rounds);
+    }
+}
+
+// cold residual graphs for every block (warm-start initial state)
+__global__ void k_init_resid(Lat2 L) {
+    const int k = blockIdx.x;
+    const int M = L.boxh * L.boxw;
+    const int by = k / L.ax.k, bx = k % L.ax.k;
+    int32_t lo_r, hr, lo_c, wc;
+    L.ay.range(by, lo_r, hr);
+    L.ax.range(bx, lo_c, wc);
+    uint8_t *gres = L.resid + (size_t)k * 4 * M;
+    for (int v = threadIdx.x; v < M; v += blockDim.x) {
+        const int r = v / L.boxw, c = v % L.boxw;
+        const bool valid = r < hr && c < wc;
+        gres[0 * M + v] = (valid && c + 1 < wc) ? L.cap : 0;
+        gres[1 * M + v] = (valid && c > 0) ? L.cap : 0;
+        gres[2 * M + v] = (valid && r + 1 < hr) ? L.cap : 0;
+        gres[3 * M + v] = (valid && r > 0) ? L.cap : 0;
+    }
+}
+
+__global__ void k_init_state(Lat2 L, int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        L.y2[i] = 1;                 // y = 1/2 (admm.py:163-164)
+        L.a0[i] = 0;
+        L.a1[i] = 0;
+        L.ybest[i] = 1;
+        L.yhat[i] = 0;
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.K; i += stride)
+        L.dirty[i] = 1u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        dope_run_state s;
+        memset(&s, 0, sizeof(s));
+        s.best_energy = INT64_MAX;
+        *L.st = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: consensus update (2D, 4-connected), one CTA per block
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int32_t new_y_at(const Lat2 &L, const int32_t *__restrict__ a_in,
+                                            int32_t R, int32_t Cc, int32_t *ypre_out) {
+    // y = clamp(yh + a - (lamw/mu) * sum_cross (yh - yh_j))   (admm.py:194-209, 230-238)
+    const int64_t G = (int64_t)R * L.W + Cc;
+    const int32_t yh = L.yhat[G];
+    const int32_t br = L.ay.owner(R), bc = L.ax.owner(Cc);
+    int32_t s = 0;
+    if (Cc > 0 && L.ax.owner(Cc - 1) != bc) s += yh - L.yhat[G - 1];
+    if (Cc + 1 < L.W && L.ax.owner(Cc + 1) != bc) s += yh - L.yhat[G + 1];
+    if (R > 0 && L.ay.owner(R - 1) != br) s += yh - L.yhat[G - L.W];
+    if (R + 1 < L.ay.dim && L.ay.owner(R + 1) != br) s += yh - L.yhat[G + L.W];
+    const int32_t ypre = yh + a_in[G] - L.q * s;
+    if (ypre_out) *ypre_out = ypre;
+    return ypre < 0 ? 0 : (ypre > 1 ? 1 : ypre);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
+    extern __shared__ __align__(16) uint8_t smem2[];
+    uint8_t *ys = smem2;                 // box-sized y cache
+    __shared__ int64_t red_e[8], red_s[8];
+    __shared__ int red_f[8];
+    __shared__ int side[5];              // self, left, right, up, down dirty marks
+
+    if (L.st->stop) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nthr = blockDim.x;
+    const int k = blockIdx.x;
+    const int by = k / L.ax.k, bx = k % L.ax.k;
+    int32_t lo_r, hr, lo_c, wc;
+    L.ay.range(by, lo_r, hr);
+    L.ax.range(bx, lo_c, wc);
+    const int BWb = L.boxw;
+    const int M = L.boxh * BWb;
+    const int p = L.st->parity;
+    const int32_t *__restrict__ a_in = p ? L.a1 : L.a0;
+    int32_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
+    const int pending = L.st->copy_best_pending;
+    if (tid < 5) side[tid] = 0;
+    __syncthreads();
+
+    int64_t e_acc = 0, ss = 0;
+    int clamped = 0, chg_self = 0, chgL = 0, chgR = 0, chgU = 0, chgD = 0;
+    for (int v = tid; v < M; v += nthr) {
+        const int r = v / BWb, c = v % BWb;
+        if (r >= hr || c >= wc) continue;
+        const int32_t R = lo_r + r, Cc = lo_c + c;
+        const int64_t G = (int64_t)R * L.W + Cc;
+        int32_t ypre;
+        const int32_t y = new_y_at(L, a_in, R, Cc, &ypre);
+        const int32_t yh = L.yhat[G];
+        const int32_t aold = a_in[G];
+        const int32_t y2old = L.y2[G];
+        clamped |= (ypre < 0 || ypre > 1);
+        if (a_out) a_out[G] = aold + yh - y;
+        L.y2[G] = 2 * y;
+        if (pending) L.ybest[G] = y2old;
+        ys[v] = (uint8_t)y;
+        e_acc += (int64_t)L.u[G] * y;
+        ss += (int64_t)((yh - y) * (yh - y));
+        const bool ychg = (2 * y != y2old);
+        chg_self |= ychg || (yh != y);
+        if (ychg) {
+            chgL |= (c == 0 && lo_c > 0);
+            chgR |= (c == wc - 1 && lo_c + wc < L.W);
+            chgU |= (r == 0 && lo_r > 0);
+            chgD |= (r == hr - 1 && lo_r + hr < L.ay.dim);
+        }
+    }
+    __syncthreads();
+    // pairs owned by this block: (v, right) and (v, down)
+    int64_t quad = 0;
+    for (int v = tid; v < M; v += nthr) {
+        const int r = v / BWb, c = v % BWb;
+        if (r >= hr || c >= wc) continue;
+        const int32_t R = lo_r + r, Cc = lo_c + c;
+        const int32_t y = ys[v];
+        if (c + 1 < wc) {
+            const int32_t d = y - ys[v + 1];
+            quad += d * d;
+        } else if (Cc + 1 < L.W) {
+            const int32_t d = y - new_y_at(L, a_in, R, Cc + 1, nullptr);
+            quad += d * d;
+        }
+        if (r + 1 < hr) {
+            const int32_t d = y - ys[v + BWb];
+            quad += d * d;
+        } else if (R + 1 < L.ay.dim) {
+            const int32_t d = y - new_y_at(L, a_in, R + 1, Cc, nullptr);
+            quad += d * d;
+        }
+    }
+    e_acc += (int64_t)L.lamw * quad;
+    e_acc = warp_sum(e_acc);
+    ss = warp_sum(ss);
+    const int fl = __any_sync(FULLMASK, clamped);
+    if (__any_sync(FULLMASK, chg_self) && lane == 0) side[0] = 1;
+    if (__any_sync(FULLMASK, chgL) && lane == 0) side[1] = 1;
+    if (__any_sync(FULLMASK, chgR) && lane == 0) side[2] = 1;
+    if (__any_sync(FULLMASK, chgU) && lane == 0) side[3] = 1;
+    if (__any_sync(FULLMASK, chgD) && lane == 0) side[4] = 1;
+    if (lane == 0) { red_e[warp] = e_acc; red_s[warp] = ss; red_f[warp] = fl; }
+    __syncthreads();
+    if (tid == 0) {
+        int64_t E = 0, S = 0;
+        int F = 0;
+        for (int w = 0; w < nthr / 32; ++w) { E += red_e[w]; S += red_s[w]; F |= red_f[w]; }
+        L.pe[k] = E;
+        L.pr[k] = S;
+        L.pf[k] = F;
+        if (side[0]) L.dirty[k] = 1u;
+        if (side[1]) L.dirty[k - 1] = 1u;
+        if (side[2]) L.dirty[k + 1] = 1u;
+        if (side[3]) L.dirty[k - L.ax.k] = 1u;
+        if (side[4]) L.dirty[k + L.ax.k] = 1u;
+    }
+}
+
+// a += yhat - y for the step-level API (admm.py:241-248), in place.
+__global__ void k_update_multipliers(Lat2 L, int64_t n) {
+    int32_t *a = L.st->parity ? L.a1 : L.a0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        a[i] += (int32_t)L.yhat[i] - (L.y2[i] >> 1);
+}
+
+// ---------------------------------------------------------------------------
+// K3: finalize one iteration (admm.py:289-307)
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(1024) k_finalize(Lat2 L) {
+    __shared__ int64_t sE[32];
+    __shared__ double sR[32];
+    __shared__ int64_t sM[32];
+    __shared__ int sF[32];
+    dope_run_state *st = L.st;
+    if (st->stop) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int64_t E = 0, mx = -1;
+    double rs = 0.0;
+    int F = 0;
+    // fixed assignment of blocks to threads and a fixed tree: deterministic
+    for (int k = tid; k < L.K; k += blockDim.x) {
+        E += L.pe[k];
+        const int64_t s = L.pr[k];
+        const double r = sqrt((double)s);
+        rs += r * r;
+        mx = s > mx ? s : mx;
+        F |= L.pf[k];
+    }
+    E = warp_sum(E);
+    for (int o = 16; o > 0; o >>= 1) {
+        rs += __shfl_xor_sync(FULLMASK, rs, o);
+        const int64_t t = __shfl_xor_sync(FULLMASK, mx, o);
+        mx = t > mx ? t : mx;
+    }
+    F = __any_sync(FULLMASK, F);
+    if (lane == 0) { sE[warp] = E; sR[warp] = rs; sM[warp] = mx; sF[warp] = F; }
+    __syncthreads();
+    if (tid == 0) {
+        int64_t E2 = 0, M2 = -1;
+        double R2 = 0.0;
+        int F2 = 0;
+        const int nw = blockDim.x / 32;
+        for (int w = 0; w < nw; ++w) {
+            E2 += sE[w];
+            R2 += sR[w];
+            M2 = sM[w] > M2 ? sM[w] : M2;
+            F2 |= sF[w];
+        }
+        const int t = st->iteration;
+        const double maxres = M2 < 0 ? 0.0 : sqrt((double)M2);
+        if (t < L.max_iters) {
+            L.tr_e[t] = E2;
+            L.tr_rs[t] = R2;
+            L.tr_mr[t] = maxres;
+            L.tr_cl[t] = F2;
+        }
+        if (E2 < st->best_energy) {
+            st->best_energy = E2;
+            st->best_iteration = t + 1;
+            st->copy_best_pending = 1;
+        } else {
+            st->copy_best_pending = 0;
+        }
+        if (L.fuse) st->parity ^= 1;
+        st->iteration = t + 1;
+        if (L.K == 0 || maxres <= L.eps) {
+            st->converged = 1;
+            st->stop = 1;
+        }
+        if (st->error) st->stop = 1;
+    }
+}
+
+// end of run: pending best copy, then state.y = best_y when not converged
+__global__ void k_finish(Lat2 L, int64_t n) {
+    const dope_run_state *st = L.st;
+    const int pending = st->copy_best_pending;
+    const int conv = st->converged;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        int32_t yb = pending ? L.y2[i] : L.ybest[i];
+        if (pending) L.ybest[i] = yb;
+        if (!conv) L.y2[i] = yb;
+    }
+}
+
+// 4*E of an arbitrary doubled labeling (y2 = 2y): 2*sum u*y2 + lamw*sum (y2_i-y2_j)^2
+__global__ void k_energy4(Lat2 L, const int32_t *__restrict__ y2, int64_t n,
+                          unsigned long long *out) {
+    int64_t acc = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int32_t c = (int32_t)(i % L.W);
+        const int64_t r = i / L.W;
+        const int32_t yi = y2[i];
+        int64_t q = 0;
+        if (c + 1 < L.W) { const int64_t d = yi - y2[i + 1]; q += d * d; }
+        if (r + 1 < L.ay.dim) { const int64_t d = yi - y2[i + L.W]; q += d * d; }
+        acc += 2 * (int64_t)L.u[i] * yi + (int64_t)L.lamw * q;
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)acc);
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+
+struct Variant {
+    int bh, bw, nt;
+    size_t smem;
+    void (*kernel)(Lat2, K1Tune);
+};
+
+template <int BH, int BW, int NT>
+static Variant make_variant() {
+    return Variant{BH, BW, NT, K1Cfg<BH, BW, NT>::SMEM, &k_block_mincut<BH, BW, NT>};
+}
+
+static const Variant *pick_variant(int maxh, int maxw) {
+    static const Variant table[] = {
+        make_variant<16, 16, 64>(),
+        make_variant<32, 32, 128>(),
+        make_variant<64, 64, 256>(),
+        make_variant<128, 128, 512>(),
+    };
+    for (const Variant &v : table)
+        if (maxh <= v.bh && maxw <= v.bw) return &v;
+    return nullptr;
+}
+
+static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var) {
+    if (!L || !L->u || !L->a[0] || !L->a[1] || !L->y2 || !L->ybest || !L->yhat || !L->resid ||
+        !L->dirty || !L->part_energy || !L->part_ressq || !L->part_flags || !L->state)
+        return DOPE_E_ARGS;
+    if (L->ndim != 2 || L->conn != 4) return DOPE_E_GEOMETRY;
+    if (L->dims[0] < 1 || L->dims[1] < 1 || L->kpa[0] < 1 || L->kpa[1] < 1) return DOPE_E_ARGS;
+    if (L->kpa[0] > L->dims[0] || L->kpa[1] > L->dims[1]) return DOPE_E_ARGS;
+    if (L->dims[0] * L->dims[1] > (int64_t)INT32_MAX) return DOPE_E_ARGS;
+    if (L->mu <= 0 || L->lamw < 0 || (L->lamw % L->mu) != 0) return DOPE_E_ARGS;
+    if (2 * (int64_t)L->lamw * 2 > 255) return DOPE_E_CAPACITY;   // r + r' = 2*cap <= 255
+    memset(&o, 0, sizeof(o));
+    o.ay = make_axis(L->dims[0], L->kpa[0]);
+    o.ax = make_axis(L->dims[1], L->kpa[1]);
+    o.W = (int32_t)L->dims[1];
+    o.lamw = L->lamw;
+    o.mu = L->mu;
+    o.q = L->lamw / L->mu;
+    o.cap = 2 * L->lamw;
+    o.warm = L->warm_start;
+    o.skip_clean = L->skip_clean;
+    o.fuse = L->fuse_multipliers;
+    o.eps = L->eps;
+    o.u = L->u;
+    o.a0 = L->a[0];
+    o.a1 = L->a[1];
+    o.y2 = L->y2;
+    o.ybest = L->ybest;
+    o.yhat = L->yhat;
+    o.resid = L->resid;
+    o.dirty = L->dirty;
+    o.pe = L->part_energy;
+    o.pr = L->part_ressq;
+    o.pf = L->part_flags;
+    o.st = L->state;
+    o.tr_e = L->trace_energy;
+    o.tr_rs = L->trace_residual_sq;
+    o.tr_mr = L->trace_max_residual;
+    o.tr_cl = L->trace_clamped;
+    o.max_iters = L->max_iters;
+    o.K = L->kpa[0] * L->kpa[1];
+    const int maxh = o.ay.base + (o.ay.rem ? 1 : 0);
+    const int maxw = o.ax.base + (o.ax.rem ? 1 : 0);
+    const Variant *v = pick_variant(maxh, maxw);
+    if (!v) return DOPE_E_GEOMETRY;
+    o.boxh = v->bh;
+    o.boxw = v->bw;
+    if (var) *var = v;
+    return DOPE_OK;
+}
+
+static K1Tune default_tune() {
+    K1Tune t;
+    t.sweep_min = 4;
+    t.sweep_mul = 2;
+    t.max_rounds = 1 << 16;
+    return t;
+}
+
+static int configure_k1(const Variant *v) {
+    static std::mutex mu;
+    static std::map<void *, bool> configured;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!configured[(void *)v->kernel]) {
+        int rc = cuda_check(cudaFuncSetAttribute(v->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)v->smem), "cudaFuncSetAttribute(K1)");
+        if (rc) return rc;
+        configured[(void *)v->kernel] = true;
+    }
+    return DOPE_OK;
+}
+
+static int launch_k1(const Lat2 &o, const Variant *v, cudaStream_t s) {
+    int rc = configure_k1(v);
+    if (rc) return rc;
+    v->kernel<<<o.K, v->nt, v->smem, s>>>(o, default_tune());
+    return cuda_check(cudaGetLastError(), "launch K1");
+}
+
+static int launch_k2(const Lat2 &o, cudaStream_t s) {
+    const size_t smem = (size_t)o.boxh * o.boxw;
+    k_consensus<<<o.K, 256, smem, s>>>(o);
+    return cuda_check(cudaGetLastError(), "launch K2");
+}
+
+static int launch_k3(const Lat2 &o, cudaStream_t s) {
+    k_finalize<<<1, 1024, 0, s>>>(o);
+    return cuda_check(cudaGetLastError(), "launch K3");
+}
+
+static int grid_for(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    return (int)(b < 1 ? 1 : b);
+}
+
+}  // namespace dope
+
+using namespace dope;
+
+extern "C" {
+
+const char *dope_backend_name(void) { return "b200-sm100a"; }
+int dope_abi_version(void) { return DOPE_ABI_VERSION; }
+const char *dope_last_cuda_error(void) { return g_last_err; }
+
+int64_t dope_resid_stride(const dope_lattice *L) {
+    if (!L || L->ndim != 2 || L->kpa[0] < 1 || L->kpa[1] < 1) return 0;
+    Axis ay = make_axis(L->dims[0], L->kpa[0]), ax = make_axis(L->dims[1], L->kpa[1]);
+    const Variant *v = pick_variant(ay.base + (ay.rem ? 1 : 0), ax.base + (ax.rem ? 1 : 0));
+    if (!v) return 0;
+    return (int64_t)4 * v->bh * v->bw;
+}
+
+int dope_lattice_check(const dope_lattice *L) {
+    Lat2 o;
+    return build_lat2(L, o, nullptr);
+}
+
+int dope_admm_init(const dope_lattice *L, void *stream) {
+    Lat2 o;
+    const Variant *v;
+    int rc = build_lat2(L, o, &v);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n = L->dims[0] * L->dims[1];
+    k_init_state<<<grid_for(n), 256, 0, s>>>(o, n);
+    rc = cuda_check(cudaGetLastError(), "init_state");
+    if (rc) return rc;
+    k_init_resid<<<o.K, 256, 0, s>>>(o);
+    return cuda_check(cudaGetLastError(), "init_resid");
+}
+
+int dope_update_blocks(const dope_lattice *L, void *stream) {
+    Lat2 o;
+    const Variant *v;
+    int rc = build_lat2(L, o, &v);
+    if (rc) return rc;
+    return launch_k1(o, v, (cudaStream_t)stream);
+}
+
+int dope_update_global(const dope_lattice *L, void *stream) {
+    Lat2 o;
+    int rc = build_lat2(L, o, nullptr);
+    if (rc) return rc;
+    return launch_k2(o, (cudaStream_t)stream);
+}
+
+int dope_update_multipliers(const dope_lattice *L, void *stream) {
+    Lat2 o;
+    int rc = build_lat2(L, o, nullptr);
+    if (rc) return rc;
+    const int64_t n = L->dims[0] * L->dims[1];
+    k_update_multipliers<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(o, n);
+    return cuda_check(cudaGetLastError(), "update_multipliers");
+}
+
+int dope_reduce_finalize(const dope_lattice *L, void *stream) {
+    Lat2 o;
+    int rc = build_lat2(L, o, nullptr);
+    if (rc) return rc;
+    return launch_k3(o, (cudaStream_t)stream);
+}
+
+int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void *stream) {
+    Lat2 o;
+    const Variant *v;
+    int rc = build_lat2(L, o, &v);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (iters <= 0) return DOPE_OK;
+    if (!use_graph) {
+        for (int i = 0; i < iters; ++i) {
+            if ((rc = launch_k1(o, v, s))) return rc;
+            if ((rc = launch_k2(o, s))) return rc;
+            if ((rc = launch_k3(o, s))) return rc;
+        }
+        return DOPE_OK;
+    }
+    // CUDA graph of `iters` iterations, cached by the lattice description
+    static std::mutex mu;
+    static std::map<std::string, cudaGraphExec_t> cache;
+    std::string key((const char *)L, sizeof(*L));
+    key.append((const char *)&iters, sizeof(iters));
+    cudaGraphExec_t exec = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) exec = it->second;
+    }
+    if (!exec) {
+        // kernel attributes must be set outside stream capture
+        if ((rc = configure_k1(v))) return rc;
+        cudaStream_t cs;
+        if ((rc = cuda_check(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream"))) return rc;
+        cudaGraph_t graph;
+        if ((rc = cuda_check(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "capture"))) return rc;
+        for (int i = 0; i < iters && !rc; ++i) {
+            rc = launch_k1(o, v, cs);
+            if (!rc) rc = launch_k2(o, cs);
+            if (!rc) rc = launch_k3(o, cs);
+        }
+        cudaError_t e = cudaStreamEndCapture(cs, &graph);
+        if (rc) return rc;
+        if ((rc = cuda_check(e, "end capture"))) return rc;
+        rc = cuda_check(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
+        cudaGraphDestroy(graph);
+        cudaStreamDestroy(cs);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(mu);
+        cache[key] = exec;
+    }
+    return cuda_check(cudaGraphLaunch(exec, s), "graph launch");
+}
+
+int dope_finish_run(const dope_lattice *L, void *stream) {
+    Lat2 o;
+    int rc = build_lat2(L, o, nullptr);
+    if (rc) return rc;
+    const int64_t n = L->dims[0] * L->dims[1];
+    k_finish<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(o, n);
+    return cuda_check(cudaGetLastError(), "finish_run");
+}
+
+int dope_energy4(const dope_lattice *L, const int32_t *y2, int64_t *out, void *stream) {
+    Lat2 o;
+    int rc = build_lat2(L, o, nullptr);
+    if (rc) return rc;
+    if (!y2 || !out) return DOPE_E_ARGS;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n = L->dims[0] * L->dims[1];
+    if ((rc = cuda_check(cudaMemsetAsync(out, 0, sizeof(int64_t), s), "memset"))) return rc;
+    k_energy4<<<grid_for(n), 256, 0, s>>>(o, y2, n, (unsigned long long *)out);
+    return cuda_check(cudaGetLastError(), "energy4");
+}
+
+}  // extern "C"

@@ -1,0 +1,140 @@
+"""GPU parity: the B200 path vs the reference's golden traces and the oracle.
+
+Integer configs must be bit-exact every iteration: block labels, energies,
+max block residual, clamped flag, final y / labels / multipliers.
+residual_sq is a float sum of sqrt(int)^2 (admm.py:295) whose summation order
+is BLAS-specific in the reference, so it is compared at rtol 1e-12.
+"""
+import numpy as np
+import pytest
+
+import paper_1704_03116_b200 as dope
+from paper_1704_03116_b200 import _lib, workloads as W
+from conftest import golden_cases, load_golden, spec_from_golden
+
+pytestmark = pytest.mark.gpu
+
+CASES_2D = [c for c in golden_cases() if c != "mini3d"]
+
+
+def model_from_golden(g):
+    dims = tuple(int(d) for d in g["dims"])
+    if "kpa" in g:
+        kpa = tuple(int(k) for k in g["kpa"])
+    else:
+        kpa = tuple(d // int(b) for d, b in zip(dims, g["block"]))
+    wl = W.Workload("g", dims, (1, 1), int(g["conn"]), g["u"], [1.0] * (2 if len(dims) == 2 else 3),
+                    float(g["lam"]), float(g["rho"]), int(g["max_iters"]), True)
+    rows, cols, vals = wl.pair_arrays()
+    model = dope.EnergyModel(g["u"].astype(np.float64), dope.SparseWeights(wl.n, rows, cols, vals),
+                             float(g["lam"]))
+    part = dope.make_partition(dope.GridShape(dims), kpa, 0)
+    return model, part
+
+
+def test_library_is_the_cuda_build():
+    lb = _lib.lib()
+    assert lb.dope_backend_name() == b"b200-sm100a"
+    import torch
+    assert torch.cuda.is_available()
+
+
+@pytest.mark.parametrize("opts", [dict(warm_start=True, skip_clean=True, use_graph=True),
+                                  dict(warm_start=False, skip_clean=False, use_graph=False),
+                                  dict(warm_start=True, skip_clean=False, use_graph=True),
+                                  dict(warm_start=False, skip_clean=True, use_graph=False)])
+@pytest.mark.parametrize("case", CASES_2D)
+def test_run_matches_reference_trace(case, opts):
+    g = load_golden(f"run_{case}.npz")
+    model, part = model_from_golden(g)
+    cfg = dope.AdmmConfig(mu0=float(g["rho"]), mu_fact=1.0, eps=0.0,
+                          max_iters=int(g["max_iters"]), **opts)
+    labels, state = dope.run(model, part, cfg)
+    assert state.iteration == int(g["iterations"])
+    assert state.converged == bool(g["converged"])
+    assert state.best_iteration == int(g["best_iteration"])
+    e = np.array([t.energy for t in state.trace])
+    assert np.array_equal(e, g["energy"])
+    assert np.array_equal([t.max_block_residual for t in state.trace], g["max_block_residual"])
+    np.testing.assert_allclose([t.residual_sq for t in state.trace], g["residual_sq"], rtol=1e-12)
+    assert np.array_equal([t.clamped for t in state.trace], g["clamped"])
+    assert np.array_equal([t.mu for t in state.trace], g["mu"])
+    assert np.array_equal(state.y, g["y"])
+    assert np.array_equal(labels, g["labels"])
+    assert np.array_equal(state.multipliers_global(), g["a"])
+    hist = np.unpackbits(g["yhat_bits"], axis=1)[:, :model.n]
+    assert np.array_equal(state.labels_global(), hist[-1])
+
+
+@pytest.mark.parametrize("case", ["c1", "mini128_b16", "ragged"])
+def test_step_api_block_labels_every_iteration(case):
+    g = load_golden(f"run_{case}.npz")
+    model, part = model_from_golden(g)
+    problems = dope.assemble_block_problems(model, part)
+    cfg = dope.AdmmConfig(mu0=float(g["rho"]), mu_fact=1.0, eps=0.0, max_iters=int(g["max_iters"]))
+    state = dope.init_state(part, float(g["rho"]))
+    hist = np.unpackbits(g["yhat_bits"], axis=1)[:, :model.n]
+    for it in range(int(g["iterations"])):
+        dope.update_blocks(state, problems, model.lam, cfg)
+        assert np.array_equal(state.labels_global(), hist[it]), it
+        dope.update_global(state, problems, part, model.lam)
+        assert state.clamped_last == bool(g["clamped"][it])
+        res = dope.block_residuals(state, part)
+        assert float(res.max()) == g["max_block_residual"][it]
+        assert dope.evaluate_energy(model, state.y) == g["energy"][it]
+        dope.update_multipliers(state, part, 1.0)
+
+
+def test_bk_maxflow_seam_matches_reference_graphs():
+    g = load_golden("bk_graphs.npz")
+    mo, po = g["m_off"], g["p_off"]
+    mism = 0
+    for k in range(len(mo) - 1):
+        sm, sp = slice(mo[k], mo[k + 1]), slice(po[k], po[k + 1])
+        tcap, cij, cji = g["tcap"][sm], g["cij"][sp], g["cji"][sp]
+        lab, flow = dope.bk_maxflow(tcap, g["pi"][sp], g["pj"][sp], cij, cji)
+        integral = np.all(tcap == np.round(tcap)) and np.all(cij == np.round(cij)) \
+            and np.all(cji == np.round(cji))
+        assert flow == pytest.approx(g["flows"][k], abs=1e-9), k
+        if integral:
+            assert np.array_equal(lab, g["labels"][sm]), k
+        else:
+            mism += int(not np.array_equal(lab, g["labels"][sm]))
+    assert mism == 0
+
+
+def test_bk_maxflow_reference_known_answers():
+    lab, flow = dope.bk_maxflow(np.array([-1.0]), [], [], [], [])
+    assert lab.tolist() == [1] and flow == 0.0
+    lab, flow = dope.bk_maxflow(np.array([2.0, -1.0, 0.0, -0.5]), [], [], [], [])
+    assert lab.tolist() == [0, 1, 0, 1]
+    g = dope.FlowGraph(2)
+    g.add_terminal(0, 4.0, 0.0)
+    g.add_terminal(1, 0.0, 4.0)
+    g.add_edge(0, 1, 1.0, 10.0)
+    labels, flow = dope.min_cut(g)
+    assert flow == pytest.approx(1.0) and labels.tolist() == [0, 1]
+    w = dope.SparseWeights(4, [0, 1, 2], [1, 2, 3], [1.0, 1.0, 1.0])
+    labels, flow = dope.solve_binary(np.zeros(4), w, 1.0)
+    assert flow == 0.0 and len(set(labels.tolist())) == 1
+
+
+@pytest.mark.parametrize("size,block,iters", [(1024, 64, 8), (512, 32, 8), (512, 128, 6)])
+def test_larger_grids_match_oracle(size, block, iters):
+    import oracle as orc
+    wl = W.disks_workload(f"t{size}", size, 16, block, 2, iters, rmin=10, rmax=150, seed=11)
+    rows, cols, vals = wl.pair_arrays()
+    model = dope.EnergyModel(wl.u.astype(np.float64), dope.SparseWeights(wl.n, rows, cols, vals),
+                             wl.lam)
+    part = dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0, materialize=False)
+    cfg = dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=iters)
+    labels, state = dope.run(model, part, cfg)
+    spec = orc.LatticeSpec(wl.dims, wl.kpa, wl.offsets, [1.0, 1.0], wl.u.astype(np.float64),
+                           wl.lam)
+    ref = orc.run(spec, 1.0, 1.0, 0.0, iters, threads=8)
+    assert state.iteration == ref["iterations"]
+    assert np.array_equal([t.energy for t in state.trace], ref["energy"])
+    assert np.array_equal([t.max_block_residual for t in state.trace], ref["max_block_residual"])
+    assert np.array_equal(state.y, ref["y"])
+    assert np.array_equal(labels, ref["labels"])
+    assert np.array_equal(state.labels_global(), ref["yhat"])
