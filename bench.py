@@ -38,7 +38,7 @@ BYTES_PER_PIXEL_ITER = 21      # read u,a,y (int32), write a,y
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--config", default="C3")
@@ -81,7 +81,7 @@ class ClockSampler:
         try:
             self._proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self._proc = None
             return
@@ -202,6 +202,10 @@ def main():
 
     sampler = ClockSampler(local)
     sampler.start()
+    t_wait = time.time()
+    while not sampler.rows and time.time() - t_wait < 5.0:   # sampler running before timing
+        step()
+        torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -228,24 +232,22 @@ def main():
     sweeps_per_run = rs.sweeps
 
     # ---- per-kernel timing pass (CUDA events on the launching stream) ----
-    evs = {"K1_block_mincut": [], "K2_consensus": [], "K3_finalize": []}
+    evs = {"K1_block_mincut": [], "K2_consensus": []}
     dev.call("dope_admm_init")
     stream = torch.cuda.current_stream()
     for it in range(iters_done):
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         e[0].record(stream)
         dev.call("dope_update_blocks")
         e[1].record(stream)
-        dev.call("dope_update_global", fuse=1)
+        dev.call("dope_update_global", fuse=1)      # + fused finalize (last CTA)
         e[2].record(stream)
-        dev.call("dope_reduce_finalize")
-        e[3].record(stream)
         evs["K1_block_mincut"].append((e[0], e[1]))
         evs["K2_consensus"].append((e[1], e[2]))
-        evs["K3_finalize"].append((e[2], e[3]))
     torch.cuda.synchronize()
     kern = {k: [a.elapsed_time(b) for a, b in v] for k, v in evs.items()}
-    kstat = {k: {"total_ms": sum(v), "avg_ms": sum(v) / len(v), "launches": len(v)}
+    kstat = {k: {"total_ms": sum(v), "avg_ms": sum(v) / len(v), "launches": len(v),
+                 "first3_ms": v[:3], "median_ms": statistics.median(v)}
              for k, v in kern.items()}
     dom = max(kstat, key=lambda k: kstat[k]["total_ms"])
     peak, peak_kind = measured_peaks()
@@ -283,7 +285,7 @@ def main():
                 e0.record()
             problems.u.copy_(u_host, non_blocking=True)
             step()
-            lab_host.copy_((dev.y2 >= 1).to(torch.int8), non_blocking=True)
+            lab_host.copy_(dev.binarize().view(torch.int8), non_blocking=True)
             tr_host.copy_(dev.tr_e, non_blocking=True)
         e1.record()
         torch.cuda.synchronize()
@@ -315,7 +317,7 @@ def main():
                        "push_relabel_sweeps_per_run": sweeps_per_run,
                        "kernels": kstat},
             "roofline": roof, "iteration_roofline": iter_roof,
-            "clocks": sampler.summary(), "gpu_launches": 3 * iters * args.steps + 2 * args.steps,
+            "clocks": sampler.summary(), "gpu_launches": (2 * iters_done + 3) * args.steps,
         }
         if e2e:
             line["e2e"] = e2e

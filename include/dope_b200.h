@@ -18,9 +18,11 @@
  *     update_multipliers admm.py:241-248
  *     block_residuals    admm.py:251-257
  *     evaluate_energy    energy.py:187-194              -> dope_update_global()
- *     run bookkeeping    admm.py:283-310 (trace, best, stop)
- *                                                       -> dope_reduce_finalize()
- *     run                admm.py:265-310                -> dope_admm_run()
+ *     run bookkeeping    admm.py:283-310 (trace, best, stop) -> last CTA of
+ *                                                          dope_update_global
+ *     run                admm.py:265-310                -> dope_admm_run(),
+ *                                                          dope_finish_run()
+ *     binarize           admm.py:260-262                -> dope_binarize()
  *
  * Conventions
  *   - Plain pointers and sizes; no framework types.  Device pointers are
@@ -58,18 +60,21 @@ extern "C" {
 /* Device-resident run bookkeeping (one per run; caller allocates
  * sizeof(dope_run_state) bytes of device memory, 8-byte aligned). */
 typedef struct dope_run_state {
-    int64_t best_energy;        /* scaled energy of the best iterate so far   */
+    int64_t best_energy;        /* energy of the best iterate so far           */
     int32_t iteration;          /* iterations completed                        */
     int32_t best_iteration;     /* admm.py:300-303 (strict <)                  */
     int32_t converged;          /* admm.py:305-307                             */
-    int32_t stop;               /* converged or error: later launches no-op    */
-    int32_t copy_best_pending;  /* last iteration set a new best; the next
-                                   consensus pass copies y into ybest          */
+    int32_t stop;               /* converged, error or finished: later
+                                   iteration launches are no-ops               */
+    int32_t ycur;               /* y buffer (0..2) holding the current iterate */
+    int32_t ybest;              /* y buffer holding the best iterate           */
     int32_t parity;             /* which multiplier buffer is current          */
     int32_t error;              /* 0 or 1 + first failing block id             */
     int32_t max_rounds_seen;    /* diagnostics: max global-relabel rounds      */
+    int32_t done_ctas;          /* last-CTA-done counter of the consensus pass */
     int64_t solves;             /* diagnostics: block solves performed         */
     int64_t sweeps;             /* diagnostics: push/relabel sweeps            */
+    int64_t energy_acc;         /* scratch of the end-of-run energy pass       */
 } dope_run_state;
 
 /* Integer lattice problem (C1, C3, C4, C5 of BASELINE.json).
@@ -93,8 +98,8 @@ typedef struct dope_lattice {
     /* caller-owned device buffers */
     const int32_t *u;           /* n   unary                                  */
     int32_t *a[2];              /* n   multipliers, ping-pong by state.parity */
-    int32_t *y2;                /* n   2*y                                    */
-    int32_t *ybest;             /* n   2*y of the best iterate                */
+    int32_t *y2[3];             /* n   2*y; three rotating iterate buffers:
+                                   current, best, and the next output         */
     uint8_t *yhat;              /* n   block labels (global layout)           */
     uint8_t *resid;             /* K * resid_stride bytes: residual graphs    */
     uint32_t *dirty;            /* K   block needs a re-solve                 */
@@ -106,6 +111,9 @@ typedef struct dope_lattice {
     double *trace_residual_sq;  /* max_iters                                  */
     double *trace_max_residual; /* max_iters                                  */
     int32_t *trace_clamped;     /* max_iters                                  */
+    int64_t *timeline;          /* optional (may be NULL): 4 int64 per block of
+                                   the last K1 launch: globaltimer start, end,
+                                   rounds, sweeps (diagnostics only)          */
 } dope_lattice;
 
 /* Library / ABI identification; "b200-sm100a". */
@@ -124,20 +132,23 @@ int dope_admm_init(const dope_lattice *L, void *stream);
 /* update_blocks: one CTA per sub-region computes 2*linear from (u, a, y,
  * y-halo) and solves the block min cut on the GPU; yhat = sink side. */
 int dope_update_blocks(const dope_lattice *L, void *stream);
-/* update_global + block_residuals + energy partials (+ update_multipliers
- * when fuse_multipliers); marks next iteration's dirty blocks. */
+/* update_global + block_residuals (+ update_multipliers when
+ * fuse_multipliers); marks next iteration's dirty blocks.  In run-loop mode
+ * (fuse_multipliers) the last CTA also finalizes the iteration: trace entry,
+ * best iterate (its energy is that of the previous iterate, whose
+ * neighbours are all in HBM already), stop rule. */
 int dope_update_global(const dope_lattice *L, void *stream);
 /* update_multipliers alone (a += yhat - y) for the step-level API. */
 int dope_update_multipliers(const dope_lattice *L, void *stream);
-/* Reduce partials, append the trace entry, track the best iterate, test
- * convergence, advance the iteration counter. */
-int dope_reduce_finalize(const dope_lattice *L, void *stream);
 /* `iters` iterations of blocks -> global -> reduce (no host sync); launches
  * become no-ops once converged.  use_graph: capture one iteration in a CUDA
  * graph and replay it. */
 int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void *stream);
-/* End of run (admm.py:308-310): if not converged, y2 <- ybest. */
+/* End of run (admm.py:300-310): energy + best check of the last iterate;
+ * the current iterate becomes the best one unless converged. */
 int dope_finish_run(const dope_lattice *L, void *stream);
+/* binarize (admm.py:260-262) of the current iterate into out[n] (0/1). */
+int dope_binarize(const dope_lattice *L, uint8_t *out, void *stream);
 /* evaluate_energy of an arbitrary doubled labeling y2 (int path):
  * out[0] = sum u*y2 * 2 + lamw * sum (y2_i - y2_j)^2, i.e. 4*E (exact). */
 int dope_energy4(const dope_lattice *L, const int32_t *y2, int64_t *out, void *stream);

@@ -27,12 +27,15 @@ class RunState(C.Structure):
         ("best_iteration", C.c_int32),
         ("converged", C.c_int32),
         ("stop", C.c_int32),
-        ("copy_best_pending", C.c_int32),
+        ("ycur", C.c_int32),
+        ("ybest", C.c_int32),
         ("parity", C.c_int32),
         ("error", C.c_int32),
         ("max_rounds_seen", C.c_int32),
+        ("done_ctas", C.c_int32),
         ("solves", C.c_int64),
         ("sweeps", C.c_int64),
+        ("energy_acc", C.c_int64),
     ]
 
 
@@ -52,8 +55,7 @@ class Lattice(C.Structure):
         ("fuse_multipliers", C.c_int32),
         ("u", C.c_void_p),
         ("a", C.c_void_p * 2),
-        ("y2", C.c_void_p),
-        ("ybest", C.c_void_p),
+        ("y2", C.c_void_p * 3),
         ("yhat", C.c_void_p),
         ("resid", C.c_void_p),
         ("dirty", C.c_void_p),
@@ -65,6 +67,7 @@ class Lattice(C.Structure):
         ("trace_residual_sq", C.c_void_p),
         ("trace_max_residual", C.c_void_p),
         ("trace_clamped", C.c_void_p),
+        ("timeline", C.c_void_p),
     ]
 
 
@@ -94,12 +97,14 @@ def lib():
     lb.dope_lattice_check.restype = C.c_int
     lb.dope_lattice_check.argtypes = [P]
     for name in ("dope_admm_init", "dope_update_blocks", "dope_update_global",
-                 "dope_update_multipliers", "dope_reduce_finalize", "dope_finish_run"):
+                 "dope_update_multipliers", "dope_finish_run"):
         f = getattr(lb, name)
         f.restype = C.c_int
         f.argtypes = [P, C.c_void_p]
     lb.dope_admm_run.restype = C.c_int
     lb.dope_admm_run.argtypes = [P, C.c_int32, C.c_int32, C.c_void_p]
+    lb.dope_binarize.restype = C.c_int
+    lb.dope_binarize.argtypes = [P, C.c_void_p, C.c_void_p]
     lb.dope_energy4.restype = C.c_int
     lb.dope_energy4.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p]
     lb.dope_bk_maxflow.restype = C.c_int
@@ -128,5 +133,4 @@ def check(rc: int, what: str) -> None:
 def exported_symbols() -> list[str]:
     return ["dope_backend_name", "dope_abi_version", "dope_last_cuda_error", "dope_resid_stride",
             "dope_lattice_check", "dope_admm_init", "dope_update_blocks", "dope_update_global",
-            "dope_update_multipliers", "dope_reduce_finalize", "dope_admm_run",
-            "dope_finish_run", "dope_energy4", "dope_bk_maxflow", "dope_bk_workspace_bytes"]
+            "dope_update_multipliers", "dope_admm_run", "dope_finish_run", "dope_binarize", "dope_energy4", "dope_bk_maxflow", "dope_bk_workspace_bytes"]

@@ -171,8 +171,7 @@ class _DeviceState:
             raise NotImplementedError(f"no K1 kernel variant for block box of {low.dims}/{low.kpa}")
         i32, u8 = torch.int32, torch.uint8
         self.a = [torch.zeros(n, dtype=i32, device=dev), torch.zeros(n, dtype=i32, device=dev)]
-        self.y2 = torch.ones(n, dtype=i32, device=dev)
-        self.ybest = torch.ones(n, dtype=i32, device=dev)
+        self.y2 = [torch.ones(n, dtype=i32, device=dev) for _ in range(3)]
         self.yhat = torch.zeros(n, dtype=u8, device=dev)
         self.resid = torch.zeros(K * stride, dtype=u8, device=dev)
         self.dirty = torch.ones(K, dtype=torch.int32, device=dev)
@@ -187,8 +186,8 @@ class _DeviceState:
         L.u = problems.u.data_ptr()
         L.a[0] = self.a[0].data_ptr()
         L.a[1] = self.a[1].data_ptr()
-        L.y2 = self.y2.data_ptr()
-        L.ybest = self.ybest.data_ptr()
+        for i in range(3):
+            L.y2[i] = self.y2[i].data_ptr()
         L.yhat = self.yhat.data_ptr()
         L.resid = self.resid.data_ptr()
         L.dirty = self.dirty.data_ptr()
@@ -215,6 +214,16 @@ class _DeviceState:
     def run_state(self) -> _lib.RunState:
         raw = self.state.cpu().numpy().tobytes()
         return _lib.RunState.from_buffer_copy(raw)
+
+    def y2_current(self):
+        return self.y2[self.run_state().ycur]
+
+    def binarize(self):
+        import torch
+        out = torch.empty(self.problems.lowering.n, dtype=torch.uint8, device=self.problems.device)
+        lb = _lib.lib()
+        _lib.check(lb.dope_binarize(C.byref(self.L), out.data_ptr(), self.stream()), "dope_binarize")
+        return out
 
     def raise_on_error(self):
         rs = self.run_state()
@@ -257,7 +266,7 @@ class AdmmState:
     def y(self) -> np.ndarray:
         if self._dev is None:
             return np.full(self._n, 0.5)
-        return self._dev.y2.double().div_(2.0).cpu().numpy()
+        return self._dev.y2_current().double().div_(2.0).cpu().numpy()
 
     @y.setter
     def y(self, value):
@@ -267,7 +276,7 @@ class AdmmState:
         v = np.asarray(value, dtype=np.float64)
         if v.shape != (self._n,) or not np.all(np.isin(v, (0.0, 0.5, 1.0))):
             raise NotImplementedError("the integer lattice path holds y in {0, 1/2, 1}")
-        self._dev.y2.copy_(torch.as_tensor((2 * v).astype(np.int32)))
+        self._dev.y2_current().copy_(torch.as_tensor((2 * v).astype(np.int32)))
         self._dev.dirty.fill_(1)
 
     def _global_to_blocks(self, vec: np.ndarray, dtype) -> list:
@@ -398,5 +407,5 @@ def run(model: EnergyModel, partition: Partition, config: AdmmConfig,
     state.converged = bool(rs.converged)
     state.best_iteration = int(rs.best_iteration)
     state.clamped_last = bool(cl[it - 1]) if it else False
-    labels = (dev.y2 >= 1).to(torch.int8).cpu().numpy()
+    labels = dev.binarize().to(torch.int8).cpu().numpy()
     return labels, state

@@ -19,9 +19,12 @@
 //   K3 k_finalize       one CTA: deterministic reduction of the partials, trace
 //                       record, best iterate (strict <), stop rule
 //                       (admm.py:283-307).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <map>
@@ -77,7 +80,8 @@ struct Lat2 {
     int32_t warm, skip_clean, fuse;
     double eps;
     const int32_t *u;
-    int32_t *a0, *a1, *y2, *ybest;
+    int32_t *a0, *a1;
+    int32_t *y2[3];        // rotating iterates: st.ycur (current), st.ybest (best)
     uint8_t *yhat, *resid;
     uint32_t *dirty;
     int64_t *pe, *pr;
@@ -86,6 +90,7 @@ struct Lat2 {
     int64_t *tr_e;
     double *tr_rs, *tr_mr;
     int32_t *tr_cl;
+    int64_t *timeline;
     int32_t max_iters;
     int32_t K;
     int32_t boxh, boxw;     // padded box used for the block layout
@@ -273,6 +278,14 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int k = blockIdx.x;
+    uint64_t t_begin = 0;
+    if (L.timeline && tid == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+        L.timeline[4 * k + 0] = (int64_t)t_begin;
+        L.timeline[4 * k + 1] = (int64_t)t_begin;
+        L.timeline[4 * k + 2] = -1;
+        L.timeline[4 * k + 3] = 0;
+    }
     if (L.st->stop) return;
     if (L.skip_clean) {
         if (L.dirty[k] == 0) return;
@@ -287,6 +300,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
     const int32_t Wg = L.W;
     const int32_t cap = L.cap;
     const int32_t *__restrict__ a_cur = L.st->parity ? L.a1 : L.a0;
+    const int32_t *__restrict__ y_cur = L.y2[L.st->ycur];
     uint8_t *gres = L.resid + (size_t)k * 4 * M;
 
     // ---- prologue: 2*linear (blockform.py:271-272 on the q==1 stencil) ----
@@ -307,12 +321,12 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
         uint8_t re = 0, rw = 0, rs = 0, rn = 0;
         if (valid) {
             const int64_t G = (int64_t)(lo_r + r) * Wg + lo_c + c;
-            const int32_t yg = L.y2[G];
+            const int32_t yg = y_cur[G];
             int32_t s = 0;
-            if (c == 0 && lo_c > 0) s += yg - L.y2[G - 1];
-            if (c == wc - 1 && lo_c + wc < Wg) s += yg - L.y2[G + 1];
-            if (r == 0 && lo_r > 0) s += yg - L.y2[G - Wg];
-            if (r == hr - 1 && lo_r + hr < L.ay.dim) s += yg - L.y2[G + Wg];
+            if (c == 0 && lo_c > 0) s += yg - y_cur[G - 1];
+            if (c == wc - 1 && lo_c + wc < Wg) s += yg - y_cur[G + 1];
+            if (r == 0 && lo_r > 0) s += yg - y_cur[G - Wg];
+            if (r == hr - 1 && lo_r + hr < L.ay.dim) s += yg - y_cur[G + Wg];
             const int32_t lin2 = 2 * L.u[G] + L.lamw * s + L.mu * (2 * a_cur[G] - yg) + L.mu;
             const bool hasE = c + 1 < wc, hasW = c > 0, hasS = r + 1 < hr, hasN = r > 0;
             if (L.warm) {
@@ -446,6 +460,13 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
         const uint4 *src = reinterpret_cast<const uint4 *>(rr);
         for (int i = tid; i < M * 4 / 16; i += NT) dst[i] = src[i];
     }
+    if (tid == 0 && L.timeline) {
+        uint64_t t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        L.timeline[4 * k + 1] = (int64_t)t_end;
+        L.timeline[4 * k + 2] = rounds;
+        L.timeline[4 * k + 3] = sweeps_done;
+    }
     if (tid == 0) {
         atomicAdd((unsigned long long *)&L.st->solves, 1ull);
         atomicAdd((unsigned long long *)&L.st->sweeps, (unsigned long long)sweeps_done);
@@ -475,14 +496,17 @@ __global__ void k_init_resid(Lat2 L) {
 __global__ void k_init_state(Lat2 L, int64_t n) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        L.y2[i] = 1;                 // y = 1/2 (admm.py:163-164)
+        L.y2[0][i] = 1;              // y = 1/2 (admm.py:163-164); best_y = copy
         L.a0[i] = 0;
         L.a1[i] = 0;
-        L.ybest[i] = 1;
         L.yhat[i] = 0;
     }
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.K; i += stride)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.K; i += stride) {
         L.dirty[i] = 1u;
+        L.pe[i] = 0;
+        L.pr[i] = 0;
+        L.pf[i] = 0;
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         dope_run_state s;
         memset(&s, 0, sizeof(s));
@@ -494,22 +518,13 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
 // ---------------------------------------------------------------------------
 // K2: consensus update (2D, 4-connected), one CTA per block
 // ---------------------------------------------------------------------------
-
-__device__ __forceinline__ int32_t new_y_at(const Lat2 &L, const int32_t *__restrict__ a_in,
-                                            int32_t R, int32_t Cc, int32_t *ypre_out) {
-    // y = clamp(yh + a - (lamw/mu) * sum_cross (yh - yh_j))   (admm.py:194-209, 230-238)
-    const int64_t G = (int64_t)R * L.W + Cc;
-    const int32_t yh = L.yhat[G];
-    const int32_t br = L.ay.owner(R), bc = L.ax.owner(Cc);
-    int32_t s = 0;
-    if (Cc > 0 && L.ax.owner(Cc - 1) != bc) s += yh - L.yhat[G - 1];
-    if (Cc + 1 < L.W && L.ax.owner(Cc + 1) != bc) s += yh - L.yhat[G + 1];
-    if (R > 0 && L.ay.owner(R - 1) != br) s += yh - L.yhat[G - L.W];
-    if (R + 1 < L.ay.dim && L.ay.owner(R + 1) != br) s += yh - L.yhat[G + L.W];
-    const int32_t ypre = yh + a_in[G] - L.q * s;
-    if (ypre_out) *ypre_out = ypre;
-    return ypre < 0 ? 0 : (ypre > 1 ? 1 : ypre);
-}
+//
+// Iteration t's K2 reads y_{t-1} (buffer st.ycur), writes y_t into the one
+// buffer that is neither ycur nor st.ybest, and -- because y_{t-1} and all of
+// its neighbours are already in HBM -- also produces the per-block partials of
+// E(y_{t-1}) (energy.py:187-194) for the previous iteration's trace entry.
+// The best iterate is therefore tracked by buffer index: no copies
+// (admm.py:300-303).  The last iterate's energy is taken by dope_finish_run.
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
@@ -518,195 +533,365 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
-__global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
-    extern __shared__ __align__(16) uint8_t smem2[];
-    uint8_t *ys = smem2;                 // box-sized y cache
-    __shared__ int64_t red_e[8], red_s[8];
-    __shared__ int red_f[8];
-    __shared__ int side[5];              // self, left, right, up, down dirty marks
-
-    if (L.st->stop) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nthr = blockDim.x;
-    const int k = blockIdx.x;
-    const int by = k / L.ax.k, bx = k % L.ax.k;
-    int32_t lo_r, hr, lo_c, wc;
-    L.ay.range(by, lo_r, hr);
-    L.ax.range(bx, lo_c, wc);
-    const int BWb = L.boxw;
-    const int M = L.boxh * BWb;
-    const int p = L.st->parity;
-    const int32_t *__restrict__ a_in = p ? L.a1 : L.a0;
-    int32_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
-    const int pending = L.st->copy_best_pending;
-    if (tid < 5) side[tid] = 0;
-    __syncthreads();
-
-    int64_t e_acc = 0, ss = 0;
-    int clamped = 0, chg_self = 0, chgL = 0, chgR = 0, chgU = 0, chgD = 0;
-    for (int v = tid; v < M; v += nthr) {
-        const int r = v / BWb, c = v % BWb;
-        if (r >= hr || c >= wc) continue;
-        const int32_t R = lo_r + r, Cc = lo_c + c;
-        const int64_t G = (int64_t)R * L.W + Cc;
-        int32_t ypre;
-        const int32_t y = new_y_at(L, a_in, R, Cc, &ypre);
-        const int32_t yh = L.yhat[G];
-        const int32_t aold = a_in[G];
-        const int32_t y2old = L.y2[G];
-        clamped |= (ypre < 0 || ypre > 1);
-        if (a_out) a_out[G] = aold + yh - y;
-        L.y2[G] = 2 * y;
-        if (pending) L.ybest[G] = y2old;
-        ys[v] = (uint8_t)y;
-        e_acc += (int64_t)L.u[G] * y;
-        ss += (int64_t)((yh - y) * (yh - y));
-        const bool ychg = (2 * y != y2old);
-        chg_self |= ychg || (yh != y);
-        if (ychg) {
-            chgL |= (c == 0 && lo_c > 0);
-            chgR |= (c == wc - 1 && lo_c + wc < L.W);
-            chgU |= (r == 0 && lo_r > 0);
-            chgD |= (r == hr - 1 && lo_r + hr < L.ay.dim);
-        }
-    }
-    __syncthreads();
-    // pairs owned by this block: (v, right) and (v, down)
-    int64_t quad = 0;
-    for (int v = tid; v < M; v += nthr) {
-        const int r = v / BWb, c = v % BWb;
-        if (r >= hr || c >= wc) continue;
-        const int32_t R = lo_r + r, Cc = lo_c + c;
-        const int32_t y = ys[v];
-        if (c + 1 < wc) {
-            const int32_t d = y - ys[v + 1];
-            quad += d * d;
-        } else if (Cc + 1 < L.W) {
-            const int32_t d = y - new_y_at(L, a_in, R, Cc + 1, nullptr);
-            quad += d * d;
-        }
-        if (r + 1 < hr) {
-            const int32_t d = y - ys[v + BWb];
-            quad += d * d;
-        } else if (R + 1 < L.ay.dim) {
-            const int32_t d = y - new_y_at(L, a_in, R + 1, Cc, nullptr);
-            quad += d * d;
-        }
-    }
-    e_acc += (int64_t)L.lamw * quad;
-    e_acc = warp_sum(e_acc);
-    ss = warp_sum(ss);
-    const int fl = __any_sync(FULLMASK, clamped);
-    if (__any_sync(FULLMASK, chg_self) && lane == 0) side[0] = 1;
-    if (__any_sync(FULLMASK, chgL) && lane == 0) side[1] = 1;
-    if (__any_sync(FULLMASK, chgR) && lane == 0) side[2] = 1;
-    if (__any_sync(FULLMASK, chgU) && lane == 0) side[3] = 1;
-    if (__any_sync(FULLMASK, chgD) && lane == 0) side[4] = 1;
-    if (lane == 0) { red_e[warp] = e_acc; red_s[warp] = ss; red_f[warp] = fl; }
-    __syncthreads();
-    if (tid == 0) {
-        int64_t E = 0, S = 0;
-        int F = 0;
-        for (int w = 0; w < nthr / 32; ++w) { E += red_e[w]; S += red_s[w]; F |= red_f[w]; }
-        L.pe[k] = E;
-        L.pr[k] = S;
-        L.pf[k] = F;
-        if (side[0]) L.dirty[k] = 1u;
-        if (side[1]) L.dirty[k - 1] = 1u;
-        if (side[2]) L.dirty[k + 1] = 1u;
-        if (side[3]) L.dirty[k - L.ax.k] = 1u;
-        if (side[4]) L.dirty[k + L.ax.k] = 1u;
-    }
+__device__ __forceinline__ int other_buffer(int cur, int best) {
+    // the y buffer that is neither the current nor the best iterate
+    if (cur == best) return (cur + 1) % 3;
+    return 3 - cur - best;
 }
 
-// a += yhat - y for the step-level API (admm.py:241-248), in place.
-__global__ void k_update_multipliers(Lat2 L, int64_t n) {
-    int32_t *a = L.st->parity ? L.a1 : L.a0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-        a[i] += (int32_t)L.yhat[i] - (L.y2[i] >> 1);
-}
-
-// ---------------------------------------------------------------------------
-// K3: finalize one iteration (admm.py:289-307)
-// ---------------------------------------------------------------------------
-
-__global__ void __launch_bounds__(1024) k_finalize(Lat2 L) {
+// Reduce the per-block partials into the trace, track the best iterate and
+// test the stop rule (admm.py:289-307); rotate the y buffers.  Executed by the
+// whole last CTA of a consensus launch.  Blocks are assigned to threads by
+// index and combined in a fixed tree, so float sums are deterministic.
+__device__ void finalize_cta(const Lat2 &L, int cur, int best_idx, int out) {
     __shared__ int64_t sE[32];
     __shared__ double sR[32];
     __shared__ int64_t sM[32];
     __shared__ int sF[32];
     dope_run_state *st = L.st;
-    if (st->stop) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int64_t E = 0, mx = -1;
     double rs = 0.0;
     int F = 0;
-    // fixed assignment of blocks to threads and a fixed tree: deterministic
-    for (int k = tid; k < L.K; k += blockDim.x) {
-        E += L.pe[k];
-        const int64_t s = L.pr[k];
-        const double r = sqrt((double)s);
-        rs += r * r;
-        mx = s > mx ? s : mx;
-        F |= L.pf[k];
+    if (L.fuse) {
+        for (int k = tid; k < L.K; k += blockDim.x) {
+            E += __ldcg(&L.pe[k]);
+            const int64_t sq = __ldcg(&L.pr[k]);
+            const double r = sqrt((double)sq);
+            rs += r * r;
+            mx = sq > mx ? sq : mx;
+            F |= __ldcg(&L.pf[k]);
+        }
+        E = warp_sum(E);
+        for (int o = 16; o > 0; o >>= 1) {
+            rs += __shfl_xor_sync(FULLMASK, rs, o);
+            const int64_t t = __shfl_xor_sync(FULLMASK, mx, o);
+            mx = t > mx ? t : mx;
+        }
+        F = __any_sync(FULLMASK, F);
+        if (lane == 0) { sE[warp] = E; sR[warp] = rs; sM[warp] = mx; sF[warp] = F; }
+        __syncthreads();
     }
-    E = warp_sum(E);
-    for (int o = 16; o > 0; o >>= 1) {
-        rs += __shfl_xor_sync(FULLMASK, rs, o);
-        const int64_t t = __shfl_xor_sync(FULLMASK, mx, o);
-        mx = t > mx ? t : mx;
-    }
-    F = __any_sync(FULLMASK, F);
-    if (lane == 0) { sE[warp] = E; sR[warp] = rs; sM[warp] = mx; sF[warp] = F; }
-    __syncthreads();
     if (tid == 0) {
-        int64_t E2 = 0, M2 = -1;
-        double R2 = 0.0;
-        int F2 = 0;
-        const int nw = blockDim.x / 32;
-        for (int w = 0; w < nw; ++w) {
-            E2 += sE[w];
-            R2 += sR[w];
-            M2 = sM[w] > M2 ? sM[w] : M2;
-            F2 |= sF[w];
+        int bidx = best_idx;
+        if (L.fuse) {
+            int64_t E2 = 0, M2 = -1;
+            double R2 = 0.0;
+            int F2 = 0;
+            const int nw = blockDim.x / 32;
+            for (int w = 0; w < nw; ++w) {
+                E2 += sE[w];
+                R2 += sR[w];
+                M2 = sM[w] > M2 ? sM[w] : M2;
+                F2 |= sF[w];
+            }
+            const int t = st->iteration;        // iterations completed before this one
+            if (t >= 1) {                       // E2 = E(y_t): trace entry of iteration t
+                if (t - 1 < L.max_iters) L.tr_e[t - 1] = E2;
+                if (E2 < st->best_energy) {
+                    st->best_energy = E2;
+                    st->best_iteration = t;
+                    bidx = cur;
+                }
+            }
+            const double maxres = M2 < 0 ? 0.0 : sqrt((double)M2);
+            if (t < L.max_iters) {
+                L.tr_rs[t] = R2;
+                L.tr_mr[t] = maxres;
+                L.tr_cl[t] = F2;
+            }
+            st->parity ^= 1;
+            st->iteration = t + 1;
+            if (L.K == 0 || maxres <= L.eps) {
+                st->converged = 1;
+                st->stop = 1;
+            }
+            if (st->error) st->stop = 1;
         }
-        const int t = st->iteration;
-        const double maxres = M2 < 0 ? 0.0 : sqrt((double)M2);
-        if (t < L.max_iters) {
-            L.tr_e[t] = E2;
-            L.tr_rs[t] = R2;
-            L.tr_mr[t] = maxres;
-            L.tr_cl[t] = F2;
-        }
-        if (E2 < st->best_energy) {
-            st->best_energy = E2;
-            st->best_iteration = t + 1;
-            st->copy_best_pending = 1;
-        } else {
-            st->copy_best_pending = 0;
-        }
-        if (L.fuse) st->parity ^= 1;
-        st->iteration = t + 1;
-        if (L.K == 0 || maxres <= L.eps) {
-            st->converged = 1;
-            st->stop = 1;
-        }
-        if (st->error) st->stop = 1;
+        st->ybest = bidx;
+        st->ycur = out;
     }
 }
 
-// end of run: pending best copy, then state.y = best_y when not converged
-__global__ void k_finish(Lat2 L, int64_t n) {
-    const dope_run_state *st = L.st;
-    const int pending = st->copy_best_pending;
-    const int conv = st->converged;
+// Per-CTA epilogue shared by the consensus kernels: reduce the thread
+// partials, publish the block's partials and dirty marks; the last CTA to
+// arrive runs finalize_cta.
+__device__ __forceinline__ void consensus_epilogue(const Lat2 &L, int k, int64_t e_acc, int64_t ss,
+                                                   int clamped, int chg_self, int chgL, int chgR,
+                                                   int chgU, int chgD, int cur, int best, int out) {
+    __shared__ int64_t red_e[32], red_s[32];
+    __shared__ int red_f[32];
+    __shared__ int last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    e_acc = warp_sum(e_acc);
+    ss = warp_sum(ss);
+    const unsigned fl = __ballot_sync(FULLMASK, clamped) ? 1u : 0u;
+    const unsigned f0 = __ballot_sync(FULLMASK, chg_self) ? 2u : 0u;
+    const unsigned f1 = __ballot_sync(FULLMASK, chgL) ? 4u : 0u;
+    const unsigned f2 = __ballot_sync(FULLMASK, chgR) ? 8u : 0u;
+    const unsigned f3 = __ballot_sync(FULLMASK, chgU) ? 16u : 0u;
+    const unsigned f4 = __ballot_sync(FULLMASK, chgD) ? 32u : 0u;
+    if (lane == 0) {
+        red_e[warp] = e_acc;
+        red_s[warp] = ss;
+        red_f[warp] = (int)(fl | f0 | f1 | f2 | f3 | f4);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int64_t E = 0, S = 0;
+        int Fm = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { E += red_e[w]; S += red_s[w]; Fm |= red_f[w]; }
+        L.pe[k] = E;
+        L.pr[k] = S;
+        L.pf[k] = Fm & 1;
+        if (Fm & 2) L.dirty[k] = 1u;
+        if (Fm & 4) L.dirty[k - 1] = 1u;
+        if (Fm & 8) L.dirty[k + 1] = 1u;
+        if (Fm & 16) L.dirty[k - L.ax.k] = 1u;
+        if (Fm & 32) L.dirty[k + L.ax.k] = 1u;
+        __threadfence();
+        const int prev = atomicAdd(&L.st->done_ctas, 1);
+        last = (prev == L.K - 1);
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        finalize_cta(L, cur, best, out);
+        if (threadIdx.x == 0) L.st->done_ctas = 0;
+    }
+}
+
+// Generic consensus (any tiling, incl. ragged): one CTA per block, scalar.
+__global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
+    if (L.st->stop) return;
+    const int tid = threadIdx.x;
+    const int k = blockIdx.x;
+    const int by = k / L.ax.k, bx = k % L.ax.k;
+    int32_t lo_r, hr, lo_c, wc;
+    L.ay.range(by, lo_r, hr);
+    L.ax.range(bx, lo_c, wc);
+    const int32_t W = L.W, H = L.ay.dim;
+    const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
+    const int32_t *__restrict__ y_in = L.y2[cur];
+    int32_t *__restrict__ y_out = L.y2[out];
+    const int p = L.st->parity;
+    const int32_t *__restrict__ a_in = p ? L.a1 : L.a0;
+    int32_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
+    const bool want_e = L.fuse && L.st->iteration >= 1;
+    const bool has_up = lo_r > 0, has_dn = lo_r + hr < H, has_lf = lo_c > 0, has_rt = lo_c + wc < W;
+
+    int64_t e_acc = 0, ss = 0;
+    int clamped = 0, chg_self = 0, chgL = 0, chgR = 0, chgU = 0, chgD = 0;
+    const int m = hr * wc;
+    for (int v = tid; v < m; v += blockDim.x) {
+        const int r = v / wc, c = v - r * wc;
+        const int32_t R = lo_r + r, Cc = lo_c + c;
+        const int64_t G = (int64_t)R * W + Cc;
+        const int32_t yh = L.yhat[G];
+        int32_t s = 0;
+        if (c == 0 && has_lf) s += yh - L.yhat[G - 1];
+        if (c == wc - 1 && has_rt) s += yh - L.yhat[G + 1];
+        if (r == 0 && has_up) s += yh - L.yhat[G - W];
+        if (r == hr - 1 && has_dn) s += yh - L.yhat[G + W];
+        const int32_t aold = a_in[G];
+        const int32_t ypre = yh + aold - L.q * s;
+        const int32_t y = ypre < 0 ? 0 : (ypre > 1 ? 1 : ypre);
+        const int32_t y2old = y_in[G];
+        clamped |= (ypre < 0 || ypre > 1);
+        if (a_out) a_out[G] = aold + yh - y;
+        y_out[G] = 2 * y;
+        ss += (yh - y) * (yh - y);
+        if (want_e) {
+            const int32_t o = y2old >> 1;
+            int32_t qd = 0;
+            if (Cc + 1 < W) qd += o ^ (y_in[G + 1] >> 1);
+            if (R + 1 < H) qd += o ^ (y_in[G + W] >> 1);
+            e_acc += (int64_t)L.u[G] * o + (int64_t)L.lamw * qd;
+        }
+        const bool ychg = (2 * y != y2old);
+        chg_self |= ychg || (yh != y);
+        if (ychg) {
+            chgL |= (c == 0 && has_lf);
+            chgR |= (c == wc - 1 && has_rt);
+            chgU |= (r == 0 && has_up);
+            chgD |= (r == hr - 1 && has_dn);
+        }
+    }
+    consensus_epilogue(L, k, e_acc, ss, clamped, chg_self, chgL, chgR, chgU, chgD, cur, best, out);
+}
+
+__device__ __forceinline__ int byte_of(uint32_t w, int i) { return (int)((w >> (8 * i)) & 0xFFu); }
+
+// Vectorized consensus for uniform tilings whose block width is a power of
+// two in [4, 128] and grid width a multiple of 4.  Thread t owns up to QPT
+// quads (4 consecutive pixels of a block row); the quads of one block row sit
+// in consecutive lanes of one warp.  All loads of a thread are issued before
+// any is used; nothing goes through shared memory.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
+    constexpr int QPT = 4;
+    if (L.st->stop) return;
+    const int tid = threadIdx.x;
+    const int k = blockIdx.x;
+    const int by = k / L.ax.k, bx = k - by * L.ax.k;
+    int32_t lo_r, hr, lo_c, wc;
+    L.ay.range(by, lo_r, hr);
+    L.ax.range(bx, lo_c, wc);
+    const int32_t W = L.W, H = L.ay.dim;
+    const int QR = 1 << lq;              // quads per block row
+    const int nq = hr << lq;
+    const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
+    const int32_t *__restrict__ y_in = L.y2[cur];
+    int32_t *__restrict__ y_out = L.y2[out];
+    const int p = L.st->parity;
+    const int32_t *__restrict__ a_in = p ? L.a1 : L.a0;
+    int32_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
+    const bool want_e = L.fuse && L.st->iteration >= 1;
+    const int32_t q = L.q;
+    const bool has_up = lo_r > 0, has_dn = lo_r + hr < H, has_lf = lo_c > 0, has_rt = lo_c + wc < W;
+
+    // ---- issue every load of this thread's quads ----
+    uint32_t yh4[QPT], up4[QPT], dn4[QPT];
+    int4 av[QPT], yo[QPT], uu[QPT], yb[QPT];
+    int lf[QPT], rt[QPT], yr[QPT];
+#pragma unroll
+    for (int j = 0; j < QPT; ++j) {
+        const int t = tid + j * NT;
+        yh4[j] = 0; up4[j] = 0; dn4[j] = 0; lf[j] = 0; rt[j] = 0; yr[j] = 0;
+        av[j] = make_int4(0, 0, 0, 0); yo[j] = av[j]; uu[j] = av[j]; yb[j] = av[j];
+        if (t < nq) {
+            const int r = t >> lq, c0 = (t & (QR - 1)) << 2;
+            const int64_t G = (int64_t)(lo_r + r) * W + lo_c + c0;
+            yh4[j] = __ldcs(reinterpret_cast<const unsigned int *>(L.yhat + G));
+            av[j] = __ldcs(reinterpret_cast<const int4 *>(a_in + G));
+            yo[j] = __ldcg(reinterpret_cast<const int4 *>(y_in + G));
+            uu[j] = __ldg(reinterpret_cast<const int4 *>(L.u + G));
+            if (want_e && lo_r + r + 1 < H) yb[j] = __ldcg(reinterpret_cast<const int4 *>(y_in + G + W));
+            if (r == 0 && has_up) up4[j] = *reinterpret_cast<const uint32_t *>(L.yhat + G - W);
+            if (r == hr - 1 && has_dn) dn4[j] = *reinterpret_cast<const uint32_t *>(L.yhat + G + W);
+            if (c0 == 0 && has_lf) lf[j] = L.yhat[G - 1];
+            if (c0 + 4 == wc && has_rt) {
+                rt[j] = L.yhat[G + 4];
+                if (want_e) yr[j] = y_in[G + 4];
+            }
+        }
+    }
+
+    // ---- consensus update + energy of the previous iterate ----
+    int e_acc = 0, ss = 0, quad = 0;
+    int clamped = 0, chg_self = 0, chgL = 0, chgR = 0, chgU = 0, chgD = 0;
+#pragma unroll
+    for (int j = 0; j < QPT; ++j) {
+        const int t = tid + j * NT;
+        const bool valid = t < nq;
+        const int r = t >> lq, c0 = (t & (QR - 1)) << 2;
+        // previous iterate as packed bits (y2 in {0,2} once t >= 1)
+        const uint32_t ob = (uint32_t)((yo[j].x >> 1) | ((yo[j].y >> 1) << 1) |
+                                       ((yo[j].z >> 1) << 2) | ((yo[j].w >> 1) << 3));
+        const uint32_t nxt = __shfl_down_sync(FULLMASK, ob, 1);
+        if (!valid) continue;
+        const int64_t G = (int64_t)(lo_r + r) * W + lo_c + c0;
+        const bool top = (r == 0 && has_up), bot = (r == hr - 1 && has_dn);
+        const bool lft = (c0 == 0 && has_lf), rgt = (c0 + 4 == wc && has_rt);
+        if (want_e) {
+            const uint32_t bb = (uint32_t)((yb[j].x >> 1) | ((yb[j].y >> 1) << 1) |
+                                           ((yb[j].z >> 1) << 2) | ((yb[j].w >> 1) << 3));
+            quad += __popc((ob ^ (ob >> 1)) & 0x7u);            // pairs inside the quad
+            if (c0 + 4 < wc) quad += (int)((ob >> 3) ^ (nxt & 1u));
+            else if (rgt) quad += (int)((ob >> 3) ^ (uint32_t)(yr[j] >> 1));
+            if (lo_r + r + 1 < H) quad += __popc(ob ^ bb);
+            e_acc += (ob & 1u ? uu[j].x : 0) + (ob & 2u ? uu[j].y : 0) + (ob & 4u ? uu[j].z : 0) +
+                     (ob & 8u ? uu[j].w : 0);
+        }
+        const int a4[4] = {av[j].x, av[j].y, av[j].z, av[j].w};
+        const int y24[4] = {yo[j].x, yo[j].y, yo[j].z, yo[j].w};
+        int y[4], an[4];
+        bool ychg_any = false;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int yh = byte_of(yh4[j], i);
+            int sx = 0;
+            if (top) sx += yh - byte_of(up4[j], i);
+            if (bot) sx += yh - byte_of(dn4[j], i);
+            if (i == 0 && lft) sx += yh - lf[j];
+            if (i == 3 && rgt) sx += yh - rt[j];
+            const int ypre = yh + a4[i] - q * sx;
+            clamped |= (unsigned)ypre > 1u;
+            y[i] = ypre < 0 ? 0 : (ypre > 1 ? 1 : ypre);
+            an[i] = a4[i] + yh - y[i];
+            ss += yh ^ y[i];
+            const bool ychg = (2 * y[i] != y24[i]);
+            ychg_any |= ychg;
+            chg_self |= ychg | (yh != y[i]);
+        }
+        if (a_out) __stcs(reinterpret_cast<int4 *>(a_out + G), make_int4(an[0], an[1], an[2], an[3]));
+        __stcg(reinterpret_cast<int4 *>(y_out + G), make_int4(2 * y[0], 2 * y[1], 2 * y[2], 2 * y[3]));
+        if (ychg_any) {
+            chgU |= top;
+            chgD |= bot;
+            chgL |= (lft && (2 * y[0] != y24[0]));
+            chgR |= (rgt && (2 * y[3] != y24[3]));
+        }
+    }
+    const int64_t e64 = (int64_t)e_acc + (int64_t)L.lamw * quad;
+    consensus_epilogue(L, k, e64, (int64_t)ss, clamped, chg_self, chgL, chgR, chgU, chgD, cur, best,
+                       out);
+}
+
+// a += yhat - y for the step-level API (admm.py:241-248), in place.
+__global__ void k_update_multipliers(Lat2 L, int64_t n) {
+    int32_t *a = L.st->parity ? L.a1 : L.a0;
+    const int32_t *y2 = L.y2[L.st->ycur];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        a[i] += (int32_t)L.yhat[i] - (y2[i] >> 1);
+}
+
+// E = u.y + lamw * sum_pairs (y_i - y_j)^2 of the current iterate (y in {0,1})
+// accumulated into st.energy_acc (exact integer sum: order-free).
+__global__ void k_energy_current(Lat2 L, int64_t n) {
+    const int32_t *y2 = L.y2[L.st->ycur];
+    int64_t acc = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        int32_t yb = pending ? L.y2[i] : L.ybest[i];
-        if (pending) L.ybest[i] = yb;
-        if (!conv) L.y2[i] = yb;
+        const int32_t c = (int32_t)(i % L.W);
+        const int64_t r = i / L.W;
+        const int32_t yi = y2[i] >> 1;
+        int32_t qd = 0;
+        if (c + 1 < L.W) qd += yi ^ (y2[i + 1] >> 1);
+        if (r + 1 < L.ay.dim) qd += yi ^ (y2[i + L.W] >> 1);
+        acc += (int64_t)L.u[i] * yi + (int64_t)L.lamw * qd;
     }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0)
+        atomicAdd((unsigned long long *)&L.st->energy_acc, (unsigned long long)acc);
+}
+
+// End of run (admm.py:300-310): trace energy + best check of the last
+// iterate, then state.y = best iterate unless converged.
+__global__ void k_finish_decide(Lat2 L) {
+    dope_run_state *st = L.st;
+    const int T = st->iteration;
+    if (T >= 1 && !st->error) {
+        const int64_t E = st->energy_acc;
+        if (T - 1 < L.max_iters) L.tr_e[T - 1] = E;
+        if (E < st->best_energy) {
+            st->best_energy = E;
+            st->best_iteration = T;
+            st->ybest = st->ycur;
+        }
+    }
+    st->energy_acc = 0;
+    if (!st->converged) st->ycur = st->ybest;
+    st->stop = 1;
+}
+
+// binarize (admm.py:260-262) of the current iterate: y >= 1/2 -> 1
+__global__ void k_binarize(Lat2 L, int64_t n, uint8_t *out) {
+    const int32_t *y2 = L.y2[L.st->ycur];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = (uint8_t)(y2[i] >= 1);
 }
 
 // 4*E of an arbitrary doubled labeling (y2 = 2y): 2*sum u*y2 + lamw*sum (y2_i-y2_j)^2
@@ -718,14 +903,16 @@ __global__ void k_energy4(Lat2 L, const int32_t *__restrict__ y2, int64_t n,
         const int32_t c = (int32_t)(i % L.W);
         const int64_t r = i / L.W;
         const int32_t yi = y2[i];
-        int64_t q = 0;
-        if (c + 1 < L.W) { const int64_t d = yi - y2[i + 1]; q += d * d; }
-        if (r + 1 < L.ay.dim) { const int64_t d = yi - y2[i + L.W]; q += d * d; }
-        acc += 2 * (int64_t)L.u[i] * yi + (int64_t)L.lamw * q;
+        int64_t qd = 0;
+        if (c + 1 < L.W) { const int64_t d = yi - y2[i + 1]; qd += d * d; }
+        if (r + 1 < L.ay.dim) { const int64_t d = yi - y2[i + L.W]; qd += d * d; }
+        acc += 2 * (int64_t)L.u[i] * yi + (int64_t)L.lamw * qd;
     }
     acc = warp_sum(acc);
     if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)acc);
 }
+
+#include "consensus_tma.cuh"
 
 // ---------------------------------------------------------------------------
 // Host side
@@ -755,7 +942,7 @@ static const Variant *pick_variant(int maxh, int maxw) {
 }
 
 static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var) {
-    if (!L || !L->u || !L->a[0] || !L->a[1] || !L->y2 || !L->ybest || !L->yhat || !L->resid ||
+    if (!L || !L->u || !L->a[0] || !L->a[1] || !L->y2[0] || !L->y2[1] || !L->y2[2] || !L->yhat || !L->resid ||
         !L->dirty || !L->part_energy || !L->part_ressq || !L->part_flags || !L->state)
         return DOPE_E_ARGS;
     if (L->ndim != 2 || L->conn != 4) return DOPE_E_GEOMETRY;
@@ -779,8 +966,9 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var) {
     o.u = L->u;
     o.a0 = L->a[0];
     o.a1 = L->a[1];
-    o.y2 = L->y2;
-    o.ybest = L->ybest;
+    o.y2[0] = L->y2[0];
+    o.y2[1] = L->y2[1];
+    o.y2[2] = L->y2[2];
     o.yhat = L->yhat;
     o.resid = L->resid;
     o.dirty = L->dirty;
@@ -792,6 +980,7 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var) {
     o.tr_rs = L->trace_residual_sq;
     o.tr_mr = L->trace_max_residual;
     o.tr_cl = L->trace_clamped;
+    o.timeline = L->timeline;
     o.max_iters = L->max_iters;
     o.K = L->kpa[0] * L->kpa[1];
     const int maxh = o.ay.base + (o.ay.rem ? 1 : 0);
@@ -832,15 +1021,102 @@ static int launch_k1(const Lat2 &o, const Variant *v, cudaStream_t s) {
     return cuda_check(cudaGetLastError(), "launch K1");
 }
 
-static int launch_k2(const Lat2 &o, cudaStream_t s) {
-    const size_t smem = (size_t)o.boxh * o.boxw;
-    k_consensus<<<o.K, 256, smem, s>>>(o);
-    return cuda_check(cudaGetLastError(), "launch K2");
+static int k2_lq(const Lat2 &o) {
+    // log2(quads per block row) when the vector kernel applies, else -1
+    if (o.W % 4 != 0 || o.ax.rem != 0) return -1;
+    for (int lq = 0; lq <= 5; ++lq)
+        if (o.ax.base == (4 << lq)) return lq;
+    return -1;
 }
 
-static int launch_k3(const Lat2 &o, cudaStream_t s) {
-    k_finalize<<<1, 1024, 0, s>>>(o);
-    return cuda_check(cudaGetLastError(), "launch K3");
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    return fn;
+}
+
+static bool make_map(CUtensorMap *m, CUtensorMapDataType dt, int esize, void *base, int64_t W,
+                     int64_t H, int bw, int bh) {
+    auto enc = tmap_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)H};
+    cuuint64_t strides[1] = {(cuuint64_t)(W * esize)};
+    cuuint32_t box[2] = {(cuuint32_t)bw, (cuuint32_t)bh};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, dt, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// persistent TMA consensus: run-loop mode, uniform tiling, 64/128-wide blocks
+template <int TW>
+static int launch_k2_tma(const Lat2 &o, cudaStream_t s) {
+    using C = TmaCfg<TW>;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(k_consensus_tma<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    });
+    TmaMaps M;
+    const int64_t W = o.W, H = o.ay.dim;
+    bool ok = make_map(&M.u, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, (void *)o.u, W, H, TW, C::TH);
+    ok = ok && make_map(&M.a[0], CU_TENSOR_MAP_DATA_TYPE_INT32, 4, o.a0, W, H, TW, C::TH);
+    ok = ok && make_map(&M.a[1], CU_TENSOR_MAP_DATA_TYPE_INT32, 4, o.a1, W, H, TW, C::TH);
+    for (int i = 0; i < 3 && ok; ++i) {
+        ok = make_map(&M.y[i], CU_TENSOR_MAP_DATA_TYPE_INT32, 4, o.y2[i], W, H, TW, C::TH + 1);
+        ok = ok && make_map(&M.yr[i], CU_TENSOR_MAP_DATA_TYPE_INT32, 4, o.y2[i], W, H, 4, C::TH);
+    }
+    ok = ok && make_map(&M.yhat, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.yhat, W, H, C::YHW, C::TH + 2);
+    if (!ok) {
+        snprintf(g_last_err, sizeof(g_last_err), "cuTensorMapEncodeTiled failed");
+        return DOPE_E_CUDA;
+    }
+    const int grid = o.K < sm_count() ? o.K : sm_count();
+    k_consensus_tma<TW><<<grid, C::NT, C::SMEM, s>>>(o, M);
+    return cuda_check(cudaGetLastError(), "launch K2 (tma)");
+}
+
+static int k2_tma_width(const Lat2 &o) {
+    // eligible: run-loop mode, uniform tiling, 64/128-wide blocks, TMA-friendly strides
+    if (!o.fuse || o.ax.rem != 0 || o.ay.rem != 0 || (o.W % 16) != 0) return 0;
+    if (o.ax.base == 64 && o.ay.base % 64 == 0) return 64;
+    if (o.ax.base == 128 && o.ay.base % 32 == 0) return 128;
+    return 0;
+}
+
+static int launch_k2(const Lat2 &o, cudaStream_t s) {
+    const int tw = k2_tma_width(o);
+    if (tw == 64 && !getenv("DOPE_NO_TMA")) return launch_k2_tma<64>(o, s);
+    if (tw == 128 && !getenv("DOPE_NO_TMA")) return launch_k2_tma<128>(o, s);
+    const int lq = k2_lq(o);
+    if (lq >= 0) {
+        const int64_t quads = (int64_t)(o.ay.base + (o.ay.rem ? 1 : 0)) << lq;
+        if (quads <= 4 * 32) k_consensus_vec<32><<<o.K, 32, 0, s>>>(o, lq);
+        else if (quads <= 4 * 64) k_consensus_vec<64><<<o.K, 64, 0, s>>>(o, lq);
+        else if (quads <= 4 * 256) k_consensus_vec<256><<<o.K, 256, 0, s>>>(o, lq);
+        else if (quads <= 4 * 1024) k_consensus_vec<1024><<<o.K, 1024, 0, s>>>(o, lq);
+        else k_consensus<<<o.K, 256, 0, s>>>(o);
+    } else {
+        k_consensus<<<o.K, 256, 0, s>>>(o);
+    }
+    return cuda_check(cudaGetLastError(), "launch K2");
 }
 
 static int grid_for(int64_t n) {
@@ -910,13 +1186,6 @@ int dope_update_multipliers(const dope_lattice *L, void *stream) {
     return cuda_check(cudaGetLastError(), "update_multipliers");
 }
 
-int dope_reduce_finalize(const dope_lattice *L, void *stream) {
-    Lat2 o;
-    int rc = build_lat2(L, o, nullptr);
-    if (rc) return rc;
-    return launch_k3(o, (cudaStream_t)stream);
-}
-
 int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void *stream) {
     Lat2 o;
     const Variant *v;
@@ -928,7 +1197,6 @@ int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void 
         for (int i = 0; i < iters; ++i) {
             if ((rc = launch_k1(o, v, s))) return rc;
             if ((rc = launch_k2(o, s))) return rc;
-            if ((rc = launch_k3(o, s))) return rc;
         }
         return DOPE_OK;
     }
@@ -953,7 +1221,6 @@ int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void 
         for (int i = 0; i < iters && !rc; ++i) {
             rc = launch_k1(o, v, cs);
             if (!rc) rc = launch_k2(o, cs);
-            if (!rc) rc = launch_k3(o, cs);
         }
         cudaError_t e = cudaStreamEndCapture(cs, &graph);
         if (rc) return rc;
@@ -973,8 +1240,21 @@ int dope_finish_run(const dope_lattice *L, void *stream) {
     int rc = build_lat2(L, o, nullptr);
     if (rc) return rc;
     const int64_t n = L->dims[0] * L->dims[1];
-    k_finish<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(o, n);
-    return cuda_check(cudaGetLastError(), "finish_run");
+    cudaStream_t s = (cudaStream_t)stream;
+    k_energy_current<<<grid_for(n), 256, 0, s>>>(o, n);
+    if ((rc = cuda_check(cudaGetLastError(), "energy_current"))) return rc;
+    k_finish_decide<<<1, 1, 0, s>>>(o);
+    return cuda_check(cudaGetLastError(), "finish_decide");
+}
+
+int dope_binarize(const dope_lattice *L, uint8_t *out, void *stream) {
+    Lat2 o;
+    int rc = build_lat2(L, o, nullptr);
+    if (rc) return rc;
+    if (!out) return DOPE_E_ARGS;
+    const int64_t n = L->dims[0] * L->dims[1];
+    k_binarize<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(o, n, out);
+    return cuda_check(cudaGetLastError(), "binarize");
 }
 
 int dope_energy4(const dope_lattice *L, const int32_t *y2, int64_t *out, void *stream) {

@@ -1,0 +1,52 @@
+"""Per-block K1 timeline on C3 (diagnostics): which iterations/blocks dominate."""
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from bench import build_problem  # noqa: E402
+from paper_1704_03116_b200 import workloads as W  # noqa: E402
+from paper_1704_03116_b200.admm import _DeviceState  # noqa: E402
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "C3"
+    iters = int(sys.argv[2]) if len(sys.argv) > 2 else 12
+    torch.cuda.set_device(0)
+    wl = W.by_name(name)
+    _, _, problems = build_problem(wl, torch.device("cuda", 0))
+    dev = _DeviceState(problems, int(wl.rho), 0.0, iters, True, True)
+    K = wl.num_blocks
+    tl = torch.zeros(4 * K, dtype=torch.int64, device="cuda")
+    dev.L.timeline = tl.data_ptr()
+    dev.call("dope_admm_init")
+    for it in range(iters):
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        dev.call("dope_update_blocks")
+        e1.record()
+        dev.call("dope_update_global", fuse=1)
+        e2.record()
+        torch.cuda.synchronize()
+        t = tl.view(K, 4).cpu().numpy()
+        solved = t[:, 2] >= 0
+        t0 = t[:, 0].min()
+        dur = (t[:, 1] - t[:, 0]) / 1e3
+        ends = (t[:, 1] - t0) / 1e3
+        starts = (t[:, 0] - t0) / 1e3
+        ds = dur[solved]
+        print(f"it {it+1:3d}: K1 {e0.elapsed_time(e1)*1e3:7.1f} us  K2 {e1.elapsed_time(e2)*1e3:6.1f} us | "
+              f"solved {solved.sum():5d}  block us: med {np.median(ds) if ds.size else 0:6.1f} "
+              f"p90 {np.percentile(ds,90) if ds.size else 0:6.1f} max {ds.max() if ds.size else 0:6.1f} | "
+              f"last start {starts.max():6.1f} last end {ends.max():6.1f} | rounds max {t[:,2].max()} "
+              f"sweeps med {np.median(t[solved,3]) if solved.any() else 0:.0f} max {t[:,3].max()}")
+    rs = dev.raise_on_error()
+    print("state", rs.iteration, rs.best_energy)
+
+
+if __name__ == "__main__":
+    main()
