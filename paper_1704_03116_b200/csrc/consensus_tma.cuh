@@ -23,8 +23,8 @@ struct TmaMaps {
 template <int TW>
 struct TmaCfg {
     static constexpr int TH = 4096 / TW;                 // tile rows (64 or 32)
-    static constexpr int NT = 256;
-    static constexpr int QPT = TH * TW / 4 / NT;         // quads per thread (4)
+    static constexpr int NT = 512;
+    static constexpr int QPT = TH * TW / 4 / NT;         // quads per thread (2)
     static constexpr int YHW = TW + 32;                  // label box width (bytes)
     static constexpr int B_U = TW * TH * 4;
     static constexpr int B_A = TW * TH * 4;
@@ -79,9 +79,8 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
 
 template <int TW>
 __device__ __forceinline__ void tma_issue_tile(const Lat2 &L, const TmaMaps &M, uint8_t *stage,
-                                               uint64_t *bar, int k, int tile, int cur, int p) {
+                                               uint64_t *bar, int by, int bx, int tile, int cur, int p) {
     using C = TmaCfg<TW>;
-    const int by = k / L.ax.k, bx = k - by * L.ax.k;
     const int x0 = bx * TW;                       // uniform tiling: lo = index * width
     const int y0 = by * L.ay.base + tile * C::TH;
     mbar_expect_tx(bar, C::TX);
@@ -92,8 +91,14 @@ __device__ __forceinline__ void tma_issue_tile(const Lat2 &L, const TmaMaps &M, 
     tma_load_2d(stage + C::O_H, &M.yhat, bar, x0 - 16, y0 - 1);
 }
 
+// packed old-iterate bits of a quad: y2 in {0,2} -> bit i = y_i
+__device__ __forceinline__ uint32_t pack_y2(const int4 v) {
+    return (uint32_t)((v.x | (v.y << 1) | (v.z << 2) | (v.w << 3)) >> 1);
+}
+
 template <int TW>
-__global__ void __launch_bounds__(256, 1) k_consensus_tma(Lat2 L, const __grid_constant__ TmaMaps M) {
+__global__ void __launch_bounds__(512, 1) k_consensus_tma(Lat2 L, const __grid_constant__ TmaMaps M,
+                                                          uint32_t kx_magic) {
     using C = TmaCfg<TW>;
     constexpr int TH = C::TH, NT = C::NT, QPT = C::QPT, QR = TW / 4, LQ = (TW == 64) ? 4 : 5;
     extern __shared__ __align__(128) uint8_t smem_t[];
@@ -109,128 +114,153 @@ __global__ void __launch_bounds__(256, 1) k_consensus_tma(Lat2 L, const __grid_c
     int32_t *__restrict__ y_out = L.y2[out];
     int32_t *__restrict__ a_out = p ? L.a0 : L.a1;
     const bool want_e = st->iteration >= 1;
-    const int32_t W = L.W, H = L.ay.dim, q = L.q, BH = L.ay.base;
-    const int tiles_per_block = BH / TH;
-    const int nblk = (L.K - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-    const int ntiles = nblk * tiles_per_block;
+    const int32_t W = L.W, H = L.ay.dim, q = L.q, BH = L.ay.base, KX = L.ax.k;
+    const int tpb = BH / TH;                          // tiles per block
+    const int G0 = gridDim.x;
+    const int nblk = (L.K - (int)blockIdx.x + G0 - 1) / G0;
+    const int ntiles = nblk * tpb;
+    // block coordinates of this CTA's kb-th block (division-free: magic = ceil(2^32 / KX))
+    auto coords = [&](int kb, int &by, int &bx) {
+        const int k = blockIdx.x + kb * G0;
+        by = (int)__umulhi((uint32_t)k, kx_magic);
+        bx = k - by * KX;
+    };
 
+    // issue cursor (thread 0 only)
+    int ikb = 0, itile = 0;
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int i = 0; i < C::STAGES && i < ntiles; ++i) {
-            const int k = blockIdx.x + (i / tiles_per_block) * gridDim.x;
-            tma_issue_tile<TW>(L, M, base + i * C::STAGE, &full[i], k, i % tiles_per_block, cur, p);
+            int by, bx;
+            coords(ikb, by, bx);
+            tma_issue_tile<TW>(L, M, base + i * C::STAGE, &full[i], by, bx, itile, cur, p);
+            if (++itile == tpb) { itile = 0; ++ikb; }
         }
     }
     __syncthreads();
 
-    int64_t e_acc = 0, ss = 0;
-    int quad_acc = 0, clamped = 0, chg_self = 0, chgL = 0, chgR = 0, chgU = 0, chgD = 0;
-    for (int i = 0; i < ntiles; ++i) {
-        const int s = i % C::STAGES;
-        const int k = blockIdx.x + (i / tiles_per_block) * gridDim.x;
-        const int tile = i % tiles_per_block;
-        const int by = k / L.ax.k, bx = k - by * L.ax.k;
-        const int lo_r = by * BH, lo_c = bx * TW;
-        const int r0 = tile * TH;                      // first block row of this tile
-        const bool has_up = lo_r > 0, has_dn = lo_r + BH < H, has_lf = lo_c > 0, has_rt = lo_c + TW < W;
-        uint8_t *sb = base + s * C::STAGE;
-        const int32_t *su = reinterpret_cast<const int32_t *>(sb + C::O_U);
-        const int32_t *sa = reinterpret_cast<const int32_t *>(sb + C::O_A);
-        const int32_t *sy = reinterpret_cast<const int32_t *>(sb + C::O_Y);
-        const int32_t *syr = reinterpret_cast<const int32_t *>(sb + C::O_YR);
-        const uint8_t *sh = sb + C::O_H;
-        mbar_wait(&full[s], (uint32_t)((i / C::STAGES) & 1));
+    // per-thread quad positions inside a tile (fixed for the whole launch)
+    int rr_[QPT], c0_[QPT];
+#pragma unroll
+    for (int j = 0; j < QPT; ++j) {
+        const int t = tid + j * NT;
+        rr_[j] = t >> LQ;
+        c0_[j] = (t & (QR - 1)) << 2;
+    }
 
+    int s = 0;
+    uint32_t phase = 0;
+    for (int kb = 0; kb < nblk; ++kb) {
+        int by, bx;
+        coords(kb, by, bx);
+        const int k = by * KX + bx;
+        const int lo_r = by * BH, lo_c = bx * TW;
+        const bool has_up = lo_r > 0, has_dn = lo_r + BH < H, has_lf = lo_c > 0, has_rt = lo_c + TW < W;
+        int64_t e_acc = 0;
+        int ss = 0, quad_acc = 0;
+        bool clamped = false, chg_self = false, chgL = false, chgR = false, chgU = false, chgD = false;
+        for (int tile = 0; tile < tpb; ++tile) {
+            uint8_t *sb = base + s * C::STAGE;
+            const int32_t *su = reinterpret_cast<const int32_t *>(sb + C::O_U);
+            const int32_t *sa = reinterpret_cast<const int32_t *>(sb + C::O_A);
+            const int32_t *sy = reinterpret_cast<const int32_t *>(sb + C::O_Y);
+            const int32_t *syr = reinterpret_cast<const int32_t *>(sb + C::O_YR);
+            const uint8_t *sh = sb + C::O_H;
+            mbar_wait(&full[s], phase);
+            const int r0 = tile * TH;
 #pragma unroll
-        for (int j = 0; j < QPT; ++j) {
-            const int t = tid + j * NT;
-            const int rr = t >> LQ, c0 = (t & (QR - 1)) << 2;   // row within tile
-            const int r = r0 + rr;                               // row within block
-            const int4 av = *reinterpret_cast<const int4 *>(sa + rr * TW + c0);
-            const int4 yo = *reinterpret_cast<const int4 *>(sy + rr * TW + c0);
-            const int4 uu = *reinterpret_cast<const int4 *>(su + rr * TW + c0);
-            const uint32_t yh4 = *reinterpret_cast<const uint32_t *>(sh + (rr + 1) * C::YHW + 16 + c0);
-            const uint32_t ob = (uint32_t)((yo.x >> 1) | ((yo.y >> 1) << 1) | ((yo.z >> 1) << 2) |
-                                           ((yo.w >> 1) << 3));
-            const uint32_t nxt = __shfl_down_sync(FULLMASK, ob, 1);
-            const bool top = (r == 0 && has_up), bot = (r == BH - 1 && has_dn);
-            const bool lft = (c0 == 0 && has_lf), rgt = (c0 + 4 == TW && has_rt);
-            if (want_e) {
-                const int4 yb = *reinterpret_cast<const int4 *>(sy + (rr + 1) * TW + c0);
-                const uint32_t bb = (uint32_t)((yb.x >> 1) | ((yb.y >> 1) << 1) | ((yb.z >> 1) << 2) |
-                                               ((yb.w >> 1) << 3));
-                int qd = __popc((ob ^ (ob >> 1)) & 0x7u);
-                if (c0 + 4 < TW) qd += (int)((ob >> 3) ^ (nxt & 1u));
-                else if (has_rt) qd += (int)((ob >> 3) ^ (uint32_t)(syr[rr * 4] >> 1));
-                if (lo_r + r + 1 < H) qd += __popc(ob ^ bb);
-                quad_acc += qd;
-                e_acc += (ob & 1u ? uu.x : 0) + (ob & 2u ? uu.y : 0) + (ob & 4u ? uu.z : 0) +
-                         (ob & 8u ? uu.w : 0);
+            for (int j = 0; j < QPT; ++j) {
+                const int rr = rr_[j], c0 = c0_[j];
+                const int r = r0 + rr;                             // row within block
+                const int off = rr * TW + c0;
+                const int4 av = *reinterpret_cast<const int4 *>(sa + off);
+                const int4 yo = *reinterpret_cast<const int4 *>(sy + off);
+                const int4 uu = *reinterpret_cast<const int4 *>(su + off);
+                const uint8_t *hrow = sh + (rr + 1) * C::YHW + 16 + c0;
+                const uint32_t yh4 = *reinterpret_cast<const uint32_t *>(hrow);
+                const uint32_t ob = pack_y2(yo);
+                const uint32_t nxt = __shfl_down_sync(FULLMASK, ob, 1);
+                if (want_e) {
+                    const int4 yb = *reinterpret_cast<const int4 *>(sy + off + TW);
+                    int qd = __popc((ob ^ (ob >> 1)) & 0x7u);
+                    uint32_t rb = nxt;
+                    if (c0 + 4 == TW) rb = has_rt ? (uint32_t)(syr[rr * 4] >> 1) : (ob >> 3);
+                    qd += (int)(((ob >> 3) ^ rb) & 1u);
+                    if (lo_r + r + 1 < H) qd += __popc(ob ^ pack_y2(yb));
+                    quad_acc += qd;
+                    e_acc += (uu.x & -(int)(ob & 1u)) + (uu.y & -(int)((ob >> 1) & 1u)) +
+                             (uu.z & -(int)((ob >> 2) & 1u)) + (uu.w & -(int)(ob >> 3));
+                }
+                // cross-block sums (non-zero only on the block border)
+                int sx0 = 0, sx1 = 0, sx2 = 0, sx3 = 0;
+                const int h0 = yh4 & 0xFF, h1 = (yh4 >> 8) & 0xFF, h2 = (yh4 >> 16) & 0xFF, h3 = yh4 >> 24;
+                const bool top = (r == 0) && has_up, bot = (r == BH - 1) && has_dn;
+                if (top | bot) {
+                    const uint32_t o4 = *reinterpret_cast<const uint32_t *>(hrow + (top ? -C::YHW : C::YHW));
+                    sx0 = h0 - (int)(o4 & 0xFF);
+                    sx1 = h1 - (int)((o4 >> 8) & 0xFF);
+                    sx2 = h2 - (int)((o4 >> 16) & 0xFF);
+                    sx3 = h3 - (int)(o4 >> 24);
+                    if (top && bot) {   // single-row blocks: both neighbours
+                        const uint32_t d4 = *reinterpret_cast<const uint32_t *>(hrow + C::YHW);
+                        sx0 += h0 - (int)(d4 & 0xFF);
+                        sx1 += h1 - (int)((d4 >> 8) & 0xFF);
+                        sx2 += h2 - (int)((d4 >> 16) & 0xFF);
+                        sx3 += h3 - (int)(d4 >> 24);
+                    }
+                }
+                const bool lft = (c0 == 0) && has_lf, rgt = (c0 + 4 == TW) && has_rt;
+                if (lft) sx0 += h0 - (int)hrow[-1];
+                if (rgt) sx3 += h3 - (int)hrow[4];
+                const int p0 = h0 + av.x - q * sx0, p1 = h1 + av.y - q * sx1;
+                const int p2 = h2 + av.z - q * sx2, p3 = h3 + av.w - q * sx3;
+                clamped |= ((unsigned)p0 | (unsigned)p1 | (unsigned)p2 | (unsigned)p3) > 1u;
+                const int y0 = min(max(p0, 0), 1), y1 = min(max(p1, 0), 1);
+                const int y2 = min(max(p2, 0), 1), y3 = min(max(p3, 0), 1);
+                const uint32_t yn = (uint32_t)(y0 | (y1 << 1) | (y2 << 2) | (y3 << 3));
+                const uint32_t hb = (uint32_t)(h0 | (h1 << 1) | (h2 << 2) | (h3 << 3));
+                ss += __popc(hb ^ yn);
+                // y changed iff new bits != old y2/2 bits (old y2 may be 1 = 1/2 at the start)
+                const bool ychg = (yo.x != 2 * y0) | (yo.y != 2 * y1) | (yo.z != 2 * y2) | (yo.w != 2 * y3);
+                chg_self |= ychg | (hb != yn);
+                const int64_t G = (int64_t)(lo_r + r) * W + lo_c + c0;
+                __stcs(reinterpret_cast<int4 *>(a_out + G),
+                       make_int4(av.x + h0 - y0, av.y + h1 - y1, av.z + h2 - y2, av.w + h3 - y3));
+                __stcg(reinterpret_cast<int4 *>(y_out + G), make_int4(2 * y0, 2 * y1, 2 * y2, 2 * y3));
+                if (ychg) {
+                    chgU |= top;
+                    chgD |= bot;
+                    chgL |= lft && (yo.x != 2 * y0);
+                    chgR |= rgt && (yo.w != 2 * y3);
+                }
             }
-            const uint32_t up4 = *reinterpret_cast<const uint32_t *>(sh + rr * C::YHW + 16 + c0);
-            const uint32_t dn4 = *reinterpret_cast<const uint32_t *>(sh + (rr + 2) * C::YHW + 16 + c0);
-            const int lfb = sh[(rr + 1) * C::YHW + 15 + c0];
-            const int rtb = sh[(rr + 1) * C::YHW + 20 + c0];
-            const int a4[4] = {av.x, av.y, av.z, av.w};
-            const int y24[4] = {yo.x, yo.y, yo.z, yo.w};
-            int y[4], an[4];
-            bool ychg_any = false;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int yh = byte_of(yh4, e);
-                int sx = 0;
-                if (top) sx += yh - byte_of(up4, e);
-                if (bot) sx += yh - byte_of(dn4, e);
-                if (e == 0 && lft) sx += yh - lfb;
-                if (e == 3 && rgt) sx += yh - rtb;
-                const int ypre = yh + a4[e] - q * sx;
-                clamped |= (unsigned)ypre > 1u;
-                y[e] = ypre < 0 ? 0 : (ypre > 1 ? 1 : ypre);
-                an[e] = a4[e] + yh - y[e];
-                ss += yh ^ y[e];
-                const bool ychg = (2 * y[e] != y24[e]);
-                ychg_any |= ychg;
-                chg_self |= ychg | (yh != y[e]);
+            // every warp is done with stage s: refill it with the tile STAGES ahead
+            __syncthreads();
+            if (tid == 0 && ikb < nblk) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                int by2, bx2;
+                coords(ikb, by2, bx2);
+                tma_issue_tile<TW>(L, M, base + s * C::STAGE, &full[s], by2, bx2, itile, cur, p);
+                if (++itile == tpb) { itile = 0; ++ikb; }
             }
-            const int64_t G = (int64_t)(lo_r + r) * W + lo_c + c0;
-            __stcs(reinterpret_cast<int4 *>(a_out + G), make_int4(an[0], an[1], an[2], an[3]));
-            __stcg(reinterpret_cast<int4 *>(y_out + G), make_int4(2 * y[0], 2 * y[1], 2 * y[2], 2 * y[3]));
-            if (ychg_any) {
-                chgU |= top;
-                chgD |= bot;
-                chgL |= (lft && (2 * y[0] != y24[0]));
-                chgR |= (rgt && (2 * y[3] != y24[3]));
-            }
+            if (++s == C::STAGES) { s = 0; phase ^= 1u; }
         }
-        // every warp is done with stage s: refill it with tile i + STAGES
-        __syncthreads();
-        if (tid == 0 && i + C::STAGES < ntiles) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            const int i2 = i + C::STAGES;
-            const int k2 = blockIdx.x + (i2 / tiles_per_block) * gridDim.x;
-            tma_issue_tile<TW>(L, M, base + s * C::STAGE, &full[s], k2, i2 % tiles_per_block, cur, p);
-        }
-        if (tile == tiles_per_block - 1) {
-            // publish this block's partials: one atomic per warp
-            const int64_t e = warp_sum(e_acc + (int64_t)L.lamw * quad_acc);
-            const int64_t sq = warp_sum(ss);
-            const bool fl = __any_sync(FULLMASK, clamped);
-            const bool f0 = __any_sync(FULLMASK, chg_self), f1 = __any_sync(FULLMASK, chgL),
-                       f2 = __any_sync(FULLMASK, chgR), f3 = __any_sync(FULLMASK, chgU),
-                       f4 = __any_sync(FULLMASK, chgD);
-            if (lane == 0) {
-                if (e) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pe[k]), (unsigned long long)e);
-                if (sq) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pr[k]), (unsigned long long)sq);
-                if (fl) atomicOr(&L.pf[k], 1);
-                if (f0) L.dirty[k] = 1u;
-                if (f1) L.dirty[k - 1] = 1u;
-                if (f2) L.dirty[k + 1] = 1u;
-                if (f3) L.dirty[k - L.ax.k] = 1u;
-                if (f4) L.dirty[k + L.ax.k] = 1u;
-            }
-            e_acc = 0; ss = 0; quad_acc = 0; clamped = 0;
-            chg_self = chgL = chgR = chgU = chgD = 0;
+        // publish this block's partials: one atomic per warp
+        const int64_t e = warp_sum(e_acc + (int64_t)L.lamw * quad_acc);
+        const int sq = warp_sum(ss);
+        const unsigned fl = __ballot_sync(FULLMASK, clamped), f0 = __ballot_sync(FULLMASK, chg_self),
+                       f1 = __ballot_sync(FULLMASK, chgL), f2 = __ballot_sync(FULLMASK, chgR),
+                       f3 = __ballot_sync(FULLMASK, chgU), f4 = __ballot_sync(FULLMASK, chgD);
+        if (lane == 0) {
+            if (e) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pe[k]), (unsigned long long)e);
+            if (sq) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pr[k]), (unsigned long long)sq);
+            if (fl) atomicOr(&L.pf[k], 1);
+            if (f0) L.dirty[k] = 1u;
+            if (f1) L.dirty[k - 1] = 1u;
+            if (f2) L.dirty[k + 1] = 1u;
+            if (f3) L.dirty[k - KX] = 1u;
+            if (f4) L.dirty[k + KX] = 1u;
         }
     }
     __syncthreads();

@@ -94,6 +94,7 @@ struct Lat2 {
     int32_t max_iters;
     int32_t K;
     int32_t boxh, boxw;     // padded box used for the block layout
+    int32_t vec4;           // all block columns start/end on 16-byte boundaries
 };
 
 // ---------------------------------------------------------------------------
@@ -194,12 +195,6 @@ __device__ int bfs_relabel(const uint64_t *__restrict__ mE, const uint64_t *__re
         R[k] = on ? mSink[idx] : 0;
         A[k] = on ? mAct[idx] : 0;
         any_act |= (A[k] != 0);
-        uint64_t nb = R[k];
-        while (nb) {
-            const int b = __ffsll((long long)nb) - 1;
-            nb &= nb - 1;
-            h[idx * 64 + b] = 0;
-        }
     }
     const bool have_active = __any_sync(FULLMASK, any_act);
     int level = 0;
@@ -281,10 +276,12 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
     uint64_t t_begin = 0;
     if (L.timeline && tid == 0) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
-        L.timeline[4 * k + 0] = (int64_t)t_begin;
-        L.timeline[4 * k + 1] = (int64_t)t_begin;
-        L.timeline[4 * k + 2] = -1;
-        L.timeline[4 * k + 3] = 0;
+        L.timeline[8 * k + 0] = (int64_t)t_begin;
+        L.timeline[8 * k + 1] = (int64_t)t_begin;
+        L.timeline[8 * k + 2] = -1;
+        L.timeline[8 * k + 3] = 0;
+        L.timeline[8 * k + 4] = (int64_t)t_begin;
+        L.timeline[8 * k + 5] = (int64_t)t_begin;
     }
     if (L.st->stop) return;
     if (L.skip_clean) {
@@ -306,50 +303,120 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
     // ---- prologue: 2*linear (blockform.py:271-272 on the q==1 stencil) ----
     // lin2 = 2u + lamw * sum_cross (y2_g - y2_j) + mu*(2a - y2_g) + mu
     if (L.warm) {
-        // residual planes are stored block-major, 4*M bytes, 16-byte chunks
-        const uint4 *src = reinterpret_cast<const uint4 *>(gres);
-        uint4 *dst = reinterpret_cast<uint4 *>(rr);
-        for (int i = tid; i < M * 4 / 16; i += NT) dst[i] = src[i];
-        __syncthreads();
+        // residual planes (block-major, 4*M bytes): asynchronous 16-byte copies
+        for (int i = tid; i < M * 4 / 16; i += NT) {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(rr + 16 * i)),
+                         "l"(gres + 16 * i)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
-#pragma unroll 4
+    const bool has_up = lo_r > 0, has_dn = lo_r + hr < L.ay.dim, has_lf = lo_c > 0,
+               has_rt = lo_c + wc < Wg;
+    if (L.vec4) {
+        // quads of 4 consecutive box nodes; int4 loads, two quads in flight per thread
+        constexpr int NQ = M / 4;
+        for (int q0 = tid; q0 < NQ; q0 += 2 * NT) {
+            int4 uq[2], aq[2], yq[2], yu[2], yd[2];
+            int yl[2], yrr[2];
+            bool ok[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int qd = q0 + j * NT;
+                const int v0 = 4 * qd, r = v0 / BW, c0 = v0 % BW;
+                ok[j] = qd < NQ && r < hr && c0 < wc;
+                uq[j] = aq[j] = yq[j] = yu[j] = yd[j] = make_int4(0, 0, 0, 0);
+                yl[j] = yrr[j] = 0;
+                if (ok[j]) {
+                    const int64_t G = (int64_t)(lo_r + r) * Wg + lo_c + c0;
+                    uq[j] = __ldg(reinterpret_cast<const int4 *>(L.u + G));
+                    aq[j] = *reinterpret_cast<const int4 *>(a_cur + G);
+                    yq[j] = *reinterpret_cast<const int4 *>(y_cur + G);
+                    if (r == 0 && has_up) yu[j] = *reinterpret_cast<const int4 *>(y_cur + G - Wg);
+                    if (r == hr - 1 && has_dn) yd[j] = *reinterpret_cast<const int4 *>(y_cur + G + Wg);
+                    if (c0 == 0 && has_lf) yl[j] = y_cur[G - 1];
+                    if (c0 + 4 == wc && has_rt) yrr[j] = y_cur[G + 4];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int qd = q0 + j * NT;
+                if (qd >= NQ) continue;
+                const int v0 = 4 * qd, r = v0 / BW, c0 = v0 % BW;
+                int4 out = make_int4(0, 0, 0, 0);
+                if (ok[j]) {
+                    const bool top = r == 0 && has_up, bot = r == hr - 1 && has_dn;
+                    const int yv[4] = {yq[j].x, yq[j].y, yq[j].z, yq[j].w};
+                    const int uv[4] = {uq[j].x, uq[j].y, uq[j].z, uq[j].w};
+                    const int av[4] = {aq[j].x, aq[j].y, aq[j].z, aq[j].w};
+                    const int uu4[4] = {yu[j].x, yu[j].y, yu[j].z, yu[j].w};
+                    const int dd4[4] = {yd[j].x, yd[j].y, yd[j].z, yd[j].w};
+                    int lin[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        int sx = 0;
+                        if (top) sx += yv[e] - uu4[e];
+                        if (bot) sx += yv[e] - dd4[e];
+                        if (e == 0 && c0 == 0 && has_lf) sx += yv[e] - yl[j];
+                        if (e == 3 && c0 + 4 == wc && has_rt) sx += yv[e] - yrr[j];
+                        lin[e] = 2 * uv[e] + L.lamw * sx + L.mu * (2 * av[e] - yv[e]) + L.mu;
+                    }
+                    out = make_int4(lin[0], lin[1], lin[2], lin[3]);
+                }
+                *reinterpret_cast<int4 *>(g + v0) = out;
+            }
+        }
+    } else {
+        for (int i = 0; i < NPT; ++i) {
+            const int v = tid + i * NT;
+            const int r = v / BW, c = v % BW;
+            int32_t lin2 = 0;
+            if (r < hr && c < wc) {
+                const int64_t G = (int64_t)(lo_r + r) * Wg + lo_c + c;
+                const int32_t yg = y_cur[G];
+                int32_t sx = 0;
+                if (c == 0 && has_lf) sx += yg - y_cur[G - 1];
+                if (c == wc - 1 && has_rt) sx += yg - y_cur[G + 1];
+                if (r == 0 && has_up) sx += yg - y_cur[G - Wg];
+                if (r == hr - 1 && has_dn) sx += yg - y_cur[G + Wg];
+                lin2 = 2 * L.u[G] + L.lamw * sx + L.mu * (2 * a_cur[G] - yg) + L.mu;
+            }
+            g[v] = lin2;
+        }
+    }
+    if (L.warm) asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    // g = lin2 + net inflow of the stored flow (warm) / cold residual graph
     for (int i = 0; i < NPT; ++i) {
         const int v = tid + i * NT;
         const int r = v / BW, c = v % BW;
-        const bool valid = (r < hr) && (c < wc);
-        int32_t gv = 0;
-        uint8_t re = 0, rw = 0, rs = 0, rn = 0;
-        if (valid) {
-            const int64_t G = (int64_t)(lo_r + r) * Wg + lo_c + c;
-            const int32_t yg = y_cur[G];
-            int32_t s = 0;
-            if (c == 0 && lo_c > 0) s += yg - y_cur[G - 1];
-            if (c == wc - 1 && lo_c + wc < Wg) s += yg - y_cur[G + 1];
-            if (r == 0 && lo_r > 0) s += yg - y_cur[G - Wg];
-            if (r == hr - 1 && lo_r + hr < L.ay.dim) s += yg - y_cur[G + Wg];
-            const int32_t lin2 = 2 * L.u[G] + L.lamw * s + L.mu * (2 * a_cur[G] - yg) + L.mu;
-            const bool hasE = c + 1 < wc, hasW = c > 0, hasS = r + 1 < hr, hasN = r > 0;
-            if (L.warm) {
-                re = rr[0 * M + v]; rw = rr[1 * M + v]; rs = rr[2 * M + v]; rn = rr[3 * M + v];
-                // net inflow of the stored flow: sum_d (r_d - cap)
-                int32_t f = 0;
-                if (hasE) f += (int32_t)re - cap;
-                if (hasW) f += (int32_t)rw - cap;
-                if (hasS) f += (int32_t)rs - cap;
-                if (hasN) f += (int32_t)rn - cap;
-                gv = lin2 + f;
-            } else {
-                re = hasE ? cap : 0; rw = hasW ? cap : 0; rs = hasS ? cap : 0; rn = hasN ? cap : 0;
-                gv = lin2;
-            }
+        if (!(r < hr && c < wc)) {
+            if (!L.warm) { rr[0 * M + v] = 0; rr[1 * M + v] = 0; rr[2 * M + v] = 0; rr[3 * M + v] = 0; }
+            continue;
         }
-        g[v] = gv;
-        if (!L.warm) {
-            rr[0 * M + v] = re; rr[1 * M + v] = rw; rr[2 * M + v] = rs; rr[3 * M + v] = rn;
+        const bool hasE = c + 1 < wc, hasW = c > 0, hasS = r + 1 < hr, hasN = r > 0;
+        if (L.warm) {
+            int32_t f = 0;
+            if (hasE) f += (int32_t)rr[0 * M + v] - cap;
+            if (hasW) f += (int32_t)rr[1 * M + v] - cap;
+            if (hasS) f += (int32_t)rr[2 * M + v] - cap;
+            if (hasN) f += (int32_t)rr[3 * M + v] - cap;
+            g[v] += f;
+        } else {
+            rr[0 * M + v] = hasE ? cap : 0;
+            rr[1 * M + v] = hasW ? cap : 0;
+            rr[2 * M + v] = hasS ? cap : 0;
+            rr[3 * M + v] = hasN ? cap : 0;
         }
     }
     __syncthreads();
 
+    if (L.timeline && tid == 0) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        L.timeline[8 * k + 4] = (int64_t)t;
+    }
     // ---- solve: rounds of (global relabel BFS, push/relabel sweeps) ----
     uint64_t *mE = masks, *mW = masks + NW, *mS = masks + 2 * NW, *mN = masks + 3 * NW;
     uint64_t *mSink = masks + 4 * NW, *mAct = masks + 5 * NW;
@@ -367,7 +434,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
             const uint32_t bN = __ballot_sync(FULLMASK, rr[3 * M + v] != 0);
             const uint32_t bK = __ballot_sync(FULLMASK, gv < 0);
             const uint32_t bA = __ballot_sync(FULLMASK, gv > 0);
-            h[v] = HINF;
+            h[v] = gv < 0 ? 0 : HINF;          // sink set: level 0 (BFS skips them)
             if (lane == 0) {
                 const int w32 = (i * NT + warp * 32) >> 5;
                 masks32[0 * 2 * NW + w32] = bE;
@@ -387,6 +454,12 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
         __syncthreads();
         const int hit = misc[0];
         const int levels = misc[1];
+        if (L.timeline && tid == 0 && rounds == 0) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            L.timeline[8 * k + 5] = (int64_t)t;
+            L.timeline[8 * k + 6] = levels;
+        }
         if (!hit) break;
         if (++rounds > T.max_rounds) {
             if (tid == 0) atomicCAS(&L.st->error, 0, k + 1);
@@ -463,9 +536,9 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
     if (tid == 0 && L.timeline) {
         uint64_t t_end;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-        L.timeline[4 * k + 1] = (int64_t)t_end;
-        L.timeline[4 * k + 2] = rounds;
-        L.timeline[4 * k + 3] = sweeps_done;
+        L.timeline[8 * k + 1] = (int64_t)t_end;
+        L.timeline[8 * k + 2] = rounds;
+        L.timeline[8 * k + 3] = sweeps_done;
     }
     if (tid == 0) {
         atomicAdd((unsigned long long *)&L.st->solves, 1ull);
@@ -989,15 +1062,21 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var) {
     if (!v) return DOPE_E_GEOMETRY;
     o.boxh = v->bh;
     o.boxw = v->bw;
+    o.vec4 = (o.W % 4 == 0) && (o.ax.rem == 0) && (o.ax.base % 4 == 0);
     if (var) *var = v;
     return DOPE_OK;
 }
 
 static K1Tune default_tune() {
-    K1Tune t;
-    t.sweep_min = 4;
-    t.sweep_mul = 2;
-    t.max_rounds = 1 << 16;
+    static K1Tune t = [] {
+        K1Tune x;
+        x.sweep_min = 1;
+        x.sweep_mul = 1;
+        x.max_rounds = 1 << 16;
+        if (const char *e = getenv("DOPE_SWEEP_MIN")) x.sweep_min = atoi(e);
+        if (const char *e = getenv("DOPE_SWEEP_MUL")) x.sweep_mul = atoi(e);
+        return x;
+    }();
     return t;
 }
 
@@ -1089,7 +1168,8 @@ static int launch_k2_tma(const Lat2 &o, cudaStream_t s) {
         return DOPE_E_CUDA;
     }
     const int grid = o.K < sm_count() ? o.K : sm_count();
-    k_consensus_tma<TW><<<grid, C::NT, C::SMEM, s>>>(o, M);
+    const uint32_t magic = (uint32_t)(((1ull << 32) + o.ax.k - 1) / o.ax.k);
+    k_consensus_tma<TW><<<grid, C::NT, C::SMEM, s>>>(o, M, magic);
     return cuda_check(cudaGetLastError(), "launch K2 (tma)");
 }
 

@@ -21,7 +21,7 @@ def main():
     _, _, problems = build_problem(wl, torch.device("cuda", 0))
     dev = _DeviceState(problems, int(wl.rho), 0.0, iters, True, True)
     K = wl.num_blocks
-    tl = torch.zeros(4 * K, dtype=torch.int64, device="cuda")
+    tl = torch.zeros(8 * K, dtype=torch.int64, device="cuda")
     dev.L.timeline = tl.data_ptr()
     dev.call("dope_admm_init")
     for it in range(iters):
@@ -32,7 +32,7 @@ def main():
         dev.call("dope_update_global", fuse=1)
         e2.record()
         torch.cuda.synchronize()
-        t = tl.view(K, 4).cpu().numpy()
+        t = tl.view(K, 8).cpu().numpy()
         solved = t[:, 2] >= 0
         t0 = t[:, 0].min()
         dur = (t[:, 1] - t[:, 0]) / 1e3
@@ -44,6 +44,14 @@ def main():
               f"p90 {np.percentile(ds,90) if ds.size else 0:6.1f} max {ds.max() if ds.size else 0:6.1f} | "
               f"last start {starts.max():6.1f} last end {ends.max():6.1f} | rounds max {t[:,2].max()} "
               f"sweeps med {np.median(t[solved,3]) if solved.any() else 0:.0f} max {t[:,3].max()}")
+        if solved.any():
+            pro = (t[solved, 4] - t[solved, 0]) / 1e3
+            bfs = (t[solved, 5] - t[solved, 4]) / 1e3
+            rest = (t[solved, 1] - t[solved, 5]) / 1e3
+            lev = t[solved, 6]
+            print(f"        prologue med {np.median(pro):5.1f} max {pro.max():5.1f} | bfs1 med {np.median(bfs):5.1f} "
+                  f"max {bfs.max():5.1f} levels med {np.median(lev):.0f} max {lev.max()} | rest med {np.median(rest):5.1f} "
+                  f"max {rest.max():5.1f}")
     rs = dev.raise_on_error()
     print("state", rs.iteration, rs.best_energy)
 
