@@ -20,10 +20,10 @@ struct TmaMaps {
     CUtensorMap u, a[2], y[3], yr[3], yhat;
 };
 
-template <int TW>
+template <int TW, int NT_ = 512, int STAGES_ = 3>
 struct TmaCfg {
     static constexpr int TH = 4096 / TW;                 // tile rows (64 or 32)
-    static constexpr int NT = 512;
+    static constexpr int NT = NT_;
     static constexpr int QPT = TH * TW / 4 / NT;         // quads per thread (2)
     static constexpr int YHW = TW + 32;                  // label box width (bytes)
     static constexpr int B_U = TW * TH * 4;
@@ -38,7 +38,7 @@ struct TmaCfg {
     static constexpr int O_H = (O_YR + B_YR + 127) / 128 * 128;
     static constexpr int STAGE = (O_H + B_H + 127) / 128 * 128;
     static constexpr int TX = B_U + B_A + B_Y + B_YR + B_H;
-    static constexpr int STAGES = 3;
+    static constexpr int STAGES = STAGES_;
     static constexpr int SMEM = STAGES * STAGE + 128;
 };
 
@@ -80,7 +80,7 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
 template <int TW>
 __device__ __forceinline__ void tma_issue_tile(const Lat2 &L, const TmaMaps &M, uint8_t *stage,
                                                uint64_t *bar, int by, int bx, int tile, int cur, int p) {
-    using C = TmaCfg<TW>;
+    using C = TmaCfg<TW>;   // box geometry does not depend on NT / STAGES
     const int x0 = bx * TW;                       // uniform tiling: lo = index * width
     const int y0 = by * L.ay.base + tile * C::TH;
     mbar_expect_tx(bar, C::TX);
@@ -96,10 +96,10 @@ __device__ __forceinline__ uint32_t pack_y2(const int4 v) {
     return (uint32_t)((v.x | (v.y << 1) | (v.z << 2) | (v.w << 3)) >> 1);
 }
 
-template <int TW>
-__global__ void __launch_bounds__(512, 1) k_consensus_tma(Lat2 L, const __grid_constant__ TmaMaps M,
+template <int TW, int NT_, int STAGES_>
+__global__ void __launch_bounds__(NT_, 1) k_consensus_tma(Lat2 L, const __grid_constant__ TmaMaps M,
                                                           uint32_t kx_magic) {
-    using C = TmaCfg<TW>;
+    using C = TmaCfg<TW, NT_, STAGES_>;
     constexpr int TH = C::TH, NT = C::NT, QPT = C::QPT, QR = TW / 4, LQ = (TW == 64) ? 4 : 5;
     extern __shared__ __align__(128) uint8_t smem_t[];
     uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_t) + 127) & ~(uintptr_t)127);
@@ -141,12 +141,17 @@ __global__ void __launch_bounds__(512, 1) k_consensus_tma(Lat2 L, const __grid_c
     __syncthreads();
 
     // per-thread quad positions inside a tile (fixed for the whole launch)
-    int rr_[QPT], c0_[QPT];
+    int off_[QPT], goff_[QPT], rr_[QPT];
+    bool cl_[QPT], cr_[QPT];
 #pragma unroll
     for (int j = 0; j < QPT; ++j) {
         const int t = tid + j * NT;
-        rr_[j] = t >> LQ;
-        c0_[j] = (t & (QR - 1)) << 2;
+        const int rr = t >> LQ, c0 = (t & (QR - 1)) << 2;
+        rr_[j] = rr;
+        off_[j] = rr * TW + c0;           // smem offset in the tile
+        goff_[j] = rr * W + c0;           // global offset from the tile origin
+        cl_[j] = c0 == 0;
+        cr_[j] = c0 + 4 == TW;
     }
 
     int s = 0;
@@ -166,42 +171,46 @@ __global__ void __launch_bounds__(512, 1) k_consensus_tma(Lat2 L, const __grid_c
             const int32_t *sa = reinterpret_cast<const int32_t *>(sb + C::O_A);
             const int32_t *sy = reinterpret_cast<const int32_t *>(sb + C::O_Y);
             const int32_t *syr = reinterpret_cast<const int32_t *>(sb + C::O_YR);
-            const uint8_t *sh = sb + C::O_H;
-            mbar_wait(&full[s], phase);
+            const uint8_t *sh = sb + C::O_H + C::YHW + 16;      // label of tile pixel (0,0)
             const int r0 = tile * TH;
+            int32_t *a_t = a_out + (int64_t)(lo_r + r0) * W + lo_c;
+            int32_t *y_t = y_out + (int64_t)(lo_r + r0) * W + lo_c;
+            mbar_wait(&full[s], phase);
 #pragma unroll
             for (int j = 0; j < QPT; ++j) {
-                const int rr = rr_[j], c0 = c0_[j];
+                const int rr = rr_[j], off = off_[j];
                 const int r = r0 + rr;                             // row within block
-                const int off = rr * TW + c0;
                 const int4 av = *reinterpret_cast<const int4 *>(sa + off);
                 const int4 yo = *reinterpret_cast<const int4 *>(sy + off);
                 const int4 uu = *reinterpret_cast<const int4 *>(su + off);
-                const uint8_t *hrow = sh + (rr + 1) * C::YHW + 16 + c0;
+                const uint8_t *hrow = sh + rr * C::YHW + (off - rr * TW);
                 const uint32_t yh4 = *reinterpret_cast<const uint32_t *>(hrow);
+                // old iterate (y2 in {0,2} from iteration 2 on) as 4 bits
                 const uint32_t ob = pack_y2(yo);
                 const uint32_t nxt = __shfl_down_sync(FULLMASK, ob, 1);
                 if (want_e) {
                     const int4 yb = *reinterpret_cast<const int4 *>(sy + off + TW);
-                    int qd = __popc((ob ^ (ob >> 1)) & 0x7u);
                     uint32_t rb = nxt;
-                    if (c0 + 4 == TW) rb = has_rt ? (uint32_t)(syr[rr * 4] >> 1) : (ob >> 3);
-                    qd += (int)(((ob >> 3) ^ rb) & 1u);
-                    if (lo_r + r + 1 < H) qd += __popc(ob ^ pack_y2(yb));
-                    quad_acc += qd;
-                    e_acc += (uu.x & -(int)(ob & 1u)) + (uu.y & -(int)((ob >> 1) & 1u)) +
-                             (uu.z & -(int)((ob >> 2) & 1u)) + (uu.w & -(int)(ob >> 3));
+                    if (cr_[j]) rb = has_rt ? (uint32_t)(syr[rr * 4] >> 1) : (ob >> 3);
+                    const uint32_t hz = (ob ^ (ob >> 1)) & 0x7u;                 // pairs inside the quad
+                    const uint32_t vt = (lo_r + r + 1 < H) ? (ob ^ pack_y2(yb)) : 0u;
+                    quad_acc += __popc(hz | (((ob >> 3) ^ rb) & 1u) << 3) + __popc(vt);
+                    e_acc += uu.x * (yo.x >> 1) + uu.y * (yo.y >> 1) + uu.z * (yo.z >> 1) +
+                             uu.w * (yo.w >> 1);
                 }
-                // cross-block sums (non-zero only on the block border)
-                int sx0 = 0, sx1 = 0, sx2 = 0, sx3 = 0;
                 const int h0 = yh4 & 0xFF, h1 = (yh4 >> 8) & 0xFF, h2 = (yh4 >> 16) & 0xFF, h3 = yh4 >> 24;
+                // cross-block sums (non-zero only on the block border)
+                const bool lft = cl_[j] && has_lf, rgt = cr_[j] && has_rt;
+                int sx0 = lft ? h0 - (int)hrow[-1] : 0;
+                int sx3 = rgt ? h3 - (int)hrow[4] : 0;
+                int sx1 = 0, sx2 = 0;
                 const bool top = (r == 0) && has_up, bot = (r == BH - 1) && has_dn;
                 if (top | bot) {
                     const uint32_t o4 = *reinterpret_cast<const uint32_t *>(hrow + (top ? -C::YHW : C::YHW));
-                    sx0 = h0 - (int)(o4 & 0xFF);
-                    sx1 = h1 - (int)((o4 >> 8) & 0xFF);
-                    sx2 = h2 - (int)((o4 >> 16) & 0xFF);
-                    sx3 = h3 - (int)(o4 >> 24);
+                    sx0 += h0 - (int)(o4 & 0xFF);
+                    sx1 += h1 - (int)((o4 >> 8) & 0xFF);
+                    sx2 += h2 - (int)((o4 >> 16) & 0xFF);
+                    sx3 += h3 - (int)(o4 >> 24);
                     if (top && bot) {   // single-row blocks: both neighbours
                         const uint32_t d4 = *reinterpret_cast<const uint32_t *>(hrow + C::YHW);
                         sx0 += h0 - (int)(d4 & 0xFF);
@@ -210,29 +219,28 @@ __global__ void __launch_bounds__(512, 1) k_consensus_tma(Lat2 L, const __grid_c
                         sx3 += h3 - (int)(d4 >> 24);
                     }
                 }
-                const bool lft = (c0 == 0) && has_lf, rgt = (c0 + 4 == TW) && has_rt;
-                if (lft) sx0 += h0 - (int)hrow[-1];
-                if (rgt) sx3 += h3 - (int)hrow[4];
                 const int p0 = h0 + av.x - q * sx0, p1 = h1 + av.y - q * sx1;
                 const int p2 = h2 + av.z - q * sx2, p3 = h3 + av.w - q * sx3;
-                clamped |= ((unsigned)p0 | (unsigned)p1 | (unsigned)p2 | (unsigned)p3) > 1u;
+                clamped |= (unsigned)(p0 | p1 | p2 | p3) > 1u;
                 const int y0 = min(max(p0, 0), 1), y1 = min(max(p1, 0), 1);
                 const int y2 = min(max(p2, 0), 1), y3 = min(max(p3, 0), 1);
                 const uint32_t yn = (uint32_t)(y0 | (y1 << 1) | (y2 << 2) | (y3 << 3));
-                const uint32_t hb = (uint32_t)(h0 | (h1 << 1) | (h2 << 2) | (h3 << 3));
+                const uint32_t hb = ((yh4 * 0x01020408u) >> 24) & 0xFu;   // 0/1 bytes -> bits 0..3
                 ss += __popc(hb ^ yn);
-                // y changed iff new bits != old y2/2 bits (old y2 may be 1 = 1/2 at the start)
-                const bool ychg = (yo.x != 2 * y0) | (yo.y != 2 * y1) | (yo.z != 2 * y2) | (yo.w != 2 * y3);
+                // y changed iff 2*y_new != old y2 (old y2 = 1, i.e. 1/2, on the first pass)
+                const uint32_t o2 = (uint32_t)(yo.x | (yo.y << 2) | (yo.z << 4) | (yo.w << 6));
+                const uint32_t n2 = (uint32_t)((y0 << 1) | (y1 << 3) | (y2 << 5) | (y3 << 7));
+                const bool ychg = o2 != n2;
                 chg_self |= ychg | (hb != yn);
-                const int64_t G = (int64_t)(lo_r + r) * W + lo_c + c0;
-                __stcs(reinterpret_cast<int4 *>(a_out + G),
+                const int go = goff_[j];
+                __stcs(reinterpret_cast<int4 *>(a_t + go),
                        make_int4(av.x + h0 - y0, av.y + h1 - y1, av.z + h2 - y2, av.w + h3 - y3));
-                __stcg(reinterpret_cast<int4 *>(y_out + G), make_int4(2 * y0, 2 * y1, 2 * y2, 2 * y3));
+                __stcg(reinterpret_cast<int4 *>(y_t + go), make_int4(2 * y0, 2 * y1, 2 * y2, 2 * y3));
                 if (ychg) {
                     chgU |= top;
                     chgD |= bot;
-                    chgL |= lft && (yo.x != 2 * y0);
-                    chgR |= rgt && (yo.w != 2 * y3);
+                    chgL |= lft && ((o2 & 3u) != (n2 & 3u));
+                    chgR |= rgt && ((o2 >> 6) != (n2 >> 6));
                 }
             }
             // every warp is done with stage s: refill it with the tile STAGES ahead

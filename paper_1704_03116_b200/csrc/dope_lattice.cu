@@ -1146,12 +1146,13 @@ static int sm_count() {
 }
 
 // persistent TMA consensus: run-loop mode, uniform tiling, 64/128-wide blocks
-template <int TW>
-static int launch_k2_tma(const Lat2 &o, cudaStream_t s) {
-    using C = TmaCfg<TW>;
+template <int TW, int NT, int ST>
+static int launch_k2_tma(const Lat2 &o, cudaStream_t s, int ctas_per_sm) {
+    using C = TmaCfg<TW, NT, ST>;
     static std::once_flag once;
     std::call_once(once, [] {
-        cudaFuncSetAttribute(k_consensus_tma<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(k_consensus_tma<TW, NT, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::SMEM);
     });
     TmaMaps M;
     const int64_t W = o.W, H = o.ay.dim;
@@ -1167,9 +1168,10 @@ static int launch_k2_tma(const Lat2 &o, cudaStream_t s) {
         snprintf(g_last_err, sizeof(g_last_err), "cuTensorMapEncodeTiled failed");
         return DOPE_E_CUDA;
     }
-    const int grid = o.K < sm_count() ? o.K : sm_count();
+    const int slots = ctas_per_sm * sm_count();
+    const int grid = o.K < slots ? o.K : slots;
     const uint32_t magic = (uint32_t)(((1ull << 32) + o.ax.k - 1) / o.ax.k);
-    k_consensus_tma<TW><<<grid, C::NT, C::SMEM, s>>>(o, M, magic);
+    k_consensus_tma<TW, NT, ST><<<grid, C::NT, C::SMEM, s>>>(o, M, magic);
     return cuda_check(cudaGetLastError(), "launch K2 (tma)");
 }
 
@@ -1183,8 +1185,20 @@ static int k2_tma_width(const Lat2 &o) {
 
 static int launch_k2(const Lat2 &o, cudaStream_t s) {
     const int tw = k2_tma_width(o);
-    if (tw == 64 && !getenv("DOPE_NO_TMA")) return launch_k2_tma<64>(o, s);
-    if (tw == 128 && !getenv("DOPE_NO_TMA")) return launch_k2_tma<128>(o, s);
+    static const int variant = getenv("DOPE_K2_VARIANT") ? atoi(getenv("DOPE_K2_VARIANT")) : 0;
+    if (tw && !getenv("DOPE_NO_TMA")) {
+        if (tw == 64) {
+            switch (variant) {
+                case 1: return launch_k2_tma<64, 256, 3>(o, s, 1);
+                case 2: return launch_k2_tma<64, 1024, 3>(o, s, 1);
+                case 3: return launch_k2_tma<64, 512, 2>(o, s, 2);
+                case 4: return launch_k2_tma<64, 256, 2>(o, s, 2);
+                case 5: return launch_k2_tma<64, 512, 4>(o, s, 1);
+                default: return launch_k2_tma<64, 512, 3>(o, s, 1);
+            }
+        }
+        return launch_k2_tma<128, 512, 3>(o, s, 1);
+    }
     const int lq = k2_lq(o);
     if (lq >= 0) {
         const int64_t quads = (int64_t)(o.ay.base + (o.ay.rem ? 1 : 0)) << lq;

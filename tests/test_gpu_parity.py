@@ -138,3 +138,44 @@ def test_larger_grids_match_oracle(size, block, iters):
     assert np.array_equal(state.y, ref["y"])
     assert np.array_equal(labels, ref["labels"])
     assert np.array_equal(state.labels_global(), ref["yhat"])
+
+
+def _c3_model():
+    wl = W.c3()
+    rows, cols, vals = wl.pair_arrays()
+    model = dope.EnergyModel(wl.u.astype(np.float64), dope.SparseWeights(wl.n, rows, cols, vals),
+                             wl.lam)
+    part = dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0, materialize=False)
+    return wl, model, part
+
+
+def test_c3_full_size_first_iterations_match_oracle():
+    """BASELINE's 4096^2 grid at full size: first 3 iterations bit-exact vs the oracle."""
+    import oracle as orc
+    wl, model, part = _c3_model()
+    iters = 3
+    cfg = dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=iters)
+    labels, state = dope.run(model, part, cfg)
+    spec = orc.LatticeSpec(wl.dims, wl.kpa, wl.offsets, [1.0, 1.0], wl.u.astype(np.float64), wl.lam)
+    ref = orc.run(spec, 1.0, 1.0, 0.0, iters, threads=16)
+    assert np.array_equal([t.energy for t in state.trace], ref["energy"])
+    assert np.array_equal([t.max_block_residual for t in state.trace], ref["max_block_residual"])
+    assert np.array_equal(state.labels_global(), ref["yhat"])
+    assert np.array_equal(labels, ref["labels"])
+
+
+def test_c3_full_run_properties():
+    """Full 100-iteration C3 run: deterministic, best-iterate energy consistent with the
+    returned labels (size-independent properties)."""
+    wl, model, part = _c3_model()
+    cfg = dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=wl.iters)
+    labels1, s1 = dope.run(model, part, cfg)
+    labels2, s2 = dope.run(model, part, dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0,
+                                                         max_iters=wl.iters, use_graph=False,
+                                                         skip_clean=False, warm_start=False))
+    assert np.array_equal(labels1, labels2)
+    assert [t.energy for t in s1.trace] == [t.energy for t in s2.trace]
+    e = [t.energy for t in s1.trace]
+    assert s1.best_iteration == int(np.argmin(e)) + 1
+    # the returned state.y is the best iterate (binary on the int path): its energy is the min
+    assert dope.evaluate_energy(model, s1.y) == min(e)
