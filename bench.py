@@ -260,8 +260,16 @@ def main():
     else:
         alg_bytes = 20.0 * wl.num_blocks
     achieved = alg_bytes / (kstat[dom]["avg_ms"] / 1e3) / 1e9
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists():
+        tj = json.loads(tfile.read_text())
+        if dom in tj:
+            traffic = tj[dom]["traffic_bytes"]
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None, "kernel": dom,
+            "frac": achieved / peak, "traffic": traffic,
+            "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one launch)" if traffic else None,
+            "kernel": dom,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
             "algorithmic_bytes_per_launch": alg_bytes}
     iter_bytes = BYTES_PER_PIXEL_ITER * n
