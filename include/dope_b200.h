@@ -111,9 +111,11 @@ typedef struct dope_lattice {
     double *trace_residual_sq;  /* max_iters                                  */
     double *trace_max_residual; /* max_iters                                  */
     int32_t *trace_clamped;     /* max_iters                                  */
-    int64_t *timeline;          /* optional (may be NULL): 4 int64 per block of
-                                   the last K1 launch: globaltimer start, end,
+    int64_t *timeline;          /* optional (may be NULL): 8 int64 per block of
+                                   the last K1 launch (2D): globaltimer stamps,
                                    rounds, sweeps (diagnostics only)          */
+    uint8_t *scratch;           /* 3D only: K * dope_scratch_stride bytes of
+                                   per-sub-region node state (may be NULL in 2D) */
 } dope_lattice;
 
 /* Library / ABI identification; "b200-sm100a". */
@@ -123,6 +125,8 @@ const char *dope_last_cuda_error(void);
 
 /* Bytes of residual state per block for this geometry (0 if unsupported). */
 int64_t dope_resid_stride(const dope_lattice *L);
+/* Bytes of per-block scratch (3D node state; 0 in 2D). */
+int64_t dope_scratch_stride(const dope_lattice *L);
 /* Validate geometry / capacities; 0 or DOPE_E_*. */
 int dope_lattice_check(const dope_lattice *L);
 

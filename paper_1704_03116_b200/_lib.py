@@ -68,6 +68,7 @@ class Lattice(C.Structure):
         ("trace_max_residual", C.c_void_p),
         ("trace_clamped", C.c_void_p),
         ("timeline", C.c_void_p),
+        ("scratch", C.c_void_p),
     ]
 
 
@@ -94,6 +95,8 @@ def lib():
     P = C.POINTER(Lattice)
     lb.dope_resid_stride.restype = C.c_int64
     lb.dope_resid_stride.argtypes = [P]
+    lb.dope_scratch_stride.restype = C.c_int64
+    lb.dope_scratch_stride.argtypes = [P]
     lb.dope_lattice_check.restype = C.c_int
     lb.dope_lattice_check.argtypes = [P]
     for name in ("dope_admm_init", "dope_update_blocks", "dope_update_global",
@@ -132,5 +135,6 @@ def check(rc: int, what: str) -> None:
 
 def exported_symbols() -> list[str]:
     return ["dope_backend_name", "dope_abi_version", "dope_last_cuda_error", "dope_resid_stride",
+            "dope_scratch_stride",
             "dope_lattice_check", "dope_admm_init", "dope_update_blocks", "dope_update_global",
             "dope_update_multipliers", "dope_admm_run", "dope_finish_run", "dope_binarize", "dope_energy4", "dope_bk_maxflow", "dope_bk_workspace_bytes"]

@@ -153,7 +153,7 @@ class _DeviceState:
         self.max_iters = max_iters
         self.L = _lib.Lattice()
         L = self.L
-        L.ndim = 2
+        L.ndim = len(low.dims)
         L.conn = low.conn
         for ax in range(3):
             L.dims[ax] = low.dims[ax] if ax < len(low.dims) else 1
@@ -175,6 +175,8 @@ class _DeviceState:
         self.yhat = torch.zeros(n, dtype=u8, device=dev)
         self.resid = torch.zeros(K * stride, dtype=u8, device=dev)
         self.dirty = torch.ones(K, dtype=torch.int32, device=dev)
+        sstride = int(lb.dope_scratch_stride(C.byref(L)))
+        self.scratch = torch.empty(max(K * sstride, 16), dtype=u8, device=dev)
         self.pe = torch.zeros(K, dtype=torch.int64, device=dev)
         self.pr = torch.zeros(K, dtype=torch.int64, device=dev)
         self.pf = torch.zeros(K, dtype=i32, device=dev)
@@ -191,6 +193,7 @@ class _DeviceState:
         L.yhat = self.yhat.data_ptr()
         L.resid = self.resid.data_ptr()
         L.dirty = self.dirty.data_ptr()
+        L.scratch = self.scratch.data_ptr()
         L.part_energy = self.pe.data_ptr()
         L.part_ressq = self.pr.data_ptr()
         L.part_flags = self.pf.data_ptr()

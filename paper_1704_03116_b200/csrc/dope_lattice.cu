@@ -73,7 +73,7 @@ __host__ __device__ inline Axis make_axis(int64_t dim, int32_t k) {
 }
 
 struct Lat2 {
-    Axis ay, ax;            // rows, cols
+    Axis az, ay, ax;        // depth (3D only; trivial in 2D), rows, cols
     int32_t W;              // grid width (row stride)
     int32_t lamw, mu, q;    // q = lamw / mu
     int32_t cap;            // pair capacity per direction = 2*lamw
@@ -93,8 +93,10 @@ struct Lat2 {
     int64_t *timeline;
     int32_t max_iters;
     int32_t K;
-    int32_t boxh, boxw;     // padded box used for the block layout
+    int32_t boxd, boxh, boxw;  // padded box used for the block layout
     int32_t vec4;           // all block columns start/end on 16-byte boundaries
+    int32_t ndim;
+    uint8_t *scratch;       // 3D: per-block node state (excess, heights)
 };
 
 // ---------------------------------------------------------------------------
@@ -144,48 +146,50 @@ __device__ __forceinline__ uint64_t shifted(const uint64_t (&R)[WPL], int lane) 
     }
 }
 
-template <int WPL, int LANES, int BW, int K>
-__device__ __forceinline__ uint64_t expand_word(const uint64_t (&R)[WPL], uint64_t mE, uint64_t mW,
-                                                uint64_t mS, uint64_t mN, int lane) {
-    // node v joins when it has a residual arc to an already reached node
-    return (mE & shifted<WPL, LANES, 1, K>(R, lane)) | (mW & shifted<WPL, LANES, -1, K>(R, lane)) |
-           (mS & shifted<WPL, LANES, BW, K>(R, lane)) | (mN & shifted<WPL, LANES, -BW, K>(R, lane));
-}
-
-template <int WPL, int LANES, int BW, int K>
+// node v joins the reached set when it has a residual arc to an already
+// reached node: direction d's mask holds "residual arc v -> v + off_d".
+// Direction order: E(+1) W(-1) S(+BW) N(-BW) [D(+PL) U(-PL) in 3D].
+template <int NW, int WPL, int LANES, int BW, int PL, int K>
 struct Expand {
     __device__ __forceinline__ static void run(const uint64_t (&R)[WPL], uint64_t (&NEW)[WPL],
-                                               const uint64_t *mE, const uint64_t *mW,
-                                               const uint64_t *mS, const uint64_t *mN, int lane) {
-        Expand<WPL, LANES, BW, K - 1>::run(R, NEW, mE, mW, mS, mN, lane);
+                                               const uint64_t *__restrict__ m, int lane) {
+        Expand<NW, WPL, LANES, BW, PL, K - 1>::run(R, NEW, m, lane);
         const int idx = lane * WPL + (K - 1);
         const bool on = lane < LANES;
-        uint64_t e = on ? mE[idx] : 0, w = on ? mW[idx] : 0, s = on ? mS[idx] : 0,
-                 n = on ? mN[idx] : 0;
-        NEW[K - 1] = expand_word<WPL, LANES, BW, K - 1>(R, e, w, s, n, lane) & ~R[K - 1];
+        uint64_t x = 0;
+        const uint64_t e = on ? m[0 * NW + idx] : 0, w = on ? m[1 * NW + idx] : 0;
+        const uint64_t sm = on ? m[2 * NW + idx] : 0, n = on ? m[3 * NW + idx] : 0;
+        x = (e & shifted<WPL, LANES, 1, K - 1>(R, lane)) | (w & shifted<WPL, LANES, -1, K - 1>(R, lane)) |
+            (sm & shifted<WPL, LANES, BW, K - 1>(R, lane)) | (n & shifted<WPL, LANES, -BW, K - 1>(R, lane));
+        if constexpr (PL > 0) {
+            const uint64_t dd = on ? m[4 * NW + idx] : 0, uu = on ? m[5 * NW + idx] : 0;
+            x |= (dd & shifted<WPL, LANES, PL, K - 1>(R, lane)) | (uu & shifted<WPL, LANES, -PL, K - 1>(R, lane));
+        }
+        NEW[K - 1] = x & ~R[K - 1];
     }
 };
-template <int WPL, int LANES, int BW>
-struct Expand<WPL, LANES, BW, 0> {
+template <int NW, int WPL, int LANES, int BW, int PL>
+struct Expand<NW, WPL, LANES, BW, PL, 0> {
     __device__ __forceinline__ static void run(const uint64_t (&)[WPL], uint64_t (&)[WPL],
-                                               const uint64_t *, const uint64_t *,
-                                               const uint64_t *, const uint64_t *, int) {}
+                                               const uint64_t *__restrict__, int) {}
 };
 
 // Global relabel: exact BFS distances to the sink set (g < 0) over residual
-// arcs, written to h[] (HINF = unreached).  Returns (on lane 0..31 of warp 0)
-// whether any active node (g > 0) is reached; `reach` receives the reached
-// set.  Early exit once every active node has a level, except when there is
-// none (then the BFS runs to completion and `reach` is the exact sink side).
-template <int NW, int BW>
-__device__ int bfs_relabel(const uint64_t *__restrict__ mE, const uint64_t *__restrict__ mW,
-                           const uint64_t *__restrict__ mS, const uint64_t *__restrict__ mN,
-                           const uint64_t *__restrict__ mSink, const uint64_t *__restrict__ mAct,
-                           uint64_t *__restrict__ reach, uint16_t *__restrict__ h, int lane,
-                           int *levels_out) {
+// arcs, written to h[] for nodes beyond the sink set (the caller has set
+// h = 0 on the sink set and HINF elsewhere).  `masks` holds NDIR direction
+// masks followed by the sink and active masks, NW words each.  Returns (on
+// every lane of the calling warp) whether any active node (g > 0) is
+// reached; `reach` receives the reached set.  Early exit once every active
+// node has a level, except when there is none (then the BFS runs to
+// completion and `reach` is the exact sink side).
+template <int NW, int BW, int PL>
+__device__ int bfs_relabel(const uint64_t *__restrict__ masks, uint64_t *__restrict__ reach,
+                           uint16_t *__restrict__ h, int lane, int *levels_out) {
+    constexpr int NDIR = PL > 0 ? 6 : 4;
     constexpr int LANES = NW < 32 ? NW : 32;
     constexpr int WPL = NW < 32 ? 1 : NW / 32;
     static_assert(NW % LANES == 0, "word layout");
+    const uint64_t *mSink = masks + NDIR * NW, *mAct = masks + (NDIR + 1) * NW;
     const bool on = lane < LANES;
     uint64_t R[WPL], A[WPL], NEW[WPL];
     bool any_act = false;
@@ -205,7 +209,7 @@ __device__ int bfs_relabel(const uint64_t *__restrict__ mE, const uint64_t *__re
             for (int k = 0; k < WPL; ++k) missing |= (A[k] & ~R[k]) != 0;
             if (!__any_sync(FULLMASK, missing)) break;
         }
-        Expand<WPL, LANES, BW, WPL>::run(R, NEW, mE, mW, mS, mN, lane);
+        Expand<NW, WPL, LANES, BW, PL, WPL>::run(R, NEW, masks, lane);
         bool grew = false;
 #pragma unroll
         for (int k = 0; k < WPL; ++k) grew |= (NEW[k] != 0);
@@ -418,8 +422,6 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
         L.timeline[8 * k + 4] = (int64_t)t;
     }
     // ---- solve: rounds of (global relabel BFS, push/relabel sweeps) ----
-    uint64_t *mE = masks, *mW = masks + NW, *mS = masks + 2 * NW, *mN = masks + 3 * NW;
-    uint64_t *mSink = masks + 4 * NW, *mAct = masks + 5 * NW;
     int rounds = 0;
     long long sweeps_done = 0;
     for (;;) {
@@ -448,7 +450,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
         __syncthreads();
         if (warp == 0) {
             int levels = 0;
-            const int hit = bfs_relabel<NW, BW>(mE, mW, mS, mN, mSink, mAct, reach, h, lane, &levels);
+            const int hit = bfs_relabel<NW, BW, 0>(masks, reach, h, lane, &levels);
             if (lane == 0) { misc[0] = hit; misc[1] = levels; }
         }
         __syncthreads();
@@ -925,14 +927,16 @@ __global__ void k_update_multipliers(Lat2 L, int64_t n) {
 __global__ void k_energy_current(Lat2 L, int64_t n) {
     const int32_t *y2 = L.y2[L.st->ycur];
     int64_t acc = 0;
+    const int64_t HW = (int64_t)L.ay.dim * L.W;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const int32_t c = (int32_t)(i % L.W);
-        const int64_t r = i / L.W;
+        const int64_t r = (i / L.W) % L.ay.dim, z = i / HW;
         const int32_t yi = y2[i] >> 1;
         int32_t qd = 0;
         if (c + 1 < L.W) qd += yi ^ (y2[i + 1] >> 1);
         if (r + 1 < L.ay.dim) qd += yi ^ (y2[i + L.W] >> 1);
+        if (z + 1 < L.az.dim) qd += yi ^ (y2[i + HW] >> 1);
         acc += (int64_t)L.u[i] * yi + (int64_t)L.lamw * qd;
     }
     acc = warp_sum(acc);
@@ -971,14 +975,16 @@ __global__ void k_binarize(Lat2 L, int64_t n, uint8_t *out) {
 __global__ void k_energy4(Lat2 L, const int32_t *__restrict__ y2, int64_t n,
                           unsigned long long *out) {
     int64_t acc = 0;
+    const int64_t HW = (int64_t)L.ay.dim * L.W;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const int32_t c = (int32_t)(i % L.W);
-        const int64_t r = i / L.W;
+        const int64_t r = (i / L.W) % L.ay.dim, z = i / HW;
         const int32_t yi = y2[i];
         int64_t qd = 0;
         if (c + 1 < L.W) { const int64_t d = yi - y2[i + 1]; qd += d * d; }
         if (r + 1 < L.ay.dim) { const int64_t d = yi - y2[i + L.W]; qd += d * d; }
+        if (z + 1 < L.az.dim) { const int64_t d = yi - y2[i + HW]; qd += d * d; }
         acc += 2 * (int64_t)L.u[i] * yi + (int64_t)L.lamw * qd;
     }
     acc = warp_sum(acc);
@@ -986,6 +992,7 @@ __global__ void k_energy4(Lat2 L, const int32_t *__restrict__ y2, int64_t n,
 }
 
 #include "consensus_tma.cuh"
+#include "lattice3d.cuh"
 
 // ---------------------------------------------------------------------------
 // Host side
@@ -1014,20 +1021,58 @@ static const Variant *pick_variant(int maxh, int maxw) {
     return nullptr;
 }
 
-static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var) {
+struct Variant3 {
+    int bd, bh, bw, nt;
+    size_t smem;
+    void (*kernel)(Lat2, K1Tune);
+};
+
+template <int BD, int BH, int BW, int NT>
+static Variant3 make_variant3() {
+    return Variant3{BD, BH, BW, NT, K1Cfg3<BD, BH, BW, NT>::SMEM, &k_block_mincut3d<BD, BH, BW, NT>};
+}
+
+static const Variant3 *pick_variant3(int maxd, int maxh, int maxw) {
+    static const Variant3 table[] = {
+        make_variant3<16, 16, 16, 256>(),
+        make_variant3<32, 32, 32, 512>(),
+    };
+    for (const Variant3 &v : table)
+        if (maxd <= v.bd && maxh <= v.bh && maxw <= v.bw) return &v;
+    return nullptr;
+}
+
+static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
+                      const Variant3 **var3 = nullptr) {
     if (!L || !L->u || !L->a[0] || !L->a[1] || !L->y2[0] || !L->y2[1] || !L->y2[2] || !L->yhat || !L->resid ||
         !L->dirty || !L->part_energy || !L->part_ressq || !L->part_flags || !L->state)
         return DOPE_E_ARGS;
-    if (L->ndim != 2 || L->conn != 4) return DOPE_E_GEOMETRY;
-    if (L->dims[0] < 1 || L->dims[1] < 1 || L->kpa[0] < 1 || L->kpa[1] < 1) return DOPE_E_ARGS;
-    if (L->kpa[0] > L->dims[0] || L->kpa[1] > L->dims[1]) return DOPE_E_ARGS;
-    if (L->dims[0] * L->dims[1] > (int64_t)INT32_MAX) return DOPE_E_ARGS;
+    const bool is3 = L->ndim == 3;
+    if (!((L->ndim == 2 && L->conn == 4) || (is3 && L->conn == 6))) return DOPE_E_GEOMETRY;
+    for (int a = 0; a < L->ndim; ++a) {
+        if (L->dims[a] < 1 || L->kpa[a] < 1) return DOPE_E_ARGS;
+        if (L->kpa[a] > L->dims[a]) return DOPE_E_ARGS;
+    }
+    const int64_t n = is3 ? L->dims[0] * L->dims[1] * L->dims[2] : L->dims[0] * L->dims[1];
+    if (n > (int64_t)INT32_MAX) return DOPE_E_ARGS;
     if (L->mu <= 0 || L->lamw < 0 || (L->lamw % L->mu) != 0) return DOPE_E_ARGS;
     if (2 * (int64_t)L->lamw * 2 > 255) return DOPE_E_CAPACITY;   // r + r' = 2*cap <= 255
+    if (is3 && !L->scratch) return DOPE_E_ARGS;
     memset(&o, 0, sizeof(o));
-    o.ay = make_axis(L->dims[0], L->kpa[0]);
-    o.ax = make_axis(L->dims[1], L->kpa[1]);
-    o.W = (int32_t)L->dims[1];
+    o.ndim = L->ndim;
+    if (is3) {
+        o.az = make_axis(L->dims[0], L->kpa[0]);
+        o.ay = make_axis(L->dims[1], L->kpa[1]);
+        o.ax = make_axis(L->dims[2], L->kpa[2]);
+        o.W = (int32_t)L->dims[2];
+        o.K = L->kpa[0] * L->kpa[1] * L->kpa[2];
+    } else {
+        o.az = make_axis(1, 1);
+        o.ay = make_axis(L->dims[0], L->kpa[0]);
+        o.ax = make_axis(L->dims[1], L->kpa[1]);
+        o.W = (int32_t)L->dims[1];
+        o.K = L->kpa[0] * L->kpa[1];
+    }
     o.lamw = L->lamw;
     o.mu = L->mu;
     o.q = L->lamw / L->mu;
@@ -1044,6 +1089,7 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var) {
     o.y2[2] = L->y2[2];
     o.yhat = L->yhat;
     o.resid = L->resid;
+    o.scratch = L->scratch;
     o.dirty = L->dirty;
     o.pe = L->part_energy;
     o.pr = L->part_ressq;
@@ -1055,15 +1101,27 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var) {
     o.tr_cl = L->trace_clamped;
     o.timeline = L->timeline;
     o.max_iters = L->max_iters;
-    o.K = L->kpa[0] * L->kpa[1];
+    const int maxd = o.az.base + (o.az.rem ? 1 : 0);
     const int maxh = o.ay.base + (o.ay.rem ? 1 : 0);
     const int maxw = o.ax.base + (o.ax.rem ? 1 : 0);
-    const Variant *v = pick_variant(maxh, maxw);
-    if (!v) return DOPE_E_GEOMETRY;
-    o.boxh = v->bh;
-    o.boxw = v->bw;
-    o.vec4 = (o.W % 4 == 0) && (o.ax.rem == 0) && (o.ax.base % 4 == 0);
-    if (var) *var = v;
+    if (is3) {
+        const Variant3 *v3 = pick_variant3(maxd, maxh, maxw);
+        if (!v3) return DOPE_E_GEOMETRY;
+        o.boxd = v3->bd;
+        o.boxh = v3->bh;
+        o.boxw = v3->bw;
+        if (var3) *var3 = v3;
+        if (var) *var = nullptr;
+    } else {
+        const Variant *v = pick_variant(maxh, maxw);
+        if (!v) return DOPE_E_GEOMETRY;
+        o.boxd = 1;
+        o.boxh = v->bh;
+        o.boxw = v->bw;
+        if (var) *var = v;
+        if (var3) *var3 = nullptr;
+    }
+    o.vec4 = !is3 && (o.W % 4 == 0) && (o.ax.rem == 0) && (o.ax.base % 4 == 0);
     return DOPE_OK;
 }
 
@@ -1093,10 +1151,42 @@ static int configure_k1(const Variant *v) {
     return DOPE_OK;
 }
 
-static int launch_k1(const Lat2 &o, const Variant *v, cudaStream_t s) {
-    int rc = configure_k1(v);
+static int configure_k1_3d(const Variant3 *v) {
+    static std::mutex mu;
+    static std::map<void *, bool> configured;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!configured[(void *)v->kernel]) {
+        int rc = cuda_check(cudaFuncSetAttribute(v->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)v->smem), "cudaFuncSetAttribute(K1-3D)");
+        if (rc) return rc;
+        configured[(void *)v->kernel] = true;
+    }
+    return DOPE_OK;
+}
+
+struct Plan {
+    Lat2 o;
+    const Variant *v = nullptr;
+    const Variant3 *v3 = nullptr;
+    int64_t n = 0;
+};
+
+static int build_plan(const dope_lattice *L, Plan &P) {
+    int rc = build_lat2(L, P.o, &P.v, &P.v3);
     if (rc) return rc;
-    v->kernel<<<o.K, v->nt, v->smem, s>>>(o, default_tune());
+    P.n = (int64_t)P.o.az.dim * P.o.ay.dim * P.o.W;
+    return DOPE_OK;
+}
+
+static int configure_plan(const Plan &P) {
+    return P.v3 ? configure_k1_3d(P.v3) : configure_k1(P.v);
+}
+
+static int launch_k1(const Plan &P, cudaStream_t s) {
+    int rc = configure_plan(P);
+    if (rc) return rc;
+    if (P.v3) P.v3->kernel<<<P.o.K, P.v3->nt, P.v3->smem, s>>>(P.o, default_tune());
+    else P.v->kernel<<<P.o.K, P.v->nt, P.v->smem, s>>>(P.o, default_tune());
     return cuda_check(cudaGetLastError(), "launch K1");
 }
 
@@ -1184,6 +1274,10 @@ static int k2_tma_width(const Lat2 &o) {
 }
 
 static int launch_k2(const Lat2 &o, cudaStream_t s) {
+    if (o.ndim == 3) {
+        k_consensus3d<<<o.K, 512, 0, s>>>(o);
+        return cuda_check(cudaGetLastError(), "launch K2-3D");
+    }
     const int tw = k2_tma_width(o);
     static const int variant = getenv("DOPE_K2_VARIANT") ? atoi(getenv("DOPE_K2_VARIANT")) : 0;
     if (tw && !getenv("DOPE_NO_TMA")) {
@@ -1230,67 +1324,80 @@ int dope_abi_version(void) { return DOPE_ABI_VERSION; }
 const char *dope_last_cuda_error(void) { return g_last_err; }
 
 int64_t dope_resid_stride(const dope_lattice *L) {
-    if (!L || L->ndim != 2 || L->kpa[0] < 1 || L->kpa[1] < 1) return 0;
+    if (!L) return 0;
+    if (L->ndim == 3) {
+        for (int a = 0; a < 3; ++a)
+            if (L->kpa[a] < 1 || L->dims[a] < 1) return 0;
+        Axis az = make_axis(L->dims[0], L->kpa[0]), ay = make_axis(L->dims[1], L->kpa[1]),
+             ax = make_axis(L->dims[2], L->kpa[2]);
+        const Variant3 *v = pick_variant3(az.base + (az.rem ? 1 : 0), ay.base + (ay.rem ? 1 : 0),
+                                          ax.base + (ax.rem ? 1 : 0));
+        return v ? (int64_t)6 * v->bd * v->bh * v->bw : 0;
+    }
+    if (L->ndim != 2 || L->kpa[0] < 1 || L->kpa[1] < 1) return 0;
     Axis ay = make_axis(L->dims[0], L->kpa[0]), ax = make_axis(L->dims[1], L->kpa[1]);
     const Variant *v = pick_variant(ay.base + (ay.rem ? 1 : 0), ax.base + (ax.rem ? 1 : 0));
     if (!v) return 0;
     return (int64_t)4 * v->bh * v->bw;
 }
 
+int64_t dope_scratch_stride(const dope_lattice *L) {
+    // 3D: excess (int32) + heights (uint16) per box node, 6 bytes (the
+    // residual planes' 6 bytes give the same figure); 2D keeps them in SMEM
+    if (!L || L->ndim != 3) return 0;
+    return dope_resid_stride(L);
+}
+
 int dope_lattice_check(const dope_lattice *L) {
-    Lat2 o;
-    return build_lat2(L, o, nullptr);
+    Plan P;
+    return build_plan(L, P);
 }
 
 int dope_admm_init(const dope_lattice *L, void *stream) {
-    Lat2 o;
-    const Variant *v;
-    int rc = build_lat2(L, o, &v);
+    Plan P;
+    int rc = build_plan(L, P);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
-    const int64_t n = L->dims[0] * L->dims[1];
-    k_init_state<<<grid_for(n), 256, 0, s>>>(o, n);
+    k_init_state<<<grid_for(P.n), 256, 0, s>>>(P.o, P.n);
     rc = cuda_check(cudaGetLastError(), "init_state");
     if (rc) return rc;
-    k_init_resid<<<o.K, 256, 0, s>>>(o);
+    if (P.v3) k_init_resid3d<<<P.o.K, 256, 0, s>>>(P.o, P.o.boxd, P.o.boxh, P.o.boxw);
+    else k_init_resid<<<P.o.K, 256, 0, s>>>(P.o);
     return cuda_check(cudaGetLastError(), "init_resid");
 }
 
 int dope_update_blocks(const dope_lattice *L, void *stream) {
-    Lat2 o;
-    const Variant *v;
-    int rc = build_lat2(L, o, &v);
+    Plan P;
+    int rc = build_plan(L, P);
     if (rc) return rc;
-    return launch_k1(o, v, (cudaStream_t)stream);
+    return launch_k1(P, (cudaStream_t)stream);
 }
 
 int dope_update_global(const dope_lattice *L, void *stream) {
-    Lat2 o;
-    int rc = build_lat2(L, o, nullptr);
+    Plan P;
+    int rc = build_plan(L, P);
     if (rc) return rc;
-    return launch_k2(o, (cudaStream_t)stream);
+    return launch_k2(P.o, (cudaStream_t)stream);
 }
 
 int dope_update_multipliers(const dope_lattice *L, void *stream) {
-    Lat2 o;
-    int rc = build_lat2(L, o, nullptr);
+    Plan P;
+    int rc = build_plan(L, P);
     if (rc) return rc;
-    const int64_t n = L->dims[0] * L->dims[1];
-    k_update_multipliers<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(o, n);
+    k_update_multipliers<<<grid_for(P.n), 256, 0, (cudaStream_t)stream>>>(P.o, P.n);
     return cuda_check(cudaGetLastError(), "update_multipliers");
 }
 
 int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void *stream) {
-    Lat2 o;
-    const Variant *v;
-    int rc = build_lat2(L, o, &v);
+    Plan P;
+    int rc = build_plan(L, P);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     if (iters <= 0) return DOPE_OK;
     if (!use_graph) {
         for (int i = 0; i < iters; ++i) {
-            if ((rc = launch_k1(o, v, s))) return rc;
-            if ((rc = launch_k2(o, s))) return rc;
+            if ((rc = launch_k1(P, s))) return rc;
+            if ((rc = launch_k2(P.o, s))) return rc;
         }
         return DOPE_OK;
     }
@@ -1307,14 +1414,14 @@ int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void 
     }
     if (!exec) {
         // kernel attributes must be set outside stream capture
-        if ((rc = configure_k1(v))) return rc;
+        if ((rc = configure_plan(P))) return rc;
         cudaStream_t cs;
         if ((rc = cuda_check(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream"))) return rc;
         cudaGraph_t graph;
         if ((rc = cuda_check(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "capture"))) return rc;
         for (int i = 0; i < iters && !rc; ++i) {
-            rc = launch_k1(o, v, cs);
-            if (!rc) rc = launch_k2(o, cs);
+            rc = launch_k1(P, cs);
+            if (!rc) rc = launch_k2(P.o, cs);
         }
         cudaError_t e = cudaStreamEndCapture(cs, &graph);
         if (rc) return rc;
@@ -1330,36 +1437,33 @@ int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void 
 }
 
 int dope_finish_run(const dope_lattice *L, void *stream) {
-    Lat2 o;
-    int rc = build_lat2(L, o, nullptr);
+    Plan P;
+    int rc = build_plan(L, P);
     if (rc) return rc;
-    const int64_t n = L->dims[0] * L->dims[1];
     cudaStream_t s = (cudaStream_t)stream;
-    k_energy_current<<<grid_for(n), 256, 0, s>>>(o, n);
+    k_energy_current<<<grid_for(P.n), 256, 0, s>>>(P.o, P.n);
     if ((rc = cuda_check(cudaGetLastError(), "energy_current"))) return rc;
-    k_finish_decide<<<1, 1, 0, s>>>(o);
+    k_finish_decide<<<1, 1, 0, s>>>(P.o);
     return cuda_check(cudaGetLastError(), "finish_decide");
 }
 
 int dope_binarize(const dope_lattice *L, uint8_t *out, void *stream) {
-    Lat2 o;
-    int rc = build_lat2(L, o, nullptr);
+    Plan P;
+    int rc = build_plan(L, P);
     if (rc) return rc;
     if (!out) return DOPE_E_ARGS;
-    const int64_t n = L->dims[0] * L->dims[1];
-    k_binarize<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(o, n, out);
+    k_binarize<<<grid_for(P.n), 256, 0, (cudaStream_t)stream>>>(P.o, P.n, out);
     return cuda_check(cudaGetLastError(), "binarize");
 }
 
 int dope_energy4(const dope_lattice *L, const int32_t *y2, int64_t *out, void *stream) {
-    Lat2 o;
-    int rc = build_lat2(L, o, nullptr);
+    Plan P;
+    int rc = build_plan(L, P);
     if (rc) return rc;
     if (!y2 || !out) return DOPE_E_ARGS;
     cudaStream_t s = (cudaStream_t)stream;
-    const int64_t n = L->dims[0] * L->dims[1];
     if ((rc = cuda_check(cudaMemsetAsync(out, 0, sizeof(int64_t), s), "memset"))) return rc;
-    k_energy4<<<grid_for(n), 256, 0, s>>>(o, y2, n, (unsigned long long *)out);
+    k_energy4<<<grid_for(P.n), 256, 0, s>>>(P.o, y2, P.n, (unsigned long long *)out);
     return cuda_check(cudaGetLastError(), "energy4");
 }
 

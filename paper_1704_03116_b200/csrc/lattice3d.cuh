@@ -1,0 +1,326 @@
+// lattice3d.cuh -- 3D 6-connected lattices (BASELINE C4: 256^3, 32^3 sub-regions).
+// Included by dope_lattice.cu inside namespace dope.
+//
+// Same algorithm and exactness argument as the 2D kernels; the
+// difference is where the block's residual graph lives.  A 32^3 sub-region has
+// 32768 nodes and 6 arcs per node: excess (int32) + 6 residual bytes + height
+// (uint16) is 12 B/node = 384 KB, more than one SM's shared memory.  K1-3D
+// therefore keeps the node state in a per-sub-region HBM scratch that stays
+// L2-resident while the CTA works on it (32 MB for 148 resident blocks vs the
+// 126 MB L2); only the BFS bit masks (8 x 4 KB) live in shared memory, where
+// one warp runs the bit-parallel global relabel with +-1 / +-BW / +-BW*BH word
+// shifts.  Residual planes double as the warm-start state (no copies).
+
+struct Geo3 {
+    int32_t lo_z, dz, lo_r, hr, lo_c, wc;
+};
+
+__device__ __forceinline__ Geo3 block_geo3(const Lat2 &L, int k, int &bz, int &by, int &bx) {
+    const int kyx = L.ay.k * L.ax.k;
+    bz = k / kyx;
+    const int rem = k - bz * kyx;
+    by = rem / L.ax.k;
+    bx = rem - by * L.ax.k;
+    Geo3 g;
+    L.az.range(bz, g.lo_z, g.dz);
+    L.ay.range(by, g.lo_r, g.hr);
+    L.ax.range(bx, g.lo_c, g.wc);
+    return g;
+}
+
+template <int BD, int BH, int BW, int NT>
+struct K1Cfg3 {
+    static constexpr int M = BD * BH * BW;
+    static constexpr int PL = BH * BW;
+    static_assert(M % NT == 0 && M % 64 == 0, "layout");
+    static constexpr int NPT = M / NT;
+    static constexpr int NW = M / 64;
+    static constexpr size_t SMEM = (size_t)9 * 8 * NW + 64;   // 8 masks + reach + misc
+};
+
+template <int BD, int BH, int BW, int NT>
+__global__ void __launch_bounds__(NT) k_block_mincut3d(Lat2 L, K1Tune T) {
+    using C = K1Cfg3<BD, BH, BW, NT>;
+    constexpr int M = C::M, NPT = C::NPT, NW = C::NW, PL = C::PL;
+    extern __shared__ __align__(16) uint8_t smem3[];
+    uint64_t *masks = reinterpret_cast<uint64_t *>(smem3);   // E W S N D U SINK ACT
+    uint64_t *reach = masks + 8 * NW;
+    int *misc = reinterpret_cast<int *>(reach + NW);
+    uint32_t *masks32 = reinterpret_cast<uint32_t *>(masks);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int k = blockIdx.x;
+    if (L.st->stop) return;
+    if (L.skip_clean && L.dirty[k] == 0) return;
+    __syncthreads();
+    if (tid == 0) L.dirty[k] = 0;
+
+    int bz, by, bx;
+    const Geo3 gb = block_geo3(L, k, bz, by, bx);
+    const int32_t W = L.W, H = L.ay.dim, D = L.az.dim;
+    const int64_t HW = (int64_t)H * W;
+    const int32_t cap = L.cap;
+    const int32_t *__restrict__ a_cur = L.st->parity ? L.a1 : L.a0;
+    const int32_t *__restrict__ y_cur = L.y2[L.st->ycur];
+    int32_t *g = reinterpret_cast<int32_t *>(L.scratch + (size_t)k * 6 * M);
+    uint16_t *h = reinterpret_cast<uint16_t *>(g + M);
+    uint8_t *rr = L.resid + (size_t)k * 6 * M;
+    const bool up_z = gb.lo_z > 0, dn_z = gb.lo_z + gb.dz < D;
+    const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
+    const bool lf_c = gb.lo_c > 0, rt_c = gb.lo_c + gb.wc < W;
+
+    // ---- prologue: 2*linear on the 6-neighbour cross-block stencil ----
+#pragma unroll 4
+    for (int i = 0; i < NPT; ++i) {
+        const int v = tid + i * NT;
+        const int z = v / PL, r = (v / BW) % BH, c = v % BW;
+        const bool valid = z < gb.dz && r < gb.hr && c < gb.wc;
+        int32_t gv = 0;
+        if (valid) {
+            const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + r) * W + gb.lo_c + c;
+            const int32_t yg = y_cur[G];
+            int32_t sx = 0;
+            if (c == 0 && lf_c) sx += yg - y_cur[G - 1];
+            if (c == gb.wc - 1 && rt_c) sx += yg - y_cur[G + 1];
+            if (r == 0 && up_r) sx += yg - y_cur[G - W];
+            if (r == gb.hr - 1 && dn_r) sx += yg - y_cur[G + W];
+            if (z == 0 && up_z) sx += yg - y_cur[G - HW];
+            if (z == gb.dz - 1 && dn_z) sx += yg - y_cur[G + HW];
+            const int32_t lin2 = 2 * L.u[G] + L.lamw * sx + L.mu * (2 * a_cur[G] - yg) + L.mu;
+            const bool has[6] = {c + 1 < gb.wc, c > 0, r + 1 < gb.hr, r > 0, z + 1 < gb.dz, z > 0};
+            if (L.warm) {
+                int32_t f = 0;
+#pragma unroll
+                for (int d = 0; d < 6; ++d)
+                    if (has[d]) f += (int32_t)rr[d * M + v] - cap;
+                gv = lin2 + f;
+            } else {
+#pragma unroll
+                for (int d = 0; d < 6; ++d) rr[d * M + v] = has[d] ? (uint8_t)cap : 0;
+                gv = lin2;
+            }
+        } else if (!L.warm) {
+#pragma unroll
+            for (int d = 0; d < 6; ++d) rr[d * M + v] = 0;
+        }
+        g[v] = gv;
+    }
+    __syncthreads();
+
+    int rounds = 0;
+    long long sweeps_done = 0;
+    for (;;) {
+#pragma unroll 2
+        for (int i = 0; i < NPT; ++i) {
+            const int v = tid + i * NT;
+            const int32_t gv = g[v];
+            uint32_t b[6];
+#pragma unroll
+            for (int d = 0; d < 6; ++d) b[d] = __ballot_sync(FULLMASK, rr[d * M + v] != 0);
+            const uint32_t bK = __ballot_sync(FULLMASK, gv < 0);
+            const uint32_t bA = __ballot_sync(FULLMASK, gv > 0);
+            h[v] = gv < 0 ? 0 : HINF;
+            if (lane == 0) {
+                const int w32 = (i * NT + warp * 32) >> 5;
+#pragma unroll
+                for (int d = 0; d < 6; ++d) masks32[d * 2 * NW + w32] = b[d];
+                masks32[6 * 2 * NW + w32] = bK;
+                masks32[7 * 2 * NW + w32] = bA;
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            int levels = 0;
+            const int hit = bfs_relabel<NW, BW, PL>(masks, reach, h, lane, &levels);
+            if (lane == 0) { misc[0] = hit; misc[1] = levels; }
+        }
+        __syncthreads();
+        const int hit = misc[0];
+        const int levels = misc[1];
+        if (!hit) break;
+        if (++rounds > T.max_rounds) {
+            if (tid == 0) atomicCAS(&L.st->error, 0, k + 1);
+            break;
+        }
+        const int cap_sweeps = T.sweep_min + T.sweep_mul * levels;
+        for (int sw = 0; sw < cap_sweeps; ++sw) {
+            ++sweeps_done;
+#pragma unroll 4
+            for (int i = 0; i < NPT; ++i) {
+                const int v = tid + i * NT;
+                const int32_t e = g[v];
+                if (e <= 0) continue;
+                const uint16_t hv = h[v];
+                if (hv == HINF || hv == 0) continue;
+                const uint16_t ht = hv - 1;
+                int32_t left = e;
+#pragma unroll
+                for (int d = 0; d < 6; ++d) {
+                    const int off = (d == 0) ? 1 : (d == 1) ? -1 : (d == 2) ? BW : (d == 3) ? -BW
+                                  : (d == 4) ? PL : -PL;
+                    const int32_t rv = rr[d * M + v];
+                    if (rv == 0) continue;
+                    const int w = v + off;
+                    if (h[w] != ht) continue;
+                    const int32_t delta = left < rv ? left : rv;
+                    rr[d * M + v] = (uint8_t)(rv - delta);
+                    rr[(d ^ 1) * M + w] = (uint8_t)(rr[(d ^ 1) * M + w] + delta);
+                    atomicAdd(&g[w], delta);
+                    left -= delta;
+                    if (left == 0) break;
+                }
+                if (left != e) atomicSub(&g[v], e - left);
+            }
+            __syncthreads();
+            int act = 0;
+#pragma unroll 4
+            for (int i = 0; i < NPT; ++i) {
+                const int v = tid + i * NT;
+                if (g[v] <= 0) continue;
+                const uint16_t hv = h[v];
+                if (hv == HINF) continue;
+                uint32_t mn = HINF;
+#pragma unroll
+                for (int d = 0; d < 6; ++d) {
+                    const int off = (d == 0) ? 1 : (d == 1) ? -1 : (d == 2) ? BW : (d == 3) ? -BW
+                                  : (d == 4) ? PL : -PL;
+                    if (rr[d * M + v] == 0) continue;
+                    const uint32_t hw = h[v + off];
+                    mn = hw < mn ? hw : mn;
+                }
+                const uint32_t nh = (mn + 1 >= (uint32_t)M) ? HINF : mn + 1;
+                if (nh != hv) h[v] = (uint16_t)nh;
+                act |= (nh != HINF);
+            }
+            if (!__syncthreads_or(act)) break;
+        }
+    }
+    // ---- epilogue: labels (sink side); the residual planes stay in place ----
+    for (int i = 0; i < NPT; ++i) {
+        const int v = tid + i * NT;
+        const int z = v / PL, r = (v / BW) % BH, c = v % BW;
+        if (z < gb.dz && r < gb.hr && c < gb.wc) {
+            const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + r) * W + gb.lo_c + c;
+            L.yhat[G] = (uint8_t)((reach[v >> 6] >> (v & 63)) & 1ull);
+        }
+    }
+    if (tid == 0) {
+        atomicAdd((unsigned long long *)&L.st->solves, 1ull);
+        atomicAdd((unsigned long long *)&L.st->sweeps, (unsigned long long)sweeps_done);
+        atomicMax(&L.st->max_rounds_seen, rounds);
+    }
+}
+
+__global__ void k_init_resid3d(Lat2 L, int boxd, int boxh, int boxw) {
+    const int k = blockIdx.x;
+    const int M = boxd * boxh * boxw, PL = boxh * boxw;
+    int bz, by, bx;
+    const Geo3 gb = block_geo3(L, k, bz, by, bx);
+    uint8_t *gres = L.resid + (size_t)k * 6 * M;
+    for (int v = threadIdx.x; v < M; v += blockDim.x) {
+        const int z = v / PL, r = (v / boxw) % boxh, c = v % boxw;
+        const bool valid = z < gb.dz && r < gb.hr && c < gb.wc;
+        const bool has[6] = {c + 1 < gb.wc, c > 0, r + 1 < gb.hr, r > 0, z + 1 < gb.dz, z > 0};
+        for (int d = 0; d < 6; ++d) gres[d * M + v] = (valid && has[d]) ? (uint8_t)L.cap : 0;
+    }
+}
+
+// Consensus for 3D (scalar, one CTA per sub-region).  Same semantics as
+// k_consensus: y_t into the free buffer, multipliers, residual partials,
+// energy partials of y_{t-1}, dirty marks for the block and its 6 face
+// neighbours, last-CTA finalize.
+__global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
+    if (L.st->stop) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int k = blockIdx.x;
+    int bz, by, bx;
+    const Geo3 gb = block_geo3(L, k, bz, by, bx);
+    const int32_t W = L.W, H = L.ay.dim, D = L.az.dim;
+    const int64_t HW = (int64_t)H * W;
+    const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
+    const int32_t *__restrict__ y_in = L.y2[cur];
+    int32_t *__restrict__ y_out = L.y2[out];
+    const int p = L.st->parity;
+    const int32_t *__restrict__ a_in = p ? L.a1 : L.a0;
+    int32_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
+    const bool want_e = L.fuse && L.st->iteration >= 1;
+    const bool up_z = gb.lo_z > 0, dn_z = gb.lo_z + gb.dz < D;
+    const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
+    const bool lf_c = gb.lo_c > 0, rt_c = gb.lo_c + gb.wc < W;
+
+    int64_t e_acc = 0, ss = 0;
+    int clamped = 0;
+    unsigned marks = 0;    // bit0 self, 1..6: -x +x -y +y -z +z neighbours
+    const int m = gb.dz * gb.hr * gb.wc, pl = gb.hr * gb.wc;
+    for (int v = tid; v < m; v += blockDim.x) {
+        const int z = v / pl, rem = v - z * pl, r = rem / gb.wc, c = rem - r * gb.wc;
+        const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + r) * W + gb.lo_c + c;
+        const int32_t yh = L.yhat[G];
+        int32_t sx = 0;
+        if (c == 0 && lf_c) sx += yh - L.yhat[G - 1];
+        if (c == gb.wc - 1 && rt_c) sx += yh - L.yhat[G + 1];
+        if (r == 0 && up_r) sx += yh - L.yhat[G - W];
+        if (r == gb.hr - 1 && dn_r) sx += yh - L.yhat[G + W];
+        if (z == 0 && up_z) sx += yh - L.yhat[G - HW];
+        if (z == gb.dz - 1 && dn_z) sx += yh - L.yhat[G + HW];
+        const int32_t aold = a_in[G];
+        const int32_t ypre = yh + aold - L.q * sx;
+        const int32_t y = ypre < 0 ? 0 : (ypre > 1 ? 1 : ypre);
+        const int32_t y2old = y_in[G];
+        clamped |= (ypre < 0 || ypre > 1);
+        if (a_out) a_out[G] = aold + yh - y;
+        y_out[G] = 2 * y;
+        ss += (yh - y) * (yh - y);
+        if (want_e) {
+            const int32_t o = y2old >> 1;
+            int32_t qd = 0;
+            const int gc = gb.lo_c + c, gr = gb.lo_r + r, gz = gb.lo_z + z;
+            if (gc + 1 < W) qd += o ^ (y_in[G + 1] >> 1);
+            if (gr + 1 < H) qd += o ^ (y_in[G + W] >> 1);
+            if (gz + 1 < D) qd += o ^ (y_in[G + HW] >> 1);
+            e_acc += (int64_t)L.u[G] * o + (int64_t)L.lamw * qd;
+        }
+        const bool ychg = (2 * y != y2old);
+        if (ychg || yh != y) marks |= 1u;
+        if (ychg) {
+            if (c == 0 && lf_c) marks |= 2u;
+            if (c == gb.wc - 1 && rt_c) marks |= 4u;
+            if (r == 0 && up_r) marks |= 8u;
+            if (r == gb.hr - 1 && dn_r) marks |= 16u;
+            if (z == 0 && up_z) marks |= 32u;
+            if (z == gb.dz - 1 && dn_z) marks |= 64u;
+        }
+    }
+    __shared__ int64_t red_e[32], red_s[32];
+    __shared__ unsigned red_f[32];
+    __shared__ int last;
+    e_acc = warp_sum(e_acc);
+    ss = warp_sum(ss);
+    for (int o = 16; o > 0; o >>= 1) marks |= __shfl_xor_sync(FULLMASK, marks, o);
+    const int fl = __any_sync(FULLMASK, clamped);
+    if (lane == 0) { red_e[warp] = e_acc; red_s[warp] = ss; red_f[warp] = marks | (fl ? 128u : 0u); }
+    __syncthreads();
+    if (tid == 0) {
+        int64_t E = 0, S = 0;
+        unsigned Fm = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { E += red_e[w]; S += red_s[w]; Fm |= red_f[w]; }
+        L.pe[k] = E;
+        L.pr[k] = S;
+        L.pf[k] = (Fm & 128u) ? 1 : 0;
+        const int KX = L.ax.k, KYX = L.ay.k * L.ax.k;
+        if (Fm & 1u) L.dirty[k] = 1u;
+        if (Fm & 2u) L.dirty[k - 1] = 1u;
+        if (Fm & 4u) L.dirty[k + 1] = 1u;
+        if (Fm & 8u) L.dirty[k - KX] = 1u;
+        if (Fm & 16u) L.dirty[k + KX] = 1u;
+        if (Fm & 32u) L.dirty[k - KYX] = 1u;
+        if (Fm & 64u) L.dirty[k + KYX] = 1u;
+        __threadfence();
+        last = (atomicAdd(&L.st->done_ctas, 1) == L.K - 1);
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        finalize_cta(L, cur, best, out);
+        if (threadIdx.x == 0) L.st->done_ctas = 0;
+    }
+}

@@ -53,6 +53,26 @@ def _check_stencil_2d4(rows: np.ndarray, cols: np.ndarray, dims) -> None:
             raise NotImplementedError("duplicate lattice pairs")
 
 
+def _check_stencil_3d6(rows: np.ndarray, cols: np.ndarray, dims) -> None:
+    D, H, W = dims
+    n = D * H * W
+    r = rows.astype(np.int64)
+    c = cols.astype(np.int64)
+    d = c - r
+    x = (d == 1) & (W > 1) & (c % W != 0)
+    y = (d == W) & ~x & (H > 1) & ((c // W) % H != 0)
+    z = (d == H * W) & ~x & ~y
+    if not np.all(x | y | z):
+        raise NotImplementedError("pairwise weights are not a 6-connected 3D lattice stencil")
+    want = (D * H * (W - 1), D * (H - 1) * W, (D - 1) * H * W)
+    got = (int(x.sum()), int(y.sum()), int(z.sum()))
+    if got != want:
+        raise NotImplementedError("pairwise weights do not cover the full 6-connected lattice")
+    for sel in (x, y, z):
+        if sel.any() and np.bincount(r[sel], minlength=n).max() > 1:
+            raise NotImplementedError("duplicate lattice pairs")
+
+
 def lower_lattice(model: EnergyModel, partition: Partition) -> LatticeLowering:
     shape = partition.shape
     if model.n != shape.n:
@@ -61,13 +81,16 @@ def lower_lattice(model: EnergyModel, partition: Partition) -> LatticeLowering:
         raise NotImplementedError("overlapping partitions (q > 1) have no B200 kernel yet")
     if not partition.k_per_axis:
         raise ValueError("partition must come from make_partition")
-    if shape.ndim != 2:
-        raise NotImplementedError("3D lattices are not lowered yet")
     w = model.weights
     if w.npairs and float(w.vals.min()) < 0:
         raise NonSubmodularError("pairwise weights contain negative entries; max-flow requires "
                                  "a submodular instance, use the icm solver instead")
-    _check_stencil_2d4(w.rows, w.cols, shape.dims)
+    if shape.ndim == 2:
+        _check_stencil_2d4(w.rows, w.cols, shape.dims)
+        conn = 4
+    else:
+        _check_stencil_3d6(w.rows, w.cols, shape.dims)
+        conn = 6
     lw = model.lam * w.vals
     if lw.size and not np.all(lw == lw[0]):
         raise NotImplementedError("non-constant pairwise weights need the float path")
@@ -77,5 +100,5 @@ def lower_lattice(model: EnergyModel, partition: Partition) -> LatticeLowering:
     u = model.unary
     if not np.all(u == np.round(u)) or np.abs(u).max(initial=0) > 2 ** 28:
         raise NotImplementedError("unary costs must be (bounded) integers on the integer path")
-    return LatticeLowering(tuple(shape.dims), tuple(partition.k_per_axis), 4, int(round(lamw_f)),
+    return LatticeLowering(tuple(shape.dims), tuple(partition.k_per_axis), conn, int(round(lamw_f)),
                            u.astype(np.int32), float(model.lam))

@@ -14,7 +14,7 @@ from conftest import golden_cases, load_golden, spec_from_golden
 
 pytestmark = pytest.mark.gpu
 
-CASES_2D = [c for c in golden_cases() if c != "mini3d"]
+CASES_ALL = golden_cases()
 
 
 def model_from_golden(g):
@@ -43,7 +43,7 @@ def test_library_is_the_cuda_build():
                                   dict(warm_start=False, skip_clean=False, use_graph=False),
                                   dict(warm_start=True, skip_clean=False, use_graph=True),
                                   dict(warm_start=False, skip_clean=True, use_graph=False)])
-@pytest.mark.parametrize("case", CASES_2D)
+@pytest.mark.parametrize("case", CASES_ALL)
 def test_run_matches_reference_trace(case, opts):
     g = load_golden(f"run_{case}.npz")
     model, part = model_from_golden(g)
@@ -66,7 +66,7 @@ def test_run_matches_reference_trace(case, opts):
     assert np.array_equal(state.labels_global(), hist[-1])
 
 
-@pytest.mark.parametrize("case", ["c1", "mini128_b16", "ragged"])
+@pytest.mark.parametrize("case", ["c1", "mini128_b16", "ragged", "mini3d"])
 def test_step_api_block_labels_every_iteration(case):
     g = load_golden(f"run_{case}.npz")
     model, part = model_from_golden(g)
@@ -179,3 +179,22 @@ def test_c3_full_run_properties():
     assert s1.best_iteration == int(np.argmin(e)) + 1
     # the returned state.y is the best iterate (binary on the int path): its energy is the min
     assert dope.evaluate_energy(model, s1.y) == min(e)
+
+
+@pytest.mark.parametrize("size,block,iters", [(96, 32, 6), (64, 16, 8)])
+def test_3d_grids_match_oracle(size, block, iters):
+    import oracle as orc
+    wl = W.c4(seed=21, size=size, block=block, iters=iters)
+    rows, cols, vals = wl.pair_arrays()
+    model = dope.EnergyModel(wl.u.astype(np.float64), dope.SparseWeights(wl.n, rows, cols, vals),
+                             wl.lam)
+    part = dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0, materialize=False)
+    labels, state = dope.run(model, part, dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0,
+                                                          max_iters=iters))
+    spec = orc.LatticeSpec(wl.dims, wl.kpa, wl.offsets, [1.0, 1.0, 1.0], wl.u.astype(np.float64),
+                           wl.lam)
+    ref = orc.run(spec, 1.0, 1.0, 0.0, iters, threads=16)
+    assert state.iteration == ref["iterations"]
+    assert np.array_equal([t.energy for t in state.trace], ref["energy"])
+    assert np.array_equal(state.labels_global(), ref["yhat"])
+    assert np.array_equal(labels, ref["labels"])
