@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-iters", type=int, default=2)
     p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--sharded", action="store_true",
+                   help="use the NCCL-sharded run loop even on one GPU (path check)")
     return p.parse_args()
 
 
@@ -117,7 +119,7 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def build_problem(wl, device):
+def build_problem(wl, device, lower=True):
     """Lower the workload (validation happens once, outside timing)."""
     import paper_1704_03116_b200 as dope
     rows, cols, vals = wl.pair_arrays()
@@ -125,7 +127,7 @@ def build_problem(wl, device):
                              wl.lam)
     del rows, cols, vals
     part = dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0, materialize=False)
-    problems = dope.assemble_block_problems(model, part)
+    problems = dope.assemble_block_problems(model, part) if lower else None
     return model, part, problems
 
 
@@ -183,16 +185,35 @@ def main():
         dist.init_process_group("nccl", init_method="env://")
     from paper_1704_03116_b200 import workloads as W
     from paper_1704_03116_b200.admm import _DeviceState
-    wl = W.by_name(args.config, seed=rank if ws > 1 else 0)
+    wl = W.by_name(args.config)
     iters = args.iters or wl.iters
-    model, part, problems = build_problem(wl, torch.device("cuda", local))
-    dev = _DeviceState(problems, int(wl.rho), 0.0, iters, True, True)
     use_graph = int(not args.no_graph)
+    if ws == 1 and not args.sharded:
+        model, part, problems = build_problem(wl, torch.device("cuda", local))
+        dev = _DeviceState(problems, int(wl.rho), 0.0, iters, True, True)
 
-    def step():
-        dev.call("dope_admm_init")
-        dev.call("dope_admm_run", iters, use_graph, fuse=1)
-        dev.call("dope_finish_run")
+        def step():
+            dev.call("dope_admm_init")
+            dev.call("dope_admm_run", iters, use_graph, fuse=1)
+            dev.call("dope_finish_run")
+    else:
+        # strong scaling: ONE grid, its block rows sharded over the ranks; halos and
+        # the 4-scalar all-reduce run over NCCL inside one CUDA graph per run
+        import paper_1704_03116_b200 as dope
+        from paper_1704_03116_b200 import sharded
+        model, part, _ = build_problem(wl, torch.device("cuda", local), lower=False)
+        cfg = dope.AdmmConfig(mu0=wl.rho, mu_fact=1.0, eps=0.0, max_iters=iters)
+        if ws == 1 and not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            dist.init_process_group("nccl", rank=0, world_size=1)
+        comm = sharded.NcclComm(rank, ws)
+        shard = sharded.shard_for_rank(model, part, cfg, rank, ws)
+        dev = shard.dev
+        problems = shard.problems
+
+        def step():
+            shard.run(comm, iters, bool(use_graph))
 
     for _ in range(args.warmup):
         step()
@@ -226,13 +247,18 @@ def main():
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    total_iters = iters_done * args.steps * ws
+    # one grid (sharded over the ranks when ws > 1): iterations of that grid per second
+    total_iters = iters_done * args.steps
     value = total_iters / (ms / 1e3)
+    n_local = problems.lowering.n
     solves_per_run = rs.solves
     sweeps_per_run = rs.sweeps
 
     # ---- per-kernel timing pass (CUDA events on the launching stream) ----
     evs = {"K1_block_mincut": [], "K2_consensus": []}
+    shard_mode = ws > 1 or args.sharded
+    if shard_mode:
+        dev.L.sharded = 0            # kernel timing on this rank's slab alone (no halos)
     dev.call("dope_admm_init")
     stream = torch.cuda.current_stream()
     for it in range(iters_done):
@@ -246,19 +272,22 @@ def main():
         evs["K2_consensus"].append((e[1], e[2]))
     torch.cuda.synchronize()
     kern = {k: [a.elapsed_time(b) for a, b in v] for k, v in evs.items()}
+    if shard_mode:
+        dev.L.sharded = 1
     kstat = {k: {"total_ms": sum(v), "avg_ms": sum(v) / len(v), "launches": len(v),
                  "first3_ms": v[:3], "median_ms": statistics.median(v)}
              for k, v in kern.items()}
     dom = max(kstat, key=lambda k: kstat[k]["total_ms"])
     peak, peak_kind = measured_peaks()
-    n = wl.n
+    n = n_local
+    k_local = problems.lowering.K
     if dom == "K2_consensus":
         alg_bytes = BYTES_PER_PIXEL_ITER * n
     elif dom == "K1_block_mincut":
         # per solved block: read u,a,y (12 B/px), write yhat (1), residual graph r/w (8)
-        alg_bytes = (12 + 1 + 8) * (n / wl.num_blocks) * (solves_per_run / iters_done)
+        alg_bytes = (12 + 1 + 8) * (n / k_local) * (solves_per_run / iters_done)
     else:
-        alg_bytes = 20.0 * wl.num_blocks
+        alg_bytes = 20.0 * k_local
     achieved = alg_bytes / (kstat[dom]["avg_ms"] / 1e3) / 1e9
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
@@ -273,14 +302,15 @@ def main():
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
             "algorithmic_bytes_per_launch": alg_bytes}
     iter_bytes = BYTES_PER_PIXEL_ITER * n
-    iter_roof = {"bytes_per_iteration": iter_bytes,
-                 "achieved_GBps": iter_bytes * (value / ws) / 1e9,
-                 "frac_of_measured_hbm": iter_bytes * (value / ws) / 1e9 / peak}
+    iter_roof = {"bytes_per_iteration_per_gpu": iter_bytes,
+                 "achieved_GBps_per_gpu": iter_bytes * value / 1e9,
+                 "frac_of_measured_hbm": iter_bytes * value / 1e9 / peak,
+                 "formula": "21 B/pixel/iteration (SURVEY 8(d)) x pixels per GPU x iterations/s"}
 
     # ---- e2e through the C ABI with host buffers ----
     e2e = None
     if not args.no_e2e:
-        u_host = torch.from_numpy(wl.u.astype(np.int32)).pin_memory()
+        u_host = problems.u.cpu().pin_memory()
         lab_host = torch.empty(n, dtype=torch.int8).pin_memory()
         tr_host = torch.empty(iters, dtype=torch.int64).pin_memory()
         for s in range(args.warmup + args.steps):
@@ -302,7 +332,7 @@ def main():
             t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_e2e = float(t.item())
-        e2e = {"value": iters_done * args.steps * ws / (ms_e2e / 1e3), "unit": "iterations/s",
+        e2e = {"value": iters_done * args.steps / (ms_e2e / 1e3), "unit": "iterations/s",
                "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": n + 8 * iters}
 
     cpu = None
@@ -313,26 +343,29 @@ def main():
         line = {
             "metric": "ADMM iterations/s", "value": value, "unit": "iterations/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if ws > 1 else "weak",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": f"{wl.name}: {wl.dims[0]}x{wl.dims[1]} 4-connected Potts, "
-                                   f"{wl.num_blocks} sub-regions of {wl.block[0]}x{wl.block[1]}, "
+            "config": {"workload": f"{wl.name}: {'x'.join(map(str, wl.dims))} {wl.conn}-connected Potts, "
+                                   f"{wl.num_blocks} sub-regions of {'x'.join(map(str, wl.block))}, "
                                    f"{iters_done} ADMM iterations per step (full run from init)",
                        "pixel_edges_per_s": value * wl.num_pairs,
                        "l2": "state ~0.4 GB > 126 MB L2 (inputs larger than L2)",
-                       "parallelism": f"{ws} replica(s)" if ws > 1 else "1 GPU",
+                       "parallelism": (f"{ws} GPUs: block rows sharded in slabs, NCCL halo "
+                                       f"rows + 4-scalar all-reduce per iteration" if ws > 1
+                                       else "1 GPU"),
                        "block_solves_per_run": solves_per_run,
                        "push_relabel_sweeps_per_run": sweeps_per_run,
                        "kernels": kstat},
             "roofline": roof, "iteration_roofline": iter_roof,
-            "clocks": sampler.summary(), "gpu_launches": (2 * iters_done + 3) * args.steps,
+            "clocks": sampler.summary(), "gpu_launches": ((2 * iters_done + 3) if ws == 1 else (8 * iters_done + 6)) * args.steps,
         }
         if e2e:
             line["e2e"] = e2e
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -116,6 +116,17 @@ typedef struct dope_lattice {
                                    rounds, sweeps (diagnostics only)          */
     uint8_t *scratch;           /* 3D only: K * dope_scratch_stride bytes of
                                    per-sub-region node state (may be NULL in 2D) */
+    /* Sharding (2D): this lattice is a slab of whole block rows of a larger
+     * grid.  y2[i] and yhat must then point one row INTO allocations that
+     * carry a ghost row above and below (2D allocations always do). */
+    int32_t ghost_up;           /* a neighbour shard exists above              */
+    int32_t ghost_dn;           /* a neighbour shard exists below              */
+    int32_t sharded;            /* run-loop consensus publishes agg[] instead
+                                   of deciding; call dope_decide after the
+                                   cross-rank all-reduce                       */
+    int64_t *agg;               /* 4: [E (sum), R2 as double bits (sum),
+                                   max block residual^2 (max), clamped (max)] */
+    void *halo;                 /* sharded: 4 * W * 4 bytes of halo staging     */
 } dope_lattice;
 
 /* Library / ABI identification; "b200-sm100a". */
@@ -129,6 +140,8 @@ int64_t dope_resid_stride(const dope_lattice *L);
 int64_t dope_scratch_stride(const dope_lattice *L);
 /* Validate geometry / capacities; 0 or DOPE_E_*. */
 int dope_lattice_check(const dope_lattice *L);
+/* Set kernel attributes ahead of CUDA-graph capture (called internally). */
+int dope_prepare_kernels(const dope_lattice *L);
 
 /* init_state (admm.py:160-168): y = 1/2, a = 0, yhat = 0, every block dirty,
  * cold residual graphs, run state reset. */
@@ -151,6 +164,34 @@ int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void 
 /* End of run (admm.py:300-310): energy + best check of the last iterate;
  * the current iterate becomes the best one unless converged. */
 int dope_finish_run(const dope_lattice *L, void *stream);
+/* Sharded run loop: apply the all-reduced agg[] (trace, best, stop). */
+int dope_decide(const dope_lattice *L, void *stream);
+/* Sharded run loop: install neighbour boundary rows into the ghost rows;
+ * which = 0: labels (uint8[W]), 1: current y2 (int32[W], marks dirty). */
+int dope_ghost_update(const dope_lattice *L, int32_t which, const void *up_row,
+                      const void *dn_row, void *stream);
+/* Sharded run loop: copy the first / last local row of the labels (which=0)
+ * or of the current iterate y2 (which=1) into staging buffers (either may be
+ * NULL) for the halo exchange. */
+int dope_pack_rows(const dope_lattice *L, int32_t which, void *first_row, void *last_row,
+                   void *stream);
+/* dope_finish_run in two halves for sharded runs: the local energy of the
+ * current iterate into state.energy_acc (all-reduce it across shards), then
+ * the final decision. */
+int dope_energy_local(const dope_lattice *L, void *stream);
+int dope_finish_decide(const dope_lattice *L, void *stream);
+/* Multi-GPU (NCCL over NVLink / NVSwitch), one rank per GPU, 2D lattices.
+ * dope_comm_unique_id on rank 0, broadcast the 128 bytes, dope_comm_init on
+ * every rank.  dope_sharded_run runs `iters` iterations of the sharded loop
+ * (K1, label halo, consensus, all-reduce of agg[], dope_decide, y halo) --
+ * captured in one CUDA graph when use_graph; dope_sharded_finish ends the
+ * run (energy of the last iterate all-reduced, final decision). */
+int dope_comm_unique_id(uint8_t *out128);
+int dope_comm_init(int32_t rank, int32_t world, const uint8_t *id128, void **comm_out);
+int dope_comm_destroy(void *comm);
+int dope_sharded_run(const dope_lattice *L, void *comm, int32_t iters, int32_t use_graph,
+                     void *stream);
+int dope_sharded_finish(const dope_lattice *L, void *comm, void *stream);
 /* binarize (admm.py:260-262) of the current iterate into out[n] (0/1). */
 int dope_binarize(const dope_lattice *L, uint8_t *out, void *stream);
 /* evaluate_energy of an arbitrary doubled labeling y2 (int path):

@@ -69,6 +69,11 @@ class Lattice(C.Structure):
         ("trace_clamped", C.c_void_p),
         ("timeline", C.c_void_p),
         ("scratch", C.c_void_p),
+        ("ghost_up", C.c_int32),
+        ("ghost_dn", C.c_int32),
+        ("sharded", C.c_int32),
+        ("agg", C.c_void_p),
+        ("halo", C.c_void_p),
     ]
 
 
@@ -100,12 +105,31 @@ def lib():
     lb.dope_lattice_check.restype = C.c_int
     lb.dope_lattice_check.argtypes = [P]
     for name in ("dope_admm_init", "dope_update_blocks", "dope_update_global",
-                 "dope_update_multipliers", "dope_finish_run"):
+                 "dope_update_multipliers", "dope_finish_run", "dope_energy_local",
+                 "dope_finish_decide"):
         f = getattr(lb, name)
         f.restype = C.c_int
         f.argtypes = [P, C.c_void_p]
     lb.dope_admm_run.restype = C.c_int
     lb.dope_admm_run.argtypes = [P, C.c_int32, C.c_int32, C.c_void_p]
+    lb.dope_prepare_kernels.restype = C.c_int
+    lb.dope_prepare_kernels.argtypes = [P]
+    lb.dope_comm_unique_id.restype = C.c_int
+    lb.dope_comm_unique_id.argtypes = [C.c_void_p]
+    lb.dope_comm_init.restype = C.c_int
+    lb.dope_comm_init.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]
+    lb.dope_comm_destroy.restype = C.c_int
+    lb.dope_comm_destroy.argtypes = [C.c_void_p]
+    lb.dope_sharded_run.restype = C.c_int
+    lb.dope_sharded_run.argtypes = [P, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+    lb.dope_sharded_finish.restype = C.c_int
+    lb.dope_sharded_finish.argtypes = [P, C.c_void_p, C.c_void_p]
+    lb.dope_pack_rows.restype = C.c_int
+    lb.dope_pack_rows.argtypes = [P, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+    lb.dope_decide.restype = C.c_int
+    lb.dope_decide.argtypes = [P, C.c_void_p]
+    lb.dope_ghost_update.restype = C.c_int
+    lb.dope_ghost_update.argtypes = [P, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
     lb.dope_binarize.restype = C.c_int
     lb.dope_binarize.argtypes = [P, C.c_void_p, C.c_void_p]
     lb.dope_energy4.restype = C.c_int
@@ -137,4 +161,7 @@ def exported_symbols() -> list[str]:
     return ["dope_backend_name", "dope_abi_version", "dope_last_cuda_error", "dope_resid_stride",
             "dope_scratch_stride",
             "dope_lattice_check", "dope_admm_init", "dope_update_blocks", "dope_update_global",
-            "dope_update_multipliers", "dope_admm_run", "dope_finish_run", "dope_binarize", "dope_energy4", "dope_bk_maxflow", "dope_bk_workspace_bytes"]
+            "dope_update_multipliers", "dope_admm_run", "dope_finish_run", "dope_binarize", "dope_decide", "dope_ghost_update",
+            "dope_pack_rows", "dope_energy_local", "dope_finish_decide", "dope_prepare_kernels",
+            "dope_comm_unique_id", "dope_comm_init", "dope_comm_destroy", "dope_sharded_run",
+            "dope_sharded_finish", "dope_energy4", "dope_bk_maxflow", "dope_bk_workspace_bytes"]

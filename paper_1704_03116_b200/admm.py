@@ -171,8 +171,15 @@ class _DeviceState:
             raise NotImplementedError(f"no K1 kernel variant for block box of {low.dims}/{low.kpa}")
         i32, u8 = torch.int32, torch.uint8
         self.a = [torch.zeros(n, dtype=i32, device=dev), torch.zeros(n, dtype=i32, device=dev)]
-        self.y2 = [torch.ones(n, dtype=i32, device=dev) for _ in range(3)]
-        self.yhat = torch.zeros(n, dtype=u8, device=dev)
+        # 2D: y2 and yhat carry one ghost row above and below (neighbour shards;
+        # unused on a single GPU), the ABI points one row into the allocation
+        g = low.dims[-1] if len(low.dims) == 2 else 0
+        self.ghost = g
+        self.y2_full = [torch.ones(n + 2 * g, dtype=i32, device=dev) for _ in range(3)]
+        self.y2 = [t[g:g + n] for t in self.y2_full]
+        self.yhat_full = torch.zeros(n + 2 * g, dtype=u8, device=dev)
+        self.yhat = self.yhat_full[g:g + n]
+        self.agg = torch.zeros(4, dtype=torch.int64, device=dev)
         self.resid = torch.zeros(K * stride, dtype=u8, device=dev)
         self.dirty = torch.ones(K, dtype=torch.int32, device=dev)
         sstride = int(lb.dope_scratch_stride(C.byref(L)))
@@ -202,6 +209,7 @@ class _DeviceState:
         L.trace_residual_sq = self.tr_rs.data_ptr()
         L.trace_max_residual = self.tr_mr.data_ptr()
         L.trace_clamped = self.tr_cl.data_ptr()
+        L.agg = self.agg.data_ptr()
         _lib.check(lb.dope_lattice_check(C.byref(L)), "dope_lattice_check")
 
     def stream(self):

@@ -86,9 +86,10 @@ __device__ __forceinline__ void tma_issue_tile(const Lat2 &L, const TmaMaps &M, 
     mbar_expect_tx(bar, C::TX);
     tma_load_2d(stage + C::O_U, &M.u, bar, x0, y0);
     tma_load_2d(stage + C::O_A, &M.a[p], bar, x0, y0);
-    tma_load_2d(stage + C::O_Y, &M.y[cur], bar, x0, y0);
-    tma_load_2d(stage + C::O_YR, &M.yr[cur], bar, x0 + TW, y0);
-    tma_load_2d(stage + C::O_H, &M.yhat, bar, x0 - 16, y0 - 1);
+    // y / labels maps start at the ghost row above the shard: +1 row
+    tma_load_2d(stage + C::O_Y, &M.y[cur], bar, x0, y0 + 1);
+    tma_load_2d(stage + C::O_YR, &M.yr[cur], bar, x0 + TW, y0 + 1);
+    tma_load_2d(stage + C::O_H, &M.yhat, bar, x0 - 16, y0);
 }
 
 // packed old-iterate bits of a quad: y2 in {0,2} -> bit i = y_i
@@ -161,7 +162,8 @@ __global__ void __launch_bounds__(NT_, 1) k_consensus_tma(Lat2 L, const __grid_c
         coords(kb, by, bx);
         const int k = by * KX + bx;
         const int lo_r = by * BH, lo_c = bx * TW;
-        const bool has_up = lo_r > 0, has_dn = lo_r + BH < H, has_lf = lo_c > 0, has_rt = lo_c + TW < W;
+        const bool has_up = lo_r > 0 || L.gup, has_dn = lo_r + BH < H || L.gdn, has_lf = lo_c > 0,
+                   has_rt = lo_c + TW < W;
         int64_t e_acc = 0;
         int ss = 0, quad_acc = 0;
         bool clamped = false, chg_self = false, chgL = false, chgR = false, chgU = false, chgD = false;
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(NT_, 1) k_consensus_tma(Lat2 L, const __grid_c
                     uint32_t rb = nxt;
                     if (cr_[j]) rb = has_rt ? (uint32_t)(syr[rr * 4] >> 1) : (ob >> 3);
                     const uint32_t hz = (ob ^ (ob >> 1)) & 0x7u;                 // pairs inside the quad
-                    const uint32_t vt = (lo_r + r + 1 < H) ? (ob ^ pack_y2(yb)) : 0u;
+                    const uint32_t vt = (lo_r + r + 1 < H || L.gdn) ? (ob ^ pack_y2(yb)) : 0u;
                     quad_acc += __popc(hz | (((ob >> 3) ^ rb) & 1u) << 3) + __popc(vt);
                     e_acc += uu.x * (yo.x >> 1) + uu.y * (yo.y >> 1) + uu.z * (yo.z >> 1) +
                              uu.w * (yo.w >> 1);
@@ -267,8 +269,8 @@ __global__ void __launch_bounds__(NT_, 1) k_consensus_tma(Lat2 L, const __grid_c
             if (f0) L.dirty[k] = 1u;
             if (f1) L.dirty[k - 1] = 1u;
             if (f2) L.dirty[k + 1] = 1u;
-            if (f3) L.dirty[k - KX] = 1u;
-            if (f4) L.dirty[k + KX] = 1u;
+            if (f3 && k - KX >= 0) L.dirty[k - KX] = 1u;
+            if (f4 && k + KX < L.K) L.dirty[k + KX] = 1u;
         }
     }
     __syncthreads();

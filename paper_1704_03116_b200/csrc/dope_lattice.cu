@@ -97,6 +97,9 @@ struct Lat2 {
     int32_t vec4;           // all block columns start/end on 16-byte boundaries
     int32_t ndim;
     uint8_t *scratch;       // 3D: per-block node state (excess, heights)
+    int32_t gup, gdn;       // a ghost row (neighbour shard) exists above / below
+    int32_t sharded;        // consensus writes local aggregates; dope_decide applies
+    int64_t *agg;           // [E, R2 (double bits), max ss, clamped] of this shard
 };
 
 // ---------------------------------------------------------------------------
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    const bool has_up = lo_r > 0, has_dn = lo_r + hr < L.ay.dim, has_lf = lo_c > 0,
+    const bool has_up = lo_r > 0 || L.gup, has_dn = lo_r + hr < L.ay.dim || L.gdn, has_lf = lo_c > 0,
                has_rt = lo_c + wc < Wg;
     if (L.vec4) {
         // quads of 4 consecutive box nodes; int4 loads, two quads in flight per thread
@@ -576,6 +579,14 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
         L.a1[i] = 0;
         L.yhat[i] = 0;
     }
+    if (L.ndim == 2) {   // ghost rows of the initial iterate: the neighbours' y = 1/2
+        for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < L.W; c += stride) {
+            L.y2[0][-L.W + c] = 1;
+            L.y2[0][(int64_t)L.ay.dim * L.W + c] = 1;
+            L.yhat[-L.W + c] = 0;
+            L.yhat[(int64_t)L.ay.dim * L.W + c] = 0;
+        }
+    }
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.K; i += stride) {
         L.dirty[i] = 1u;
         L.pe[i] = 0;
@@ -618,6 +629,45 @@ __device__ __forceinline__ int other_buffer(int cur, int best) {
 // test the stop rule (admm.py:289-307); rotate the y buffers.  Executed by the
 // whole last CTA of a consensus launch.  Blocks are assigned to threads by
 // index and combined in a fixed tree, so float sums are deterministic.
+// Apply one iteration's global aggregates to the run state (admm.py:289-307):
+// trace entry, best iterate by buffer index (strict <), parity, stop rule,
+// y-buffer rotation.  E2 is the energy of the previous iterate (y_{t}),
+// R2/M2/F2 the residual sum, max block residual^2 and clamp flag of this one.
+__device__ void apply_iteration(const Lat2 &L, int64_t E2, double R2, int64_t M2, int F2, int cur,
+                                int best_idx, int out) {
+    dope_run_state *st = L.st;
+    int bidx = best_idx;
+    const int t = st->iteration;        // iterations completed before this one
+    if (t >= 1) {
+        if (t - 1 < L.max_iters) L.tr_e[t - 1] = E2;
+        if (E2 < st->best_energy) {
+            st->best_energy = E2;
+            st->best_iteration = t;
+            bidx = cur;
+        }
+    }
+    const double maxres = M2 < 0 ? 0.0 : sqrt((double)M2);
+    if (t < L.max_iters) {
+        L.tr_rs[t] = R2;
+        L.tr_mr[t] = maxres;
+        L.tr_cl[t] = F2;
+    }
+    st->parity ^= 1;
+    st->iteration = t + 1;
+    if (L.K == 0 || maxres <= L.eps) {
+        st->converged = 1;
+        st->stop = 1;
+    }
+    if (st->error) st->stop = 1;
+    st->ybest = bidx;
+    st->ycur = out;
+}
+
+// Reduce the per-block partials (run-loop mode) and apply them -- or, when
+// sharded, publish this shard's aggregates for the cross-rank all-reduce and
+// leave the decision to dope_decide.  Executed by the whole last CTA of a
+// consensus launch; blocks are assigned to threads by index and combined in a
+// fixed tree, so float sums are deterministic.
 __device__ void finalize_cta(const Lat2 &L, int cur, int best_idx, int out) {
     __shared__ int64_t sE[32];
     __shared__ double sR[32];
@@ -625,66 +675,110 @@ __device__ void finalize_cta(const Lat2 &L, int cur, int best_idx, int out) {
     __shared__ int sF[32];
     dope_run_state *st = L.st;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (!L.fuse) {                       // step-level API: rotate only
+        if (tid == 0) {
+            st->ybest = best_idx;
+            st->ycur = out;
+        }
+        return;
+    }
     int64_t E = 0, mx = -1;
     double rs = 0.0;
     int F = 0;
-    if (L.fuse) {
-        for (int k = tid; k < L.K; k += blockDim.x) {
-            E += __ldcg(&L.pe[k]);
-            const int64_t sq = __ldcg(&L.pr[k]);
-            const double r = sqrt((double)sq);
-            rs += r * r;
-            mx = sq > mx ? sq : mx;
-            F |= __ldcg(&L.pf[k]);
-        }
-        E = warp_sum(E);
-        for (int o = 16; o > 0; o >>= 1) {
-            rs += __shfl_xor_sync(FULLMASK, rs, o);
-            const int64_t t = __shfl_xor_sync(FULLMASK, mx, o);
-            mx = t > mx ? t : mx;
-        }
-        F = __any_sync(FULLMASK, F);
-        if (lane == 0) { sE[warp] = E; sR[warp] = rs; sM[warp] = mx; sF[warp] = F; }
-        __syncthreads();
+    for (int k = tid; k < L.K; k += blockDim.x) {
+        E += __ldcg(&L.pe[k]);
+        const int64_t sq = __ldcg(&L.pr[k]);
+        const double r = sqrt((double)sq);
+        rs += r * r;
+        mx = sq > mx ? sq : mx;
+        F |= __ldcg(&L.pf[k]);
     }
+    E = warp_sum(E);
+    for (int o = 16; o > 0; o >>= 1) {
+        rs += __shfl_xor_sync(FULLMASK, rs, o);
+        const int64_t t = __shfl_xor_sync(FULLMASK, mx, o);
+        mx = t > mx ? t : mx;
+    }
+    F = __any_sync(FULLMASK, F);
+    if (lane == 0) { sE[warp] = E; sR[warp] = rs; sM[warp] = mx; sF[warp] = F; }
+    __syncthreads();
     if (tid == 0) {
-        int bidx = best_idx;
-        if (L.fuse) {
-            int64_t E2 = 0, M2 = -1;
-            double R2 = 0.0;
-            int F2 = 0;
-            const int nw = blockDim.x / 32;
-            for (int w = 0; w < nw; ++w) {
-                E2 += sE[w];
-                R2 += sR[w];
-                M2 = sM[w] > M2 ? sM[w] : M2;
-                F2 |= sF[w];
-            }
-            const int t = st->iteration;        // iterations completed before this one
-            if (t >= 1) {                       // E2 = E(y_t): trace entry of iteration t
-                if (t - 1 < L.max_iters) L.tr_e[t - 1] = E2;
-                if (E2 < st->best_energy) {
-                    st->best_energy = E2;
-                    st->best_iteration = t;
-                    bidx = cur;
+        int64_t E2 = 0, M2 = -1;
+        double R2 = 0.0;
+        int F2 = 0;
+        const int nw = blockDim.x / 32;
+        for (int w = 0; w < nw; ++w) {
+            E2 += sE[w];
+            R2 += sR[w];
+            M2 = sM[w] > M2 ? sM[w] : M2;
+            F2 |= sF[w];
+        }
+        if (L.sharded) {
+            L.agg[0] = E2;
+            L.agg[1] = __double_as_longlong(R2);
+            L.agg[2] = M2;
+            L.agg[3] = F2;
+        } else {
+            apply_iteration(L, E2, R2, M2, F2, cur, best_idx, out);
+        }
+    }
+}
+
+// Sharded mode: apply the all-reduced aggregates (identical on every rank).
+__global__ void k_decide(Lat2 L) {
+    dope_run_state *st = L.st;
+    if (st->stop) return;
+    const int cur = st->ycur, best = st->ybest;
+    apply_iteration(L, L.agg[0], __longlong_as_double(L.agg[1]), L.agg[2], (int)L.agg[3], cur, best,
+                    other_buffer(cur, best));
+}
+
+// Sharded mode: copy this shard's first and last local rows (labels or the
+// current iterate) into caller staging buffers for the halo exchange.
+__global__ void k_pack_rows(Lat2 L, int which, void *first, void *last) {
+    const int32_t W = L.W;
+    const int64_t lastoff = (int64_t)(L.ay.dim - 1) * W;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < W; c += gridDim.x * blockDim.x) {
+        if (which == 0) {
+            if (first) static_cast<uint8_t *>(first)[c] = L.yhat[c];
+            if (last) static_cast<uint8_t *>(last)[c] = L.yhat[lastoff + c];
+        } else {
+            const int32_t *y = L.y2[L.st->ycur];
+            if (first) static_cast<int32_t *>(first)[c] = y[c];
+            if (last) static_cast<int32_t *>(last)[c] = y[lastoff + c];
+        }
+    }
+}
+
+// Sharded mode: install the neighbour shards' boundary rows into the ghost
+// rows.  which == 0: labels (uint8); which == 1: current iterate y2 (int32),
+// marking the local boundary block row dirty where the neighbour's y changed
+// (it enters this shard's block objectives, blockform.py:271).
+__global__ void k_ghost_update(Lat2 L, int which, const void *up_new, const void *dn_new) {
+    const int32_t W = L.W;
+    const int64_t below = (int64_t)L.ay.dim * W;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < W; c += gridDim.x * blockDim.x) {
+        if (which == 0) {
+            if (L.gup && up_new) L.yhat[-W + c] = static_cast<const uint8_t *>(up_new)[c];
+            if (L.gdn && dn_new) L.yhat[below + c] = static_cast<const uint8_t *>(dn_new)[c];
+        } else {
+            int32_t *y = L.y2[L.st->ycur];
+            const int bx = L.ax.owner(c);
+            if (L.gup && up_new) {
+                const int32_t v = static_cast<const int32_t *>(up_new)[c];
+                if (y[-W + c] != v) {
+                    L.dirty[bx] = 1u;
+                    y[-W + c] = v;
                 }
             }
-            const double maxres = M2 < 0 ? 0.0 : sqrt((double)M2);
-            if (t < L.max_iters) {
-                L.tr_rs[t] = R2;
-                L.tr_mr[t] = maxres;
-                L.tr_cl[t] = F2;
+            if (L.gdn && dn_new) {
+                const int32_t v = static_cast<const int32_t *>(dn_new)[c];
+                if (y[below + c] != v) {
+                    L.dirty[(L.ay.k - 1) * L.ax.k + bx] = 1u;
+                    y[below + c] = v;
+                }
             }
-            st->parity ^= 1;
-            st->iteration = t + 1;
-            if (L.K == 0 || maxres <= L.eps) {
-                st->converged = 1;
-                st->stop = 1;
-            }
-            if (st->error) st->stop = 1;
         }
-        st->ybest = bidx;
-        st->ycur = out;
     }
 }
 
@@ -722,8 +816,8 @@ __device__ __forceinline__ void consensus_epilogue(const Lat2 &L, int k, int64_t
         if (Fm & 2) L.dirty[k] = 1u;
         if (Fm & 4) L.dirty[k - 1] = 1u;
         if (Fm & 8) L.dirty[k + 1] = 1u;
-        if (Fm & 16) L.dirty[k - L.ax.k] = 1u;
-        if (Fm & 32) L.dirty[k + L.ax.k] = 1u;
+        if ((Fm & 16) && k - L.ax.k >= 0) L.dirty[k - L.ax.k] = 1u;
+        if ((Fm & 32) && k + L.ax.k < L.K) L.dirty[k + L.ax.k] = 1u;
         __threadfence();
         const int prev = atomicAdd(&L.st->done_ctas, 1);
         last = (prev == L.K - 1);
@@ -753,7 +847,8 @@ __global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
     const int32_t *__restrict__ a_in = p ? L.a1 : L.a0;
     int32_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
     const bool want_e = L.fuse && L.st->iteration >= 1;
-    const bool has_up = lo_r > 0, has_dn = lo_r + hr < H, has_lf = lo_c > 0, has_rt = lo_c + wc < W;
+    const bool has_up = lo_r > 0 || L.gup, has_dn = lo_r + hr < H || L.gdn, has_lf = lo_c > 0,
+               has_rt = lo_c + wc < W;
 
     int64_t e_acc = 0, ss = 0;
     int clamped = 0, chg_self = 0, chgL = 0, chgR = 0, chgU = 0, chgD = 0;
@@ -780,7 +875,7 @@ __global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
             const int32_t o = y2old >> 1;
             int32_t qd = 0;
             if (Cc + 1 < W) qd += o ^ (y_in[G + 1] >> 1);
-            if (R + 1 < H) qd += o ^ (y_in[G + W] >> 1);
+            if (R + 1 < H || L.gdn) qd += o ^ (y_in[G + W] >> 1);
             e_acc += (int64_t)L.u[G] * o + (int64_t)L.lamw * qd;
         }
         const bool ychg = (2 * y != y2old);
@@ -823,7 +918,8 @@ __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
     int32_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
     const bool want_e = L.fuse && L.st->iteration >= 1;
     const int32_t q = L.q;
-    const bool has_up = lo_r > 0, has_dn = lo_r + hr < H, has_lf = lo_c > 0, has_rt = lo_c + wc < W;
+    const bool has_up = lo_r > 0 || L.gup, has_dn = lo_r + hr < H || L.gdn, has_lf = lo_c > 0,
+               has_rt = lo_c + wc < W;
 
     // ---- issue every load of this thread's quads ----
     uint32_t yh4[QPT], up4[QPT], dn4[QPT];
@@ -841,7 +937,8 @@ __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
             av[j] = __ldcs(reinterpret_cast<const int4 *>(a_in + G));
             yo[j] = __ldcg(reinterpret_cast<const int4 *>(y_in + G));
             uu[j] = __ldg(reinterpret_cast<const int4 *>(L.u + G));
-            if (want_e && lo_r + r + 1 < H) yb[j] = __ldcg(reinterpret_cast<const int4 *>(y_in + G + W));
+            if (want_e && (lo_r + r + 1 < H || L.gdn))
+                yb[j] = __ldcg(reinterpret_cast<const int4 *>(y_in + G + W));
             if (r == 0 && has_up) up4[j] = *reinterpret_cast<const uint32_t *>(L.yhat + G - W);
             if (r == hr - 1 && has_dn) dn4[j] = *reinterpret_cast<const uint32_t *>(L.yhat + G + W);
             if (c0 == 0 && has_lf) lf[j] = L.yhat[G - 1];
@@ -874,7 +971,7 @@ __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
             quad += __popc((ob ^ (ob >> 1)) & 0x7u);            // pairs inside the quad
             if (c0 + 4 < wc) quad += (int)((ob >> 3) ^ (nxt & 1u));
             else if (rgt) quad += (int)((ob >> 3) ^ (uint32_t)(yr[j] >> 1));
-            if (lo_r + r + 1 < H) quad += __popc(ob ^ bb);
+            if (lo_r + r + 1 < H || L.gdn) quad += __popc(ob ^ bb);
             e_acc += (ob & 1u ? uu[j].x : 0) + (ob & 2u ? uu[j].y : 0) + (ob & 4u ? uu[j].z : 0) +
                      (ob & 8u ? uu[j].w : 0);
         }
@@ -935,7 +1032,7 @@ __global__ void k_energy_current(Lat2 L, int64_t n) {
         const int32_t yi = y2[i] >> 1;
         int32_t qd = 0;
         if (c + 1 < L.W) qd += yi ^ (y2[i + 1] >> 1);
-        if (r + 1 < L.ay.dim) qd += yi ^ (y2[i + L.W] >> 1);
+        if (r + 1 < L.ay.dim || L.gdn) qd += yi ^ (y2[i + L.W] >> 1);
         if (z + 1 < L.az.dim) qd += yi ^ (y2[i + HW] >> 1);
         acc += (int64_t)L.u[i] * yi + (int64_t)L.lamw * qd;
     }
@@ -983,7 +1080,7 @@ __global__ void k_energy4(Lat2 L, const int32_t *__restrict__ y2, int64_t n,
         const int32_t yi = y2[i];
         int64_t qd = 0;
         if (c + 1 < L.W) { const int64_t d = yi - y2[i + 1]; qd += d * d; }
-        if (r + 1 < L.ay.dim) { const int64_t d = yi - y2[i + L.W]; qd += d * d; }
+        if (r + 1 < L.ay.dim || L.gdn) { const int64_t d = yi - y2[i + L.W]; qd += d * d; }
         if (z + 1 < L.az.dim) { const int64_t d = yi - y2[i + HW]; qd += d * d; }
         acc += 2 * (int64_t)L.u[i] * yi + (int64_t)L.lamw * qd;
     }
@@ -1101,6 +1198,12 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
     o.tr_cl = L->trace_clamped;
     o.timeline = L->timeline;
     o.max_iters = L->max_iters;
+    o.gup = L->ghost_up;
+    o.gdn = L->ghost_dn;
+    o.sharded = L->sharded;
+    o.agg = L->agg;
+    if (o.sharded && (!o.agg || is3 || o.ay.rem != 0)) return DOPE_E_ARGS;
+    if ((o.gup || o.gdn) && is3) return DOPE_E_GEOMETRY;
     const int maxd = o.az.base + (o.az.rem ? 1 : 0);
     const int maxh = o.ay.base + (o.ay.rem ? 1 : 0);
     const int maxw = o.ax.base + (o.ax.rem ? 1 : 0);
@@ -1249,11 +1352,12 @@ static int launch_k2_tma(const Lat2 &o, cudaStream_t s, int ctas_per_sm) {
     bool ok = make_map(&M.u, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, (void *)o.u, W, H, TW, C::TH);
     ok = ok && make_map(&M.a[0], CU_TENSOR_MAP_DATA_TYPE_INT32, 4, o.a0, W, H, TW, C::TH);
     ok = ok && make_map(&M.a[1], CU_TENSOR_MAP_DATA_TYPE_INT32, 4, o.a1, W, H, TW, C::TH);
+    // y2 and yhat carry one ghost row above and below the shard (caller-owned)
     for (int i = 0; i < 3 && ok; ++i) {
-        ok = make_map(&M.y[i], CU_TENSOR_MAP_DATA_TYPE_INT32, 4, o.y2[i], W, H, TW, C::TH + 1);
-        ok = ok && make_map(&M.yr[i], CU_TENSOR_MAP_DATA_TYPE_INT32, 4, o.y2[i], W, H, 4, C::TH);
+        ok = make_map(&M.y[i], CU_TENSOR_MAP_DATA_TYPE_INT32, 4, o.y2[i] - W, W, H + 2, TW, C::TH + 1);
+        ok = ok && make_map(&M.yr[i], CU_TENSOR_MAP_DATA_TYPE_INT32, 4, o.y2[i] - W, W, H + 2, 4, C::TH);
     }
-    ok = ok && make_map(&M.yhat, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.yhat, W, H, C::YHW, C::TH + 2);
+    ok = ok && make_map(&M.yhat, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.yhat - W, W, H + 2, C::YHW, C::TH + 2);
     if (!ok) {
         snprintf(g_last_err, sizeof(g_last_err), "cuTensorMapEncodeTiled failed");
         return DOPE_E_CUDA;
@@ -1353,6 +1457,26 @@ int dope_lattice_check(const dope_lattice *L) {
     return build_plan(L, P);
 }
 
+int dope_prepare_kernels(const dope_lattice *L) {
+    // kernel attributes (dynamic shared memory) must be set outside stream capture
+    Plan P;
+    int rc = build_plan(L, P);
+    if (rc) return rc;
+    if ((rc = configure_plan(P))) return rc;
+    if (P.o.ndim == 2 && P.o.fuse) {
+        const int tw = k2_tma_width(P.o);
+        if (tw == 64)
+            return cuda_check(cudaFuncSetAttribute(k_consensus_tma<64, 512, 3>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   TmaCfg<64, 512, 3>::SMEM), "attr K2");
+        if (tw == 128)
+            return cuda_check(cudaFuncSetAttribute(k_consensus_tma<128, 512, 3>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   TmaCfg<128, 512, 3>::SMEM), "attr K2");
+    }
+    return DOPE_OK;
+}
+
 int dope_admm_init(const dope_lattice *L, void *stream) {
     Plan P;
     int rc = build_plan(L, P);
@@ -1414,7 +1538,7 @@ int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void 
     }
     if (!exec) {
         // kernel attributes must be set outside stream capture
-        if ((rc = configure_plan(P))) return rc;
+        if ((rc = dope_prepare_kernels(L))) return rc;
         cudaStream_t cs;
         if ((rc = cuda_check(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream"))) return rc;
         cudaGraph_t graph;
@@ -1444,6 +1568,51 @@ int dope_finish_run(const dope_lattice *L, void *stream) {
     k_energy_current<<<grid_for(P.n), 256, 0, s>>>(P.o, P.n);
     if ((rc = cuda_check(cudaGetLastError(), "energy_current"))) return rc;
     k_finish_decide<<<1, 1, 0, s>>>(P.o);
+    return cuda_check(cudaGetLastError(), "finish_decide");
+}
+
+int dope_decide(const dope_lattice *L, void *stream) {
+    Plan P;
+    int rc = build_plan(L, P);
+    if (rc) return rc;
+    if (!P.o.sharded) return DOPE_E_ARGS;
+    k_decide<<<1, 1, 0, (cudaStream_t)stream>>>(P.o);
+    return cuda_check(cudaGetLastError(), "decide");
+}
+
+int dope_ghost_update(const dope_lattice *L, int32_t which, const void *up_row, const void *dn_row,
+                      void *stream) {
+    Plan P;
+    int rc = build_plan(L, P);
+    if (rc) return rc;
+    if (which != 0 && which != 1) return DOPE_E_ARGS;
+    k_ghost_update<<<(P.o.W + 255) / 256, 256, 0, (cudaStream_t)stream>>>(P.o, which, up_row, dn_row);
+    return cuda_check(cudaGetLastError(), "ghost_update");
+}
+
+int dope_pack_rows(const dope_lattice *L, int32_t which, void *first_row, void *last_row,
+                   void *stream) {
+    Plan P;
+    int rc = build_plan(L, P);
+    if (rc) return rc;
+    if (which != 0 && which != 1) return DOPE_E_ARGS;
+    k_pack_rows<<<(P.o.W + 255) / 256, 256, 0, (cudaStream_t)stream>>>(P.o, which, first_row, last_row);
+    return cuda_check(cudaGetLastError(), "pack_rows");
+}
+
+int dope_energy_local(const dope_lattice *L, void *stream) {
+    Plan P;
+    int rc = build_plan(L, P);
+    if (rc) return rc;
+    k_energy_current<<<grid_for(P.n), 256, 0, (cudaStream_t)stream>>>(P.o, P.n);
+    return cuda_check(cudaGetLastError(), "energy_local");
+}
+
+int dope_finish_decide(const dope_lattice *L, void *stream) {
+    Plan P;
+    int rc = build_plan(L, P);
+    if (rc) return rc;
+    k_finish_decide<<<1, 1, 0, (cudaStream_t)stream>>>(P.o);
     return cuda_check(cudaGetLastError(), "finish_decide");
 }
 
