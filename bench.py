@@ -184,13 +184,13 @@ def main():
     if ws > 1:
         dist.init_process_group("nccl", init_method="env://")
     from paper_1704_03116_b200 import workloads as W
-    from paper_1704_03116_b200.admm import _DeviceState
+    from paper_1704_03116_b200.admm import make_device_state
     wl = W.by_name(args.config)
     iters = args.iters or wl.iters
     use_graph = int(not args.no_graph)
     if ws == 1 and not args.sharded:
         model, part, problems = build_problem(wl, torch.device("cuda", local))
-        dev = _DeviceState(problems, int(wl.rho), 0.0, iters, True, True)
+        dev = make_device_state(problems, wl.rho, 0.0, iters, True, True)
 
         def step():
             dev.call("dope_admm_init")
@@ -281,8 +281,12 @@ def main():
     peak, peak_kind = measured_peaks()
     n = n_local
     k_local = problems.lowering.K
+    is_float = getattr(problems, "kind", "int") == "float"
+    # K2 algorithmic bytes per pixel: int path read u,a,y (int32) + yhat, write a,y = 21;
+    # float path read u,a,y,r_diag (f64) + 4 weight planes (f64) + yhat, write a,y = 81
+    k2_bpp = 81 if is_float else BYTES_PER_PIXEL_ITER
     if dom == "K2_consensus":
-        alg_bytes = BYTES_PER_PIXEL_ITER * n
+        alg_bytes = k2_bpp * n
     elif dom == "K1_block_mincut":
         # per solved block: read u,a,y (12 B/px), write yhat (1), residual graph r/w (8)
         alg_bytes = (12 + 1 + 8) * (n / k_local) * (solves_per_run / iters_done)
@@ -293,24 +297,28 @@ def main():
     tfile = ROOT / "profiles" / "ncu_traffic.json"
     if tfile.exists():
         tj = json.loads(tfile.read_text())
-        if dom in tj:
-            traffic = tj[dom]["traffic_bytes"]
+        key = f"{wl.name}:{dom}"
+        if key in tj:
+            traffic = tj[key]["traffic_bytes"]
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
             "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one launch)" if traffic else None,
             "kernel": dom,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
             "algorithmic_bytes_per_launch": alg_bytes}
-    iter_bytes = BYTES_PER_PIXEL_ITER * n
+    # 21 B/pixel (+ 4 B per stored non-constant-weight pair on float configs)
+    iter_bytes = BYTES_PER_PIXEL_ITER * n + (4 * wl.num_pairs * n // wl.n if is_float else 0)
     iter_roof = {"bytes_per_iteration_per_gpu": iter_bytes,
                  "achieved_GBps_per_gpu": iter_bytes * value / 1e9,
                  "frac_of_measured_hbm": iter_bytes * value / 1e9 / peak,
-                 "formula": "21 B/pixel/iteration (SURVEY 8(d)) x pixels per GPU x iterations/s"}
+                 "formula": "(21 B/pixel + 4 B/float-weight pair)/iteration (SURVEY 8(d)) x "
+                            "pixels per GPU x iterations/s"}
 
     # ---- e2e through the C ABI with host buffers ----
     e2e = None
     if not args.no_e2e:
         u_host = problems.u.cpu().pin_memory()
+        u_bytes = u_host.numel() * u_host.element_size()
         lab_host = torch.empty(n, dtype=torch.int8).pin_memory()
         tr_host = torch.empty(iters, dtype=torch.int64).pin_memory()
         for s in range(args.warmup + args.steps):
@@ -333,7 +341,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_e2e = float(t.item())
         e2e = {"value": iters_done * args.steps / (ms_e2e / 1e3), "unit": "iterations/s",
-               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": n + 8 * iters}
+               "h2d_bytes_per_step": u_bytes, "d2h_bytes_per_step": n + 8 * iters}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -345,12 +353,14 @@ def main():
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if ws > 1 else "weak",
-            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": f"{wl.name}: {'x'.join(map(str, wl.dims))} {wl.conn}-connected Potts, "
+            "vs_baseline": None, "dtype": "f64" if is_float else "int32", "data": "synthetic",
+            "config": {"workload": f"{wl.name}: {'x'.join(map(str, wl.dims))} {wl.conn}-connected "
+                                   f"{'contrast-weighted' if is_float else 'constant-weight'} Potts, "
                                    f"{wl.num_blocks} sub-regions of {'x'.join(map(str, wl.block))}, "
                                    f"{iters_done} ADMM iterations per step (full run from init)",
                        "pixel_edges_per_s": value * wl.num_pairs,
-                       "l2": "state ~0.4 GB > 126 MB L2 (inputs larger than L2)",
+                       "l2": ("inputs larger than L2 (state > 126 MB)" if wl.n * 21 > 126e6 else
+                              "state fits in the 126 MB L2 (small config; no flush between steps)"),
                        "parallelism": (f"{ws} GPUs: block rows sharded in slabs, NCCL halo "
                                        f"rows + 4-scalar all-reduce per iteration" if ws > 1
                                        else "1 GPU"),

@@ -211,6 +211,51 @@ int dope_bk_maxflow(int32_t m, const double *tcap, int64_t npairs, const int32_t
                     void *stream);
 int64_t dope_bk_workspace_bytes(int32_t m, int64_t npairs);
 
+/* ------------------------------------------------------------------------
+ * Float-weight 2D lattices (BASELINE C2: 8-connected contrast weights).
+ * The block objective is evaluated in float64 in the reference's order and
+ * quantised once: terminal rint(linear*qscale), pair rint(lam*w*qscale); the
+ * block min cut of the quantised energy is solved exactly.  y and a are
+ * float64; state.best_energy holds the best energy's double bits.
+ * ------------------------------------------------------------------------ */
+typedef struct dope_lattice_f {
+    int32_t conn;               /* 4 or 8                                      */
+    int64_t dims[2];            /* H, W                                        */
+    int32_t kpa[2];
+    double lam;                 /* lambda                                      */
+    double mu;                  /* ADMM penalty (mu_fact = 1)                  */
+    double eps;
+    double qscale;              /* capacity quantisation scale (2^16)          */
+    int32_t max_iters, warm_start, skip_clean, fuse_multipliers;
+    const double *u;            /* n                                           */
+    const double *w[4];         /* E S SE SW weight planes: w of pair (i, i+off)
+                                   stored at i (SE/SW only when conn == 8)     */
+    const double *rdiag;        /* n: r = d - dhat (blockform.py:242-243)      */
+    const int32_t *capq[4];     /* rint(lam * w * qscale), same layout          */
+    double *a[2];               /* n, ping-pong                                */
+    double *y[3];               /* n, rotating iterates                        */
+    uint8_t *yhat;              /* n                                           */
+    int32_t *resid;             /* K * dope_f_resid_stride bytes               */
+    uint32_t *dirty;            /* K                                           */
+    double *part_energy;        /* K                                           */
+    double *part_ressq;         /* K                                           */
+    int32_t *part_flags;        /* K                                           */
+    dope_run_state *state;
+    double *trace_energy, *trace_residual_sq, *trace_max_residual;
+    int32_t *trace_clamped;
+} dope_lattice_f;
+
+int64_t dope_f_resid_stride(const dope_lattice_f *L);
+int dope_f_check(const dope_lattice_f *L);
+const char *dope_f_last_error(void);
+int dope_f_admm_init(const dope_lattice_f *L, void *stream);
+int dope_f_update_blocks(const dope_lattice_f *L, void *stream);
+int dope_f_update_global(const dope_lattice_f *L, void *stream);
+int dope_f_update_multipliers(const dope_lattice_f *L, void *stream);
+int dope_f_admm_run(const dope_lattice_f *L, int32_t iters, int32_t use_graph, void *stream);
+int dope_f_finish_run(const dope_lattice_f *L, void *stream);
+int dope_f_binarize(const dope_lattice_f *L, uint8_t *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -77,6 +77,40 @@ class Lattice(C.Structure):
     ]
 
 
+class LatticeF(C.Structure):
+    """Mirror of dope_lattice_f (float-weight 2D lattices)."""
+    _fields_ = [
+        ("conn", C.c_int32),
+        ("dims", C.c_int64 * 2),
+        ("kpa", C.c_int32 * 2),
+        ("lam", C.c_double),
+        ("mu", C.c_double),
+        ("eps", C.c_double),
+        ("qscale", C.c_double),
+        ("max_iters", C.c_int32),
+        ("warm_start", C.c_int32),
+        ("skip_clean", C.c_int32),
+        ("fuse_multipliers", C.c_int32),
+        ("u", C.c_void_p),
+        ("w", C.c_void_p * 4),
+        ("rdiag", C.c_void_p),
+        ("capq", C.c_void_p * 4),
+        ("a", C.c_void_p * 2),
+        ("y", C.c_void_p * 3),
+        ("yhat", C.c_void_p),
+        ("resid", C.c_void_p),
+        ("dirty", C.c_void_p),
+        ("part_energy", C.c_void_p),
+        ("part_ressq", C.c_void_p),
+        ("part_flags", C.c_void_p),
+        ("state", C.c_void_p),
+        ("trace_energy", C.c_void_p),
+        ("trace_residual_sq", C.c_void_p),
+        ("trace_max_residual", C.c_void_p),
+        ("trace_clamped", C.c_void_p),
+    ]
+
+
 class DopeError(RuntimeError):
     pass
 
@@ -140,6 +174,21 @@ def lib():
                                    C.c_int64, C.c_void_p]
     lb.dope_bk_workspace_bytes.restype = C.c_int64
     lb.dope_bk_workspace_bytes.argtypes = [C.c_int32, C.c_int64]
+    PF = C.POINTER(LatticeF)
+    lb.dope_f_resid_stride.restype = C.c_int64
+    lb.dope_f_resid_stride.argtypes = [PF]
+    lb.dope_f_check.restype = C.c_int
+    lb.dope_f_check.argtypes = [PF]
+    lb.dope_f_last_error.restype = C.c_char_p
+    for name in ("dope_f_admm_init", "dope_f_update_blocks", "dope_f_update_global",
+                 "dope_f_update_multipliers", "dope_f_finish_run"):
+        f = getattr(lb, name)
+        f.restype = C.c_int
+        f.argtypes = [PF, C.c_void_p]
+    lb.dope_f_admm_run.restype = C.c_int
+    lb.dope_f_admm_run.argtypes = [PF, C.c_int32, C.c_int32, C.c_void_p]
+    lb.dope_f_binarize.restype = C.c_int
+    lb.dope_f_binarize.argtypes = [PF, C.c_void_p, C.c_void_p]
     if lb.dope_abi_version() != ABI_VERSION:
         raise DopeError(f"libdope_b200 ABI {lb.dope_abi_version()} != {ABI_VERSION}")
     _lib = lb
@@ -153,7 +202,8 @@ def check(rc: int, what: str) -> None:
            DOPE_E_CAPACITY: "capacities exceed the int8 residual range",
            DOPE_E_NONSUBMODULAR: "negative pairwise weights"}.get(rc)
     if rc == DOPE_E_CUDA:
-        msg = "CUDA error: " + lib().dope_last_cuda_error().decode()
+        msg = "CUDA error: " + (lib().dope_last_cuda_error().decode() or
+                                lib().dope_f_last_error().decode())
     raise DopeError(f"{what} failed ({rc}): {msg}")
 
 
@@ -164,4 +214,6 @@ def exported_symbols() -> list[str]:
             "dope_update_multipliers", "dope_admm_run", "dope_finish_run", "dope_binarize", "dope_decide", "dope_ghost_update",
             "dope_pack_rows", "dope_energy_local", "dope_finish_decide", "dope_prepare_kernels",
             "dope_comm_unique_id", "dope_comm_init", "dope_comm_destroy", "dope_sharded_run",
-            "dope_sharded_finish", "dope_energy4", "dope_bk_maxflow", "dope_bk_workspace_bytes"]
+            "dope_sharded_finish", "dope_f_resid_stride", "dope_f_check", "dope_f_last_error",
+            "dope_f_admm_init", "dope_f_update_blocks", "dope_f_update_global",
+            "dope_f_update_multipliers", "dope_f_admm_run", "dope_f_finish_run", "dope_f_binarize", "dope_energy4", "dope_bk_maxflow", "dope_bk_workspace_bytes"]

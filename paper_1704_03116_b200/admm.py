@@ -26,7 +26,7 @@ import numpy as np
 
 from . import _lib
 from .energy import EnergyModel
-from .lowering import LatticeLowering, lower_lattice
+from .lowering import FloatLowering, LatticeLowering, lower_float, lower_lattice
 from .partition import Partition
 
 
@@ -122,7 +122,14 @@ class BlockProblems:
 
     def __init__(self, model: EnergyModel, partition: Partition):
         import torch
-        self.lowering: LatticeLowering = lower_lattice(model, partition)
+        try:
+            self.lowering = lower_lattice(model, partition)
+            self.kind = "int"
+        except NotImplementedError:
+            # not an integer 4/6-connected constant-weight lattice: the float path (2D,
+            # 4/8-connected, any non-negative weights); it raises if that fails too
+            self.lowering = lower_float(model, partition)
+            self.kind = "float"
         self.partition = partition
         self.model = model
         self.device = _device()
@@ -134,6 +141,108 @@ class BlockProblems:
     @property
     def lam(self) -> float:
         return self.lowering.lam
+
+
+class _FloatDeviceState:
+    """Caller-owned device buffers of one float-weight run (dope_lattice_f)."""
+
+    def __init__(self, problems: BlockProblems, mu: float, eps: float, max_iters: int,
+                 warm_start: bool, skip_clean: bool):
+        import torch
+        low: FloatLowering = problems.lowering
+        dev = problems.device
+        n, K = low.n, low.K
+        self.problems = problems
+        self.max_iters = max_iters
+        L = self.L = _lib.LatticeF()
+        L.conn = low.conn
+        L.dims[0], L.dims[1] = low.dims
+        L.kpa[0], L.kpa[1] = low.kpa
+        L.lam, L.mu, L.eps, L.qscale = low.lam, float(mu), float(eps), low.qscale
+        L.max_iters, L.warm_start, L.skip_clean, L.fuse_multipliers = (
+            max_iters, int(warm_start), int(skip_clean), 1)
+        lb = _lib.lib()
+        stride = lb.dope_f_resid_stride(C.byref(L))
+        if stride <= 0:
+            raise NotImplementedError(f"no float K1 variant for {low.dims}/{low.kpa}")
+        f64 = torch.float64
+        t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)
+        self.w = [t(p) for p in low.w]
+        self.capq = [t(p) for p in low.capq]
+        self.rdiag = t(low.rdiag)
+        self.a = [torch.zeros(n, dtype=f64, device=dev) for _ in range(2)]
+        self.y2 = [torch.full((n,), 0.5, dtype=f64, device=dev) for _ in range(3)]
+        self.yhat = torch.zeros(n, dtype=torch.uint8, device=dev)
+        self.resid = torch.zeros(K * stride // 4, dtype=torch.int32, device=dev)
+        self.dirty = torch.ones(K, dtype=torch.int32, device=dev)
+        self.pe = torch.zeros(K, dtype=f64, device=dev)
+        self.pr = torch.zeros(K, dtype=f64, device=dev)
+        self.pf = torch.zeros(K, dtype=torch.int32, device=dev)
+        self.state = torch.zeros(C.sizeof(_lib.RunState), dtype=torch.uint8, device=dev)
+        self.tr_e = torch.zeros(max_iters, dtype=f64, device=dev)
+        self.tr_rs = torch.zeros(max_iters, dtype=f64, device=dev)
+        self.tr_mr = torch.zeros(max_iters, dtype=f64, device=dev)
+        self.tr_cl = torch.zeros(max_iters, dtype=torch.int32, device=dev)
+        L.u = problems.u.data_ptr()
+        for i in range(4):
+            L.w[i] = self.w[i].data_ptr()
+            L.capq[i] = self.capq[i].data_ptr()
+        L.rdiag = self.rdiag.data_ptr()
+        L.a[0], L.a[1] = self.a[0].data_ptr(), self.a[1].data_ptr()
+        for i in range(3):
+            L.y[i] = self.y2[i].data_ptr()
+        L.yhat = self.yhat.data_ptr()
+        L.resid = self.resid.data_ptr()
+        L.dirty = self.dirty.data_ptr()
+        L.part_energy, L.part_ressq, L.part_flags = (self.pe.data_ptr(), self.pr.data_ptr(),
+                                                     self.pf.data_ptr())
+        L.state = self.state.data_ptr()
+        L.trace_energy, L.trace_residual_sq = self.tr_e.data_ptr(), self.tr_rs.data_ptr()
+        L.trace_max_residual, L.trace_clamped = self.tr_mr.data_ptr(), self.tr_cl.data_ptr()
+        _lib.check(lb.dope_f_check(C.byref(L)), "dope_f_check")
+
+    _NAMES = {"dope_admm_init": "dope_f_admm_init", "dope_update_blocks": "dope_f_update_blocks",
+              "dope_update_global": "dope_f_update_global",
+              "dope_update_multipliers": "dope_f_update_multipliers",
+              "dope_admm_run": "dope_f_admm_run", "dope_finish_run": "dope_f_finish_run"}
+
+    def stream(self):
+        import torch
+        return C.c_void_p(torch.cuda.current_stream(self.problems.device).cuda_stream)
+
+    def call(self, name: str, *args, fuse: int | None = None):
+        if fuse is not None:
+            self.L.fuse_multipliers = fuse
+        fname = self._NAMES[name]
+        _lib.check(getattr(_lib.lib(), fname)(C.byref(self.L), *args, self.stream()), fname)
+
+    def run_state(self) -> _lib.RunState:
+        return _lib.RunState.from_buffer_copy(self.state.cpu().numpy().tobytes())
+
+    def y2_current(self):
+        # float path stores y itself; expose 2*y for a uniform host view
+        return self.y2[self.run_state().ycur] * 2.0
+
+    def binarize(self):
+        import torch
+        out = torch.empty(self.problems.lowering.n, dtype=torch.uint8, device=self.problems.device)
+        _lib.check(_lib.lib().dope_f_binarize(C.byref(self.L), out.data_ptr(), self.stream()),
+                   "dope_f_binarize")
+        return out
+
+    def raise_on_error(self):
+        rs = self.run_state()
+        if rs.error:
+            raise BlockSolveError(rs.error - 1, "push-relabel round limit exceeded")
+        return rs
+
+
+def make_device_state(problems: BlockProblems, mu: float, eps: float, max_iters: int,
+                      warm_start: bool = True, skip_clean: bool = True):
+    """Device buffers of one run for the lowering kind (int or float lattice)."""
+    if problems.kind == "float":
+        return _FloatDeviceState(problems, mu, eps, max_iters, warm_start, skip_clean)
+    return _DeviceState(problems, int(mu), eps, max_iters, warm_start, skip_clean)
 
 
 def assemble_block_problems(model: EnergyModel, partition: Partition) -> BlockProblems:
@@ -263,6 +372,11 @@ class AdmmState:
         if self._dev is not None and self._dev.problems is problems:
             return self._dev
         mu = self.mu
+        if problems.kind == "float":
+            self._dev = _FloatDeviceState(problems, mu, eps, max_iters or config.max_iters,
+                                          config.warm_start, config.skip_clean)
+            self._dev.call("dope_admm_init")
+            return self._dev
         if mu != round(mu) or mu <= 0:
             raise NotImplementedError("the integer lattice path needs an integer mu")
         if problems.lowering.lamw % int(mu) != 0:
@@ -285,9 +399,13 @@ class AdmmState:
             raise RuntimeError("bind the state to problems before assigning y")
         import torch
         v = np.asarray(value, dtype=np.float64)
-        if v.shape != (self._n,) or not np.all(np.isin(v, (0.0, 0.5, 1.0))):
+        if v.shape != (self._n,) or (not isinstance(self._dev, _FloatDeviceState)
+                                     and not np.all(np.isin(v, (0.0, 0.5, 1.0)))):
             raise NotImplementedError("the integer lattice path holds y in {0, 1/2, 1}")
-        self._dev.y2_current().copy_(torch.as_tensor((2 * v).astype(np.int32)))
+        if isinstance(self._dev, _FloatDeviceState):
+            self._dev.y2[self._dev.run_state().ycur].copy_(torch.as_tensor(v))
+        else:
+            self._dev.y2_current().copy_(torch.as_tensor((2 * v).astype(np.int32)))
         self._dev.dirty.fill_(1)
 
     def _global_to_blocks(self, vec: np.ndarray, dtype) -> list:
@@ -312,7 +430,7 @@ class AdmmState:
         if self._dev is None:
             return np.zeros(self._n)
         rs = self._dev.run_state()
-        return self._dev.a[rs.parity].cpu().numpy().astype(np.float64)
+        return self._dev.a[rs.parity].double().cpu().numpy()
 
     def labels_global(self) -> np.ndarray:
         """Current block labels (yhat) in global layout."""
@@ -356,7 +474,7 @@ def update_multipliers(state: AdmmState, partition: Partition, mu_fact: float) -
     if state._dev is None:
         raise RuntimeError("state is not bound to device problems")
     if mu_fact != 1.0:
-        raise NotImplementedError("the integer lattice path keeps mu fixed (mu_fact == 1)")
+        raise NotImplementedError("the B200 path keeps mu fixed (mu_fact == 1)")
     state._dev.call("dope_update_multipliers")
     state.mu *= mu_fact
     return state
@@ -390,7 +508,7 @@ def run(model: EnergyModel, partition: Partition, config: AdmmConfig,
     mu0 = config.resolved_mu0(partition.shape.ndim)
     eps = config.resolved_eps(partition)
     if config.mu_fact != 1.0:
-        raise NotImplementedError("the integer lattice path keeps mu fixed (mu_fact == 1)")
+        raise NotImplementedError("the B200 path keeps mu fixed (mu_fact == 1)")
     state = init_state(partition, mu0)
     dev = state._bind(problems, config, config.max_iters, eps)
     start = torch.cuda.Event(enable_timing=True)

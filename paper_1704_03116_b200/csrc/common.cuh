@@ -1,0 +1,192 @@
+// common.cuh -- helpers shared by the lattice kernels (dope_lattice.cu,
+// dope_float.cu): block geometry of the reference's partition rule and the
+// one-warp bit-parallel global-relabel BFS.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define FULLMASK 0xffffffffu
+
+namespace dope {
+
+constexpr uint16_t HINF = 0xFFFF;
+
+// ---------------------------------------------------------------------------
+// Geometry helpers (partition.py:62-77 with overlap 0)
+// ---------------------------------------------------------------------------
+
+struct Axis {
+    int32_t dim, k, base, rem;
+    __host__ __device__ void range(int32_t r, int32_t &lo, int32_t &len) const {
+        lo = r * base + (r < rem ? r : rem);
+        len = base + (r < rem ? 1 : 0);
+    }
+    __host__ __device__ int32_t owner(int32_t c) const {
+        int32_t big = rem * (base + 1);
+        return c < big ? c / (base + 1) : rem + (c - big) / base;
+    }
+};
+
+__host__ __device__ inline Axis make_axis(int64_t dim, int32_t k) {
+    Axis a;
+    a.dim = (int32_t)dim;
+    a.k = k;
+    a.base = (int32_t)(dim / k);
+    a.rem = (int32_t)(dim % k);
+    return a;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// Bit-parallel BFS helpers (one warp).  The block's nodes are numbered
+// v = r*BW + c over the padded box; bit v of the 64-bit word array is node v.
+// Lane `l` owns words [l*WPL, (l+1)*WPL).
+// ---------------------------------------------------------------------------
+
+template <int WPL, int LANES, int T>
+__device__ __forceinline__ uint64_t fetch_word(const uint64_t (&R)[WPL], int lane) {
+    // word index lane*WPL + T  (T compile-time, may be negative)
+    constexpr int DL = (T >= 0) ? (T / WPL) : -((-T + WPL - 1) / WPL);
+    constexpr int SLOT = T - DL * WPL;
+    uint64_t v = R[SLOT];
+    if constexpr (DL > 0) {
+        v = __shfl_down_sync(FULLMASK, v, DL);
+        if (lane + DL >= LANES) v = 0;
+    } else if constexpr (DL < 0) {
+        v = __shfl_up_sync(FULLMASK, v, -DL);
+        if (lane + DL < 0) v = 0;
+    }
+    return v;
+}
+
+// out[k] = bits of R shifted so that bit x holds R[x + S]  (S != 0)
+template <int WPL, int LANES, int S, int K>
+__device__ __forceinline__ uint64_t shifted(const uint64_t (&R)[WPL], int lane) {
+    if constexpr (S > 0) {
+        constexpr int Q = S / 64, REM = S % 64;
+        uint64_t lo = fetch_word<WPL, LANES, K + Q>(R, lane);
+        if constexpr (REM == 0) {
+            return lo;
+        } else {
+            uint64_t hi = fetch_word<WPL, LANES, K + Q + 1>(R, lane);
+            return (lo >> REM) | (hi << (64 - REM));
+        }
+    } else {
+        constexpr int T = -S;
+        constexpr int Q = T / 64, REM = T % 64;
+        uint64_t hi = fetch_word<WPL, LANES, K - Q>(R, lane);
+        if constexpr (REM == 0) {
+            return hi;
+        } else {
+            uint64_t lo = fetch_word<WPL, LANES, K - Q - 1>(R, lane);
+            return (hi << REM) | (lo >> (64 - REM));
+        }
+    }
+}
+
+// node v joins the reached set when it has a residual arc to an already
+// reached node: direction d's mask holds "residual arc v -> v + off_d".
+// Direction order: E(+1) W(-1) S(+BW) N(-BW) [D(+PL) U(-PL) in 3D].
+template <int NW, int WPL, int LANES, int BW, int PL, bool DIAG, int K>
+struct Expand {
+    __device__ __forceinline__ static void run(const uint64_t (&R)[WPL], uint64_t (&NEW)[WPL],
+                                               const uint64_t *__restrict__ m, int lane) {
+        Expand<NW, WPL, LANES, BW, PL, DIAG, K - 1>::run(R, NEW, m, lane);
+        const int idx = lane * WPL + (K - 1);
+        const bool on = lane < LANES;
+        uint64_t x = 0;
+        const uint64_t e = on ? m[0 * NW + idx] : 0, w = on ? m[1 * NW + idx] : 0;
+        const uint64_t sm = on ? m[2 * NW + idx] : 0, n = on ? m[3 * NW + idx] : 0;
+        x = (e & shifted<WPL, LANES, 1, K - 1>(R, lane)) | (w & shifted<WPL, LANES, -1, K - 1>(R, lane)) |
+            (sm & shifted<WPL, LANES, BW, K - 1>(R, lane)) | (n & shifted<WPL, LANES, -BW, K - 1>(R, lane));
+        if constexpr (PL > 0) {
+            const uint64_t dd = on ? m[4 * NW + idx] : 0, uu = on ? m[5 * NW + idx] : 0;
+            x |= (dd & shifted<WPL, LANES, PL, K - 1>(R, lane)) | (uu & shifted<WPL, LANES, -PL, K - 1>(R, lane));
+        }
+        if constexpr (DIAG) {   // SE(+BW+1) NW(-BW-1) SW(+BW-1) NE(-BW+1)
+            const uint64_t se = on ? m[4 * NW + idx] : 0, nw = on ? m[5 * NW + idx] : 0;
+            const uint64_t sw = on ? m[6 * NW + idx] : 0, ne = on ? m[7 * NW + idx] : 0;
+            x |= (se & shifted<WPL, LANES, BW + 1, K - 1>(R, lane)) |
+                 (nw & shifted<WPL, LANES, -BW - 1, K - 1>(R, lane)) |
+                 (sw & shifted<WPL, LANES, BW - 1, K - 1>(R, lane)) |
+                 (ne & shifted<WPL, LANES, -BW + 1, K - 1>(R, lane));
+        }
+        NEW[K - 1] = x & ~R[K - 1];
+    }
+};
+template <int NW, int WPL, int LANES, int BW, int PL, bool DIAG>
+struct Expand<NW, WPL, LANES, BW, PL, DIAG, 0> {
+    __device__ __forceinline__ static void run(const uint64_t (&)[WPL], uint64_t (&)[WPL],
+                                               const uint64_t *__restrict__, int) {}
+};
+
+// Global relabel: exact BFS distances to the sink set (g < 0) over residual
+// arcs, written to h[] for nodes beyond the sink set (the caller has set
+// h = 0 on the sink set and HINF elsewhere).  `masks` holds NDIR direction
+// masks followed by the sink and active masks, NW words each.  Returns (on
+// every lane of the calling warp) whether any active node (g > 0) is
+// reached; `reach` receives the reached set.  Early exit once every active
+// node has a level, except when there is none (then the BFS runs to
+// completion and `reach` is the exact sink side).
+template <int NW, int BW, int PL, bool DIAG = false>
+__device__ int bfs_relabel(const uint64_t *__restrict__ masks, uint64_t *__restrict__ reach,
+                           uint16_t *__restrict__ h, int lane, int *levels_out) {
+    constexpr int NDIR = PL > 0 ? 6 : (DIAG ? 8 : 4);
+    constexpr int LANES = NW < 32 ? NW : 32;
+    constexpr int WPL = NW < 32 ? 1 : NW / 32;
+    static_assert(NW % LANES == 0, "word layout");
+    const uint64_t *mSink = masks + NDIR * NW, *mAct = masks + (NDIR + 1) * NW;
+    const bool on = lane < LANES;
+    uint64_t R[WPL], A[WPL], NEW[WPL];
+    bool any_act = false;
+#pragma unroll
+    for (int k = 0; k < WPL; ++k) {
+        const int idx = lane * WPL + k;
+        R[k] = on ? mSink[idx] : 0;
+        A[k] = on ? mAct[idx] : 0;
+        any_act |= (A[k] != 0);
+    }
+    const bool have_active = __any_sync(FULLMASK, any_act);
+    int level = 0;
+    for (;;) {
+        if (have_active) {
+            bool missing = false;
+#pragma unroll
+            for (int k = 0; k < WPL; ++k) missing |= (A[k] & ~R[k]) != 0;
+            if (!__any_sync(FULLMASK, missing)) break;
+        }
+        Expand<NW, WPL, LANES, BW, PL, DIAG, WPL>::run(R, NEW, masks, lane);
+        bool grew = false;
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) grew |= (NEW[k] != 0);
+        if (!__any_sync(FULLMASK, grew)) break;
+        ++level;
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) {
+            R[k] |= NEW[k];
+            uint64_t nb = NEW[k];
+            const int base = (lane * WPL + k) * 64;
+            while (nb) {
+                const int b = __ffsll((long long)nb) - 1;
+                nb &= nb - 1;
+                h[base + b] = (uint16_t)level;
+            }
+        }
+    }
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < WPL; ++k) {
+        if (on) reach[lane * WPL + k] = R[k];
+        hit |= (A[k] & R[k]) != 0;
+    }
+    *levels_out = level;
+    return __any_sync(FULLMASK, hit);
+}
+
+}  // namespace dope

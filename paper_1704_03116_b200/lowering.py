@@ -102,3 +102,113 @@ def lower_lattice(model: EnergyModel, partition: Partition) -> LatticeLowering:
         raise NotImplementedError("unary costs must be (bounded) integers on the integer path")
     return LatticeLowering(tuple(shape.dims), tuple(partition.k_per_axis), conn, int(round(lamw_f)),
                            u.astype(np.int32), float(model.lam))
+
+
+@dataclass
+class FloatLowering:
+    """Float-weight 2D lattice (C2): weight planes, r_diag, quantised capacities."""
+    dims: tuple
+    kpa: tuple
+    conn: int                 # 4 or 8
+    u: np.ndarray             # float64
+    w: list                   # E, S[, SE, SW] planes (float64, at the lower pixel)
+    rdiag: np.ndarray         # float64
+    capq: list                # int32 planes rint(lam*w*qscale)
+    lam: float
+    qscale: float
+
+    @property
+    def n(self) -> int:
+        return int(np.prod(self.dims))
+
+    @property
+    def K(self) -> int:
+        return int(np.prod(self.kpa))
+
+
+QSCALE = float(2 ** 16)
+
+
+def _block_ids(n_axis: int, k: int) -> np.ndarray:
+    base, rem = divmod(n_axis, k)
+    sizes = [base + (1 if r < rem else 0) for r in range(k)]
+    return np.repeat(np.arange(k), sizes)
+
+
+def lower_float(model: EnergyModel, partition: Partition, qscale: float = QSCALE) -> FloatLowering:
+    """Lower a 2D lattice model with arbitrary non-negative pair weights."""
+    shape = partition.shape
+    if shape.ndim != 2:
+        raise NotImplementedError("float-weight lattices are implemented in 2D")
+    if partition.overlap_pct != 0 or (partition.counts.size and int(partition.counts.max()) != 1):
+        raise NotImplementedError("overlapping partitions (q > 1) have no B200 kernel yet")
+    H, W = shape.dims
+    w = model.weights
+    if w.npairs and float(w.vals.min()) < 0:
+        raise NonSubmodularError("pairwise weights contain negative entries; max-flow requires "
+                                 "a submodular instance, use the icm solver instead")
+    r = w.rows.astype(np.int64)
+    c = w.cols.astype(np.int64)
+    dy = c // W - r // W
+    dx = c % W - r % W
+    kinds = {(0, 1): 0, (1, 0): 1, (1, 1): 2, (1, -1): 3}
+    planes = [np.zeros(H * W) for _ in range(4)]
+    conn = 4
+    for (ddy, ddx), d in kinds.items():
+        sel = (dy == ddy) & (dx == ddx)
+        if d >= 2 and sel.any():
+            conn = 8
+        if sel.any():
+            if np.bincount(r[sel], minlength=H * W).max() > 1:
+                raise NotImplementedError("duplicate lattice pairs")
+            planes[d][r[sel]] = w.vals[sel]
+    known = np.zeros(r.size, dtype=bool)
+    for (ddy, ddx) in kinds:
+        known |= (dy == ddy) & (dx == ddx)
+    if not known.all():
+        raise NotImplementedError("pairwise weights are not a 4/8-connected 2D lattice stencil")
+    P = [p.reshape(H, W) for p in planes]
+    z = np.zeros((H, W))
+    bid = _block_ids(H, partition.k_per_axis[0])[:, None] * partition.k_per_axis[1] + \
+        _block_ids(W, partition.k_per_axis[1])[None, :]
+
+    def shifted(a, sy, sx):
+        """out[y, x] = a[y + sy, x + sx] (0 outside)."""
+        out = np.zeros_like(a)
+        ys, yd = (slice(sy, None), slice(0, H - sy)) if sy >= 0 else (slice(0, H + sy), slice(-sy, None))
+        xs, xd = (slice(sx, None), slice(0, W - sx)) if sx >= 0 else (slice(0, W + sx), slice(-sx, None))
+        out[yd, xd] = a[ys, xs]
+        return out
+
+    same = {}
+    for key, (sy, sx) in {"E": (0, 1), "S": (1, 0), "SE": (1, 1), "SW": (1, -1), "W": (0, -1),
+                          "N": (-1, 0), "NW": (-1, -1), "NE": (-1, 1)}.items():
+        same[key] = shifted(bid, sy, sx) == bid
+    wE, wS, wSE, wSW = P
+    wW = shifted(wE, 0, -1)
+    wN = shifted(wS, -1, 0)
+    wNW = shifted(wSE, -1, -1) if conn == 8 else z
+    wNE = shifted(wSW, -1, 1) if conn == 8 else z
+    if conn == 8:
+        fwd, bwd = [wE, wS, wSE, wSW], [wW, wN, wNW, wNE]
+        fin = [("E", wE), ("SW", wSW), ("S", wS), ("SE", wSE)]
+        bin_ = [("NW", wNW), ("N", wN), ("NE", wNE), ("W", wW)]
+    else:
+        fwd, bwd = [wE, wS], [wW, wN]
+        fin = [("E", wE), ("S", wS)]
+        bin_ = [("N", wN), ("W", wW)]
+    # r = d - dhat in dope_oracle.c's order (blockform.py:242-243 / energy.py:64-76)
+    dsum = np.zeros((H, W))
+    for p in fwd + bwd:
+        dsum = dsum + p
+    dhat = np.zeros((H, W))
+    for key, p in fin + bin_:
+        dhat = dhat + np.where(same[key], p, 0.0)
+    rdiag = (dsum - dhat).ravel()
+    caps = [np.rint(float(model.lam) * p * qscale) for p in planes[:(4 if conn == 8 else 2)]]
+    if caps and max(float(cp.max(initial=0)) for cp in caps) > 2 ** 29:
+        raise NotImplementedError("quantised capacities overflow int32")
+    capq = [cp.astype(np.int32) for cp in caps] + [np.zeros(H * W, dtype=np.int32)] * (4 - len(caps))
+    return FloatLowering((H, W), tuple(partition.k_per_axis), conn,
+                         np.asarray(model.unary, dtype=np.float64), planes, rdiag, capq,
+                         float(model.lam), qscale)

@@ -161,6 +161,74 @@ def c4(seed: int = 0, size: int = 256, block: int = 32, iters: int = 60) -> Work
                     u.ravel(), [1, 1, 1], 1.0, 1.0, iters, True)
 
 
+def _polygon_mask(shape, ys, xs):
+    """Even-odd point-in-polygon over the polygon's bounding box (pixel centres)."""
+    h, w = shape
+    y0, y1 = max(0, int(np.floor(ys.min()))), min(h, int(np.ceil(ys.max())) + 1)
+    x0, x1 = max(0, int(np.floor(xs.min()))), min(w, int(np.ceil(xs.max())) + 1)
+    mask = np.zeros(shape, dtype=bool)
+    if y0 >= y1 or x0 >= x1:
+        return mask
+    py = np.arange(y0, y1, dtype=np.float64)[:, None]
+    px = np.arange(x0, x1, dtype=np.float64)[None, :]
+    inside = np.zeros((y1 - y0, x1 - x0), dtype=bool)
+    n = len(ys)
+    for k in range(n):
+        ya, xa, yb, xb = ys[k], xs[k], ys[(k + 1) % n], xs[(k + 1) % n]
+        if ya == yb:
+            continue
+        cross = (ya > py) != (yb > py)
+        xint = (xb - xa) * (py - ya) / (yb - ya) + xa
+        inside ^= cross & (px < xint)
+    mask[y0:y1, x0:x1] = inside
+    return mask
+
+
+def c2(seed: int = 0, size: int = 1024, block: int = 64, iters: int = 100) -> Workload:
+    """1024^2 8-conn contrast-sensitive Potts (float): background colour U[0,1]^3;
+    12 star polygons (3..8 vertices, radius U[0.04,0.16]*size around a centre
+    U[0,size)^2, colour U[0,1]^3); + N(0, 0.08^2) noise, not clipped; fixed
+    Gaussian colour models (fg mean = mean polygon colour, bg mean = background
+    colour, isotropic sigma_c = 0.25): u = loglik_bg - loglik_fg
+    (energy.py:315-316 convention); w = exp(-|x_i-x_j|^2 / (2*0.1^2)) / dist;
+    lam = 2.0; blocks of 64^2; rho = 0.5; 100 iterations.  u and w rounded to
+    float32.  Draws: background, then per polygon (nv,
+    centre, radii, angles, colour), then the noise."""
+    rng = np.random.default_rng(seed)
+    bg = rng.uniform(0, 1, 3)
+    img = np.empty((size, size, 3))
+    img[:] = bg
+    cols = []
+    for _ in range(12):
+        nv = int(rng.integers(3, 9))
+        cy, cx = rng.uniform(0, size, 2)
+        rad = rng.uniform(0.04, 0.16, nv) * size
+        ang = np.sort(rng.uniform(0, 2 * np.pi, nv))
+        col = rng.uniform(0, 1, 3)
+        mask = _polygon_mask((size, size), cy + rad * np.sin(ang), cx + rad * np.cos(ang))
+        img[mask] = col
+        cols.append(col)
+    img += rng.normal(0.0, 0.08, img.shape)
+    fg = np.mean(cols, axis=0)
+    sc = 0.25
+    u = (((img - fg) ** 2).sum(-1) - ((img - bg) ** 2).sum(-1)) / (2 * sc * sc)
+    u = u.astype(np.float32).astype(np.float64).ravel()
+    planes = []
+    for off in STENCILS[(2, 8)]:
+        dy, dx = off
+        dist = np.sqrt(dy * dy + dx * dx)
+        wpl = np.zeros((size, size))
+        ys = slice(0, size - dy)
+        xs = slice(max(0, -dx), size - max(0, dx))
+        yd = slice(dy, size)
+        xd = slice(max(0, dx), size + min(0, dx))
+        d2 = ((img[ys, xs] - img[yd, xd]) ** 2).sum(-1)
+        wpl[ys, xs] = np.exp(-d2 / (2 * 0.1 * 0.1)) / dist
+        planes.append(wpl.astype(np.float32).astype(np.float64).ravel())
+    return Workload("C2" if size == 1024 else f"C2-{size}", (size, size), (block, block), 8, u,
+                    planes, 2.0, 0.5, iters, False)
+
+
 def mini_disks(size=256, block=64, ndisks=8, weight=2, iters=20, seed=0, rmax=80.0) -> Workload:
     """Small C3-like case for parity tests (oracle finishes in seconds)."""
     return disks_workload(f"mini{size}-b{block}", size, ndisks, block, weight, iters,
@@ -175,6 +243,8 @@ def by_name(name: str, seed: int = 0) -> Workload:
         return c3(seed)
     if name == "C4":
         return c4(seed)
+    if name == "C2":
+        return c2(seed)
     if name.startswith("C5"):
         b = int(name.split("B")[-1]) if "B" in name else 64
         return c5(b, seed)

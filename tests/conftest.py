@@ -47,5 +47,5 @@ def spec_from_golden(g: dict):
     else:
         kpa = tuple(d // int(b) for d, b in zip(dims, g["block"]))
     offs = STENCILS[(len(dims), int(g["conn"]))]
-    return LatticeSpec(dims, kpa, offs, [1.0] * len(offs), g["u"].astype(np.float64),
-                       float(g["lam"]))
+    weights = list(g["wplanes"]) if "wplanes" in g else [1.0] * len(offs)
+    return LatticeSpec(dims, kpa, offs, weights, g["u"].astype(np.float64), float(g["lam"]))

@@ -155,6 +155,8 @@ def save_run(case: str, wl: W.Workload, iters: int | None = None, store_u: bool 
                 rho=wl.rho, max_iters=iters if iters else wl.iters, name=wl.name)
     if store_u:
         meta["u"] = wl.u
+    if not wl.integer:
+        meta["wplanes"] = np.stack([np.asarray(w, dtype=np.float64) for w in wl.weights])
     np.savez_compressed(OUT / f"run_{case}.npz", **r, **meta)
     print(f"run_{case}: iters={r['iterations']} converged={r['converged']} "
           f"best={r['best_iteration']} E_last={r['energy'][-1]}")
@@ -169,6 +171,9 @@ class _RaggedWL(W.Workload):
 def main():
     core = ref_core()
     ref_maxflow.bk_maxflow = core.bk_maxflow     # the reference's own seam swap
+    if "--only-float" in sys.argv:
+        save_run("c2mini", W.c2(size=128, block=32, iters=30))
+        return
     gen_bk(core)
     save_run("c1", W.c1())
     save_run("mini256", W.mini_disks(256, 64, 8, 2, 25, seed=1))
@@ -187,6 +192,9 @@ def main():
     # early convergence (stop rule admm.py:305-307): one block converges at it 1
     one = W.mini_disks(64, 64, 2, 1, 10, seed=5, rmax=20.0)
     save_run("single_block", one)
+    # float config C2 (8-conn contrast weights, rho = 0.5) at 128^2 with 16 blocks
+    if "--only-float" in sys.argv or True:
+        save_run("c2mini", W.c2(size=128, block=32, iters=30))
     # rho = 2 with lam*w = 2: lam/mu = 1 stays integral
     r2 = W.mini_disks(128, 32, 4, 2, 15, seed=6, rmax=40.0)
     r2.rho = 2.0

@@ -14,7 +14,7 @@ from conftest import golden_cases, load_golden, spec_from_golden
 
 pytestmark = pytest.mark.gpu
 
-CASES_ALL = golden_cases()
+CASES_ALL = [c for c in golden_cases() if not c.startswith("c2")]   # integer configs
 
 
 def model_from_golden(g):
@@ -198,3 +198,42 @@ def test_3d_grids_match_oracle(size, block, iters):
     assert np.array_equal([t.energy for t in state.trace], ref["energy"])
     assert np.array_equal(state.labels_global(), ref["yhat"])
     assert np.array_equal(labels, ref["labels"])
+
+
+def _float_model(wl):
+    rows, cols, vals = wl.pair_arrays()
+    model = dope.EnergyModel(wl.u, dope.SparseWeights(wl.n, rows, cols, vals), wl.lam)
+    part = dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0, materialize=False)
+    return model, part
+
+
+def test_float_c2mini_matches_reference_within_tolerance():
+    """C2-like float config vs the reference trace: BASELINE's bar is final energy
+    within 1e-5 relative and <= 0.01 % label disagreement; we also check every
+    iteration's energy and the block labels."""
+    g = load_golden("run_c2mini.npz")
+    wl = W.c2(size=128, block=32, iters=int(g["max_iters"]))
+    assert np.array_equal(wl.u, g["u"])
+    model, part = _float_model(wl)
+    cfg = dope.AdmmConfig(mu0=float(g["rho"]), mu_fact=1.0, eps=0.0, max_iters=int(g["max_iters"]))
+    labels, state = dope.run(model, part, cfg)
+    e = np.array([t.energy for t in state.trace])
+    np.testing.assert_allclose(e, g["energy"], rtol=1e-5)
+    assert abs(e[-1] - g["energy"][-1]) <= 1e-5 * abs(g["energy"][-1])
+    assert np.mean(labels != g["labels"]) <= 1e-4
+    hist = np.unpackbits(g["yhat_bits"], axis=1)[:, :model.n]
+    assert np.mean(state.labels_global() != hist[state.iteration - 1]) <= 1e-4
+
+
+@pytest.mark.parametrize("size,block,iters", [(256, 64, 20), (512, 64, 10)])
+def test_float_grids_match_oracle_within_tolerance(size, block, iters):
+    import oracle as orc
+    wl = W.c2(seed=5, size=size, block=block, iters=iters)
+    model, part = _float_model(wl)
+    labels, state = dope.run(model, part, dope.AdmmConfig(mu0=wl.rho, mu_fact=1.0, eps=0.0,
+                                                          max_iters=iters))
+    spec = orc.LatticeSpec(wl.dims, wl.kpa, wl.offsets, wl.weights, wl.u, wl.lam)
+    ref = orc.run(spec, wl.rho, 1.0, 0.0, iters, threads=16)
+    e = np.array([t.energy for t in state.trace])
+    np.testing.assert_allclose(e, ref["energy"], rtol=1e-5)
+    assert np.mean(labels != ref["labels"]) <= 1e-4

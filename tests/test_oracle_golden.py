@@ -60,11 +60,18 @@ def test_oracle_run_matches_reference_trace(case):
     assert out["best_iteration"] == int(g["best_iteration"])
     hist = np.unpackbits(g["yhat_bits"], axis=1)[:, :spec.n]
     assert np.array_equal(out["yhat_history"], hist)
-    assert np.array_equal(out["energy"], g["energy"])
-    assert np.array_equal(out["max_block_residual"], g["max_block_residual"])
-    np.testing.assert_allclose(out["residual_sq"], g["residual_sq"], rtol=1e-12)
     assert np.array_equal(out["clamped"], g["clamped"])
     assert np.array_equal(out["mu"], g["mu"])
-    assert np.array_equal(out["y"], g["y"])
-    assert np.array_equal(out["a"], g["a"])
     assert np.array_equal(out["labels"], g["labels"])
+    if "wplanes" in g:   # float config: the reference's BLAS dot order is not restated
+        np.testing.assert_allclose(out["energy"], g["energy"], rtol=1e-13)
+        np.testing.assert_allclose(out["max_block_residual"], g["max_block_residual"], rtol=1e-13)
+        np.testing.assert_allclose(out["residual_sq"], g["residual_sq"], rtol=1e-12)
+        np.testing.assert_allclose(out["y"], g["y"], atol=1e-12)
+        np.testing.assert_allclose(out["a"], g["a"], atol=1e-12)
+    else:                # integer configs: bit-exact
+        assert np.array_equal(out["energy"], g["energy"])
+        assert np.array_equal(out["max_block_residual"], g["max_block_residual"])
+        np.testing.assert_allclose(out["residual_sq"], g["residual_sq"], rtol=1e-12)
+        assert np.array_equal(out["y"], g["y"])
+        assert np.array_equal(out["a"], g["a"])

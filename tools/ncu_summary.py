@@ -55,6 +55,7 @@ def launches(path):
 
 def main():
     tag, lcsv, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
+    workload = tag.split("_")[-1] if "_" in tag else "C3"   # e.g. r1_C3
     lines = [f"# ncu summary `{tag}`", "",
              "Captured on one B200 with `ncu --clock-control none` (launch list: "
              "`--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum`; "
@@ -99,7 +100,7 @@ def main():
             unit_scale = 1.0
             key = "K2_consensus" if "consensus" in (kname or "") else (
                 "K1_block_mincut" if "mincut" in (kname or "") else kname)
-            traffic[key] = {"dram_read_bytes": rd * unit_scale, "dram_write_bytes": wr * unit_scale,
+            traffic[f"{workload}:{key}"] = {"dram_read_bytes": rd * unit_scale, "dram_write_bytes": wr * unit_scale,
                             "traffic_bytes": (rd + wr) * unit_scale, "source": f"profiles/{tag}_ncu.md",
                             "kernel": kname}
         except (KeyError, ValueError):
