@@ -246,6 +246,6 @@ def by_name(name: str, seed: int = 0) -> Workload:
     if name == "C2":
         return c2(seed)
     if name.startswith("C5"):
-        b = int(name.split("B")[-1]) if "B" in name else 64
+        b = int(name.split("-B")[-1]) if "-B" in name else 64
         return c5(b, seed)
     raise KeyError(name)
