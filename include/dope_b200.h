@@ -69,18 +69,27 @@ typedef struct dope_run_state {
     int32_t ycur;               /* y buffer (0..2) holding the current iterate */
     int32_t ybest;              /* y buffer holding the best iterate           */
     int32_t parity;             /* which multiplier buffer is current          */
-    int32_t error;              /* 0 or 1 + first failing block id             */
+    int32_t error;              /* 0, 1 + first failing block id, or -1 when
+                                   the multipliers would leave int16          */
     int32_t max_rounds_seen;    /* diagnostics: max global-relabel rounds      */
     int32_t done_ctas;          /* last-CTA-done counter of the consensus pass */
     int64_t solves;             /* diagnostics: block solves performed         */
     int64_t sweeps;             /* diagnostics: push/relabel sweeps            */
     int64_t energy_acc;         /* scratch of the end-of-run energy pass       */
+    int64_t unary2;             /* sum u * y2 of the current iterate (kept
+                                   incrementally: u is read only where y moved) */
+    int32_t a_bound;            /* multiplier passes so far: an upper bound on
+                                   |a| (int16 storage; the run loop stops with
+                                   error -1 at 32000)                          */
+    int32_t reserved_;
 } dope_run_state;
 
 /* Integer lattice problem (C1, C3, C4, C5 of BASELINE.json).
  * Scaling: all quantities that are half-integers in the reference are held
  * doubled: y2 = 2*y (y = 1/2 at init, {0,1} afterwards), block terminal
- * capacity 2*linear, pair capacity 2*lambda*w.  Energies are exact integers. */
+ * capacity 2*linear, pair capacity 2*lambda*w.  Energies are exact integers.
+ * Storage: y2 as uint8 (values 0, 1, 2), multipliers as int16 (|a| grows by
+ * at most 1 per iteration; runs are limited to 32000 iterations), u int32. */
 typedef struct dope_lattice {
     int32_t ndim;               /* 2 or 3                                     */
     int32_t conn;               /* 4 (2D) or 6 (3D)                           */
@@ -97,13 +106,14 @@ typedef struct dope_lattice {
                                    update_multipliers (the run loop)          */
     /* caller-owned device buffers */
     const int32_t *u;           /* n   unary                                  */
-    int32_t *a[2];              /* n   multipliers, ping-pong by state.parity */
-    int32_t *y2[3];             /* n   2*y; three rotating iterate buffers:
+    int16_t *a[2];              /* n   multipliers, ping-pong by state.parity */
+    uint8_t *y2[3];             /* n   2*y; three rotating iterate buffers:
                                    current, best, and the next output         */
     uint8_t *yhat;              /* n   block labels (global layout)           */
     uint8_t *resid;             /* K * resid_stride bytes: residual graphs    */
     uint32_t *dirty;            /* K   block needs a re-solve                 */
-    int64_t *part_energy;       /* K   per-block energy partials              */
+    int64_t *part_energy;       /* K   per-block pair-energy partials          */
+    int64_t *part_unary;        /* K   per-block change of sum u*y2           */
     int64_t *part_ressq;        /* K   per-block sum (yhat - y)^2             */
     int32_t *part_flags;        /* K   bit0: clamped                          */
     dope_run_state *state;      /* 1                                          */
@@ -172,7 +182,7 @@ int dope_ghost_update(const dope_lattice *L, int32_t which, const void *up_row,
                       const void *dn_row, void *stream);
 /* Sharded run loop: copy the first / last local row of the labels (which=0)
  * or of the current iterate y2 (which=1) into staging buffers (either may be
- * NULL) for the halo exchange. */
+ * NULL) for the halo exchange (labels: W bytes; y2: W bytes). */
 int dope_pack_rows(const dope_lattice *L, int32_t which, void *first_row, void *last_row,
                    void *stream);
 /* dope_finish_run in two halves for sharded runs: the local energy of the

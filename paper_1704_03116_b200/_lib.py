@@ -36,6 +36,9 @@ class RunState(C.Structure):
         ("solves", C.c_int64),
         ("sweeps", C.c_int64),
         ("energy_acc", C.c_int64),
+        ("unary2", C.c_int64),
+        ("a_bound", C.c_int32),
+        ("reserved_", C.c_int32),
     ]
 
 
@@ -60,6 +63,7 @@ class Lattice(C.Structure):
         ("resid", C.c_void_p),
         ("dirty", C.c_void_p),
         ("part_energy", C.c_void_p),
+        ("part_unary", C.c_void_p),
         ("part_ressq", C.c_void_p),
         ("part_flags", C.c_void_p),
         ("state", C.c_void_p),

@@ -279,12 +279,14 @@ class _DeviceState:
         if stride <= 0:
             raise NotImplementedError(f"no K1 kernel variant for block box of {low.dims}/{low.kpa}")
         i32, u8 = torch.int32, torch.uint8
-        self.a = [torch.zeros(n, dtype=i32, device=dev), torch.zeros(n, dtype=i32, device=dev)]
+        # multipliers fit int16 (|a| <= t + 1, max_iters is capped below 32000);
+        # 2y in {0, 1, 2} is one byte
+        self.a = [torch.zeros(n, dtype=torch.int16, device=dev) for _ in range(2)]
         # 2D: y2 and yhat carry one ghost row above and below (neighbour shards;
         # unused on a single GPU), the ABI points one row into the allocation
         g = low.dims[-1] if len(low.dims) == 2 else 0
         self.ghost = g
-        self.y2_full = [torch.ones(n + 2 * g, dtype=i32, device=dev) for _ in range(3)]
+        self.y2_full = [torch.ones(n + 2 * g, dtype=u8, device=dev) for _ in range(3)]
         self.y2 = [t[g:g + n] for t in self.y2_full]
         self.yhat_full = torch.zeros(n + 2 * g, dtype=u8, device=dev)
         self.yhat = self.yhat_full[g:g + n]
@@ -294,6 +296,7 @@ class _DeviceState:
         sstride = int(lb.dope_scratch_stride(C.byref(L)))
         self.scratch = torch.empty(max(K * sstride, 16), dtype=u8, device=dev)
         self.pe = torch.zeros(K, dtype=torch.int64, device=dev)
+        self.pu = torch.zeros(K, dtype=torch.int64, device=dev)
         self.pr = torch.zeros(K, dtype=torch.int64, device=dev)
         self.pf = torch.zeros(K, dtype=i32, device=dev)
         self.state = torch.zeros(C.sizeof(_lib.RunState), dtype=u8, device=dev)
@@ -311,6 +314,7 @@ class _DeviceState:
         L.dirty = self.dirty.data_ptr()
         L.scratch = self.scratch.data_ptr()
         L.part_energy = self.pe.data_ptr()
+        L.part_unary = self.pu.data_ptr()
         L.part_ressq = self.pr.data_ptr()
         L.part_flags = self.pf.data_ptr()
         L.state = self.state.data_ptr()
@@ -347,9 +351,19 @@ class _DeviceState:
 
     def raise_on_error(self):
         rs = self.run_state()
+        if rs.error == -1:
+            raise OverflowError("a multiplier left the int16 range (|a| > 32000); "
+                                "the run exceeded the iteration range the compressed state holds")
         if rs.error:
             raise BlockSolveError(rs.error - 1, "push-relabel round limit exceeded")
         return rs
+
+    def reset_unary(self):
+        """Recompute the running unary term sum u*y2 after a host write of y."""
+        import torch
+        off = _lib.RunState.unary2.offset
+        val = (self.problems.u.to(torch.int64) * self.y2_current().to(torch.int64)).sum()
+        self.state[off:off + 8].view(torch.int64).copy_(val.reshape(1))
 
 
 class AdmmState:
@@ -405,7 +419,8 @@ class AdmmState:
         if isinstance(self._dev, _FloatDeviceState):
             self._dev.y2[self._dev.run_state().ycur].copy_(torch.as_tensor(v))
         else:
-            self._dev.y2_current().copy_(torch.as_tensor((2 * v).astype(np.int32)))
+            self._dev.y2_current().copy_(torch.as_tensor((2 * v).astype(np.uint8)))
+            self._dev.reset_unary()
         self._dev.dirty.fill_(1)
 
     def _global_to_blocks(self, vec: np.ndarray, dtype) -> list:

@@ -11,6 +11,25 @@ namespace dope {
 
 constexpr uint16_t HINF = 0xFFFF;
 
+// storage of the integer path: y2 in {0,1,2} as bytes, multipliers as int16
+typedef uint8_t ystore_t;
+typedef int16_t astore_t;
+
+__device__ __forceinline__ int byte_at(uint32_t w, int i) { return (int)((w >> (8 * i)) & 0xFFu); }
+__device__ __forceinline__ void unpack_a4(uint2 v, int (&a)[4]) {
+    a[0] = (int)(int16_t)(v.x & 0xFFFFu);
+    a[1] = (int)(int16_t)(v.x >> 16);
+    a[2] = (int)(int16_t)(v.y & 0xFFFFu);
+    a[3] = (int)(int16_t)(v.y >> 16);
+}
+__device__ __forceinline__ uint2 pack_a4(int a0, int a1, int a2, int a3) {
+    return make_uint2((uint32_t)(uint16_t)a0 | ((uint32_t)(uint16_t)a1 << 16),
+                      (uint32_t)(uint16_t)a2 | ((uint32_t)(uint16_t)a3 << 16));
+}
+__device__ __forceinline__ uint32_t pack_y4(int y0, int y1, int y2, int y3) {
+    return (uint32_t)y0 | ((uint32_t)y1 << 8) | ((uint32_t)y2 << 16) | ((uint32_t)y3 << 24);
+}
+
 // ---------------------------------------------------------------------------
 // Geometry helpers (partition.py:62-77 with overlap 0)
 // ---------------------------------------------------------------------------

@@ -17,27 +17,29 @@
 //     CTA runs finalize_cta, which also clears them for the next iteration.
 
 struct TmaMaps {
-    CUtensorMap u, a[2], y[3], yr[3], yhat;
+    CUtensorMap a[2], y[3], yr[3], yhat;
 };
 
+// Stage layout of one TH x TW tile: multipliers (int16), previous iterate y2
+// (uint8, +1 row below), the 16-byte column right of the tile (its first byte is
+// the right-halo y2), labels with a 1-row / 16-byte halo.  u is not streamed:
+// the unary energy is kept incrementally (u gathered only where y changes).
 template <int TW, int NT_ = 512, int STAGES_ = 3>
 struct TmaCfg {
     static constexpr int TH = 4096 / TW;                 // tile rows (64 or 32)
     static constexpr int NT = NT_;
-    static constexpr int QPT = TH * TW / 4 / NT;         // quads per thread (2)
+    static constexpr int QPT = TH * TW / 4 / NT;         // quads per thread
     static constexpr int YHW = TW + 32;                  // label box width (bytes)
-    static constexpr int B_U = TW * TH * 4;
-    static constexpr int B_A = TW * TH * 4;
-    static constexpr int B_Y = TW * (TH + 1) * 4;
-    static constexpr int B_YR = 4 * TH * 4;
+    static constexpr int B_A = TW * TH * 2;
+    static constexpr int B_Y = TW * (TH + 1);
+    static constexpr int B_YR = 16 * TH;
     static constexpr int B_H = YHW * (TH + 2);
-    static constexpr int O_U = 0;
-    static constexpr int O_A = O_U + B_U;
-    static constexpr int O_Y = O_A + B_A;
+    static constexpr int O_A = 0;
+    static constexpr int O_Y = (O_A + B_A + 127) / 128 * 128;
     static constexpr int O_YR = (O_Y + B_Y + 127) / 128 * 128;
     static constexpr int O_H = (O_YR + B_YR + 127) / 128 * 128;
     static constexpr int STAGE = (O_H + B_H + 127) / 128 * 128;
-    static constexpr int TX = B_U + B_A + B_Y + B_YR + B_H;
+    static constexpr int TX = B_A + B_Y + B_YR + B_H;
     static constexpr int STAGES = STAGES_;
     static constexpr int SMEM = STAGES * STAGE + 128;
 };
@@ -84,7 +86,6 @@ __device__ __forceinline__ void tma_issue_tile(const Lat2 &L, const TmaMaps &M, 
     const int x0 = bx * TW;                       // uniform tiling: lo = index * width
     const int y0 = by * L.ay.base + tile * C::TH;
     mbar_expect_tx(bar, C::TX);
-    tma_load_2d(stage + C::O_U, &M.u, bar, x0, y0);
     tma_load_2d(stage + C::O_A, &M.a[p], bar, x0, y0);
     // y / labels maps start at the ghost row above the shard: +1 row
     tma_load_2d(stage + C::O_Y, &M.y[cur], bar, x0, y0 + 1);
@@ -92,9 +93,34 @@ __device__ __forceinline__ void tma_issue_tile(const Lat2 &L, const TmaMaps &M, 
     tma_load_2d(stage + C::O_H, &M.yhat, bar, x0 - 16, y0);
 }
 
-// packed old-iterate bits of a quad: y2 in {0,2} -> bit i = y_i
-__device__ __forceinline__ uint32_t pack_y2(const int4 v) {
-    return (uint32_t)((v.x | (v.y << 1) | (v.z << 2) | (v.w << 3)) >> 1);
+// 4 bytes (each 0 or 1) -> 4 bits
+__device__ __forceinline__ uint32_t bits_b01(uint32_t w) { return ((w * 0x01020408u) >> 24) & 0xFu; }
+// 4 bits -> 4 bytes (each 0 or 1)
+__device__ __forceinline__ uint32_t bytes_b01(uint32_t b) { return (b * 0x00204081u) & 0x01010101u; }
+
+// One quad (4 consecutive pixels of a row) of the consensus update.
+//   h4  : labels (bytes 0/1)         a2  : multipliers (int16 x 4)
+//   cnt : per-pixel count of cross-block neighbours (bytes)
+//   nb  : per-pixel sum of their labels (bytes)
+// y = clamp(h + a - q * sx) with sx = cnt*h - nb (the solve_global stencil,
+// admm.py:194-238); sx enters biased by 4 so the bytewise subtraction never
+// borrows.  Returns the new y as bits; writes the new multipliers.
+__device__ __forceinline__ uint32_t quad_update(uint32_t h4, uint2 a2, uint32_t cnt, uint32_t nb, int q,
+                                                int q4, uint2 &an, uint32_t &clp) {
+    const uint32_t sb = ((cnt & (h4 * 0xFFu)) | 0x04040404u) - nb;   // bytes: sx + 4
+    const int a0 = (int)__byte_perm(a2.x, 0, 0x9910), a1 = (int)a2.x >> 16;
+    const int a3_ = (int)a2.y >> 16, a2_ = (int)__byte_perm(a2.y, 0, 0x9910);
+    const int h0 = __byte_perm(h4, 0, 0x4440), h1 = __byte_perm(h4, 0, 0x4441);
+    const int h2 = __byte_perm(h4, 0, 0x4442), h3 = __byte_perm(h4, 0, 0x4443);
+    const int p0 = a0 + h0 + q4 - q * (int)__byte_perm(sb, 0, 0x4440);
+    const int p1 = a1 + h1 + q4 - q * (int)__byte_perm(sb, 0, 0x4441);
+    const int p2 = a2_ + h2 + q4 - q * (int)__byte_perm(sb, 0, 0x4442);
+    const int p3 = a3_ + h3 + q4 - q * (int)__byte_perm(sb, 0, 0x4443);
+    clp |= (uint32_t)(p0 | p1) | (uint32_t)(p2 | p3);   // all in {0,1} <=> OR <= 1
+    const int y0 = p0 > 0, y1 = p1 > 0, y2 = p2 > 0, y3 = p3 > 0;
+    an.x = __byte_perm((uint32_t)(a0 + h0 - y0), (uint32_t)(a1 + h1 - y1), 0x5410);
+    an.y = __byte_perm((uint32_t)(a2_ + h2 - y2), (uint32_t)(a3_ + h3 - y3), 0x5410);
+    return (uint32_t)(y0 | (y1 << 1) | (y2 << 2) | (y3 << 3));
 }
 
 template <int TW, int NT_, int STAGES_>
@@ -103,7 +129,8 @@ __global__ void __launch_bounds__(NT_, 1) k_consensus_tma(Lat2 L, const __grid_c
     using C = TmaCfg<TW, NT_, STAGES_>;
     constexpr int TH = C::TH, NT = C::NT, QPT = C::QPT, QR = TW / 4, LQ = (TW == 64) ? 4 : 5;
     extern __shared__ __align__(128) uint8_t smem_t[];
-    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_t) + 127) & ~(uintptr_t)127);
+    // keep the shared address space visible to the compiler (LDS, not generic LD)
+    uint8_t *base = smem_t + ((128u - (smem_u32(smem_t) & 127u)) & 127u);
     __shared__ __align__(8) uint64_t full[C::STAGES];
     __shared__ int last;
 
@@ -112,22 +139,21 @@ __global__ void __launch_bounds__(NT_, 1) k_consensus_tma(Lat2 L, const __grid_c
     const int tid = threadIdx.x, lane = tid & 31;
     const int cur = st->ycur, best = st->ybest, out = other_buffer(cur, best);
     const int p = st->parity;
-    int32_t *__restrict__ y_out = L.y2[out];
-    int32_t *__restrict__ a_out = p ? L.a0 : L.a1;
+    ystore_t *__restrict__ y_out = L.y2[out];
+    astore_t *__restrict__ a_out = p ? L.a0 : L.a1;
     const bool want_e = st->iteration >= 1;
     const int32_t W = L.W, H = L.ay.dim, q = L.q, BH = L.ay.base, KX = L.ax.k;
+    const int q4 = 4 * q;
     const int tpb = BH / TH;                          // tiles per block
     const int G0 = gridDim.x;
     const int nblk = (L.K - (int)blockIdx.x + G0 - 1) / G0;
     const int ntiles = nblk * tpb;
-    // block coordinates of this CTA's kb-th block (division-free: magic = ceil(2^32 / KX))
     auto coords = [&](int kb, int &by, int &bx) {
         const int k = blockIdx.x + kb * G0;
         by = (int)__umulhi((uint32_t)k, kx_magic);
         bx = k - by * KX;
     };
 
-    // issue cursor (thread 0 only)
     int ikb = 0, itile = 0;
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) mbar_init(&full[s], 1);
@@ -141,18 +167,12 @@ __global__ void __launch_bounds__(NT_, 1) k_consensus_tma(Lat2 L, const __grid_c
     }
     __syncthreads();
 
-    // per-thread quad positions inside a tile (fixed for the whole launch)
-    int off_[QPT], goff_[QPT], rr_[QPT];
-    bool cl_[QPT], cr_[QPT];
+    int rr_[QPT], c0_[QPT];
 #pragma unroll
     for (int j = 0; j < QPT; ++j) {
         const int t = tid + j * NT;
-        const int rr = t >> LQ, c0 = (t & (QR - 1)) << 2;
-        rr_[j] = rr;
-        off_[j] = rr * TW + c0;           // smem offset in the tile
-        goff_[j] = rr * W + c0;           // global offset from the tile origin
-        cl_[j] = c0 == 0;
-        cr_[j] = c0 + 4 == TW;
+        rr_[j] = t >> LQ;
+        c0_[j] = (t & (QR - 1)) << 2;
     }
 
     int s = 0;
@@ -164,85 +184,67 @@ __global__ void __launch_bounds__(NT_, 1) k_consensus_tma(Lat2 L, const __grid_c
         const int lo_r = by * BH, lo_c = bx * TW;
         const bool has_up = lo_r > 0 || L.gup, has_dn = lo_r + BH < H || L.gdn, has_lf = lo_c > 0,
                    has_rt = lo_c + TW < W;
-        int64_t e_acc = 0;
+        const bool last_row_pairs = lo_r + BH < H || L.gdn;   // pairs below the block's last row
+        int64_t du = 0;
         int ss = 0, quad_acc = 0;
-        bool clamped = false, chg_self = false, chgL = false, chgR = false, chgU = false, chgD = false;
+        uint32_t fl = 0, clp = 0;   // fl: bit1 self, bit2 left, bit3 right, bit4 up, bit5 down
         for (int tile = 0; tile < tpb; ++tile) {
-            uint8_t *sb = base + s * C::STAGE;
-            const int32_t *su = reinterpret_cast<const int32_t *>(sb + C::O_U);
-            const int32_t *sa = reinterpret_cast<const int32_t *>(sb + C::O_A);
-            const int32_t *sy = reinterpret_cast<const int32_t *>(sb + C::O_Y);
-            const int32_t *syr = reinterpret_cast<const int32_t *>(sb + C::O_YR);
+            const uint8_t *sb = base + s * C::STAGE;
+            const astore_t *sa = reinterpret_cast<const astore_t *>(sb + C::O_A);
+            const uint8_t *sy = sb + C::O_Y;
+            const uint8_t *syr = sb + C::O_YR;
             const uint8_t *sh = sb + C::O_H + C::YHW + 16;      // label of tile pixel (0,0)
             const int r0 = tile * TH;
-            int32_t *a_t = a_out + (int64_t)(lo_r + r0) * W + lo_c;
-            int32_t *y_t = y_out + (int64_t)(lo_r + r0) * W + lo_c;
+            const int64_t gt = (int64_t)(lo_r + r0) * W + lo_c;   // global index of tile (0,0)
             mbar_wait(&full[s], phase);
 #pragma unroll
             for (int j = 0; j < QPT; ++j) {
-                const int rr = rr_[j], off = off_[j];
+                const int rr = rr_[j], c0 = c0_[j];
                 const int r = r0 + rr;                             // row within block
-                const int4 av = *reinterpret_cast<const int4 *>(sa + off);
-                const int4 yo = *reinterpret_cast<const int4 *>(sy + off);
-                const int4 uu = *reinterpret_cast<const int4 *>(su + off);
-                const uint8_t *hrow = sh + rr * C::YHW + (off - rr * TW);
-                const uint32_t yh4 = *reinterpret_cast<const uint32_t *>(hrow);
-                // old iterate (y2 in {0,2} from iteration 2 on) as 4 bits
-                const uint32_t ob = pack_y2(yo);
-                const uint32_t nxt = __shfl_down_sync(FULLMASK, ob, 1);
+                const uint2 av = *reinterpret_cast<const uint2 *>(sa + rr * TW + c0);
+                const uint32_t yo = *reinterpret_cast<const uint32_t *>(sy + rr * TW + c0);
+                const uint8_t *hrow = sh + rr * C::YHW + c0;
+                const uint32_t h4 = *reinterpret_cast<const uint32_t *>(hrow);
+                const bool cr = c0 + 4 == TW;
                 if (want_e) {
-                    const int4 yb = *reinterpret_cast<const int4 *>(sy + off + TW);
-                    uint32_t rb = nxt;
-                    if (cr_[j]) rb = has_rt ? (uint32_t)(syr[rr * 4] >> 1) : (ob >> 3);
-                    const uint32_t hz = (ob ^ (ob >> 1)) & 0x7u;                 // pairs inside the quad
-                    const uint32_t vt = (lo_r + r + 1 < H || L.gdn) ? (ob ^ pack_y2(yb)) : 0u;
-                    quad_acc += __popc(hz | (((ob >> 3) ^ rb) & 1u) << 3) + __popc(vt);
-                    e_acc += uu.x * (yo.x >> 1) + uu.y * (yo.y >> 1) + uu.z * (yo.z >> 1) +
-                             uu.w * (yo.w >> 1);
+                    // E(y_{t-1}) pair terms: bytes are 0/2, so each differing
+                    // pair is exactly one set bit of the XOR
+                    const uint32_t nxt = __shfl_down_sync(FULLMASK, yo, 1);
+                    uint32_t rw = nxt;
+                    if (cr) rw = has_rt ? (uint32_t)syr[rr * 16] : (yo >> 24);
+                    const uint32_t yb = (r + 1 < BH || last_row_pairs)
+                                            ? *reinterpret_cast<const uint32_t *>(sy + (rr + 1) * TW + c0)
+                                            : yo;
+                    quad_acc += __popc(yo ^ __funnelshift_r(yo, rw, 8)) + __popc(yo ^ yb);
                 }
-                const int h0 = yh4 & 0xFF, h1 = (yh4 >> 8) & 0xFF, h2 = (yh4 >> 16) & 0xFF, h3 = yh4 >> 24;
-                // cross-block sums (non-zero only on the block border)
-                const bool lft = cl_[j] && has_lf, rgt = cr_[j] && has_rt;
-                int sx0 = lft ? h0 - (int)hrow[-1] : 0;
-                int sx3 = rgt ? h3 - (int)hrow[4] : 0;
-                int sx1 = 0, sx2 = 0;
+                // cross-block neighbours of this quad
+                const bool lft = (c0 == 0) && has_lf, rgt = cr && has_rt;
                 const bool top = (r == 0) && has_up, bot = (r == BH - 1) && has_dn;
-                if (top | bot) {
-                    const uint32_t o4 = *reinterpret_cast<const uint32_t *>(hrow + (top ? -C::YHW : C::YHW));
-                    sx0 += h0 - (int)(o4 & 0xFF);
-                    sx1 += h1 - (int)((o4 >> 8) & 0xFF);
-                    sx2 += h2 - (int)((o4 >> 16) & 0xFF);
-                    sx3 += h3 - (int)(o4 >> 24);
-                    if (top && bot) {   // single-row blocks: both neighbours
-                        const uint32_t d4 = *reinterpret_cast<const uint32_t *>(hrow + C::YHW);
-                        sx0 += h0 - (int)(d4 & 0xFF);
-                        sx1 += h1 - (int)((d4 >> 8) & 0xFF);
-                        sx2 += h2 - (int)((d4 >> 16) & 0xFF);
-                        sx3 += h3 - (int)(d4 >> 24);
-                    }
-                }
-                const int p0 = h0 + av.x - q * sx0, p1 = h1 + av.y - q * sx1;
-                const int p2 = h2 + av.z - q * sx2, p3 = h3 + av.w - q * sx3;
-                clamped |= (unsigned)(p0 | p1 | p2 | p3) > 1u;
-                const int y0 = min(max(p0, 0), 1), y1 = min(max(p1, 0), 1);
-                const int y2 = min(max(p2, 0), 1), y3 = min(max(p3, 0), 1);
-                const uint32_t yn = (uint32_t)(y0 | (y1 << 1) | (y2 << 2) | (y3 << 3));
-                const uint32_t hb = ((yh4 * 0x01020408u) >> 24) & 0xFu;   // 0/1 bytes -> bits 0..3
+                uint32_t cnt = 0, nb = 0;
+                if (top) { cnt += 0x01010101u; nb += *reinterpret_cast<const uint32_t *>(hrow - C::YHW); }
+                if (bot) { cnt += 0x01010101u; nb += *reinterpret_cast<const uint32_t *>(hrow + C::YHW); }
+                if (lft) { cnt += 1u; nb += hrow[-1]; }
+                if (rgt) { cnt += 1u << 24; nb += (uint32_t)hrow[4] << 24; }
+                uint2 an;
+                const uint32_t yn = quad_update(h4, av, cnt, nb, q, q4, an, clp);
+                const uint32_t hb = bits_b01(h4);
                 ss += __popc(hb ^ yn);
-                // y changed iff 2*y_new != old y2 (old y2 = 1, i.e. 1/2, on the first pass)
-                const uint32_t o2 = (uint32_t)(yo.x | (yo.y << 2) | (yo.z << 4) | (yo.w << 6));
-                const uint32_t n2 = (uint32_t)((y0 << 1) | (y1 << 3) | (y2 << 5) | (y3 << 7));
-                const bool ychg = o2 != n2;
-                chg_self |= ychg | (hb != yn);
-                const int go = goff_[j];
-                __stcs(reinterpret_cast<int4 *>(a_t + go),
-                       make_int4(av.x + h0 - y0, av.y + h1 - y1, av.z + h2 - y2, av.w + h3 - y3));
-                __stcg(reinterpret_cast<int4 *>(y_t + go), make_int4(2 * y0, 2 * y1, 2 * y2, 2 * y3));
-                if (ychg) {
-                    chgU |= top;
-                    chgD |= bot;
-                    chgL |= lft && ((o2 & 3u) != (n2 & 3u));
-                    chgR |= rgt && ((o2 >> 6) != (n2 >> 6));
+                const uint32_t yw = bytes_b01(yn) << 1;            // y2 bytes 0/2
+                const uint32_t chg = yw ^ yo;
+                fl |= (chg | (hb ^ yn)) ? 2u : 0u;
+                const int64_t G = gt + (int64_t)rr * W + c0;
+                __stcs(reinterpret_cast<uint2 *>(a_out + G), an);
+                __stcg(reinterpret_cast<unsigned int *>(y_out + G), yw);
+                if (chg) {
+                    // running unary term u * (y2_new - y2_old) where y moved
+                    const int4 uv = __ldg(reinterpret_cast<const int4 *>(L.u + G));
+                    du += (int64_t)uv.x * ((int)(yw & 0xFFu) - (int)(yo & 0xFFu)) +
+                          (int64_t)uv.y * ((int)((yw >> 8) & 0xFFu) - (int)((yo >> 8) & 0xFFu)) +
+                          (int64_t)uv.z * ((int)((yw >> 16) & 0xFFu) - (int)((yo >> 16) & 0xFFu)) +
+                          (int64_t)uv.w * ((int)(yw >> 24) - (int)(yo >> 24));
+                    const uint32_t em = (lft ? 4u : 0u) | (rgt ? 8u : 0u) | (top ? 16u : 0u) | (bot ? 32u : 0u);
+                    const uint32_t mk = 0x30u | ((chg & 0xFFu) ? 4u : 0u) | ((chg >> 24) ? 8u : 0u);
+                    fl |= em & mk;
                 }
             }
             // every warp is done with stage s: refill it with the tile STAGES ahead
@@ -256,21 +258,23 @@ __global__ void __launch_bounds__(NT_, 1) k_consensus_tma(Lat2 L, const __grid_c
             }
             if (++s == C::STAGES) { s = 0; phase ^= 1u; }
         }
-        // publish this block's partials: one atomic per warp
-        const int64_t e = warp_sum(e_acc + (int64_t)L.lamw * quad_acc);
-        const int sq = warp_sum(ss);
-        const unsigned fl = __ballot_sync(FULLMASK, clamped), f0 = __ballot_sync(FULLMASK, chg_self),
-                       f1 = __ballot_sync(FULLMASK, chgL), f2 = __ballot_sync(FULLMASK, chgR),
-                       f3 = __ballot_sync(FULLMASK, chgU), f4 = __ballot_sync(FULLMASK, chgD);
+        // publish this block's partials: one atomic per warp (redux.sync)
+        const int e = (int)__reduce_add_sync(FULLMASK, (unsigned)quad_acc);
+        const int sq = (int)__reduce_add_sync(FULLMASK, (unsigned)ss);
+        const uint32_t f = __reduce_or_sync(FULLMASK, fl | (clp > 1u ? 1u : 0u));
+        int64_t u2 = 0;
+        if (__any_sync(FULLMASK, du != 0)) u2 = warp_sum(du);
         if (lane == 0) {
-            if (e) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pe[k]), (unsigned long long)e);
+            if (e) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pe[k]),
+                             (unsigned long long)((int64_t)L.lamw * e));
+            if (u2) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pu[k]), (unsigned long long)u2);
             if (sq) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pr[k]), (unsigned long long)sq);
-            if (fl) atomicOr(&L.pf[k], 1);
-            if (f0) L.dirty[k] = 1u;
-            if (f1) L.dirty[k - 1] = 1u;
-            if (f2) L.dirty[k + 1] = 1u;
-            if (f3 && k - KX >= 0) L.dirty[k - KX] = 1u;
-            if (f4 && k + KX < L.K) L.dirty[k + KX] = 1u;
+            if (f & 1u) atomicOr(&L.pf[k], 1);
+            if (f & 2u) L.dirty[k] = 1u;
+            if (f & 4u) L.dirty[k - 1] = 1u;
+            if (f & 8u) L.dirty[k + 1] = 1u;
+            if ((f & 16u) && k - KX >= 0) L.dirty[k - KX] = 1u;
+            if ((f & 32u) && k + KX < L.K) L.dirty[k + KX] = 1u;
         }
     }
     __syncthreads();
@@ -282,14 +286,7 @@ __global__ void __launch_bounds__(NT_, 1) k_consensus_tma(Lat2 L, const __grid_c
     __syncthreads();
     if (last) {
         __threadfence();
-        finalize_cta(L, cur, best, out);
-        __syncthreads();
-        // partials were accumulated: clear them for the next iteration
-        for (int k = tid; k < L.K; k += blockDim.x) {
-            L.pe[k] = 0;
-            L.pr[k] = 0;
-            L.pf[k] = 0;
-        }
+        finalize_cta(L, cur, best, out);   // partials are cleared by the next K1
         if (tid == 0) st->done_ctas = 0;
     }
 }

@@ -77,12 +77,12 @@ struct Comm {
 
 static int nc(ncclResult_t r) { return r == ncclSuccess ? DOPE_OK : DOPE_E_CUDA; }
 
-// halo buffer layout (caller-owned, 4 rows of W * 4 bytes):
+// halo buffer layout (caller-owned, 4 slots of W * 4 bytes; each row uses W bytes):
 //   [0] send first row, [1] send last row, [2] recv from above, [3] recv from below
 static int exchange(const dope_lattice *L, const Comm &C, int which, cudaStream_t s) {
     Nccl &N = nccl();
     const size_t W = (size_t)L->dims[1];
-    const size_t bytes = which == 0 ? W : 4 * W;
+    const size_t bytes = W;   // labels and y2 are both one byte per pixel
     uint8_t *h = static_cast<uint8_t *>(L->halo);
     uint8_t *first = h, *last = h + 4 * W, *up = h + 8 * W, *dn = h + 12 * W;
     int rc = dope_pack_rows(L, which, first, last, s);

@@ -54,11 +54,11 @@ struct Lat2 {
     int32_t warm, skip_clean, fuse;
     double eps;
     const int32_t *u;
-    int32_t *a0, *a1;
-    int32_t *y2[3];        // rotating iterates: st.ycur (current), st.ybest (best)
+    astore_t *a0, *a1;
+    ystore_t *y2[3];       // rotating iterates: st.ycur (current), st.ybest (best)
     uint8_t *yhat, *resid;
     uint32_t *dirty;
-    int64_t *pe, *pr;
+    int64_t *pe, *pr, *pu;
     int32_t *pf;
     dope_run_state *st;
     int64_t *tr_e;
@@ -127,6 +127,12 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
         L.timeline[8 * k + 5] = (int64_t)t_begin;
     }
     if (L.st->stop) return;
+    if (tid == 0) {   // this iteration's consensus partials (the TMA pass accumulates)
+        L.pe[k] = 0;
+        L.pu[k] = 0;
+        L.pr[k] = 0;
+        L.pf[k] = 0;
+    }
     if (L.skip_clean) {
         if (L.dirty[k] == 0) return;
     }
@@ -139,8 +145,8 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
     L.ax.range(bx, lo_c, wc);
     const int32_t Wg = L.W;
     const int32_t cap = L.cap;
-    const int32_t *__restrict__ a_cur = L.st->parity ? L.a1 : L.a0;
-    const int32_t *__restrict__ y_cur = L.y2[L.st->ycur];
+    const astore_t *__restrict__ a_cur = L.st->parity ? L.a1 : L.a0;
+    const ystore_t *__restrict__ y_cur = L.y2[L.st->ycur];
     uint8_t *gres = L.resid + (size_t)k * 4 * M;
 
     // ---- prologue: 2*linear (blockform.py:271-272 on the q==1 stencil) ----
@@ -158,10 +164,12 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
     const bool has_up = lo_r > 0 || L.gup, has_dn = lo_r + hr < L.ay.dim || L.gdn, has_lf = lo_c > 0,
                has_rt = lo_c + wc < Wg;
     if (L.vec4) {
-        // quads of 4 consecutive box nodes; int4 loads, two quads in flight per thread
+        // quads of 4 consecutive box nodes: int4 of u, 8 B of a, 4 B of y2
         constexpr int NQ = M / 4;
         for (int q0 = tid; q0 < NQ; q0 += 2 * NT) {
-            int4 uq[2], aq[2], yq[2], yu[2], yd[2];
+            int4 uq[2];
+            uint2 aq[2];
+            uint32_t yq[2], yu[2], yd[2];
             int yl[2], yrr[2];
             bool ok[2];
 #pragma unroll
@@ -169,15 +177,17 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
                 const int qd = q0 + j * NT;
                 const int v0 = 4 * qd, r = v0 / BW, c0 = v0 % BW;
                 ok[j] = qd < NQ && r < hr && c0 < wc;
-                uq[j] = aq[j] = yq[j] = yu[j] = yd[j] = make_int4(0, 0, 0, 0);
+                uq[j] = make_int4(0, 0, 0, 0);
+                aq[j] = make_uint2(0, 0);
+                yq[j] = yu[j] = yd[j] = 0;
                 yl[j] = yrr[j] = 0;
                 if (ok[j]) {
                     const int64_t G = (int64_t)(lo_r + r) * Wg + lo_c + c0;
                     uq[j] = __ldg(reinterpret_cast<const int4 *>(L.u + G));
-                    aq[j] = *reinterpret_cast<const int4 *>(a_cur + G);
-                    yq[j] = *reinterpret_cast<const int4 *>(y_cur + G);
-                    if (r == 0 && has_up) yu[j] = *reinterpret_cast<const int4 *>(y_cur + G - Wg);
-                    if (r == hr - 1 && has_dn) yd[j] = *reinterpret_cast<const int4 *>(y_cur + G + Wg);
+                    aq[j] = *reinterpret_cast<const uint2 *>(a_cur + G);
+                    yq[j] = *reinterpret_cast<const uint32_t *>(y_cur + G);
+                    if (r == 0 && has_up) yu[j] = *reinterpret_cast<const uint32_t *>(y_cur + G - Wg);
+                    if (r == hr - 1 && has_dn) yd[j] = *reinterpret_cast<const uint32_t *>(y_cur + G + Wg);
                     if (c0 == 0 && has_lf) yl[j] = y_cur[G - 1];
                     if (c0 + 4 == wc && has_rt) yrr[j] = y_cur[G + 4];
                 }
@@ -190,20 +200,19 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
                 int4 out = make_int4(0, 0, 0, 0);
                 if (ok[j]) {
                     const bool top = r == 0 && has_up, bot = r == hr - 1 && has_dn;
-                    const int yv[4] = {yq[j].x, yq[j].y, yq[j].z, yq[j].w};
                     const int uv[4] = {uq[j].x, uq[j].y, uq[j].z, uq[j].w};
-                    const int av[4] = {aq[j].x, aq[j].y, aq[j].z, aq[j].w};
-                    const int uu4[4] = {yu[j].x, yu[j].y, yu[j].z, yu[j].w};
-                    const int dd4[4] = {yd[j].x, yd[j].y, yd[j].z, yd[j].w};
+                    int av[4];
+                    unpack_a4(aq[j], av);
                     int lin[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
+                        const int yv = byte_at(yq[j], e);
                         int sx = 0;
-                        if (top) sx += yv[e] - uu4[e];
-                        if (bot) sx += yv[e] - dd4[e];
-                        if (e == 0 && c0 == 0 && has_lf) sx += yv[e] - yl[j];
-                        if (e == 3 && c0 + 4 == wc && has_rt) sx += yv[e] - yrr[j];
-                        lin[e] = 2 * uv[e] + L.lamw * sx + L.mu * (2 * av[e] - yv[e]) + L.mu;
+                        if (top) sx += yv - byte_at(yu[j], e);
+                        if (bot) sx += yv - byte_at(yd[j], e);
+                        if (e == 0 && c0 == 0 && has_lf) sx += yv - yl[j];
+                        if (e == 3 && c0 + 4 == wc && has_rt) sx += yv - yrr[j];
+                        lin[e] = 2 * uv[e] + L.lamw * sx + L.mu * (2 * av[e] - yv) + L.mu;
                     }
                     out = make_int4(lin[0], lin[1], lin[2], lin[3]);
                 }
@@ -219,11 +228,11 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
                 const int64_t G = (int64_t)(lo_r + r) * Wg + lo_c + c;
                 const int32_t yg = y_cur[G];
                 int32_t sx = 0;
-                if (c == 0 && has_lf) sx += yg - y_cur[G - 1];
-                if (c == wc - 1 && has_rt) sx += yg - y_cur[G + 1];
-                if (r == 0 && has_up) sx += yg - y_cur[G - Wg];
-                if (r == hr - 1 && has_dn) sx += yg - y_cur[G + Wg];
-                lin2 = 2 * L.u[G] + L.lamw * sx + L.mu * (2 * a_cur[G] - yg) + L.mu;
+                if (c == 0 && has_lf) sx += yg - (int32_t)y_cur[G - 1];
+                if (c == wc - 1 && has_rt) sx += yg - (int32_t)y_cur[G + 1];
+                if (r == 0 && has_up) sx += yg - (int32_t)y_cur[G - Wg];
+                if (r == hr - 1 && has_dn) sx += yg - (int32_t)y_cur[G + Wg];
+                lin2 = 2 * L.u[G] + L.lamw * sx + L.mu * (2 * (int32_t)a_cur[G] - yg) + L.mu;
             }
             g[v] = lin2;
         }
@@ -427,6 +436,7 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
         L.dirty[i] = 1u;
         L.pe[i] = 0;
         L.pr[i] = 0;
+        L.pu[i] = 0;
         L.pf[i] = 0;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -437,16 +447,29 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
     }
 }
 
+// sum u * y2 of the initial iterate (y2 = 1): the running unary term starts at sum u
+__global__ void k_init_unary(Lat2 L, int64_t n) {
+    int64_t acc = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) acc += L.u[i];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0)
+        atomicAdd(reinterpret_cast<unsigned long long *>(&L.st->unary2), (unsigned long long)acc);
+}
+
 // ---------------------------------------------------------------------------
 // K2: consensus update (2D, 4-connected), one CTA per block
 // ---------------------------------------------------------------------------
 //
 // Iteration t's K2 reads y_{t-1} (buffer st.ycur), writes y_t into the one
 // buffer that is neither ycur nor st.ybest, and -- because y_{t-1} and all of
-// its neighbours are already in HBM -- also produces the per-block partials of
-// E(y_{t-1}) (energy.py:187-194) for the previous iteration's trace entry.
-// The best iterate is therefore tracked by buffer index: no copies
-// (admm.py:300-303).  The last iterate's energy is taken by dope_finish_run.
+// its neighbours are already in HBM -- produces the per-block pair-energy
+// partials of E(y_{t-1}) (energy.py:187-194) for the previous iteration's
+// trace entry.  The unary part u.y is kept incrementally in st.unary2
+// (= sum u*y2): each pass adds u*(y2_t - y2_{t-1}) where y moved, so u is only
+// read where the labeling changed.  The best iterate is tracked by buffer
+// index: no copies (admm.py:300-303).  The last iterate's energy is taken by
+// dope_finish_run.
 
 __device__ __forceinline__ int other_buffer(int cur, int best) {
     // the y buffer that is neither the current nor the best iterate
@@ -454,10 +477,6 @@ __device__ __forceinline__ int other_buffer(int cur, int best) {
     return 3 - cur - best;
 }
 
-// Reduce the per-block partials into the trace, track the best iterate and
-// test the stop rule (admm.py:289-307); rotate the y buffers.  Executed by the
-// whole last CTA of a consensus launch.  Blocks are assigned to threads by
-// index and combined in a fixed tree, so float sums are deterministic.
 // Apply one iteration's global aggregates to the run state (admm.py:289-307):
 // trace entry, best iterate by buffer index (strict <), parity, stop rule,
 // y-buffer rotation.  E2 is the energy of the previous iterate (y_{t}),
@@ -487,35 +506,31 @@ __device__ void apply_iteration(const Lat2 &L, int64_t E2, double R2, int64_t M2
         st->converged = 1;
         st->stop = 1;
     }
+    if (!st->error && st->a_bound >= 32000) st->error = -1;   // int16 multipliers
     if (st->error) st->stop = 1;
     st->ybest = bidx;
     st->ycur = out;
 }
 
-// Reduce the per-block partials (run-loop mode) and apply them -- or, when
+// Reduce the per-block partials and apply them (run-loop mode) -- or, when
 // sharded, publish this shard's aggregates for the cross-rank all-reduce and
-// leave the decision to dope_decide.  Executed by the whole last CTA of a
-// consensus launch; blocks are assigned to threads by index and combined in a
-// fixed tree, so float sums are deterministic.
+// leave the decision to dope_decide.  Always advances the running unary term.
+// Executed by the whole last CTA of a consensus launch; blocks are assigned to
+// threads by index and combined in a fixed tree, so float sums are
+// deterministic.
 __device__ void finalize_cta(const Lat2 &L, int cur, int best_idx, int out) {
-    __shared__ int64_t sE[32];
+    __shared__ int64_t sE[32], sU[32];
     __shared__ double sR[32];
     __shared__ int64_t sM[32];
     __shared__ int sF[32];
     dope_run_state *st = L.st;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (!L.fuse) {                       // step-level API: rotate only
-        if (tid == 0) {
-            st->ybest = best_idx;
-            st->ycur = out;
-        }
-        return;
-    }
-    int64_t E = 0, mx = -1;
+    int64_t E = 0, U = 0, mx = -1;
     double rs = 0.0;
     int F = 0;
     for (int k = tid; k < L.K; k += blockDim.x) {
         E += __ldcg(&L.pe[k]);
+        U += __ldcg(&L.pu[k]);
         const int64_t sq = __ldcg(&L.pr[k]);
         const double r = sqrt((double)sq);
         rs += r * r;
@@ -523,26 +538,34 @@ __device__ void finalize_cta(const Lat2 &L, int cur, int best_idx, int out) {
         F |= __ldcg(&L.pf[k]);
     }
     E = warp_sum(E);
+    U = warp_sum(U);
     for (int o = 16; o > 0; o >>= 1) {
         rs += __shfl_xor_sync(FULLMASK, rs, o);
         const int64_t t = __shfl_xor_sync(FULLMASK, mx, o);
         mx = t > mx ? t : mx;
     }
     F = __any_sync(FULLMASK, F);
-    if (lane == 0) { sE[warp] = E; sR[warp] = rs; sM[warp] = mx; sF[warp] = F; }
+    if (lane == 0) { sE[warp] = E; sU[warp] = U; sR[warp] = rs; sM[warp] = mx; sF[warp] = F; }
     __syncthreads();
     if (tid == 0) {
-        int64_t E2 = 0, M2 = -1;
+        int64_t E2 = 0, U2 = 0, M2 = -1;
         double R2 = 0.0;
         int F2 = 0;
         const int nw = blockDim.x / 32;
         for (int w = 0; w < nw; ++w) {
             E2 += sE[w];
+            U2 += sU[w];
             R2 += sR[w];
             M2 = sM[w] > M2 ? sM[w] : M2;
             F2 |= sF[w];
         }
-        if (L.sharded) {
+        E2 += st->unary2 / 2;            // E(y_{t-1}) = u.y_{t-1} + pair terms
+        st->unary2 += U2;                // now sum u*y2_t
+        if (L.fuse) st->a_bound += 1;    // this pass updated the multipliers
+        if (!L.fuse) {                   // step-level API: rotate only
+            st->ybest = best_idx;
+            st->ycur = out;
+        } else if (L.sharded) {
             L.agg[0] = E2;
             L.agg[1] = __double_as_longlong(R2);
             L.agg[2] = M2;
@@ -563,65 +586,57 @@ __global__ void k_decide(Lat2 L) {
 }
 
 // Sharded mode: copy this shard's first and last local rows (labels or the
-// current iterate) into caller staging buffers for the halo exchange.
+// current iterate, both bytes) into caller staging buffers for the halo exchange.
 __global__ void k_pack_rows(Lat2 L, int which, void *first, void *last) {
     const int32_t W = L.W;
     const int64_t lastoff = (int64_t)(L.ay.dim - 1) * W;
+    const uint8_t *src = which == 0 ? L.yhat : L.y2[L.st->ycur];
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < W; c += gridDim.x * blockDim.x) {
-        if (which == 0) {
-            if (first) static_cast<uint8_t *>(first)[c] = L.yhat[c];
-            if (last) static_cast<uint8_t *>(last)[c] = L.yhat[lastoff + c];
-        } else {
-            const int32_t *y = L.y2[L.st->ycur];
-            if (first) static_cast<int32_t *>(first)[c] = y[c];
-            if (last) static_cast<int32_t *>(last)[c] = y[lastoff + c];
-        }
+        if (first) static_cast<uint8_t *>(first)[c] = src[c];
+        if (last) static_cast<uint8_t *>(last)[c] = src[lastoff + c];
     }
 }
 
 // Sharded mode: install the neighbour shards' boundary rows into the ghost
-// rows.  which == 0: labels (uint8); which == 1: current iterate y2 (int32),
-// marking the local boundary block row dirty where the neighbour's y changed
-// (it enters this shard's block objectives, blockform.py:271).
+// rows.  which == 0: labels; which == 1: current iterate y2, marking the local
+// boundary block row dirty where the neighbour's y changed (it enters this
+// shard's block objectives, blockform.py:271).
 __global__ void k_ghost_update(Lat2 L, int which, const void *up_new, const void *dn_new) {
     const int32_t W = L.W;
     const int64_t below = (int64_t)L.ay.dim * W;
+    const uint8_t *up = static_cast<const uint8_t *>(up_new), *dn = static_cast<const uint8_t *>(dn_new);
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < W; c += gridDim.x * blockDim.x) {
         if (which == 0) {
-            if (L.gup && up_new) L.yhat[-W + c] = static_cast<const uint8_t *>(up_new)[c];
-            if (L.gdn && dn_new) L.yhat[below + c] = static_cast<const uint8_t *>(dn_new)[c];
+            if (L.gup && up) L.yhat[-W + c] = up[c];
+            if (L.gdn && dn) L.yhat[below + c] = dn[c];
         } else {
-            int32_t *y = L.y2[L.st->ycur];
+            uint8_t *y = L.y2[L.st->ycur];
             const int bx = L.ax.owner(c);
-            if (L.gup && up_new) {
-                const int32_t v = static_cast<const int32_t *>(up_new)[c];
-                if (y[-W + c] != v) {
-                    L.dirty[bx] = 1u;
-                    y[-W + c] = v;
-                }
+            if (L.gup && up && y[-W + c] != up[c]) {
+                L.dirty[bx] = 1u;
+                y[-W + c] = up[c];
             }
-            if (L.gdn && dn_new) {
-                const int32_t v = static_cast<const int32_t *>(dn_new)[c];
-                if (y[below + c] != v) {
-                    L.dirty[(L.ay.k - 1) * L.ax.k + bx] = 1u;
-                    y[below + c] = v;
-                }
+            if (L.gdn && dn && y[below + c] != dn[c]) {
+                L.dirty[(L.ay.k - 1) * L.ax.k + bx] = 1u;
+                y[below + c] = dn[c];
             }
         }
     }
 }
 
-// Per-CTA epilogue shared by the consensus kernels: reduce the thread
-// partials, publish the block's partials and dirty marks; the last CTA to
-// arrive runs finalize_cta.
-__device__ __forceinline__ void consensus_epilogue(const Lat2 &L, int k, int64_t e_acc, int64_t ss,
-                                                   int clamped, int chg_self, int chgL, int chgR,
-                                                   int chgU, int chgD, int cur, int best, int out) {
-    __shared__ int64_t red_e[32], red_s[32];
+// Per-CTA epilogue shared by the scalar / vector consensus kernels: reduce the
+// thread partials, publish the block's partials and dirty marks; the last CTA
+// to arrive runs finalize_cta.
+__device__ __forceinline__ void consensus_epilogue(const Lat2 &L, int k, int64_t e_acc, int64_t du,
+                                                   int64_t ss, int clamped, int chg_self, int chgL,
+                                                   int chgR, int chgU, int chgD, int cur, int best,
+                                                   int out) {
+    __shared__ int64_t red_e[32], red_s[32], red_u[32];
     __shared__ int red_f[32];
     __shared__ int last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     e_acc = warp_sum(e_acc);
+    du = warp_sum(du);
     ss = warp_sum(ss);
     const unsigned fl = __ballot_sync(FULLMASK, clamped) ? 1u : 0u;
     const unsigned f0 = __ballot_sync(FULLMASK, chg_self) ? 2u : 0u;
@@ -631,15 +646,22 @@ __device__ __forceinline__ void consensus_epilogue(const Lat2 &L, int k, int64_t
     const unsigned f4 = __ballot_sync(FULLMASK, chgD) ? 32u : 0u;
     if (lane == 0) {
         red_e[warp] = e_acc;
+        red_u[warp] = du;
         red_s[warp] = ss;
         red_f[warp] = (int)(fl | f0 | f1 | f2 | f3 | f4);
     }
     __syncthreads();
     if (tid == 0) {
-        int64_t E = 0, S = 0;
+        int64_t E = 0, S = 0, U = 0;
         int Fm = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { E += red_e[w]; S += red_s[w]; Fm |= red_f[w]; }
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            E += red_e[w];
+            U += red_u[w];
+            S += red_s[w];
+            Fm |= red_f[w];
+        }
         L.pe[k] = E;
+        L.pu[k] = U;
         L.pr[k] = S;
         L.pf[k] = Fm & 1;
         if (Fm & 2) L.dirty[k] = 1u;
@@ -659,6 +681,13 @@ __device__ __forceinline__ void consensus_epilogue(const Lat2 &L, int k, int64_t
     }
 }
 
+// Multiplier range: |a| moves by at most 1 per pass (yhat, y in {0, 1}), so
+// st.a_bound (passes so far) bounds it; the run loop stops at 32000 passes
+// (apply_iteration) and the step-level pass checks each value.
+__device__ __forceinline__ void check_a(const Lat2 &L, int a) {
+    if (a > 32000 || a < -32000) atomicCAS(&L.st->error, 0, -1);
+}
+
 // Generic consensus (any tiling, incl. ragged): one CTA per block, scalar.
 __global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
     if (L.st->stop) return;
@@ -670,16 +699,16 @@ __global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
     L.ax.range(bx, lo_c, wc);
     const int32_t W = L.W, H = L.ay.dim;
     const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
-    const int32_t *__restrict__ y_in = L.y2[cur];
-    int32_t *__restrict__ y_out = L.y2[out];
+    const ystore_t *__restrict__ y_in = L.y2[cur];
+    ystore_t *__restrict__ y_out = L.y2[out];
     const int p = L.st->parity;
-    const int32_t *__restrict__ a_in = p ? L.a1 : L.a0;
-    int32_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
+    const astore_t *__restrict__ a_in = p ? L.a1 : L.a0;
+    astore_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
     const bool want_e = L.fuse && L.st->iteration >= 1;
     const bool has_up = lo_r > 0 || L.gup, has_dn = lo_r + hr < H || L.gdn, has_lf = lo_c > 0,
                has_rt = lo_c + wc < W;
 
-    int64_t e_acc = 0, ss = 0;
+    int64_t e_acc = 0, du = 0, ss = 0;
     int clamped = 0, chg_self = 0, chgL = 0, chgR = 0, chgU = 0, chgD = 0;
     const int m = hr * wc;
     for (int v = tid; v < m; v += blockDim.x) {
@@ -697,15 +726,16 @@ __global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
         const int32_t y = ypre < 0 ? 0 : (ypre > 1 ? 1 : ypre);
         const int32_t y2old = y_in[G];
         clamped |= (ypre < 0 || ypre > 1);
-        if (a_out) a_out[G] = aold + yh - y;
-        y_out[G] = 2 * y;
+        if (a_out) a_out[G] = (astore_t)(aold + yh - y);
+        y_out[G] = (ystore_t)(2 * y);
         ss += (yh - y) * (yh - y);
+        if (2 * y != y2old) du += (int64_t)L.u[G] * (2 * y - y2old);
         if (want_e) {
             const int32_t o = y2old >> 1;
             int32_t qd = 0;
             if (Cc + 1 < W) qd += o ^ (y_in[G + 1] >> 1);
             if (R + 1 < H || L.gdn) qd += o ^ (y_in[G + W] >> 1);
-            e_acc += (int64_t)L.u[G] * o + (int64_t)L.lamw * qd;
+            e_acc += (int64_t)L.lamw * qd;
         }
         const bool ychg = (2 * y != y2old);
         chg_self |= ychg || (yh != y);
@@ -716,10 +746,8 @@ __global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
             chgD |= (r == hr - 1 && has_dn);
         }
     }
-    consensus_epilogue(L, k, e_acc, ss, clamped, chg_self, chgL, chgR, chgU, chgD, cur, best, out);
+    consensus_epilogue(L, k, e_acc, du, ss, clamped, chg_self, chgL, chgR, chgU, chgD, cur, best, out);
 }
-
-__device__ __forceinline__ int byte_of(uint32_t w, int i) { return (int)((w >> (8 * i)) & 0xFFu); }
 
 // Vectorized consensus for uniform tilings whose block width is a power of
 // two in [4, 128] and grid width a multiple of 4.  Thread t owns up to QPT
@@ -740,34 +768,34 @@ __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
     const int QR = 1 << lq;              // quads per block row
     const int nq = hr << lq;
     const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
-    const int32_t *__restrict__ y_in = L.y2[cur];
-    int32_t *__restrict__ y_out = L.y2[out];
+    const ystore_t *__restrict__ y_in = L.y2[cur];
+    ystore_t *__restrict__ y_out = L.y2[out];
     const int p = L.st->parity;
-    const int32_t *__restrict__ a_in = p ? L.a1 : L.a0;
-    int32_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
+    const astore_t *__restrict__ a_in = p ? L.a1 : L.a0;
+    astore_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
     const bool want_e = L.fuse && L.st->iteration >= 1;
     const int32_t q = L.q;
     const bool has_up = lo_r > 0 || L.gup, has_dn = lo_r + hr < H || L.gdn, has_lf = lo_c > 0,
                has_rt = lo_c + wc < W;
 
     // ---- issue every load of this thread's quads ----
-    uint32_t yh4[QPT], up4[QPT], dn4[QPT];
-    int4 av[QPT], yo[QPT], uu[QPT], yb[QPT];
+    uint32_t yh4[QPT], up4[QPT], dn4[QPT], yo[QPT], yb[QPT];
+    uint2 av[QPT];
     int lf[QPT], rt[QPT], yr[QPT];
 #pragma unroll
     for (int j = 0; j < QPT; ++j) {
         const int t = tid + j * NT;
-        yh4[j] = 0; up4[j] = 0; dn4[j] = 0; lf[j] = 0; rt[j] = 0; yr[j] = 0;
-        av[j] = make_int4(0, 0, 0, 0); yo[j] = av[j]; uu[j] = av[j]; yb[j] = av[j];
+        yh4[j] = up4[j] = dn4[j] = yo[j] = yb[j] = 0;
+        av[j] = make_uint2(0, 0);
+        lf[j] = rt[j] = yr[j] = 0;
         if (t < nq) {
             const int r = t >> lq, c0 = (t & (QR - 1)) << 2;
             const int64_t G = (int64_t)(lo_r + r) * W + lo_c + c0;
             yh4[j] = __ldcs(reinterpret_cast<const unsigned int *>(L.yhat + G));
-            av[j] = __ldcs(reinterpret_cast<const int4 *>(a_in + G));
-            yo[j] = __ldcg(reinterpret_cast<const int4 *>(y_in + G));
-            uu[j] = __ldg(reinterpret_cast<const int4 *>(L.u + G));
+            av[j] = __ldcs(reinterpret_cast<const uint2 *>(a_in + G));
+            yo[j] = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G));
             if (want_e && (lo_r + r + 1 < H || L.gdn))
-                yb[j] = __ldcg(reinterpret_cast<const int4 *>(y_in + G + W));
+                yb[j] = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G + W));
             if (r == 0 && has_up) up4[j] = *reinterpret_cast<const uint32_t *>(L.yhat + G - W);
             if (r == hr - 1 && has_dn) dn4[j] = *reinterpret_cast<const uint32_t *>(L.yhat + G + W);
             if (c0 == 0 && has_lf) lf[j] = L.yhat[G - 1];
@@ -778,8 +806,9 @@ __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
         }
     }
 
-    // ---- consensus update + energy of the previous iterate ----
-    int e_acc = 0, ss = 0, quad = 0;
+    // ---- consensus update + pair energy of the previous iterate ----
+    int64_t du = 0;
+    int ss = 0, quad = 0;
     int clamped = 0, chg_self = 0, chgL = 0, chgR = 0, chgU = 0, chgD = 0;
 #pragma unroll
     for (int j = 0; j < QPT; ++j) {
@@ -787,33 +816,31 @@ __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
         const bool valid = t < nq;
         const int r = t >> lq, c0 = (t & (QR - 1)) << 2;
         // previous iterate as packed bits (y2 in {0,2} once t >= 1)
-        const uint32_t ob = (uint32_t)((yo[j].x >> 1) | ((yo[j].y >> 1) << 1) |
-                                       ((yo[j].z >> 1) << 2) | ((yo[j].w >> 1) << 3));
+        const uint32_t ob = (uint32_t)((byte_at(yo[j], 0) >> 1) | ((byte_at(yo[j], 1) >> 1) << 1) |
+                                       ((byte_at(yo[j], 2) >> 1) << 2) | ((byte_at(yo[j], 3) >> 1) << 3));
         const uint32_t nxt = __shfl_down_sync(FULLMASK, ob, 1);
         if (!valid) continue;
         const int64_t G = (int64_t)(lo_r + r) * W + lo_c + c0;
         const bool top = (r == 0 && has_up), bot = (r == hr - 1 && has_dn);
         const bool lft = (c0 == 0 && has_lf), rgt = (c0 + 4 == wc && has_rt);
         if (want_e) {
-            const uint32_t bb = (uint32_t)((yb[j].x >> 1) | ((yb[j].y >> 1) << 1) |
-                                           ((yb[j].z >> 1) << 2) | ((yb[j].w >> 1) << 3));
+            const uint32_t bb = (uint32_t)((byte_at(yb[j], 0) >> 1) | ((byte_at(yb[j], 1) >> 1) << 1) |
+                                           ((byte_at(yb[j], 2) >> 1) << 2) | ((byte_at(yb[j], 3) >> 1) << 3));
             quad += __popc((ob ^ (ob >> 1)) & 0x7u);            // pairs inside the quad
             if (c0 + 4 < wc) quad += (int)((ob >> 3) ^ (nxt & 1u));
             else if (rgt) quad += (int)((ob >> 3) ^ (uint32_t)(yr[j] >> 1));
             if (lo_r + r + 1 < H || L.gdn) quad += __popc(ob ^ bb);
-            e_acc += (ob & 1u ? uu[j].x : 0) + (ob & 2u ? uu[j].y : 0) + (ob & 4u ? uu[j].z : 0) +
-                     (ob & 8u ? uu[j].w : 0);
         }
-        const int a4[4] = {av[j].x, av[j].y, av[j].z, av[j].w};
-        const int y24[4] = {yo[j].x, yo[j].y, yo[j].z, yo[j].w};
+        int a4[4];
+        unpack_a4(av[j], a4);
         int y[4], an[4];
         bool ychg_any = false;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int yh = byte_of(yh4[j], i);
+            const int yh = byte_at(yh4[j], i);
             int sx = 0;
-            if (top) sx += yh - byte_of(up4[j], i);
-            if (bot) sx += yh - byte_of(dn4[j], i);
+            if (top) sx += yh - byte_at(up4[j], i);
+            if (bot) sx += yh - byte_at(dn4[j], i);
             if (i == 0 && lft) sx += yh - lf[j];
             if (i == 3 && rgt) sx += yh - rt[j];
             const int ypre = yh + a4[i] - q * sx;
@@ -821,37 +848,43 @@ __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
             y[i] = ypre < 0 ? 0 : (ypre > 1 ? 1 : ypre);
             an[i] = a4[i] + yh - y[i];
             ss += yh ^ y[i];
-            const bool ychg = (2 * y[i] != y24[i]);
+            const int yold = byte_at(yo[j], i);
+            const bool ychg = (2 * y[i] != yold);
+            if (ychg) du += (int64_t)__ldg(L.u + G + i) * (2 * y[i] - yold);
             ychg_any |= ychg;
             chg_self |= ychg | (yh != y[i]);
         }
-        if (a_out) __stcs(reinterpret_cast<int4 *>(a_out + G), make_int4(an[0], an[1], an[2], an[3]));
-        __stcg(reinterpret_cast<int4 *>(y_out + G), make_int4(2 * y[0], 2 * y[1], 2 * y[2], 2 * y[3]));
+        if (a_out) __stcs(reinterpret_cast<uint2 *>(a_out + G), pack_a4(an[0], an[1], an[2], an[3]));
+        __stcg(reinterpret_cast<unsigned int *>(y_out + G), pack_y4(2 * y[0], 2 * y[1], 2 * y[2], 2 * y[3]));
         if (ychg_any) {
             chgU |= top;
             chgD |= bot;
-            chgL |= (lft && (2 * y[0] != y24[0]));
-            chgR |= (rgt && (2 * y[3] != y24[3]));
+            chgL |= (lft && (2 * y[0] != byte_at(yo[j], 0)));
+            chgR |= (rgt && (2 * y[3] != byte_at(yo[j], 3)));
         }
     }
-    const int64_t e64 = (int64_t)e_acc + (int64_t)L.lamw * quad;
-    consensus_epilogue(L, k, e64, (int64_t)ss, clamped, chg_self, chgL, chgR, chgU, chgD, cur, best,
-                       out);
+    const int64_t e64 = (int64_t)L.lamw * quad;
+    consensus_epilogue(L, k, e64, du, (int64_t)ss, clamped, chg_self, chgL, chgR, chgU, chgD, cur,
+                       best, out);
 }
 
 // a += yhat - y for the step-level API (admm.py:241-248), in place.
 __global__ void k_update_multipliers(Lat2 L, int64_t n) {
-    int32_t *a = L.st->parity ? L.a1 : L.a0;
-    const int32_t *y2 = L.y2[L.st->ycur];
+    astore_t *a = L.st->parity ? L.a1 : L.a0;
+    const ystore_t *y2 = L.y2[L.st->ycur];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-        a[i] += (int32_t)L.yhat[i] - (y2[i] >> 1);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int an = (int)a[i] + (int)L.yhat[i] - (y2[i] >> 1);
+        check_a(L, an);
+        a[i] = (astore_t)an;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) L.st->a_bound += 1;
 }
 
-// E = u.y + lamw * sum_pairs (y_i - y_j)^2 of the current iterate (y in {0,1})
-// accumulated into st.energy_acc (exact integer sum: order-free).
+// E of the current iterate into st.energy_acc: pair terms here, plus the
+// running unary term u.y = unary2 / 2 (exact integer sums: order-free).
 __global__ void k_energy_current(Lat2 L, int64_t n) {
-    const int32_t *y2 = L.y2[L.st->ycur];
+    const ystore_t *y2 = L.y2[L.st->ycur];
     int64_t acc = 0;
     const int64_t HW = (int64_t)L.ay.dim * L.W;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -863,8 +896,9 @@ __global__ void k_energy_current(Lat2 L, int64_t n) {
         if (c + 1 < L.W) qd += yi ^ (y2[i + 1] >> 1);
         if (r + 1 < L.ay.dim || L.gdn) qd += yi ^ (y2[i + L.W] >> 1);
         if (z + 1 < L.az.dim) qd += yi ^ (y2[i + HW] >> 1);
-        acc += (int64_t)L.u[i] * yi + (int64_t)L.lamw * qd;
+        acc += (int64_t)L.lamw * qd;
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) acc += L.st->unary2 / 2;
     acc = warp_sum(acc);
     if ((threadIdx.x & 31) == 0)
         atomicAdd((unsigned long long *)&L.st->energy_acc, (unsigned long long)acc);
@@ -891,7 +925,7 @@ __global__ void k_finish_decide(Lat2 L) {
 
 // binarize (admm.py:260-262) of the current iterate: y >= 1/2 -> 1
 __global__ void k_binarize(Lat2 L, int64_t n, uint8_t *out) {
-    const int32_t *y2 = L.y2[L.st->ycur];
+    const ystore_t *y2 = L.y2[L.st->ycur];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
         out[i] = (uint8_t)(y2[i] >= 1);
@@ -909,7 +943,7 @@ __global__ void k_energy4(Lat2 L, const int32_t *__restrict__ y2, int64_t n,
         const int32_t yi = y2[i];
         int64_t qd = 0;
         if (c + 1 < L.W) { const int64_t d = yi - y2[i + 1]; qd += d * d; }
-        if (r + 1 < L.ay.dim || L.gdn) { const int64_t d = yi - y2[i + L.W]; qd += d * d; }
+        if (r + 1 < L.ay.dim) { const int64_t d = yi - y2[i + L.W]; qd += d * d; }
         if (z + 1 < L.az.dim) { const int64_t d = yi - y2[i + HW]; qd += d * d; }
         acc += 2 * (int64_t)L.u[i] * yi + (int64_t)L.lamw * qd;
     }
@@ -917,6 +951,7 @@ __global__ void k_energy4(Lat2 L, const int32_t *__restrict__ y2, int64_t n,
     if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)acc);
 }
 
+// ---------------------------------------------------------------------------
 #include "consensus_tma.cuh"
 #include "lattice3d.cuh"
 
@@ -971,7 +1006,7 @@ static const Variant3 *pick_variant3(int maxd, int maxh, int maxw) {
 static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
                       const Variant3 **var3 = nullptr) {
     if (!L || !L->u || !L->a[0] || !L->a[1] || !L->y2[0] || !L->y2[1] || !L->y2[2] || !L->yhat || !L->resid ||
-        !L->dirty || !L->part_energy || !L->part_ressq || !L->part_flags || !L->state)
+        !L->dirty || !L->part_energy || !L->part_unary || !L->part_ressq || !L->part_flags || !L->state)
         return DOPE_E_ARGS;
     const bool is3 = L->ndim == 3;
     if (!((L->ndim == 2 && L->conn == 4) || (is3 && L->conn == 6))) return DOPE_E_GEOMETRY;
@@ -1018,6 +1053,7 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
     o.scratch = L->scratch;
     o.dirty = L->dirty;
     o.pe = L->part_energy;
+    o.pu = L->part_unary;
     o.pr = L->part_ressq;
     o.pf = L->part_flags;
     o.st = L->state;
@@ -1053,7 +1089,10 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
         if (var) *var = v;
         if (var3) *var3 = nullptr;
     }
-    o.vec4 = !is3 && (o.W % 4 == 0) && (o.ax.rem == 0) && (o.ax.base % 4 == 0);
+    // quad loads: 4 labels / 4 y2 bytes as one word, 4 multipliers as 8 bytes
+    const uintptr_t al = (uintptr_t)o.y2[0] | (uintptr_t)o.y2[1] | (uintptr_t)o.y2[2] | (uintptr_t)o.yhat |
+                         ((uintptr_t)o.a0 >> 1) | ((uintptr_t)o.a1 >> 1) | ((uintptr_t)o.u >> 2);
+    o.vec4 = !is3 && (o.W % 4 == 0) && (o.ax.rem == 0) && (o.ax.base % 4 == 0) && (al % 4 == 0);
     return DOPE_OK;
 }
 
@@ -1169,22 +1208,26 @@ static int sm_count() {
 
 // persistent TMA consensus: run-loop mode, uniform tiling, 64/128-wide blocks
 template <int TW, int NT, int ST>
+static int k2_tma_attr() {
+    return cuda_check(cudaFuncSetAttribute(k_consensus_tma<TW, NT, ST>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           TmaCfg<TW, NT, ST>::SMEM),
+                      "attr K2");
+}
+
+template <int TW, int NT, int ST>
 static int launch_k2_tma(const Lat2 &o, cudaStream_t s, int ctas_per_sm) {
     using C = TmaCfg<TW, NT, ST>;
     static std::once_flag once;
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(k_consensus_tma<TW, NT, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::SMEM);
-    });
+    std::call_once(once, [] { k2_tma_attr<TW, NT, ST>(); });
     TmaMaps M;
     const int64_t W = o.W, H = o.ay.dim;
-    bool ok = make_map(&M.u, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, (void *)o.u, W, H, TW, C::TH);
-    ok = ok && make_map(&M.a[0], CU_TENSOR_MAP_DATA_TYPE_INT32, 4, o.a0, W, H, TW, C::TH);
-    ok = ok && make_map(&M.a[1], CU_TENSOR_MAP_DATA_TYPE_INT32, 4, o.a1, W, H, TW, C::TH);
+    bool ok = make_map(&M.a[0], CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, o.a0, W, H, TW, C::TH);
+    ok = ok && make_map(&M.a[1], CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, o.a1, W, H, TW, C::TH);
     // y2 and yhat carry one ghost row above and below the shard (caller-owned)
     for (int i = 0; i < 3 && ok; ++i) {
-        ok = make_map(&M.y[i], CU_TENSOR_MAP_DATA_TYPE_INT32, 4, o.y2[i] - W, W, H + 2, TW, C::TH + 1);
-        ok = ok && make_map(&M.yr[i], CU_TENSOR_MAP_DATA_TYPE_INT32, 4, o.y2[i] - W, W, H + 2, 4, C::TH);
+        ok = make_map(&M.y[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.y2[i] - W, W, H + 2, TW, C::TH + 1);
+        ok = ok && make_map(&M.yr[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.y2[i] - W, W, H + 2, 16, C::TH);
     }
     ok = ok && make_map(&M.yhat, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.yhat - W, W, H + 2, C::YHW, C::TH + 2);
     if (!ok) {
@@ -1198,9 +1241,15 @@ static int launch_k2_tma(const Lat2 &o, cudaStream_t s, int ctas_per_sm) {
     return cuda_check(cudaGetLastError(), "launch K2 (tma)");
 }
 
+constexpr int K2_NT = 512, K2_STAGES = 8;
+
 static int k2_tma_width(const Lat2 &o) {
     // eligible: run-loop mode, uniform tiling, 64/128-wide blocks, TMA-friendly strides
-    if (!o.fuse || o.ax.rem != 0 || o.ay.rem != 0 || (o.W % 16) != 0) return 0;
+    if (!o.fuse || o.ax.rem != 0 || o.ay.rem != 0 || (o.W % 16) != 0 || o.ndim != 2) return 0;
+    // TMA global addresses must be 16-byte aligned (y2 / yhat maps start one row up)
+    const uintptr_t al = (uintptr_t)(o.y2[0] - o.W) | (uintptr_t)(o.y2[1] - o.W) | (uintptr_t)(o.y2[2] - o.W) |
+                         (uintptr_t)(o.yhat - o.W) | (uintptr_t)o.a0 | (uintptr_t)o.a1;
+    if (al % 16 != 0 || !o.vec4) return 0;
     if (o.ax.base == 64 && o.ay.base % 64 == 0) return 64;
     if (o.ax.base == 128 && o.ay.base % 32 == 0) return 128;
     return 0;
@@ -1214,17 +1263,21 @@ static int launch_k2(const Lat2 &o, cudaStream_t s) {
     const int tw = k2_tma_width(o);
     static const int variant = getenv("DOPE_K2_VARIANT") ? atoi(getenv("DOPE_K2_VARIANT")) : 0;
     if (tw && !getenv("DOPE_NO_TMA")) {
+        // ~20 KB per stage: deep rings keep enough bytes in flight per SM
+        // (Little's law) for a kernel that moves ~7 B per pixel
         if (tw == 64) {
             switch (variant) {
-                case 1: return launch_k2_tma<64, 256, 3>(o, s, 1);
-                case 2: return launch_k2_tma<64, 1024, 3>(o, s, 1);
-                case 3: return launch_k2_tma<64, 512, 2>(o, s, 2);
-                case 4: return launch_k2_tma<64, 256, 2>(o, s, 2);
-                case 5: return launch_k2_tma<64, 512, 4>(o, s, 1);
-                default: return launch_k2_tma<64, 512, 3>(o, s, 1);
+                case 1: return launch_k2_tma<64, 512, 4>(o, s, 1);
+                case 2: return launch_k2_tma<64, 512, 6>(o, s, 1);
+                case 3: return launch_k2_tma<64, 256, 4>(o, s, 2);
+                case 4: return launch_k2_tma<64, 1024, 8>(o, s, 1);
+                case 5: return launch_k2_tma<64, 512, 3>(o, s, 1);
+                case 6: return launch_k2_tma<64, 512, 10>(o, s, 1);
+                case 7: return launch_k2_tma<64, 256, 5>(o, s, 2);
+                default: return launch_k2_tma<64, K2_NT, K2_STAGES>(o, s, 1);
             }
         }
-        return launch_k2_tma<128, 512, 3>(o, s, 1);
+        return launch_k2_tma<128, K2_NT, K2_STAGES>(o, s, 1);
     }
     const int lq = k2_lq(o);
     if (lq >= 0) {
@@ -1294,14 +1347,8 @@ int dope_prepare_kernels(const dope_lattice *L) {
     if ((rc = configure_plan(P))) return rc;
     if (P.o.ndim == 2 && P.o.fuse) {
         const int tw = k2_tma_width(P.o);
-        if (tw == 64)
-            return cuda_check(cudaFuncSetAttribute(k_consensus_tma<64, 512, 3>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   TmaCfg<64, 512, 3>::SMEM), "attr K2");
-        if (tw == 128)
-            return cuda_check(cudaFuncSetAttribute(k_consensus_tma<128, 512, 3>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   TmaCfg<128, 512, 3>::SMEM), "attr K2");
+        if (tw == 64) return k2_tma_attr<64, K2_NT, K2_STAGES>();
+        if (tw == 128) return k2_tma_attr<128, K2_NT, K2_STAGES>();
     }
     return DOPE_OK;
 }
@@ -1313,6 +1360,9 @@ int dope_admm_init(const dope_lattice *L, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     k_init_state<<<grid_for(P.n), 256, 0, s>>>(P.o, P.n);
     rc = cuda_check(cudaGetLastError(), "init_state");
+    if (rc) return rc;
+    k_init_unary<<<grid_for(P.n), 256, 0, s>>>(P.o, P.n);
+    rc = cuda_check(cudaGetLastError(), "init_unary");
     if (rc) return rc;
     if (P.v3) k_init_resid3d<<<P.o.K, 256, 0, s>>>(P.o, P.o.boxd, P.o.boxh, P.o.boxw);
     else k_init_resid<<<P.o.K, 256, 0, s>>>(P.o);

@@ -59,8 +59,8 @@ __global__ void __launch_bounds__(NT) k_block_mincut3d(Lat2 L, K1Tune T) {
     const int32_t W = L.W, H = L.ay.dim, D = L.az.dim;
     const int64_t HW = (int64_t)H * W;
     const int32_t cap = L.cap;
-    const int32_t *__restrict__ a_cur = L.st->parity ? L.a1 : L.a0;
-    const int32_t *__restrict__ y_cur = L.y2[L.st->ycur];
+    const astore_t *__restrict__ a_cur = L.st->parity ? L.a1 : L.a0;
+    const ystore_t *__restrict__ y_cur = L.y2[L.st->ycur];
     int32_t *g = reinterpret_cast<int32_t *>(L.scratch + (size_t)k * 6 * M);
     uint16_t *h = reinterpret_cast<uint16_t *>(g + M);
     uint8_t *rr = L.resid + (size_t)k * 6 * M;
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut3d(Lat2 L, K1Tune T) {
         int32_t gv = 0;
         if (valid) {
             const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + r) * W + gb.lo_c + c;
-            const int32_t yg = y_cur[G];
+            const int32_t yg = (int32_t)y_cur[G];
             int32_t sx = 0;
             if (c == 0 && lf_c) sx += yg - y_cur[G - 1];
             if (c == gb.wc - 1 && rt_c) sx += yg - y_cur[G + 1];
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut3d(Lat2 L, K1Tune T) {
             if (r == gb.hr - 1 && dn_r) sx += yg - y_cur[G + W];
             if (z == 0 && up_z) sx += yg - y_cur[G - HW];
             if (z == gb.dz - 1 && dn_z) sx += yg - y_cur[G + HW];
-            const int32_t lin2 = 2 * L.u[G] + L.lamw * sx + L.mu * (2 * a_cur[G] - yg) + L.mu;
+            const int32_t lin2 = 2 * L.u[G] + L.lamw * sx + L.mu * (2 * (int32_t)a_cur[G] - yg) + L.mu;
             const bool has[6] = {c + 1 < gb.wc, c > 0, r + 1 < gb.hr, r > 0, z + 1 < gb.dz, z > 0};
             if (L.warm) {
                 int32_t f = 0;
@@ -237,17 +237,17 @@ __global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
     const int32_t W = L.W, H = L.ay.dim, D = L.az.dim;
     const int64_t HW = (int64_t)H * W;
     const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
-    const int32_t *__restrict__ y_in = L.y2[cur];
-    int32_t *__restrict__ y_out = L.y2[out];
+    const ystore_t *__restrict__ y_in = L.y2[cur];
+    ystore_t *__restrict__ y_out = L.y2[out];
     const int p = L.st->parity;
-    const int32_t *__restrict__ a_in = p ? L.a1 : L.a0;
-    int32_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
+    const astore_t *__restrict__ a_in = p ? L.a1 : L.a0;
+    astore_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
     const bool want_e = L.fuse && L.st->iteration >= 1;
     const bool up_z = gb.lo_z > 0, dn_z = gb.lo_z + gb.dz < D;
     const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
     const bool lf_c = gb.lo_c > 0, rt_c = gb.lo_c + gb.wc < W;
 
-    int64_t e_acc = 0, ss = 0;
+    int64_t e_acc = 0, ss = 0, du = 0;
     int clamped = 0;
     unsigned marks = 0;    // bit0 self, 1..6: -x +x -y +y -z +z neighbours
     const int m = gb.dz * gb.hr * gb.wc, pl = gb.hr * gb.wc;
@@ -262,13 +262,13 @@ __global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
         if (r == gb.hr - 1 && dn_r) sx += yh - L.yhat[G + W];
         if (z == 0 && up_z) sx += yh - L.yhat[G - HW];
         if (z == gb.dz - 1 && dn_z) sx += yh - L.yhat[G + HW];
-        const int32_t aold = a_in[G];
+        const int32_t aold = (int32_t)a_in[G];
         const int32_t ypre = yh + aold - L.q * sx;
         const int32_t y = ypre < 0 ? 0 : (ypre > 1 ? 1 : ypre);
-        const int32_t y2old = y_in[G];
+        const int32_t y2old = (int32_t)y_in[G];
         clamped |= (ypre < 0 || ypre > 1);
-        if (a_out) a_out[G] = aold + yh - y;
-        y_out[G] = 2 * y;
+        if (a_out) a_out[G] = (astore_t)(aold + yh - y);
+        y_out[G] = (ystore_t)(2 * y);
         ss += (yh - y) * (yh - y);
         if (want_e) {
             const int32_t o = y2old >> 1;
@@ -277,11 +277,12 @@ __global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
             if (gc + 1 < W) qd += o ^ (y_in[G + 1] >> 1);
             if (gr + 1 < H) qd += o ^ (y_in[G + W] >> 1);
             if (gz + 1 < D) qd += o ^ (y_in[G + HW] >> 1);
-            e_acc += (int64_t)L.u[G] * o + (int64_t)L.lamw * qd;
+            e_acc += (int64_t)L.lamw * qd;
         }
         const bool ychg = (2 * y != y2old);
         if (ychg || yh != y) marks |= 1u;
         if (ychg) {
+            du += (int64_t)L.u[G] * (2 * y - y2old);
             if (c == 0 && lf_c) marks |= 2u;
             if (c == gb.wc - 1 && rt_c) marks |= 4u;
             if (r == 0 && up_r) marks |= 8u;
@@ -290,20 +291,22 @@ __global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
             if (z == gb.dz - 1 && dn_z) marks |= 64u;
         }
     }
-    __shared__ int64_t red_e[32], red_s[32];
+    __shared__ int64_t red_e[32], red_s[32], red_u[32];
     __shared__ unsigned red_f[32];
     __shared__ int last;
     e_acc = warp_sum(e_acc);
     ss = warp_sum(ss);
+    du = warp_sum(du);
     for (int o = 16; o > 0; o >>= 1) marks |= __shfl_xor_sync(FULLMASK, marks, o);
     const int fl = __any_sync(FULLMASK, clamped);
-    if (lane == 0) { red_e[warp] = e_acc; red_s[warp] = ss; red_f[warp] = marks | (fl ? 128u : 0u); }
+    if (lane == 0) { red_e[warp] = e_acc; red_s[warp] = ss; red_u[warp] = du; red_f[warp] = marks | (fl ? 128u : 0u); }
     __syncthreads();
     if (tid == 0) {
-        int64_t E = 0, S = 0;
+        int64_t E = 0, S = 0, U = 0;
         unsigned Fm = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { E += red_e[w]; S += red_s[w]; Fm |= red_f[w]; }
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { E += red_e[w]; S += red_s[w]; U += red_u[w]; Fm |= red_f[w]; }
         L.pe[k] = E;
+        L.pu[k] = U;
         L.pr[k] = S;
         L.pf[k] = (Fm & 128u) ? 1 : 0;
         const int KX = L.ax.k, KYX = L.ay.k * L.ax.k;

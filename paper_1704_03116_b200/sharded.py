@@ -88,7 +88,6 @@ class GpuShard:
         L.fuse_multipliers = 1
         _lib.check(_lib.lib().dope_lattice_check(C.byref(L)), "dope_lattice_check (shard)")
         self.W = W
-        self.rows_i32 = [torch.zeros(W, dtype=torch.int32, device=dev) for _ in range(4)]
         self.rows_u8 = [torch.zeros(W, dtype=torch.uint8, device=dev) for _ in range(4)]
 
     # -- kernels ------------------------------------------------------------
@@ -115,7 +114,7 @@ class GpuShard:
 
     def staging(self, which):
         """(send_first, send_last, recv_up, recv_dn) buffers for labels / y."""
-        return self.rows_u8 if which == 0 else self.rows_i32
+        return self.rows_u8   # labels and y2 are both one byte per pixel
 
     def pack_rows(self, which):
         first, last, _, _ = self.staging(which)
