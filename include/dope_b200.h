@@ -84,6 +84,9 @@ typedef struct dope_run_state {
     int32_t reserved_;
 } dope_run_state;
 
+/* Length (int64 elements) of dope_lattice.part_cta. */
+#define DOPE_PART_CTA_LEN 1032
+
 /* Integer lattice problem (C1, C3, C4, C5 of BASELINE.json).
  * Scaling: all quantities that are half-integers in the reference are held
  * doubled: y2 = 2*y (y = 1/2 at init, {0,1} afterwards), block terminal
@@ -116,6 +119,9 @@ typedef struct dope_lattice {
     int64_t *part_unary;        /* K   per-block change of sum u*y2           */
     int64_t *part_ressq;        /* K   per-block sum (yhat - y)^2             */
     int32_t *part_flags;        /* K   bit0: clamped                          */
+    int64_t *part_cta;          /* DOPE_PART_CTA_LEN: per-CTA aggregates of the
+                                   persistent consensus pass (2D run loop);
+                                   zeroed by dope_admm_init                    */
     dope_run_state *state;      /* 1                                          */
     int64_t *trace_energy;      /* max_iters                                  */
     double *trace_residual_sq;  /* max_iters                                  */

@@ -19,6 +19,9 @@ DOPE_E_CUDA = -4
 DOPE_E_NONSUBMODULAR = -5
 
 
+PART_CTA_LEN = 1032   # DOPE_PART_CTA_LEN
+
+
 class RunState(C.Structure):
     """Mirror of dope_run_state."""
     _fields_ = [
@@ -66,6 +69,7 @@ class Lattice(C.Structure):
         ("part_unary", C.c_void_p),
         ("part_ressq", C.c_void_p),
         ("part_flags", C.c_void_p),
+        ("part_cta", C.c_void_p),
         ("state", C.c_void_p),
         ("trace_energy", C.c_void_p),
         ("trace_residual_sq", C.c_void_p),

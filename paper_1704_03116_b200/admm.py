@@ -299,6 +299,7 @@ class _DeviceState:
         self.pu = torch.zeros(K, dtype=torch.int64, device=dev)
         self.pr = torch.zeros(K, dtype=torch.int64, device=dev)
         self.pf = torch.zeros(K, dtype=i32, device=dev)
+        self.pc = torch.zeros(_lib.PART_CTA_LEN, dtype=torch.int64, device=dev)
         self.state = torch.zeros(C.sizeof(_lib.RunState), dtype=u8, device=dev)
         self.tr_e = torch.zeros(max_iters, dtype=torch.int64, device=dev)
         self.tr_rs = torch.zeros(max_iters, dtype=torch.float64, device=dev)
@@ -317,6 +318,7 @@ class _DeviceState:
         L.part_unary = self.pu.data_ptr()
         L.part_ressq = self.pr.data_ptr()
         L.part_flags = self.pf.data_ptr()
+        L.part_cta = self.pc.data_ptr()
         L.state = self.state.data_ptr()
         L.trace_energy = self.tr_e.data_ptr()
         L.trace_residual_sq = self.tr_rs.data_ptr()

@@ -1,20 +1,22 @@
 // consensus_tma.cuh -- persistent, TMA-pipelined consensus pass (K2) for
 // uniform tilings with 64- or 128-wide blocks.  Included by dope_lattice.cu
-// inside namespace dope (uses Lat2, finalize_cta, other_buffer, warp_sum).
+// inside namespace dope (uses Lat2, reduce_blocks, finalize_apply, other_buffer).
 //
 // Same arithmetic as k_consensus_vec (solve_global + clamp admm.py:194-238,
 // update_multipliers admm.py:241-248, block residuals admm.py:251-257, energy
 // of the previous iterate energy.py:187-194), organised for HBM:
-//   * grid = one CTA per SM; each CTA walks its blocks as tiles of TH x TW
-//     pixels (64x64, or 32 rows of a 128-wide block);
-//   * per tile, one thread issues 2D TMA loads (cp.async.bulk.tensor) of u,
-//     a, y (+ the row below), the y column right of the tile and the label
-//     tile with a 1-row / 16-byte halo into a 3-stage shared-memory ring,
-//     completion tracked by mbarriers -- two tiles are always in flight while
-//     the CTA computes the third;
-//   * results go straight from registers to HBM (16-byte streaming stores);
-//   * per-block partials are accumulated with one atomic per warp; the last
-//     CTA runs finalize_cta, which also clears them for the next iteration.
+//   * persistent grid (a few CTAs per SM); each CTA walks its blocks as tiles
+//     of TH x TW pixels (64x64, or 32 rows of a 128-wide block);
+//   * per tile, one thread issues 2D TMA loads (cp.async.bulk.tensor) of the
+//     int16 multipliers, the uint8 iterate y2 (+ the row below), the y2
+//     column right of the tile and the label tile with a 1-row / 16-byte halo
+//     into a STAGES-deep shared-memory ring, completion tracked by mbarriers;
+//     u is not streamed (the unary energy is kept incrementally);
+//   * results go straight from registers to HBM (8-byte multiplier quads,
+//     4-byte iterate quads);
+//   * per-block partials are accumulated with one atomic per warp (the next
+//     K1 clears them); each CTA then folds its own blocks into pass-wide
+//     aggregates, so the last CTA only adds up one residual sum per CTA.
 
 struct TmaMaps {
     CUtensorMap a[2], y[3], yr[3], yhat;
@@ -124,7 +126,7 @@ __device__ __forceinline__ uint32_t quad_update(uint32_t h4, uint2 a2, uint32_t 
 }
 
 template <int TW, int NT_, int STAGES_>
-__global__ void __launch_bounds__(NT_, 1) k_consensus_tma(Lat2 L, const __grid_constant__ TmaMaps M,
+__global__ void __launch_bounds__(NT_, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 1))) k_consensus_tma(Lat2 L, const __grid_constant__ TmaMaps M,
                                                           uint32_t kx_magic) {
     using C = TmaCfg<TW, NT_, STAGES_>;
     constexpr int TH = C::TH, NT = C::NT, QPT = C::QPT, QR = TW / 4, LQ = (TW == 64) ? 4 : 5;
@@ -133,10 +135,19 @@ __global__ void __launch_bounds__(NT_, 1) k_consensus_tma(Lat2 L, const __grid_c
     uint8_t *base = smem_t + ((128u - (smem_u32(smem_t) & 127u)) & 127u);
     __shared__ __align__(8) uint64_t full[C::STAGES];
     __shared__ int last;
+    // per-block accumulators, double-buffered by block parity: warps add into
+    // acc[kb & 1] before the block's last barrier, thread 0 drains it after
+    __shared__ unsigned long long accU[2];
+    __shared__ unsigned int accE[2], accS[2], accF[2];
 
     dope_run_state *st = L.st;
     if (st->stop) return;
     const int tid = threadIdx.x, lane = tid & 31;
+    if (L.timeline && tid == 0) {   // diagnostics: CTA start (slot 6 of entry blockIdx)
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        L.timeline[8 * blockIdx.x + 6] = (int64_t)t;
+    }
     const int cur = st->ycur, best = st->ybest, out = other_buffer(cur, best);
     const int p = st->parity;
     ystore_t *__restrict__ y_out = L.y2[out];
@@ -155,6 +166,16 @@ __global__ void __launch_bounds__(NT_, 1) k_consensus_tma(Lat2 L, const __grid_c
     };
 
     int ikb = 0, itile = 0;
+    // thread 0: this CTA's pass aggregates (blocks in a fixed order)
+    int64_t cE = 0, cU = 0, cM = -1;
+    double cR = 0.0;
+    int cF = 0;
+    if (tid < 2) {
+        accU[tid] = 0;
+        accE[tid] = 0;
+        accS[tid] = 0;
+        accF[tid] = 0;
+    }
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -247,38 +268,79 @@ __global__ void __launch_bounds__(NT_, 1) k_consensus_tma(Lat2 L, const __grid_c
                     fl |= em & mk;
                 }
             }
+            const int ab = kb & 1;
+            if (tile == tpb - 1) {
+                // block done in this warp: one shared atomic per quantity
+                const unsigned e = __reduce_add_sync(FULLMASK, (unsigned)quad_acc);
+                const unsigned sq = __reduce_add_sync(FULLMASK, (unsigned)ss);
+                const unsigned f = __reduce_or_sync(FULLMASK, fl | (clp > 1u ? 1u : 0u));
+                int64_t u2 = 0;
+                if (__any_sync(FULLMASK, du != 0)) u2 = warp_sum(du);
+                if (lane == 0) {
+                    if (e) atomicAdd(&accE[ab], e);
+                    if (sq) atomicAdd(&accS[ab], sq);
+                    if (f) atomicOr(&accF[ab], f);
+                    if (u2) atomicAdd(&accU[ab], (unsigned long long)u2);
+                }
+            }
             // every warp is done with stage s: refill it with the tile STAGES ahead
             __syncthreads();
-            if (tid == 0 && ikb < nblk) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                int by2, bx2;
-                coords(ikb, by2, bx2);
-                tma_issue_tile<TW>(L, M, base + s * C::STAGE, &full[s], by2, bx2, itile, cur, p);
-                if (++itile == tpb) { itile = 0; ++ikb; }
+            if (tid == 0) {
+                if (ikb < nblk) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    int by2, bx2;
+                    coords(ikb, by2, bx2);
+                    tma_issue_tile<TW>(L, M, base + s * C::STAGE, &full[s], by2, bx2, itile, cur, p);
+                    if (++itile == tpb) { itile = 0; ++ikb; }
+                }
+                if (tile == tpb - 1) {
+                    // drain block k: per-block partials (diagnostics / step API
+                    // parity), dirty marks, and this CTA's running aggregates
+                    const int64_t e = (int64_t)L.lamw * accE[ab];
+                    const int64_t u2 = (int64_t)accU[ab];
+                    const int64_t sq = accS[ab];
+                    const unsigned f = accF[ab];
+                    accE[ab] = 0;
+                    accS[ab] = 0;
+                    accF[ab] = 0;
+                    accU[ab] = 0;
+                    L.pe[k] = e;
+                    L.pu[k] = u2;
+                    L.pr[k] = sq;
+                    L.pf[k] = (int)(f & 1u);
+                    cE += e;
+                    cU += u2;
+                    cM = sq > cM ? sq : cM;
+                    const double r = sqrt((double)sq);
+                    cR += r * r;
+                    cF |= (int)(f & 1u);
+                    if (f & 2u) L.dirty[k] = 1u;
+                    if (f & 4u) L.dirty[k - 1] = 1u;
+                    if (f & 8u) L.dirty[k + 1] = 1u;
+                    if ((f & 16u) && k - KX >= 0) L.dirty[k - KX] = 1u;
+                    if ((f & 32u) && k + KX < L.K) L.dirty[k + KX] = 1u;
+                }
             }
             if (++s == C::STAGES) { s = 0; phase ^= 1u; }
         }
-        // publish this block's partials: one atomic per warp (redux.sync)
-        const int e = (int)__reduce_add_sync(FULLMASK, (unsigned)quad_acc);
-        const int sq = (int)__reduce_add_sync(FULLMASK, (unsigned)ss);
-        const uint32_t f = __reduce_or_sync(FULLMASK, fl | (clp > 1u ? 1u : 0u));
-        int64_t u2 = 0;
-        if (__any_sync(FULLMASK, du != 0)) u2 = warp_sum(du);
-        if (lane == 0) {
-            if (e) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pe[k]),
-                             (unsigned long long)((int64_t)L.lamw * e));
-            if (u2) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pu[k]), (unsigned long long)u2);
-            if (sq) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pr[k]), (unsigned long long)sq);
-            if (f & 1u) atomicOr(&L.pf[k], 1);
-            if (f & 2u) L.dirty[k] = 1u;
-            if (f & 4u) L.dirty[k - 1] = 1u;
-            if (f & 8u) L.dirty[k + 1] = 1u;
-            if ((f & 16u) && k - KX >= 0) L.dirty[k - KX] = 1u;
-            if ((f & 32u) && k + KX < L.K) L.dirty[k + KX] = 1u;
-        }
     }
-    __syncthreads();
+    // fold this CTA's aggregates into the pass-wide ones (exact integer
+    // atomics; the float residual sum per CTA, for the last CTA to add up by
+    // CTA index -- deterministic)
+    // this CTA's blocks are complete: fold their partials into the pass-wide
+    // aggregates (exact integer atomics; the float residual sum per CTA, in a
+    // fixed order, for the last CTA to add up by CTA index)
     if (tid == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[0]), (unsigned long long)cE);
+        atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[1]), (unsigned long long)cU);
+        atomicMax(reinterpret_cast<unsigned long long *>(&L.pc[2]), (unsigned long long)(cM + 1));
+        if (cF) atomicOr(reinterpret_cast<unsigned long long *>(&L.pc[3]), 1ull);
+        L.pc[8 + blockIdx.x] = __double_as_longlong(cR);
+        if (L.timeline) {   // diagnostics: CTA end (slot 7)
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            L.timeline[8 * blockIdx.x + 7] = (int64_t)t;
+        }
         __threadfence();
         const int prev = atomicAdd(&st->done_ctas, 1);
         last = (prev == (int)gridDim.x - 1);
@@ -286,7 +348,36 @@ __global__ void __launch_bounds__(NT_, 1) k_consensus_tma(Lat2 L, const __grid_c
     __syncthreads();
     if (last) {
         __threadfence();
-        finalize_cta(L, cur, best, out);   // partials are cleared by the next K1
-        if (tid == 0) st->done_ctas = 0;
+        dope_run_state s0;
+        int64_t E2 = 0, U2 = 0, M2 = 0, F2 = 0;
+        if (tid == 0) {   // in flight together with the residual loads
+            s0 = *st;
+            E2 = __ldcg(&L.pc[0]);
+            U2 = __ldcg(&L.pc[1]);
+            M2 = __ldcg(&L.pc[2]) - 1;
+            F2 = __ldcg(&L.pc[3]);
+        }
+        // residual sum over CTAs in index order (deterministic)
+        __shared__ double sR[NT_ / 32];
+        double R = 0.0;
+        for (int i = tid; i < (int)gridDim.x; i += NT) R += __longlong_as_double(__ldcg(&L.pc[8 + i]));
+        for (int o = 16; o > 0; o >>= 1) R += __shfl_xor_sync(FULLMASK, R, o);
+        if (lane == 0) sR[tid >> 5] = R;
+        __syncthreads();
+        if (tid == 0) {
+            double R2 = 0.0;
+            for (int w = 0; w < NT / 32; ++w) R2 += sR[w];
+            L.pc[0] = 0;
+            L.pc[1] = 0;
+            L.pc[2] = 0;
+            L.pc[3] = 0;
+            finalize_apply(L, s0, E2, U2, R2, M2, (int)F2, cur, best, out);
+            st->done_ctas = 0;
+            if (L.timeline && (int)gridDim.x < L.K) {   // diagnostics: finalize end
+                uint64_t t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                L.timeline[8 * gridDim.x + 7] = (int64_t)t;
+            }
+        }
     }
 }

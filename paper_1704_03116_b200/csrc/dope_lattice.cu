@@ -60,6 +60,7 @@ struct Lat2 {
     uint32_t *dirty;
     int64_t *pe, *pr, *pu;
     int32_t *pf;
+    int64_t *pc;   // [0] E, [1] U, [2] M2 + 1 (max), [3] F (or), [8 + cta] R2 bits
     dope_run_state *st;
     int64_t *tr_e;
     double *tr_rs, *tr_mr;
@@ -424,6 +425,8 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
         L.a1[i] = 0;
         L.yhat[i] = 0;
     }
+    if (blockIdx.x == 0 && L.pc)
+        for (int i = threadIdx.x; i < DOPE_PART_CTA_LEN; i += blockDim.x) L.pc[i] = 0;
     if (L.ndim == 2) {   // ghost rows of the initial iterate: the neighbours' y = 1/2
         for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < L.W; c += stride) {
             L.y2[0][-L.W + c] = 1;
@@ -481,14 +484,16 @@ __device__ __forceinline__ int other_buffer(int cur, int best) {
 // trace entry, best iterate by buffer index (strict <), parity, stop rule,
 // y-buffer rotation.  E2 is the energy of the previous iterate (y_{t}),
 // R2/M2/F2 the residual sum, max block residual^2 and clamp flag of this one.
-__device__ void apply_iteration(const Lat2 &L, int64_t E2, double R2, int64_t M2, int F2, int cur,
-                                int best_idx, int out) {
+// s0 is a snapshot of the run state taken by the caller (its fields are read
+// in one go instead of one dependent round trip per field).
+__device__ void apply_iteration(const Lat2 &L, const dope_run_state &s0, int64_t E2, double R2, int64_t M2,
+                                int F2, int cur, int best_idx, int out) {
     dope_run_state *st = L.st;
     int bidx = best_idx;
-    const int t = st->iteration;        // iterations completed before this one
+    const int t = s0.iteration;         // iterations completed before this one
     if (t >= 1) {
         if (t - 1 < L.max_iters) L.tr_e[t - 1] = E2;
-        if (E2 < st->best_energy) {
+        if (E2 < s0.best_energy) {
             st->best_energy = E2;
             st->best_iteration = t;
             bidx = cur;
@@ -500,80 +505,121 @@ __device__ void apply_iteration(const Lat2 &L, int64_t E2, double R2, int64_t M2
         L.tr_mr[t] = maxres;
         L.tr_cl[t] = F2;
     }
-    st->parity ^= 1;
+    st->parity = s0.parity ^ 1;
     st->iteration = t + 1;
+    int stop = 0;
     if (L.K == 0 || maxres <= L.eps) {
         st->converged = 1;
-        st->stop = 1;
+        stop = 1;
     }
-    if (!st->error && st->a_bound >= 32000) st->error = -1;   // int16 multipliers
-    if (st->error) st->stop = 1;
+    int err = s0.error;
+    if (!err && s0.a_bound >= 32000) {   // int16 multipliers
+        err = -1;
+        st->error = -1;
+    }
+    if (err || stop) st->stop = 1;
     st->ybest = bidx;
     st->ycur = out;
 }
 
-// Reduce the per-block partials and apply them (run-loop mode) -- or, when
-// sharded, publish this shard's aggregates for the cross-rank all-reduce and
-// leave the decision to dope_decide.  Always advances the running unary term.
-// Executed by the whole last CTA of a consensus launch; blocks are assigned to
-// threads by index and combined in a fixed tree, so float sums are
-// deterministic.
-__device__ void finalize_cta(const Lat2 &L, int cur, int best_idx, int out) {
-    __shared__ int64_t sE[32], sU[32];
-    __shared__ double sR[32];
-    __shared__ int64_t sM[32];
-    __shared__ int sF[32];
+// Apply one consensus pass's global aggregates (pair energy E of y_{t-1},
+// unary change U, residual sum R2, max block residual^2 M2, clamp flag F):
+// run-loop decision, or -- when sharded -- publish them for the cross-rank
+// all-reduce and leave the decision to dope_decide.  Always advances the
+// running unary term.  One thread.
+__device__ void finalize_apply(const Lat2 &L, dope_run_state s0, int64_t E2, int64_t U2, double R2,
+                               int64_t M2, int F2, int cur, int best_idx, int out) {
     dope_run_state *st = L.st;
+    E2 += s0.unary2 / 2;             // E(y_{t-1}) = u.y_{t-1} + pair terms
+    st->unary2 = s0.unary2 + U2;     // now sum u*y2_t
+    if (L.fuse) st->a_bound = ++s0.a_bound;   // this pass updated the multipliers
+    if (!L.fuse) {                   // step-level API: rotate only
+        st->ybest = best_idx;
+        st->ycur = out;
+    } else if (L.sharded) {
+        L.agg[0] = E2;
+        L.agg[1] = __double_as_longlong(R2);
+        L.agg[2] = M2;
+        L.agg[3] = F2;
+    } else {
+        apply_iteration(L, s0, E2, R2, M2, F2, cur, best_idx, out);
+    }
+}
+
+// Reduce per-block partials of the blocks first, first + stride, ... (< K) over
+// the calling CTA: thread-strided, then a fixed shuffle tree and warp order,
+// so the float sum is deterministic.  Result valid in thread 0.
+struct Aggr {
+    int64_t E, U, M;
+    double R;
+    int F;
+};
+
+__device__ Aggr reduce_blocks(const Lat2 &L, int first, int stride, int count) {
+    __shared__ int64_t sE[32], sU[32], sM[32];
+    __shared__ double sR[32];
+    __shared__ int sF[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    int64_t E = 0, U = 0, mx = -1;
-    double rs = 0.0;
-    int F = 0;
-    for (int k = tid; k < L.K; k += blockDim.x) {
-        E += __ldcg(&L.pe[k]);
-        U += __ldcg(&L.pu[k]);
-        const int64_t sq = __ldcg(&L.pr[k]);
-        const double r = sqrt((double)sq);
-        rs += r * r;
-        mx = sq > mx ? sq : mx;
-        F |= __ldcg(&L.pf[k]);
+    Aggr a{0, 0, -1, 0.0, 0};
+    // batches of UNR blocks per thread: all loads of a batch are in flight
+    // together (a strided loop would pay one L2 round trip per block)
+    constexpr int UNR = 8;
+    for (int i0 = tid; i0 < count; i0 += blockDim.x * UNR) {
+        int64_t e[UNR], u[UNR], sq[UNR];
+        int f[UNR];
+#pragma unroll
+        for (int j = 0; j < UNR; ++j) {
+            const int i = i0 + j * blockDim.x;
+            const bool in = i < count;
+            const int k = first + i * stride;
+            e[j] = in ? __ldcg(&L.pe[k]) : 0;
+            u[j] = in ? __ldcg(&L.pu[k]) : 0;
+            sq[j] = in ? __ldcg(&L.pr[k]) : -1;
+            f[j] = in ? __ldcg(&L.pf[k]) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < UNR; ++j) {
+            a.E += e[j];
+            a.U += u[j];
+            a.F |= f[j];
+            if (sq[j] >= 0) {
+                const double r = sqrt((double)sq[j]);
+                a.R += r * r;
+                a.M = sq[j] > a.M ? sq[j] : a.M;
+            }
+        }
     }
-    E = warp_sum(E);
-    U = warp_sum(U);
+    a.E = warp_sum(a.E);
+    a.U = warp_sum(a.U);
     for (int o = 16; o > 0; o >>= 1) {
-        rs += __shfl_xor_sync(FULLMASK, rs, o);
-        const int64_t t = __shfl_xor_sync(FULLMASK, mx, o);
-        mx = t > mx ? t : mx;
+        a.R += __shfl_xor_sync(FULLMASK, a.R, o);
+        const int64_t t = __shfl_xor_sync(FULLMASK, a.M, o);
+        a.M = t > a.M ? t : a.M;
     }
-    F = __any_sync(FULLMASK, F);
-    if (lane == 0) { sE[warp] = E; sU[warp] = U; sR[warp] = rs; sM[warp] = mx; sF[warp] = F; }
+    a.F = __any_sync(FULLMASK, a.F);
+    __syncthreads();   // the shared scratch may be reused by consecutive calls
+    if (lane == 0) { sE[warp] = a.E; sU[warp] = a.U; sR[warp] = a.R; sM[warp] = a.M; sF[warp] = a.F; }
     __syncthreads();
     if (tid == 0) {
-        int64_t E2 = 0, U2 = 0, M2 = -1;
-        double R2 = 0.0;
-        int F2 = 0;
+        a = Aggr{0, 0, -1, 0.0, 0};
         const int nw = blockDim.x / 32;
         for (int w = 0; w < nw; ++w) {
-            E2 += sE[w];
-            U2 += sU[w];
-            R2 += sR[w];
-            M2 = sM[w] > M2 ? sM[w] : M2;
-            F2 |= sF[w];
-        }
-        E2 += st->unary2 / 2;            // E(y_{t-1}) = u.y_{t-1} + pair terms
-        st->unary2 += U2;                // now sum u*y2_t
-        if (L.fuse) st->a_bound += 1;    // this pass updated the multipliers
-        if (!L.fuse) {                   // step-level API: rotate only
-            st->ybest = best_idx;
-            st->ycur = out;
-        } else if (L.sharded) {
-            L.agg[0] = E2;
-            L.agg[1] = __double_as_longlong(R2);
-            L.agg[2] = M2;
-            L.agg[3] = F2;
-        } else {
-            apply_iteration(L, E2, R2, M2, F2, cur, best_idx, out);
+            a.E += sE[w];
+            a.U += sU[w];
+            a.R += sR[w];
+            a.M = sM[w] > a.M ? sM[w] : a.M;
+            a.F |= sF[w];
         }
     }
+    return a;
+}
+
+// Last CTA of a one-CTA-per-block consensus launch: reduce all K blocks' partials.
+__device__ void finalize_cta(const Lat2 &L, int cur, int best_idx, int out) {
+    dope_run_state s0;
+    if (threadIdx.x == 0) s0 = *L.st;   // in flight during the reduction
+    const Aggr a = reduce_blocks(L, 0, 1, L.K);
+    if (threadIdx.x == 0) finalize_apply(L, s0, a.E, a.U, a.R, a.M, a.F, cur, best_idx, out);
 }
 
 // Sharded mode: apply the all-reduced aggregates (identical on every rank).
@@ -581,7 +627,8 @@ __global__ void k_decide(Lat2 L) {
     dope_run_state *st = L.st;
     if (st->stop) return;
     const int cur = st->ycur, best = st->ybest;
-    apply_iteration(L, L.agg[0], __longlong_as_double(L.agg[1]), L.agg[2], (int)L.agg[3], cur, best,
+    const dope_run_state s0 = *st;
+    apply_iteration(L, s0, L.agg[0], __longlong_as_double(L.agg[1]), L.agg[2], (int)L.agg[3], cur, best,
                     other_buffer(cur, best));
 }
 
@@ -1006,7 +1053,8 @@ static const Variant3 *pick_variant3(int maxd, int maxh, int maxw) {
 static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
                       const Variant3 **var3 = nullptr) {
     if (!L || !L->u || !L->a[0] || !L->a[1] || !L->y2[0] || !L->y2[1] || !L->y2[2] || !L->yhat || !L->resid ||
-        !L->dirty || !L->part_energy || !L->part_unary || !L->part_ressq || !L->part_flags || !L->state)
+        !L->dirty || !L->part_energy || !L->part_unary || !L->part_ressq || !L->part_flags || !L->state ||
+        (L->ndim == 2 && !L->part_cta))
         return DOPE_E_ARGS;
     const bool is3 = L->ndim == 3;
     if (!((L->ndim == 2 && L->conn == 4) || (is3 && L->conn == 6))) return DOPE_E_GEOMETRY;
@@ -1056,6 +1104,7 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
     o.pu = L->part_unary;
     o.pr = L->part_ressq;
     o.pf = L->part_flags;
+    o.pc = L->part_cta;
     o.st = L->state;
     o.tr_e = L->trace_energy;
     o.tr_rs = L->trace_residual_sq;
@@ -1234,14 +1283,17 @@ static int launch_k2_tma(const Lat2 &o, cudaStream_t s, int ctas_per_sm) {
         snprintf(g_last_err, sizeof(g_last_err), "cuTensorMapEncodeTiled failed");
         return DOPE_E_CUDA;
     }
-    const int slots = ctas_per_sm * sm_count();
-    const int grid = o.K < slots ? o.K : slots;
+    int grid = ctas_per_sm * sm_count();
+    grid = grid < DOPE_PART_CTA_LEN - 8 ? grid : DOPE_PART_CTA_LEN - 8;   // one residual slot per CTA
+    grid = o.K < grid ? o.K : grid;
     const uint32_t magic = (uint32_t)(((1ull << 32) + o.ax.k - 1) / o.ax.k);
     k_consensus_tma<TW, NT, ST><<<grid, C::NT, C::SMEM, s>>>(o, M, magic);
     return cuda_check(cudaGetLastError(), "launch K2 (tma)");
 }
 
-constexpr int K2_NT = 512, K2_STAGES = 8;
+// measured on C3 (tools/k2_variants.sh): 4 CTAs x 4 warps x 2 stages per SM
+// beat 1-2 fat CTAs with deeper rings (more independent warps, cheap barriers)
+constexpr int K2_NT = 128, K2_STAGES = 2, K2_CPS = 4;
 
 static int k2_tma_width(const Lat2 &o) {
     // eligible: run-loop mode, uniform tiling, 64/128-wide blocks, TMA-friendly strides
@@ -1268,16 +1320,16 @@ static int launch_k2(const Lat2 &o, cudaStream_t s) {
         if (tw == 64) {
             switch (variant) {
                 case 1: return launch_k2_tma<64, 512, 4>(o, s, 1);
-                case 2: return launch_k2_tma<64, 512, 6>(o, s, 1);
+                case 2: return launch_k2_tma<64, 512, 8>(o, s, 1);
                 case 3: return launch_k2_tma<64, 256, 4>(o, s, 2);
-                case 4: return launch_k2_tma<64, 1024, 8>(o, s, 1);
-                case 5: return launch_k2_tma<64, 512, 3>(o, s, 1);
-                case 6: return launch_k2_tma<64, 512, 10>(o, s, 1);
+                case 4: return launch_k2_tma<64, 128, 3>(o, s, 3);
+                case 5: return launch_k2_tma<64, 256, 3>(o, s, 2);
+                case 6: return launch_k2_tma<64, 128, 4>(o, s, 2);
                 case 7: return launch_k2_tma<64, 256, 5>(o, s, 2);
-                default: return launch_k2_tma<64, K2_NT, K2_STAGES>(o, s, 1);
+                default: return launch_k2_tma<64, K2_NT, K2_STAGES>(o, s, K2_CPS);
             }
         }
-        return launch_k2_tma<128, K2_NT, K2_STAGES>(o, s, 1);
+        return launch_k2_tma<128, K2_NT, K2_STAGES>(o, s, K2_CPS);
     }
     const int lq = k2_lq(o);
     if (lq >= 0) {

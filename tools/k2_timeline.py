@@ -1,0 +1,52 @@
+"""Per-CTA timeline of the persistent TMA consensus pass (diagnostics):
+CTA start / end spread and the last-CTA finalize tail."""
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from bench import build_problem  # noqa: E402
+from paper_1704_03116_b200 import workloads as W  # noqa: E402
+from paper_1704_03116_b200.admm import _DeviceState  # noqa: E402
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "C3"
+    iters = int(sys.argv[2]) if len(sys.argv) > 2 else 12
+    torch.cuda.set_device(0)
+    wl = W.by_name(name)
+    _, _, problems = build_problem(wl, torch.device("cuda", 0))
+    dev = _DeviceState(problems, int(wl.rho), 0.0, iters, True, True)
+    K = wl.num_blocks
+    tl = torch.zeros(8 * K, dtype=torch.int64, device="cuda")
+    dev.L.timeline = tl.data_ptr()
+    dev.call("dope_admm_init")
+    G = torch.cuda.get_device_properties(0).multi_processor_count
+    for it in range(iters):
+        dev.call("dope_update_blocks")
+        tl.zero_()
+        e1, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e1.record()
+        dev.call("dope_update_global", fuse=1)
+        e2.record()
+        torch.cuda.synchronize()
+        t = tl.view(K, 8).cpu().numpy()
+        st = t[:, 6][t[:, 6] > 0]
+        en = t[:, 7][: len(st)]
+        if st.size == 0:
+            print(f"it {it+1}: no TMA timeline (generic consensus path)")
+            continue
+        t0 = st.min()
+        fin = t[len(st), 7] if len(st) < K else 0
+        print(f"it {it+1:3d}: K2 {e1.elapsed_time(e2)*1e3:6.1f} us | ctas {len(st)} start spread "
+              f"{(st.max()-t0)/1e3:5.1f} us | end min {(en.min()-t0)/1e3:5.1f} med {(np.median(en)-t0)/1e3:5.1f} "
+              f"max {(en.max()-t0)/1e3:5.1f} us | finalize end {(fin-t0)/1e3 if fin else float('nan'):5.1f} us")
+    dev.raise_on_error()
+
+
+if __name__ == "__main__":
+    main()
