@@ -85,7 +85,7 @@ typedef struct dope_run_state {
 } dope_run_state;
 
 /* Length (int64 elements) of dope_lattice.part_cta. */
-#define DOPE_PART_CTA_LEN 1032
+#define DOPE_PART_CTA_LEN 8
 
 /* Integer lattice problem (C1, C3, C4, C5 of BASELINE.json).
  * Scaling: all quantities that are half-integers in the reference are held
@@ -109,19 +109,22 @@ typedef struct dope_lattice {
                                    update_multipliers (the run loop)          */
     /* caller-owned device buffers */
     const int32_t *u;           /* n   unary                                  */
-    int16_t *a[2];              /* n   multipliers, ping-pong by state.parity */
+    int16_t *a;                 /* n   multipliers, updated in place          */
     uint8_t *y2[3];             /* n   2*y; three rotating iterate buffers:
                                    current, best, and the next output         */
     uint8_t *yhat;              /* n   block labels (global layout)           */
     uint8_t *resid;             /* K * resid_stride bytes: residual graphs    */
-    uint32_t *dirty;            /* K   block needs a re-solve                 */
+    uint32_t *dirty;            /* 2K: [0, K) block needs a re-solve (init 1);
+                                   [K, 2K) iteration + 1 of the block's last
+                                   solve (init 0)                              */
     int64_t *part_energy;       /* K   per-block pair-energy partials          */
     int64_t *part_unary;        /* K   per-block change of sum u*y2           */
     int64_t *part_ressq;        /* K   per-block sum (yhat - y)^2             */
     int32_t *part_flags;        /* K   bit0: clamped                          */
-    int64_t *part_cta;          /* DOPE_PART_CTA_LEN: per-CTA aggregates of the
-                                   persistent consensus pass (2D run loop);
-                                   zeroed by dope_admm_init                    */
+    int64_t *part_cta;          /* DOPE_PART_CTA_LEN: pass-wide aggregates and
+                                   the block claim counter of the persistent
+                                   consensus pass (2D); zeroed by
+                                   dope_admm_init                              */
     dope_run_state *state;      /* 1                                          */
     int64_t *trace_energy;      /* max_iters                                  */
     double *trace_residual_sq;  /* max_iters                                  */

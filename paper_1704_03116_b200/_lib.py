@@ -19,7 +19,7 @@ DOPE_E_CUDA = -4
 DOPE_E_NONSUBMODULAR = -5
 
 
-PART_CTA_LEN = 1032   # DOPE_PART_CTA_LEN
+PART_CTA_LEN = 8   # DOPE_PART_CTA_LEN
 
 
 class RunState(C.Structure):
@@ -60,7 +60,7 @@ class Lattice(C.Structure):
         ("skip_clean", C.c_int32),
         ("fuse_multipliers", C.c_int32),
         ("u", C.c_void_p),
-        ("a", C.c_void_p * 2),
+        ("a", C.c_void_p),
         ("y2", C.c_void_p * 3),
         ("yhat", C.c_void_p),
         ("resid", C.c_void_p),

@@ -223,6 +223,9 @@ class _FloatDeviceState:
         # float path stores y itself; expose 2*y for a uniform host view
         return self.y2[self.run_state().ycur] * 2.0
 
+    def multipliers(self):
+        return self.a[self.run_state().parity]
+
     def binarize(self):
         import torch
         out = torch.empty(self.problems.lowering.n, dtype=torch.uint8, device=self.problems.device)
@@ -281,7 +284,7 @@ class _DeviceState:
         i32, u8 = torch.int32, torch.uint8
         # multipliers fit int16 (|a| <= t + 1, max_iters is capped below 32000);
         # 2y in {0, 1, 2} is one byte
-        self.a = [torch.zeros(n, dtype=torch.int16, device=dev) for _ in range(2)]
+        self.a = torch.zeros(n, dtype=torch.int16, device=dev)   # updated in place
         # 2D: y2 and yhat carry one ghost row above and below (neighbour shards;
         # unused on a single GPU), the ABI points one row into the allocation
         g = low.dims[-1] if len(low.dims) == 2 else 0
@@ -292,7 +295,9 @@ class _DeviceState:
         self.yhat = self.yhat_full[g:g + n]
         self.agg = torch.zeros(4, dtype=torch.int64, device=dev)
         self.resid = torch.zeros(K * stride, dtype=u8, device=dev)
-        self.dirty = torch.ones(K, dtype=torch.int32, device=dev)
+        # [0, K): re-solve flags; [K, 2K): iteration + 1 of each block's last solve
+        self.dirty = torch.zeros(2 * K, dtype=torch.int32, device=dev)
+        self.dirty[:K] = 1
         sstride = int(lb.dope_scratch_stride(C.byref(L)))
         self.scratch = torch.empty(max(K * sstride, 16), dtype=u8, device=dev)
         self.pe = torch.zeros(K, dtype=torch.int64, device=dev)
@@ -306,8 +311,7 @@ class _DeviceState:
         self.tr_mr = torch.zeros(max_iters, dtype=torch.float64, device=dev)
         self.tr_cl = torch.zeros(max_iters, dtype=i32, device=dev)
         L.u = problems.u.data_ptr()
-        L.a[0] = self.a[0].data_ptr()
-        L.a[1] = self.a[1].data_ptr()
+        L.a = self.a.data_ptr()
         for i in range(3):
             L.y2[i] = self.y2[i].data_ptr()
         L.yhat = self.yhat.data_ptr()
@@ -343,6 +347,9 @@ class _DeviceState:
 
     def y2_current(self):
         return self.y2[self.run_state().ycur]
+
+    def multipliers(self):
+        return self.a
 
     def binarize(self):
         import torch
@@ -423,7 +430,7 @@ class AdmmState:
         else:
             self._dev.y2_current().copy_(torch.as_tensor((2 * v).astype(np.uint8)))
             self._dev.reset_unary()
-        self._dev.dirty.fill_(1)
+        self._dev.dirty[:self._dev.problems.lowering.K].fill_(1)
 
     def _global_to_blocks(self, vec: np.ndarray, dtype) -> list:
         out = []
@@ -446,8 +453,7 @@ class AdmmState:
     def multipliers_global(self) -> np.ndarray:
         if self._dev is None:
             return np.zeros(self._n)
-        rs = self._dev.run_state()
-        return self._dev.a[rs.parity].double().cpu().numpy()
+        return self._dev.multipliers().double().cpu().numpy()
 
     def labels_global(self) -> np.ndarray:
         """Current block labels (yhat) in global layout."""

@@ -19,13 +19,21 @@
 //     aggregates, so the last CTA only adds up one residual sum per CTA.
 
 struct TmaMaps {
-    CUtensorMap a[2], y[3], yr[3], yhat;
+    CUtensorMap a, y[3], yr[3], yhat;
+    CUtensorMap hrow, hcol;   // labels: one row of TW, a 16-byte column of TH rows
+    CUtensorMap arow, acol;   // multipliers: one row of TW, an 8-wide column of TH rows
 };
 
-// Stage layout of one TH x TW tile: multipliers (int16), previous iterate y2
-// (uint8, +1 row below), the 16-byte column right of the tile (its first byte is
-// the right-halo y2), labels with a 1-row / 16-byte halo.  u is not streamed:
-// the unary energy is kept incrementally (u gathered only where y changes).
+// Stage layout of one TH x TW tile.
+// Solved block (re-solved by this iteration's K1): multipliers (int16),
+// previous iterate y2 (uint8, +1 row below), the 16-byte column right of the
+// tile (its first byte is the right-halo y2), labels with a 1-row / 16-byte
+// halo.
+// Clean block (not re-solved): its interior is a fixed point of the update
+// (y == yhat there and neither moves), so only y2 and the
+// labels just across the block boundary are streamed (its own labels equal
+// y2 / 2); ring multipliers are read directly.
+// u is never streamed: the unary energy is kept incrementally.
 template <int TW, int NT_ = 512, int STAGES_ = 3>
 struct TmaCfg {
     static constexpr int TH = 4096 / TW;                 // tile rows (64 or 32)
@@ -42,6 +50,14 @@ struct TmaCfg {
     static constexpr int O_H = (O_YR + B_YR + 127) / 128 * 128;
     static constexpr int STAGE = (O_H + B_H + 127) / 128 * 128;
     static constexpr int TX = B_A + B_Y + B_YR + B_H;
+    // clean tiles: neighbour labels in the (unused) multiplier area
+    // clean tiles: neighbour labels and the ring multipliers (8-wide
+    // columns at both edges, first / last row) in the unused multiplier area
+    static constexpr int O_HUP = O_A, O_HDN = O_A + 128, O_HL = O_A + 256, O_HR = O_HL + 16 * TH;
+    static constexpr int O_AL = O_HR + 16 * TH, O_AR = O_AL + 16 * TH;
+    static constexpr int O_AT = O_AR + 16 * TH, O_AB = O_AT + 2 * TW;
+    static_assert(O_AB + 2 * TW <= O_Y, "clean boxes fit the multiplier area");
+    static constexpr int TX_CLEAN = B_Y + B_YR + 2 * TW + 2 * 16 * TH + 2 * 16 * TH + 2 * 2 * TW;
     static constexpr int STAGES = STAGES_;
     static constexpr int SMEM = STAGES * STAGE + 128;
 };
@@ -83,16 +99,32 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
 
 template <int TW>
 __device__ __forceinline__ void tma_issue_tile(const Lat2 &L, const TmaMaps &M, uint8_t *stage,
-                                               uint64_t *bar, int by, int bx, int tile, int cur, int p) {
+                                               uint64_t *bar, int by, int bx, int tile, int cur,
+                                               bool solved) {
     using C = TmaCfg<TW>;   // box geometry does not depend on NT / STAGES
     const int x0 = bx * TW;                       // uniform tiling: lo = index * width
     const int y0 = by * L.ay.base + tile * C::TH;
-    mbar_expect_tx(bar, C::TX);
-    tma_load_2d(stage + C::O_A, &M.a[p], bar, x0, y0);
-    // y / labels maps start at the ghost row above the shard: +1 row
-    tma_load_2d(stage + C::O_Y, &M.y[cur], bar, x0, y0 + 1);
-    tma_load_2d(stage + C::O_YR, &M.yr[cur], bar, x0 + TW, y0 + 1);
-    tma_load_2d(stage + C::O_H, &M.yhat, bar, x0 - 16, y0);
+    // y2 / label maps start at the ghost row above the shard: +1 row
+    if (solved) {
+        mbar_expect_tx(bar, C::TX);
+        tma_load_2d(stage + C::O_A, &M.a, bar, x0, y0);
+        tma_load_2d(stage + C::O_Y, &M.y[cur], bar, x0, y0 + 1);
+        tma_load_2d(stage + C::O_YR, &M.yr[cur], bar, x0 + TW, y0 + 1);
+        tma_load_2d(stage + C::O_H, &M.yhat, bar, x0 - 16, y0);
+    } else {
+        // out-of-range boxes (grid edges) are zero-filled and still counted
+        mbar_expect_tx(bar, C::TX_CLEAN);
+        tma_load_2d(stage + C::O_Y, &M.y[cur], bar, x0, y0 + 1);
+        tma_load_2d(stage + C::O_YR, &M.yr[cur], bar, x0 + TW, y0 + 1);
+        tma_load_2d(stage + C::O_HUP, &M.hrow, bar, x0, y0);
+        tma_load_2d(stage + C::O_HDN, &M.hrow, bar, x0, y0 + C::TH + 1);
+        tma_load_2d(stage + C::O_HL, &M.hcol, bar, x0 - 16, y0 + 1);
+        tma_load_2d(stage + C::O_HR, &M.hcol, bar, x0 + TW, y0 + 1);
+        tma_load_2d(stage + C::O_AL, &M.acol, bar, x0, y0);
+        tma_load_2d(stage + C::O_AR, &M.acol, bar, x0 + TW - 8, y0);
+        tma_load_2d(stage + C::O_AT, &M.arow, bar, x0, y0);
+        tma_load_2d(stage + C::O_AB, &M.arow, bar, x0, y0 + C::TH - 1);
+    }
 }
 
 // 4 bytes (each 0 or 1) -> 4 bits
@@ -125,69 +157,201 @@ __device__ __forceinline__ uint32_t quad_update(uint32_t h4, uint2 a2, uint32_t 
     return (uint32_t)(y0 | (y1 << 1) | (y2 << 2) | (y3 << 3));
 }
 
+// Stage descriptor written by the producer before it arms the stage's barrier
+// (the arrive has release semantics; consumers read it after the wait).
+struct StageInfo {
+    int k;          // block id, or -1: no more work
+    int tile;       // tile index within the block
+    int flags;      // bit0 re-solved this iteration, bit1 interior clamp memo, bit2 last tile
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Warp-specialised: NT consumer threads compute, one producer warp (lane 0)
+// claims blocks, issues the TMA loads, and drains each finished block's
+// partials -- consumers never wait on a CTA-wide barrier, only on their
+// stage's "full" mbarrier; the producer waits on the stage's "empty" one.
+// Block scheduling is static round-robin by default (dyn = 0) or a
+// pass-wide claim counter (dyn = 1).  Every pass-wide aggregate is an exact
+// integer (the residual sum included, see rsq_excess), so results do not
+// depend on which CTA took a block.
 template <int TW, int NT_, int STAGES_>
-__global__ void __launch_bounds__(NT_, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 1))) k_consensus_tma(Lat2 L, const __grid_constant__ TmaMaps M,
-                                                          uint32_t kx_magic) {
+__global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 1)))
+    k_consensus_tma(Lat2 L, const __grid_constant__ TmaMaps M, uint32_t kx_magic, int dyn) {
     using C = TmaCfg<TW, NT_, STAGES_>;
     constexpr int TH = C::TH, NT = C::NT, QPT = C::QPT, QR = TW / 4, LQ = (TW == 64) ? 4 : 5;
+    constexpr int ST = C::STAGES;
     extern __shared__ __align__(128) uint8_t smem_t[];
     // keep the shared address space visible to the compiler (LDS, not generic LD)
     uint8_t *base = smem_t + ((128u - (smem_u32(smem_t) & 127u)) & 127u);
-    __shared__ __align__(8) uint64_t full[C::STAGES];
-    __shared__ int last;
-    // per-block accumulators, double-buffered by block parity: warps add into
-    // acc[kb & 1] before the block's last barrier, thread 0 drains it after
-    __shared__ unsigned long long accU[2];
-    __shared__ unsigned int accE[2], accS[2], accF[2];
+    __shared__ __align__(8) uint64_t full[ST], empty[ST];
+    __shared__ StageInfo sinfo[ST];
+    // per-stage block accumulators (filled at a block's last tile, drained by
+    // the producer before the stage is refilled)
+    __shared__ unsigned long long accU[ST];
+    __shared__ unsigned int accE[ST], accS[ST], accF[ST];
 
     dope_run_state *st = L.st;
     if (st->stop) return;
     const int tid = threadIdx.x, lane = tid & 31;
-    if (L.timeline && tid == 0) {   // diagnostics: CTA start (slot 6 of entry blockIdx)
-        uint64_t t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        L.timeline[8 * blockIdx.x + 6] = (int64_t)t;
-    }
     const int cur = st->ycur, best = st->ybest, out = other_buffer(cur, best);
-    const int p = st->parity;
+    const int iter = st->iteration;
     ystore_t *__restrict__ y_out = L.y2[out];
-    astore_t *__restrict__ a_out = p ? L.a0 : L.a1;
-    const bool want_e = st->iteration >= 1;
-    const int32_t W = L.W, H = L.ay.dim, q = L.q, BH = L.ay.base, KX = L.ax.k;
+    astore_t *a_out = L.a;   // in place
+    const bool want_e = iter >= 1;
+    const int32_t W = L.W, H = L.ay.dim, q = L.q, BH = L.ay.base, KX = L.ax.k, K = L.K;
     const int q4 = 4 * q;
     const int tpb = BH / TH;                          // tiles per block
-    const int G0 = gridDim.x;
-    const int nblk = (L.K - (int)blockIdx.x + G0 - 1) / G0;
-    const int ntiles = nblk * tpb;
-    auto coords = [&](int kb, int &by, int &bx) {
-        const int k = blockIdx.x + kb * G0;
-        by = (int)__umulhi((uint32_t)k, kx_magic);
-        bx = k - by * KX;
-    };
 
-    int ikb = 0, itile = 0;
-    // thread 0: this CTA's pass aggregates (blocks in a fixed order)
-    int64_t cE = 0, cU = 0, cM = -1;
-    double cR = 0.0;
-    int cF = 0;
-    if (tid < 2) {
-        accU[tid] = 0;
-        accE[tid] = 0;
-        accS[tid] = 0;
-        accF[tid] = 0;
-    }
-    if (tid == 0) {
-        for (int s = 0; s < C::STAGES; ++s) mbar_init(&full[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int i = 0; i < C::STAGES && i < ntiles; ++i) {
-            int by, bx;
-            coords(ikb, by, bx);
-            tma_issue_tile<TW>(L, M, base + i * C::STAGE, &full[i], by, bx, itile, cur, p);
-            if (++itile == tpb) { itile = 0; ++ikb; }
+    if (tid == NT) {
+        if (L.timeline) {   // diagnostics: CTA start (slot 6 of entry blockIdx)
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            L.timeline[8 * blockIdx.x + 6] = (int64_t)t;
         }
+        for (int i = 0; i < ST; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], NT / 32);
+            accU[i] = 0;
+            accE[i] = 0;
+            accS[i] = 0;
+            accF[i] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
+    if (tid >= NT) {
+        // ================= producer warp =================
+        if (tid != NT) return;
+        unsigned long long *work = reinterpret_cast<unsigned long long *>(&L.pc[6]);
+        constexpr int CA = 3;                          // blocks claimed ahead
+        int nk[CA] = {};
+        uint32_t nep[CA] = {};
+        int nmemo[CA] = {};
+        int nstatic = 0;
+        auto claim = [&]() -> int {
+            if (!dyn) return (int)blockIdx.x + (nstatic++) * (int)gridDim.x;
+            return (int)atomicAdd(work, 1ull);
+        };
+#pragma unroll
+        for (int i = 0; i < CA; ++i) nk[i] = (i == 0 || nk[i - 1] < K) ? claim() : K;
+#pragma unroll
+        for (int i = 0; i + 1 < CA; ++i)
+            if (nk[i] < K) {
+                nep[i] = L.dirty[K + nk[i]];
+                nmemo[i] = L.pf[nk[i]];
+            }
+        // this CTA's pass aggregates (exact integers)
+        int64_t cE = 0, cU = 0, cM = -1, cS = 0, cX = 0;
+        int cF = 0;
+        auto drain = [&](int s) {
+            const StageInfo info = sinfo[s];
+            if (!(info.flags & 4)) return;
+            const int k = info.k;
+            const int64_t e = (int64_t)L.lamw * accE[s];
+            const int64_t u2 = (int64_t)accU[s];
+            const int64_t sq = accS[s];
+            const unsigned f = accF[s];
+            accE[s] = 0;
+            accS[s] = 0;
+            accF[s] = 0;
+            accU[s] = 0;
+            const bool memo = (info.flags & 1) ? (f & 64u) != 0 : (info.flags & 2) != 0;
+            const int clamped = ((f & 1u) || memo) ? 1 : 0;
+            L.pe[k] = e;
+            L.pu[k] = u2;
+            L.pr[k] = sq;
+            L.pf[k] = clamped | (memo ? 64 : 0);
+            cE += e;
+            cU += u2;
+            cM = sq > cM ? sq : cM;
+            cS += sq;
+            cX += rsq_excess(sq);
+            cF |= clamped;
+            if (f & 2u) L.dirty[k] = 1u;
+            if (f & 4u) L.dirty[k - 1] = 1u;
+            if (f & 8u) L.dirty[k + 1] = 1u;
+            if ((f & 16u) && k - KX >= 0) L.dirty[k - KX] = 1u;
+            if ((f & 32u) && k + KX < K) L.dirty[k + KX] = 1u;
+        };
+        int pk = -1, ptile = tpb, pflags = 0;
+        int n = 0;
+        for (;; ++n) {
+            const int s = n % ST;
+            if (n >= ST) {
+                mbar_wait(&empty[s], ((n / ST) - 1) & 1);
+                drain(s);
+            }
+            if (ptile == tpb) {   // next block
+                if (nk[0] >= K) {
+                    sinfo[s].k = -1;
+                    mbar_arrive(&full[s]);
+                    break;
+                }
+                pk = nk[0];
+                pflags = ((!L.skip_clean || nep[0] == (uint32_t)(iter + 1)) ? 1 : 0) | ((nmemo[0] & 64) ? 2 : 0);
+                ptile = 0;
+#pragma unroll
+                for (int i = 0; i + 1 < CA; ++i) {
+                    nk[i] = nk[i + 1];
+                    nep[i] = nep[i + 1];
+                    nmemo[i] = nmemo[i + 1];
+                }
+                if (nk[CA - 2] < K) {   // claimed last time: its claim has returned
+                    nep[CA - 2] = L.dirty[K + nk[CA - 2]];
+                    nmemo[CA - 2] = L.pf[nk[CA - 2]];
+                }
+                nk[CA - 1] = nk[CA - 2] < K ? claim() : K;
+            }
+            sinfo[s].k = pk;
+            sinfo[s].tile = ptile;
+            sinfo[s].flags = pflags | (ptile == tpb - 1 ? 4 : 0);
+            const int by = (int)__umulhi((uint32_t)pk, kx_magic), bx = pk - by * KX;
+            tma_issue_tile<TW>(L, M, base + s * C::STAGE, &full[s], by, bx, ptile, cur, pflags & 1);
+            ++ptile;
+        }
+        // drain the stages still in flight when the end marker went out
+        for (int m = (n - ST + 1 > 0 ? n - ST + 1 : 0); m < n; ++m) {
+            const int s = m % ST;
+            mbar_wait(&empty[s], (m / ST) & 1);
+            drain(s);
+        }
+        // fold this CTA's aggregates into the pass-wide ones (exact integer atomics)
+        if (cE) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[0]), (unsigned long long)cE);
+        if (cU) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[1]), (unsigned long long)cU);
+        if (cM >= 0) atomicMax(reinterpret_cast<unsigned long long *>(&L.pc[2]), (unsigned long long)(cM + 1));
+        if (cF) atomicOr(reinterpret_cast<unsigned long long *>(&L.pc[3]), 1ull);
+        if (cS) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[4]), (unsigned long long)cS);
+        if (cX) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[5]), (unsigned long long)cX);
+        if (L.timeline) {   // diagnostics: CTA end (slot 7)
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            L.timeline[8 * blockIdx.x + 7] = (int64_t)t;
+        }
+        __threadfence();
+        if (atomicAdd(&st->done_ctas, 1) == (int)gridDim.x - 1) {
+            // last CTA: apply the pass
+            __threadfence();
+            const dope_run_state s0 = *st;
+            const int64_t E2 = __ldcg(&L.pc[0]), U2 = __ldcg(&L.pc[1]), M2 = __ldcg(&L.pc[2]) - 1;
+            const int F2 = (int)__ldcg(&L.pc[3]);
+            const double R2 = rsq_total(__ldcg(&L.pc[4]), __ldcg(&L.pc[5]));
+            for (int i = 0; i < 8; ++i) L.pc[i] = 0;   // incl. the claim counter
+            finalize_apply(L, s0, E2, U2, R2, M2, F2, cur, best, out);
+            st->done_ctas = 0;
+            if (L.timeline && (int)gridDim.x < L.K) {   // diagnostics: finalize end
+                uint64_t t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                L.timeline[8 * gridDim.x + 7] = (int64_t)t;
+            }
+        }
+        return;
+    }
+
+    // ================= consumer warps =================
     int rr_[QPT], c0_[QPT];
 #pragma unroll
     for (int j = 0; j < QPT; ++j) {
@@ -195,21 +359,24 @@ __global__ void __launch_bounds__(NT_, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 1))) 
         rr_[j] = t >> LQ;
         c0_[j] = (t & (QR - 1)) << 2;
     }
-
-    int s = 0;
-    uint32_t phase = 0;
-    for (int kb = 0; kb < nblk; ++kb) {
-        int by, bx;
-        coords(kb, by, bx);
-        const int k = by * KX + bx;
+    int64_t du = 0;
+    int ss = 0, quad_acc = 0;
+    // fl: bit1 self, bit2 left, bit3 right, bit4 up, bit5 down
+    // clp: OR of the pre-clamp values of ring quads, clpi: interior quads
+    uint32_t fl = 0, clp = 0, clpi = 0;
+    for (int n = 0;; ++n) {
+        const int s = n % ST;
+        mbar_wait(&full[s], (n / ST) & 1);
+        const StageInfo info = sinfo[s];
+        if (info.k < 0) break;
+        const int k = info.k, tile = info.tile;
+        const bool solved = info.flags & 1;
+        const int by = (int)__umulhi((uint32_t)k, kx_magic), bx = k - by * KX;
         const int lo_r = by * BH, lo_c = bx * TW;
         const bool has_up = lo_r > 0 || L.gup, has_dn = lo_r + BH < H || L.gdn, has_lf = lo_c > 0,
                    has_rt = lo_c + TW < W;
         const bool last_row_pairs = lo_r + BH < H || L.gdn;   // pairs below the block's last row
-        int64_t du = 0;
-        int ss = 0, quad_acc = 0;
-        uint32_t fl = 0, clp = 0;   // fl: bit1 self, bit2 left, bit3 right, bit4 up, bit5 down
-        for (int tile = 0; tile < tpb; ++tile) {
+        {
             const uint8_t *sb = base + s * C::STAGE;
             const astore_t *sa = reinterpret_cast<const astore_t *>(sb + C::O_A);
             const uint8_t *sy = sb + C::O_Y;
@@ -217,43 +384,33 @@ __global__ void __launch_bounds__(NT_, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 1))) 
             const uint8_t *sh = sb + C::O_H + C::YHW + 16;      // label of tile pixel (0,0)
             const int r0 = tile * TH;
             const int64_t gt = (int64_t)(lo_r + r0) * W + lo_c;   // global index of tile (0,0)
-            mbar_wait(&full[s], phase);
-#pragma unroll
-            for (int j = 0; j < QPT; ++j) {
-                const int rr = rr_[j], c0 = c0_[j];
-                const int r = r0 + rr;                             // row within block
-                const uint2 av = *reinterpret_cast<const uint2 *>(sa + rr * TW + c0);
-                const uint32_t yo = *reinterpret_cast<const uint32_t *>(sy + rr * TW + c0);
-                const uint8_t *hrow = sh + rr * C::YHW + c0;
-                const uint32_t h4 = *reinterpret_cast<const uint32_t *>(hrow);
-                const bool cr = c0 + 4 == TW;
-                if (want_e) {
-                    // E(y_{t-1}) pair terms: bytes are 0/2, so each differing
-                    // pair is exactly one set bit of the XOR
-                    const uint32_t nxt = __shfl_down_sync(FULLMASK, yo, 1);
-                    uint32_t rw = nxt;
-                    if (cr) rw = has_rt ? (uint32_t)syr[rr * 16] : (yo >> 24);
-                    const uint32_t yb = (r + 1 < BH || last_row_pairs)
-                                            ? *reinterpret_cast<const uint32_t *>(sy + (rr + 1) * TW + c0)
-                                            : yo;
-                    quad_acc += __popc(yo ^ __funnelshift_r(yo, rw, 8)) + __popc(yo ^ yb);
-                }
-                // cross-block neighbours of this quad
-                const bool lft = (c0 == 0) && has_lf, rgt = cr && has_rt;
-                const bool top = (r == 0) && has_up, bot = (r == BH - 1) && has_dn;
-                uint32_t cnt = 0, nb = 0;
-                if (top) { cnt += 0x01010101u; nb += *reinterpret_cast<const uint32_t *>(hrow - C::YHW); }
-                if (bot) { cnt += 0x01010101u; nb += *reinterpret_cast<const uint32_t *>(hrow + C::YHW); }
-                if (lft) { cnt += 1u; nb += hrow[-1]; }
-                if (rgt) { cnt += 1u << 24; nb += (uint32_t)hrow[4] << 24; }
+            // E(y_{t-1}) pair terms of one quad: bytes are 0/2, so each
+            // differing pair is exactly one set bit of the XOR (all lanes call
+            // this together: the right neighbour comes from the next lane)
+            auto pair_energy = [&](int rr, int c0, uint32_t yo) {
+                const uint32_t nxt = __shfl_down_sync(FULLMASK, yo, 1);
+                uint32_t rw = nxt;
+                if (c0 + 4 == TW) rw = has_rt ? (uint32_t)syr[rr * 16] : (yo >> 24);
+                const uint32_t yb = (r0 + rr + 1 < BH || last_row_pairs)
+                                        ? *reinterpret_cast<const uint32_t *>(sy + (rr + 1) * TW + c0)
+                                        : yo;
+                quad_acc += __popc(yo ^ __funnelshift_r(yo, rw, 8)) + __popc(yo ^ yb);
+            };
+            // consensus update of one quad given its multipliers, own labels
+            // and cross-block neighbour labels (count / sum per pixel)
+            auto update = [&](int rr, int c0, uint32_t yo, uint32_t h4, uint2 av, uint32_t cnt, uint32_t nb,
+                              bool lft, bool rgt, bool top, bool bot, bool ring) {
+                const int64_t G = gt + (int64_t)rr * W + c0;
                 uint2 an;
-                const uint32_t yn = quad_update(h4, av, cnt, nb, q, q4, an, clp);
+                uint32_t cq = 0;
+                const uint32_t yn = quad_update(h4, av, cnt, nb, q, q4, an, cq);
+                if (ring) clp |= cq;
+                else clpi |= cq;
                 const uint32_t hb = bits_b01(h4);
                 ss += __popc(hb ^ yn);
                 const uint32_t yw = bytes_b01(yn) << 1;            // y2 bytes 0/2
                 const uint32_t chg = yw ^ yo;
                 fl |= (chg | (hb ^ yn)) ? 2u : 0u;
-                const int64_t G = gt + (int64_t)rr * W + c0;
                 __stcs(reinterpret_cast<uint2 *>(a_out + G), an);
                 __stcg(reinterpret_cast<unsigned int *>(y_out + G), yw);
                 if (chg) {
@@ -267,117 +424,90 @@ __global__ void __launch_bounds__(NT_, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 1))) 
                     const uint32_t mk = 0x30u | ((chg & 0xFFu) ? 4u : 0u) | ((chg >> 24) ? 8u : 0u);
                     fl |= em & mk;
                 }
-            }
-            const int ab = kb & 1;
-            if (tile == tpb - 1) {
-                // block done in this warp: one shared atomic per quantity
-                const unsigned e = __reduce_add_sync(FULLMASK, (unsigned)quad_acc);
-                const unsigned sq = __reduce_add_sync(FULLMASK, (unsigned)ss);
-                const unsigned f = __reduce_or_sync(FULLMASK, fl | (clp > 1u ? 1u : 0u));
-                int64_t u2 = 0;
-                if (__any_sync(FULLMASK, du != 0)) u2 = warp_sum(du);
-                if (lane == 0) {
-                    if (e) atomicAdd(&accE[ab], e);
-                    if (sq) atomicAdd(&accS[ab], sq);
-                    if (f) atomicOr(&accF[ab], f);
-                    if (u2) atomicAdd(&accU[ab], (unsigned long long)u2);
+            };
+            if (solved) {
+#pragma unroll
+                for (int j = 0; j < QPT; ++j) {
+                    const int rr = rr_[j], c0 = c0_[j];
+                    const int r = r0 + rr;                         // row within block
+                    const uint32_t yo = *reinterpret_cast<const uint32_t *>(sy + rr * TW + c0);
+                    if (want_e) pair_energy(rr, c0, yo);
+                    const bool lft = (c0 == 0) && has_lf, rgt = (c0 + 4 == TW) && has_rt;
+                    const bool top = (r == 0) && has_up, bot = (r == BH - 1) && has_dn;
+                    const uint8_t *hrow = sh + rr * C::YHW + c0;
+                    const uint2 av = *reinterpret_cast<const uint2 *>(sa + rr * TW + c0);
+                    const uint32_t h4 = *reinterpret_cast<const uint32_t *>(hrow);
+                    uint32_t cnt = 0, nb = 0;
+                    if (top) { cnt += 0x01010101u; nb += *reinterpret_cast<const uint32_t *>(hrow - C::YHW); }
+                    if (bot) { cnt += 0x01010101u; nb += *reinterpret_cast<const uint32_t *>(hrow + C::YHW); }
+                    if (lft) { cnt += 1u; nb += hrow[-1]; }
+                    if (rgt) { cnt += 1u << 24; nb += (uint32_t)hrow[4] << 24; }
+                    update(rr, c0, yo, h4, av, cnt, nb, lft, rgt, top, bot, lft | rgt | top | bot);
+                }
+            } else {
+                // clean block: the interior is a fixed point, so the bulk pass
+                // only carries y into the rotating buffer (and the energy); the
+                // ring quads -- the only ones a neighbour's new labels can move
+                // -- are updated in a second pass spread over all threads
+                const bool tile_top = tile == 0 && has_up, tile_bot = tile == tpb - 1 && has_dn;
+#pragma unroll
+                for (int j = 0; j < QPT; ++j) {
+                    const int rr = rr_[j], c0 = c0_[j];
+                    const uint32_t yo = *reinterpret_cast<const uint32_t *>(sy + rr * TW + c0);
+                    if (want_e) pair_energy(rr, c0, yo);
+                    const bool ring = (c0 == 0 && has_lf) || (c0 + 4 == TW && has_rt) || (rr == 0 && tile_top) ||
+                                      (rr == TH - 1 && tile_bot);
+                    if (!ring) __stcg(reinterpret_cast<unsigned int *>(y_out + gt + (int64_t)rr * W + c0), yo);
+                }
+                // ring candidates: first and last tile row, then the edge
+                // quads of the rows in between
+                constexpr int NCAND = 2 * QR + 2 * (TH - 2);
+                for (int i = tid; i < NCAND; i += NT) {
+                    int rr, c0;
+                    if (i < QR) { rr = 0; c0 = 4 * i; }
+                    else if (i < 2 * QR) { rr = TH - 1; c0 = 4 * (i - QR); }
+                    else { const int jj = i - 2 * QR; rr = 1 + (jj >> 1); c0 = (jj & 1) ? TW - 4 : 0; }
+                    const bool lft = (c0 == 0) && has_lf, rgt = (c0 + 4 == TW) && has_rt;
+                    const bool top = rr == 0 && tile_top, bot = rr == TH - 1 && tile_bot;
+                    if (!(lft | rgt | top | bot)) continue;
+                    const uint32_t yo = *reinterpret_cast<const uint32_t *>(sy + rr * TW + c0);
+                    uint2 av;
+                    if (lft) av = *reinterpret_cast<const uint2 *>(sb + C::O_AL + rr * 16);
+                    else if (rgt) av = *reinterpret_cast<const uint2 *>(sb + C::O_AR + rr * 16 + 8);
+                    else if (top) av = *reinterpret_cast<const uint2 *>(sb + C::O_AT + 2 * c0);
+                    else av = *reinterpret_cast<const uint2 *>(sb + C::O_AB + 2 * c0);
+                    const uint32_t h4 = yo >> 1;                   // own labels == y2 / 2
+                    uint32_t cnt = 0, nb = 0;
+                    if (top) { cnt += 0x01010101u; nb += *reinterpret_cast<const uint32_t *>(sb + C::O_HUP + c0); }
+                    if (bot) { cnt += 0x01010101u; nb += *reinterpret_cast<const uint32_t *>(sb + C::O_HDN + c0); }
+                    if (lft) { cnt += 1u; nb += sb[C::O_HL + rr * 16 + 15]; }
+                    if (rgt) { cnt += 1u << 24; nb += (uint32_t)sb[C::O_HR + rr * 16] << 24; }
+                    update(rr, c0, yo, h4, av, cnt, nb, lft, rgt, top, bot, true);
                 }
             }
-            // every warp is done with stage s: refill it with the tile STAGES ahead
-            __syncthreads();
-            if (tid == 0) {
-                if (ikb < nblk) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    int by2, bx2;
-                    coords(ikb, by2, bx2);
-                    tma_issue_tile<TW>(L, M, base + s * C::STAGE, &full[s], by2, bx2, itile, cur, p);
-                    if (++itile == tpb) { itile = 0; ++ikb; }
-                }
-                if (tile == tpb - 1) {
-                    // drain block k: per-block partials (diagnostics / step API
-                    // parity), dirty marks, and this CTA's running aggregates
-                    const int64_t e = (int64_t)L.lamw * accE[ab];
-                    const int64_t u2 = (int64_t)accU[ab];
-                    const int64_t sq = accS[ab];
-                    const unsigned f = accF[ab];
-                    accE[ab] = 0;
-                    accS[ab] = 0;
-                    accF[ab] = 0;
-                    accU[ab] = 0;
-                    L.pe[k] = e;
-                    L.pu[k] = u2;
-                    L.pr[k] = sq;
-                    L.pf[k] = (int)(f & 1u);
-                    cE += e;
-                    cU += u2;
-                    cM = sq > cM ? sq : cM;
-                    const double r = sqrt((double)sq);
-                    cR += r * r;
-                    cF |= (int)(f & 1u);
-                    if (f & 2u) L.dirty[k] = 1u;
-                    if (f & 4u) L.dirty[k - 1] = 1u;
-                    if (f & 8u) L.dirty[k + 1] = 1u;
-                    if ((f & 16u) && k - KX >= 0) L.dirty[k - KX] = 1u;
-                    if ((f & 32u) && k + KX < L.K) L.dirty[k + KX] = 1u;
-                }
+        }
+        if (info.flags & 4) {
+            // block done in this warp: one shared atomic per quantity
+            const unsigned e = __reduce_add_sync(FULLMASK, (unsigned)quad_acc);
+            const unsigned sq = __reduce_add_sync(FULLMASK, (unsigned)ss);
+            const unsigned f = __reduce_or_sync(FULLMASK, fl | (clp > 1u ? 1u : 0u) | (clpi > 1u ? 64u : 0u));
+            int64_t u2 = 0;
+            if (__any_sync(FULLMASK, du != 0)) u2 = warp_sum(du);
+            if (lane == 0) {
+                if (e) atomicAdd(&accE[s], e);
+                if (sq) atomicAdd(&accS[s], sq);
+                if (f) atomicOr(&accF[s], f);
+                if (u2) atomicAdd(&accU[s], (unsigned long long)u2);
             }
-            if (++s == C::STAGES) { s = 0; phase ^= 1u; }
+            du = 0;
+            ss = 0;
+            quad_acc = 0;
+            fl = 0;
+            clp = 0;
+            clpi = 0;
         }
-    }
-    // fold this CTA's aggregates into the pass-wide ones (exact integer
-    // atomics; the float residual sum per CTA, for the last CTA to add up by
-    // CTA index -- deterministic)
-    // this CTA's blocks are complete: fold their partials into the pass-wide
-    // aggregates (exact integer atomics; the float residual sum per CTA, in a
-    // fixed order, for the last CTA to add up by CTA index)
-    if (tid == 0) {
-        atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[0]), (unsigned long long)cE);
-        atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[1]), (unsigned long long)cU);
-        atomicMax(reinterpret_cast<unsigned long long *>(&L.pc[2]), (unsigned long long)(cM + 1));
-        if (cF) atomicOr(reinterpret_cast<unsigned long long *>(&L.pc[3]), 1ull);
-        L.pc[8 + blockIdx.x] = __double_as_longlong(cR);
-        if (L.timeline) {   // diagnostics: CTA end (slot 7)
-            uint64_t t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            L.timeline[8 * blockIdx.x + 7] = (int64_t)t;
-        }
-        __threadfence();
-        const int prev = atomicAdd(&st->done_ctas, 1);
-        last = (prev == (int)gridDim.x - 1);
-    }
-    __syncthreads();
-    if (last) {
-        __threadfence();
-        dope_run_state s0;
-        int64_t E2 = 0, U2 = 0, M2 = 0, F2 = 0;
-        if (tid == 0) {   // in flight together with the residual loads
-            s0 = *st;
-            E2 = __ldcg(&L.pc[0]);
-            U2 = __ldcg(&L.pc[1]);
-            M2 = __ldcg(&L.pc[2]) - 1;
-            F2 = __ldcg(&L.pc[3]);
-        }
-        // residual sum over CTAs in index order (deterministic)
-        __shared__ double sR[NT_ / 32];
-        double R = 0.0;
-        for (int i = tid; i < (int)gridDim.x; i += NT) R += __longlong_as_double(__ldcg(&L.pc[8 + i]));
-        for (int o = 16; o > 0; o >>= 1) R += __shfl_xor_sync(FULLMASK, R, o);
-        if (lane == 0) sR[tid >> 5] = R;
-        __syncthreads();
-        if (tid == 0) {
-            double R2 = 0.0;
-            for (int w = 0; w < NT / 32; ++w) R2 += sR[w];
-            L.pc[0] = 0;
-            L.pc[1] = 0;
-            L.pc[2] = 0;
-            L.pc[3] = 0;
-            finalize_apply(L, s0, E2, U2, R2, M2, (int)F2, cur, best, out);
-            st->done_ctas = 0;
-            if (L.timeline && (int)gridDim.x < L.K) {   // diagnostics: finalize end
-                uint64_t t;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                L.timeline[8 * gridDim.x + 7] = (int64_t)t;
-            }
-        }
+        // this warp is done with stage s
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
     }
 }

@@ -54,13 +54,14 @@ struct Lat2 {
     int32_t warm, skip_clean, fuse;
     double eps;
     const int32_t *u;
-    astore_t *a0, *a1;
+    astore_t *a;            // multipliers, updated in place
     ystore_t *y2[3];       // rotating iterates: st.ycur (current), st.ybest (best)
     uint8_t *yhat, *resid;
     uint32_t *dirty;
     int64_t *pe, *pr, *pu;
     int32_t *pf;
-    int64_t *pc;   // [0] E, [1] U, [2] M2 + 1 (max), [3] F (or), [8 + cta] R2 bits
+    int64_t *pc;   // [0] E, [1] U, [2] M2 + 1 (max), [3] F (or), [4] sum ss, [5] sum rsq_excess,
+                   // [6] block claim counter of the persistent consensus pass
     dope_run_state *st;
     int64_t *tr_e;
     double *tr_rs, *tr_mr;
@@ -128,17 +129,14 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
         L.timeline[8 * k + 5] = (int64_t)t_begin;
     }
     if (L.st->stop) return;
-    if (tid == 0) {   // this iteration's consensus partials (the TMA pass accumulates)
-        L.pe[k] = 0;
-        L.pu[k] = 0;
-        L.pr[k] = 0;
-        L.pf[k] = 0;
-    }
     if (L.skip_clean) {
         if (L.dirty[k] == 0) return;
     }
     __syncthreads();
-    if (tid == 0) L.dirty[k] = 0;
+    if (tid == 0) {
+        L.dirty[k] = 0;
+        L.dirty[L.K + k] = (uint32_t)L.st->iteration + 1u;   // solve epoch (consensus fast path)
+    }
 
     const int by = k / L.ax.k, bx = k % L.ax.k;
     int32_t lo_r, hr, lo_c, wc;
@@ -146,7 +144,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
     L.ax.range(bx, lo_c, wc);
     const int32_t Wg = L.W;
     const int32_t cap = L.cap;
-    const astore_t *__restrict__ a_cur = L.st->parity ? L.a1 : L.a0;
+    const astore_t *__restrict__ a_cur = L.a;
     const ystore_t *__restrict__ y_cur = L.y2[L.st->ycur];
     uint8_t *gres = L.resid + (size_t)k * 4 * M;
 
@@ -421,8 +419,7 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         L.y2[0][i] = 1;              // y = 1/2 (admm.py:163-164); best_y = copy
-        L.a0[i] = 0;
-        L.a1[i] = 0;
+        L.a[i] = 0;
         L.yhat[i] = 0;
     }
     if (blockIdx.x == 0 && L.pc)
@@ -546,21 +543,32 @@ __device__ void finalize_apply(const Lat2 &L, dope_run_state s0, int64_t E2, int
     }
 }
 
+// Residual sum of squares, admm.py:295: sum over blocks of fl(fl(sqrt(ss))^2).
+// Each term is ss + e with e an exact multiple of 2^-53 (|e| <= 4 ulp(ss)), so
+// the sum is kept exactly as two integers (sum ss, sum e * 2^53) and rounded
+// once: deterministic whatever order the blocks are visited in.
+__device__ __forceinline__ int64_t rsq_excess(int64_t ss) {
+    const double r = sqrt((double)ss);
+    const double t = __dmul_rn(r, r);                      // fl(r^2), no contraction
+    return (int64_t)((t - (double)ss) * 9007199254740992.0);   // exact (Sterbenz), x 2^53
+}
+__device__ __forceinline__ double rsq_total(int64_t sum_ss, int64_t sum_excess) {
+    return (double)sum_ss + (double)sum_excess * 0x1p-53;
+}
+
 // Reduce per-block partials of the blocks first, first + stride, ... (< K) over
 // the calling CTA: thread-strided, then a fixed shuffle tree and warp order,
 // so the float sum is deterministic.  Result valid in thread 0.
 struct Aggr {
-    int64_t E, U, M;
-    double R;
+    int64_t E, U, M, S, X;
     int F;
 };
 
 __device__ Aggr reduce_blocks(const Lat2 &L, int first, int stride, int count) {
-    __shared__ int64_t sE[32], sU[32], sM[32];
-    __shared__ double sR[32];
+    __shared__ int64_t sE[32], sU[32], sM[32], sS[32], sX[32];
     __shared__ int sF[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    Aggr a{0, 0, -1, 0.0, 0};
+    Aggr a{0, 0, -1, 0, 0, 0};
     // batches of UNR blocks per thread: all loads of a batch are in flight
     // together (a strided loop would pay one L2 round trip per block)
     constexpr int UNR = 8;
@@ -581,32 +589,34 @@ __device__ Aggr reduce_blocks(const Lat2 &L, int first, int stride, int count) {
         for (int j = 0; j < UNR; ++j) {
             a.E += e[j];
             a.U += u[j];
-            a.F |= f[j];
+            a.F |= f[j] & 1;
             if (sq[j] >= 0) {
-                const double r = sqrt((double)sq[j]);
-                a.R += r * r;
+                a.S += sq[j];
+                a.X += rsq_excess(sq[j]);
                 a.M = sq[j] > a.M ? sq[j] : a.M;
             }
         }
     }
     a.E = warp_sum(a.E);
     a.U = warp_sum(a.U);
+    a.S = warp_sum(a.S);
+    a.X = warp_sum(a.X);
     for (int o = 16; o > 0; o >>= 1) {
-        a.R += __shfl_xor_sync(FULLMASK, a.R, o);
         const int64_t t = __shfl_xor_sync(FULLMASK, a.M, o);
         a.M = t > a.M ? t : a.M;
     }
     a.F = __any_sync(FULLMASK, a.F);
     __syncthreads();   // the shared scratch may be reused by consecutive calls
-    if (lane == 0) { sE[warp] = a.E; sU[warp] = a.U; sR[warp] = a.R; sM[warp] = a.M; sF[warp] = a.F; }
+    if (lane == 0) { sE[warp] = a.E; sU[warp] = a.U; sS[warp] = a.S; sX[warp] = a.X; sM[warp] = a.M; sF[warp] = a.F; }
     __syncthreads();
     if (tid == 0) {
-        a = Aggr{0, 0, -1, 0.0, 0};
+        a = Aggr{0, 0, -1, 0, 0, 0};
         const int nw = blockDim.x / 32;
         for (int w = 0; w < nw; ++w) {
             a.E += sE[w];
             a.U += sU[w];
-            a.R += sR[w];
+            a.S += sS[w];
+            a.X += sX[w];
             a.M = sM[w] > a.M ? sM[w] : a.M;
             a.F |= sF[w];
         }
@@ -619,7 +629,7 @@ __device__ void finalize_cta(const Lat2 &L, int cur, int best_idx, int out) {
     dope_run_state s0;
     if (threadIdx.x == 0) s0 = *L.st;   // in flight during the reduction
     const Aggr a = reduce_blocks(L, 0, 1, L.K);
-    if (threadIdx.x == 0) finalize_apply(L, s0, a.E, a.U, a.R, a.M, a.F, cur, best_idx, out);
+    if (threadIdx.x == 0) finalize_apply(L, s0, a.E, a.U, rsq_total(a.S, a.X), a.M, a.F, cur, best_idx, out);
 }
 
 // Sharded mode: apply the all-reduced aggregates (identical on every rank).
@@ -748,9 +758,9 @@ __global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
     const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
     const ystore_t *__restrict__ y_in = L.y2[cur];
     ystore_t *__restrict__ y_out = L.y2[out];
-    const int p = L.st->parity;
-    const astore_t *__restrict__ a_in = p ? L.a1 : L.a0;
-    astore_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
+    // multipliers are updated in place (a_{t+1}[p] depends on a_t[p] only)
+    const astore_t *a_in = L.a;
+    astore_t *a_out = L.fuse ? L.a : nullptr;
     const bool want_e = L.fuse && L.st->iteration >= 1;
     const bool has_up = lo_r > 0 || L.gup, has_dn = lo_r + hr < H || L.gdn, has_lf = lo_c > 0,
                has_rt = lo_c + wc < W;
@@ -817,9 +827,9 @@ __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
     const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
     const ystore_t *__restrict__ y_in = L.y2[cur];
     ystore_t *__restrict__ y_out = L.y2[out];
-    const int p = L.st->parity;
-    const astore_t *__restrict__ a_in = p ? L.a1 : L.a0;
-    astore_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
+    // multipliers are updated in place (a_{t+1}[p] depends on a_t[p] only)
+    const astore_t *a_in = L.a;
+    astore_t *a_out = L.fuse ? L.a : nullptr;
     const bool want_e = L.fuse && L.st->iteration >= 1;
     const int32_t q = L.q;
     const bool has_up = lo_r > 0 || L.gup, has_dn = lo_r + hr < H || L.gdn, has_lf = lo_c > 0,
@@ -917,7 +927,7 @@ __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
 
 // a += yhat - y for the step-level API (admm.py:241-248), in place.
 __global__ void k_update_multipliers(Lat2 L, int64_t n) {
-    astore_t *a = L.st->parity ? L.a1 : L.a0;
+    astore_t *a = L.a;
     const ystore_t *y2 = L.y2[L.st->ycur];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -1052,7 +1062,7 @@ static const Variant3 *pick_variant3(int maxd, int maxh, int maxw) {
 
 static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
                       const Variant3 **var3 = nullptr) {
-    if (!L || !L->u || !L->a[0] || !L->a[1] || !L->y2[0] || !L->y2[1] || !L->y2[2] || !L->yhat || !L->resid ||
+    if (!L || !L->u || !L->a || !L->y2[0] || !L->y2[1] || !L->y2[2] || !L->yhat || !L->resid ||
         !L->dirty || !L->part_energy || !L->part_unary || !L->part_ressq || !L->part_flags || !L->state ||
         (L->ndim == 2 && !L->part_cta))
         return DOPE_E_ARGS;
@@ -1091,8 +1101,7 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
     o.fuse = L->fuse_multipliers;
     o.eps = L->eps;
     o.u = L->u;
-    o.a0 = L->a[0];
-    o.a1 = L->a[1];
+    o.a = L->a;
     o.y2[0] = L->y2[0];
     o.y2[1] = L->y2[1];
     o.y2[2] = L->y2[2];
@@ -1140,7 +1149,7 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
     }
     // quad loads: 4 labels / 4 y2 bytes as one word, 4 multipliers as 8 bytes
     const uintptr_t al = (uintptr_t)o.y2[0] | (uintptr_t)o.y2[1] | (uintptr_t)o.y2[2] | (uintptr_t)o.yhat |
-                         ((uintptr_t)o.a0 >> 1) | ((uintptr_t)o.a1 >> 1) | ((uintptr_t)o.u >> 2);
+                         ((uintptr_t)o.a >> 1) | ((uintptr_t)o.u >> 2);
     o.vec4 = !is3 && (o.W % 4 == 0) && (o.ax.rem == 0) && (o.ax.base % 4 == 0) && (al % 4 == 0);
     return DOPE_OK;
 }
@@ -1271,23 +1280,26 @@ static int launch_k2_tma(const Lat2 &o, cudaStream_t s, int ctas_per_sm) {
     std::call_once(once, [] { k2_tma_attr<TW, NT, ST>(); });
     TmaMaps M;
     const int64_t W = o.W, H = o.ay.dim;
-    bool ok = make_map(&M.a[0], CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, o.a0, W, H, TW, C::TH);
-    ok = ok && make_map(&M.a[1], CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, o.a1, W, H, TW, C::TH);
+    bool ok = make_map(&M.a, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, o.a, W, H, TW, C::TH);
     // y2 and yhat carry one ghost row above and below the shard (caller-owned)
     for (int i = 0; i < 3 && ok; ++i) {
         ok = make_map(&M.y[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.y2[i] - W, W, H + 2, TW, C::TH + 1);
         ok = ok && make_map(&M.yr[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.y2[i] - W, W, H + 2, 16, C::TH);
     }
     ok = ok && make_map(&M.yhat, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.yhat - W, W, H + 2, C::YHW, C::TH + 2);
+    ok = ok && make_map(&M.hrow, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.yhat - W, W, H + 2, TW, 1);
+    ok = ok && make_map(&M.hcol, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.yhat - W, W, H + 2, 16, C::TH);
+    ok = ok && make_map(&M.arow, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, o.a, W, H, TW, 1);
+    ok = ok && make_map(&M.acol, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, o.a, W, H, 8, C::TH);
     if (!ok) {
         snprintf(g_last_err, sizeof(g_last_err), "cuTensorMapEncodeTiled failed");
         return DOPE_E_CUDA;
     }
     int grid = ctas_per_sm * sm_count();
-    grid = grid < DOPE_PART_CTA_LEN - 8 ? grid : DOPE_PART_CTA_LEN - 8;   // one residual slot per CTA
     grid = o.K < grid ? o.K : grid;
     const uint32_t magic = (uint32_t)(((1ull << 32) + o.ax.k - 1) / o.ax.k);
-    k_consensus_tma<TW, NT, ST><<<grid, C::NT, C::SMEM, s>>>(o, M, magic);
+    static const int dyn = getenv("DOPE_K2_DYNAMIC") ? 1 : 0;
+    k_consensus_tma<TW, NT, ST><<<grid, C::NT + 32, C::SMEM, s>>>(o, M, magic, dyn);
     return cuda_check(cudaGetLastError(), "launch K2 (tma)");
 }
 
@@ -1300,7 +1312,7 @@ static int k2_tma_width(const Lat2 &o) {
     if (!o.fuse || o.ax.rem != 0 || o.ay.rem != 0 || (o.W % 16) != 0 || o.ndim != 2) return 0;
     // TMA global addresses must be 16-byte aligned (y2 / yhat maps start one row up)
     const uintptr_t al = (uintptr_t)(o.y2[0] - o.W) | (uintptr_t)(o.y2[1] - o.W) | (uintptr_t)(o.y2[2] - o.W) |
-                         (uintptr_t)(o.yhat - o.W) | (uintptr_t)o.a0 | (uintptr_t)o.a1;
+                         (uintptr_t)(o.yhat - o.W) | (uintptr_t)o.a;
     if (al % 16 != 0 || !o.vec4) return 0;
     if (o.ax.base == 64 && o.ay.base % 64 == 0) return 64;
     if (o.ax.base == 128 && o.ay.base % 32 == 0) return 128;
@@ -1319,13 +1331,13 @@ static int launch_k2(const Lat2 &o, cudaStream_t s) {
         // (Little's law) for a kernel that moves ~7 B per pixel
         if (tw == 64) {
             switch (variant) {
-                case 1: return launch_k2_tma<64, 512, 4>(o, s, 1);
-                case 2: return launch_k2_tma<64, 512, 8>(o, s, 1);
-                case 3: return launch_k2_tma<64, 256, 4>(o, s, 2);
-                case 4: return launch_k2_tma<64, 128, 3>(o, s, 3);
-                case 5: return launch_k2_tma<64, 256, 3>(o, s, 2);
-                case 6: return launch_k2_tma<64, 128, 4>(o, s, 2);
-                case 7: return launch_k2_tma<64, 256, 5>(o, s, 2);
+                case 1: return launch_k2_tma<64, 128, 3>(o, s, 3);
+                case 2: return launch_k2_tma<64, 128, 4>(o, s, 2);
+                case 3: return launch_k2_tma<64, 256, 2>(o, s, 2);
+                case 4: return launch_k2_tma<64, 256, 3>(o, s, 2);
+                case 5: return launch_k2_tma<64, 128, 2>(o, s, 5);
+                case 6: return launch_k2_tma<64, 512, 4>(o, s, 1);
+                case 7: return launch_k2_tma<64, 128, 3>(o, s, 2);
                 default: return launch_k2_tma<64, K2_NT, K2_STAGES>(o, s, K2_CPS);
             }
         }

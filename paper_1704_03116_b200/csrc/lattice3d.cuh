@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut3d(Lat2 L, K1Tune T) {
     const int32_t W = L.W, H = L.ay.dim, D = L.az.dim;
     const int64_t HW = (int64_t)H * W;
     const int32_t cap = L.cap;
-    const astore_t *__restrict__ a_cur = L.st->parity ? L.a1 : L.a0;
+    const astore_t *__restrict__ a_cur = L.a;
     const ystore_t *__restrict__ y_cur = L.y2[L.st->ycur];
     int32_t *g = reinterpret_cast<int32_t *>(L.scratch + (size_t)k * 6 * M);
     uint16_t *h = reinterpret_cast<uint16_t *>(g + M);
@@ -239,9 +239,9 @@ __global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
     const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
     const ystore_t *__restrict__ y_in = L.y2[cur];
     ystore_t *__restrict__ y_out = L.y2[out];
-    const int p = L.st->parity;
-    const astore_t *__restrict__ a_in = p ? L.a1 : L.a0;
-    astore_t *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
+    // multipliers are updated in place (a_{t+1}[p] depends on a_t[p] only)
+    const astore_t *a_in = L.a;
+    astore_t *a_out = L.fuse ? L.a : nullptr;
     const bool want_e = L.fuse && L.st->iteration >= 1;
     const bool up_z = gb.lo_z > 0, dn_z = gb.lo_z + gb.dz < D;
     const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
