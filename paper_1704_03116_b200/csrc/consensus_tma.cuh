@@ -34,11 +34,13 @@ struct TmaMaps {
 // labels just across the block boundary are streamed (its own labels equal
 // y2 / 2); ring multipliers are read directly.
 // u is never streamed: the unary energy is kept incrementally.
-template <int TW, int NT_ = 512, int STAGES_ = 3>
+template <int TW, int TH_, int NT_ = 128, int STAGES_ = 8>
 struct TmaCfg {
-    static constexpr int TH = 4096 / TW;                 // tile rows (64 or 32)
+    static constexpr int TH = TH_;                       // tile rows
     static constexpr int NT = NT_;
     static constexpr int QPT = TH * TW / 4 / NT;         // quads per thread
+    static_assert(QPT >= 1 && QPT * NT * 4 == TH * TW, "whole quads per thread");
+    static_assert(TH % 8 == 0, "128-byte aligned clean boxes");
     static constexpr int YHW = TW + 32;                  // label box width (bytes)
     static constexpr int B_A = TW * TH * 2;
     static constexpr int B_Y = TW * (TH + 1);
@@ -97,11 +99,11 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
-template <int TW>
+template <int TW, int TH>
 __device__ __forceinline__ void tma_issue_tile(const Lat2 &L, const TmaMaps &M, uint8_t *stage,
                                                uint64_t *bar, int by, int bx, int tile, int cur,
                                                bool solved) {
-    using C = TmaCfg<TW>;   // box geometry does not depend on NT / STAGES
+    using C = TmaCfg<TW, TH, TW * TH / 4>;   // box geometry does not depend on NT / STAGES
     const int x0 = bx * TW;                       // uniform tiling: lo = index * width
     const int y0 = by * L.ay.base + tile * C::TH;
     // y2 / label maps start at the ghost row above the shard: +1 row
@@ -177,10 +179,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // pass-wide claim counter (dyn = 1).  Every pass-wide aggregate is an exact
 // integer (the residual sum included, see rsq_excess), so results do not
 // depend on which CTA took a block.
-template <int TW, int NT_, int STAGES_>
+template <int TW, int TH_, int NT_, int STAGES_>
 __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 1)))
     k_consensus_tma(Lat2 L, const __grid_constant__ TmaMaps M, uint32_t kx_magic, int dyn) {
-    using C = TmaCfg<TW, NT_, STAGES_>;
+    using C = TmaCfg<TW, TH_, NT_, STAGES_>;
     constexpr int TH = C::TH, NT = C::NT, QPT = C::QPT, QR = TW / 4, LQ = (TW == 64) ? 4 : 5;
     constexpr int ST = C::STAGES;
     extern __shared__ __align__(128) uint8_t smem_t[];
@@ -310,7 +312,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
             sinfo[s].tile = ptile;
             sinfo[s].flags = pflags | (ptile == tpb - 1 ? 4 : 0);
             const int by = (int)__umulhi((uint32_t)pk, kx_magic), bx = pk - by * KX;
-            tma_issue_tile<TW>(L, M, base + s * C::STAGE, &full[s], by, bx, ptile, cur, pflags & 1);
+            tma_issue_tile<TW, TH>(L, M, base + s * C::STAGE, &full[s], by, bx, ptile, cur, pflags & 1);
             ++ptile;
         }
         // drain the stages still in flight when the end marker went out
@@ -459,14 +461,16 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
                                       (rr == TH - 1 && tile_bot);
                     if (!ring) __stcg(reinterpret_cast<unsigned int *>(y_out + gt + (int64_t)rr * W + c0), yo);
                 }
-                // ring candidates: first and last tile row, then the edge
-                // quads of the rows in between
-                constexpr int NCAND = 2 * QR + 2 * (TH - 2);
-                for (int i = tid; i < NCAND; i += NT) {
+                // ring candidates: the block's first / last row when this tile
+                // holds it, then the two edge quads of the remaining rows
+                const int nT = tile_top ? QR : 0, nB = tile_bot ? QR : 0;
+                const int rlo = tile_top ? 1 : 0, rhi = tile_bot ? TH - 1 : TH;
+                const int ncand = nT + nB + 2 * (rhi - rlo);
+                for (int i = tid; i < ncand; i += NT) {
                     int rr, c0;
-                    if (i < QR) { rr = 0; c0 = 4 * i; }
-                    else if (i < 2 * QR) { rr = TH - 1; c0 = 4 * (i - QR); }
-                    else { const int jj = i - 2 * QR; rr = 1 + (jj >> 1); c0 = (jj & 1) ? TW - 4 : 0; }
+                    if (i < nT) { rr = 0; c0 = 4 * i; }
+                    else if (i < nT + nB) { rr = TH - 1; c0 = 4 * (i - nT); }
+                    else { const int jj = i - nT - nB; rr = rlo + (jj >> 1); c0 = (jj & 1) ? TW - 4 : 0; }
                     const bool lft = (c0 == 0) && has_lf, rgt = (c0 + 4 == TW) && has_rt;
                     const bool top = rr == 0 && tile_top, bot = rr == TH - 1 && tile_bot;
                     if (!(lft | rgt | top | bot)) continue;

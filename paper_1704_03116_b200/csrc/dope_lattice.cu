@@ -146,15 +146,19 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
     const int32_t cap = L.cap;
     const astore_t *__restrict__ a_cur = L.a;
     const ystore_t *__restrict__ y_cur = L.y2[L.st->ycur];
-    uint8_t *gres = L.resid + (size_t)k * 4 * M;
+    // stored residual graph: E and S planes only (the W / N residual of an
+    // arc pair is 2*cap minus the forward one: r(v->w) + r(w->v) = 2*cap)
+    uint8_t *gres = L.resid + (size_t)k * 2 * M;
 
     // ---- prologue: 2*linear (blockform.py:271-272 on the q==1 stencil) ----
     // lin2 = 2u + lamw * sum_cross (y2_g - y2_j) + mu*(2a - y2_g) + mu
     if (L.warm) {
-        // residual planes (block-major, 4*M bytes): asynchronous 16-byte copies
-        for (int i = tid; i < M * 4 / 16; i += NT) {
+        // E and S residual planes (block-major, 2*M bytes): asynchronous
+        // 16-byte copies into shared planes 0 (E) and 2 (S)
+        for (int i = tid; i < M * 2 / 16; i += NT) {
+            const int so = (i < M / 16) ? 16 * i : 2 * M + 16 * (i - M / 16);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                             (uint32_t)__cvta_generic_to_shared(rr + 16 * i)),
+                             (uint32_t)__cvta_generic_to_shared(rr + so)),
                          "l"(gres + 16 * i)
                          : "memory");
         }
@@ -243,17 +247,20 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
         const int v = tid + i * NT;
         const int r = v / BW, c = v % BW;
         if (!(r < hr && c < wc)) {
-            if (!L.warm) { rr[0 * M + v] = 0; rr[1 * M + v] = 0; rr[2 * M + v] = 0; rr[3 * M + v] = 0; }
+            rr[0 * M + v] = 0;
+            rr[1 * M + v] = 0;
+            rr[2 * M + v] = 0;
+            rr[3 * M + v] = 0;
             continue;
         }
         const bool hasE = c + 1 < wc, hasW = c > 0, hasS = r + 1 < hr, hasN = r > 0;
         if (L.warm) {
-            int32_t f = 0;
-            if (hasE) f += (int32_t)rr[0 * M + v] - cap;
-            if (hasW) f += (int32_t)rr[1 * M + v] - cap;
-            if (hasS) f += (int32_t)rr[2 * M + v] - cap;
-            if (hasN) f += (int32_t)rr[3 * M + v] - cap;
-            g[v] += f;
+            const int32_t rE = hasE ? rr[0 * M + v] : cap, rS = hasS ? rr[2 * M + v] : cap;
+            const int32_t rW = hasW ? 2 * cap - rr[0 * M + v - 1] : cap;
+            const int32_t rN = hasN ? 2 * cap - rr[2 * M + v - BW] : cap;
+            rr[1 * M + v] = hasW ? (uint8_t)rW : 0;
+            rr[3 * M + v] = hasN ? (uint8_t)rN : 0;
+            g[v] += (rE - cap) + (rW - cap) + (rS - cap) + (rN - cap);
         } else {
             rr[0 * M + v] = hasE ? cap : 0;
             rr[1 * M + v] = hasW ? cap : 0;
@@ -377,10 +384,12 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
             L.yhat[G] = (uint8_t)((reach[v >> 6] >> (v & 63)) & 1ull);
         }
     }
-    if (L.warm) {
+    if (L.warm) {   // E and S planes back
         uint4 *dst = reinterpret_cast<uint4 *>(gres);
-        const uint4 *src = reinterpret_cast<const uint4 *>(rr);
-        for (int i = tid; i < M * 4 / 16; i += NT) dst[i] = src[i];
+        for (int i = tid; i < M * 2 / 16; i += NT) {
+            const int so = (i < M / 16) ? 16 * i : 2 * M + 16 * (i - M / 16);
+            dst[i] = *reinterpret_cast<const uint4 *>(rr + so);
+        }
     }
     if (tid == 0 && L.timeline) {
         uint64_t t_end;
@@ -404,14 +413,12 @@ __global__ void k_init_resid(Lat2 L) {
     int32_t lo_r, hr, lo_c, wc;
     L.ay.range(by, lo_r, hr);
     L.ax.range(bx, lo_c, wc);
-    uint8_t *gres = L.resid + (size_t)k * 4 * M;
+    uint8_t *gres = L.resid + (size_t)k * 2 * M;   // E and S planes
     for (int v = threadIdx.x; v < M; v += blockDim.x) {
         const int r = v / L.boxw, c = v % L.boxw;
         const bool valid = r < hr && c < wc;
         gres[0 * M + v] = (valid && c + 1 < wc) ? L.cap : 0;
-        gres[1 * M + v] = (valid && c > 0) ? L.cap : 0;
-        gres[2 * M + v] = (valid && r + 1 < hr) ? L.cap : 0;
-        gres[3 * M + v] = (valid && r > 0) ? L.cap : 0;
+        gres[1 * M + v] = (valid && r + 1 < hr) ? L.cap : 0;
     }
 }
 
@@ -1265,19 +1272,23 @@ static int sm_count() {
 }
 
 // persistent TMA consensus: run-loop mode, uniform tiling, 64/128-wide blocks
-template <int TW, int NT, int ST>
+template <int TW, int TH, int NT, int ST>
 static int k2_tma_attr() {
-    return cuda_check(cudaFuncSetAttribute(k_consensus_tma<TW, NT, ST>,
+    return cuda_check(cudaFuncSetAttribute(k_consensus_tma<TW, TH, NT, ST>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           TmaCfg<TW, NT, ST>::SMEM),
+                                           TmaCfg<TW, TH, NT, ST>::SMEM),
                       "attr K2");
 }
 
-template <int TW, int NT, int ST>
+template <int TW, int TH, int NT, int ST>
 static int launch_k2_tma(const Lat2 &o, cudaStream_t s, int ctas_per_sm) {
-    using C = TmaCfg<TW, NT, ST>;
+    using C = TmaCfg<TW, TH, NT, ST>;
+    if (o.ay.base % TH != 0) {
+        snprintf(g_last_err, sizeof(g_last_err), "K2 tile height %d does not divide the block height", TH);
+        return DOPE_E_GEOMETRY;
+    }
     static std::once_flag once;
-    std::call_once(once, [] { k2_tma_attr<TW, NT, ST>(); });
+    std::call_once(once, [] { k2_tma_attr<TW, TH, NT, ST>(); });
     TmaMaps M;
     const int64_t W = o.W, H = o.ay.dim;
     bool ok = make_map(&M.a, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, o.a, W, H, TW, C::TH);
@@ -1299,13 +1310,12 @@ static int launch_k2_tma(const Lat2 &o, cudaStream_t s, int ctas_per_sm) {
     grid = o.K < grid ? o.K : grid;
     const uint32_t magic = (uint32_t)(((1ull << 32) + o.ax.k - 1) / o.ax.k);
     static const int dyn = getenv("DOPE_K2_DYNAMIC") ? 1 : 0;
-    k_consensus_tma<TW, NT, ST><<<grid, C::NT + 32, C::SMEM, s>>>(o, M, magic, dyn);
+    k_consensus_tma<TW, TH, NT, ST><<<grid, C::NT + 32, C::SMEM, s>>>(o, M, magic, dyn);
     return cuda_check(cudaGetLastError(), "launch K2 (tma)");
 }
 
-// measured on C3 (tools/k2_variants.sh): 4 CTAs x 4 warps x 2 stages per SM
-// beat 1-2 fat CTAs with deeper rings (more independent warps, cheap barriers)
-constexpr int K2_NT = 128, K2_STAGES = 2, K2_CPS = 4;
+// measured on C3 (tools/k2_variants.sh)
+constexpr int K2_TH = 64, K2_NT = 128, K2_STAGES = 2, K2_CPS = 4;
 
 static int k2_tma_width(const Lat2 &o) {
     // eligible: run-loop mode, uniform tiling, 64/128-wide blocks, TMA-friendly strides
@@ -1314,8 +1324,8 @@ static int k2_tma_width(const Lat2 &o) {
     const uintptr_t al = (uintptr_t)(o.y2[0] - o.W) | (uintptr_t)(o.y2[1] - o.W) | (uintptr_t)(o.y2[2] - o.W) |
                          (uintptr_t)(o.yhat - o.W) | (uintptr_t)o.a;
     if (al % 16 != 0 || !o.vec4) return 0;
-    if (o.ax.base == 64 && o.ay.base % 64 == 0) return 64;
-    if (o.ax.base == 128 && o.ay.base % 32 == 0) return 128;
+    if (o.ax.base == 64 && o.ay.base % K2_TH == 0) return 64;
+    if (o.ax.base == 128 && o.ay.base % (K2_TH / 2) == 0) return 128;
     return 0;
 }
 
@@ -1327,21 +1337,19 @@ static int launch_k2(const Lat2 &o, cudaStream_t s) {
     const int tw = k2_tma_width(o);
     static const int variant = getenv("DOPE_K2_VARIANT") ? atoi(getenv("DOPE_K2_VARIANT")) : 0;
     if (tw && !getenv("DOPE_NO_TMA")) {
-        // ~20 KB per stage: deep rings keep enough bytes in flight per SM
-        // (Little's law) for a kernel that moves ~7 B per pixel
         if (tw == 64) {
             switch (variant) {
-                case 1: return launch_k2_tma<64, 128, 3>(o, s, 3);
-                case 2: return launch_k2_tma<64, 128, 4>(o, s, 2);
-                case 3: return launch_k2_tma<64, 256, 2>(o, s, 2);
-                case 4: return launch_k2_tma<64, 256, 3>(o, s, 2);
-                case 5: return launch_k2_tma<64, 128, 2>(o, s, 5);
-                case 6: return launch_k2_tma<64, 512, 4>(o, s, 1);
-                case 7: return launch_k2_tma<64, 128, 3>(o, s, 2);
-                default: return launch_k2_tma<64, K2_NT, K2_STAGES>(o, s, K2_CPS);
+                case 1: return launch_k2_tma<64, 16, 128, 6>(o, s, 4);
+                case 2: return launch_k2_tma<64, 32, 128, 4>(o, s, 4);
+                case 3: return launch_k2_tma<64, 16, 64, 8>(o, s, 6);
+                case 4: return launch_k2_tma<64, 16, 128, 10>(o, s, 4);
+                case 5: return launch_k2_tma<64, 32, 128, 3>(o, s, 4);
+                case 6: return launch_k2_tma<64, 16, 128, 8>(o, s, 4);
+                case 7: return launch_k2_tma<64, 16, 256, 8>(o, s, 2);
+                default: return launch_k2_tma<64, K2_TH, K2_NT, K2_STAGES>(o, s, K2_CPS);
             }
         }
-        return launch_k2_tma<128, K2_NT, K2_STAGES>(o, s, K2_CPS);
+        return launch_k2_tma<128, K2_TH / 2, K2_NT, K2_STAGES>(o, s, K2_CPS);
     }
     const int lq = k2_lq(o);
     if (lq >= 0) {
@@ -1388,7 +1396,7 @@ int64_t dope_resid_stride(const dope_lattice *L) {
     Axis ay = make_axis(L->dims[0], L->kpa[0]), ax = make_axis(L->dims[1], L->kpa[1]);
     const Variant *v = pick_variant(ay.base + (ay.rem ? 1 : 0), ax.base + (ax.rem ? 1 : 0));
     if (!v) return 0;
-    return (int64_t)4 * v->bh * v->bw;
+    return (int64_t)2 * v->bh * v->bw;   // E and S residual planes
 }
 
 int64_t dope_scratch_stride(const dope_lattice *L) {
@@ -1411,8 +1419,8 @@ int dope_prepare_kernels(const dope_lattice *L) {
     if ((rc = configure_plan(P))) return rc;
     if (P.o.ndim == 2 && P.o.fuse) {
         const int tw = k2_tma_width(P.o);
-        if (tw == 64) return k2_tma_attr<64, K2_NT, K2_STAGES>();
-        if (tw == 128) return k2_tma_attr<128, K2_NT, K2_STAGES>();
+        if (tw == 64) return k2_tma_attr<64, K2_TH, K2_NT, K2_STAGES>();
+        if (tw == 128) return k2_tma_attr<128, K2_TH / 2, K2_NT, K2_STAGES>();
     }
     return DOPE_OK;
 }

@@ -66,7 +66,7 @@ def _lattice(dims=(256, 256), kpa=(4, 4), lamw=3, mu=1):
 def test_geometry_checks_without_gpu():
     lb = _lib.lib()
     L = _lattice()
-    assert lb.dope_resid_stride(C.byref(L)) == 4 * 64 * 64
+    assert lb.dope_resid_stride(C.byref(L)) == 2 * 64 * 64   # E and S residual planes
     assert lb.dope_resid_stride(C.byref(_lattice((256, 256), (16, 16)))) == 4 * 16 * 16
     assert lb.dope_resid_stride(C.byref(_lattice((2048, 2048), (16, 16)))) == 4 * 128 * 128
     assert lb.dope_resid_stride(C.byref(_lattice((70, 53), (3, 4)))) == 4 * 32 * 32

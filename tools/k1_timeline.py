@@ -25,6 +25,7 @@ def main():
     dev.L.timeline = tl.data_ptr()
     dev.call("dope_admm_init")
     for it in range(iters):
+        tl.view(K, 8)[:, 2] = -1   # blocks K1 does not solve keep rounds = -1
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record()
         dev.call("dope_update_blocks")
@@ -34,10 +35,10 @@ def main():
         torch.cuda.synchronize()
         t = tl.view(K, 8).cpu().numpy()
         solved = t[:, 2] >= 0
-        t0 = t[:, 0].min()
+        t0 = t[solved, 0].min() if solved.any() else 0
         dur = (t[:, 1] - t[:, 0]) / 1e3
-        ends = (t[:, 1] - t0) / 1e3
-        starts = (t[:, 0] - t0) / 1e3
+        ends = (t[solved, 1] - t0) / 1e3 if solved.any() else np.zeros(1)
+        starts = (t[solved, 0] - t0) / 1e3 if solved.any() else np.zeros(1)
         ds = dur[solved]
         print(f"it {it+1:3d}: K1 {e0.elapsed_time(e1)*1e3:7.1f} us  K2 {e1.elapsed_time(e2)*1e3:6.1f} us | "
               f"solved {solved.sum():5d}  block us: med {np.median(ds) if ds.size else 0:6.1f} "
