@@ -67,9 +67,9 @@ def test_geometry_checks_without_gpu():
     lb = _lib.lib()
     L = _lattice()
     assert lb.dope_resid_stride(C.byref(L)) == 2 * 64 * 64   # E and S residual planes
-    assert lb.dope_resid_stride(C.byref(_lattice((256, 256), (16, 16)))) == 4 * 16 * 16
-    assert lb.dope_resid_stride(C.byref(_lattice((2048, 2048), (16, 16)))) == 4 * 128 * 128
-    assert lb.dope_resid_stride(C.byref(_lattice((70, 53), (3, 4)))) == 4 * 32 * 32
+    assert lb.dope_resid_stride(C.byref(_lattice((256, 256), (16, 16)))) == 2 * 16 * 16
+    assert lb.dope_resid_stride(C.byref(_lattice((2048, 2048), (16, 16)))) == 2 * 128 * 128
+    assert lb.dope_resid_stride(C.byref(_lattice((70, 53), (3, 4)))) == 2 * 32 * 32
     assert lb.dope_resid_stride(C.byref(_lattice((1024, 1024), (4, 4)))) == 0   # 256^2 blocks
     # null buffers are rejected before any launch
     assert lb.dope_lattice_check(C.byref(L)) == _lib.DOPE_E_ARGS
