@@ -119,6 +119,26 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def kernel_bytes(wl, n, k_local, solves_per_iter, is_float):
+    """Algorithmic bytes per launch of each kernel (DESIGN.md §4 states them).
+
+    K1, per solved block (int): read u (4 B/px), multipliers (2), iterate (1)
+    and the stored E/S residual planes (2); write labels (1) and the planes (2)
+    = 12 B/px.  K2 (int): every pixel reads and writes its 1-byte iterate into
+    the rotating buffer (2 B/px); a re-solved block additionally reads and
+    writes its int16 multipliers and reads its labels (+5 B/px); the generic
+    (non-TMA) consensus moves the full 7 B/px everywhere.  Float path (C2):
+    f64 state, K1 = 44 B/px per solved block, K2 = 81 B/px.
+    """
+    bpx = n / max(k_local, 1)
+    if is_float:
+        return {"K1_block_mincut": 44.0 * bpx * solves_per_iter, "K2_consensus": 81.0 * n}
+    bh, bw = wl.block[-2], wl.block[-1]
+    tma = len(wl.block) == 2 and bw in (64, 128) and wl.dims[-1] % bw == 0 and wl.dims[0] % bh == 0
+    k2 = 2.0 * n + 5.0 * bpx * solves_per_iter if tma else 7.0 * n
+    return {"K1_block_mincut": 12.0 * bpx * solves_per_iter, "K2_consensus": k2}
+
+
 def build_problem(wl, device, lower=True):
     """Lower the workload (validation happens once, outside timing)."""
     import paper_1704_03116_b200 as dope
@@ -282,16 +302,11 @@ def main():
     n = n_local
     k_local = problems.lowering.K
     is_float = getattr(problems, "kind", "int") == "float"
-    # K2 algorithmic bytes per pixel: int path read u,a,y (int32) + yhat, write a,y = 21;
-    # float path read u,a,y,r_diag (f64) + 4 weight planes (f64) + yhat, write a,y = 81
-    k2_bpp = 81 if is_float else BYTES_PER_PIXEL_ITER
-    if dom == "K2_consensus":
-        alg_bytes = k2_bpp * n
-    elif dom == "K1_block_mincut":
-        # per solved block: read u,a,y (12 B/px), write yhat (1), residual graph r/w (8)
-        alg_bytes = (12 + 1 + 8) * (n / k_local) * (solves_per_run / iters_done)
-    else:
-        alg_bytes = 20.0 * k_local
+    alg = kernel_bytes(wl, n, k_local, solves_per_run / max(iters_done, 1), is_float)
+    for kname, st_ in kstat.items():   # per-kernel roofline beside the timings
+        st_["algorithmic_bytes_per_launch"] = alg[kname]
+        st_["achieved_GBps"] = alg[kname] / (st_["avg_ms"] / 1e3) / 1e9
+    alg_bytes = alg[dom]
     achieved = alg_bytes / (kstat[dom]["avg_ms"] / 1e3) / 1e9
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
