@@ -128,9 +128,12 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
         L.timeline[8 * k + 4] = (int64_t)t_begin;
         L.timeline[8 * k + 5] = (int64_t)t_begin;
     }
-    if (L.st->stop) return;
-    if (L.skip_clean) {
-        if (L.dirty[k] == 0) return;
+    {
+        // both flags in one round trip: a clean CTA must leave its slot fast
+        // (4096 CTAs churn through ~5 slots per SM)
+        const int stop = L.st->stop;
+        const uint32_t dk = L.skip_clean ? L.dirty[k] : 1u;
+        if (stop || dk == 0) return;
     }
     __syncthreads();
     if (tid == 0) {
@@ -168,15 +171,17 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
                has_rt = lo_c + wc < Wg;
     if (L.vec4) {
         // quads of 4 consecutive box nodes: int4 of u, 8 B of a, 4 B of y2
+        // every quad of this thread in one batch of loads (one round trip)
         constexpr int NQ = M / 4;
-        for (int q0 = tid; q0 < NQ; q0 += 2 * NT) {
-            int4 uq[2];
-            uint2 aq[2];
-            uint32_t yq[2], yu[2], yd[2];
-            int yl[2], yrr[2];
-            bool ok[2];
+        constexpr int QU = (NQ / NT) < 1 ? 1 : ((NQ / NT) > 4 ? 4 : (NQ / NT));
+        for (int q0 = tid; q0 < NQ; q0 += QU * NT) {
+            int4 uq[QU];
+            uint2 aq[QU];
+            uint32_t yq[QU], yu[QU], yd[QU];
+            int yl[QU], yrr[QU];
+            bool ok[QU];
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
+            for (int j = 0; j < QU; ++j) {
                 const int qd = q0 + j * NT;
                 const int v0 = 4 * qd, r = v0 / BW, c0 = v0 % BW;
                 ok[j] = qd < NQ && r < hr && c0 < wc;
@@ -196,7 +201,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
                 }
             }
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
+            for (int j = 0; j < QU; ++j) {
                 const int qd = q0 + j * NT;
                 if (qd >= NQ) continue;
                 const int v0 = 4 * qd, r = v0 / BW, c0 = v0 % BW;
@@ -242,7 +247,41 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
     }
     if (L.warm) asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
+    if (L.timeline && tid == 0) {   // diagnostics: prologue loads done
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        L.timeline[8 * k + 7] = (int64_t)t;
+    }
     // g = lin2 + net inflow of the stored flow (warm) / cold residual graph
+    if (L.warm) {
+        // quads of 4 nodes: W = 2cap - E(west), N = 2cap - S(north) bytewise
+        // (no borrow: every residual is <= 2cap), node sums in 16-bit lanes
+        const uint32_t CAP2 = 0x01010101u * (uint32_t)(2 * cap);
+        for (int q = tid; q < M / 4; q += NT) {
+            const int v0 = 4 * q, r = v0 / BW, c0 = v0 % BW;
+            const int nv = r < hr ? wc - c0 : 0;                   // valid nodes in this quad
+            const uint32_t vm = nv >= 4 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - nv))));
+            const uint32_t E = *reinterpret_cast<const uint32_t *>(rr + v0);
+            const uint32_t S = *reinterpret_cast<const uint32_t *>(rr + 2 * M + v0);
+            const uint32_t ep = c0 > 0 ? (uint32_t)rr[v0 - 1] : 0u;
+            const uint32_t W = (CAP2 - ((E << 8) | ep)) & vm & (c0 == 0 ? 0xFFFFFF00u : 0xFFFFFFFFu);
+            const uint32_t N = r > 0 ? (CAP2 - *reinterpret_cast<const uint32_t *>(rr + 2 * M + v0 - BW)) & vm : 0u;
+            *reinterpret_cast<uint32_t *>(rr + 1 * M + v0) = W;
+            *reinterpret_cast<uint32_t *>(rr + 3 * M + v0) = N;
+            const uint32_t lo = (E & 0x00FF00FFu) + (W & 0x00FF00FFu) + (S & 0x00FF00FFu) + (N & 0x00FF00FFu);
+            const uint32_t hi = ((E >> 8) & 0x00FF00FFu) + ((W >> 8) & 0x00FF00FFu) + ((S >> 8) & 0x00FF00FFu) +
+                                ((N >> 8) & 0x00FF00FFu);
+            const int vert = (r > 0) + (r + 1 < hr);
+            int4 gv = *reinterpret_cast<const int4 *>(g + v0);
+            // arcs per node: E if c+1 < wc, W if c > 0, plus the vertical ones
+            auto deg = [&](int c) { return (c < wc) ? (vert + (c > 0) + (c + 1 < wc)) : 0; };
+            gv.x += (int)(lo & 0xFFFFu) - cap * deg(c0);
+            gv.y += (int)(hi & 0xFFFFu) - cap * deg(c0 + 1);
+            gv.z += (int)(lo >> 16) - cap * deg(c0 + 2);
+            gv.w += (int)(hi >> 16) - cap * deg(c0 + 3);
+            if (nv > 0) *reinterpret_cast<int4 *>(g + v0) = gv;
+        }
+    } else
     for (int i = 0; i < NPT; ++i) {
         const int v = tid + i * NT;
         const int r = v / BW, c = v % BW;
@@ -376,12 +415,23 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
     }
 
     // ---- epilogue: labels (sink side), residual graph, stats ----
-    for (int i = 0; i < NPT; ++i) {
-        const int v = tid + i * NT;
-        const int r = v / BW, c = v % BW;
-        if (r < hr && c < wc) {
-            const int64_t G = (int64_t)(lo_r + r) * Wg + lo_c + c;
-            L.yhat[G] = (uint8_t)((reach[v >> 6] >> (v & 63)) & 1ull);
+    if (L.vec4) {   // 4 labels per 32-bit store (quads never straddle the block edge)
+        for (int q = tid; q < M / 4; q += NT) {
+            const int v0 = 4 * q, r = v0 / BW, c0 = v0 % BW;
+            if (r < hr && c0 < wc) {
+                const uint32_t b = (uint32_t)(reach[v0 >> 6] >> (v0 & 63)) & 0xFu;
+                const int64_t G = (int64_t)(lo_r + r) * Wg + lo_c + c0;
+                *reinterpret_cast<uint32_t *>(L.yhat + G) = (b * 0x00204081u) & 0x01010101u;
+            }
+        }
+    } else {
+        for (int i = 0; i < NPT; ++i) {
+            const int v = tid + i * NT;
+            const int r = v / BW, c = v % BW;
+            if (r < hr && c < wc) {
+                const int64_t G = (int64_t)(lo_r + r) * Wg + lo_c + c;
+                L.yhat[G] = (uint8_t)((reach[v >> 6] >> (v & 63)) & 1ull);
+            }
         }
     }
     if (L.warm) {   // E and S planes back
