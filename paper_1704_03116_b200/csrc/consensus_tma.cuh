@@ -1,6 +1,6 @@
 // consensus_tma.cuh -- persistent, TMA-pipelined consensus pass (K2) for
 // uniform tilings with 64- or 128-wide blocks.  Included by dope_lattice.cu
-// inside namespace dope (uses Lat2, reduce_blocks, finalize_apply, other_buffer).
+// inside namespace dope (uses Lat2, CtaAgg, pass_tail, other_buffer).
 //
 // Same arithmetic as k_consensus_vec (solve_global + clamp admm.py:194-238,
 // update_multipliers admm.py:241-248, block residuals admm.py:251-257, energy
@@ -249,9 +249,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
                 nep[i] = L.dirty[K + nk[i]];
                 nmemo[i] = L.pf[nk[i]];
             }
-        // this CTA's pass aggregates (exact integers)
-        int64_t cE = 0, cU = 0, cM = -1, cS = 0, cX = 0;
-        int cF = 0;
+        CtaAgg agg;   // this CTA's pass aggregates (exact integers)
         auto drain = [&](int s) {
             const StageInfo info = sinfo[s];
             if (!(info.flags & 4)) return;
@@ -270,12 +268,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
             L.pu[k] = u2;
             L.pr[k] = sq;
             L.pf[k] = clamped | (memo ? 64 : 0);
-            cE += e;
-            cU += u2;
-            cM = sq > cM ? sq : cM;
-            cS += sq;
-            cX += rsq_excess(sq);
-            cF |= clamped;
+            agg.add_block(e, u2, sq, clamped);
             if (f & 2u) L.dirty[k] = 1u;
             if (f & 4u) L.dirty[k - 1] = 1u;
             if (f & 8u) L.dirty[k + 1] = 1u;
@@ -324,35 +317,12 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
             mbar_wait(&empty[s], (m / ST) & 1);
             drain(s);
         }
-        // fold this CTA's aggregates into the pass-wide ones (exact integer atomics)
-        if (cE) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[0]), (unsigned long long)cE);
-        if (cU) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[1]), (unsigned long long)cU);
-        if (cM >= 0) atomicMax(reinterpret_cast<unsigned long long *>(&L.pc[2]), (unsigned long long)(cM + 1));
-        if (cF) atomicOr(reinterpret_cast<unsigned long long *>(&L.pc[3]), 1ull);
-        if (cS) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[4]), (unsigned long long)cS);
-        if (cX) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[5]), (unsigned long long)cX);
         if (L.timeline) {   // diagnostics: CTA end (slot 7)
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             L.timeline[8 * blockIdx.x + 7] = (int64_t)t;
         }
-        __threadfence();
-        if (atomicAdd(&st->done_ctas, 1) == (int)gridDim.x - 1) {
-            // last CTA: apply the pass
-            __threadfence();
-            const dope_run_state s0 = *st;
-            const int64_t E2 = __ldcg(&L.pc[0]), U2 = __ldcg(&L.pc[1]), M2 = __ldcg(&L.pc[2]) - 1;
-            const int F2 = (int)__ldcg(&L.pc[3]);
-            const double R2 = rsq_total(__ldcg(&L.pc[4]), __ldcg(&L.pc[5]));
-            for (int i = 0; i < 8; ++i) L.pc[i] = 0;   // incl. the claim counter
-            finalize_apply(L, s0, E2, U2, R2, M2, F2, cur, best, out);
-            st->done_ctas = 0;
-            if (L.timeline && (int)gridDim.x < L.K) {   // diagnostics: finalize end
-                uint64_t t;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                L.timeline[8 * gridDim.x + 7] = (int64_t)t;
-            }
-        }
+        pass_tail(L, agg, cur, best, out);
         return;
     }
 

@@ -613,82 +613,6 @@ __device__ __forceinline__ double rsq_total(int64_t sum_ss, int64_t sum_excess) 
     return (double)sum_ss + (double)sum_excess * 0x1p-53;
 }
 
-// Reduce per-block partials of the blocks first, first + stride, ... (< K) over
-// the calling CTA: thread-strided, then a fixed shuffle tree and warp order,
-// so the float sum is deterministic.  Result valid in thread 0.
-struct Aggr {
-    int64_t E, U, M, S, X;
-    int F;
-};
-
-__device__ Aggr reduce_blocks(const Lat2 &L, int first, int stride, int count) {
-    __shared__ int64_t sE[32], sU[32], sM[32], sS[32], sX[32];
-    __shared__ int sF[32];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    Aggr a{0, 0, -1, 0, 0, 0};
-    // batches of UNR blocks per thread: all loads of a batch are in flight
-    // together (a strided loop would pay one L2 round trip per block)
-    constexpr int UNR = 8;
-    for (int i0 = tid; i0 < count; i0 += blockDim.x * UNR) {
-        int64_t e[UNR], u[UNR], sq[UNR];
-        int f[UNR];
-#pragma unroll
-        for (int j = 0; j < UNR; ++j) {
-            const int i = i0 + j * blockDim.x;
-            const bool in = i < count;
-            const int k = first + i * stride;
-            e[j] = in ? __ldcg(&L.pe[k]) : 0;
-            u[j] = in ? __ldcg(&L.pu[k]) : 0;
-            sq[j] = in ? __ldcg(&L.pr[k]) : -1;
-            f[j] = in ? __ldcg(&L.pf[k]) : 0;
-        }
-#pragma unroll
-        for (int j = 0; j < UNR; ++j) {
-            a.E += e[j];
-            a.U += u[j];
-            a.F |= f[j] & 1;
-            if (sq[j] >= 0) {
-                a.S += sq[j];
-                a.X += rsq_excess(sq[j]);
-                a.M = sq[j] > a.M ? sq[j] : a.M;
-            }
-        }
-    }
-    a.E = warp_sum(a.E);
-    a.U = warp_sum(a.U);
-    a.S = warp_sum(a.S);
-    a.X = warp_sum(a.X);
-    for (int o = 16; o > 0; o >>= 1) {
-        const int64_t t = __shfl_xor_sync(FULLMASK, a.M, o);
-        a.M = t > a.M ? t : a.M;
-    }
-    a.F = __any_sync(FULLMASK, a.F);
-    __syncthreads();   // the shared scratch may be reused by consecutive calls
-    if (lane == 0) { sE[warp] = a.E; sU[warp] = a.U; sS[warp] = a.S; sX[warp] = a.X; sM[warp] = a.M; sF[warp] = a.F; }
-    __syncthreads();
-    if (tid == 0) {
-        a = Aggr{0, 0, -1, 0, 0, 0};
-        const int nw = blockDim.x / 32;
-        for (int w = 0; w < nw; ++w) {
-            a.E += sE[w];
-            a.U += sU[w];
-            a.S += sS[w];
-            a.X += sX[w];
-            a.M = sM[w] > a.M ? sM[w] : a.M;
-            a.F |= sF[w];
-        }
-    }
-    return a;
-}
-
-// Last CTA of a one-CTA-per-block consensus launch: reduce all K blocks' partials.
-__device__ void finalize_cta(const Lat2 &L, int cur, int best_idx, int out) {
-    dope_run_state s0;
-    if (threadIdx.x == 0) s0 = *L.st;   // in flight during the reduction
-    const Aggr a = reduce_blocks(L, 0, 1, L.K);
-    if (threadIdx.x == 0) finalize_apply(L, s0, a.E, a.U, rsq_total(a.S, a.X), a.M, a.F, cur, best_idx, out);
-}
-
 // Sharded mode: apply the all-reduced aggregates (identical on every rank).
 __global__ void k_decide(Lat2 L) {
     dope_run_state *st = L.st;
@@ -738,16 +662,54 @@ __global__ void k_ghost_update(Lat2 L, int which, const void *up_new, const void
     }
 }
 
-// Per-CTA epilogue shared by the scalar / vector consensus kernels: reduce the
-// thread partials, publish the block's partials and dirty marks; the last CTA
-// to arrive runs finalize_cta.
-__device__ __forceinline__ void consensus_epilogue(const Lat2 &L, int k, int64_t e_acc, int64_t du,
-                                                   int64_t ss, int clamped, int chg_self, int chgL,
-                                                   int chgR, int chgU, int chgD, int cur, int best,
-                                                   int out) {
+// This CTA's exact pass aggregates (thread 0): pair energy, unary change,
+// max block ss, clamp flag, sum ss, sum of residual excesses (rsq_excess).
+struct CtaAgg {
+    int64_t E = 0, U = 0, M = -1, S = 0, X = 0;
+    int F = 0;
+    __device__ void add_block(int64_t e, int64_t u, int64_t ss, int clamped) {
+        E += e;
+        U += u;
+        M = ss > M ? ss : M;
+        S += ss;
+        X += rsq_excess(ss);
+        F |= clamped;
+    }
+};
+
+// One thread per CTA, after its last block: fold the CTA's aggregates into
+// the pass-wide ones (order-free integer atomics); the last CTA to arrive
+// applies the pass (trace, best iterate, stop rule, buffer rotation).
+__device__ void pass_tail(const Lat2 &L, const CtaAgg &c, int cur, int best, int out) {
+    if (c.E) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[0]), (unsigned long long)c.E);
+    if (c.U) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[1]), (unsigned long long)c.U);
+    if (c.M >= 0) atomicMax(reinterpret_cast<unsigned long long *>(&L.pc[2]), (unsigned long long)(c.M + 1));
+    if (c.F) atomicOr(reinterpret_cast<unsigned long long *>(&L.pc[3]), 1ull);
+    if (c.S) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[4]), (unsigned long long)c.S);
+    if (c.X) atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[5]), (unsigned long long)c.X);
+    __threadfence();
+    dope_run_state *st = L.st;
+    if (atomicAdd(&st->done_ctas, 1) == (int)(gridDim.x * gridDim.y * gridDim.z) - 1) {
+        __threadfence();
+        const dope_run_state s0 = *st;
+        const int64_t E2 = __ldcg(&L.pc[0]), U2 = __ldcg(&L.pc[1]), M2 = __ldcg(&L.pc[2]) - 1;
+        const int F2 = (int)__ldcg(&L.pc[3]);
+        const double R2 = rsq_total(__ldcg(&L.pc[4]), __ldcg(&L.pc[5]));
+        for (int i = 0; i < 8; ++i) L.pc[i] = 0;   // incl. the claim counter
+        finalize_apply(L, s0, E2, U2, R2, M2, F2, cur, best, out);
+        st->done_ctas = 0;
+    }
+}
+
+// Per-block epilogue of the scalar / vector consensus kernels: reduce the
+// thread partials; thread 0 publishes the block's partials and dirty marks
+// and folds them into the CTA aggregates.  Ends with a barrier (the shared
+// scratch is reused by the CTA's next block).
+__device__ __forceinline__ void block_epilogue(const Lat2 &L, int k, int64_t e_acc, int64_t du, int64_t ss,
+                                               int clamped, int chg_self, int chgL, int chgR, int chgU,
+                                               int chgD, CtaAgg &agg) {
     __shared__ int64_t red_e[32], red_s[32], red_u[32];
     __shared__ int red_f[32];
-    __shared__ int last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     e_acc = warp_sum(e_acc);
     du = warp_sum(du);
@@ -783,16 +745,9 @@ __device__ __forceinline__ void consensus_epilogue(const Lat2 &L, int k, int64_t
         if (Fm & 8) L.dirty[k + 1] = 1u;
         if ((Fm & 16) && k - L.ax.k >= 0) L.dirty[k - L.ax.k] = 1u;
         if ((Fm & 32) && k + L.ax.k < L.K) L.dirty[k + L.ax.k] = 1u;
-        __threadfence();
-        const int prev = atomicAdd(&L.st->done_ctas, 1);
-        last = (prev == L.K - 1);
+        agg.add_block(E, U, S, Fm & 1);
     }
     __syncthreads();
-    if (last) {
-        __threadfence();
-        finalize_cta(L, cur, best, out);
-        if (threadIdx.x == 0) L.st->done_ctas = 0;
-    }
 }
 
 // Multiplier range: |a| moves by at most 1 per pass (yhat, y in {0, 1}), so
@@ -806,13 +761,14 @@ __device__ __forceinline__ void check_a(const Lat2 &L, int a) {
 __global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
     if (L.st->stop) return;
     const int tid = threadIdx.x;
-    const int k = blockIdx.x;
+    CtaAgg agg;
+    const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
+    for (int k = blockIdx.x; k < L.K; k += gridDim.x) {
     const int by = k / L.ax.k, bx = k % L.ax.k;
     int32_t lo_r, hr, lo_c, wc;
     L.ay.range(by, lo_r, hr);
     L.ax.range(bx, lo_c, wc);
     const int32_t W = L.W, H = L.ay.dim;
-    const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
     const ystore_t *__restrict__ y_in = L.y2[cur];
     ystore_t *__restrict__ y_out = L.y2[out];
     // multipliers are updated in place (a_{t+1}[p] depends on a_t[p] only)
@@ -860,7 +816,9 @@ __global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
             chgD |= (r == hr - 1 && has_dn);
         }
     }
-    consensus_epilogue(L, k, e_acc, du, ss, clamped, chg_self, chgL, chgR, chgU, chgD, cur, best, out);
+    block_epilogue(L, k, e_acc, du, ss, clamped, chg_self, chgL, chgR, chgU, chgD, agg);
+    }
+    if (tid == 0) pass_tail(L, agg, cur, best, out);
 }
 
 // Vectorized consensus for uniform tilings whose block width is a power of
@@ -873,7 +831,9 @@ __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
     constexpr int QPT = 4;
     if (L.st->stop) return;
     const int tid = threadIdx.x;
-    const int k = blockIdx.x;
+    CtaAgg agg;
+    const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
+    for (int k = blockIdx.x; k < L.K; k += gridDim.x) {
     const int by = k / L.ax.k, bx = k - by * L.ax.k;
     int32_t lo_r, hr, lo_c, wc;
     L.ay.range(by, lo_r, hr);
@@ -881,7 +841,6 @@ __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
     const int32_t W = L.W, H = L.ay.dim;
     const int QR = 1 << lq;              // quads per block row
     const int nq = hr << lq;
-    const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
     const ystore_t *__restrict__ y_in = L.y2[cur];
     ystore_t *__restrict__ y_out = L.y2[out];
     // multipliers are updated in place (a_{t+1}[p] depends on a_t[p] only)
@@ -978,8 +937,9 @@ __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
         }
     }
     const int64_t e64 = (int64_t)L.lamw * quad;
-    consensus_epilogue(L, k, e64, du, (int64_t)ss, clamped, chg_self, chgL, chgR, chgU, chgD, cur,
-                       best, out);
+    block_epilogue(L, k, e64, du, (int64_t)ss, clamped, chg_self, chgL, chgR, chgU, chgD, agg);
+    }
+    if (tid == 0) pass_tail(L, agg, cur, best, out);
 }
 
 // a += yhat - y for the step-level API (admm.py:241-248), in place.
@@ -1404,13 +1364,18 @@ static int launch_k2(const Lat2 &o, cudaStream_t s) {
     const int lq = k2_lq(o);
     if (lq >= 0) {
         const int64_t quads = (int64_t)(o.ay.base + (o.ay.rem ? 1 : 0)) << lq;
-        if (quads <= 4 * 32) k_consensus_vec<32><<<o.K, 32, 0, s>>>(o, lq);
-        else if (quads <= 4 * 64) k_consensus_vec<64><<<o.K, 64, 0, s>>>(o, lq);
-        else if (quads <= 4 * 256) k_consensus_vec<256><<<o.K, 256, 0, s>>>(o, lq);
-        else if (quads <= 4 * 1024) k_consensus_vec<1024><<<o.K, 1024, 0, s>>>(o, lq);
-        else k_consensus<<<o.K, 256, 0, s>>>(o);
+        // persistent grids (a few thousand threads per SM): the last-CTA
+        // counter and the aggregate atomics scale with CTAs, not blocks
+        const int sms = sm_count();
+        auto grid = [&](int per_sm) { return o.K < per_sm * sms ? o.K : per_sm * sms; };
+        if (quads <= 4 * 32) k_consensus_vec<32><<<grid(32), 32, 0, s>>>(o, lq);
+        else if (quads <= 4 * 64) k_consensus_vec<64><<<grid(24), 64, 0, s>>>(o, lq);
+        else if (quads <= 4 * 256) k_consensus_vec<256><<<grid(8), 256, 0, s>>>(o, lq);
+        else if (quads <= 4 * 1024) k_consensus_vec<1024><<<grid(2), 1024, 0, s>>>(o, lq);
+        else k_consensus<<<grid(8), 256, 0, s>>>(o);
     } else {
-        k_consensus<<<o.K, 256, 0, s>>>(o);
+        const int sms = sm_count();
+        k_consensus<<<o.K < 8 * sms ? o.K : 8 * sms, 256, 0, s>>>(o);
     }
     return cuda_check(cudaGetLastError(), "launch K2");
 }

@@ -293,7 +293,6 @@ __global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
     }
     __shared__ int64_t red_e[32], red_s[32], red_u[32];
     __shared__ unsigned red_f[32];
-    __shared__ int last;
     e_acc = warp_sum(e_acc);
     ss = warp_sum(ss);
     du = warp_sum(du);
@@ -317,13 +316,8 @@ __global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
         if (Fm & 16u) L.dirty[k + KX] = 1u;
         if (Fm & 32u) L.dirty[k - KYX] = 1u;
         if (Fm & 64u) L.dirty[k + KYX] = 1u;
-        __threadfence();
-        last = (atomicAdd(&L.st->done_ctas, 1) == L.K - 1);
-    }
-    __syncthreads();
-    if (last) {
-        __threadfence();
-        finalize_cta(L, cur, best, out);
-        if (threadIdx.x == 0) L.st->done_ctas = 0;
+        CtaAgg agg;
+        agg.add_block(E, U, S, (Fm & 128u) ? 1 : 0);
+        pass_tail(L, agg, cur, best, out);
     }
 }
