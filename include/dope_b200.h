@@ -275,6 +275,52 @@ int dope_f_admm_run(const dope_lattice_f *L, int32_t iters, int32_t use_graph, v
 int dope_f_finish_run(const dope_lattice_f *L, void *stream);
 int dope_f_binarize(const dope_lattice_f *L, uint8_t *out, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * General lattice path: box partitions WITH overlap
+ * (make_partition overlap_pct 10 / 25: pixel block counts q in {1, 2, 4}, every
+ * block owns a copy of its pixels' labels and multipliers), float64 4- or
+ * 8-connected weights, mu schedule mu_t = mu0 * mu_fact^t and the eps stop
+ * rule -- the reference's default AdmmConfig.  Replaces admm.run /
+ * update_blocks / update_global / update_multipliers (admm.py:113-252) with
+ * blockform.py:48-105 evaluated per copy on the lattice stencil.  Float
+ * parity bar (final energy within 1e-5 relative, <= 0.01 % labels).
+ * ------------------------------------------------------------------------- */
+typedef struct dope_general {
+    int32_t conn;               /* 4 or 8                                      */
+    int64_t dims[2];            /* H, W                                        */
+    int32_t kpa[2];             /* blocks per axis                             */
+    int32_t box[2];             /* largest block extent per axis               */
+    double lam, mu0, mu_fact, eps;
+    double qscale;              /* capacity quantisation scale (2^16)          */
+    int32_t max_iters, warm_start;
+    const double *u;            /* n                                           */
+    const double *w[4];         /* E S SE SW weight planes (pair stored at its
+                                   lower pixel; SE/SW only when conn == 8)     */
+    const uint8_t *q;           /* n: blocks holding each pixel                */
+    const int32_t *ranges;      /* 2*KY + 2*KX: row lo[KY], row len[KY],
+                                   col lo[KX], col len[KX] (partition.py:62-77) */
+    double *a;                  /* K * dope_g_copy_stride: per-copy multipliers */
+    uint8_t *yhat;              /* K * dope_g_copy_stride: per-copy labels     */
+    int32_t *resid;             /* K * conn * dope_g_copy_stride: residuals    */
+    double *y[3];               /* n: rotating iterates (current, best, next)  */
+    double *part_energy;        /* dope_g_partials(): energy partials          */
+    double *part_ressq;         /* K: ||yhat_k - S_k y||^2                     */
+    int32_t *part_flags;        /* dope_g_partials(): clamp flags (zeroed)     */
+    double *scal;               /* 1: current mu                               */
+    dope_run_state *state;
+    double *trace_energy, *trace_residual_sq, *trace_max_residual, *trace_mu;
+    int32_t *trace_clamped;     /* max_iters each                              */
+} dope_general;
+
+int64_t dope_g_copy_stride(const dope_general *L);
+int64_t dope_g_partials(const dope_general *L);
+int dope_g_check(const dope_general *L);
+const char *dope_g_last_error(void);
+int dope_g_admm_init(const dope_general *L, void *stream);
+int dope_g_admm_run(const dope_general *L, int32_t iters, int32_t use_graph, void *stream);
+int dope_g_finish_run(const dope_general *L, void *stream);
+int dope_g_binarize(const dope_general *L, uint8_t *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -119,6 +119,41 @@ class LatticeF(C.Structure):
     ]
 
 
+class General(C.Structure):
+    """Mirror of dope_general (overlapping partitions, mu schedule)."""
+    _fields_ = [
+        ("conn", C.c_int32),
+        ("dims", C.c_int64 * 2),
+        ("kpa", C.c_int32 * 2),
+        ("box", C.c_int32 * 2),
+        ("lam", C.c_double),
+        ("mu0", C.c_double),
+        ("mu_fact", C.c_double),
+        ("eps", C.c_double),
+        ("qscale", C.c_double),
+        ("max_iters", C.c_int32),
+        ("warm_start", C.c_int32),
+        ("u", C.c_void_p),
+        ("w", C.c_void_p * 4),
+        ("q", C.c_void_p),
+        ("ranges", C.c_void_p),
+        ("a", C.c_void_p),
+        ("yhat", C.c_void_p),
+        ("resid", C.c_void_p),
+        ("y", C.c_void_p * 3),
+        ("part_energy", C.c_void_p),
+        ("part_ressq", C.c_void_p),
+        ("part_flags", C.c_void_p),
+        ("scal", C.c_void_p),
+        ("state", C.c_void_p),
+        ("trace_energy", C.c_void_p),
+        ("trace_residual_sq", C.c_void_p),
+        ("trace_max_residual", C.c_void_p),
+        ("trace_mu", C.c_void_p),
+        ("trace_clamped", C.c_void_p),
+    ]
+
+
 class DopeError(RuntimeError):
     pass
 
@@ -197,6 +232,22 @@ def lib():
     lb.dope_f_admm_run.argtypes = [PF, C.c_int32, C.c_int32, C.c_void_p]
     lb.dope_f_binarize.restype = C.c_int
     lb.dope_f_binarize.argtypes = [PF, C.c_void_p, C.c_void_p]
+    PG = C.POINTER(General)
+    for name in ("dope_g_copy_stride", "dope_g_partials"):
+        f = getattr(lb, name)
+        f.restype = C.c_int64
+        f.argtypes = [PG]
+    lb.dope_g_check.restype = C.c_int
+    lb.dope_g_check.argtypes = [PG]
+    lb.dope_g_last_error.restype = C.c_char_p
+    for name in ("dope_g_admm_init", "dope_g_finish_run"):
+        f = getattr(lb, name)
+        f.restype = C.c_int
+        f.argtypes = [PG, C.c_void_p]
+    lb.dope_g_admm_run.restype = C.c_int
+    lb.dope_g_admm_run.argtypes = [PG, C.c_int32, C.c_int32, C.c_void_p]
+    lb.dope_g_binarize.restype = C.c_int
+    lb.dope_g_binarize.argtypes = [PG, C.c_void_p, C.c_void_p]
     if lb.dope_abi_version() != ABI_VERSION:
         raise DopeError(f"libdope_b200 ABI {lb.dope_abi_version()} != {ABI_VERSION}")
     _lib = lb

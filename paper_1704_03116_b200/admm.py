@@ -526,12 +526,15 @@ def run(model: EnergyModel, partition: Partition, config: AdmmConfig,
     import torch
     if config.solver.kind != "maxflow":
         raise NotImplementedError("only the max-flow block solver has a B200 kernel")
+    overlap = partition.overlap_pct != 0 or bool(partition.counts.size and int(partition.counts.max()) > 1)
+    if overlap or config.mu_fact != 1.0:
+        # overlapping partitions / growing mu: the general path
+        from .general import run_general
+        return run_general(model, partition, config, use_graph=config.use_graph)
     if problems is None:
         problems = assemble_block_problems(model, partition)
     mu0 = config.resolved_mu0(partition.shape.ndim)
     eps = config.resolved_eps(partition)
-    if config.mu_fact != 1.0:
-        raise NotImplementedError("the B200 path keeps mu fixed (mu_fact == 1)")
     state = init_state(partition, mu0)
     dev = state._bind(problems, config, config.max_iters, eps)
     start = torch.cuda.Event(enable_timing=True)

@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 #include "dope_b200.h"
+#include "mincut_core.cuh"
 
 namespace dope_f {
 using namespace dope;
@@ -81,23 +82,9 @@ __device__ __forceinline__ int64_t pair_low(const LatF &L, int64_t G, int d, int
 // K1f: block min cut, quantised float capacities, 4/8 directions
 // ---------------------------------------------------------------------------
 template <int BH, int BW, int NT, int NDIR>
-struct K1FCfg {
-    static constexpr int M = BH * BW;
-    static constexpr int NPT = M / NT;
-    static constexpr int NW = M / 64;
-    static constexpr size_t OFF_G = 0;
-    static constexpr size_t OFF_R = OFF_G + 4 * (size_t)M;
-    static constexpr size_t OFF_H = OFF_R + 4 * (size_t)NDIR * M;
-    static constexpr size_t OFF_MASK = OFF_H + 2 * (size_t)M;
-    static constexpr size_t OFF_REACH = OFF_MASK + 8 * (size_t)(NDIR + 2) * NW;
-    static constexpr size_t OFF_MISC = OFF_REACH + 8 * (size_t)NW;
-    static constexpr size_t SMEM = OFF_MISC + 64;
-};
-
-template <int BH, int BW, int NT, int NDIR>
 __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, int sweep_mul) {
     using Cf = K1FCfg<BH, BW, NT, NDIR>;
-    constexpr int M = Cf::M, NPT = Cf::NPT, NW = Cf::NW;
+    constexpr int M = Cf::M, NPT = Cf::NPT;
     extern __shared__ __align__(16) uint8_t smem[];
     int32_t *g = reinterpret_cast<int32_t *>(smem + Cf::OFF_G);
     int32_t *rr = reinterpret_cast<int32_t *>(smem + Cf::OFF_R);
@@ -105,8 +92,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
     uint64_t *masks = reinterpret_cast<uint64_t *>(smem + Cf::OFF_MASK);
     uint64_t *reach = reinterpret_cast<uint64_t *>(smem + Cf::OFF_REACH);
     int *misc = reinterpret_cast<int *>(smem + Cf::OFF_MISC);
-    uint32_t *masks32 = reinterpret_cast<uint32_t *>(masks);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     const int k = blockIdx.x;
     if (L.st->stop) return;
     if (L.skip_clean && L.dirty[k] == 0) return;
@@ -176,85 +162,8 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
     }
     __syncthreads();
 
-    constexpr int OFFS[8] = {1, -1, BW, -BW, BW + 1, -BW - 1, BW - 1, -BW + 1};
-    int rounds = 0;
-    for (;;) {
-        for (int i = 0; i < NPT; ++i) {
-            const int v = tid + i * NT;
-            const int32_t gvv = g[v];
-            uint32_t b[NDIR];
-#pragma unroll
-            for (int d = 0; d < NDIR; ++d) b[d] = __ballot_sync(FULLMASK, rr[d * M + v] != 0);
-            const uint32_t bK = __ballot_sync(FULLMASK, gvv < 0);
-            const uint32_t bA = __ballot_sync(FULLMASK, gvv > 0);
-            h[v] = gvv < 0 ? 0 : HINF;
-            if (lane == 0) {
-                const int w32 = (i * NT + warp * 32) >> 5;
-#pragma unroll
-                for (int d = 0; d < NDIR; ++d) masks32[d * 2 * NW + w32] = b[d];
-                masks32[NDIR * 2 * NW + w32] = bK;
-                masks32[(NDIR + 1) * 2 * NW + w32] = bA;
-            }
-        }
-        __syncthreads();
-        if (warp == 0) {
-            int levels = 0;
-            const int hit = bfs_relabel<NW, BW, 0, NDIR == 8>(masks, reach, h, lane, &levels);
-            if (lane == 0) { misc[0] = hit; misc[1] = levels; }
-        }
-        __syncthreads();
-        const int hit = misc[0], levels = misc[1];
-        if (!hit) break;
-        if (++rounds > (1 << 16)) {
-            if (tid == 0) atomicCAS(&L.st->error, 0, k + 1);
-            break;
-        }
-        const int cap_sweeps = sweep_min + sweep_mul * levels;
-        for (int sw = 0; sw < cap_sweeps; ++sw) {
-            for (int i = 0; i < NPT; ++i) {
-                const int v = tid + i * NT;
-                const int32_t e = g[v];
-                if (e <= 0) continue;
-                const uint16_t hv = h[v];
-                if (hv == HINF || hv == 0) continue;
-                const uint16_t ht = hv - 1;
-                int32_t left = e;
-#pragma unroll
-                for (int d = 0; d < NDIR; ++d) {
-                    const int32_t rv = rr[d * M + v];
-                    if (rv == 0) continue;
-                    const int w = v + OFFS[d];
-                    if (h[w] != ht) continue;
-                    const int32_t delta = left < rv ? left : rv;
-                    rr[d * M + v] = rv - delta;
-                    rr[(d ^ 1) * M + w] += delta;
-                    atomicAdd(&g[w], delta);
-                    left -= delta;
-                    if (left == 0) break;
-                }
-                if (left != e) atomicSub(&g[v], e - left);
-            }
-            __syncthreads();
-            int act = 0;
-            for (int i = 0; i < NPT; ++i) {
-                const int v = tid + i * NT;
-                if (g[v] <= 0) continue;
-                const uint16_t hv = h[v];
-                if (hv == HINF) continue;
-                uint32_t mn = HINF;
-#pragma unroll
-                for (int d = 0; d < NDIR; ++d) {
-                    if (rr[d * M + v] == 0) continue;
-                    const uint32_t hw = h[v + OFFS[d]];
-                    mn = hw < mn ? hw : mn;
-                }
-                const uint32_t nh = (mn + 1 >= (uint32_t)M) ? HINF : mn + 1;
-                if (nh != hv) h[v] = (uint16_t)nh;
-                act |= (nh != HINF);
-            }
-            if (!__syncthreads_or(act)) break;
-        }
-    }
+    if (mincut_solve<BH, BW, NT, NDIR>(g, rr, h, masks, reach, misc, sweep_min, sweep_mul) < 0 && tid == 0)
+        atomicCAS(&L.st->error, 0, k + 1);
     for (int i = 0; i < NPT; ++i) {
         const int v = tid + i * NT;
         const int r = v / BW, c = v % BW;

@@ -135,14 +135,10 @@ def _block_ids(n_axis: int, k: int) -> np.ndarray:
     return np.repeat(np.arange(k), sizes)
 
 
-def lower_float(model: EnergyModel, partition: Partition, qscale: float = QSCALE) -> FloatLowering:
-    """Lower a 2D lattice model with arbitrary non-negative pair weights."""
-    shape = partition.shape
-    if shape.ndim != 2:
-        raise NotImplementedError("float-weight lattices are implemented in 2D")
-    if partition.overlap_pct != 0 or (partition.counts.size and int(partition.counts.max()) != 1):
-        raise NotImplementedError("overlapping partitions (q > 1) have no B200 kernel yet")
-    H, W = shape.dims
+def lattice_planes(model: EnergyModel, dims) -> tuple:
+    """Weight planes E, S, SE, SW (pair stored at its lower pixel) of a 2D
+    4/8-connected lattice model, and its connectivity."""
+    H, W = dims
     w = model.weights
     if w.npairs and float(w.vals.min()) < 0:
         raise NonSubmodularError("pairwise weights contain negative entries; max-flow requires "
@@ -167,6 +163,18 @@ def lower_float(model: EnergyModel, partition: Partition, qscale: float = QSCALE
         known |= (dy == ddy) & (dx == ddx)
     if not known.all():
         raise NotImplementedError("pairwise weights are not a 4/8-connected 2D lattice stencil")
+    return planes, conn
+
+
+def lower_float(model: EnergyModel, partition: Partition, qscale: float = QSCALE) -> FloatLowering:
+    """Lower a 2D lattice model with arbitrary non-negative pair weights."""
+    shape = partition.shape
+    if shape.ndim != 2:
+        raise NotImplementedError("float-weight lattices are implemented in 2D")
+    if partition.overlap_pct != 0 or (partition.counts.size and int(partition.counts.max()) != 1):
+        raise NotImplementedError("overlapping partitions (q > 1) have no B200 kernel yet")
+    H, W = shape.dims
+    planes, conn = lattice_planes(model, shape.dims)
     P = [p.reshape(H, W) for p in planes]
     z = np.zeros((H, W))
     bid = _block_ids(H, partition.k_per_axis[0])[:, None] * partition.k_per_axis[1] + \

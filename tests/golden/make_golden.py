@@ -162,6 +162,66 @@ def save_run(case: str, wl: W.Workload, iters: int | None = None, store_u: bool 
           f"best={r['best_iteration']} E_last={r['energy'][-1]}")
 
 
+def ref_run_general(wl: W.Workload, overlap: int, mu0, mu_fact: float, eps, iters: int):
+    """admm.run on an (optionally overlapping) partition with an arbitrary mu
+    schedule; per-copy block labels / multipliers in block order."""
+    rows, cols, vals = wl.pair_arrays()
+    shape = GridShape(wl.dims)
+    model = EnergyModel(wl.u.astype(np.float64), SparseWeights(wl.n, rows, cols, vals), wl.lam)
+    part = make_partition(shape, wl.kpa, overlap)
+    cfg = ref_admm.AdmmConfig(mu0=mu0, mu_fact=mu_fact, eps=eps, max_iters=iters)
+    hist = []
+    orig = ref_admm.update_blocks
+
+    def recording(state, problems, lam, config):
+        out = orig(state, problems, lam, config)
+        hist.append(np.concatenate([np.asarray(l, dtype=np.uint8) for l in state.block_labels]))
+        return out
+
+    ref_admm.update_blocks = recording
+    try:
+        labels, state = ref_admm.run(model, part, cfg)
+    finally:
+        ref_admm.update_blocks = orig
+    tr = state.trace
+    return dict(
+        mu=np.array([t.mu for t in tr]), energy=np.array([t.energy for t in tr]),
+        residual_sq=np.array([t.residual_sq for t in tr]),
+        max_block_residual=np.array([t.max_block_residual for t in tr]),
+        clamped=np.array([t.clamped for t in tr]),
+        yhat_bits=np.packbits(np.array(hist, dtype=np.uint8), axis=1),
+        y=state.y, labels=np.asarray(labels, dtype=np.int8),
+        a_copies=np.concatenate([np.asarray(m, dtype=np.float64) for m in state.multipliers]),
+        converged=state.converged, iterations=state.iteration,
+        best_iteration=state.best_iteration, counts=part.counts,
+        eps=cfg.resolved_eps(part), mu0=cfg.resolved_mu0(shape.ndim))
+
+
+def save_general(case: str, wl: W.Workload, overlap: int, mu0, mu_fact: float, eps, iters: int):
+    r = ref_run_general(wl, overlap, mu0, mu_fact, eps, iters)
+    meta = dict(dims=np.array(wl.dims), block=np.array(wl.block), conn=wl.conn, lam=wl.lam,
+                overlap=overlap, mu_fact=mu_fact, max_iters=iters, name=wl.name, u=wl.u,
+                wplanes=np.stack([np.asarray(w, dtype=np.float64) for w in wl.weights]))
+    np.savez_compressed(OUT / f"gen_{case}.npz", **r, **meta)
+    print(f"gen_{case}: iters={r['iterations']} converged={r['converged']} "
+          f"best={r['best_iteration']} E_last={r['energy'][-1]} qmax={int(r['counts'].max())}")
+
+
+def main_general():
+    """General path: overlapping partitions (q in {1,2,4})
+    and the reference's default mu schedule (mu_fact = 1.05, eps from the
+    block size)."""
+    # contrast-weighted 8-conn image, 4x4 blocks grown by 25 %, default config
+    save_general("c2ov25", W.c2(size=64, block=16, iters=50), 25, None, 1.05, None, 50)
+    save_general("c2ov25_long", W.c2(size=64, block=16, iters=25), 25, None, 1.05, 0.0, 25)
+    # integer 4-conn disks, 4x4 blocks grown by 10 %, fixed mu (lam*w/mu = 2)
+    ov = W.mini_disks(128, 32, 6, 2, 20, seed=8, rmax=40.0)
+    save_general("int_ov10", ov, 10, 1.0, 1.0, 0.0, 20)
+    # non-overlapping tiling with the default growing mu and eps (converges)
+    save_general("mufact", W.mini_disks(128, 32, 6, 2, 50, seed=9, rmax=40.0), 0, None, 1.05, None, 50)
+    save_general("mufact_long", W.mini_disks(128, 32, 6, 2, 20, seed=9, rmax=40.0), 0, 4.0, 1.05, 0.0, 20)
+
+
 class _RaggedWL(W.Workload):
     @property
     def kpa(self):
@@ -173,6 +233,9 @@ def main():
     ref_maxflow.bk_maxflow = core.bk_maxflow     # the reference's own seam swap
     if "--only-float" in sys.argv:
         save_run("c2mini", W.c2(size=128, block=32, iters=30))
+        return
+    if "--only-general" in sys.argv:
+        main_general()
         return
     gen_bk(core)
     save_run("c1", W.c1())
@@ -199,6 +262,7 @@ def main():
     r2 = W.mini_disks(128, 32, 4, 2, 15, seed=6, rmax=40.0)
     r2.rho = 2.0
     save_run("rho2", r2)
+    main_general()
 
 
 if __name__ == "__main__":

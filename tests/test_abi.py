@@ -30,28 +30,27 @@ def test_library_loads_and_exports_every_declared_symbol():
 def test_struct_layouts_match_header(tmp_path):
     """The ctypes mirrors agree with the C compiler's layout of the header."""
     import subprocess
+    mirrors = {"L": ("dope_lattice", _lib.Lattice), "S": ("dope_run_state", _lib.RunState),
+               "F": ("dope_lattice_f", _lib.LatticeF), "G": ("dope_general", _lib.General)}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "dope_b200.h"', 'int main(){']
-    for f, _ in _lib.Lattice._fields_:
-        lines.append(f'printf("L %s %zu\\n", offsetof(dope_lattice, {f}));'.replace("%s", f))
-    for f, _ in _lib.RunState._fields_:
-        lines.append(f'printf("S %s %zu\\n", offsetof(dope_run_state, {f}));'.replace("%s", f))
-    lines.append('printf("Z L %zu\\n", sizeof(dope_lattice));')
-    lines.append('printf("Z S %zu\\n", sizeof(dope_run_state));')
+    for tag, (cname, py) in mirrors.items():
+        for f, _ in py._fields_:
+            lines.append(f'printf("{tag} {f} %zu\\n", offsetof({cname}, {f}));')
+        lines.append(f'printf("Z {tag} %zu\\n", sizeof({cname}));')
     lines.append('return 0;}')
     src = tmp_path / "off.c"
     src.write_text("\n".join(lines))
     exe = tmp_path / "off"
     subprocess.run(["gcc", f"-I{ROOT / 'include'}", str(src), "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    assert out
     for line in filter(None, out):
         kind, name, val = line.split()
         val = int(val)
-        if kind == "L":
-            assert getattr(_lib.Lattice, name).offset == val, name
-        elif kind == "S":
-            assert getattr(_lib.RunState, name).offset == val, name
+        if kind == "Z":
+            assert C.sizeof(mirrors[name][1]) == val, name
         else:
-            assert C.sizeof(_lib.Lattice if name == "L" else _lib.RunState) == val
+            assert getattr(mirrors[kind][1], name).offset == val, (kind, name)
 
 
 def _lattice(dims=(256, 256), kpa=(4, 4), lamw=3, mu=1):

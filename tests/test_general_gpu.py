@@ -1,0 +1,72 @@
+"""General path vs the reference: overlapping partitions
+(overlap_pct 10 / 25, q in {1, 2, 4}) and the reference's default growing mu.
+
+Fixtures gen_*.npz are admm.run outputs of the reference itself
+(tests/golden/make_golden.py, main_general).  Float parity bar (BASELINE):
+final energy within 1e-5 relative and <= 0.01 % label disagreement; we also
+hold every iteration's energy and mu, the stop iteration and the per-copy
+multipliers to tight tolerances.
+"""
+import numpy as np
+import pytest
+
+import paper_1704_03116_b200 as dope
+from paper_1704_03116_b200 import workloads as W
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["c2ov25", "c2ov25_long", "int_ov10", "mufact", "mufact_long"]
+
+
+def _model(g):
+    dims = tuple(int(d) for d in g["dims"])
+    conn = int(g["conn"])
+    wp = g["wplanes"]
+    weights = [float(w) for w in wp] if wp.ndim == 1 else [np.asarray(w) for w in wp]
+    wl = W.Workload("g", dims, tuple(int(b) for b in g["block"]), conn, g["u"], weights,
+                    float(g["lam"]), 1.0, int(g["max_iters"]), wp.ndim == 1)
+    rows, cols, vals = wl.pair_arrays()
+    model = dope.EnergyModel(np.asarray(g["u"], dtype=np.float64), dope.SparseWeights(wl.n, rows, cols, vals),
+                             float(g["lam"]))
+    part = dope.make_partition(dope.GridShape(dims), wl.kpa, int(g["overlap"]))
+    cfg = dope.AdmmConfig(mu0=float(g["mu0"]), mu_fact=float(g["mu_fact"]), eps=float(g["eps"]),
+                          max_iters=int(g["max_iters"]))
+    return model, part, cfg
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_general_matches_reference(case):
+    g = load_golden(f"gen_{case}.npz")
+    model, part, cfg = _model(g)
+    if int(g["overlap"]):
+        assert int(part.counts.max()) > 1
+    labels, state = dope.run(model, part, cfg)
+    it = int(g["iterations"])
+    assert state.iteration == it
+    assert state.converged == bool(g["converged"])
+    e = np.array([t.energy for t in state.trace])
+    np.testing.assert_allclose(e, g["energy"], rtol=1e-6, atol=1e-9)
+    np.testing.assert_allclose([t.mu for t in state.trace], g["mu"], rtol=1e-12)
+    np.testing.assert_allclose([t.max_block_residual for t in state.trace], g["max_block_residual"],
+                               rtol=1e-6, atol=1e-9)
+    assert abs(e[-1] - g["energy"][-1]) <= 1e-5 * abs(g["energy"][-1])
+    assert state.best_iteration == int(g["best_iteration"])
+    dis = np.count_nonzero(labels != g["labels"])
+    assert dis <= 1e-4 * labels.size, dis
+    np.testing.assert_allclose(state.y, g["y"], atol=1e-6)
+    a = np.concatenate(state.multipliers)
+    np.testing.assert_allclose(a, g["a_copies"], atol=1e-6)
+    # per-iteration block labels (every copy)
+    hist = np.unpackbits(g["yhat_bits"], axis=1)[:, :a.size]
+    assert np.array_equal(np.concatenate(state.block_labels).astype(np.uint8), hist[it - 1])
+
+
+def test_general_graph_and_eager_agree():
+    g = load_golden("gen_int_ov10.npz")
+    model, part, cfg = _model(g)
+    l1, s1 = dope.run(model, part, cfg)
+    cfg.use_graph = False
+    l2, s2 = dope.run(model, part, cfg)
+    assert np.array_equal(l1, l2)
+    assert [t.energy for t in s1.trace] == [t.energy for t in s2.trace]
