@@ -70,3 +70,28 @@ def test_general_graph_and_eager_agree():
     l2, s2 = dope.run(model, part, cfg)
     assert np.array_equal(l1, l2)
     assert [t.energy for t in s1.trace] == [t.energy for t in s2.trace]
+
+
+@pytest.mark.parametrize("overlap,conn", [(25, 8), (10, 4)])
+def test_general_vs_oracle_256(overlap, conn):
+    """256^2, 8x8 blocks of 32 grown by the overlap, growing mu: B200 vs the
+    general-path oracle (itself pinned to the reference's fixtures)."""
+    import general as og
+    if conn == 8:
+        wl = W.c2(size=256, block=32, iters=12)
+    else:
+        wl = W.mini_disks(256, 32, 8, 2, 12, seed=11, rmax=60.0)
+    rows, cols, vals = wl.pair_arrays()
+    model = dope.EnergyModel(np.asarray(wl.u, dtype=np.float64), dope.SparseWeights(wl.n, rows, cols, vals),
+                             wl.lam)
+    part = dope.make_partition(dope.GridShape(wl.dims), wl.kpa, overlap)
+    cfg = dope.AdmmConfig(mu0=2.0, mu_fact=1.05, eps=0.0, max_iters=12)
+    labels, state = dope.run(model, part, cfg)
+    from paper_1704_03116_b200.lowering import lattice_planes
+    planes, c = lattice_planes(model, wl.dims)
+    assert c == conn
+    spec = og.GeneralSpec(wl.dims, conn, wl.u, planes, wl.lam, wl.kpa, overlap)
+    ref = og.run(spec, 2.0, 1.05, 0.0, 12)
+    assert state.iteration == ref["iterations"]
+    np.testing.assert_allclose([t.energy for t in state.trace], ref["energy"], rtol=1e-6)
+    assert np.count_nonzero(labels != ref["labels"]) <= 1e-4 * labels.size
