@@ -166,6 +166,151 @@ def cpu_baseline(wl, iters: int):
                       f"(oracle C port of admm.run + BK, {threads} threads), {dt:.1f} s"}
 
 
+def is_general(wl) -> bool:
+    return bool(wl.meta) and "overlap" in wl.meta
+
+
+def general_model(wl):
+    import paper_1704_03116_b200 as dope
+    rows, cols, vals = wl.pair_arrays()
+    model = dope.EnergyModel(np.asarray(wl.u, dtype=np.float64), dope.SparseWeights(wl.n, rows, cols, vals),
+                             wl.lam)
+    part = dope.make_partition(dope.GridShape(wl.dims), wl.kpa, int(wl.meta["overlap"]))
+    return model, part
+
+
+def cpu_baseline_general(wl, iters: int):
+    """General-path oracle (numpy + the oracle's BK, one host thread) on a
+    bounded sample: the first `iters` iterations of the same workload."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import general as og
+    from paper_1704_03116_b200.lowering import lattice_planes
+    model, _ = general_model(wl)
+    planes, conn = lattice_planes(model, wl.dims)
+    spec = og.GeneralSpec(wl.dims, conn, wl.u, planes, wl.lam, wl.kpa, int(wl.meta["overlap"]))
+    t0 = time.perf_counter()
+    out = og.run(spec, wl.meta["mu0"], wl.meta["mu_fact"], 0.0, iters)
+    dt = time.perf_counter() - t0
+    return {"value": out["iterations"] / dt, "unit": "iterations/s", "cores": 1, "kind": "port",
+            "sample": f"{wl.name}: first {out['iterations']} ADMM iterations from init_state "
+                      f"(general-path oracle: numpy stencil + BK restatement, 1 thread), {dt:.1f} s"}
+
+
+def run_general_bench(args, wl):
+    """One GPU, general path (overlap + growing mu): same contract fields."""
+    import torch
+    from paper_1704_03116_b200.general import GeneralDevice, lower_general
+    iters = args.iters or wl.iters
+    model, part = general_model(wl)
+    low = lower_general(model, part)
+    gd = GeneralDevice(low, wl.meta["mu0"], wl.meta["mu_fact"], 0.0, iters)
+    use_graph = not args.no_graph
+
+    def step():
+        gd.init()
+        gd.run(iters, use_graph)
+        gd.finish()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    rs = gd.run_state()
+    iters_done = int(rs.iteration)
+    sampler = ClockSampler(0)
+    sampler.start()
+    t_wait = time.time()
+    while not sampler.rows and time.time() - t_wait < 5.0:
+        step()
+        torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    sampler.stop()
+    ms = e0.elapsed_time(e1)
+    value = iters_done * args.steps / (ms / 1e3)
+    # per-kernel timing (eager launches on the stream)
+    gd.init()
+    kt = {"K1_block_mincut": [], "K2_consensus": []}
+    stream = torch.cuda.current_stream()
+    for _ in range(iters_done):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(stream)
+        gd.step_blocks()
+        ev[1].record(stream)
+        gd.step_global()
+        ev[2].record(stream)
+        kt["K1_block_mincut"].append(ev)
+    torch.cuda.synchronize()
+    k1 = [e[0].elapsed_time(e[1]) for e in kt["K1_block_mincut"]]
+    k2 = [e[1].elapsed_time(e[2]) for e in kt["K1_block_mincut"]]
+    ncopy = sum(b.size for b in part.blocks)
+    n = low.n
+    nd = low.conn
+    # algorithmic bytes (DESIGN §4, general path): K1 per copy pixel: u, y, a
+    # (f64) + q + weights (8 B per direction pair, 2 directions per pair) +
+    # residual planes r/w (4 B x conn x 2) + label; global step per pixel: the
+    # copies' labels and multipliers (q x 9 B), weights, u, q, y out, and per
+    # copy the multiplier update (r/w 16 B) + residual, energy pass (y, u, w)
+    k1b = ncopy * (8 + 8 + 8 + 1 + 4 * nd + 8 * nd + 1)
+    k2b = ncopy * (9 + 16 + 1) + n * (8 + 1 + 4 * nd + 8 + 8 + 8 + 4 * nd)
+    kstat = {}
+    for name, v, b in (("K1_block_mincut", k1, k1b), ("K2_consensus", k2, k2b)):
+        kstat[name] = {"total_ms": sum(v), "avg_ms": sum(v) / len(v), "launches": len(v),
+                       "median_ms": statistics.median(v), "algorithmic_bytes_per_launch": b,
+                       "achieved_GBps": b / (sum(v) / len(v) / 1e3) / 1e9}
+    dom = max(kstat, key=lambda k: kstat[k]["total_ms"])
+    peak, peak_kind = measured_peaks()
+    roof = {"bound": "hbm", "achieved": kstat[dom]["achieved_GBps"], "peak": peak, "unit": "GB/s",
+            "frac": kstat[dom]["achieved_GBps"] / peak, "traffic": None, "kernel": dom,
+            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+            "algorithmic_bytes_per_launch": kstat[dom]["algorithmic_bytes_per_launch"]}
+    # e2e: unaries and weights from pinned host memory, labels + trace back
+    e2e = None
+    if not args.no_e2e:
+        u_host = gd.u.cpu().pin_memory()
+        w_host = [w.cpu().pin_memory() for w in gd.w]
+        lab = torch.empty(n, dtype=torch.uint8).pin_memory()
+        trh = torch.empty(iters, dtype=torch.float64).pin_memory()
+        hb = u_host.numel() * 8 + sum(w.numel() * 8 for w in w_host)
+        for s in range(args.warmup + args.steps):
+            if s == args.warmup:
+                torch.cuda.synchronize()
+                f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                f0.record()
+            gd.u.copy_(u_host, non_blocking=True)
+            for wd, wh in zip(gd.w, w_host):
+                wd.copy_(wh, non_blocking=True)
+            step()
+            lab.copy_(gd.binarize(), non_blocking=True)
+            trh.copy_(gd.tr["e"], non_blocking=True)
+        f1.record()
+        torch.cuda.synchronize()
+        e2e = {"value": iters_done * args.steps / (f0.elapsed_time(f1) / 1e3), "unit": "iterations/s",
+               "h2d_bytes_per_step": hb, "d2h_bytes_per_step": n + 8 * iters}
+    line = {"metric": "ADMM iterations/s", "value": value, "unit": "iterations/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{wl.name}: {wl.dims[0]}x{wl.dims[1]} {nd}-connected contrast-weighted "
+                                   f"Potts, {part.k} sub-regions of {wl.block[0]}x{wl.block[1]} grown by "
+                                   f"{wl.meta['overlap']} % (q in {{1,2,4}}), mu0 {wl.meta['mu0']}, "
+                                   f"mu_fact {wl.meta['mu_fact']}, {iters_done} ADMM iterations per step",
+                       "pixel_edges_per_s": value * wl.num_pairs, "path": "general (overlap, growing mu)",
+                       "l2": "state fits in the 126 MB L2 (no flush between steps)",
+                       "parallelism": "1 GPU", "kernels": kstat},
+            "roofline": roof, "clocks": sampler.summary(),
+            "gpu_launches": (5 * iters_done + 4) * args.steps}
+    if e2e:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_general(wl, args.cpu_sample_iters)
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -175,7 +320,7 @@ def run_reference(args):
     iters = max(1, args.cpu_sample_iters)
     vals = []
     for s in range(args.warmup + args.steps):
-        r = cpu_baseline(wl, iters)
+        r = cpu_baseline_general(wl, iters) if is_general(wl) else cpu_baseline(wl, iters)
         if s >= args.warmup:
             vals.append(r["value"])
     v = statistics.mean(vals)
@@ -183,7 +328,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * iters / v,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{wl.name} {wl.dims[0]}x{wl.dims[1]} 4-conn, "
+            "config": {"workload": f"{wl.name} {wl.dims[0]}x{wl.dims[1]} {wl.conn}-conn, "
                                    f"{wl.num_blocks} sub-regions of {wl.block[0]}x{wl.block[1]}; "
                                    f"each step = first {iters} iterations",
                        "pixel_edges_per_s": v * wl.num_pairs},
@@ -206,6 +351,10 @@ def main():
     from paper_1704_03116_b200 import workloads as W
     from paper_1704_03116_b200.admm import make_device_state
     wl = W.by_name(args.config)
+    if is_general(wl):
+        if ws > 1:
+            raise SystemExit("the general-path bench runs on one GPU")
+        return run_general_bench(args, wl)
     iters = args.iters or wl.iters
     use_graph = int(not args.no_graph)
     if ws == 1 and not args.sharded:

@@ -318,6 +318,9 @@ int dope_g_check(const dope_general *L);
 const char *dope_g_last_error(void);
 int dope_g_admm_init(const dope_general *L, void *stream);
 int dope_g_admm_run(const dope_general *L, int32_t iters, int32_t use_graph, void *stream);
+int dope_g_update_blocks(const dope_general *L, void *stream);   /* one K1 pass   */
+int dope_g_update_global(const dope_general *L, void *stream);   /* global step,
+                           residuals + multipliers, energy, trace / stop    */
 int dope_g_finish_run(const dope_general *L, void *stream);
 int dope_g_binarize(const dope_general *L, uint8_t *out, void *stream);
 

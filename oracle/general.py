@@ -19,7 +19,8 @@ overlapping box partition with an arbitrary mu schedule:
 The stencil form replaces the reference's sparse matrices; float operation
 order differs (results agree within the float parity bar).  Pinned against
 the reference's own fixtures (tests/golden/gen_*.npz) by
-tests/test_oracle_golden.py.  Only tests/ import this module.
+tests/test_oracle_general.py.  Only tests/ and bench.py's CPU-baseline leg
+import this module.
 """
 from __future__ import annotations
 
@@ -93,31 +94,41 @@ class GeneralSpec:
         return out
 
 
-def _block_terms(spec: GeneralSpec, k: int):
-    """Per-box arrays of block k: in-box mask per direction, dhat, r_diag."""
-    (r0, r1), (c0, c1) = spec.boxes[k]
-    inbox = np.zeros((spec.H, spec.W), dtype=bool)
-    inbox[r0:r1, c0:c1] = True
-    q = spec.q
-    dhat = np.zeros((spec.H, spec.W))
-    nin = []
-    for (dy, dx), w in zip(spec.dirs, spec.wd):
-        nb_in = spec.shift(inbox.astype(np.float64), dy, dx) > 0
-        nq = spec.shift(q, dy, dx, fill=1.0)
-        nin.append((nb_in, nq))
-        dhat += np.where(nb_in & (w != 0), w / (q * nq), 0.0)
-    rdiag = spec.deg / (q * q) - dhat
-    return inbox, nin, rdiag
+class _Block:
+    """Block k on its window (box plus a one-pixel ring, clipped to the grid):
+    every quantity the block touches lives there."""
+
+    def __init__(self, spec: GeneralSpec, k: int):
+        (r0, r1), (c0, c1) = spec.boxes[k]
+        H, W = spec.H, spec.W
+        self.box = (r0, r1, c0, c1)
+        self.wr0, self.wr1 = max(0, r0 - 1), min(H, r1 + 1)
+        self.wc0, self.wc1 = max(0, c0 - 1), min(W, c1 + 1)
+        self.win = (slice(self.wr0, self.wr1), slice(self.wc0, self.wc1))
+        self.bl = (slice(r0 - self.wr0, r1 - self.wr0), slice(c0 - self.wc0, c1 - self.wc0))   # box in window
+        shp = (self.wr1 - self.wr0, self.wc1 - self.wc0)
+        self.inbox = np.zeros(shp, dtype=bool)
+        self.inbox[self.bl] = True
+        self.q = spec.q[self.win]
+        self.deg = spec.deg[self.win]
+        self.wd = [w[self.win] for w in spec.wd]
+        self.nin, dhat = [], np.zeros(shp)
+        for (dy, dx), w in zip(spec.dirs, self.wd):
+            nb_in = spec.shift(self.inbox.astype(np.float64), dy, dx) > 0
+            nq = spec.shift(self.q, dy, dx, fill=1.0)
+            self.nin.append((nb_in, nq))
+            dhat += np.where(nb_in & (w != 0), w / (self.q * nq), 0.0)
+        self.rdiag = self.deg / (self.q * self.q) - dhat
 
 
 def run(spec: GeneralSpec, mu0: float, mu_fact: float, eps: float, max_iters: int) -> dict:
     H, W = spec.H, spec.W
-    q, lam = spec.q, spec.lam
-    K = len(spec.boxes)
-    terms = [_block_terms(spec, k) for k in range(K)]
+    lam = spec.lam
+    blocks = [_Block(spec, k) for k in range(len(spec.boxes))]
+    nf = 4 if spec.conn == 8 else 2
     y = np.full((H, W), 0.5)
-    a = [np.zeros((r1 - r0, c1 - c0)) for (r0, r1), (c0, c1) in spec.boxes]
-    yh = [np.zeros((r1 - r0, c1 - c0), dtype=np.int8) for (r0, r1), (c0, c1) in spec.boxes]
+    a = [np.zeros((b.box[1] - b.box[0], b.box[3] - b.box[2])) for b in blocks]
+    yh = [np.zeros_like(x, dtype=np.int8) for x in a]
     mu = float(mu0)
     best_e, best_y, best_it = math.inf, y.copy(), 0
     tr = dict(mu=[], energy=[], residual_sq=[], max_block_residual=[], clamped=[])
@@ -125,21 +136,22 @@ def run(spec: GeneralSpec, mu0: float, mu_fact: float, eps: float, max_iters: in
     it = 0
     for it in range(1, max_iters + 1):
         # ---- block solves (blockform.py:89-105, maxflow.py:73-113) ----
-        for k, ((r0, r1), (c0, c1)) in enumerate(spec.boxes):
-            inbox, nin, rdiag = terms[k]
-            cy = (spec.deg / q) * (1.0 - 1.0 / q) * y
-            for ((dy, dx), w), (nb_in, nq) in zip(zip(spec.dirs, spec.wd), nin):
-                ny = spec.shift(y, dy, dx)
+        for k, b in enumerate(blocks):
+            q = b.q
+            yw = y[b.win]
+            cy = (b.deg / q) * (1.0 - 1.0 / q) * yw
+            for ((dy, dx), w), (nb_in, nq) in zip(zip(spec.dirs, b.wd), b.nin):
+                ny = spec.shift(yw, dy, dx)
                 cy += np.where(nb_in, (-w / q) * (1.0 - 1.0 / nq) * ny, (-w / q) * ny)
-            lin = spec.u / q + lam * (cy + rdiag * y) + mu * ((0.0 - y) + 0.5)
-            blin = lin[r0:r1, c0:c1] + mu * a[k]
-            hb, wb = r1 - r0, c1 - c0
+            lin = spec.u[b.win] / q + lam * (cy + b.rdiag * yw) + mu * ((0.0 - yw) + 0.5)
+            blin = lin[b.bl] + mu * a[k]
+            hb, wb = blin.shape
             idx = np.arange(hb * wb).reshape(hb, wb)
             pi, pj, cap = [], [], []
-            for t, (dy, dx) in enumerate(spec.dirs[: (4 if spec.conn == 8 else 2)]):
+            for t, (dy, dx) in enumerate(spec.dirs[:nf]):
                 ys, xs = slice(0, hb - max(0, dy)), slice(max(0, -dx), wb - max(0, dx))
                 yt, xt = slice(dy, hb - max(0, dy) + dy), slice(max(0, -dx) + dx, wb - max(0, dx) + dx)
-                wq = spec.wd[t][r0:r1, c0:c1] / (q[r0:r1, c0:c1] * spec.shift(q, dy, dx, 1.0)[r0:r1, c0:c1])
+                wq = (b.wd[t] / (q * spec.shift(q, dy, dx, 1.0)))[b.bl]
                 wsel = wq[ys, xs]
                 m = wsel != 0
                 pi.append(idx[ys, xs][m])
@@ -152,25 +164,25 @@ def run(spec: GeneralSpec, mu0: float, mu_fact: float, eps: float, max_iters: in
             yh[k] = np.asarray(labels, dtype=np.int8).reshape(hb, wb)
         # ---- global step (admm.py:136-180) ----
         acc = np.zeros((H, W))
-        for k, ((r0, r1), (c0, c1)) in enumerate(spec.boxes):
-            inbox, nin, rdiag = terms[k]
-            t = np.zeros((H, W))
-            t[r0:r1, c0:c1] = yh[k]
-            acc[r0:r1, c0:c1] += mu * (yh[k] + a[k]) - lam * (rdiag[r0:r1, c0:c1] * yh[k])
-            ct = np.where(inbox, (spec.deg / q) * (1.0 - 1.0 / q) * t, 0.0)
-            for ((dy, dx), w), (nb_in, nq) in zip(zip(spec.dirs, spec.wd), nin):
+        for k, b in enumerate(blocks):
+            q = b.q
+            t = np.zeros(q.shape)
+            t[b.bl] = yh[k]
+            accw = acc[b.win]
+            accw[b.bl] += mu * (yh[k] + a[k]) - lam * (b.rdiag[b.bl] * yh[k])
+            ct = np.where(b.inbox, (b.deg / q) * (1.0 - 1.0 / q) * t, 0.0)
+            for ((dy, dx), w), (nb_in, nq) in zip(zip(spec.dirs, b.wd), b.nin):
                 # contribution of neighbour i = p + off to pixel p: c_k[i, p] yhat_i
                 ti = spec.shift(t, dy, dx)
-                ct += np.where(nb_in, np.where(inbox, (-w / nq) * (1.0 - 1.0 / q), -w / nq) * ti, 0.0)
-            acc -= lam * ct
-        y = acc / (mu * q)
+                ct += np.where(nb_in, np.where(b.inbox, (-w / nq) * (1.0 - 1.0 / q), -w / nq) * ti, 0.0)
+            accw -= lam * ct
+        y = acc / (mu * spec.q)
         clamped = bool((y < 0).any() or (y > 1).any())
         y = np.clip(y, 0.0, 1.0)
         # ---- residuals, energy, trace, best, multipliers, stop ----
-        res = np.array([math.sqrt(float(np.sum((yh[k] - y[r0:r1, c0:c1]) ** 2)))
-                        for k, ((r0, r1), (c0, c1)) in enumerate(spec.boxes)])
+        res = np.array([math.sqrt(float(np.sum((yh[k] - y[b.win][b.bl]) ** 2))) for k, b in enumerate(blocks)])
         e = float(np.sum(spec.u * y))
-        for t, (dy, dx) in enumerate(spec.dirs[: (4 if spec.conn == 8 else 2)]):
+        for t, (dy, dx) in enumerate(spec.dirs[:nf]):
             e += lam * float(np.sum(spec.wd[t] * (y - spec.shift(y, dy, dx)) ** 2))
         tr["mu"].append(mu)
         tr["energy"].append(e)
@@ -179,8 +191,8 @@ def run(spec: GeneralSpec, mu0: float, mu_fact: float, eps: float, max_iters: in
         tr["clamped"].append(clamped)
         if e < best_e:
             best_e, best_y, best_it = e, y.copy(), it
-        for k, ((r0, r1), (c0, c1)) in enumerate(spec.boxes):
-            a[k] = a[k] + (yh[k] - y[r0:r1, c0:c1])
+        for k, b in enumerate(blocks):
+            a[k] = a[k] + (yh[k] - y[b.win][b.bl])
         mu *= mu_fact
         if res.max() <= eps:
             converged = True

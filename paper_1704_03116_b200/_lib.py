@@ -240,7 +240,7 @@ def lib():
     lb.dope_g_check.restype = C.c_int
     lb.dope_g_check.argtypes = [PG]
     lb.dope_g_last_error.restype = C.c_char_p
-    for name in ("dope_g_admm_init", "dope_g_finish_run"):
+    for name in ("dope_g_admm_init", "dope_g_finish_run", "dope_g_update_blocks", "dope_g_update_global"):
         f = getattr(lb, name)
         f.restype = C.c_int
         f.argtypes = [PG, C.c_void_p]

@@ -528,14 +528,23 @@ static int configure(const VarG *v) {
     return rc;
 }
 
-static int one_iteration(const LatG &o, const VarG *v, cudaStream_t s) {
-    const int M = o.boxh * o.boxw;
+static int blocks_pass(const LatG &o, const VarG *v, cudaStream_t s) {
     v->kernel<<<o.K, v->nt, v->smem, s>>>(o, 1, 1);
+    return cuda_check(cudaGetLastError(), "general K1");
+}
+
+static int global_pass(const LatG &o, cudaStream_t s) {
+    const int M = o.boxh * o.boxw;
     k_global_g<<<o.npe, 256, 0, s>>>(o, o.boxw, M);
     k_residual_g<<<o.K, 256, 0, s>>>(o, o.boxw, M);
     k_energy_g<<<o.npe, 256, 0, s>>>(o);
     k_finalize_g<<<1, 1, 0, s>>>(o);
-    return cuda_check(cudaGetLastError(), "general iteration");
+    return cuda_check(cudaGetLastError(), "general global step");
+}
+
+static int one_iteration(const LatG &o, const VarG *v, cudaStream_t s) {
+    int rc = blocks_pass(o, v, s);
+    return rc ? rc : global_pass(o, s);
 }
 
 }  // namespace dope_g
@@ -616,6 +625,22 @@ int dope_g_admm_run(const dope_general *L, int32_t iters, int32_t use_graph, voi
         cache[key] = exec;
     }
     return cuda_check(cudaGraphLaunch(exec, s), "graph launch");
+}
+
+int dope_g_update_blocks(const dope_general *L, void *stream) {
+    LatG o;
+    const VarG *v;
+    int rc = build(L, o, &v);
+    if (rc) return rc;
+    if ((rc = configure(v))) return rc;
+    return blocks_pass(o, v, (cudaStream_t)stream);
+}
+
+int dope_g_update_global(const dope_general *L, void *stream) {
+    LatG o;
+    int rc = build(L, o, nullptr);
+    if (rc) return rc;
+    return global_pass(o, (cudaStream_t)stream);
 }
 
 int dope_g_finish_run(const dope_general *L, void *stream) {

@@ -157,6 +157,12 @@ class GeneralDevice:
         self._check(_lib.lib().dope_g_admm_run(C.byref(self.L), iters, int(use_graph), self.stream()),
                     "dope_g_admm_run")
 
+    def step_blocks(self):
+        self._check(_lib.lib().dope_g_update_blocks(C.byref(self.L), self.stream()), "dope_g_update_blocks")
+
+    def step_global(self):
+        self._check(_lib.lib().dope_g_update_global(C.byref(self.L), self.stream()), "dope_g_update_global")
+
     def finish(self):
         self._check(_lib.lib().dope_g_finish_run(C.byref(self.L), self.stream()), "dope_g_finish_run")
 

@@ -245,6 +245,14 @@ def by_name(name: str, seed: int = 0) -> Workload:
         return c4(seed)
     if name == "C2":
         return c2(seed)
+    if name == "C2-OV25":
+        # general path: C2's image on 32^2 blocks grown by
+        # 25 % (q in {1, 2, 4}), the reference's default growing mu (mu0 100,
+        # mu_fact 1.05), eps = 0 so every run does its 50 iterations
+        wl = c2(seed, size=1024, block=32, iters=50)
+        wl.name = "C2-ov25"
+        wl.meta = dict(wl.meta or {}, overlap=25, mu0=100.0, mu_fact=1.05)
+        return wl
     if name.startswith("C5"):
         b = int(name.split("-B")[-1]) if "-B" in name else 64
         return c5(b, seed)
