@@ -535,6 +535,11 @@ def run(model: EnergyModel, partition: Partition, config: AdmmConfig,
         problems = assemble_block_problems(model, partition)
     mu0 = config.resolved_mu0(partition.shape.ndim)
     eps = config.resolved_eps(partition)
+    if problems.kind != "float" and partition.shape.ndim == 2 and (
+            mu0 != round(mu0) or problems.lowering.lamw % int(round(mu0)) != 0):
+        # the exact integer path needs mu | lambda*w; otherwise the general path
+        from .general import run_general
+        return run_general(model, partition, config, use_graph=config.use_graph)
     state = init_state(partition, mu0)
     dev = state._bind(problems, config, config.max_iters, eps)
     start = torch.cuda.Event(enable_timing=True)

@@ -95,3 +95,21 @@ def test_general_vs_oracle_256(overlap, conn):
     assert state.iteration == ref["iterations"]
     np.testing.assert_allclose([t.energy for t in state.trace], ref["energy"], rtol=1e-6)
     assert np.count_nonzero(labels != ref["labels"]) <= 1e-4 * labels.size
+
+
+def test_default_config_on_integer_model_uses_general_path():
+    """mu0 = 100 with mu_fact = 1 does not divide lambda*w: run() takes the
+    general path and still matches the general oracle."""
+    import general as og
+    wl = W.mini_disks(128, 32, 6, 2, 10, seed=12, rmax=40.0)
+    rows, cols, vals = wl.pair_arrays()
+    model = dope.EnergyModel(np.asarray(wl.u, dtype=np.float64), dope.SparseWeights(wl.n, rows, cols, vals),
+                             wl.lam)
+    part = dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0)
+    cfg = dope.AdmmConfig(mu0=None, mu_fact=1.0, eps=0.0, max_iters=10)
+    labels, state = dope.run(model, part, cfg)
+    from paper_1704_03116_b200.lowering import lattice_planes
+    planes, c = lattice_planes(model, wl.dims)
+    ref = og.run(og.GeneralSpec(wl.dims, c, wl.u, planes, wl.lam, wl.kpa, 0), 100.0, 1.0, 0.0, 10)
+    np.testing.assert_allclose([t.energy for t in state.trace], ref["energy"], rtol=1e-6)
+    assert np.array_equal(labels, ref["labels"])
