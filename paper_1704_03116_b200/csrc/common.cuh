@@ -15,6 +15,12 @@ constexpr uint16_t HINF = 0xFFFF;
 typedef uint8_t ystore_t;
 typedef int16_t astore_t;
 
+// Programmatic dependent launch: wait for the preceding kernel in the stream
+// (a no-op when this kernel was not launched with the PDL attribute), and
+// let the next one launch once every CTA of this grid has called it.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 __device__ __forceinline__ int byte_at(uint32_t w, int i) { return (int)((w >> (8 * i)) & 0xFFu); }
 __device__ __forceinline__ void unpack_a4(uint2 v, int (&a)[4]) {
     a[0] = (int)(int16_t)(v.x & 0xFFFFu);

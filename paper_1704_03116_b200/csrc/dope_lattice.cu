@@ -128,6 +128,8 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
         L.timeline[8 * k + 4] = (int64_t)t_begin;
         L.timeline[8 * k + 5] = (int64_t)t_begin;
     }
+    griddep_wait();     // the previous consensus pass (PDL launch)
+    griddep_launch();   // all K1 CTAs are resident: the consensus pass may launch
     {
         // both flags in one round trip: a clean CTA must leave its slot fast
         // (4096 CTAs churn through ~5 slots per SM)
@@ -759,6 +761,8 @@ __device__ __forceinline__ void check_a(const Lat2 &L, int a) {
 
 // Generic consensus (any tiling, incl. ragged): one CTA per block, scalar.
 __global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
+    griddep_wait();
+    griddep_launch();
     if (L.st->stop) return;
     const int tid = threadIdx.x;
     CtaAgg agg;
@@ -829,6 +833,8 @@ __global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
 template <int NT>
 __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
     constexpr int QPT = 4;
+    griddep_wait();
+    griddep_launch();
     if (L.st->stop) return;
     const int tid = threadIdx.x;
     CtaAgg agg;
@@ -1228,11 +1234,32 @@ static int configure_plan(const Plan &P) {
     return P.v3 ? configure_k1_3d(P.v3) : configure_k1(P.v);
 }
 
+// Launch with programmatic stream serialisation (PDL): the kernel may start
+// while the previous one drains; it orders itself with griddep_wait().
+// DOPE_NO_PDL=1 falls back to plain launches (same results).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+    static const bool off = getenv("DOPE_NO_PDL") != nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = off ? 0 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 static int launch_k1(const Plan &P, cudaStream_t s) {
     int rc = configure_plan(P);
     if (rc) return rc;
     if (P.v3) P.v3->kernel<<<P.o.K, P.v3->nt, P.v3->smem, s>>>(P.o, default_tune());
-    else P.v->kernel<<<P.o.K, P.v->nt, P.v->smem, s>>>(P.o, default_tune());
+    else return cuda_check(launch_pdl(P.v->kernel, dim3(P.o.K), dim3(P.v->nt), P.v->smem, s, P.o, default_tune()),
+                           "launch K1");
     return cuda_check(cudaGetLastError(), "launch K1");
 }
 
@@ -1320,8 +1347,9 @@ static int launch_k2_tma(const Lat2 &o, cudaStream_t s, int ctas_per_sm) {
     grid = o.K < grid ? o.K : grid;
     const uint32_t magic = (uint32_t)(((1ull << 32) + o.ax.k - 1) / o.ax.k);
     static const int dyn = getenv("DOPE_K2_DYNAMIC") ? 1 : 0;
-    k_consensus_tma<TW, TH, NT, ST><<<grid, C::NT + 32, C::SMEM, s>>>(o, M, magic, dyn);
-    return cuda_check(cudaGetLastError(), "launch K2 (tma)");
+    return cuda_check(launch_pdl(k_consensus_tma<TW, TH, NT, ST>, dim3(grid), dim3(C::NT + 32), (size_t)C::SMEM, s,
+                                 o, M, magic, dyn),
+                      "launch K2 (tma)");
 }
 
 // measured on C3 (tools/k2_variants.sh)
@@ -1341,6 +1369,23 @@ static int k2_tma_width(const Lat2 &o) {
 
 static int launch_k2(const Lat2 &o, cudaStream_t s) {
     if (o.ndim == 3) {
+        // vector path: whole x quads per block row, 4-byte aligned rows
+        const uintptr_t al = (uintptr_t)o.y2[0] | (uintptr_t)o.y2[1] | (uintptr_t)o.y2[2] | (uintptr_t)o.yhat |
+                             ((uintptr_t)o.a >> 1);
+        int lq = -1;
+        for (int l = 0; l <= 5; ++l)
+            if (o.ax.base == (4 << l)) lq = l;
+        if (!getenv("DOPE_NO_VEC3") && lq >= 0 && o.ax.rem == 0 && o.W % 4 == 0 && al % 4 == 0) {
+            const int sms = sm_count();
+            const int v3 = getenv("DOPE_VEC3_NT") ? atoi(getenv("DOPE_VEC3_NT")) : 256;
+            if (v3 == 512)
+                return cuda_check(launch_pdl(k_consensus3d_vec<512>, dim3(o.K < 4 * sms ? o.K : 4 * sms), dim3(512),
+                                             0, s, o, lq),
+                                  "launch K2-3D (vec)");
+            return cuda_check(launch_pdl(k_consensus3d_vec<256>, dim3(o.K < 4 * sms ? o.K : 4 * sms), dim3(256), 0,
+                                         s, o, lq),
+                              "launch K2-3D (vec)");
+        }
         k_consensus3d<<<o.K, 512, 0, s>>>(o);
         return cuda_check(cudaGetLastError(), "launch K2-3D");
     }
@@ -1368,14 +1413,17 @@ static int launch_k2(const Lat2 &o, cudaStream_t s) {
         // counter and the aggregate atomics scale with CTAs, not blocks
         const int sms = sm_count();
         auto grid = [&](int per_sm) { return o.K < per_sm * sms ? o.K : per_sm * sms; };
-        if (quads <= 4 * 32) k_consensus_vec<32><<<grid(32), 32, 0, s>>>(o, lq);
-        else if (quads <= 4 * 64) k_consensus_vec<64><<<grid(24), 64, 0, s>>>(o, lq);
-        else if (quads <= 4 * 256) k_consensus_vec<256><<<grid(8), 256, 0, s>>>(o, lq);
-        else if (quads <= 4 * 1024) k_consensus_vec<1024><<<grid(2), 1024, 0, s>>>(o, lq);
-        else k_consensus<<<grid(8), 256, 0, s>>>(o);
+        cudaError_t e;
+        if (quads <= 4 * 32) e = launch_pdl(k_consensus_vec<32>, dim3(grid(32)), dim3(32), 0, s, o, lq);
+        else if (quads <= 4 * 64) e = launch_pdl(k_consensus_vec<64>, dim3(grid(24)), dim3(64), 0, s, o, lq);
+        else if (quads <= 4 * 256) e = launch_pdl(k_consensus_vec<256>, dim3(grid(8)), dim3(256), 0, s, o, lq);
+        else if (quads <= 4 * 1024) e = launch_pdl(k_consensus_vec<1024>, dim3(grid(2)), dim3(1024), 0, s, o, lq);
+        else e = launch_pdl(k_consensus, dim3(grid(8)), dim3(256), 0, s, o);
+        return cuda_check(e, "launch K2");
     } else {
         const int sms = sm_count();
-        k_consensus<<<o.K < 8 * sms ? o.K : 8 * sms, 256, 0, s>>>(o);
+        return cuda_check(launch_pdl(k_consensus, dim3(o.K < 8 * sms ? o.K : 8 * sms), dim3(256), 0, s, o),
+                          "launch K2");
     }
     return cuda_check(cudaGetLastError(), "launch K2");
 }

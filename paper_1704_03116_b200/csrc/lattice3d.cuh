@@ -321,3 +321,155 @@ __global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
         pass_tail(L, agg, cur, best, out);
     }
 }
+
+// Vectorised 3D consensus (blocks whose x extent is a multiple of 4 on a grid
+// whose width is too): thread t owns quads of 4 consecutive x voxels; the
+// quads of one block row sit in consecutive lanes, so the energy's +x pair of
+// a quad's last voxel comes from the next lane.  Loads are issued in batches
+// of 4 quads before any is used.  Persistent over blocks; same arithmetic as
+// k_consensus3d.
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_consensus3d_vec(Lat2 L, int lq) {
+    constexpr int QB = 4;   // quads per load batch
+    griddep_wait();
+    griddep_launch();
+    if (L.st->stop) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    CtaAgg agg;
+    const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
+    const ystore_t *__restrict__ y_in = L.y2[cur];
+    ystore_t *__restrict__ y_out = L.y2[out];
+    const astore_t *a_in = L.a;
+    astore_t *a_out = L.fuse ? L.a : nullptr;
+    const bool want_e = L.fuse && L.st->iteration >= 1;
+    const int32_t W = L.W, H = L.ay.dim, D = L.az.dim, q = L.q;
+    const int64_t HW = (int64_t)H * W;
+    const int QR = 1 << lq;
+    __shared__ int64_t red_e[NT / 32], red_s[NT / 32], red_u[NT / 32];
+    __shared__ unsigned red_f[NT / 32];
+    for (int k = blockIdx.x; k < L.K; k += gridDim.x) {
+        int bz, by, bx;
+        const Geo3 gb = block_geo3(L, k, bz, by, bx);
+        const bool up_z = gb.lo_z > 0, dn_z = gb.lo_z + gb.dz < D;
+        const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
+        const bool lf_c = gb.lo_c > 0, rt_c = gb.lo_c + gb.wc < W;
+        const int nq = (gb.dz * gb.hr) << lq;
+        int64_t e_acc = 0, du = 0;
+        int ss = 0;
+        unsigned marks = 0, clamp_or = 0;   // marks: bit0 self, 1..6 -x +x -y +y -z +z
+        for (int t0 = 0; t0 < nq; t0 += QB * NT) {
+            uint32_t yh4[QB], yo[QB], nb[QB], cnt[QB], yb[QB], yz[QB];
+            uint2 av[QB];
+            int yr[QB];
+#pragma unroll
+            for (int j = 0; j < QB; ++j) {
+                const int t = t0 + tid + j * NT;
+                yh4[j] = yo[j] = nb[j] = cnt[j] = yb[j] = yz[j] = 0;
+                av[j] = make_uint2(0, 0);
+                yr[j] = 0;
+                if (t < nq) {
+                    const int row = t >> lq, c0 = (t & (QR - 1)) << 2;
+                    const int z = row / gb.hr, r = row - z * gb.hr;
+                    const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + r) * W + gb.lo_c + c0;
+                    yh4[j] = __ldcs(reinterpret_cast<const unsigned int *>(L.yhat + G));
+                    av[j] = __ldcs(reinterpret_cast<const uint2 *>(a_in + G));
+                    yo[j] = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G));
+                    if (want_e) {
+                        if (gb.lo_r + r + 1 < H) yb[j] = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G + W));
+                        if (gb.lo_z + z + 1 < D) yz[j] = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G + HW));
+                        if (c0 + 4 == gb.wc && gb.lo_c + c0 + 4 < W) yr[j] = y_in[G + 4];
+                    }
+                    // cross-block neighbour labels: count / sum per voxel (bytes)
+                    if (r == 0 && up_r) { cnt[j] += 0x01010101u; nb[j] += *reinterpret_cast<const uint32_t *>(L.yhat + G - W); }
+                    if (r == gb.hr - 1 && dn_r) { cnt[j] += 0x01010101u; nb[j] += *reinterpret_cast<const uint32_t *>(L.yhat + G + W); }
+                    if (z == 0 && up_z) { cnt[j] += 0x01010101u; nb[j] += *reinterpret_cast<const uint32_t *>(L.yhat + G - HW); }
+                    if (z == gb.dz - 1 && dn_z) { cnt[j] += 0x01010101u; nb[j] += *reinterpret_cast<const uint32_t *>(L.yhat + G + HW); }
+                    if (c0 == 0 && lf_c) { cnt[j] += 1u; nb[j] += L.yhat[G - 1]; }
+                    if (c0 + 4 == gb.wc && rt_c) { cnt[j] += 1u << 24; nb[j] += (uint32_t)L.yhat[G + 4] << 24; }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < QB; ++j) {
+                const int t = t0 + tid + j * NT;
+                const uint32_t nxt = __shfl_down_sync(FULLMASK, yo[j], 1);
+                if (t >= nq) continue;
+                const int row = t >> lq, c0 = (t & (QR - 1)) << 2;
+                const int z = row / gb.hr, r = row - z * gb.hr;
+                const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + r) * W + gb.lo_c + c0;
+                if (want_e) {
+                    // y2 bytes are 0/2: each differing pair is one set bit of the XOR
+                    uint32_t rw;
+                    if (c0 + 4 < gb.wc) rw = nxt;
+                    else rw = (gb.lo_c + c0 + 4 < W) ? (uint32_t)yr[j] : (yo[j] >> 24);
+                    int qd = __popc(yo[j] ^ __funnelshift_r(yo[j], rw, 8));
+                    if (gb.lo_r + r + 1 < H) qd += __popc(yo[j] ^ yb[j]);
+                    if (gb.lo_z + z + 1 < D) qd += __popc(yo[j] ^ yz[j]);
+                    e_acc += (int64_t)L.lamw * qd;
+                }
+                // y = clamp(h + a - q*sx), sx = cnt*h - nb (biased by 4)
+                const uint32_t h4 = yh4[j];
+                const uint32_t sb = ((cnt[j] & (h4 * 0xFFu)) | 0x04040404u) - nb[j];
+                int a4[4];
+                unpack_a4(av[j], a4);
+                int y[4], an[4];
+                uint32_t yw = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int h = (int)((h4 >> (8 * i)) & 0xFFu);
+                    const int p = a4[i] + h + 4 * q - q * (int)((sb >> (8 * i)) & 0xFFu);
+                    clamp_or |= (uint32_t)p;
+                    y[i] = p > 0 ? 1 : 0;
+                    an[i] = a4[i] + h - y[i];
+                    ss += h ^ y[i];
+                    yw |= (uint32_t)(2 * y[i]) << (8 * i);
+                }
+                if (a_out) __stcs(reinterpret_cast<uint2 *>(a_out + G), pack_a4(an[0], an[1], an[2], an[3]));
+                __stcg(reinterpret_cast<unsigned int *>(y_out + G), yw);
+                const uint32_t chg = yw ^ yo[j];
+                const uint32_t hb = ((h4 * 0x01020408u) >> 24) & 0xFu;
+                const uint32_t yb4 = (uint32_t)(y[0] | (y[1] << 1) | (y[2] << 2) | (y[3] << 3));
+                if (chg | (hb ^ yb4)) marks |= 1u;
+                if (chg) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int dy = (int)((yw >> (8 * i)) & 0xFFu) - (int)((yo[j] >> (8 * i)) & 0xFFu);
+                        if (dy) du += (int64_t)__ldg(L.u + G + i) * dy;
+                    }
+                    if (c0 == 0 && lf_c && (chg & 0xFFu)) marks |= 2u;
+                    if (c0 + 4 == gb.wc && rt_c && (chg >> 24)) marks |= 4u;
+                    if (r == 0 && up_r) marks |= 8u;
+                    if (r == gb.hr - 1 && dn_r) marks |= 16u;
+                    if (z == 0 && up_z) marks |= 32u;
+                    if (z == gb.dz - 1 && dn_z) marks |= 64u;
+                }
+            }
+        }
+        // block reduction
+        e_acc = warp_sum(e_acc);
+        du = warp_sum(du);
+        const int sq = (int)__reduce_add_sync(FULLMASK, (unsigned)ss);
+        const unsigned fm = __reduce_or_sync(FULLMASK, marks | (clamp_or > 1u ? 128u : 0u));
+        if (lane == 0) { red_e[warp] = e_acc; red_s[warp] = sq; red_u[warp] = du; red_f[warp] = fm; }
+        __syncthreads();
+        if (tid == 0) {
+            int64_t E = 0, S = 0, U = 0;
+            unsigned Fm = 0;
+            for (int w = 0; w < NT / 32; ++w) { E += red_e[w]; S += red_s[w]; U += red_u[w]; Fm |= red_f[w]; }
+            L.pe[k] = E;
+            L.pu[k] = U;
+            L.pr[k] = S;
+            L.pf[k] = (Fm & 128u) ? 1 : 0;
+            const int KX = L.ax.k, KYX = L.ay.k * L.ax.k;
+            if (Fm & 1u) L.dirty[k] = 1u;
+            if (Fm & 2u) L.dirty[k - 1] = 1u;
+            if (Fm & 4u) L.dirty[k + 1] = 1u;
+            if (Fm & 8u) L.dirty[k - KX] = 1u;
+            if (Fm & 16u) L.dirty[k + KX] = 1u;
+            if (Fm & 32u) L.dirty[k - KYX] = 1u;
+            if (Fm & 64u) L.dirty[k + KYX] = 1u;
+            agg.add_block(E, U, S, (Fm & 128u) ? 1 : 0);
+        }
+        __syncthreads();
+    }
+    if (tid == 0) pass_tail(L, agg, cur, best, out);
+}
