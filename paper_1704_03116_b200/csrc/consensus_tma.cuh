@@ -167,8 +167,28 @@ __device__ __forceinline__ uint32_t quad_update(uint32_t h4, uint2 a2, uint32_t 
 struct StageInfo {
     int k;          // block id, or -1: no more work
     int tile;       // tile index within the block
-    int flags;      // bit0 re-solved this iteration, bit1 interior clamp memo, bit2 last tile
+    int flags;      // bit0 re-solved this iteration, bit1 interior clamp memo, bit2 last tile,
+                    // bits 3-6 neighbour across L / R / U / D re-solved this iteration,
+                    // bits 8-15 ring-group clamp memos (see ring_group)
 };
+
+// Ring groups of a block's boundary quads (clamp memos, part_flags bits
+// 8-15): 0 left edge, 1 right edge, 2 top edge, 3 bottom edge, 4-7 corners
+// TL TR BL BR; -1 = interior.  A group of a clean block can only move when a
+// neighbour across one of its sides was re-solved this iteration.
+__device__ __forceinline__ int ring_group(bool lft, bool rgt, bool top, bool bot) {
+    if (top) return lft ? 4 : (rgt ? 5 : 2);
+    if (bot) return lft ? 6 : (rgt ? 7 : 3);
+    if (lft) return 0;
+    if (rgt) return 1;
+    return -1;
+}
+
+// groups touching the re-solved sides (side bits: 1 L, 2 R, 4 U, 8 D)
+__device__ __forceinline__ uint32_t active_groups(uint32_t sides) {
+    const uint32_t L = sides & 1u, R = (sides >> 1) & 1u, U = (sides >> 2) & 1u, D = (sides >> 3) & 1u;
+    return L | (R << 1) | (U << 2) | (D << 3) | ((L | U) << 4) | ((R | U) << 5) | ((L | D) << 6) | ((R | D) << 7);
+}
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -239,6 +259,20 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
         int nk[CA] = {};
         uint32_t nep[CA] = {};
         int nmemo[CA] = {};
+        uint32_t nside[CA] = {};                       // neighbours re-solved (L R U D bits)
+        const int KY = K / KX;
+        const uint32_t ep_now = (uint32_t)(iter + 1);
+        // side bits of block kk: the neighbour's solve epoch is this iteration
+        // (a ghost row from another shard is always treated as moved)
+        auto sides_of = [&](int kk) -> uint32_t {
+            const int by = (int)__umulhi((uint32_t)kk, kx_magic), bx = kk - by * KX;
+            uint32_t sd = 0;
+            if (bx > 0 && L.dirty[K + kk - 1] == ep_now) sd |= 1u;
+            if (bx + 1 < KX && L.dirty[K + kk + 1] == ep_now) sd |= 2u;
+            if (by > 0 ? L.dirty[K + kk - KX] == ep_now : L.gup != 0) sd |= 4u;
+            if (by + 1 < KY ? L.dirty[K + kk + KX] == ep_now : L.gdn != 0) sd |= 8u;
+            return sd;
+        };
         int nstatic = 0;
         auto claim = [&]() -> int {
             if (!dyn) return (int)blockIdx.x + (nstatic++) * (int)gridDim.x;
@@ -251,6 +285,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
             if (nk[i] < K) {
                 nep[i] = L.dirty[K + nk[i]];
                 nmemo[i] = L.pf[nk[i]];
+                nside[i] = sides_of(nk[i]);
             }
         CtaAgg agg;   // this CTA's pass aggregates (exact integers)
         auto drain = [&](int s) {
@@ -265,12 +300,19 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
             accS[s] = 0;
             accF[s] = 0;
             accU[s] = 0;
-            const bool memo = (info.flags & 1) ? (f & 64u) != 0 : (info.flags & 2) != 0;
-            const int clamped = ((f & 1u) || memo) ? 1 : 0;
+            const bool solved = info.flags & 1;
+            const bool memo = solved ? (f & 64u) != 0 : (info.flags & 2) != 0;
+            // ring groups: recomputed ones take this pass's clamp bits, the
+            // others (clean block, no re-solved neighbour on their sides) keep
+            // their memo
+            const uint32_t fresh = (f >> 8) & 0xFFu;
+            const uint32_t act = solved ? 0xFFu : active_groups((uint32_t)(info.flags >> 3) & 0xFu);
+            const uint32_t gbits = (fresh & act) | (((uint32_t)info.flags >> 8) & 0xFFu & ~act);
+            const int clamped = (gbits || memo) ? 1 : 0;
             L.pe[k] = e;
             L.pu[k] = u2;
             L.pr[k] = sq;
-            L.pf[k] = clamped | (memo ? 64 : 0);
+            L.pf[k] = clamped | (memo ? 64 : 0) | (int)(gbits << 8);
             agg.add_block(e, u2, sq, clamped);
             if (f & 2u) L.dirty[k] = 1u;
             if (f & 4u) L.dirty[k - 1] = 1u;
@@ -293,17 +335,20 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
                     break;
                 }
                 pk = nk[0];
-                pflags = ((!L.skip_clean || nep[0] == (uint32_t)(iter + 1)) ? 1 : 0) | ((nmemo[0] & 64) ? 2 : 0);
+                pflags = ((!L.skip_clean || nep[0] == (uint32_t)(iter + 1)) ? 1 : 0) | ((nmemo[0] & 64) ? 2 : 0) |
+                         (int)(nside[0] << 3) | (nmemo[0] & 0xFF00);
                 ptile = 0;
 #pragma unroll
                 for (int i = 0; i + 1 < CA; ++i) {
                     nk[i] = nk[i + 1];
                     nep[i] = nep[i + 1];
                     nmemo[i] = nmemo[i + 1];
+                    nside[i] = nside[i + 1];
                 }
                 if (nk[CA - 2] < K) {   // claimed last time: its claim has returned
                     nep[CA - 2] = L.dirty[K + nk[CA - 2]];
                     nmemo[CA - 2] = L.pf[nk[CA - 2]];
+                    nside[CA - 2] = sides_of(nk[CA - 2]);
                 }
                 nk[CA - 1] = nk[CA - 2] < K ? claim() : K;
             }
@@ -340,8 +385,8 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
     int64_t du = 0;
     int ss = 0, quad_acc = 0;
     // fl: bit1 self, bit2 left, bit3 right, bit4 up, bit5 down
-    // clp: OR of the pre-clamp values of ring quads, clpi: interior quads
-    uint32_t fl = 0, clp = 0, clpi = 0;
+    // gcl: ring-group clamp bits; clpi: OR of the interior quads' pre-clamp values
+    uint32_t fl = 0, gcl = 0, clpi = 0;
     for (int n = 0;; ++n) {
         const int s = n % ST;
         mbar_wait(&full[s], (n / ST) & 1);
@@ -377,12 +422,12 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
             // consensus update of one quad given its multipliers, own labels
             // and cross-block neighbour labels (count / sum per pixel)
             auto update = [&](int rr, int c0, uint32_t yo, uint32_t h4, uint2 av, uint32_t cnt, uint32_t nb,
-                              bool lft, bool rgt, bool top, bool bot, bool ring) {
+                              bool lft, bool rgt, bool top, bool bot, int grp) {
                 const int64_t G = gt + (int64_t)rr * W + c0;
                 uint2 an;
                 uint32_t cq = 0;
                 const uint32_t yn = quad_update(h4, av, cnt, nb, q, q4, an, cq);
-                if (ring) clp |= cq;
+                if (grp >= 0) gcl |= (cq > 1u ? 1u : 0u) << grp;
                 else clpi |= cq;
                 const uint32_t hb = bits_b01(h4);
                 ss += __popc(hb ^ yn);
@@ -420,22 +465,60 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
                     if (bot) { cnt += 0x01010101u; nb += *reinterpret_cast<const uint32_t *>(hrow + C::YHW); }
                     if (lft) { cnt += 1u; nb += hrow[-1]; }
                     if (rgt) { cnt += 1u << 24; nb += (uint32_t)hrow[4] << 24; }
-                    update(rr, c0, yo, h4, av, cnt, nb, lft, rgt, top, bot, lft | rgt | top | bot);
+                    update(rr, c0, yo, h4, av, cnt, nb, lft, rgt, top, bot, ring_group(lft, rgt, top, bot));
                 }
             } else {
                 // clean block: the interior is a fixed point, so the bulk pass
                 // only carries y into the rotating buffer (and the energy); the
                 // ring quads -- the only ones a neighbour's new labels can move
                 // -- are updated in a second pass spread over all threads
+                // -- and only on the sides whose neighbour was re-solved.  The
+                // bulk pass works on 16-byte chunks (4 quads per thread step).
                 const bool tile_top = tile == 0 && has_up, tile_bot = tile == tpb - 1 && has_dn;
+                const uint32_t act = active_groups((uint32_t)(info.flags >> 3) & 0xFu);
+                constexpr int CPR = TW / 16, NCH = TH * TW / 16;   // chunks per row / per tile
+                for (int ci = tid; ci < NCH; ci += NT) {
+                    const int rr = ci / CPR, cc = (ci % CPR) * 16;
+                    const uint4 yo = *reinterpret_cast<const uint4 *>(sy + rr * TW + cc);
+                    if (want_e) {
+                        // pairs of the previous iterate: bytes are 0/2, so each
+                        // differing pair is one set bit of the XOR
+                        const uint32_t nx = __shfl_down_sync(FULLMASK, yo.x, 1);
+                        uint32_t rw = nx;
+                        if (cc + 16 == TW) rw = has_rt ? (uint32_t)syr[rr * 16] : (yo.w >> 24);
+                        const uint4 yb = (r0 + rr + 1 < BH || last_row_pairs)
+                                             ? *reinterpret_cast<const uint4 *>(sy + (rr + 1) * TW + cc)
+                                             : yo;
+                        quad_acc += __popc(yo.x ^ __funnelshift_r(yo.x, yo.y, 8)) +
+                                    __popc(yo.y ^ __funnelshift_r(yo.y, yo.z, 8)) +
+                                    __popc(yo.z ^ __funnelshift_r(yo.z, yo.w, 8)) +
+                                    __popc(yo.w ^ __funnelshift_r(yo.w, rw, 8)) + __popc(yo.x ^ yb.x) +
+                                    __popc(yo.y ^ yb.y) + __popc(yo.z ^ yb.z) + __popc(yo.w ^ yb.w);
+                    }
+                    // carry y into the rotating buffer, except the words of
+                    // active ring quads (the ring pass writes those)
+                    uint32_t skip = 0;
+                    const bool trow = rr == 0 && tile_top, brow = rr == TH - 1 && tile_bot;
+                    if (trow || brow) {
 #pragma unroll
-                for (int j = 0; j < QPT; ++j) {
-                    const int rr = rr_[j], c0 = c0_[j];
-                    const uint32_t yo = *reinterpret_cast<const uint32_t *>(sy + rr * TW + c0);
-                    if (want_e) pair_energy(rr, c0, yo);
-                    const bool ring = (c0 == 0 && has_lf) || (c0 + 4 == TW && has_rt) || (rr == 0 && tile_top) ||
-                                      (rr == TH - 1 && tile_bot);
-                    if (!ring) __stcg(reinterpret_cast<unsigned int *>(y_out + gt + (int64_t)rr * W + c0), yo);
+                        for (int w = 0; w < 4; ++w) {
+                            const int c0 = cc + 4 * w;
+                            const int grp = ring_group(c0 == 0 && has_lf, c0 + 4 == TW && has_rt, trow, brow);
+                            if (grp >= 0 && ((act >> grp) & 1u)) skip |= 1u << w;
+                        }
+                    } else {
+                        if (cc == 0 && has_lf && (act & 1u)) skip |= 1u;
+                        if (cc + 16 == TW && has_rt && (act & 2u)) skip |= 8u;
+                    }
+                    const int64_t G = gt + (int64_t)rr * W + cc;
+                    if (!skip) {
+                        __stcg(reinterpret_cast<uint4 *>(y_out + G), yo);
+                    } else {
+                        const uint32_t wv[4] = {yo.x, yo.y, yo.z, yo.w};
+#pragma unroll
+                        for (int w = 0; w < 4; ++w)
+                            if (!((skip >> w) & 1u)) __stcg(reinterpret_cast<unsigned int *>(y_out + G) + w, wv[w]);
+                    }
                 }
                 // ring candidates: the block's first / last row when this tile
                 // holds it, then the two edge quads of the remaining rows
@@ -449,7 +532,8 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
                     else { const int jj = i - nT - nB; rr = rlo + (jj >> 1); c0 = (jj & 1) ? TW - 4 : 0; }
                     const bool lft = (c0 == 0) && has_lf, rgt = (c0 + 4 == TW) && has_rt;
                     const bool top = rr == 0 && tile_top, bot = rr == TH - 1 && tile_bot;
-                    if (!(lft | rgt | top | bot)) continue;
+                    const int grp = ring_group(lft, rgt, top, bot);
+                    if (grp < 0 || !((act >> grp) & 1u)) continue;   // fixed point: copied by the bulk pass
                     const uint32_t yo = *reinterpret_cast<const uint32_t *>(sy + rr * TW + c0);
                     uint2 av;
                     if (lft) av = *reinterpret_cast<const uint2 *>(sb + C::O_AL + rr * 16);
@@ -462,7 +546,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
                     if (bot) { cnt += 0x01010101u; nb += *reinterpret_cast<const uint32_t *>(sb + C::O_HDN + c0); }
                     if (lft) { cnt += 1u; nb += sb[C::O_HL + rr * 16 + 15]; }
                     if (rgt) { cnt += 1u << 24; nb += (uint32_t)sb[C::O_HR + rr * 16] << 24; }
-                    update(rr, c0, yo, h4, av, cnt, nb, lft, rgt, top, bot, true);
+                    update(rr, c0, yo, h4, av, cnt, nb, lft, rgt, top, bot, grp);
                 }
             }
         }
@@ -470,7 +554,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
             // block done in this warp: one shared atomic per quantity
             const unsigned e = __reduce_add_sync(FULLMASK, (unsigned)quad_acc);
             const unsigned sq = __reduce_add_sync(FULLMASK, (unsigned)ss);
-            const unsigned f = __reduce_or_sync(FULLMASK, fl | (clp > 1u ? 1u : 0u) | (clpi > 1u ? 64u : 0u));
+            const unsigned f = __reduce_or_sync(FULLMASK, fl | (gcl << 8) | (clpi > 1u ? 64u : 0u));
             int64_t u2 = 0;
             if (__any_sync(FULLMASK, du != 0)) u2 = warp_sum(du);
             if (lane == 0) {
@@ -483,7 +567,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
             ss = 0;
             quad_acc = 0;
             fl = 0;
-            clp = 0;
+            gcl = 0;
             clpi = 0;
         }
         // this warp is done with stage s
