@@ -480,7 +480,78 @@ def main():
 
     # ---- e2e through the C ABI with host buffers ----
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and ws == 1 and not args.sharded:
+        # production pipelining: every step copies its unaries from pinned
+        # host memory and reads its labels + trace back, but the copies run
+        # on a second stream behind / ahead of the previous / next step's
+        # solve (double-buffered device inputs and outputs)
+        import ctypes as C
+        from paper_1704_03116_b200 import _lib
+        u_host = problems.u.cpu().pin_memory()
+        u_bytes = u_host.numel() * u_host.element_size()
+        U = [problems.u, torch.empty_like(problems.u)]
+        lab_dev = [torch.empty(n, dtype=torch.uint8, device=problems.u.device) for _ in range(2)]
+        tr_dev = [torch.empty_like(dev.tr_e) for _ in range(2)]
+        lab_host = [torch.empty(n, dtype=torch.uint8).pin_memory() for _ in range(2)]
+        tr_host = [torch.empty(dev.tr_e.numel(), dtype=dev.tr_e.dtype).pin_memory() for _ in range(2)]
+        # both on non-default streams: the legacy default stream would
+        # serialise with the copy stream
+        comp = torch.cuda.Stream()
+        cs = torch.cuda.Stream()        # host -> device
+        co = torch.cuda.Stream()        # device -> host (its own queue: a D2H waiting
+        comp.wait_stream(torch.cuda.current_stream())   # for a solve must not hold up the next H2D)
+        used = [torch.cuda.Event() for _ in range(2)]     # compute on buffer i finished
+        ready = [torch.cuda.Event() for _ in range(2)]    # input copy into buffer i finished
+        fetched = [torch.cuda.Event() for _ in range(2)]  # results of buffer i are on the host
+        lb = _lib.lib()
+        binarize = lb.dope_f_binarize if is_float else lb.dope_binarize
+        total = args.warmup + args.steps
+
+        def h2d(i, first):
+            with torch.cuda.stream(cs):
+                if not first:
+                    cs.wait_event(used[i])
+                U[i].copy_(u_host, non_blocking=True)
+                ready[i].record(cs)
+
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        h2d(0, True)
+        for s in range(total):
+            i = s % 2
+            if s == args.warmup:
+                torch.cuda.synchronize()
+                e0.record(comp)
+                h2d(i, True)            # this step's copy inside the timed region
+            comp.wait_event(ready[i])
+            if s >= 2:
+                comp.wait_event(fetched[i])   # output buffers i are free again
+            dev.L.u = U[i].data_ptr()
+            with torch.cuda.stream(comp):
+                step()
+                _lib.check(binarize(C.byref(dev.L), lab_dev[i].data_ptr(), C.c_void_p(comp.cuda_stream)),
+                           "binarize")
+                tr_dev[i].copy_(dev.tr_e)
+            used[i].record(comp)
+            with torch.cuda.stream(co):
+                co.wait_event(used[i])
+                lab_host[i].copy_(lab_dev[i], non_blocking=True)
+                tr_host[i].copy_(tr_dev[i], non_blocking=True)
+                fetched[i].record(co)
+            if s + 1 < total and s + 1 != args.warmup:
+                h2d((s + 1) % 2, False)   # next step's input overlaps this solve
+        comp.wait_stream(cs)
+        comp.wait_stream(co)
+        e1.record(comp)
+        torch.cuda.synchronize()
+        torch.cuda.current_stream().wait_stream(comp)
+        dev.L.u = problems.u.data_ptr()
+        ms_e2e = e0.elapsed_time(e1)
+        e2e = {"value": iters_done * args.steps / (ms_e2e / 1e3), "unit": "iterations/s",
+               "h2d_bytes_per_step": u_bytes, "d2h_bytes_per_step": n + 8 * iters,
+               "pipelining": "double-buffered: step s+1's H2D and step s's D2H on copy streams "
+                             "overlap the solves"}
+    elif not args.no_e2e:
         u_host = problems.u.cpu().pin_memory()
         u_bytes = u_host.numel() * u_host.element_size()
         lab_host = torch.empty(n, dtype=torch.int8).pin_memory()
