@@ -262,7 +262,11 @@ __device__ void apply_f(const LatF &L, double E2, double R2, double M2, int F2, 
     st->ycur = out;
 }
 
-__global__ void __launch_bounds__(256) k_consensus_f(LatF L) {
+// K2f threads per CTA: a 64^2 block is 4096 pixels, so 1024 threads give each
+// thread 4 (the per-pixel work is a chain of dependent loads)
+constexpr int K2F_NT = 1024;
+
+__global__ void __launch_bounds__(K2F_NT) k_consensus_f(LatF L) {
     if (L.st->stop) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int k = blockIdx.x;
@@ -282,18 +286,28 @@ __global__ void __launch_bounds__(256) k_consensus_f(LatF L) {
     if (tid == 0) nbmark = 0;
     __syncthreads();
 
+    // read-only planes through restrict-qualified pointers: the loads of
+    // the next pixels may be issued ahead of this pixel's stores
+    const double *__restrict__ uu = L.u;
+    const double *__restrict__ rdg = L.rdiag;
+    const double *__restrict__ w0 = L.w[0];
+    const double *__restrict__ w1 = L.w[1];
+    const double *__restrict__ w2 = L.w[2];
+    const double *__restrict__ w3 = L.w[3];
+    const uint8_t *__restrict__ yhp = L.yhat;
     double e_acc = 0.0, ss = 0.0;
     int clamped = 0;
     unsigned marks = 0;
     const int m = hr * wc;
-    for (int v = tid; v < m; v += blockDim.x) {
+#pragma unroll 4
+    for (int v = tid; v < m; v += K2F_NT) {
         const int r = v / wc, c = v - r * wc;
         const int32_t R = lo_r + r, Cc = lo_c + c;
         const int64_t G = (int64_t)R * W + Cc;
-        const double yh = (double)L.yhat[G];
+        const double yh = (double)yhp[G];
         const double av = a_in[G];
         // own-block term and cross-block coupling sums, in block-id order
-        double own = L.mu * (yh + av) - L.lam * (L.rdiag[G] * yh);
+        double own = L.mu * (yh + av) - L.lam * (rdg[G] * yh);
         int nb_blk[8];
         double nb_term[8];
         int64_t nb_idx[8];
@@ -344,16 +358,16 @@ __global__ void __launch_bounds__(256) k_consensus_f(LatF L) {
         if (want_e) {
             double q = 0.0;
             // pairs owned by this pixel: E S SE SW (forward planes)
-            if (Cc + 1 < W) { const double d = yold - y_in[G + 1]; q += L.w[0][G] * (d * d); }
+            if (Cc + 1 < W) { const double d = yold - y_in[G + 1]; q += w0[G] * (d * d); }
             if (R + 1 < H) {
                 const double d = yold - y_in[G + W];
-                q += L.w[1][G] * (d * d);
+                q += w1[G] * (d * d);
                 if (L.ndir == 8) {
-                    if (Cc + 1 < W) { const double d2 = yold - y_in[G + W + 1]; q += L.w[2][G] * (d2 * d2); }
-                    if (Cc > 0) { const double d3 = yold - y_in[G + W - 1]; q += L.w[3][G] * (d3 * d3); }
+                    if (Cc + 1 < W) { const double d2 = yold - y_in[G + W + 1]; q += w2[G] * (d2 * d2); }
+                    if (Cc > 0) { const double d3 = yold - y_in[G + W - 1]; q += w3[G] * (d3 * d3); }
                 }
             }
-            e_acc += L.u[G] * yold + L.lam * q;
+            e_acc += uu[G] * yold + L.lam * q;
         }
         const bool ychg = (y != yold);
         if (ychg || (av + (yh - y)) != av) marks |= 1u;
@@ -366,8 +380,9 @@ __global__ void __launch_bounds__(256) k_consensus_f(LatF L) {
             }
         }
     }
-    __shared__ double red_e[8], red_s[8];
-    __shared__ int red_f[8];
+    constexpr int NWARP = K2F_NT / 32;
+    __shared__ double red_e[NWARP], red_s[NWARP];
+    __shared__ int red_f[NWARP];
     __shared__ int last;
     e_acc = warp_sum(e_acc);
     ss = warp_sum(ss);
@@ -383,7 +398,7 @@ __global__ void __launch_bounds__(256) k_consensus_f(LatF L) {
     if (tid == 0) {
         double E = 0.0, S = 0.0;
         int F = 0;
-        for (int w = 0; w < 8; ++w) { E += red_e[w]; S += red_s[w]; F |= red_f[w]; }
+        for (int w = 0; w < NWARP; ++w) { E += red_e[w]; S += red_s[w]; F |= red_f[w]; }
         L.pe[k] = E;
         L.pr[k] = S;
         L.pf[k] = F;
@@ -399,8 +414,8 @@ __global__ void __launch_bounds__(256) k_consensus_f(LatF L) {
     __syncthreads();
     if (last) {
         __threadfence();
-        __shared__ double sE[8], sR[8], sM[8];
-        __shared__ int sF[8];
+        __shared__ double sE[NWARP], sR[NWARP], sM[NWARP];
+        __shared__ int sF[NWARP];
         if (!L.fuse) {
             if (tid == 0) {
                 L.st->ybest = best;
@@ -431,7 +446,7 @@ __global__ void __launch_bounds__(256) k_consensus_f(LatF L) {
         if (tid == 0) {
             double E2 = 0.0, RR = 0.0, MM = -1.0;
             int FF = 0;
-            for (int w = 0; w < 8; ++w) {
+            for (int w = 0; w < NWARP; ++w) {
                 E2 += sE[w]; RR += sR[w]; MM = sM[w] > MM ? sM[w] : MM; FF |= sF[w];
             }
             apply_f(L, E2, RR, MM, FF, cur, best, out);
@@ -627,7 +642,7 @@ static int launch_k1(const LatF &o, const VarF *v, cudaStream_t s) {
 }
 
 static int launch_k2(const LatF &o, cudaStream_t s) {
-    k_consensus_f<<<o.K, 256, 0, s>>>(o);
+    k_consensus_f<<<o.K, K2F_NT, 0, s>>>(o);
     return cuda_check(cudaGetLastError(), "launch K2f");
 }
 
