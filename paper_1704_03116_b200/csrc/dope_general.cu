@@ -260,16 +260,27 @@ __global__ void __launch_bounds__(256) k_global_g(LatG L, int boxw, int M) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
         const int R = (int)(p / L.W), Cc = (int)(p - (int64_t)R * L.W);
         const double qp = (double)L.q[p];
-        // candidate blocks: the base-range owner +-1 on each axis
+        // the pixel's stencil, loaded once: weights and neighbour block counts
+        double wd[8], qd[8];
+        double d = 0.0;
+#pragma unroll
+        for (int dd = 0; dd < 8; ++dd) {
+            wd[dd] = dd < L.ndir ? wpair(L, R, Cc, dd) : 0.0;
+            qd[dd] = wd[dd] != 0.0 ? (double)L.q[(int64_t)(R + dy_of(dd)) * L.W + Cc + dx_of(dd)] : 1.0;
+            d += wd[dd];
+        }
+        // candidate blocks: the base-range owner +-1 on each axis (boxes grow
+        // by less than a block length, so nothing further holds the pixel or
+        // its ring), in block order
         int by0 = R / (baseY > 0 ? baseY : 1), bx0 = Cc / (baseX > 0 ? baseX : 1);
         by0 = by0 >= L.KY ? L.KY - 1 : by0;
         bx0 = bx0 >= L.KX ? L.KX - 1 : bx0;
         double acc = 0.0;
-        for (int by = by0 - 2; by <= by0 + 2; ++by) {
+        for (int by = by0 - 1; by <= by0 + 1; ++by) {
             if (by < 0 || by >= L.KY) continue;
             const int lr = L.rg[by], hr = L.rg[L.KY + by];
             if (R < lr - 1 || R > lr + hr) continue;
-            for (int bx = bx0 - 2; bx <= bx0 + 2; ++bx) {
+            for (int bx = bx0 - 1; bx <= bx0 + 1; ++bx) {
                 if (bx < 0 || bx >= L.KX) continue;
                 const int lc = L.rg[2 * L.KY + bx], wc = L.rg[2 * L.KY + L.KX + bx];
                 if (Cc < lc - 1 || Cc > lc + wc) continue;
@@ -277,24 +288,22 @@ __global__ void __launch_bounds__(256) k_global_g(LatG L, int boxw, int M) {
                 const Box b{lr, hr, lc, wc};
                 const uint8_t *yk = L.yhat + (size_t)k * M;
                 const bool inb = b.holds(R, Cc);
-                double ct = 0.0;
+                double ct = 0.0, dhat = 0.0;
+#pragma unroll
+                for (int dd = 0; dd < 8; ++dd) {
+                    if (wd[dd] == 0.0) continue;
+                    const int rn = R + dy_of(dd), cn = Cc + dx_of(dd);
+                    if (!b.holds(rn, cn)) continue;
+                    const double yi = yk[(rn - lr) * boxw + (cn - lc)];
+                    ct += inb ? (-wd[dd] / qd[dd]) * (1.0 - 1.0 / qp) * yi : (-wd[dd] / qd[dd]) * yi;
+                    dhat += wd[dd] / (qp * qd[dd]);
+                }
                 if (inb) {
                     const int v = (R - lr) * boxw + (Cc - lc);
                     const double yh = yk[v];
-                    double d, dhat;
-                    degrees(L, b, R, Cc, qp, d, dhat);
                     const double rdiag = d / (qp * qp) - dhat;
                     acc += mu * (yh + L.a[(size_t)k * M + v]) - L.lam * (rdiag * yh);
-                    ct = (d / qp) * (1.0 - 1.0 / qp) * yh;
-                }
-                for (int dd = 0; dd < L.ndir; ++dd) {
-                    const double w = wpair(L, R, Cc, dd);
-                    if (w == 0.0) continue;
-                    const int rn = R + dy_of(dd), cn = Cc + dx_of(dd);
-                    if (!b.holds(rn, cn)) continue;
-                    const double qi = (double)L.q[(int64_t)rn * L.W + cn];
-                    const double yi = yk[(rn - lr) * boxw + (cn - lc)];
-                    ct += inb ? (-w / qi) * (1.0 - 1.0 / qp) * yi : (-w / qi) * yi;
+                    ct += (d / qp) * (1.0 - 1.0 / qp) * yh;
                 }
                 acc -= L.lam * ct;
             }
@@ -380,21 +389,45 @@ __global__ void __launch_bounds__(256) k_energy_g(LatG L) {
 // finalize: trace, best iterate (strict <), mu *= mu_fact, stop rule
 // (admm.py:228-249); one thread, fixed summation order
 // ---------------------------------------------------------------------------
-__global__ void k_finalize_g(LatG L) {
+__global__ void __launch_bounds__(1024) k_finalize_g(LatG L) {
     dope_run_state *st = L.st;
     if (st->stop) return;
-    double E = 0.0;
+    // fixed-order reduction over the partials: thread-strided, then a fixed
+    // shuffle tree and warp order (deterministic)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double E = 0.0, R2 = 0.0, mx = 0.0;
     int cl = 0;
-    for (int i = 0; i < L.npe; ++i) {
+    for (int i = tid; i < L.npe; i += blockDim.x) {
         E += L.pe[i];
         cl |= L.pcl[i];
         L.pcl[i] = 0;
     }
-    double R2 = 0.0, mx = 0.0;
-    for (int k = 0; k < L.K; ++k) {
+    for (int k = tid; k < L.K; k += blockDim.x) {
         const double r = sqrt(L.pr[k]);
         R2 += r * r;
         mx = r > mx ? r : mx;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        E += __shfl_xor_sync(FULLMASK, E, o);
+        R2 += __shfl_xor_sync(FULLMASK, R2, o);
+        const double m2 = __shfl_xor_sync(FULLMASK, mx, o);
+        mx = m2 > mx ? m2 : mx;
+    }
+    cl = __any_sync(FULLMASK, cl);
+    __shared__ double sE[32], sR[32], sM[32];
+    __shared__ int sC[32];
+    if (lane == 0) { sE[warp] = E; sR[warp] = R2; sM[warp] = mx; sC[warp] = cl; }
+    __syncthreads();
+    if (tid != 0) return;
+    E = 0.0;
+    R2 = 0.0;
+    mx = 0.0;
+    cl = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        E += sE[w];
+        R2 += sR[w];
+        mx = sM[w] > mx ? sM[w] : mx;
+        cl |= sC[w];
     }
     const int t = st->iteration;
     const double mu = L.scal[0];
@@ -538,7 +571,7 @@ static int global_pass(const LatG &o, cudaStream_t s) {
     k_global_g<<<o.npe, 256, 0, s>>>(o, o.boxw, M);
     k_residual_g<<<o.K, 256, 0, s>>>(o, o.boxw, M);
     k_energy_g<<<o.npe, 256, 0, s>>>(o);
-    k_finalize_g<<<1, 1, 0, s>>>(o);
+    k_finalize_g<<<1, 1024, 0, s>>>(o);
     return cuda_check(cudaGetLastError(), "general global step");
 }
 
