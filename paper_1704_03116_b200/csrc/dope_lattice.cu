@@ -466,11 +466,19 @@ __global__ void k_init_resid(Lat2 L) {
     L.ay.range(by, lo_r, hr);
     L.ax.range(bx, lo_c, wc);
     uint8_t *gres = L.resid + (size_t)k * 2 * M;   // E and S planes
-    for (int v = threadIdx.x; v < M; v += blockDim.x) {
-        const int r = v / L.boxw, c = v % L.boxw;
-        const bool valid = r < hr && c < wc;
-        gres[0 * M + v] = (valid && c + 1 < wc) ? L.cap : 0;
-        gres[1 * M + v] = (valid && r + 1 < hr) ? L.cap : 0;
+    // 4 nodes per 32-bit store (box widths are multiples of 16)
+    for (int q = threadIdx.x; q < M / 4; q += blockDim.x) {
+        const int v0 = 4 * q, r = v0 / L.boxw, c0 = v0 % L.boxw;
+        uint32_t e = 0, sv = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = c0 + i;
+            const bool valid = r < hr && c < wc;
+            e |= (uint32_t)((valid && c + 1 < wc) ? L.cap : 0) << (8 * i);
+            sv |= (uint32_t)((valid && r + 1 < hr) ? L.cap : 0) << (8 * i);
+        }
+        reinterpret_cast<uint32_t *>(gres)[q] = e;
+        reinterpret_cast<uint32_t *>(gres + M)[q] = sv;
     }
 }
 
@@ -507,13 +515,37 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
 }
 
 // sum u * y2 of the initial iterate (y2 = 1): the running unary term starts at sum u
+// Sum of a per-thread int64 partial over the CTA, one atomic per CTA
+// (a per-warp atomic on one address serialises thousands of updates).
+__device__ __forceinline__ void cta_atomic_add(int64_t v, int64_t *dst) {
+    __shared__ int64_t red[32];
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
+        for (int w = 0; w < nw; ++w) t += red[w];
+        if (t) atomicAdd(reinterpret_cast<unsigned long long *>(dst), (unsigned long long)t);
+    }
+}
+
 __global__ void k_init_unary(Lat2 L, int64_t n) {
     int64_t acc = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) acc += L.u[i];
-    acc = warp_sum(acc);
-    if ((threadIdx.x & 31) == 0)
-        atomicAdd(reinterpret_cast<unsigned long long *>(&L.st->unary2), (unsigned long long)acc);
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (((uintptr_t)L.u & 15) == 0) {   // 16-byte loads
+        const int4 *u4 = reinterpret_cast<const int4 *>(L.u);
+        for (int64_t i = t0; i < n / 4; i += stride) {
+            const int4 v = __ldg(u4 + i);
+            acc += (int64_t)v.x + v.y + v.z + v.w;
+        }
+        for (int64_t i = n / 4 * 4 + t0; i < n; i += stride) acc += L.u[i];
+    } else {
+        for (int64_t i = t0; i < n; i += stride) acc += L.u[i];
+    }
+    cta_atomic_add(acc, &L.st->unary2);
 }
 
 // ---------------------------------------------------------------------------
@@ -982,6 +1014,29 @@ __global__ void k_energy_current(Lat2 L, int64_t n) {
     acc = warp_sum(acc);
     if ((threadIdx.x & 31) == 0)
         atomicAdd((unsigned long long *)&L.st->energy_acc, (unsigned long long)acc);
+}
+
+// Vector form of k_energy_current for grids whose width is a multiple of 4:
+// one 4-byte word of y2 per step, pairs as XOR + popcount on the 0/2 bytes.
+__global__ void k_energy_current_vec(Lat2 L, uint32_t nwords) {
+    const ystore_t *y2 = L.y2[L.st->ycur];
+    const uint32_t W4 = (uint32_t)L.W >> 2, H = (uint32_t)L.ay.dim, D = (uint32_t)L.az.dim;
+    const int64_t HW = (int64_t)H * L.W;
+    int64_t acc = 0;
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += gridDim.x * blockDim.x) {
+        const uint32_t row = w / W4, c4 = w - row * W4;
+        const uint32_t r = row % H, z = row / H;
+        const int64_t G = 4 * (int64_t)w;
+        const uint32_t y = *reinterpret_cast<const uint32_t *>(y2 + G);
+        const uint32_t nx = c4 + 1 < W4 ? *reinterpret_cast<const uint32_t *>(y2 + G + 4) : (y >> 24);
+        int qd = __popc(y ^ __funnelshift_r(y, nx, 8));
+        if (r + 1 < H || L.gdn) qd += __popc(y ^ *reinterpret_cast<const uint32_t *>(y2 + G + L.W));
+        if (z + 1 < D) qd += __popc(y ^ *reinterpret_cast<const uint32_t *>(y2 + G + HW));
+        acc += qd;
+    }
+    acc *= L.lamw;
+    if (blockIdx.x == 0 && threadIdx.x == 0) acc += L.st->unary2 / 2;
+    cta_atomic_add(acc, &L.st->energy_acc);
 }
 
 // End of run (admm.py:300-310): trace energy + best check of the last
@@ -1574,13 +1629,21 @@ int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void 
     return cuda_check(cudaGraphLaunch(exec, s), "graph launch");
 }
 
+static int launch_energy_current(const Lat2 &o, int64_t n, cudaStream_t s) {
+    const uintptr_t al = (uintptr_t)o.y2[0] | (uintptr_t)o.y2[1] | (uintptr_t)o.y2[2];
+    if (o.W % 4 == 0 && al % 4 == 0 && n / 4 < (int64_t)UINT32_MAX)
+        k_energy_current_vec<<<grid_for(n / 4), 256, 0, s>>>(o, (uint32_t)(n / 4));
+    else
+        k_energy_current<<<grid_for(n), 256, 0, s>>>(o, n);
+    return cuda_check(cudaGetLastError(), "energy_current");
+}
+
 int dope_finish_run(const dope_lattice *L, void *stream) {
     Plan P;
     int rc = build_plan(L, P);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
-    k_energy_current<<<grid_for(P.n), 256, 0, s>>>(P.o, P.n);
-    if ((rc = cuda_check(cudaGetLastError(), "energy_current"))) return rc;
+    if ((rc = launch_energy_current(P.o, P.n, s))) return rc;
     k_finish_decide<<<1, 1, 0, s>>>(P.o);
     return cuda_check(cudaGetLastError(), "finish_decide");
 }
@@ -1618,8 +1681,7 @@ int dope_energy_local(const dope_lattice *L, void *stream) {
     Plan P;
     int rc = build_plan(L, P);
     if (rc) return rc;
-    k_energy_current<<<grid_for(P.n), 256, 0, (cudaStream_t)stream>>>(P.o, P.n);
-    return cuda_check(cudaGetLastError(), "energy_local");
+    return launch_energy_current(P.o, P.n, (cudaStream_t)stream);
 }
 
 int dope_finish_decide(const dope_lattice *L, void *stream) {
