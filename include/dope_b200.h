@@ -324,6 +324,30 @@ int dope_g_update_global(const dope_general *L, void *stream);   /* global step,
 int dope_g_finish_run(const dope_general *L, void *stream);
 int dope_g_binarize(const dope_general *L, uint8_t *out, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Model construction on the GPU.  `dims` and `offs`
+ * (the half window, grid.py:80-116, offsets row-major) are HOST arrays; all
+ * other pointers are device buffers.
+ * ------------------------------------------------------------------------- */
+const char *dope_in_last_error(void);
+/* number of pairs of the half window over the grid (-1: bad arguments)     */
+int64_t dope_in_pair_count(int32_t ndim, const int64_t *dims, int32_t noff, const int32_t *offs);
+/* length of the partial-sum arrays the reductions below write              */
+int64_t dope_in_partials(int64_t n);
+/* build_potts_weights (energy.py:124-162): rows/cols/vals of every pair in
+ * the reference's order; vals = exp(-|x_i - x_j|^2 / (2 sigma^2)) or 1     */
+int dope_in_potts_weights(int32_t ndim, const int64_t *dims, int32_t channels, const double *data,
+                          int32_t noff, const int32_t *offs, double sigma, int32_t contrast,
+                          int64_t *rows, int64_t *cols, double *vals, void *stream);
+/* estimate_sigma (energy.py:165-184): per-CTA partial sums of |x_i - x_j|^2 */
+int dope_in_sq_diff(int32_t ndim, const int64_t *dims, int32_t channels, const double *data,
+                    int32_t noff, const int32_t *offs, double *partials, void *stream);
+/* compute_unaries (energy.py:298-323); seeds may be NULL                    */
+int dope_in_unaries(int64_t n, int32_t channels, const double *data, const int8_t *seeds,
+                    const double *fg_centroids, const double *bg_centroids, const double *fg_weights,
+                    const double *bg_weights, int32_t nclusters, double bandwidth, double *u,
+                    double *partials, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -232,6 +232,21 @@ def lib():
     lb.dope_f_admm_run.argtypes = [PF, C.c_int32, C.c_int32, C.c_void_p]
     lb.dope_f_binarize.restype = C.c_int
     lb.dope_f_binarize.argtypes = [PF, C.c_void_p, C.c_void_p]
+    lb.dope_in_last_error.restype = C.c_char_p
+    lb.dope_in_pair_count.restype = C.c_int64
+    lb.dope_in_pair_count.argtypes = [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]
+    lb.dope_in_partials.restype = C.c_int64
+    lb.dope_in_partials.argtypes = [C.c_int64]
+    lb.dope_in_potts_weights.restype = C.c_int
+    lb.dope_in_potts_weights.argtypes = [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
+                                         C.c_double, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lb.dope_in_sq_diff.restype = C.c_int
+    lb.dope_in_sq_diff.argtypes = [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
+                                   C.c_void_p, C.c_void_p]
+    lb.dope_in_unaries.restype = C.c_int
+    lb.dope_in_unaries.argtypes = [C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_void_p, C.c_void_p,
+                                   C.c_void_p]
     PG = C.POINTER(General)
     for name in ("dope_g_copy_stride", "dope_g_partials"):
         f = getattr(lb, name)

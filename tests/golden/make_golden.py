@@ -222,6 +222,43 @@ def main_general():
     save_general("mufact_long", W.mini_disks(128, 32, 6, 2, 20, seed=9, rmax=40.0), 0, 4.0, 1.05, 0.0, 20)
 
 
+def main_inputs():
+    """Model construction: the reference's weight,
+    sigma, colour-model and unary builders on small synthetic images."""
+    from dope.energy import build_potts_weights, compute_unaries, estimate_sigma, fit_color_model
+    from dope.grid import GridImage
+    rng = np.random.default_rng(31)
+    h, w = 48, 64
+    yy, xx = np.meshgrid(np.arange(h), np.arange(w), indexing="ij")
+    blob = ((yy - 20.0) ** 2 / 120.0 + (xx - 30.0) ** 2 / 300.0) < 1.0
+    rgb = np.where(blob[..., None], [0.8, 0.3, 0.2], [0.2, 0.5, 0.7]) + rng.normal(0, 0.07, (h, w, 3))
+    seeds = np.zeros((h, w), dtype=np.int8)
+    seeds[18:22, 24:36] = 2          # foreground strokes
+    seeds[2:4, 2:60] = 1             # background strokes
+    seeds[44:46, 10:50] = 1
+    img = GridImage(GridShape((h, w)), np.clip(rgb, 0, 1).reshape(-1, 3), seeds.ravel())
+    out = dict(data=img.data, seeds=img.seeds, dims=np.array((h, w)))
+    for k in (3, 5):
+        s = estimate_sigma(img, k)
+        wts = build_potts_weights(img, k, s, contrast=True)
+        out[f"sigma{k}"] = s
+        out[f"rows{k}"], out[f"cols{k}"], out[f"vals{k}"] = wts.rows, wts.cols, wts.vals
+    cm = fit_color_model(img, rng=np.random.default_rng(0))
+    out.update(fg_c=cm.fg_centroids, bg_c=cm.bg_centroids, fg_w=cm.fg_weights, bg_w=cm.bg_weights,
+               bw=cm.bandwidth, u=compute_unaries(img, cm))
+    np.savez_compressed(OUT / "inputs_2d.npz", **out)
+    vol = np.clip(0.5 + 0.3 * np.sin(np.arange(12 * 10 * 8) * 0.37) + rng.normal(0, 0.05, 960), 0, 1)
+    img3 = GridImage(GridShape((12, 10, 8)), vol)
+    out3 = dict(data=img3.data, dims=np.array((12, 10, 8)))
+    for k in (3, 5):
+        s = estimate_sigma(img3, k)
+        wts = build_potts_weights(img3, k, s, contrast=True)
+        out3[f"sigma{k}"] = s
+        out3[f"rows{k}"], out3[f"cols{k}"], out3[f"vals{k}"] = wts.rows, wts.cols, wts.vals
+    np.savez_compressed(OUT / "inputs_3d.npz", **out3)
+    print("inputs:", {k: out[f"vals{k}"].size for k in (3, 5)}, {k: out3[f"vals{k}"].size for k in (3, 5)})
+
+
 class _RaggedWL(W.Workload):
     @property
     def kpa(self):
@@ -236,6 +273,9 @@ def main():
         return
     if "--only-general" in sys.argv:
         main_general()
+        return
+    if "--only-inputs" in sys.argv:
+        main_inputs()
         return
     gen_bk(core)
     save_run("c1", W.c1())
@@ -263,6 +303,7 @@ def main():
     r2.rho = 2.0
     save_run("rho2", r2)
     main_general()
+    main_inputs()
 
 
 if __name__ == "__main__":
