@@ -221,8 +221,10 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
     dope_run_state *st = L.st;
     const int tid = threadIdx.x, lane = tid & 31;
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&M.y[0])) : "memory");
-    griddep_wait();     // K1's labels and solve epochs (PDL launch)
-    griddep_launch();   // every CTA is resident: the next K1 may launch and wait
+    if (L.pdl) {
+        griddep_wait();     // K1's labels and solve epochs (PDL launch)
+        griddep_launch();   // every CTA is resident: the next K1 may launch and wait
+    }
     if (st->stop) return;
     const int cur = st->ycur, best = st->ybest, out = other_buffer(cur, best);
     const int iter = st->iteration;

@@ -76,6 +76,7 @@ struct Lat2 {
     int32_t gup, gdn;       // a ghost row (neighbour shard) exists above / below
     int32_t sharded;        // consensus writes local aggregates; dope_decide applies
     int64_t *agg;           // [E, R2 (double bits), max ss, clamped] of this shard
+    int32_t pdl;            // launched with programmatic dependent launch (DOPE_PDL=1)
 };
 
 // ---------------------------------------------------------------------------
@@ -128,8 +129,10 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
         L.timeline[8 * k + 4] = (int64_t)t_begin;
         L.timeline[8 * k + 5] = (int64_t)t_begin;
     }
-    griddep_wait();     // the previous consensus pass (PDL launch)
-    griddep_launch();   // all K1 CTAs are resident: the consensus pass may launch
+    if (L.pdl) {
+        griddep_wait();     // the previous consensus pass (PDL launch)
+        griddep_launch();   // all K1 CTAs are resident: the consensus pass may launch
+    }
     {
         // both flags in one round trip: a clean CTA must leave its slot fast
         // (4096 CTAs churn through ~5 slots per SM)
@@ -793,8 +796,10 @@ __device__ __forceinline__ void check_a(const Lat2 &L, int a) {
 
 // Generic consensus (any tiling, incl. ragged): one CTA per block, scalar.
 __global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
-    griddep_wait();
-    griddep_launch();
+    if (L.pdl) {
+        griddep_wait();
+        griddep_launch();
+    }
     if (L.st->stop) return;
     const int tid = threadIdx.x;
     CtaAgg agg;
@@ -865,8 +870,10 @@ __global__ void __launch_bounds__(256) k_consensus(Lat2 L) {
 template <int NT>
 __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
     constexpr int QPT = 4;
-    griddep_wait();
-    griddep_launch();
+    if (L.pdl) {
+        griddep_wait();
+        griddep_launch();
+    }
     if (L.st->stop) return;
     const int tid = threadIdx.x;
     CtaAgg agg;
@@ -1228,6 +1235,7 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
     // quad loads: 4 labels / 4 y2 bytes as one word, 4 multipliers as 8 bytes
     const uintptr_t al = (uintptr_t)o.y2[0] | (uintptr_t)o.y2[1] | (uintptr_t)o.y2[2] | (uintptr_t)o.yhat |
                          ((uintptr_t)o.a >> 1) | ((uintptr_t)o.u >> 2);
+    o.pdl = getenv("DOPE_PDL") != nullptr;
     o.vec4 = !is3 && (o.W % 4 == 0) && (o.ax.rem == 0) && (o.ax.base % 4 == 0) && (al % 4 == 0);
     return DOPE_OK;
 }
@@ -1289,13 +1297,14 @@ static int configure_plan(const Plan &P) {
     return P.v3 ? configure_k1_3d(P.v3) : configure_k1(P.v);
 }
 
-// Launch with programmatic stream serialisation (PDL): the kernel may start
-// while the previous one drains; it orders itself with griddep_wait().
-// DOPE_NO_PDL=1 falls back to plain launches (same results).
+// Launch with programmatic stream serialisation (PDL) when DOPE_PDL=1: the
+// kernel may start while the previous one drains and orders itself with
+// griddep_wait().  Off by default: measured neutral on C3 and 5-10 % slower on
+// C5 (early-launched CTAs hold SM slots); same results either way.
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args... args) {
-    static const bool off = getenv("DOPE_NO_PDL") != nullptr;
+    static const bool off = getenv("DOPE_PDL") == nullptr;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;

@@ -331,8 +331,10 @@ __global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
 template <int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_consensus3d_vec(Lat2 L, int lq) {
     constexpr int QB = 4;   // quads per load batch
-    griddep_wait();
-    griddep_launch();
+    if (L.pdl) {
+        griddep_wait();
+        griddep_launch();
+    }
     if (L.st->stop) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     CtaAgg agg;
