@@ -348,6 +348,20 @@ int dope_in_unaries(int64_t n, int32_t channels, const double *data, const int8_
                     const double *bg_weights, int32_t nclusters, double bandwidth, double *u,
                     double *partials, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Whole-grid serial graph cut (cli.run_serial ->
+ * maxflow.solve_binary on the full image).  2D lattice, 4- or 8-connected:
+ * tcap = signed terminal capacity (maxflow.py:73-97), w[0..3] = E S SE SW pair
+ * weights (device, pair stored at its lower pixel), capacities lam * w.  One
+ * cooperative kernel; labels = nodes reaching the sink side (ties -> 0).
+ * stats (device, 3 int64): global-relabel rounds (-1: round limit), sweeps.
+ * ------------------------------------------------------------------------- */
+const char *dope_gc_last_error(void);
+int64_t dope_gc_workspace_bytes(int64_t H, int64_t W, int32_t conn);
+int dope_gc_mincut(int64_t H, int64_t W, int32_t conn, const double *tcap, const double *const *w,
+                   double lam, double qscale, uint8_t *labels, int64_t *stats, void *workspace,
+                   int64_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

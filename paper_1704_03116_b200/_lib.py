@@ -247,6 +247,12 @@ def lib():
     lb.dope_in_unaries.argtypes = [C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_void_p, C.c_void_p,
                                    C.c_void_p]
+    lb.dope_gc_last_error.restype = C.c_char_p
+    lb.dope_gc_workspace_bytes.restype = C.c_int64
+    lb.dope_gc_workspace_bytes.argtypes = [C.c_int64, C.c_int64, C.c_int32]
+    lb.dope_gc_mincut.restype = C.c_int
+    lb.dope_gc_mincut.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_double,
+                                  C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
     PG = C.POINTER(General)
     for name in ("dope_g_copy_stride", "dope_g_partials"):
         f = getattr(lb, name)
