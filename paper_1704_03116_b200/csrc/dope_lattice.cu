@@ -1096,6 +1096,7 @@ __global__ void k_energy4(Lat2 L, const int32_t *__restrict__ y2, int64_t n,
 // ---------------------------------------------------------------------------
 #include "consensus_tma.cuh"
 #include "lattice3d.cuh"
+#include "lattice3d_smem.cuh"
 
 // ---------------------------------------------------------------------------
 // Host side
@@ -1266,6 +1267,16 @@ static int configure_k1(const Variant *v) {
     return DOPE_OK;
 }
 
+// 32^3 boxes with 2*cap <= 15 run the shared-memory kernel (lattice3d_smem.cuh);
+// DOPE_K1_3D=l2 forces the HBM-scratch kernel (diagnostics).
+static bool use_k1_3d_smem(const Lat2 &o, const Variant3 *v) {
+    static const bool off = [] {
+        const char *e = getenv("DOPE_K1_3D");
+        return e && strcmp(e, "l2") == 0;
+    }();
+    return !off && v->bd == 32 && v->bh == 32 && v->bw == 32 && 2 * o.cap <= 15;
+}
+
 static int configure_k1_3d(const Variant3 *v) {
     static std::mutex mu;
     static std::map<void *, bool> configured;
@@ -1274,6 +1285,11 @@ static int configure_k1_3d(const Variant3 *v) {
         int rc = cuda_check(cudaFuncSetAttribute(v->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)v->smem), "cudaFuncSetAttribute(K1-3D)");
         if (rc) return rc;
+        if (v->bd == 32) {
+            rc = cuda_check(cudaFuncSetAttribute(k_block_mincut3d_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)k1s::SMEM), "cudaFuncSetAttribute(K1-3D smem)");
+            if (rc) return rc;
+        }
         configured[(void *)v->kernel] = true;
     }
     return DOPE_OK;
@@ -1321,7 +1337,8 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 static int launch_k1(const Plan &P, cudaStream_t s) {
     int rc = configure_plan(P);
     if (rc) return rc;
-    if (P.v3) P.v3->kernel<<<P.o.K, P.v3->nt, P.v3->smem, s>>>(P.o, default_tune());
+    if (P.v3 && use_k1_3d_smem(P.o, P.v3)) k_block_mincut3d_s<<<P.o.K, k1s::NT, k1s::SMEM, s>>>(P.o, default_tune());
+    else if (P.v3) P.v3->kernel<<<P.o.K, P.v3->nt, P.v3->smem, s>>>(P.o, default_tune());
     else return cuda_check(launch_pdl(P.v->kernel, dim3(P.o.K), dim3(P.v->nt), P.v->smem, s, P.o, default_tune()),
                            "launch K1");
     return cuda_check(cudaGetLastError(), "launch K1");

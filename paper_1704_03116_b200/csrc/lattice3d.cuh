@@ -38,21 +38,20 @@ struct K1Cfg3 {
     static constexpr size_t SMEM = (size_t)9 * 8 * NW + 64;   // 8 masks + reach + misc
 };
 
+// Solve of sub-region k with its node state in the per-block HBM scratch.
+// The E, S, D residual planes (0, 2, 4) are the persistent truth between
+// solves; a warm start re-derives W, N, U (r(v->v-off) = 2cap - r(v-off->v))
+// so the shared-memory kernel below, which stores only E/S/D, and this one
+// can alternate on the same block.
 template <int BD, int BH, int BW, int NT>
-__global__ void __launch_bounds__(NT) k_block_mincut3d(Lat2 L, K1Tune T) {
+__device__ __forceinline__ void mincut3d_l2(const Lat2 &L, const K1Tune &T, int k, uint8_t *smem3) {
     using C = K1Cfg3<BD, BH, BW, NT>;
     constexpr int M = C::M, NPT = C::NPT, NW = C::NW, PL = C::PL;
-    extern __shared__ __align__(16) uint8_t smem3[];
     uint64_t *masks = reinterpret_cast<uint64_t *>(smem3);   // E W S N D U SINK ACT
     uint64_t *reach = masks + 8 * NW;
     int *misc = reinterpret_cast<int *>(reach + NW);
     uint32_t *masks32 = reinterpret_cast<uint32_t *>(masks);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int k = blockIdx.x;
-    if (L.st->stop) return;
-    if (L.skip_clean && L.dirty[k] == 0) return;
-    __syncthreads();
-    if (tid == 0) L.dirty[k] = 0;
 
     int bz, by, bx;
     const Geo3 gb = block_geo3(L, k, bz, by, bx);
@@ -90,8 +89,18 @@ __global__ void __launch_bounds__(NT) k_block_mincut3d(Lat2 L, K1Tune T) {
             if (L.warm) {
                 int32_t f = 0;
 #pragma unroll
-                for (int d = 0; d < 6; ++d)
-                    if (has[d]) f += (int32_t)rr[d * M + v] - cap;
+                for (int d = 0; d < 6; ++d) {
+                    if (!has[d]) continue;
+                    int32_t r;
+                    if (d & 1) {   // reverse arc: from the forward plane of the neighbour
+                        const int off = d == 1 ? 1 : d == 3 ? BW : PL;
+                        r = 2 * cap - (int32_t)rr[(d - 1) * M + v - off];
+                        rr[d * M + v] = (uint8_t)r;
+                    } else {
+                        r = rr[d * M + v];
+                    }
+                    f += r - cap;
+                }
                 gv = lin2 + f;
             } else {
 #pragma unroll
@@ -208,6 +217,17 @@ __global__ void __launch_bounds__(NT) k_block_mincut3d(Lat2 L, K1Tune T) {
         atomicAdd((unsigned long long *)&L.st->sweeps, (unsigned long long)sweeps_done);
         atomicMax(&L.st->max_rounds_seen, rounds);
     }
+}
+
+template <int BD, int BH, int BW, int NT>
+__global__ void __launch_bounds__(NT) k_block_mincut3d(Lat2 L, K1Tune T) {
+    extern __shared__ __align__(16) uint8_t smem3[];
+    const int k = blockIdx.x;
+    if (L.st->stop) return;
+    if (L.skip_clean && L.dirty[k] == 0) return;
+    __syncthreads();
+    if (threadIdx.x == 0) L.dirty[k] = 0;
+    mincut3d_l2<BD, BH, BW, NT>(L, T, k, smem3);
 }
 
 __global__ void k_init_resid3d(Lat2 L, int boxd, int boxh, int boxw) {

@@ -1,0 +1,329 @@
+// lattice3d_smem.cuh -- K1-3D with the whole 32^3 sub-region in shared memory.
+// Included by dope_lattice.cu inside namespace dope, after lattice3d.cuh.
+//
+// The HBM-scratch kernel (lattice3d.cuh) pays an L2 round trip for every
+// excess / height / residual access of every sweep.  Here a 32^3 block's
+// residual graph is packed into 184 KB of shared memory:
+//   * excess: int16, two per 32-bit word, biased by 2^15 so that a packed
+//     atomicAdd of (delta << 16*half) never carries into the other half
+//     (|excess| <= |2*linear| + 6*cap <= 32000 is checked per block; a block
+//     that could leave the range runs the HBM-scratch body instead);
+//   * heights: uint16;
+//   * residuals of the E, S, D arcs only, 4 bits each (2*cap <= 15), eight per
+//     word; the reverse arc's residual is 2cap - forward.  A push moves flow
+//     on one edge, and only the higher endpoint of an edge can push in a
+//     sweep, so a nibble has one writer per sweep; atomics only keep the
+//     neighbouring nibbles of the same word intact;
+//   * the global relabel runs on all 32 warps: warp w owns plane z = w, lane l
+//     row y = l, one 32-bit reach word per row.  +-x is a shift, +-y a
+//     shuffle, +-z a double-buffered shared row, one barrier per BFS level.
+// Node-parallel phases (prologue, push, relabel, epilogue) map v = z*1024 +
+// y*32 + x with z the loop index, y the warp and x the lane (conflict-free).
+// Labels, flows and the exactness argument are those of DESIGN.md §2.
+
+namespace k1s {
+constexpr int B = 32, M = B * B * B, NT = 1024, PLANE = B * B;
+constexpr int NIBW = M / 8;                                // nibble words per plane
+constexpr size_t OFF_G = 0;                                // uint32[M/2] packed excess
+constexpr size_t OFF_H = OFF_G + 2 * (size_t)M;            // uint16[M]
+constexpr size_t OFF_F = OFF_H + 2 * (size_t)M;            // uint32[3][M/8] E,S,D residual nibbles
+constexpr size_t OFF_R = OFF_F + 3 * 4 * (size_t)NIBW;     // uint32[2][1024] reach rows
+constexpr size_t OFF_K = OFF_R + 2 * 4 * 1024;             // uint32[2][1024] sink / active rows
+constexpr size_t OFF_MISC = OFF_K + 2 * 4 * 1024;
+constexpr size_t SMEM = OFF_MISC + 64;
+constexpr int BIAS = 32768;
+constexpr int GMAX = 32000;
+static_assert(SMEM <= 227 * 1024, "shared memory");
+static_assert(K1Cfg3<32, 32, 32, NT>::SMEM <= SMEM, "fallback body fits");
+}  // namespace k1s
+
+__device__ __forceinline__ int32_t s3_getg(const uint32_t *G2, int v) {
+    return (int32_t)((G2[v >> 1] >> ((v & 1) << 4)) & 0xffffu) - k1s::BIAS;
+}
+__device__ __forceinline__ void s3_addg(uint32_t *G2, int v, int32_t d) {
+    atomicAdd(&G2[v >> 1], (uint32_t)d << ((v & 1) << 4));
+}
+__device__ __forceinline__ int32_t s3_nib(const uint32_t *P, int v) {
+    return (int32_t)((P[v >> 3] >> ((v & 7) << 2)) & 0xfu);
+}
+__device__ __forceinline__ void s3_addnib(uint32_t *P, int v, int32_t d) {
+    atomicAdd(&P[v >> 3], (uint32_t)d << ((v & 7) << 2));
+}
+// eight nibbles -> eight bits (bit i set iff nibble i != 0)
+__device__ __forceinline__ uint32_t s3_nz8(uint32_t x) {
+    uint32_t t = (x | (x >> 1) | (x >> 2) | (x >> 3)) & 0x11111111u;
+    t = (t | (t >> 3)) & 0x03030303u;
+    t = (t | (t >> 6)) & 0x000F000Fu;
+    return (t | (t >> 12)) & 0xFFu;
+}
+__device__ __forceinline__ uint32_t s3_nz32(uint4 w) {
+    return s3_nz8(w.x) | (s3_nz8(w.y) << 8) | (s3_nz8(w.z) << 16) | (s3_nz8(w.w) << 24);
+}
+__device__ __forceinline__ uint4 s3_xor(uint4 w, uint32_t c) {
+    return make_uint4(w.x ^ c, w.y ^ c, w.z ^ c, w.w ^ c);
+}
+
+// out of line so that its registers do not count against the fast path
+__device__ __noinline__ void mincut3d_l2_fallback(const Lat2 &L, const K1Tune &T, int k, uint8_t *smem) {
+    mincut3d_l2<k1s::B, k1s::B, k1s::B, k1s::NT>(L, T, k, smem);
+}
+
+__global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune T) {
+    using namespace k1s;
+    extern __shared__ __align__(16) uint8_t sm3[];
+    uint32_t *G2 = reinterpret_cast<uint32_t *>(sm3 + OFF_G);
+    uint16_t *h = reinterpret_cast<uint16_t *>(sm3 + OFF_H);
+    uint32_t *FE = reinterpret_cast<uint32_t *>(sm3 + OFF_F);
+    uint32_t *FS = FE + NIBW, *FD = FE + 2 * NIBW;
+    uint32_t *Rb = reinterpret_cast<uint32_t *>(sm3 + OFF_R);
+    uint32_t *Kb = reinterpret_cast<uint32_t *>(sm3 + OFF_K);   // [0] sink rows, [1] active rows
+    int *misc = reinterpret_cast<int *>(sm3 + OFF_MISC);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int k = blockIdx.x;
+    if (L.st->stop) return;
+    if (L.skip_clean && L.dirty[k] == 0) return;
+    __syncthreads();
+    if (tid == 0) L.dirty[k] = 0;
+
+    int bz, by, bx;
+    const Geo3 gb = block_geo3(L, k, bz, by, bx);
+    const int32_t W = L.W, H = L.ay.dim, D = L.az.dim;
+    const int64_t HW = (int64_t)H * W;
+    const int32_t cap = L.cap, cap2 = 2 * cap;
+    const astore_t *__restrict__ a_cur = L.a;
+    const ystore_t *__restrict__ y_cur = L.y2[L.st->ycur];
+    uint8_t *rr = L.resid + (size_t)k * 6 * M;   // planes 0 (E), 2 (S), 4 (D)
+    const bool up_z = gb.lo_z > 0, dn_z = gb.lo_z + gb.dz < D;
+    const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
+    const bool lf_c = gb.lo_c > 0, rt_c = gb.lo_c + gb.wc < W;
+    const bool xin = lane < gb.wc, yin = warp < gb.hr;
+
+    // ---- prologue: 2*linear, residual nibbles, packed excess ----
+    int over = 0;
+#pragma unroll 2
+    for (int z = 0; z < B; ++z) {
+        const int v = z * PLANE + tid;
+        const bool valid = xin && yin && z < gb.dz;
+        int32_t gv = 0, fE = 0, fS = 0, fD = 0;
+        if (valid) {
+            const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + warp) * W + gb.lo_c + lane;
+            const int32_t yg = (int32_t)y_cur[G];
+            int32_t sx = 0;
+            if (lane == 0 && lf_c) sx += yg - y_cur[G - 1];
+            if (lane == gb.wc - 1 && rt_c) sx += yg - y_cur[G + 1];
+            if (warp == 0 && up_r) sx += yg - y_cur[G - W];
+            if (warp == gb.hr - 1 && dn_r) sx += yg - y_cur[G + W];
+            if (z == 0 && up_z) sx += yg - y_cur[G - HW];
+            if (z == gb.dz - 1 && dn_z) sx += yg - y_cur[G + HW];
+            gv = 2 * L.u[G] + L.lamw * sx + L.mu * (2 * (int32_t)a_cur[G] - yg) + L.mu;
+            over |= (gv > GMAX - 6 * cap) | (gv < -(GMAX - 6 * cap));
+            const bool hE = lane + 1 < gb.wc, hS = warp + 1 < gb.hr, hD = z + 1 < gb.dz;
+            if (L.warm) {
+                fE = hE ? rr[v] : 0;
+                fS = hS ? rr[2 * M + v] : 0;
+                fD = hD ? rr[4 * M + v] : 0;
+                // excess = 2*linear + sum over the 6 arcs of (residual - cap)
+                int32_t f = (hE ? fE - cap : 0) + (hS ? fS - cap : 0) + (hD ? fD - cap : 0);
+                if (lane > 0) f += cap - rr[v - 1];
+                if (warp > 0) f += cap - rr[2 * M + v - B];
+                if (z > 0) f += cap - rr[4 * M + v - PLANE];
+                gv += f;
+            } else {
+                fE = hE ? cap : 0;
+                fS = hS ? cap : 0;
+                fD = hD ? cap : 0;
+            }
+        }
+        // pack: 8 lanes -> one nibble word per plane, 2 lanes -> one excess word
+        uint32_t nE = (uint32_t)fE << ((lane & 7) << 2), nS = (uint32_t)fS << ((lane & 7) << 2),
+                 nD = (uint32_t)fD << ((lane & 7) << 2);
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            nE |= __shfl_xor_sync(FULLMASK, nE, o);
+            nS |= __shfl_xor_sync(FULLMASK, nS, o);
+            nD |= __shfl_xor_sync(FULLMASK, nD, o);
+        }
+        if ((lane & 7) == 0) {
+            FE[v >> 3] = nE;
+            FS[v >> 3] = nS;
+            FD[v >> 3] = nD;
+        }
+        const uint32_t gb16 = (uint32_t)(gv + BIAS) & 0xffffu;
+        const uint32_t hi = __shfl_down_sync(FULLMASK, gb16, 1);
+        if ((lane & 1) == 0) G2[v >> 1] = gb16 | (hi << 16);
+    }
+    if (__syncthreads_or(over)) {
+        // this block's excess could leave int16: solve it with the HBM-scratch body
+        mincut3d_l2_fallback(L, T, k, sm3);
+        return;
+    }
+
+    // row geometry of the BFS ownership (z = warp, y = lane)
+    const int oz = warp, oy = lane;
+    const bool rvalid = oz < gb.dz && oy < gb.hr;
+    const uint32_t xmask = gb.wc >= 32 ? 0xffffffffu : ((1u << gb.wc) - 1u);
+    const uint32_t existE = rvalid ? (xmask >> 1) : 0u;
+    const uint32_t existS = (rvalid && oy + 1 < gb.hr) ? xmask : 0u;
+    const uint32_t existD = (rvalid && oz + 1 < gb.dz) ? xmask : 0u;
+    const uint32_t full = (uint32_t)cap2 * 0x11111111u;
+    const int rowv = oz * PLANE + oy * B;   // first node of the owned row
+
+    int rounds = 0;
+    long long sweeps_done = 0;
+    uint32_t R = 0;
+    for (;;) {
+        // ---- sink / active rows and initial heights (node-parallel) ----
+#pragma unroll 4
+        for (int z = 0; z < B; ++z) {
+            const int v = z * PLANE + tid;
+            const int32_t gv = s3_getg(G2, v);
+            const uint32_t bK = __ballot_sync(FULLMASK, gv < 0);
+            const uint32_t bA = __ballot_sync(FULLMASK, gv > 0);
+            h[v] = gv < 0 ? 0 : HINF;
+            if (lane == 0) {
+                Kb[z * B + warp] = bK;
+                Kb[1024 + z * B + warp] = bA;
+            }
+        }
+        if (tid == 0) { misc[0] = 0; misc[1] = 0; misc[2] = 0; }
+        __syncthreads();
+        // ---- direction masks of the owned row from the nibble planes ----
+        const uint4 wE = *reinterpret_cast<const uint4 *>(FE + (rowv >> 3));
+        const uint4 wS = *reinterpret_cast<const uint4 *>(FS + (rowv >> 3));
+        const uint4 wD = *reinterpret_cast<const uint4 *>(FD + (rowv >> 3));
+        const uint32_t mE = s3_nz32(wE);
+        const uint32_t mW = (s3_nz32(s3_xor(wE, full)) & existE) << 1;
+        const uint32_t mS = s3_nz32(wS);
+        const uint32_t mD = s3_nz32(wD);
+        const uint32_t nfS = s3_nz32(s3_xor(wS, full)) & existS;   // arc (y+1) -> y has residual
+        uint32_t mN = __shfl_up_sync(FULLMASK, nfS, 1);
+        if (oy == 0) mN = 0;
+        uint32_t mU = 0;
+        if (oz > 0) {
+            const uint4 wU = *reinterpret_cast<const uint4 *>(FD + ((rowv - PLANE) >> 3));
+            const uint32_t exU = (rvalid && oz - 1 < gb.dz) ? xmask : 0u;
+            mU = s3_nz32(s3_xor(wU, full)) & exU;
+        }
+        R = Kb[oz * B + oy];
+        const uint32_t A = Kb[1024 + oz * B + oy];
+        const bool have_active = __syncthreads_or(A != 0);
+        Rb[oz * B + oy] = R;
+        __syncthreads();
+
+        // ---- global relabel: BFS over residual arcs from the sink set ----
+        int level = 0, cur = 0;
+        for (;;) {
+            const uint32_t *Rc = Rb + cur * 1024;
+            const uint32_t ryp = __shfl_down_sync(FULLMASK, R, 1), rym = __shfl_up_sync(FULLMASK, R, 1);
+            const uint32_t rzp = oz + 1 < B ? Rc[(oz + 1) * B + oy] : 0u;
+            const uint32_t rzm = oz > 0 ? Rc[(oz - 1) * B + oy] : 0u;
+            const uint32_t nw = ((mE & (R >> 1)) | (mW & (R << 1)) | (mS & ryp) | (mN & rym) | (mD & rzp) |
+                                 (mU & rzm)) & ~R;
+            R |= nw;
+            Rb[(cur ^ 1) * 1024 + oz * B + oy] = R;
+            const int lv = level + 1;
+            uint32_t b = nw;
+            while (b) {
+                const int x = __ffs(b) - 1;
+                b &= b - 1;
+                h[rowv + x] = (uint16_t)lv;
+            }
+            const uint32_t fl = (nw != 0 ? 1u : 0u) | ((A & ~R) != 0 ? 2u : 0u);
+            const uint32_t wf = __reduce_or_sync(FULLMASK, fl);
+            const int slot = level % 3;
+            if (lane == 0 && wf) atomicOr(reinterpret_cast<unsigned *>(&misc[slot]), wf);
+            if (tid == 0) misc[(level + 1) % 3] = 0;
+            __syncthreads();
+            const int f = misc[slot];
+            if (f & 1) level = lv;
+            cur ^= 1;
+            if (!(f & 1)) break;                  // no growth: BFS complete
+            if (have_active && !(f & 2)) break;   // every active node has a height
+        }
+        const int hit = __syncthreads_or((A & R) != 0);
+        if (!hit) break;
+        if (++rounds > T.max_rounds) {
+            if (tid == 0) atomicCAS(&L.st->error, 0, k + 1);
+            break;
+        }
+        // ---- push / relabel sweeps ----
+        const int cap_sweeps = T.sweep_min + T.sweep_mul * level;
+        for (int sw = 0; sw < cap_sweeps; ++sw) {
+            ++sweeps_done;
+#pragma unroll 2
+            for (int z = 0; z < B; ++z) {
+                const int v = z * PLANE + tid;
+                const int32_t e = s3_getg(G2, v);
+                if (e <= 0) continue;
+                const uint16_t hv = h[v];
+                if (hv == HINF || hv == 0) continue;
+                const uint16_t ht = hv - 1;
+                int32_t left = e;
+#pragma unroll
+                for (int d = 0; d < 6; ++d) {
+                    int32_t r;
+                    int w;
+                    if (d == 0) { r = s3_nib(FE, v); w = v + 1; }
+                    else if (d == 1) { if (lane == 0) continue; r = cap2 - s3_nib(FE, v - 1); w = v - 1; }
+                    else if (d == 2) { r = s3_nib(FS, v); w = v + B; }
+                    else if (d == 3) { if (warp == 0) continue; r = cap2 - s3_nib(FS, v - B); w = v - B; }
+                    else if (d == 4) { r = s3_nib(FD, v); w = v + PLANE; }
+                    else { if (z == 0) continue; r = cap2 - s3_nib(FD, v - PLANE); w = v - PLANE; }
+                    if (r == 0) continue;
+                    if (h[w] != ht) continue;
+                    const int32_t delta = left < r ? left : r;
+                    if (d == 0) s3_addnib(FE, v, -delta);
+                    else if (d == 1) s3_addnib(FE, w, delta);
+                    else if (d == 2) s3_addnib(FS, v, -delta);
+                    else if (d == 3) s3_addnib(FS, w, delta);
+                    else if (d == 4) s3_addnib(FD, v, -delta);
+                    else s3_addnib(FD, w, delta);
+                    s3_addg(G2, w, delta);
+                    left -= delta;
+                    if (left == 0) break;
+                }
+                if (left != e) s3_addg(G2, v, -(e - left));
+            }
+            __syncthreads();
+            int act = 0;
+#pragma unroll 2
+            for (int z = 0; z < B; ++z) {
+                const int v = z * PLANE + tid;
+                if (s3_getg(G2, v) <= 0) continue;
+                const uint16_t hv = h[v];
+                if (hv == HINF) continue;
+                uint32_t mn = HINF;
+                if (s3_nib(FE, v)) mn = min(mn, (uint32_t)h[v + 1]);
+                if (lane > 0 && s3_nib(FE, v - 1) != cap2) mn = min(mn, (uint32_t)h[v - 1]);
+                if (s3_nib(FS, v)) mn = min(mn, (uint32_t)h[v + B]);
+                if (warp > 0 && s3_nib(FS, v - B) != cap2) mn = min(mn, (uint32_t)h[v - B]);
+                if (s3_nib(FD, v)) mn = min(mn, (uint32_t)h[v + PLANE]);
+                if (z > 0 && s3_nib(FD, v - PLANE) != cap2) mn = min(mn, (uint32_t)h[v - PLANE]);
+                const uint32_t nh = (mn + 1 >= (uint32_t)M) ? HINF : mn + 1;
+                if (nh != hv) h[v] = (uint16_t)nh;
+                act |= (nh != HINF);
+            }
+            if (!__syncthreads_or(act)) break;
+        }
+    }
+    // ---- epilogue: labels (sink side) and the E/S/D residual planes ----
+    Rb[oz * B + oy] = R;
+    __syncthreads();
+#pragma unroll 4
+    for (int z = 0; z < B; ++z) {
+        const int v = z * PLANE + tid;
+        if (!(xin && yin && z < gb.dz)) continue;
+        const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + warp) * W + gb.lo_c + lane;
+        L.yhat[G] = (uint8_t)((Rb[z * B + warp] >> lane) & 1u);
+        if (L.warm) {
+            rr[v] = (uint8_t)s3_nib(FE, v);
+            rr[2 * M + v] = (uint8_t)s3_nib(FS, v);
+            rr[4 * M + v] = (uint8_t)s3_nib(FD, v);
+        }
+    }
+    if (tid == 0) {
+        atomicAdd((unsigned long long *)&L.st->solves, 1ull);
+        atomicAdd((unsigned long long *)&L.st->sweeps, (unsigned long long)sweeps_done);
+        atomicMax(&L.st->max_rounds_seen, rounds);
+    }
+}

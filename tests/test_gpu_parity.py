@@ -5,6 +5,8 @@ max block residual, clamped flag, final y / labels / multipliers.
 residual_sq is a float sum of sqrt(int)^2 (admm.py:295) whose summation order
 is BLAS-specific in the reference, so it is compared at rtol 1e-12.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -195,6 +197,47 @@ def test_3d_grids_match_oracle(size, block, iters):
                            wl.lam)
     ref = orc.run(spec, 1.0, 1.0, 0.0, iters, threads=16)
     assert state.iteration == ref["iterations"]
+    assert np.array_equal([t.energy for t in state.trace], ref["energy"])
+    assert np.array_equal(state.labels_global(), ref["yhat"])
+    assert np.array_equal(labels, ref["labels"])
+
+
+@pytest.mark.parametrize("size,kpa,lam,uscale,iters", [
+    (96, (3, 3, 3), 3.0, 1, 6),        # 32^3 boxes, 2cap = 12: shared-memory K1-3D
+    (80, (3, 3, 3), 1.0, 1, 8),        # ragged 27/27/26 boxes inside the 32^3 layout
+    (64, (2, 2, 2), 1.0, 5000, 5),     # |2u| > 32000 - 6cap: per-block HBM-scratch fallback
+    (64, (2, 2, 2), 4.0, 1, 5),        # 2cap = 16 > 15: HBM-scratch kernel
+    (64, (4, 2, 2), 2.0, 1, 6),        # mixed 16/32 box extents
+])
+def test_3d_k1_paths_match_oracle(size, kpa, lam, uscale, iters):
+    import oracle as orc
+    wl = W.c4(seed=5, size=size, block=size // kpa[0], iters=iters)
+    u = wl.u.astype(np.float64)
+    if uscale != 1:   # a few slabs of huge unaries: only their blocks leave int16 excess
+        u3 = u.reshape(wl.dims).copy()
+        u3[: size // 2] *= uscale
+        u = u3.ravel()
+    rows, cols, vals = wl.pair_arrays()
+    model = dope.EnergyModel(u, dope.SparseWeights(wl.n, rows, cols, vals), lam)
+    part = dope.make_partition(dope.GridShape(wl.dims), kpa, 0, materialize=False)
+    labels, state = dope.run(model, part, dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=iters))
+    spec = orc.LatticeSpec(wl.dims, kpa, wl.offsets, [1.0, 1.0, 1.0], u, lam)
+    ref = orc.run(spec, 1.0, 1.0, 0.0, iters, threads=16)
+    assert state.iteration == ref["iterations"]
+    assert np.array_equal([t.energy for t in state.trace], ref["energy"])
+    assert np.array_equal(state.labels_global(), ref["yhat"])
+    assert np.array_equal(labels, ref["labels"])
+
+
+def test_c4_full_size_first_iterations_match_oracle():
+    import oracle as orc
+    wl = W.c4(iters=3)
+    rows, cols, vals = wl.pair_arrays()
+    model = dope.EnergyModel(wl.u.astype(np.float64), dope.SparseWeights(wl.n, rows, cols, vals), wl.lam)
+    part = dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0, materialize=False)
+    labels, state = dope.run(model, part, dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=3))
+    spec = orc.LatticeSpec(wl.dims, wl.kpa, wl.offsets, [1.0, 1.0, 1.0], wl.u.astype(np.float64), wl.lam)
+    ref = orc.run(spec, 1.0, 1.0, 0.0, 3, threads=os.cpu_count() or 16)
     assert np.array_equal([t.energy for t in state.trace], ref["energy"])
     assert np.array_equal(state.labels_global(), ref["yhat"])
     assert np.array_equal(labels, ref["labels"])
