@@ -77,6 +77,8 @@ struct Lat2 {
     int32_t sharded;        // consensus writes local aggregates; dope_decide applies
     int64_t *agg;           // [E, R2 (double bits), max ss, clamped] of this shard
     int32_t pdl;            // launched with programmatic dependent launch (DOPE_PDL=1)
+    int32_t nib3;           // 3D: shared-memory K1 with nibble residual planes (lattice3d_smem.cuh)
+    int32_t q3;             // 3D: u / a / y rows can be read as quads (W % 4 == 0, aligned)
 };
 
 // ---------------------------------------------------------------------------
@@ -1238,6 +1240,14 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
                          ((uintptr_t)o.a >> 1) | ((uintptr_t)o.u >> 2);
     o.pdl = getenv("DOPE_PDL") != nullptr;
     o.vec4 = !is3 && (o.W % 4 == 0) && (o.ax.rem == 0) && (o.ax.base % 4 == 0) && (al % 4 == 0);
+    o.q3 = is3 && (o.W % 4 == 0) && (al % 4 == 0);
+    // 32^3 boxes with 2*cap <= 15 run the shared-memory K1 (nibble residuals);
+    // DOPE_K1_3D=l2 forces the HBM-scratch kernel (diagnostics)
+    static const bool k1_3d_l2 = [] {
+        const char *e = getenv("DOPE_K1_3D");
+        return e && strcmp(e, "l2") == 0;
+    }();
+    o.nib3 = is3 && !k1_3d_l2 && o.boxd == 32 && o.boxh == 32 && o.boxw == 32 && 2 * o.cap <= 15;
     return DOPE_OK;
 }
 
@@ -1265,16 +1275,6 @@ static int configure_k1(const Variant *v) {
         configured[(void *)v->kernel] = true;
     }
     return DOPE_OK;
-}
-
-// 32^3 boxes with 2*cap <= 15 run the shared-memory kernel (lattice3d_smem.cuh);
-// DOPE_K1_3D=l2 forces the HBM-scratch kernel (diagnostics).
-static bool use_k1_3d_smem(const Lat2 &o, const Variant3 *v) {
-    static const bool off = [] {
-        const char *e = getenv("DOPE_K1_3D");
-        return e && strcmp(e, "l2") == 0;
-    }();
-    return !off && v->bd == 32 && v->bh == 32 && v->bw == 32 && 2 * o.cap <= 15;
 }
 
 static int configure_k1_3d(const Variant3 *v) {
@@ -1337,7 +1337,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 static int launch_k1(const Plan &P, cudaStream_t s) {
     int rc = configure_plan(P);
     if (rc) return rc;
-    if (P.v3 && use_k1_3d_smem(P.o, P.v3)) k_block_mincut3d_s<<<P.o.K, k1s::NT, k1s::SMEM, s>>>(P.o, default_tune());
+    if (P.v3 && P.o.nib3) k_block_mincut3d_s<<<P.o.K, k1s::NT, k1s::SMEM, s>>>(P.o, default_tune());
     else if (P.v3) P.v3->kernel<<<P.o.K, P.v3->nt, P.v3->smem, s>>>(P.o, default_tune());
     else return cuda_check(launch_pdl(P.v->kernel, dim3(P.o.K), dim3(P.v->nt), P.v->smem, s, P.o, default_tune()),
                            "launch K1");
@@ -1580,7 +1580,8 @@ int dope_admm_init(const dope_lattice *L, void *stream) {
     k_init_unary<<<grid_for(P.n), 256, 0, s>>>(P.o, P.n);
     rc = cuda_check(cudaGetLastError(), "init_unary");
     if (rc) return rc;
-    if (P.v3) k_init_resid3d<<<P.o.K, 256, 0, s>>>(P.o, P.o.boxd, P.o.boxh, P.o.boxw);
+    if (P.v3 && P.o.nib3) k_init_resid3d_nib<<<P.o.K, 256, 0, s>>>(P.o);
+    else if (P.v3) k_init_resid3d<<<P.o.K, 256, 0, s>>>(P.o, P.o.boxd, P.o.boxh, P.o.boxw);
     else k_init_resid<<<P.o.K, 256, 0, s>>>(P.o);
     return cuda_check(cudaGetLastError(), "init_resid");
 }

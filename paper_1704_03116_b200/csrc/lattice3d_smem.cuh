@@ -63,6 +63,12 @@ __device__ __forceinline__ uint4 s3_xor(uint4 w, uint32_t c) {
     return make_uint4(w.x ^ c, w.y ^ c, w.z ^ c, w.w ^ c);
 }
 
+__device__ __forceinline__ int64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return (int64_t)t;
+}
+
 // out of line so that its registers do not count against the fast path
 __device__ __noinline__ void mincut3d_l2_fallback(const Lat2 &L, const K1Tune &T, int k, uint8_t *smem) {
     mincut3d_l2<k1s::B, k1s::B, k1s::B, k1s::NT>(L, T, k, smem);
@@ -80,10 +86,25 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
     int *misc = reinterpret_cast<int *>(sm3 + OFF_MISC);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int k = blockIdx.x;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm3 + OFF_MISC + 32);
     if (L.st->stop) return;
     if (L.skip_clean && L.dirty[k] == 0) return;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
     if (tid == 0) L.dirty[k] = 0;
+    // diagnostics (L.timeline): [0] start [1] end [2] rounds [3] sweeps
+    // [4] prologue end [5] first relabel end [6] its levels [7] ns in relabels
+    const bool tl = L.timeline && tid == 0;
+    int64_t t_bfs = 0;
+    if (tl) {
+        const int64_t t = gtimer();
+        L.timeline[8 * k + 0] = t;
+        L.timeline[8 * k + 4] = t;
+        L.timeline[8 * k + 5] = t;
+    }
 
     int bz, by, bx;
     const Geo3 gb = block_geo3(L, k, bz, by, bx);
@@ -92,79 +113,234 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
     const int32_t cap = L.cap, cap2 = 2 * cap;
     const astore_t *__restrict__ a_cur = L.a;
     const ystore_t *__restrict__ y_cur = L.y2[L.st->ycur];
-    uint8_t *rr = L.resid + (size_t)k * 6 * M;   // planes 0 (E), 2 (S), 4 (D)
+    // persistent residuals: nibble planes E, S, D (uint32[3][M/8]) at the
+    // start of the block's resid slot; the fallback body uses byte planes
+    uint8_t *rr = L.resid + (size_t)k * 6 * M;
+    uint32_t *gF = reinterpret_cast<uint32_t *>(rr);
     const bool up_z = gb.lo_z > 0, dn_z = gb.lo_z + gb.dz < D;
     const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
     const bool lf_c = gb.lo_c > 0, rt_c = gb.lo_c + gb.wc < W;
     const bool xin = lane < gb.wc, yin = warp < gb.hr;
 
-    // ---- prologue: 2*linear, residual nibbles, packed excess ----
+    // ---- prologue ----
+    // (1) the persistent E/S/D nibble planes (48 KB) stream in by one bulk copy
+    //     while (2) 2*linear is computed from u, a, y; (3) then the excess adds
+    //     the stored flow: excess = 2*linear + sum over the 6 arcs of (r - cap).
+    if (L.warm) {
+        if (tid == 0) {
+            mbar_expect_tx(bar, 3 * NIBW * 4);
+#pragma unroll
+            for (int p = 0; p < 3; ++p)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                    ::"r"(smem_u32(FE + p * NIBW)), "l"(gF + p * NIBW), "r"(NIBW * 4), "r"(smem_u32(bar))
+                    : "memory");
+        }
+    }
     int over = 0;
-#pragma unroll 2
-    for (int z = 0; z < B; ++z) {
-        const int v = z * PLANE + tid;
-        const bool valid = xin && yin && z < gb.dz;
-        int32_t gv = 0, fE = 0, fS = 0, fD = 0;
-        if (valid) {
-            const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + warp) * W + gb.lo_c + lane;
-            const int32_t yg = (int32_t)y_cur[G];
-            int32_t sx = 0;
-            if (lane == 0 && lf_c) sx += yg - y_cur[G - 1];
-            if (lane == gb.wc - 1 && rt_c) sx += yg - y_cur[G + 1];
-            if (warp == 0 && up_r) sx += yg - y_cur[G - W];
-            if (warp == gb.hr - 1 && dn_r) sx += yg - y_cur[G + W];
-            if (z == 0 && up_z) sx += yg - y_cur[G - HW];
-            if (z == gb.dz - 1 && dn_z) sx += yg - y_cur[G + HW];
-            gv = 2 * L.u[G] + L.lamw * sx + L.mu * (2 * (int32_t)a_cur[G] - yg) + L.mu;
-            over |= (gv > GMAX - 6 * cap) | (gv < -(GMAX - 6 * cap));
-            const bool hE = lane + 1 < gb.wc, hS = warp + 1 < gb.hr, hD = z + 1 < gb.dz;
-            if (L.warm) {
-                fE = hE ? rr[v] : 0;
-                fS = hS ? rr[2 * M + v] : 0;
-                fD = hD ? rr[4 * M + v] : 0;
-                // excess = 2*linear + sum over the 6 arcs of (residual - cap)
-                int32_t f = (hE ? fE - cap : 0) + (hS ? fS - cap : 0) + (hD ? fD - cap : 0);
-                if (lane > 0) f += cap - rr[v - 1];
-                if (warp > 0) f += cap - rr[2 * M + v - B];
-                if (z > 0) f += cap - rr[4 * M + v - PLANE];
-                gv += f;
-            } else {
-                fE = hE ? cap : 0;
-                fS = hS ? cap : 0;
-                fD = hD ? cap : 0;
+    const int32_t lim = GMAX - 6 * cap;
+    const bool quads = L.q3 && (gb.lo_c % 4 == 0) && (gb.wc % 4 == 0);
+    if (quads) {
+        // thread -> 4 consecutive x of one row; 128 rows per pass, 8 passes
+        const int x0 = (tid & 7) * 4;
+#pragma unroll 1
+        for (int p0 = 0; p0 < 8; p0 += 4) {
+            int4 u4[4];
+            uint2 a4[4];
+            uint32_t y4[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int row = (p0 + j) * 128 + (tid >> 3), z = row >> 5, y = row & 31;
+                u4[j] = make_int4(0, 0, 0, 0);
+                a4[j] = make_uint2(0, 0);
+                y4[j] = 0;
+                if (z < gb.dz && y < gb.hr && x0 < gb.wc) {
+                    const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + y) * W + gb.lo_c + x0;
+                    u4[j] = __ldg(reinterpret_cast<const int4 *>(L.u + G));
+                    a4[j] = *reinterpret_cast<const uint2 *>(a_cur + G);
+                    y4[j] = *reinterpret_cast<const uint32_t *>(y_cur + G);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int row = (p0 + j) * 128 + (tid >> 3), z = row >> 5, y = row & 31;
+                const int v0 = z * PLANE + y * B + x0;
+                const bool valid = z < gb.dz && y < gb.hr && x0 < gb.wc;
+                int32_t g[4] = {0, 0, 0, 0};
+                if (valid) {
+                    const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + y) * W + gb.lo_c + x0;
+                    int32_t yv[4], sx[4] = {0, 0, 0, 0};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) yv[e] = (int32_t)((y4[j] >> (8 * e)) & 0xffu);
+                    if (x0 == 0 && lf_c) sx[0] += yv[0] - y_cur[G - 1];
+                    if (x0 + 4 == gb.wc && rt_c) sx[3] += yv[3] - y_cur[G + 4];
+                    const bool yb = (y == 0 && up_r), yt = (y == gb.hr - 1 && dn_r);
+                    const bool zb = (z == 0 && up_z), zt = (z == gb.dz - 1 && dn_z);
+                    const uint32_t n_yb = yb ? *reinterpret_cast<const uint32_t *>(y_cur + G - W) : 0u;
+                    const uint32_t n_yt = yt ? *reinterpret_cast<const uint32_t *>(y_cur + G + W) : 0u;
+                    const uint32_t n_zb = zb ? *reinterpret_cast<const uint32_t *>(y_cur + G - HW) : 0u;
+                    const uint32_t n_zt = zt ? *reinterpret_cast<const uint32_t *>(y_cur + G + HW) : 0u;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        if (yb) sx[e] += yv[e] - (int32_t)((n_yb >> (8 * e)) & 0xffu);
+                        if (yt) sx[e] += yv[e] - (int32_t)((n_yt >> (8 * e)) & 0xffu);
+                        if (zb) sx[e] += yv[e] - (int32_t)((n_zb >> (8 * e)) & 0xffu);
+                        if (zt) sx[e] += yv[e] - (int32_t)((n_zt >> (8 * e)) & 0xffu);
+                    }
+                    const int32_t uu[4] = {u4[j].x, u4[j].y, u4[j].z, u4[j].w};
+                    const uint32_t aw[2] = {a4[j].x, a4[j].y};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int32_t av = (int32_t)(int16_t)((aw[e >> 1] >> (16 * (e & 1))) & 0xffffu);
+                        g[e] = 2 * uu[e] + L.lamw * sx[e] + L.mu * (2 * av - yv[e]) + L.mu;
+                        over |= (g[e] > lim) | (g[e] < -lim);
+                    }
+                }
+                if (!L.warm) {   // cold residual graph: every existing arc at cap
+                    uint32_t nE = 0, nS = 0, nD = 0;
+                    if (valid) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            if (x0 + e + 1 < gb.wc) nE |= (uint32_t)cap << (4 * e);
+                            if (y + 1 < gb.hr) nS |= (uint32_t)cap << (4 * e);
+                            if (z + 1 < gb.dz) nD |= (uint32_t)cap << (4 * e);
+                        }
+                    }
+                    reinterpret_cast<uint16_t *>(FE)[v0 >> 2] = (uint16_t)nE;
+                    reinterpret_cast<uint16_t *>(FS)[v0 >> 2] = (uint16_t)nS;
+                    reinterpret_cast<uint16_t *>(FD)[v0 >> 2] = (uint16_t)nD;
+                }
+                uint2 gw;
+                gw.x = ((uint32_t)(g[0] + BIAS) & 0xffffu) | ((uint32_t)(g[1] + BIAS) << 16);
+                gw.y = ((uint32_t)(g[2] + BIAS) & 0xffffu) | ((uint32_t)(g[3] + BIAS) << 16);
+                *reinterpret_cast<uint2 *>(G2 + (v0 >> 1)) = gw;
             }
         }
-        // pack: 8 lanes -> one nibble word per plane, 2 lanes -> one excess word
-        uint32_t nE = (uint32_t)fE << ((lane & 7) << 2), nS = (uint32_t)fS << ((lane & 7) << 2),
-                 nD = (uint32_t)fD << ((lane & 7) << 2);
+        if (L.warm) {
+            mbar_wait(bar, 0);
+#pragma unroll 2
+            for (int p = 0; p < 8; ++p) {
+                const int row = p * 128 + (tid >> 3), z = row >> 5, y = row & 31;
+                const int v0 = z * PLANE + y * B + x0;
+                if (!(z < gb.dz && y < gb.hr && x0 < gb.wc)) continue;
+                int32_t f[4];
 #pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-            nE |= __shfl_xor_sync(FULLMASK, nE, o);
-            nS |= __shfl_xor_sync(FULLMASK, nS, o);
-            nD |= __shfl_xor_sync(FULLMASK, nD, o);
+                for (int e = 0; e < 4; ++e) {
+                    const int v = v0 + e, x = x0 + e;
+                    int32_t t = 0;
+                    if (x + 1 < gb.wc) t += s3_nib(FE, v) - cap;
+                    if (x > 0) t += cap - s3_nib(FE, v - 1);
+                    if (y + 1 < gb.hr) t += s3_nib(FS, v) - cap;
+                    if (y > 0) t += cap - s3_nib(FS, v - B);
+                    if (z + 1 < gb.dz) t += s3_nib(FD, v) - cap;
+                    if (z > 0) t += cap - s3_nib(FD, v - PLANE);
+                    f[e] = t;
+                }
+                uint2 gw = *reinterpret_cast<const uint2 *>(G2 + (v0 >> 1));
+                gw.x += (uint32_t)f[0] + ((uint32_t)f[1] << 16);
+                gw.y += (uint32_t)f[2] + ((uint32_t)f[3] << 16);
+                *reinterpret_cast<uint2 *>(G2 + (v0 >> 1)) = gw;
+            }
         }
-        if ((lane & 7) == 0) {
-            FE[v >> 3] = nE;
-            FS[v >> 3] = nS;
-            FD[v >> 3] = nD;
+    } else {
+        // scalar prologue (blocks whose x range is not quad-aligned): lane = x
+#pragma unroll 2
+        for (int z = 0; z < B; ++z) {
+            const int v = z * PLANE + tid;
+            const bool valid = xin && yin && z < gb.dz;
+            int32_t gv = 0;
+            if (valid) {
+                const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + warp) * W + gb.lo_c + lane;
+                const int32_t yg = (int32_t)y_cur[G];
+                int32_t sx = 0;
+                if (lane == 0 && lf_c) sx += yg - y_cur[G - 1];
+                if (lane == gb.wc - 1 && rt_c) sx += yg - y_cur[G + 1];
+                if (warp == 0 && up_r) sx += yg - y_cur[G - W];
+                if (warp == gb.hr - 1 && dn_r) sx += yg - y_cur[G + W];
+                if (z == 0 && up_z) sx += yg - y_cur[G - HW];
+                if (z == gb.dz - 1 && dn_z) sx += yg - y_cur[G + HW];
+                gv = 2 * L.u[G] + L.lamw * sx + L.mu * (2 * (int32_t)a_cur[G] - yg) + L.mu;
+                over |= (gv > lim) | (gv < -lim);
+            }
+            if (!L.warm) {
+                const uint32_t sh = (lane & 7) << 2;
+                uint32_t nE = (valid && lane + 1 < gb.wc) ? (uint32_t)cap << sh : 0u;
+                uint32_t nS = (valid && warp + 1 < gb.hr) ? (uint32_t)cap << sh : 0u;
+                uint32_t nD = (valid && z + 1 < gb.dz) ? (uint32_t)cap << sh : 0u;
+#pragma unroll
+                for (int o = 1; o < 8; o <<= 1) {
+                    nE |= __shfl_xor_sync(FULLMASK, nE, o);
+                    nS |= __shfl_xor_sync(FULLMASK, nS, o);
+                    nD |= __shfl_xor_sync(FULLMASK, nD, o);
+                }
+                if ((lane & 7) == 0) {
+                    FE[v >> 3] = nE;
+                    FS[v >> 3] = nS;
+                    FD[v >> 3] = nD;
+                }
+            }
+            const uint32_t gb16 = (uint32_t)(gv + BIAS) & 0xffffu;
+            const uint32_t hi = __shfl_down_sync(FULLMASK, gb16, 1);
+            if ((lane & 1) == 0) G2[v >> 1] = gb16 | (hi << 16);
         }
-        const uint32_t gb16 = (uint32_t)(gv + BIAS) & 0xffffu;
-        const uint32_t hi = __shfl_down_sync(FULLMASK, gb16, 1);
-        if ((lane & 1) == 0) G2[v >> 1] = gb16 | (hi << 16);
+        if (L.warm) {
+            mbar_wait(bar, 0);
+#pragma unroll 2
+            for (int z = 0; z < B; ++z) {
+                const int v = z * PLANE + tid;
+                int32_t f = 0;
+                if (xin && yin && z < gb.dz) {
+                    if (lane + 1 < gb.wc) f += s3_nib(FE, v) - cap;
+                    if (lane > 0) f += cap - s3_nib(FE, v - 1);
+                    if (warp + 1 < gb.hr) f += s3_nib(FS, v) - cap;
+                    if (warp > 0) f += cap - s3_nib(FS, v - B);
+                    if (z + 1 < gb.dz) f += s3_nib(FD, v) - cap;
+                    if (z > 0) f += cap - s3_nib(FD, v - PLANE);
+                }
+                const int32_t fo = __shfl_down_sync(FULLMASK, f, 1);
+                if ((lane & 1) == 0) G2[v >> 1] += (uint32_t)f + ((uint32_t)fo << 16);
+            }
+        }
     }
     if (__syncthreads_or(over)) {
-        // this block's excess could leave int16: solve it with the HBM-scratch body
+        // this block's excess could leave int16: solve it with the HBM-scratch
+        // body on byte planes, then repack its E/S/D residuals as nibbles
+        if (L.warm) {
+            // forward planes from the nibbles; reverse planes zeroed (the body
+            // derives the existing ones; the others must read as "no arc")
+            for (int v = tid; v < M; v += NT) {
+                rr[v] = (uint8_t)s3_nib(FE, v);
+                rr[M + v] = 0;
+                rr[2 * M + v] = (uint8_t)s3_nib(FS, v);
+                rr[3 * M + v] = 0;
+                rr[4 * M + v] = (uint8_t)s3_nib(FD, v);
+                rr[5 * M + v] = 0;
+            }
+        }
+        __syncthreads();
         mincut3d_l2_fallback(L, T, k, sm3);
+        if (L.warm) {
+            __syncthreads();
+            for (int w = tid; w < 3 * NIBW; w += NT) {
+                const int p = w / NIBW, v0 = (w - p * NIBW) * 8;
+                uint32_t x = 0;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) x |= (uint32_t)rr[2 * p * M + v0 + e] << (4 * e);
+                FE[w] = x;
+            }
+            __syncthreads();
+            for (int w = tid; w < 3 * NIBW; w += NT) gF[w] = FE[w];
+        }
         return;
     }
 
+    if (tl) L.timeline[8 * k + 4] = gtimer();
     // row geometry of the BFS ownership (z = warp, y = lane)
     const int oz = warp, oy = lane;
     const bool rvalid = oz < gb.dz && oy < gb.hr;
     const uint32_t xmask = gb.wc >= 32 ? 0xffffffffu : ((1u << gb.wc) - 1u);
     const uint32_t existE = rvalid ? (xmask >> 1) : 0u;
     const uint32_t existS = (rvalid && oy + 1 < gb.hr) ? xmask : 0u;
-    const uint32_t existD = (rvalid && oz + 1 < gb.dz) ? xmask : 0u;
     const uint32_t full = (uint32_t)cap2 * 0x11111111u;
     const int rowv = oz * PLANE + oy * B;   // first node of the owned row
 
@@ -204,6 +380,7 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
             const uint32_t exU = (rvalid && oz - 1 < gb.dz) ? xmask : 0u;
             mU = s3_nz32(s3_xor(wU, full)) & exU;
         }
+        const int64_t t0 = tl ? gtimer() : 0;
         R = Kb[oz * B + oy];
         const uint32_t A = Kb[1024 + oz * B + oy];
         const bool have_active = __syncthreads_or(A != 0);
@@ -241,6 +418,14 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
             if (have_active && !(f & 2)) break;   // every active node has a height
         }
         const int hit = __syncthreads_or((A & R) != 0);
+        if (tl) {
+            const int64_t t1 = gtimer();
+            t_bfs += t1 - t0;
+            if (rounds == 0) {
+                L.timeline[8 * k + 5] = t1;
+                L.timeline[8 * k + 6] = level;
+            }
+        }
         if (!hit) break;
         if (++rounds > T.max_rounds) {
             if (tid == 0) atomicCAS(&L.st->error, 0, k + 1);
@@ -311,19 +496,46 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
     __syncthreads();
 #pragma unroll 4
     for (int z = 0; z < B; ++z) {
-        const int v = z * PLANE + tid;
         if (!(xin && yin && z < gb.dz)) continue;
         const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + warp) * W + gb.lo_c + lane;
         L.yhat[G] = (uint8_t)((Rb[z * B + warp] >> lane) & 1u);
-        if (L.warm) {
-            rr[v] = (uint8_t)s3_nib(FE, v);
-            rr[2 * M + v] = (uint8_t)s3_nib(FS, v);
-            rr[4 * M + v] = (uint8_t)s3_nib(FD, v);
+    }
+    if (L.warm) {   // E/S/D nibble planes back (48 KB, 16-byte stores)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const int w = (j * NT + tid) * 4;
+            *reinterpret_cast<uint4 *>(gF + w) = *reinterpret_cast<const uint4 *>(FE + w);
         }
+    }
+    if (tl) {
+        L.timeline[8 * k + 1] = gtimer();
+        L.timeline[8 * k + 2] = rounds;
+        L.timeline[8 * k + 3] = sweeps_done;
+        L.timeline[8 * k + 7] = t_bfs;
     }
     if (tid == 0) {
         atomicAdd((unsigned long long *)&L.st->solves, 1ull);
         atomicAdd((unsigned long long *)&L.st->sweeps, (unsigned long long)sweeps_done);
         atomicMax(&L.st->max_rounds_seen, rounds);
+    }
+}
+
+// cold residual graph in the nibble layout: every existing E/S/D arc at cap
+__global__ void k_init_resid3d_nib(Lat2 L) {
+    using namespace k1s;
+    const int k = blockIdx.x;
+    int bz, by, bx;
+    const Geo3 gb = block_geo3(L, k, bz, by, bx);
+    uint32_t *gF = reinterpret_cast<uint32_t *>(L.resid + (size_t)k * 6 * M);
+    for (int w = threadIdx.x; w < 3 * NIBW; w += blockDim.x) {
+        const int p = w / NIBW, v0 = (w - p * NIBW) * 8;
+        uint32_t x = 0;
+        for (int e = 0; e < 8; ++e) {
+            const int v = v0 + e, z = v / PLANE, r = (v / B) % B, c = v % B;
+            if (!(z < gb.dz && r < gb.hr && c < gb.wc)) continue;
+            const bool has = p == 0 ? c + 1 < gb.wc : p == 1 ? r + 1 < gb.hr : z + 1 < gb.dz;
+            if (has) x |= (uint32_t)L.cap << (4 * e);
+        }
+        gF[w] = x;
     }
 }
