@@ -21,6 +21,9 @@
 // y*32 + x with z the loop index, y the warp and x the lane (conflict-free).
 // Labels, flows and the exactness argument are those of DESIGN.md §2.
 
+#ifndef K1S_QB
+#define K1S_QB 2
+#endif
 namespace k1s {
 constexpr int B = 32, M = B * B * B, NT = 1024, PLANE = B * B;
 constexpr int NIBW = M / 8;                                // nibble words per plane
@@ -29,7 +32,9 @@ constexpr size_t OFF_H = OFF_G + 2 * (size_t)M;            // uint16[M]
 constexpr size_t OFF_F = OFF_H + 2 * (size_t)M;            // uint32[3][M/8] E,S,D residual nibbles
 constexpr size_t OFF_R = OFF_F + 3 * 4 * (size_t)NIBW;     // uint32[2][1024] reach rows
 constexpr size_t OFF_K = OFF_R + 2 * 4 * 1024;             // uint32[2][1024] sink / active rows
-constexpr size_t OFF_MISC = OFF_K + 2 * 4 * 1024;
+constexpr size_t OFF_SLOT = OFF_K + 2 * 4 * 1024;           // uint16[32 warps][32] batches
+constexpr size_t OFF_FLAG = OFF_SLOT + 2 * 32 * 32;          // uint32[2][32] row-activity flags
+constexpr size_t OFF_MISC = OFF_FLAG + 2 * 4 * 32;
 constexpr size_t SMEM = OFF_MISC + 64;
 constexpr int BIAS = 32768;
 constexpr int GMAX = 32000;
@@ -69,6 +74,93 @@ __device__ __forceinline__ int64_t gtimer() {
     return (int64_t)t;
 }
 
+
+__device__ __forceinline__ uint32_t s3_lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Warp-level stream compaction: the set bits of `word` (lane i <-> node v of
+// lane i) join the warp's batch `slots[0..cnt)`; every full batch of 32 runs
+// `work(node)` with one node per lane.  Returns the new batch fill.
+template <class F>
+__device__ __forceinline__ int s3_enqueue(uint16_t *slots, uint32_t word, int cnt, int lane, int v, F &&work) {
+    while (word) {
+        const bool mine = (word >> lane) & 1u;
+        const int rank = __popc(word & s3_lanemask_lt());
+        const int room = 32 - cnt;
+        if (mine && rank < room) slots[cnt + rank] = (uint16_t)v;
+        const int n = __popc(word);
+        word = __ballot_sync(FULLMASK, mine && rank >= room);
+        if (n >= room) {
+            __syncwarp();
+            work((int)slots[lane]);
+            __syncwarp();
+            cnt = 0;
+        } else {
+            cnt += n;
+        }
+    }
+    return cnt;
+}
+
+// push the excess of active node v along its admissible arcs (h[w] = h[v]-1),
+// E W S N D U order
+__device__ __forceinline__ void s3_push(uint32_t *G2, const uint16_t *h, uint32_t *FE, uint32_t *FS,
+                                        uint32_t *FD, uint32_t *Fr, int v, int32_t cap2) {
+    using namespace k1s;
+    const int32_t e = s3_getg(G2, v);
+    const uint16_t ht = h[v] - 1;
+    const int x = v & (B - 1), y = (v >> 5) & (B - 1), z = v >> 10;
+    int32_t left = e;
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+        int32_t r;
+        int w;
+        if (d == 0) { r = s3_nib(FE, v); w = v + 1; }
+        else if (d == 1) { if (x == 0) continue; r = cap2 - s3_nib(FE, v - 1); w = v - 1; }
+        else if (d == 2) { r = s3_nib(FS, v); w = v + B; }
+        else if (d == 3) { if (y == 0) continue; r = cap2 - s3_nib(FS, v - B); w = v - B; }
+        else if (d == 4) { r = s3_nib(FD, v); w = v + PLANE; }
+        else { if (z == 0) continue; r = cap2 - s3_nib(FD, v - PLANE); w = v - PLANE; }
+        if (r == 0) continue;
+        if (h[w] != ht) continue;
+        const int32_t delta = left < r ? left : r;
+        if (d == 0) s3_addnib(FE, v, -delta);
+        else if (d == 1) s3_addnib(FE, w, delta);
+        else if (d == 2) s3_addnib(FS, v, -delta);
+        else if (d == 3) s3_addnib(FS, w, delta);
+        else if (d == 4) s3_addnib(FD, v, -delta);
+        else s3_addnib(FD, w, delta);
+        s3_addg(G2, w, delta);
+        atomicOr(&Fr[(w >> 5) & (B - 1)], 1u << (w >> 10));
+        left -= delta;
+        if (left == 0) break;
+    }
+    if (left != e) s3_addg(G2, v, -(e - left));
+    if (left) atomicOr(&Fr[y], 1u << z);
+}
+
+// h[v] = 1 + min height over v's residual arcs (HINF when none or >= M);
+// returns whether v stays below HINF
+__device__ __forceinline__ int s3_relabel(uint16_t *h, const uint32_t *FE, const uint32_t *FS,
+                                          const uint32_t *FD, uint32_t *Fp, int v, int32_t cap2) {
+    using namespace k1s;
+    const int x = v & (B - 1), y = (v >> 5) & (B - 1), z = v >> 10;
+    uint32_t mn = HINF;
+    if (s3_nib(FE, v)) mn = min(mn, (uint32_t)h[v + 1]);
+    if (x > 0 && s3_nib(FE, v - 1) != cap2) mn = min(mn, (uint32_t)h[v - 1]);
+    if (s3_nib(FS, v)) mn = min(mn, (uint32_t)h[v + B]);
+    if (y > 0 && s3_nib(FS, v - B) != cap2) mn = min(mn, (uint32_t)h[v - B]);
+    if (s3_nib(FD, v)) mn = min(mn, (uint32_t)h[v + PLANE]);
+    if (z > 0 && s3_nib(FD, v - PLANE) != cap2) mn = min(mn, (uint32_t)h[v - PLANE]);
+    const uint32_t nh = (mn + 1 >= (uint32_t)M) ? HINF : mn + 1;
+    if (nh != h[v]) h[v] = (uint16_t)nh;
+    if (nh != HINF) atomicOr(&Fp[y], 1u << z);
+    return nh != HINF;
+}
+
 // out of line so that its registers do not count against the fast path
 __device__ __noinline__ void mincut3d_l2_fallback(const Lat2 &L, const K1Tune &T, int k, uint8_t *smem) {
     mincut3d_l2<k1s::B, k1s::B, k1s::B, k1s::NT>(L, T, k, smem);
@@ -85,6 +177,10 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
     uint32_t *Kb = reinterpret_cast<uint32_t *>(sm3 + OFF_K);   // [0] sink rows, [1] active rows
     int *misc = reinterpret_cast<int *>(sm3 + OFF_MISC);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint16_t *slots = reinterpret_cast<uint16_t *>(sm3 + OFF_SLOT) + warp * 32;
+    // row-activity flags: word y, bit z <=> row (z, y) may hold a node to push
+    // (Fp) / to relabel (Fr); warp w scans the rows of word w
+    uint32_t *Fp = reinterpret_cast<uint32_t *>(sm3 + OFF_FLAG), *Fr = Fp + 32;
     const int k = blockIdx.x;
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm3 + OFF_MISC + 32);
     if (L.st->stop) return;
@@ -141,52 +237,68 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
     const int32_t lim = GMAX - 6 * cap;
     const bool quads = L.q3 && (gb.lo_c % 4 == 0) && (gb.wc % 4 == 0);
     if (quads) {
-        // thread -> 4 consecutive x of one row; 128 rows per pass, 8 passes
+        // thread -> 4 consecutive x of one row; 128 rows per pass, 8 passes.
+        // Every load of a pass (incl. the cross-block neighbour rows) is
+        // issued before any is used.
         const int x0 = (tid & 7) * 4;
+        const int xs = (x0 & 7) * 4;   // bit offset of the quad in its nibble word
+        constexpr int QB = K1S_QB;     // rows per thread in flight
 #pragma unroll 1
-        for (int p0 = 0; p0 < 8; p0 += 4) {
-            int4 u4[4];
-            uint2 a4[4];
-            uint32_t y4[4];
+        for (int p0 = 0; p0 < 8; p0 += QB) {
+            int4 u4[QB];
+            uint2 a4[QB];
+            uint32_t y4[QB], ny[QB], nz[QB], nx[QB];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < QB; ++j) {
                 const int row = (p0 + j) * 128 + (tid >> 3), z = row >> 5, y = row & 31;
                 u4[j] = make_int4(0, 0, 0, 0);
                 a4[j] = make_uint2(0, 0);
-                y4[j] = 0;
+                y4[j] = ny[j] = nz[j] = nx[j] = 0;
                 if (z < gb.dz && y < gb.hr && x0 < gb.wc) {
                     const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + y) * W + gb.lo_c + x0;
                     u4[j] = __ldg(reinterpret_cast<const int4 *>(L.u + G));
                     a4[j] = *reinterpret_cast<const uint2 *>(a_cur + G);
                     y4[j] = *reinterpret_cast<const uint32_t *>(y_cur + G);
+                    // one cross-block row per axis (both sides only when the block is 1 thick: below)
+                    if (y == 0 && up_r) ny[j] = *reinterpret_cast<const uint32_t *>(y_cur + G - W);
+                    else if (y == gb.hr - 1 && dn_r) ny[j] = *reinterpret_cast<const uint32_t *>(y_cur + G + W);
+                    if (z == 0 && up_z) nz[j] = *reinterpret_cast<const uint32_t *>(y_cur + G - HW);
+                    else if (z == gb.dz - 1 && dn_z) nz[j] = *reinterpret_cast<const uint32_t *>(y_cur + G + HW);
+                    if (x0 == 0 && lf_c) nx[j] = y_cur[G - 1];
+                    if (x0 + 4 == gb.wc && rt_c) nx[j] |= (uint32_t)y_cur[G + 4] << 8;
                 }
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < QB; ++j) {
                 const int row = (p0 + j) * 128 + (tid >> 3), z = row >> 5, y = row & 31;
                 const int v0 = z * PLANE + y * B + x0;
                 const bool valid = z < gb.dz && y < gb.hr && x0 < gb.wc;
                 int32_t g[4] = {0, 0, 0, 0};
                 if (valid) {
-                    const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + y) * W + gb.lo_c + x0;
-                    int32_t yv[4], sx[4] = {0, 0, 0, 0};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) yv[e] = (int32_t)((y4[j] >> (8 * e)) & 0xffu);
-                    if (x0 == 0 && lf_c) sx[0] += yv[0] - y_cur[G - 1];
-                    if (x0 + 4 == gb.wc && rt_c) sx[3] += yv[3] - y_cur[G + 4];
                     const bool yb = (y == 0 && up_r), yt = (y == gb.hr - 1 && dn_r);
                     const bool zb = (z == 0 && up_z), zt = (z == gb.dz - 1 && dn_z);
-                    const uint32_t n_yb = yb ? *reinterpret_cast<const uint32_t *>(y_cur + G - W) : 0u;
-                    const uint32_t n_yt = yt ? *reinterpret_cast<const uint32_t *>(y_cur + G + W) : 0u;
-                    const uint32_t n_zb = zb ? *reinterpret_cast<const uint32_t *>(y_cur + G - HW) : 0u;
-                    const uint32_t n_zt = zt ? *reinterpret_cast<const uint32_t *>(y_cur + G + HW) : 0u;
+                    int32_t yv[4], sx[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        if (yb) sx[e] += yv[e] - (int32_t)((n_yb >> (8 * e)) & 0xffu);
-                        if (yt) sx[e] += yv[e] - (int32_t)((n_yt >> (8 * e)) & 0xffu);
-                        if (zb) sx[e] += yv[e] - (int32_t)((n_zb >> (8 * e)) & 0xffu);
-                        if (zt) sx[e] += yv[e] - (int32_t)((n_zt >> (8 * e)) & 0xffu);
+                        yv[e] = (int32_t)((y4[j] >> (8 * e)) & 0xffu);
+                        const int32_t by = (int32_t)((ny[j] >> (8 * e)) & 0xffu);
+                        const int32_t bz = (int32_t)((nz[j] >> (8 * e)) & 0xffu);
+                        sx[e] = ((yb || yt) ? yv[e] - by : 0) + ((zb || zt) ? yv[e] - bz : 0);
                     }
+                    if (yb && yt) {   // 1-row block with neighbours on both sides
+                        const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + y) * W + gb.lo_c + x0;
+                        const uint32_t o = *reinterpret_cast<const uint32_t *>(y_cur + G + W);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) sx[e] += yv[e] - (int32_t)((o >> (8 * e)) & 0xffu);
+                    }
+                    if (zb && zt) {
+                        const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + y) * W + gb.lo_c + x0;
+                        const uint32_t o = *reinterpret_cast<const uint32_t *>(y_cur + G + HW);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) sx[e] += yv[e] - (int32_t)((o >> (8 * e)) & 0xffu);
+                    }
+                    if (x0 == 0 && lf_c) sx[0] += yv[0] - (int32_t)(nx[j] & 0xffu);
+                    if (x0 + 4 == gb.wc && rt_c) sx[3] += yv[3] - (int32_t)((nx[j] >> 8) & 0xffu);
                     const int32_t uu[4] = {u4[j].x, u4[j].y, u4[j].z, u4[j].w};
                     const uint32_t aw[2] = {a4[j].x, a4[j].y};
 #pragma unroll
@@ -216,24 +328,34 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
                 *reinterpret_cast<uint2 *>(G2 + (v0 >> 1)) = gw;
             }
         }
+        if (tl) L.timeline[8 * k + 5] = gtimer();
         if (L.warm) {
             mbar_wait(bar, 0);
+            if (tl) L.timeline[8 * k + 6] = gtimer();
+            // excess += sum over arcs of (r - cap); one nibble word per plane
+            // and direction covers the quad
 #pragma unroll 2
             for (int p = 0; p < 8; ++p) {
                 const int row = p * 128 + (tid >> 3), z = row >> 5, y = row & 31;
                 const int v0 = z * PLANE + y * B + x0;
                 if (!(z < gb.dz && y < gb.hr && x0 < gb.wc)) continue;
+                const uint32_t wE = FE[v0 >> 3] >> xs;
+                const uint32_t wS = FS[v0 >> 3] >> xs;
+                const uint32_t wD = FD[v0 >> 3] >> xs;
+                const uint32_t wW = x0 > 0 ? FE[(v0 - 1) >> 3] >> (((v0 - 1) & 7) * 4) : 0u;
+                const uint32_t wN = y > 0 ? FS[(v0 - B) >> 3] >> xs : 0u;
+                const uint32_t wU = z > 0 ? FD[(v0 - PLANE) >> 3] >> xs : 0u;
                 int32_t f[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const int v = v0 + e, x = x0 + e;
+                    const int x = x0 + e;
                     int32_t t = 0;
-                    if (x + 1 < gb.wc) t += s3_nib(FE, v) - cap;
-                    if (x > 0) t += cap - s3_nib(FE, v - 1);
-                    if (y + 1 < gb.hr) t += s3_nib(FS, v) - cap;
-                    if (y > 0) t += cap - s3_nib(FS, v - B);
-                    if (z + 1 < gb.dz) t += s3_nib(FD, v) - cap;
-                    if (z > 0) t += cap - s3_nib(FD, v - PLANE);
+                    if (x + 1 < gb.wc) t += (int32_t)((wE >> (4 * e)) & 0xfu) - cap;
+                    if (x > 0) t += cap - (int32_t)((e == 0 ? wW : (wE >> (4 * (e - 1)))) & 0xfu);
+                    if (y + 1 < gb.hr) t += (int32_t)((wS >> (4 * e)) & 0xfu) - cap;
+                    if (y > 0) t += cap - (int32_t)((wN >> (4 * e)) & 0xfu);
+                    if (z + 1 < gb.dz) t += (int32_t)((wD >> (4 * e)) & 0xfu) - cap;
+                    if (z > 0) t += cap - (int32_t)((wU >> (4 * e)) & 0xfu);
                     f[e] = t;
                 }
                 uint2 gw = *reinterpret_cast<const uint2 *>(G2 + (v0 >> 1));
@@ -349,6 +471,7 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
     uint32_t R = 0;
     for (;;) {
         // ---- sink / active rows and initial heights (node-parallel) ----
+        uint32_t ra = 0;
 #pragma unroll 4
         for (int z = 0; z < B; ++z) {
             const int v = z * PLANE + tid;
@@ -356,10 +479,15 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
             const uint32_t bK = __ballot_sync(FULLMASK, gv < 0);
             const uint32_t bA = __ballot_sync(FULLMASK, gv > 0);
             h[v] = gv < 0 ? 0 : HINF;
+            ra |= (bA != 0u ? 1u : 0u) << z;
             if (lane == 0) {
                 Kb[z * B + warp] = bK;
                 Kb[1024 + z * B + warp] = bA;
             }
+        }
+        if (lane == 0) {
+            Fp[warp] = ra;
+            Fr[warp] = 0;
         }
         if (tid == 0) { misc[0] = 0; misc[1] = 0; misc[2] = 0; }
         __syncthreads();
@@ -421,10 +549,7 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
         if (tl) {
             const int64_t t1 = gtimer();
             t_bfs += t1 - t0;
-            if (rounds == 0) {
-                L.timeline[8 * k + 5] = t1;
-                L.timeline[8 * k + 6] = level;
-            }
+
         }
         if (!hit) break;
         if (++rounds > T.max_rounds) {
@@ -435,58 +560,47 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
         const int cap_sweeps = T.sweep_min + T.sweep_mul * level;
         for (int sw = 0; sw < cap_sweeps; ++sw) {
             ++sweeps_done;
-#pragma unroll 2
-            for (int z = 0; z < B; ++z) {
+            // push: each warp scans its rows (z, warp) and packs the active
+            // nodes into batches of 32, so a lane works on an active node
+            // instead of idling behind one (the active set is sparse after
+            // the first sweeps)
+            int cnt = 0;
+            uint32_t rows = Fp[warp];
+            __syncwarp();
+            if (lane == 0) Fp[warp] = 0;
+            while (rows) {
+                const int z = __ffs(rows) - 1;
+                rows &= rows - 1;
                 const int v = z * PLANE + tid;
-                const int32_t e = s3_getg(G2, v);
-                if (e <= 0) continue;
                 const uint16_t hv = h[v];
-                if (hv == HINF || hv == 0) continue;
-                const uint16_t ht = hv - 1;
-                int32_t left = e;
-#pragma unroll
-                for (int d = 0; d < 6; ++d) {
-                    int32_t r;
-                    int w;
-                    if (d == 0) { r = s3_nib(FE, v); w = v + 1; }
-                    else if (d == 1) { if (lane == 0) continue; r = cap2 - s3_nib(FE, v - 1); w = v - 1; }
-                    else if (d == 2) { r = s3_nib(FS, v); w = v + B; }
-                    else if (d == 3) { if (warp == 0) continue; r = cap2 - s3_nib(FS, v - B); w = v - B; }
-                    else if (d == 4) { r = s3_nib(FD, v); w = v + PLANE; }
-                    else { if (z == 0) continue; r = cap2 - s3_nib(FD, v - PLANE); w = v - PLANE; }
-                    if (r == 0) continue;
-                    if (h[w] != ht) continue;
-                    const int32_t delta = left < r ? left : r;
-                    if (d == 0) s3_addnib(FE, v, -delta);
-                    else if (d == 1) s3_addnib(FE, w, delta);
-                    else if (d == 2) s3_addnib(FS, v, -delta);
-                    else if (d == 3) s3_addnib(FS, w, delta);
-                    else if (d == 4) s3_addnib(FD, v, -delta);
-                    else s3_addnib(FD, w, delta);
-                    s3_addg(G2, w, delta);
-                    left -= delta;
-                    if (left == 0) break;
-                }
-                if (left != e) s3_addg(G2, v, -(e - left));
+                const bool p = s3_getg(G2, v) > 0 && hv != HINF && hv != 0;
+                cnt = s3_enqueue(slots, __ballot_sync(FULLMASK, p), cnt, lane, v,
+                                 [&](int u) { s3_push(G2, h, FE, FS, FD, Fr, u, cap2); });
+            }
+            if (cnt) {
+                __syncwarp();
+                if (lane < cnt) s3_push(G2, h, FE, FS, FD, Fr, slots[lane], cap2);
+                __syncwarp();
             }
             __syncthreads();
+            // relabel every node that still holds excess
             int act = 0;
-#pragma unroll 2
-            for (int z = 0; z < B; ++z) {
+            cnt = 0;
+            rows = Fr[warp];
+            __syncwarp();
+            if (lane == 0) Fr[warp] = 0;
+            while (rows) {
+                const int z = __ffs(rows) - 1;
+                rows &= rows - 1;
                 const int v = z * PLANE + tid;
-                if (s3_getg(G2, v) <= 0) continue;
-                const uint16_t hv = h[v];
-                if (hv == HINF) continue;
-                uint32_t mn = HINF;
-                if (s3_nib(FE, v)) mn = min(mn, (uint32_t)h[v + 1]);
-                if (lane > 0 && s3_nib(FE, v - 1) != cap2) mn = min(mn, (uint32_t)h[v - 1]);
-                if (s3_nib(FS, v)) mn = min(mn, (uint32_t)h[v + B]);
-                if (warp > 0 && s3_nib(FS, v - B) != cap2) mn = min(mn, (uint32_t)h[v - B]);
-                if (s3_nib(FD, v)) mn = min(mn, (uint32_t)h[v + PLANE]);
-                if (z > 0 && s3_nib(FD, v - PLANE) != cap2) mn = min(mn, (uint32_t)h[v - PLANE]);
-                const uint32_t nh = (mn + 1 >= (uint32_t)M) ? HINF : mn + 1;
-                if (nh != hv) h[v] = (uint16_t)nh;
-                act |= (nh != HINF);
+                const bool p = s3_getg(G2, v) > 0 && h[v] != HINF;
+                cnt = s3_enqueue(slots, __ballot_sync(FULLMASK, p), cnt, lane, v,
+                                 [&](int u) { act |= s3_relabel(h, FE, FS, FD, Fp, u, cap2); });
+            }
+            if (cnt) {
+                __syncwarp();
+                if (lane < cnt) act |= s3_relabel(h, FE, FS, FD, Fp, slots[lane], cap2);
+                __syncwarp();
             }
             if (!__syncthreads_or(act)) break;
         }
