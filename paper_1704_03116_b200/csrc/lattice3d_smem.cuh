@@ -328,10 +328,8 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
                 *reinterpret_cast<uint2 *>(G2 + (v0 >> 1)) = gw;
             }
         }
-        if (tl) L.timeline[8 * k + 5] = gtimer();
         if (L.warm) {
             mbar_wait(bar, 0);
-            if (tl) L.timeline[8 * k + 6] = gtimer();
             // excess += sum over arcs of (r - cap); one nibble word per plane
             // and direction covers the quad
 #pragma unroll 2
@@ -549,7 +547,10 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
         if (tl) {
             const int64_t t1 = gtimer();
             t_bfs += t1 - t0;
-
+            if (rounds == 0) {
+                L.timeline[8 * k + 5] = t1;
+                L.timeline[8 * k + 6] = level;
+            }
         }
         if (!hit) break;
         if (++rounds > T.max_rounds) {
