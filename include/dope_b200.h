@@ -114,9 +114,12 @@ typedef struct dope_lattice {
                                    current, best, and the next output         */
     uint8_t *yhat;              /* n   block labels (global layout)           */
     uint8_t *resid;             /* K * resid_stride bytes: residual graphs    */
-    uint32_t *dirty;            /* 2K: [0, K) block needs a re-solve (init 1);
-                                   [K, 2K) iteration + 1 of the block's last
-                                   solve (init 0)                              */
+    uint32_t *dirty;            /* 2K (3D: 6K): [0, K) block needs a re-solve
+                                   (init 1); [K, 2K) iteration + 1 of the
+                                   block's last solve; 3D only: [2K, 5K) pass
+                                   + 1 at which y buffer b last received block
+                                   k's iterate, [5K, 6K) pass + 1 of the last
+                                   change of block k's iterate                  */
     int64_t *part_energy;       /* K   per-block pair-energy partials          */
     int64_t *part_unary;        /* K   per-block change of sum u*y2           */
     int64_t *part_ressq;        /* K   per-block sum (yhat - y)^2             */

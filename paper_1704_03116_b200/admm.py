@@ -295,8 +295,9 @@ class _DeviceState:
         self.yhat = self.yhat_full[g:g + n]
         self.agg = torch.zeros(4, dtype=torch.int64, device=dev)
         self.resid = torch.zeros(K * stride, dtype=u8, device=dev)
-        # [0, K): re-solve flags; [K, 2K): iteration + 1 of each block's last solve
-        self.dirty = torch.zeros(2 * K, dtype=torch.int32, device=dev)
+        # [0, K): re-solve flags; [K, 2K): iteration + 1 of each block's last solve;
+        # 3D also [2K, 6K): y-buffer stamps of the clean-block consensus pass
+        self.dirty = torch.zeros((6 if len(low.dims) == 3 else 2) * K, dtype=torch.int32, device=dev)
         self.dirty[:K] = 1
         sstride = int(lb.dope_scratch_stride(C.byref(L)))
         self.scratch = torch.empty(max(K * sstride, 16), dtype=u8, device=dev)
@@ -430,7 +431,10 @@ class AdmmState:
         else:
             self._dev.y2_current().copy_(torch.as_tensor((2 * v).astype(np.uint8)))
             self._dev.reset_unary()
-        self._dev.dirty[:self._dev.problems.lowering.K].fill_(1)
+        K = self._dev.problems.lowering.K
+        self._dev.dirty[:K].fill_(1)
+        if self._dev.dirty.numel() > 2 * K:   # y buffers rewritten: no stamp holds
+            self._dev.dirty[2 * K:].zero_()
 
     def _global_to_blocks(self, vec: np.ndarray, dtype) -> list:
         out = []

@@ -504,6 +504,9 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
             L.yhat[(int64_t)L.ay.dim * L.W + c] = 0;
         }
     }
+    if (L.ndim == 3)   // solve epochs and the y-buffer stamps of the clean-block pass
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 5 * (int64_t)L.K; i += stride)
+            L.dirty[L.K + i] = 0u;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.K; i += stride) {
         L.dirty[i] = 1u;
         L.pe[i] = 0;
@@ -1473,6 +1476,13 @@ static int launch_k2(const Lat2 &o, cudaStream_t s) {
         int lq = -1;
         for (int l = 0; l <= 5; ++l)
             if (o.ax.base == (4 << l)) lq = l;
+        if (!getenv("DOPE_NO_VEC3") && !getenv("DOPE_NO_PLANE3") && lq == 3 && o.ax.rem == 0 &&
+            o.ay.base == 32 && o.ay.rem == 0 && o.W % 4 == 0 && al % 8 == 0) {
+            const int sms = sm_count();
+            return cuda_check(launch_pdl(k_consensus3d_plane, dim3(o.K < 4 * sms ? o.K : 4 * sms), dim3(256), 0, s,
+                                         o),
+                              "launch K2-3D (plane)");
+        }
         if (!getenv("DOPE_NO_VEC3") && lq >= 0 && o.ax.rem == 0 && o.W % 4 == 0 && al % 4 == 0) {
             const int sms = sm_count();
             const int v3 = getenv("DOPE_VEC3_NT") ? atoi(getenv("DOPE_VEC3_NT")) : 256;

@@ -226,7 +226,10 @@ __global__ void __launch_bounds__(NT) k_block_mincut3d(Lat2 L, K1Tune T) {
     if (L.st->stop) return;
     if (L.skip_clean && L.dirty[k] == 0) return;
     __syncthreads();
-    if (threadIdx.x == 0) L.dirty[k] = 0;
+    if (threadIdx.x == 0) {
+        L.dirty[k] = 0;
+        L.dirty[L.K + k] = (uint32_t)L.st->iteration + 1u;   // solve epoch
+    }
     mincut3d_l2<BD, BH, BW, NT>(L, T, k, smem3);
 }
 
@@ -243,6 +246,12 @@ __global__ void k_init_resid3d(Lat2 L, int boxd, int boxh, int boxw) {
         for (int d = 0; d < 6; ++d) gres[d * M + v] = (valid && has[d]) ? (uint8_t)L.cap : 0;
     }
 }
+
+// y-buffer stamps of the 3D clean-block pass (dirty[2K, 6K), zeroed by
+// init_state): [2K + b*K + k] = pass + 1 at which buffer b last received
+// block k's iterate, [5K + k] = pass + 1 of the last pass that changed it.
+__device__ __forceinline__ uint32_t *ybuf_stamp(const Lat2 &L, int b) { return L.dirty + (size_t)(2 + b) * L.K; }
+__device__ __forceinline__ uint32_t *ychg_stamp(const Lat2 &L) { return L.dirty + (size_t)5 * L.K; }
 
 // Consensus for 3D (scalar, one CTA per sub-region).  Same semantics as
 // k_consensus: y_t into the free buffer, multipliers, residual partials,
@@ -302,6 +311,7 @@ __global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
         const bool ychg = (2 * y != y2old);
         if (ychg || yh != y) marks |= 1u;
         if (ychg) {
+            marks |= 256u;
             du += (int64_t)L.u[G] * (2 * y - y2old);
             if (c == 0 && lf_c) marks |= 2u;
             if (c == gb.wc - 1 && rt_c) marks |= 4u;
@@ -336,6 +346,8 @@ __global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
         if (Fm & 16u) L.dirty[k + KX] = 1u;
         if (Fm & 32u) L.dirty[k - KYX] = 1u;
         if (Fm & 64u) L.dirty[k + KYX] = 1u;
+        ybuf_stamp(L, out)[k] = (uint32_t)L.st->iteration + 1u;
+        if (Fm & 256u) ychg_stamp(L)[k] = (uint32_t)L.st->iteration + 1u;
         CtaAgg agg;
         agg.add_block(E, U, S, (Fm & 128u) ? 1 : 0);
         pass_tail(L, agg, cur, best, out);
@@ -363,7 +375,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_consensus3d_vec(Lat2 L, int l
     ystore_t *__restrict__ y_out = L.y2[out];
     const astore_t *a_in = L.a;
     astore_t *a_out = L.fuse ? L.a : nullptr;
-    const bool want_e = L.fuse && L.st->iteration >= 1;
+    const int it = L.st->iteration;
+    const bool want_e = L.fuse && it >= 1;
+    // clean-block pass: needs the multipliers updated here, re-solves skipped
+    // for unchanged blocks, and energy partials from an earlier pass (it >= 2)
+    const bool clean_ok = L.fuse && L.skip_clean && it >= 2;
+    const uint32_t ep = (uint32_t)it + 1u;
     const int32_t W = L.W, H = L.ay.dim, D = L.az.dim, q = L.q;
     const int64_t HW = (int64_t)H * W;
     const int QR = 1 << lq;
@@ -376,6 +393,40 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_consensus3d_vec(Lat2 L, int l
         const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
         const bool lf_c = gb.lo_c > 0, rt_c = gb.lo_c + gb.wc < W;
         const int nq = (gb.dz * gb.hr) << lq;
+        if (clean_ok) {
+            // Fixed point: a block K1 did not re-solve had yhat == y and no y
+            // change in the previous pass (else it would be dirty); with none
+            // of its 6 neighbours re-solved either, every voxel's pre-clamp
+            // value repeats: y, a, clamp status, residual 0, and the pair
+            // energy of y_{t-1} equals the stored partial.  Only the output
+            // buffer may need the block's iterate.
+            const int KX = L.ax.k, KYX = L.ay.k * L.ax.k;
+            const uint32_t *epo = L.dirty + L.K;
+            bool fast = epo[k] != ep;
+            fast = fast && !(lf_c && epo[k - 1] == ep) && !(rt_c && epo[k + 1] == ep);
+            fast = fast && !(up_r && epo[k - KX] == ep) && !(dn_r && epo[k + KX] == ep);
+            fast = fast && !(up_z && epo[k - KYX] == ep) && !(dn_z && epo[k + KYX] == ep);
+            if (fast) {
+                const uint32_t st_out = ybuf_stamp(L, out)[k];
+                if (st_out == 0u || st_out < ychg_stamp(L)[k]) {
+                    for (int t = tid; t < nq; t += NT) {
+                        const int row = t >> lq, c0 = (t & (QR - 1)) << 2;
+                        const int z = row / gb.hr, r = row - z * gb.hr;
+                        const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + r) * W + gb.lo_c + c0;
+                        __stcg(reinterpret_cast<unsigned int *>(y_out + G),
+                               __ldcg(reinterpret_cast<const unsigned int *>(y_in + G)));
+                    }
+                }
+                __syncthreads();   // every thread has read the stamps
+                if (tid == 0) {
+                    ybuf_stamp(L, out)[k] = ep;
+                    L.pu[k] = 0;
+                    L.pr[k] = 0;
+                    agg.add_block(L.pe[k], 0, 0, L.pf[k]);
+                }
+                continue;
+            }
+        }
         int64_t e_acc = 0, du = 0;
         int ss = 0;
         unsigned marks = 0, clamp_or = 0;   // marks: bit0 self, 1..6 -x +x -y +y -z +z
@@ -452,6 +503,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_consensus3d_vec(Lat2 L, int l
                 const uint32_t yb4 = (uint32_t)(y[0] | (y[1] << 1) | (y[2] << 2) | (y[3] << 3));
                 if (chg | (hb ^ yb4)) marks |= 1u;
                 if (chg) {
+                    marks |= 256u;
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const int dy = (int)((yw >> (8 * i)) & 0xFFu) - (int)((yo[j] >> (8 * i)) & 0xFFu);
@@ -489,6 +541,204 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_consensus3d_vec(Lat2 L, int l
             if (Fm & 16u) L.dirty[k + KX] = 1u;
             if (Fm & 32u) L.dirty[k - KYX] = 1u;
             if (Fm & 64u) L.dirty[k + KYX] = 1u;
+            ybuf_stamp(L, out)[k] = (uint32_t)it + 1u;
+            if (Fm & 256u) ychg_stamp(L)[k] = (uint32_t)it + 1u;
+            agg.add_block(E, U, S, (Fm & 128u) ? 1 : 0);
+        }
+        __syncthreads();
+    }
+    if (tid == 0) pass_tail(L, agg, cur, best, out);
+}
+
+// 3D consensus for blocks whose (y, x) face is 32 x 32 (C4's 32^3 tiling):
+// thread t owns the quad (r = t / 8, c0 = 4 * (t % 8)) of every z-plane of
+// the block, so the per-quad geometry is fixed and planes are visited in
+// batches of ZB (all loads of a batch issued first).  The pair energy of
+// y_{t-1} takes the +x partner from the next lane, the +y partner from the
+// lane 8 up (rows r % 4 != 3) and the +z partner from the same thread's next
+// plane, reading memory only across warps / blocks.  Same arithmetic, marks,
+// stamps and clean-block pass as k_consensus3d_vec.
+#ifndef K2P_ZB
+#define K2P_ZB 4
+#endif
+#ifndef K2P_MINB
+#define K2P_MINB 4
+#endif
+__global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
+    constexpr int NT = 256, ZB = K2P_ZB;
+    if (L.pdl) {
+        griddep_wait();
+        griddep_launch();
+    }
+    if (L.st->stop) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r = tid >> 3, c0 = (tid & 7) << 2;
+    CtaAgg agg;
+    const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
+    const ystore_t *__restrict__ y_in = L.y2[cur];
+    ystore_t *__restrict__ y_out = L.y2[out];
+    const astore_t *a_in = L.a;
+    astore_t *a_out = L.fuse ? L.a : nullptr;
+    const int it = L.st->iteration;
+    const bool want_e = L.fuse && it >= 1;
+    const bool clean_ok = L.fuse && L.skip_clean && it >= 2;
+    const uint32_t ep = (uint32_t)it + 1u;
+    const int32_t W = L.W, H = L.ay.dim, D = L.az.dim, q = L.q;
+    const int64_t HW = (int64_t)H * W;
+    __shared__ int64_t red_e[NT / 32], red_s[NT / 32], red_u[NT / 32];
+    __shared__ unsigned red_f[NT / 32];
+    for (int k = blockIdx.x; k < L.K; k += gridDim.x) {
+        int bz, by, bx;
+        const Geo3 gb = block_geo3(L, k, bz, by, bx);
+        const bool up_z = gb.lo_z > 0, dn_z = gb.lo_z + gb.dz < D;
+        const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
+        const bool lf_c = gb.lo_c > 0, rt_c = gb.lo_c + gb.wc < W;
+        const int64_t G0 = ((int64_t)gb.lo_z * H + gb.lo_r + r) * W + gb.lo_c + c0;
+        if (clean_ok) {   // clean-block pass (k_consensus3d_vec)
+            const int KX = L.ax.k, KYX = L.ay.k * L.ax.k;
+            const uint32_t *epo = L.dirty + L.K;
+            bool fast = epo[k] != ep;
+            fast = fast && !(lf_c && epo[k - 1] == ep) && !(rt_c && epo[k + 1] == ep);
+            fast = fast && !(up_r && epo[k - KX] == ep) && !(dn_r && epo[k + KX] == ep);
+            fast = fast && !(up_z && epo[k - KYX] == ep) && !(dn_z && epo[k + KYX] == ep);
+            if (fast) {
+                const uint32_t st_out = ybuf_stamp(L, out)[k];
+                if (st_out == 0u || st_out < ychg_stamp(L)[k]) {
+                    for (int z0 = 0; z0 < gb.dz; z0 += 8) {   // 8 planes of loads in flight
+                        uint32_t v[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            v[j] = z0 + j < gb.dz ? *reinterpret_cast<const unsigned int *>(y_in + G0 + (z0 + j) * HW) : 0u;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            if (z0 + j < gb.dz) *reinterpret_cast<unsigned int *>(y_out + G0 + (z0 + j) * HW) = v[j];
+                    }
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    ybuf_stamp(L, out)[k] = ep;
+                    L.pu[k] = 0;
+                    L.pr[k] = 0;
+                    agg.add_block(L.pe[k], 0, 0, L.pf[k]);
+                }
+                continue;
+            }
+        }
+        const bool top = r == 0 && up_r, bot = r == 31 && dn_r;
+        const bool lft = c0 == 0 && lf_c, rgt = c0 == 28 && rt_c;
+        const bool ydn = gb.lo_r + r + 1 < H;             // the +y partner exists
+        const bool yld = ydn && (lane >> 3) == 3;          // ... and sits in another warp / block
+        const bool xnx = gb.lo_c + c0 + 4 < W;             // the +x partner of the quad's last voxel
+        int64_t e_acc = 0, du = 0;
+        int ss = 0;
+        unsigned marks = 0, clamp_or = 0;
+        for (int z0 = 0; z0 < gb.dz; z0 += ZB) {
+            const int zl = min(z0 + ZB, gb.dz) - 1;        // last plane of the batch
+            uint32_t yh4[ZB], yo[ZB], nb[ZB], cnt[ZB], yb[ZB];
+            uint2 av[ZB];
+            int yr[ZB];
+            uint32_t yz = 0;
+#pragma unroll
+            for (int j = 0; j < ZB; ++j) {
+                const int z = z0 + j;
+                yh4[j] = yo[j] = nb[j] = cnt[j] = yb[j] = 0;
+                av[j] = make_uint2(0, 0);
+                yr[j] = 0;
+                if (z <= zl) {
+                    const int64_t G = G0 + z * HW;
+                    yh4[j] = __ldcs(reinterpret_cast<const unsigned int *>(L.yhat + G));
+                    av[j] = __ldcs(reinterpret_cast<const uint2 *>(a_in + G));
+                    yo[j] = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G));
+                    if (want_e) {
+                        if (yld) yb[j] = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G + W));
+                        if (c0 == 28 && xnx) yr[j] = y_in[G + 4];
+                        if (z == zl && gb.lo_z + z + 1 < D)
+                            yz = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G + HW));
+                    }
+                    if (top) { cnt[j] += 0x01010101u; nb[j] += *reinterpret_cast<const uint32_t *>(L.yhat + G - W); }
+                    if (bot) { cnt[j] += 0x01010101u; nb[j] += *reinterpret_cast<const uint32_t *>(L.yhat + G + W); }
+                    if (z == 0 && up_z) { cnt[j] += 0x01010101u; nb[j] += *reinterpret_cast<const uint32_t *>(L.yhat + G - HW); }
+                    if (z == gb.dz - 1 && dn_z) { cnt[j] += 0x01010101u; nb[j] += *reinterpret_cast<const uint32_t *>(L.yhat + G + HW); }
+                    if (lft) { cnt[j] += 1u; nb[j] += L.yhat[G - 1]; }
+                    if (rgt) { cnt[j] += 1u << 24; nb[j] += (uint32_t)L.yhat[G + 4] << 24; }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < ZB; ++j) {
+                const int z = z0 + j;
+                const uint32_t nxt = __shfl_down_sync(FULLMASK, yo[j], 1);
+                const uint32_t dnv = __shfl_down_sync(FULLMASK, yo[j], 8);
+                if (z > zl) continue;   // uniform over the CTA
+                const int64_t G = G0 + z * HW;
+                if (want_e) {
+                    const uint32_t rw = c0 < 28 ? nxt : (xnx ? (uint32_t)yr[j] : (yo[j] >> 24));
+                    int qd = __popc(yo[j] ^ __funnelshift_r(yo[j], rw, 8));
+                    if (ydn) qd += __popc(yo[j] ^ (yld ? yb[j] : dnv));
+                    if (gb.lo_z + z + 1 < D) qd += __popc(yo[j] ^ (z < zl ? yo[j + 1 < ZB ? j + 1 : j] : yz));
+                    e_acc += (int64_t)L.lamw * qd;
+                }
+                const uint32_t h4 = yh4[j];
+                const uint32_t sb = ((cnt[j] & (h4 * 0xFFu)) | 0x04040404u) - nb[j];
+                int a4[4];
+                unpack_a4(av[j], a4);
+                int y[4], an[4];
+                uint32_t yw = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int h = (int)((h4 >> (8 * i)) & 0xFFu);
+                    const int p = a4[i] + h + 4 * q - q * (int)((sb >> (8 * i)) & 0xFFu);
+                    clamp_or |= (uint32_t)p;
+                    y[i] = p > 0 ? 1 : 0;
+                    an[i] = a4[i] + h - y[i];
+                    ss += h ^ y[i];
+                    yw |= (uint32_t)(2 * y[i]) << (8 * i);
+                }
+                if (a_out) __stcs(reinterpret_cast<uint2 *>(a_out + G), pack_a4(an[0], an[1], an[2], an[3]));
+                __stcg(reinterpret_cast<unsigned int *>(y_out + G), yw);
+                const uint32_t chg = yw ^ yo[j];
+                const uint32_t hb = ((h4 * 0x01020408u) >> 24) & 0xFu;
+                const uint32_t yb4 = (uint32_t)(y[0] | (y[1] << 1) | (y[2] << 2) | (y[3] << 3));
+                if (chg | (hb ^ yb4)) marks |= 1u;
+                if (chg) {
+                    marks |= 256u;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int dy = (int)((yw >> (8 * i)) & 0xFFu) - (int)((yo[j] >> (8 * i)) & 0xFFu);
+                        if (dy) du += (int64_t)__ldg(L.u + G + i) * dy;
+                    }
+                    if (lft && (chg & 0xFFu)) marks |= 2u;
+                    if (rgt && (chg >> 24)) marks |= 4u;
+                    if (top) marks |= 8u;
+                    if (bot) marks |= 16u;
+                    if (z == 0 && up_z) marks |= 32u;
+                    if (z == gb.dz - 1 && dn_z) marks |= 64u;
+                }
+            }
+        }
+        e_acc = warp_sum(e_acc);
+        du = warp_sum(du);
+        const int sq = (int)__reduce_add_sync(FULLMASK, (unsigned)ss);
+        const unsigned fm = __reduce_or_sync(FULLMASK, marks | (clamp_or > 1u ? 128u : 0u));
+        if (lane == 0) { red_e[warp] = e_acc; red_s[warp] = sq; red_u[warp] = du; red_f[warp] = fm; }
+        __syncthreads();
+        if (tid == 0) {
+            int64_t E = 0, S = 0, U = 0;
+            unsigned Fm = 0;
+            for (int w = 0; w < NT / 32; ++w) { E += red_e[w]; S += red_s[w]; U += red_u[w]; Fm |= red_f[w]; }
+            L.pe[k] = E;
+            L.pu[k] = U;
+            L.pr[k] = S;
+            L.pf[k] = (Fm & 128u) ? 1 : 0;
+            const int KX = L.ax.k, KYX = L.ay.k * L.ax.k;
+            if (Fm & 1u) L.dirty[k] = 1u;
+            if (Fm & 2u) L.dirty[k - 1] = 1u;
+            if (Fm & 4u) L.dirty[k + 1] = 1u;
+            if (Fm & 8u) L.dirty[k - KX] = 1u;
+            if (Fm & 16u) L.dirty[k + KX] = 1u;
+            if (Fm & 32u) L.dirty[k - KYX] = 1u;
+            if (Fm & 64u) L.dirty[k + KYX] = 1u;
+            ybuf_stamp(L, out)[k] = ep;
+            if (Fm & 256u) ychg_stamp(L)[k] = ep;
             agg.add_block(E, U, S, (Fm & 128u) ? 1 : 0);
         }
         __syncthreads();

@@ -190,7 +190,10 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (tid == 0) L.dirty[k] = 0;
+    if (tid == 0) {
+        L.dirty[k] = 0;
+        L.dirty[L.K + k] = (uint32_t)L.st->iteration + 1u;   // solve epoch (clean-block K2 pass)
+    }
     // diagnostics (L.timeline): [0] start [1] end [2] rounds [3] sweeps
     // [4] prologue end [5] first relabel end [6] its levels [7] ns in relabels
     const bool tl = L.timeline && tid == 0;
