@@ -138,17 +138,20 @@ typedef struct dope_lattice {
                                    rounds, sweeps (diagnostics only)          */
     uint8_t *scratch;           /* 3D only: K * dope_scratch_stride bytes of
                                    per-sub-region node state (may be NULL in 2D) */
-    /* Sharding (2D): this lattice is a slab of whole block rows of a larger
-     * grid.  y2[i] and yhat must then point one row INTO allocations that
-     * carry a ghost row above and below (2D allocations always do). */
-    int32_t ghost_up;           /* a neighbour shard exists above              */
-    int32_t ghost_dn;           /* a neighbour shard exists below              */
+    /* Sharding: this lattice is a slab of whole block rows (2D) or whole
+     * block planes (3D, along the depth axis) of a larger grid.  y2[i] and
+     * yhat must then point one row (2D) / one plane (3D) INTO allocations
+     * that carry a ghost row / plane on each side (2D allocations always do;
+     * 3D ones only need them on a side whose ghost flag is set). */
+    int32_t ghost_up;           /* a neighbour shard exists above / before     */
+    int32_t ghost_dn;           /* a neighbour shard exists below / after      */
     int32_t sharded;            /* run-loop consensus publishes agg[] instead
                                    of deciding; call dope_decide after the
                                    cross-rank all-reduce                       */
     int64_t *agg;               /* 4: [E (sum), R2 as double bits (sum),
                                    max block residual^2 (max), clamped (max)] */
-    void *halo;                 /* sharded: 4 * W * 4 bytes of halo staging     */
+    void *halo;                 /* sharded: 16 * U bytes of halo staging, U = W
+                                   (2D) or dims[1] * dims[2] (3D)              */
 } dope_lattice;
 
 /* Library / ABI identification; "b200-sm100a". */
@@ -188,13 +191,15 @@ int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void 
 int dope_finish_run(const dope_lattice *L, void *stream);
 /* Sharded run loop: apply the all-reduced agg[] (trace, best, stop). */
 int dope_decide(const dope_lattice *L, void *stream);
-/* Sharded run loop: install neighbour boundary rows into the ghost rows;
- * which = 0: labels (uint8[W]), 1: current y2 (int32[W], marks dirty). */
+/* Sharded run loop: install the neighbour shards' boundary rows (2D) /
+ * planes (3D) into the ghost rows / planes; which = 0: labels (uint8[U]),
+ * 1: current y2 (uint8[U], marks the adjacent local blocks dirty where it
+ * changed). */
 int dope_ghost_update(const dope_lattice *L, int32_t which, const void *up_row,
                       const void *dn_row, void *stream);
-/* Sharded run loop: copy the first / last local row of the labels (which=0)
- * or of the current iterate y2 (which=1) into staging buffers (either may be
- * NULL) for the halo exchange (labels: W bytes; y2: W bytes). */
+/* Sharded run loop: copy the first / last local row (2D) / plane (3D) of the
+ * labels (which=0) or of the current iterate y2 (which=1) into staging
+ * buffers (either may be NULL) for the halo exchange (U bytes each). */
 int dope_pack_rows(const dope_lattice *L, int32_t which, void *first_row, void *last_row,
                    void *stream);
 /* dope_finish_run in two halves for sharded runs: the local energy of the
@@ -202,7 +207,8 @@ int dope_pack_rows(const dope_lattice *L, int32_t which, void *first_row, void *
  * the final decision. */
 int dope_energy_local(const dope_lattice *L, void *stream);
 int dope_finish_decide(const dope_lattice *L, void *stream);
-/* Multi-GPU (NCCL over NVLink / NVSwitch), one rank per GPU, 2D lattices.
+/* Multi-GPU (NCCL over NVLink / NVSwitch), one rank per GPU, 2D and 3D
+ * lattices (slabs of block rows / block planes).
  * dope_comm_unique_id on rank 0, broadcast the 128 bytes, dope_comm_init on
  * every rank.  dope_sharded_run runs `iters` iterations of the sharded loop
  * (K1, label halo, consensus, all-reduce of agg[], dope_decide, y halo) --

@@ -285,9 +285,9 @@ class _DeviceState:
         # multipliers fit int16 (|a| <= t + 1, max_iters is capped below 32000);
         # 2y in {0, 1, 2} is one byte
         self.a = torch.zeros(n, dtype=torch.int16, device=dev)   # updated in place
-        # 2D: y2 and yhat carry one ghost row above and below (neighbour shards;
-        # unused on a single GPU), the ABI points one row into the allocation
-        g = low.dims[-1] if len(low.dims) == 2 else 0
+        # y2 and yhat carry one ghost row (2D) / plane (3D) on each side (neighbour
+        # shards; unused on a single GPU), the ABI points one unit into the allocation
+        g = int(np.prod(low.dims[1:]))   # one ghost row (2D) / plane (3D) on each side
         self.ghost = g
         self.y2_full = [torch.ones(n + 2 * g, dtype=u8, device=dev) for _ in range(3)]
         self.y2 = [t[g:g + n] for t in self.y2_full]

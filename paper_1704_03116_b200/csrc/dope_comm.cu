@@ -81,8 +81,10 @@ static int nc(ncclResult_t r) { return r == ncclSuccess ? DOPE_OK : DOPE_E_CUDA;
 //   [0] send first row, [1] send last row, [2] recv from above, [3] recv from below
 static int exchange(const dope_lattice *L, const Comm &C, int which, cudaStream_t s) {
     Nccl &N = nccl();
-    const size_t W = (size_t)L->dims[1];
-    const size_t bytes = W;   // labels and y2 are both one byte per pixel
+    // the exchanged unit: a row (2D, slabs of block rows) or a plane (3D, slabs
+    // of block planes); labels and y2 are both one byte per pixel
+    const size_t W = L->ndim == 3 ? (size_t)L->dims[1] * L->dims[2] : (size_t)L->dims[1];
+    const size_t bytes = W;
     uint8_t *h = static_cast<uint8_t *>(L->halo);
     uint8_t *first = h, *last = h + 4 * W, *up = h + 8 * W, *dn = h + 12 * W;
     int rc = dope_pack_rows(L, which, first, last, s);

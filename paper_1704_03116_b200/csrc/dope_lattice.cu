@@ -73,7 +73,8 @@ struct Lat2 {
     int32_t vec4;           // all block columns start/end on 16-byte boundaries
     int32_t ndim;
     uint8_t *scratch;       // 3D: per-block node state (excess, heights)
-    int32_t gup, gdn;       // a ghost row (neighbour shard) exists above / below
+    int32_t gup, gdn;       // 2D: a ghost row (neighbour shard) exists above / below
+    int32_t gzu, gzd;       // 3D: a ghost plane (neighbour shard) exists before / after
     int32_t sharded;        // consensus writes local aggregates; dope_decide applies
     int64_t *agg;           // [E, R2 (double bits), max ss, clamped] of this shard
     int32_t pdl;            // launched with programmatic dependent launch (DOPE_PDL=1)
@@ -503,6 +504,18 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
             L.yhat[-L.W + c] = 0;
             L.yhat[(int64_t)L.ay.dim * L.W + c] = 0;
         }
+    } else if (L.gzu || L.gzd) {   // 3D shards: ghost planes
+        const int64_t HW = (int64_t)L.ay.dim * L.W, below = (int64_t)L.az.dim * HW;
+        for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < HW; c += stride) {
+            if (L.gzu) {
+                L.y2[0][-HW + c] = 1;
+                L.yhat[-HW + c] = 0;
+            }
+            if (L.gzd) {
+                L.y2[0][below + c] = 1;
+                L.yhat[below + c] = 0;
+            }
+        }
     }
     if (L.ndim == 3)   // solve epochs and the y-buffer stamps of the clean-block pass
         for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 5 * (int64_t)L.K; i += stride)
@@ -668,10 +681,11 @@ __global__ void k_decide(Lat2 L) {
 // Sharded mode: copy this shard's first and last local rows (labels or the
 // current iterate, both bytes) into caller staging buffers for the halo exchange.
 __global__ void k_pack_rows(Lat2 L, int which, void *first, void *last) {
-    const int32_t W = L.W;
-    const int64_t lastoff = (int64_t)(L.ay.dim - 1) * W;
+    // the exchanged unit: a row (2D, slabs of block rows) or a plane (3D, slabs of block planes)
+    const int64_t P = L.ndim == 3 ? (int64_t)L.ay.dim * L.W : (int64_t)L.W;
+    const int64_t lastoff = ((L.ndim == 3 ? (int64_t)L.az.dim : (int64_t)L.ay.dim) - 1) * P;
     const uint8_t *src = which == 0 ? L.yhat : L.y2[L.st->ycur];
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < W; c += gridDim.x * blockDim.x) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < P; c += (int64_t)gridDim.x * blockDim.x) {
         if (first) static_cast<uint8_t *>(first)[c] = src[c];
         if (last) static_cast<uint8_t *>(last)[c] = src[lastoff + c];
     }
@@ -682,6 +696,29 @@ __global__ void k_pack_rows(Lat2 L, int which, void *first, void *last) {
 // boundary block row dirty where the neighbour's y changed (it enters this
 // shard's block objectives, blockform.py:271).
 __global__ void k_ghost_update(Lat2 L, int which, const void *up_new, const void *dn_new) {
+    if (L.ndim == 3) {   // ghost planes; a changed ghost y marks the adjacent local block
+        const int64_t HW = (int64_t)L.ay.dim * L.W, below = (int64_t)L.az.dim * HW;
+        const uint8_t *up = static_cast<const uint8_t *>(up_new), *dn = static_cast<const uint8_t *>(dn_new);
+        for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < HW; c += (int64_t)gridDim.x * blockDim.x) {
+            if (which == 0) {
+                if (L.gzu && up) L.yhat[-HW + c] = up[c];
+                if (L.gzd && dn) L.yhat[below + c] = dn[c];
+            } else {
+                uint8_t *y = L.y2[L.st->ycur];
+                const int r = (int)(c / L.W), col = (int)(c - (int64_t)r * L.W);
+                const int kyx = L.ay.owner(r) * L.ax.k + L.ax.owner(col);
+                if (L.gzu && up && y[-HW + c] != up[c]) {
+                    L.dirty[kyx] = 1u;
+                    y[-HW + c] = up[c];
+                }
+                if (L.gzd && dn && y[below + c] != dn[c]) {
+                    L.dirty[(L.az.k - 1) * L.ay.k * L.ax.k + kyx] = 1u;
+                    y[below + c] = dn[c];
+                }
+            }
+        }
+        return;
+    }
     const int32_t W = L.W;
     const int64_t below = (int64_t)L.ay.dim * W;
     const uint8_t *up = static_cast<const uint8_t *>(up_new), *dn = static_cast<const uint8_t *>(dn_new);
@@ -1019,7 +1056,7 @@ __global__ void k_energy_current(Lat2 L, int64_t n) {
         int32_t qd = 0;
         if (c + 1 < L.W) qd += yi ^ (y2[i + 1] >> 1);
         if (r + 1 < L.ay.dim || L.gdn) qd += yi ^ (y2[i + L.W] >> 1);
-        if (z + 1 < L.az.dim) qd += yi ^ (y2[i + HW] >> 1);
+        if (z + 1 < L.az.dim || L.gzd) qd += yi ^ (y2[i + HW] >> 1);
         acc += (int64_t)L.lamw * qd;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) acc += L.st->unary2 / 2;
@@ -1043,7 +1080,7 @@ __global__ void k_energy_current_vec(Lat2 L, uint32_t nwords) {
         const uint32_t nx = c4 + 1 < W4 ? *reinterpret_cast<const uint32_t *>(y2 + G + 4) : (y >> 24);
         int qd = __popc(y ^ __funnelshift_r(y, nx, 8));
         if (r + 1 < H || L.gdn) qd += __popc(y ^ *reinterpret_cast<const uint32_t *>(y2 + G + L.W));
-        if (z + 1 < D) qd += __popc(y ^ *reinterpret_cast<const uint32_t *>(y2 + G + HW));
+        if (z + 1 < D || L.gzd) qd += __popc(y ^ *reinterpret_cast<const uint32_t *>(y2 + G + HW));
         acc += qd;
     }
     acc *= L.lamw;
@@ -1212,12 +1249,13 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
     o.tr_cl = L->trace_clamped;
     o.timeline = L->timeline;
     o.max_iters = L->max_iters;
-    o.gup = L->ghost_up;
-    o.gdn = L->ghost_dn;
+    o.gup = is3 ? 0 : L->ghost_up;
+    o.gdn = is3 ? 0 : L->ghost_dn;
+    o.gzu = is3 ? L->ghost_up : 0;
+    o.gzd = is3 ? L->ghost_dn : 0;
     o.sharded = L->sharded;
     o.agg = L->agg;
-    if (o.sharded && (!o.agg || is3 || o.ay.rem != 0)) return DOPE_E_ARGS;
-    if ((o.gup || o.gdn) && is3) return DOPE_E_GEOMETRY;
+    if (o.sharded && (!o.agg || (is3 ? o.az.rem != 0 : o.ay.rem != 0))) return DOPE_E_ARGS;
     const int maxd = o.az.base + (o.az.rem ? 1 : 0);
     const int maxh = o.ay.base + (o.ay.rem ? 1 : 0);
     const int maxw = o.ax.base + (o.ax.rem ? 1 : 0);
@@ -1717,7 +1755,8 @@ int dope_ghost_update(const dope_lattice *L, int32_t which, const void *up_row, 
     int rc = build_plan(L, P);
     if (rc) return rc;
     if (which != 0 && which != 1) return DOPE_E_ARGS;
-    k_ghost_update<<<(P.o.W + 255) / 256, 256, 0, (cudaStream_t)stream>>>(P.o, which, up_row, dn_row);
+    const int64_t unit = P.o.ndim == 3 ? (int64_t)P.o.ay.dim * P.o.W : (int64_t)P.o.W;
+    k_ghost_update<<<grid_for(unit), 256, 0, (cudaStream_t)stream>>>(P.o, which, up_row, dn_row);
     return cuda_check(cudaGetLastError(), "ghost_update");
 }
 
@@ -1727,7 +1766,8 @@ int dope_pack_rows(const dope_lattice *L, int32_t which, void *first_row, void *
     int rc = build_plan(L, P);
     if (rc) return rc;
     if (which != 0 && which != 1) return DOPE_E_ARGS;
-    k_pack_rows<<<(P.o.W + 255) / 256, 256, 0, (cudaStream_t)stream>>>(P.o, which, first_row, last_row);
+    const int64_t unit = P.o.ndim == 3 ? (int64_t)P.o.ay.dim * P.o.W : (int64_t)P.o.W;
+    k_pack_rows<<<grid_for(unit), 256, 0, (cudaStream_t)stream>>>(P.o, which, first_row, last_row);
     return cuda_check(cudaGetLastError(), "pack_rows");
 }
 

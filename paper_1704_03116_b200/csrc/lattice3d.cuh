@@ -63,7 +63,7 @@ __device__ __forceinline__ void mincut3d_l2(const Lat2 &L, const K1Tune &T, int 
     int32_t *g = reinterpret_cast<int32_t *>(L.scratch + (size_t)k * 6 * M);
     uint16_t *h = reinterpret_cast<uint16_t *>(g + M);
     uint8_t *rr = L.resid + (size_t)k * 6 * M;
-    const bool up_z = gb.lo_z > 0, dn_z = gb.lo_z + gb.dz < D;
+    const bool up_z = gb.lo_z > 0 || L.gzu, dn_z = gb.lo_z + gb.dz < D || L.gzd;   // ghost planes: shards
     const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
     const bool lf_c = gb.lo_c > 0, rt_c = gb.lo_c + gb.wc < W;
 
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
     const astore_t *a_in = L.a;
     astore_t *a_out = L.fuse ? L.a : nullptr;
     const bool want_e = L.fuse && L.st->iteration >= 1;
-    const bool up_z = gb.lo_z > 0, dn_z = gb.lo_z + gb.dz < D;
+    const bool up_z = gb.lo_z > 0 || L.gzu, dn_z = gb.lo_z + gb.dz < D || L.gzd;   // ghost planes: shards
     const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
     const bool lf_c = gb.lo_c > 0, rt_c = gb.lo_c + gb.wc < W;
 
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
             const int gc = gb.lo_c + c, gr = gb.lo_r + r, gz = gb.lo_z + z;
             if (gc + 1 < W) qd += o ^ (y_in[G + 1] >> 1);
             if (gr + 1 < H) qd += o ^ (y_in[G + W] >> 1);
-            if (gz + 1 < D) qd += o ^ (y_in[G + HW] >> 1);
+            if (gz + 1 < D || L.gzd) qd += o ^ (y_in[G + HW] >> 1);
             e_acc += (int64_t)L.lamw * qd;
         }
         const bool ychg = (2 * y != y2old);
@@ -344,8 +344,8 @@ __global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
         if (Fm & 4u) L.dirty[k + 1] = 1u;
         if (Fm & 8u) L.dirty[k - KX] = 1u;
         if (Fm & 16u) L.dirty[k + KX] = 1u;
-        if (Fm & 32u) L.dirty[k - KYX] = 1u;
-        if (Fm & 64u) L.dirty[k + KYX] = 1u;
+        if ((Fm & 32u) && k - KYX >= 0) L.dirty[k - KYX] = 1u;
+        if ((Fm & 64u) && k + KYX < L.K) L.dirty[k + KYX] = 1u;
         ybuf_stamp(L, out)[k] = (uint32_t)L.st->iteration + 1u;
         if (Fm & 256u) ychg_stamp(L)[k] = (uint32_t)L.st->iteration + 1u;
         CtaAgg agg;
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_consensus3d_vec(Lat2 L, int l
     for (int k = blockIdx.x; k < L.K; k += gridDim.x) {
         int bz, by, bx;
         const Geo3 gb = block_geo3(L, k, bz, by, bx);
-        const bool up_z = gb.lo_z > 0, dn_z = gb.lo_z + gb.dz < D;
+        const bool up_z = gb.lo_z > 0 || L.gzu, dn_z = gb.lo_z + gb.dz < D || L.gzd;   // ghost planes: shards
         const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
         const bool lf_c = gb.lo_c > 0, rt_c = gb.lo_c + gb.wc < W;
         const int nq = (gb.dz * gb.hr) << lq;
@@ -405,7 +405,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_consensus3d_vec(Lat2 L, int l
             bool fast = epo[k] != ep;
             fast = fast && !(lf_c && epo[k - 1] == ep) && !(rt_c && epo[k + 1] == ep);
             fast = fast && !(up_r && epo[k - KX] == ep) && !(dn_r && epo[k + KX] == ep);
-            fast = fast && !(up_z && epo[k - KYX] == ep) && !(dn_z && epo[k + KYX] == ep);
+            fast = fast && !(gb.lo_z > 0 && epo[k - KYX] == ep) && !(gb.lo_z + gb.dz < D && epo[k + KYX] == ep);
+            fast = fast && !(gb.lo_z == 0 && L.gzu) && !(gb.lo_z + gb.dz == D && L.gzd);   // other rank's solves unknown
             if (fast) {
                 const uint32_t st_out = ybuf_stamp(L, out)[k];
                 if (st_out == 0u || st_out < ychg_stamp(L)[k]) {
@@ -449,7 +450,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_consensus3d_vec(Lat2 L, int l
                     yo[j] = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G));
                     if (want_e) {
                         if (gb.lo_r + r + 1 < H) yb[j] = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G + W));
-                        if (gb.lo_z + z + 1 < D) yz[j] = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G + HW));
+                        if (gb.lo_z + z + 1 < D || L.gzd) yz[j] = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G + HW));
                         if (c0 + 4 == gb.wc && gb.lo_c + c0 + 4 < W) yr[j] = y_in[G + 4];
                     }
                     // cross-block neighbour labels: count / sum per voxel (bytes)
@@ -476,7 +477,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_consensus3d_vec(Lat2 L, int l
                     else rw = (gb.lo_c + c0 + 4 < W) ? (uint32_t)yr[j] : (yo[j] >> 24);
                     int qd = __popc(yo[j] ^ __funnelshift_r(yo[j], rw, 8));
                     if (gb.lo_r + r + 1 < H) qd += __popc(yo[j] ^ yb[j]);
-                    if (gb.lo_z + z + 1 < D) qd += __popc(yo[j] ^ yz[j]);
+                    if (gb.lo_z + z + 1 < D || L.gzd) qd += __popc(yo[j] ^ yz[j]);
                     e_acc += (int64_t)L.lamw * qd;
                 }
                 // y = clamp(h + a - q*sx), sx = cnt*h - nb (biased by 4)
@@ -539,8 +540,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_consensus3d_vec(Lat2 L, int l
             if (Fm & 4u) L.dirty[k + 1] = 1u;
             if (Fm & 8u) L.dirty[k - KX] = 1u;
             if (Fm & 16u) L.dirty[k + KX] = 1u;
-            if (Fm & 32u) L.dirty[k - KYX] = 1u;
-            if (Fm & 64u) L.dirty[k + KYX] = 1u;
+            if ((Fm & 32u) && k - KYX >= 0) L.dirty[k - KYX] = 1u;
+            if ((Fm & 64u) && k + KYX < L.K) L.dirty[k + KYX] = 1u;
             ybuf_stamp(L, out)[k] = (uint32_t)it + 1u;
             if (Fm & 256u) ychg_stamp(L)[k] = (uint32_t)it + 1u;
             agg.add_block(E, U, S, (Fm & 128u) ? 1 : 0);
@@ -590,7 +591,7 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
     for (int k = blockIdx.x; k < L.K; k += gridDim.x) {
         int bz, by, bx;
         const Geo3 gb = block_geo3(L, k, bz, by, bx);
-        const bool up_z = gb.lo_z > 0, dn_z = gb.lo_z + gb.dz < D;
+        const bool up_z = gb.lo_z > 0 || L.gzu, dn_z = gb.lo_z + gb.dz < D || L.gzd;   // ghost planes: shards
         const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
         const bool lf_c = gb.lo_c > 0, rt_c = gb.lo_c + gb.wc < W;
         const int64_t G0 = ((int64_t)gb.lo_z * H + gb.lo_r + r) * W + gb.lo_c + c0;
@@ -600,7 +601,8 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
             bool fast = epo[k] != ep;
             fast = fast && !(lf_c && epo[k - 1] == ep) && !(rt_c && epo[k + 1] == ep);
             fast = fast && !(up_r && epo[k - KX] == ep) && !(dn_r && epo[k + KX] == ep);
-            fast = fast && !(up_z && epo[k - KYX] == ep) && !(dn_z && epo[k + KYX] == ep);
+            fast = fast && !(gb.lo_z > 0 && epo[k - KYX] == ep) && !(gb.lo_z + gb.dz < D && epo[k + KYX] == ep);
+            fast = fast && !(gb.lo_z == 0 && L.gzu) && !(gb.lo_z + gb.dz == D && L.gzd);   // other rank's solves unknown
             if (fast) {
                 const uint32_t st_out = ybuf_stamp(L, out)[k];
                 if (st_out == 0u || st_out < ychg_stamp(L)[k]) {
@@ -652,7 +654,7 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
                     if (want_e) {
                         if (yld) yb[j] = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G + W));
                         if (c0 == 28 && xnx) yr[j] = y_in[G + 4];
-                        if (z == zl && gb.lo_z + z + 1 < D)
+                        if (z == zl && (gb.lo_z + z + 1 < D || L.gzd))
                             yz = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G + HW));
                     }
                     if (top) { cnt[j] += 0x01010101u; nb[j] += *reinterpret_cast<const uint32_t *>(L.yhat + G - W); }
@@ -674,7 +676,7 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
                     const uint32_t rw = c0 < 28 ? nxt : (xnx ? (uint32_t)yr[j] : (yo[j] >> 24));
                     int qd = __popc(yo[j] ^ __funnelshift_r(yo[j], rw, 8));
                     if (ydn) qd += __popc(yo[j] ^ (yld ? yb[j] : dnv));
-                    if (gb.lo_z + z + 1 < D) qd += __popc(yo[j] ^ (z < zl ? yo[j + 1 < ZB ? j + 1 : j] : yz));
+                    if (gb.lo_z + z + 1 < D || L.gzd) qd += __popc(yo[j] ^ (z < zl ? yo[j + 1 < ZB ? j + 1 : j] : yz));
                     e_acc += (int64_t)L.lamw * qd;
                 }
                 const uint32_t h4 = yh4[j];
@@ -735,8 +737,8 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
             if (Fm & 4u) L.dirty[k + 1] = 1u;
             if (Fm & 8u) L.dirty[k - KX] = 1u;
             if (Fm & 16u) L.dirty[k + KX] = 1u;
-            if (Fm & 32u) L.dirty[k - KYX] = 1u;
-            if (Fm & 64u) L.dirty[k + KYX] = 1u;
+            if ((Fm & 32u) && k - KYX >= 0) L.dirty[k - KYX] = 1u;
+            if ((Fm & 64u) && k + KYX < L.K) L.dirty[k + KYX] = 1u;
             ybuf_stamp(L, out)[k] = ep;
             if (Fm & 256u) ychg_stamp(L)[k] = ep;
             agg.add_block(E, U, S, (Fm & 128u) ? 1 : 0);

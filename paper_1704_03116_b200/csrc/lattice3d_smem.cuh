@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
     // start of the block's resid slot; the fallback body uses byte planes
     uint8_t *rr = L.resid + (size_t)k * 6 * M;
     uint32_t *gF = reinterpret_cast<uint32_t *>(rr);
-    const bool up_z = gb.lo_z > 0, dn_z = gb.lo_z + gb.dz < D;
+    const bool up_z = gb.lo_z > 0 || L.gzu, dn_z = gb.lo_z + gb.dz < D || L.gzd;   // ghost planes: shards
     const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
     const bool lf_c = gb.lo_c > 0, rt_c = gb.lo_c + gb.wc < W;
     const bool xin = lane < gb.wc, yin = warp < gb.hr;

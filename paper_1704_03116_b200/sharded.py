@@ -1,12 +1,13 @@
-"""Multi-GPU sharding of the ADMM loop: slabs of block rows, halo exchange.
+"""Multi-GPU sharding of the ADMM loop: slabs of block rows (2D) or block
+planes (3D, along the depth axis), halo exchange.
 
 The reference parallelises `update_blocks` over sub-regions with a thread
 pool (admm.py:186-190) and keeps everything else global.  Here the
 sub-regions are sharded across GPUs as contiguous slabs of block rows.  Within
 an iteration the only cross-shard data are one-pixel halos:
 
-  1. K1 on every shard (the block objective reads y of the row above/below the
-     slab from the ghost rows);
+  1. K1 on every shard (the block objective reads y of the row / plane
+     above and below the slab from the ghost rows / planes);
   2. exchange of the label (yhat) boundary rows -> ghost rows;
   3. consensus pass on every shard -> local aggregates
      [energy of y_{t-1}, sum of block residuals^2, max block residual^2, clamp];
@@ -63,32 +64,33 @@ class _Problems:
 
 
 class GpuShard:
-    """One slab of whole block rows on the current CUDA device (product executor)."""
+    """One slab of whole block rows (2D) / block planes (3D) on the current
+    CUDA device (product executor)."""
 
     def __init__(self, full: LatticeLowering, kb0: int, kb1: int, mu: int, eps: float,
                  max_iters: int, warm_start: bool = True, skip_clean: bool = True):
         import torch
-        H, W = full.dims
-        ky, kx = full.kpa
-        if H % ky:
+        dims, kpa = tuple(full.dims), tuple(full.kpa)
+        n0, k0 = dims[0], kpa[0]   # the sharded axis: rows (2D) / planes (3D)
+        if n0 % k0:
             raise NotImplementedError("sharding needs a uniform tiling along the sharded axis")
-        bh = H // ky
+        bh = n0 // k0
         self.kb0, self.kb1, self.bh = kb0, kb1, bh
         self.r0, self.r1 = kb0 * bh, kb1 * bh
-        u = full.u.reshape(H, W)[self.r0:self.r1].ravel()
-        low = LatticeLowering((self.r1 - self.r0, W), (kb1 - kb0, kx), full.conn, full.lamw,
-                              np.ascontiguousarray(u), full.lam)
+        u = full.u.reshape(dims)[self.r0:self.r1].ravel()
+        low = LatticeLowering((self.r1 - self.r0,) + dims[1:], (kb1 - kb0,) + kpa[1:], full.conn,
+                              full.lamw, np.ascontiguousarray(u), full.lam)
         dev = _device()
         self.problems = _Problems(low, dev)
         self.dev = _DeviceState(self.problems, mu, eps, max_iters, warm_start, skip_clean)
         L = self.dev.L
         L.ghost_up = int(kb0 > 0)
-        L.ghost_dn = int(kb1 < ky)
+        L.ghost_dn = int(kb1 < k0)
         L.sharded = 1
         L.fuse_multipliers = 1
         _lib.check(_lib.lib().dope_lattice_check(C.byref(L)), "dope_lattice_check (shard)")
-        self.W = W
-        self.rows_u8 = [torch.zeros(W, dtype=torch.uint8, device=dev) for _ in range(4)]
+        self.W = int(np.prod(dims[1:]))   # exchanged unit: one row (2D) / plane (3D), bytes
+        self.rows_u8 = [torch.zeros(self.W, dtype=torch.uint8, device=dev) for _ in range(4)]
 
     # -- kernels ------------------------------------------------------------
     def call(self, name, *args):
@@ -238,11 +240,9 @@ def run_virtual(model: EnergyModel, partition: Partition, config: AdmmConfig, sh
 
     Returns (labels, trace, state_fields) assembled from the shards."""
     full = lower_lattice(model, partition)
-    if len(full.dims) != 2:
-        raise NotImplementedError("sharding is implemented for 2D lattices")
     if config.mu_fact != 1.0:
         raise NotImplementedError("the integer lattice path keeps mu fixed (mu_fact == 1)")
-    mu0 = config.resolved_mu0(2)
+    mu0 = config.resolved_mu0(len(full.dims))
     eps = config.resolved_eps(partition)
     slabs = shard_block_rows(full.kpa[0], shards)
     sh = [GpuShard(full, a, b, int(mu0), eps, config.max_iters, config.warm_start,
@@ -307,7 +307,7 @@ class NcclShard(GpuShard):
     def __init__(self, *args, **kw):
         import torch
         super().__init__(*args, **kw)
-        self.halo = torch.zeros(4 * 4 * self.W, dtype=torch.uint8, device=self.problems.device)
+        self.halo = torch.zeros(16 * self.W, dtype=torch.uint8, device=self.problems.device)
         self.dev.L.halo = self.halo.data_ptr()
 
     def run(self, comm: NcclComm, iters: int, use_graph: bool = True):
@@ -322,9 +322,7 @@ class NcclShard(GpuShard):
 def shard_for_rank(model: EnergyModel, partition: Partition, config: AdmmConfig, rank: int,
                    world: int, cls=NcclShard):
     full = lower_lattice(model, partition)
-    if len(full.dims) != 2:
-        raise NotImplementedError("sharding is implemented for 2D lattices")
-    mu0 = config.resolved_mu0(2)
+    mu0 = config.resolved_mu0(len(full.dims))
     kb0, kb1 = shard_block_rows(full.kpa[0], world)[rank]
     return cls(full, kb0, kb1, int(mu0), config.resolved_eps(partition), config.max_iters,
                config.warm_start, config.skip_clean)

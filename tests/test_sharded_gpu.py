@@ -68,3 +68,38 @@ def test_nccl_single_rank_graph_matches_single_gpu():
     assert [t.energy for t in trace] == [t.energy for t in s1.trace]
     assert np.array_equal(labels, labels1)
     assert st["best_iteration"] == s1.best_iteration
+
+
+@pytest.mark.parametrize("size,block,shards", [(96, 32, 3), (128, 32, 2), (64, 16, 4)])
+def test_virtual_3d_shards_match_single_gpu(size, block, shards):
+    """3D: slabs of block planes with ghost planes (C4's multi-GPU layout)."""
+    wl = W.c4(seed=4, size=size, block=block, iters=10)
+    model, part = _model(wl)
+    cfg = dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=wl.iters)
+    labels1, s1 = dope.run(model, part, cfg)
+    labels, trace, st = sharded.run_virtual(model, part, cfg, shards)
+    assert st["iterations"] == s1.iteration
+    assert [t.energy for t in trace] == [t.energy for t in s1.trace]
+    assert [t.max_block_residual for t in trace] == [t.max_block_residual for t in s1.trace]
+    np.testing.assert_allclose([t.residual_sq for t in trace], [t.residual_sq for t in s1.trace], rtol=1e-12)
+    assert [t.clamped for t in trace] == [t.clamped for t in s1.trace]
+    assert np.array_equal(labels, labels1)
+    assert np.array_equal(st["yhat"], s1.labels_global())
+    assert np.array_equal(st["y"], s1.y)
+
+
+def test_nccl_single_rank_graph_matches_single_gpu_3d():
+    wl = W.c4(seed=6, size=64, block=32, iters=12)
+    model, part = _model(wl)
+    cfg = dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=wl.iters)
+    labels1, s1 = dope.run(model, part, cfg)
+    comm = sharded.NcclComm(0, 1)
+    try:
+        sh = sharded.shard_for_rank(model, part, cfg, 0, 1)
+        sh.run(comm, cfg.max_iters, use_graph=True)
+        labels, trace, st = sharded.collect([sh], 1.0, cfg)
+    finally:
+        comm.close()
+    assert [t.energy for t in trace] == [t.energy for t in s1.trace]
+    assert np.array_equal(labels, labels1)
+    assert st["best_iteration"] == s1.best_iteration
