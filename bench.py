@@ -596,9 +596,9 @@ def main():
                        "pixel_edges_per_s": value * wl.num_pairs,
                        "l2": ("inputs larger than L2 (state > 126 MB)" if wl.n * 21 > 126e6 else
                               "state fits in the 126 MB L2 (small config; no flush between steps)"),
-                       "parallelism": (f"{ws} GPUs: block rows sharded in slabs, NCCL halo "
-                                       f"rows + 4-scalar all-reduce per iteration" if ws > 1
-                                       else "1 GPU"),
+                       "parallelism": (f"{ws} GPUs: block {'planes' if len(wl.dims) == 3 else 'rows'} "
+                                       f"sharded in slabs, NCCL halo {'planes' if len(wl.dims) == 3 else 'rows'}"
+                                       f" + 4-scalar all-reduce per iteration" if ws > 1 else "1 GPU"),
                        "block_solves_per_run": solves_per_run,
                        "push_relabel_sweeps_per_run": sweeps_per_run,
                        "kernels": kstat},
