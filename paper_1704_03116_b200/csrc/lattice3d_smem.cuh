@@ -647,13 +647,15 @@ __global__ void k_init_resid3d_nib(Lat2 L) {
     uint32_t *gF = reinterpret_cast<uint32_t *>(L.resid + (size_t)k * 6 * M);
     for (int w = threadIdx.x; w < 3 * NIBW; w += blockDim.x) {
         const int p = w / NIBW, v0 = (w - p * NIBW) * 8;
-        uint32_t x = 0;
-        for (int e = 0; e < 8; ++e) {
-            const int v = v0 + e, z = v / PLANE, r = (v / B) % B, c = v % B;
-            if (!(z < gb.dz && r < gb.hr && c < gb.wc)) continue;
-            const bool has = p == 0 ? c + 1 < gb.wc : p == 1 ? r + 1 < gb.hr : z + 1 < gb.dz;
-            if (has) x |= (uint32_t)L.cap << (4 * e);
+        const int z = v0 / PLANE, r = (v0 / B) % B, c0 = v0 % B;
+        // nibbles e with an existing arc: x = c0 + e inside the row (E: x + 1 inside)
+        int n = 0;
+        if (z < gb.dz && r < gb.hr) {
+            if (p == 0) n = gb.wc - 1 - c0;
+            else if ((p == 1 && r + 1 < gb.hr) || (p == 2 && z + 1 < gb.dz)) n = gb.wc - c0;
         }
-        gF[w] = x;
+        n = n < 0 ? 0 : (n > 8 ? 8 : n);
+        const uint32_t m = n == 8 ? 0xffffffffu : ((1u << (4 * n)) - 1u);
+        gF[w] = ((uint32_t)L.cap * 0x11111111u) & m;
     }
 }

@@ -166,3 +166,144 @@ class CpuShard:
 
     def labels(self):
         return (self.final_y2 >= 1).astype(np.int8)
+
+
+class CpuShardND:
+    """GpuShard interface for 2D and 3D lattices (slab of whole blocks along
+    axis 0 with one ghost row / plane on each side), vectorised numpy + the
+    oracle's BK per block.  Same per-shard semantics as the kernels."""
+
+    def __init__(self, u, dims, kpa, lamw, mu, max_iters, kb0, kb1):
+        dims, kpa = tuple(dims), tuple(kpa)
+        self.nd = len(dims)
+        self.bs = tuple(d // k for d, k in zip(dims, kpa))
+        self.kpa = kpa
+        self.kb0, self.kb1 = kb0, kb1
+        self.r0, self.r1 = kb0 * self.bs[0], kb1 * self.bs[0]
+        self.ldims = (self.r1 - self.r0,) + dims[1:]
+        self.u = u.reshape(dims)[self.r0:self.r1].astype(np.int64)
+        self.lamw, self.mu, self.q = lamw, mu, lamw // mu
+        self.gup, self.gdn = kb0 > 0, kb1 < kpa[0]
+        self.max_iters = max_iters
+        self.W = int(np.prod(dims[1:]))
+        self.agg = torch.zeros(4, dtype=torch.int64)
+        self.energy_acc = torch.zeros(1, dtype=torch.int64)
+        self.rows_u8 = [torch.zeros(self.W, dtype=torch.uint8) for _ in range(4)]
+        # block-internal pairs (forward neighbours along every axis), block-local indices
+        idx = np.arange(int(np.prod(self.bs))).reshape(self.bs)
+        pi, pj = [], []
+        for ax in range(self.nd):
+            lo = [slice(None)] * self.nd
+            hi = [slice(None)] * self.nd
+            lo[ax], hi[ax] = slice(0, -1), slice(1, None)
+            pi.append(idx[tuple(lo)].ravel())
+            pj.append(idx[tuple(hi)].ravel())
+        self.pi = np.concatenate(pi).astype(np.int32)
+        self.pj = np.concatenate(pj).astype(np.int32)
+
+    def init(self):
+        shp = (self.ldims[0] + 2,) + self.ldims[1:]
+        self.y2 = np.ones(shp, dtype=np.int64)
+        self.yh = np.zeros(shp, dtype=np.int64)
+        self.a = np.zeros(self.ldims, dtype=np.int64)
+        self.y2_prev = None
+        self.best_e, self.best_it, self.best_y2 = None, 0, self.y2[1:-1].copy()
+        self.it, self.converged, self.stop = 0, False, False
+        self.trace_e, self.trace_mr, self.trace_rs, self.trace_cl = [], [], [], []
+
+    def _cross(self, arr):
+        """sum over cross-block neighbours j of (arr_v - arr_j) for every local voxel
+        (arr carries the ghost layers along axis 0)."""
+        loc = arr[1:-1]
+        s = np.zeros(self.ldims, dtype=np.int64)
+        for ax in range(self.nd):
+            n, b = self.ldims[ax], self.bs[ax]
+            c = np.arange(n)
+            shape = [1] * self.nd
+            shape[ax] = n
+            low = (c % b == 0).reshape(shape)
+            high = (c % b == b - 1).reshape(shape)
+            if ax == 0:
+                prev, nxt = arr[:-2], arr[2:]
+                has_prev = np.ones(n, bool)
+                has_prev[0] = self.gup
+                has_next = np.ones(n, bool)
+                has_next[-1] = self.gdn
+            else:
+                prev = np.roll(loc, 1, axis=ax)
+                nxt = np.roll(loc, -1, axis=ax)
+                has_prev = c > 0
+                has_next = c < n - 1
+            s += np.where(low & has_prev.reshape(shape), loc - prev, 0)
+            s += np.where(high & has_next.reshape(shape), loc - nxt, 0)
+        return s
+
+    def _blocks(self):
+        nb = [self.ldims[a] // self.bs[a] for a in range(self.nd)]
+        for k in np.ndindex(*nb):
+            yield tuple(slice(k[a] * self.bs[a], (k[a] + 1) * self.bs[a]) for a in range(self.nd))
+
+    def update_blocks(self):
+        if self.stop:
+            return
+        s = self._cross(self.y2)
+        lin = (2 * self.u + self.lamw * s + self.mu * (2 * self.a - self.y2[1:-1]) + self.mu) / 2.0
+        cap = np.full(self.pi.size, float(self.lamw))
+        for sl in self._blocks():
+            labels, _ = orc.bk_maxflow(lin[sl].ravel().astype(np.float64), self.pi, self.pj, cap, cap)
+            gl = (slice(sl[0].start + 1, sl[0].stop + 1),) + sl[1:]
+            self.yh[gl] = labels.reshape(self.bs)
+
+    def staging(self, which):
+        return self.rows_u8
+
+    def pack_rows(self, which):
+        first, last, _, _ = self.staging(which)
+        src = self.yh if which == 0 else self.y2
+        first.copy_(torch.from_numpy(src[1].ravel().astype(np.uint8)))
+        last.copy_(torch.from_numpy(src[self.ldims[0]].ravel().astype(np.uint8)))
+        return first, last
+
+    def ghost_update(self, which, up, dn):
+        dst = self.yh if which == 0 else self.y2
+        if up is not None and self.gup:
+            dst[0] = up.numpy().reshape(self.ldims[1:])
+        if dn is not None and self.gdn:
+            dst[self.ldims[0] + 1] = dn.numpy().reshape(self.ldims[1:])
+
+    def _pair_energy(self, yo):
+        e = 0
+        for ax in range(1, self.nd):
+            e += int(np.abs(np.diff(yo[1:-1], axis=ax)).sum())
+        last = self.ldims[0] + 1 if self.gdn else self.ldims[0]
+        e += int(np.abs(yo[2:last + 1] - yo[1:last]).sum())
+        return self.lamw * e
+
+    def update_global(self):
+        if self.stop:
+            return
+        ypre = self.yh[1:-1] + self.a - self.q * self._cross(self.yh)
+        clamped = int(np.any((ypre < 0) | (ypre > 1)))
+        y_new = np.clip(ypre, 0, 1)
+        yh = self.yh[1:-1]
+        ss_blocks = np.array([int(((yh[sl] - y_new[sl]) ** 2).sum()) for sl in self._blocks()])
+        e = 0
+        if self.it >= 1:
+            yo = self.y2 >> 1
+            e = int((self.u * yo[1:-1]).sum()) + self._pair_energy(yo)
+        rs = float(np.sum(np.sqrt(ss_blocks.astype(np.float64)) ** 2))
+        self.agg[0] = e
+        self.agg[1:2].view(torch.float64)[0] = rs
+        self.agg[2] = int(ss_blocks.max())
+        self.agg[3] = clamped
+        self.a = self.a + yh - y_new
+        self.y2_prev = self.y2.copy()
+        self.y2[1:-1] = 2 * y_new
+
+    decide = CpuShard.decide
+    finish_decide = CpuShard.finish_decide
+    labels = CpuShard.labels
+
+    def energy_local(self):
+        yo = self.y2 >> 1
+        self.energy_acc[0] = int((self.u * yo[1:-1]).sum()) + self._pair_energy(yo)

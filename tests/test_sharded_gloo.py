@@ -32,12 +32,12 @@ def _worker(rank, world, port, case, out_dir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from cpu_shard import CpuShard
+    from cpu_shard import CpuShard, CpuShardND
     from paper_1704_03116_b200 import sharded
     u, dims, kpa, lamw, iters = case
     slabs = sharded.shard_block_rows(kpa[0], world)
     kb0, kb1 = slabs[rank]
-    sh = CpuShard(u, dims, kpa, lamw, 1, iters, kb0, kb1)
+    sh = (CpuShard if len(dims) == 2 else CpuShardND)(u, dims, kpa, lamw, 1, iters, kb0, kb1)
     sharded.run_shards([sh], sharded.DistComm(), iters)
     np.savez(Path(out_dir) / f"rank{rank}.npz", labels=sh.labels(), energy=np.array(sh.trace_e),
              maxres=np.array(sh.trace_mr), rs=np.array(sh.trace_rs), it=sh.it,
@@ -57,6 +57,27 @@ def test_gloo_two_rank_sharded_run_matches_oracle(world, tmp_path):
     ref = orc.run(spec, 1.0, 1.0, 0.0, wl.iters)
     labels = np.concatenate([o["labels"].ravel() for o in outs])
     for o in outs:   # every rank made the same decisions
+        assert int(o["it"]) == ref["iterations"]
+        assert int(o["best"]) == ref["best_iteration"]
+        assert np.array_equal(o["energy"], ref["energy"])
+        assert np.array_equal(o["maxres"], ref["max_block_residual"])
+        np.testing.assert_allclose(o["rs"], ref["residual_sq"], rtol=1e-12)
+    assert np.array_equal(labels, ref["labels"])
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_two_rank_sharded_run_3d_matches_oracle(world, tmp_path):
+    """3D (C4's layout): slabs of block planes, ghost-plane halos over gloo."""
+    import oracle as orc
+    from paper_1704_03116_b200 import workloads as W
+    wl = W.c4(seed=8, size=16, block=8, iters=6)
+    case = (wl.u, wl.dims, wl.kpa, int(wl.lam), wl.iters)
+    mp.spawn(_worker, args=(world, _free_port(), case, str(tmp_path)), nprocs=world, join=True)
+    outs = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
+    spec = orc.LatticeSpec(wl.dims, wl.kpa, wl.offsets, [1.0, 1.0, 1.0], wl.u.astype(np.float64), wl.lam)
+    ref = orc.run(spec, 1.0, 1.0, 0.0, wl.iters)
+    labels = np.concatenate([o["labels"].ravel() for o in outs])
+    for o in outs:
         assert int(o["it"]) == ref["iterations"]
         assert int(o["best"]) == ref["best_iteration"]
         assert np.array_equal(o["energy"], ref["energy"])

@@ -59,8 +59,8 @@ def main():
     lines = [f"# ncu summary `{tag}`", "",
              "Captured on one B200 with `ncu --clock-control none` (launch list: "
              "`--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum`; "
-             "per-kernel: `--set full --import-source on`), driver `tools/profile_round.sh` (launch list: the bench command itself; full sets: `tools/prof_run.py C3 20`, launch 8) "
-             "(C3 4096^2; prof_run launches one kernel at a time, no CUDA graph).  "
+             f"per-kernel: `--set full --import-source on`), driver `tools/profile_round.sh` (launch list: the bench command itself; full sets: `tools/prof_run.py {workload} 20`, launch 8) "
+             "(prof_run launches one kernel at a time, no CUDA graph).  "
              "ncu serialises launches and flushes caches, so compare SHARES, not absolutes.", "",
              "## Launch list", "", "| kernel | launches | total us | share | avg us | DRAM MB/launch |",
              "|---|---|---|---|---|---|"]
