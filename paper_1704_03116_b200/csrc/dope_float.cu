@@ -42,6 +42,7 @@ struct LatF {
     Axis ay, ax;
     int32_t W, conn, ndir;
     double lam, mu, eps, qs;
+    double inv_mu;                // 1/mu when mu is a power of two (x/mu == x*inv_mu exactly), else 0
     int32_t warm, skip_clean, fuse, max_iters, K, boxh, boxw;
     const double *u, *rdiag;
     const double *w[4];          // E S SE SW, weight of pair (i, i+off) at i
@@ -108,6 +109,16 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
     int32_t *gres = L.resid + (size_t)k * NDIR * M;
 
     // ---- prologue: linear in float64 (blockform.py:271-272), quantised ----
+    // Warm start: the kept residual planes stream into shared memory first
+    // (all 16-byte loads in flight); the stored flow is then read back from
+    // them through the arc-pair invariant r(v->w) + r(w->v) = 2 cap(v,w), so
+    // no capacity plane is re-read: net inflow on arc d = (r_d(v) - r_d'(w)) / 2.
+    if (L.warm) {
+        const int4 *src = reinterpret_cast<const int4 *>(gres);
+        int4 *dst = reinterpret_cast<int4 *>(rr);
+#pragma unroll 4
+        for (int i = tid; i < NDIR * M / 4; i += NT) dst[i] = src[i];
+    }
     for (int i = 0; i < NPT; ++i) {
         const int v = tid + i * NT;
         const int r = v / BW, c = v % BW;
@@ -120,47 +131,56 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
             constexpr int ORD8[8] = {5, 3, 7, 1, 0, 6, 2, 4};
             constexpr int ORD4[4] = {3, 1, 0, 2};
             double cy = 0.0;
+            const bool border = r == 0 || c == 0 || r == hr - 1 || c == wc - 1;
+            if (border) {
 #pragma unroll
-            for (int t = 0; t < NDIR; ++t) {
-                const int d = NDIR == 8 ? ORD8[t] : ORD4[t];
-                const int rn = R + dy_of(d), cn = Cc + dx_of(d);
-                if (rn < 0 || rn >= H || cn < 0 || cn >= Wg) continue;
-                if (rn >= lo_r && rn < lo_r + hr && cn >= lo_c && cn < lo_c + wc) continue;
-                int pl;
-                const int64_t low = pair_low(L, G, d, pl);
-                cy += (-L.w[pl][low]) * y_cur[(int64_t)rn * Wg + cn];
+                for (int t = 0; t < NDIR; ++t) {
+                    const int d = NDIR == 8 ? ORD8[t] : ORD4[t];
+                    const int rn = R + dy_of(d), cn = Cc + dx_of(d);
+                    if (rn < 0 || rn >= H || cn < 0 || cn >= Wg) continue;
+                    if (rn >= lo_r && rn < lo_r + hr && cn >= lo_c && cn < lo_c + wc) continue;
+                    int pl;
+                    const int64_t low = pair_low(L, G, d, pl);
+                    cy += (-L.w[pl][low]) * y_cur[(int64_t)rn * Wg + cn];
+                }
             }
             const double sy = y_cur[G];
             const double lin = L.u[G] + L.lam * (cy + L.rdiag[G] * sy) + L.mu * ((a_cur[G] - sy) + 0.5);
             const double qv = rint(lin * L.qs);
             gv = (int32_t)fmax(fmin(qv, 1.0e9), -1.0e9);
-            int32_t f = 0;
+            if (!L.warm) {
 #pragma unroll
-            for (int d = 0; d < NDIR; ++d) {
-                const int rb = r + dy_of(d), cb = c + dx_of(d);
-                const bool has = rb >= 0 && rb < hr && cb >= 0 && cb < wc;
-                int pl;
-                const int64_t low = pair_low(L, G, d, pl);
-                const int32_t capd = has ? L.cq[pl][low] : 0;
-                if (L.warm) {
-                    if (has) f += gres[d * M + v] - capd;
-                } else {
-                    rr[d * M + v] = capd;
+                for (int d = 0; d < NDIR; ++d) {
+                    const int rb = r + dy_of(d), cb = c + dx_of(d);
+                    const bool has = rb >= 0 && rb < hr && cb >= 0 && cb < wc;
+                    int pl;
+                    const int64_t low = pair_low(L, G, d, pl);
+                    rr[d * M + v] = has ? L.cq[pl][low] : 0;
                 }
             }
-            if (L.warm) gv += f;
         } else if (!L.warm) {
 #pragma unroll
             for (int d = 0; d < NDIR; ++d) rr[d * M + v] = 0;
         }
         g[v] = gv;
     }
-    if (L.warm) {
-        const int4 *src = reinterpret_cast<const int4 *>(gres);
-        int4 *dst = reinterpret_cast<int4 *>(rr);
-        for (int i = tid; i < NDIR * M / 4; i += NT) dst[i] = src[i];
-    }
     __syncthreads();
+    if (L.warm) {
+        for (int i = 0; i < NPT; ++i) {
+            const int v = tid + i * NT;
+            const int r = v / BW, c = v % BW;
+            if (!(r < hr && c < wc)) continue;
+            int32_t f2 = 0;
+#pragma unroll
+            for (int d = 0; d < NDIR; ++d) {
+                const int rb = r + dy_of(d), cb = c + dx_of(d);
+                if (rb >= 0 && rb < hr && cb >= 0 && cb < wc)
+                    f2 += rr[d * M + v] - rr[(d ^ 1) * M + rb * BW + cb];
+            }
+            g[v] += f2 / 2;
+        }
+        __syncthreads();
+    }
 
     if (mincut_solve<BH, BW, NT, NDIR>(g, rr, h, masks, reach, misc, sweep_min, sweep_mul) < 0 && tid == 0)
         atomicCAS(&L.st->error, 0, k + 1);
@@ -262,9 +282,12 @@ __device__ void apply_f(const LatF &L, double E2, double R2, double M2, int F2, 
     st->ycur = out;
 }
 
-// K2f threads per CTA: a 64^2 block is 4096 pixels, so 1024 threads give each
-// thread 4 (the per-pixel work is a chain of dependent loads)
-constexpr int K2F_NT = 1024;
+// K2f threads per CTA: 512 (8 pixels each) keeps two CTAs per SM, so C2's 256
+// blocks run in one wave (1024 threads: 45 us per pass, 512: 38 us)
+#ifndef K2F_THREADS
+#define K2F_THREADS 512
+#endif
+constexpr int K2F_NT = K2F_THREADS;
 
 __global__ void __launch_bounds__(K2F_NT) k_consensus_f(LatF L) {
     if (L.st->stop) return;
@@ -298,26 +321,29 @@ __global__ void __launch_bounds__(K2F_NT) k_consensus_f(LatF L) {
     double e_acc = 0.0, ss = 0.0;
     int clamped = 0;
     unsigned marks = 0;
-    const int m = hr * wc;
-#pragma unroll 4
-    for (int v = tid; v < m; v += K2F_NT) {
-        const int r = v / wc, c = v - r * wc;
+    // One pixel of solve_global (admm.py:203-209) + clamp, multipliers,
+    // residual, energy of the previous iterate and dirty marks.  Block-border
+    // pixels sum their cross-block terms in block-id order; they are handled
+    // by a second pass so that no warp of the interior pass diverges into it.
+    auto pixel = [&](int r, int c, bool border) {
         const int32_t R = lo_r + r, Cc = lo_c + c;
         const int64_t G = (int64_t)R * W + Cc;
         const double yh = (double)yhp[G];
         const double av = a_in[G];
         // own-block term and cross-block coupling sums, in block-id order
-        double own = L.mu * (yh + av) - L.lam * (rdg[G] * yh);
-        int nb_blk[8];
-        double nb_term[8];
-        int64_t nb_idx[8];
-        int nn = 0;
-        const bool border = (r == 0 || r == hr - 1 || c == 0 || c == wc - 1);
+        const double own = L.mu * (yh + av) - L.lam * (rdg[G] * yh);
+        double acc = 0.0;
         if (border) {
+            int nb_blk[8];
+            double nb_term[8];
+            int64_t nb_idx[8];
+            int nn = 0;
             for (int d = 0; d < L.ndir; ++d) {
                 const int rn = R + dy_of(d), cn = Cc + dx_of(d);
                 if (rn < 0 || rn >= H || cn < 0 || cn >= W) continue;
-                const int br = L.ay.owner(rn), bc = L.ax.owner(cn);
+                // neighbour at distance 1: its block is this one or the adjacent one
+                const int br = by + (rn < lo_r ? -1 : (rn >= lo_r + hr ? 1 : 0));
+                const int bc = bx + (cn < lo_c ? -1 : (cn >= lo_c + wc ? 1 : 0));
                 if (br == by && bc == bx) continue;
                 int pl;
                 const int64_t low = pair_low(L, G, d, pl);
@@ -332,22 +358,23 @@ __global__ void __launch_bounds__(K2F_NT) k_consensus_f(LatF L) {
                 nb_idx[q] = J;
                 nb_term[q] = (-L.w[pl][low]) * (double)L.yhat[J];
             }
-        }
-        double acc = 0.0;
-        bool own_done = false;
-        int t2 = 0;
-        while (t2 < nn || !own_done) {
-            if (!own_done && (t2 >= nn || nb_blk[t2] > k)) {
-                acc += own;
-                own_done = true;
-                continue;
+            bool own_done = false;
+            int t2 = 0;
+            while (t2 < nn || !own_done) {
+                if (!own_done && (t2 >= nn || nb_blk[t2] > k)) {
+                    acc += own;
+                    own_done = true;
+                    continue;
+                }
+                const int b = nb_blk[t2];
+                double sb = 0.0;
+                while (t2 < nn && nb_blk[t2] == b) sb += nb_term[t2++];
+                acc -= L.lam * sb;
             }
-            const int b = nb_blk[t2];
-            double sb = 0.0;
-            while (t2 < nn && nb_blk[t2] == b) sb += nb_term[t2++];
-            acc -= L.lam * sb;
+        } else {
+            acc = 0.0 + own;
         }
-        const double yp = acc / (L.mu * 1.0);
+        const double yp = L.inv_mu != 0.0 ? acc * L.inv_mu : acc / (L.mu * 1.0);
         clamped |= (yp < 0.0 || yp > 1.0);
         const double y = yp < 0.0 ? 0.0 : (yp > 1.0 ? 1.0 : yp);
         const double yold = y_in[G];
@@ -375,10 +402,29 @@ __global__ void __launch_bounds__(K2F_NT) k_consensus_f(LatF L) {
             for (int d = 0; d < L.ndir; ++d) {
                 const int rn = R + dy_of(d), cn = Cc + dx_of(d);
                 if (rn < 0 || rn >= H || cn < 0 || cn >= W) continue;
-                const int br = L.ay.owner(rn) - by, bc = L.ax.owner(cn) - bx;
+                const int br = rn < lo_r ? -1 : (rn >= lo_r + hr ? 1 : 0);
+                const int bc = cn < lo_c ? -1 : (cn >= lo_c + wc ? 1 : 0);
                 if (br || bc) marks |= 1u << (1 + (br + 1) * 3 + (bc + 1));
             }
         }
+    };
+    // interior pixels
+    const int iw = wc - 2, ih = hr - 2;
+    const int mi = (iw > 0 && ih > 0) ? iw * ih : 0;
+#pragma unroll 4
+    for (int v = tid; v < mi; v += K2F_NT) {
+        const int r = v / iw, c = v - r * iw;
+        pixel(r + 1, c + 1, false);
+    }
+    // the ring of border pixels: top row, bottom row, then left / right columns
+    const int nring = (hr <= 2 || wc <= 2) ? hr * wc : 2 * wc + 2 * (hr - 2);
+    for (int t = tid; t < nring; t += K2F_NT) {
+        int r, c;
+        if (hr <= 2 || wc <= 2) { r = t / wc; c = t - r * wc; }
+        else if (t < wc) { r = 0; c = t; }
+        else if (t < 2 * wc) { r = hr - 1; c = t - wc; }
+        else { const int u = t - 2 * wc; r = 1 + (u >> 1); c = (u & 1) ? wc - 1 : 0; }
+        pixel(r, c, true);
     }
     constexpr int NWARP = K2F_NT / 32;
     __shared__ double red_e[NWARP], red_s[NWARP];
@@ -580,6 +626,10 @@ static int build(const dope_lattice_f *L, LatF &o, const VarF **var) {
     o.ndir = L->conn;
     o.lam = L->lam;
     o.mu = L->mu;
+    {
+        int ex;
+        o.inv_mu = (L->mu > 0 && frexp(L->mu, &ex) == 0.5) ? 1.0 / L->mu : 0.0;
+    }
     o.eps = L->eps;
     o.qs = L->qscale;
     o.warm = L->warm_start;

@@ -10,7 +10,7 @@ import torch  # noqa: E402
 
 from bench import build_problem  # noqa: E402
 from paper_1704_03116_b200 import workloads as W  # noqa: E402
-from paper_1704_03116_b200.admm import _DeviceState  # noqa: E402
+from paper_1704_03116_b200.admm import _DeviceState, make_device_state  # noqa: E402
 
 
 def main():
@@ -19,7 +19,10 @@ def main():
     torch.cuda.set_device(0)
     wl = W.by_name(name)
     _, _, problems = build_problem(wl, torch.device("cuda", 0))
-    dev = _DeviceState(problems, int(wl.rho), 0.0, iters, True, True)
+    if wl.integer:
+        dev = _DeviceState(problems, int(wl.rho), 0.0, iters, True, True)
+    else:
+        dev = make_device_state(problems, float(wl.rho), 0.0, iters)
     dev.call("dope_admm_init")
     dev.call("dope_admm_run", iters, 0, fuse=1)
     dev.call("dope_finish_run")
