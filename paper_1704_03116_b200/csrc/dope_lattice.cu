@@ -1309,11 +1309,13 @@ static K1Tune tune_3d() {
     return t;
 }
 
+// 2D K1: a global relabel every 3 sweeps (measured over C1/C3/C5: C3 16.0k ->
+// 17.5k it/s, C1 25k -> 41k, C5 +1-4 % vs 1 + levels sweeps per round).
 static K1Tune default_tune() {
     static K1Tune t = [] {
         K1Tune x;
-        x.sweep_min = 1;
-        x.sweep_mul = 1;
+        x.sweep_min = 3;
+        x.sweep_mul = 0;
         x.max_rounds = 1 << 16;
         if (const char *e = getenv("DOPE_SWEEP_MIN")) x.sweep_min = atoi(e);
         if (const char *e = getenv("DOPE_SWEEP_MUL")) x.sweep_mul = atoi(e);
