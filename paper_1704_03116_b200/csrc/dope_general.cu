@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -562,7 +563,9 @@ static int configure(const VarG *v) {
 }
 
 static int blocks_pass(const LatG &o, const VarG *v, cudaStream_t s) {
-    v->kernel<<<o.K, v->nt, v->smem, s>>>(o, 1, 1);
+    static const int smin = getenv("DOPE_SWEEPG_MIN") ? atoi(getenv("DOPE_SWEEPG_MIN")) : 1;
+    static const int smul = getenv("DOPE_SWEEPG_MUL") ? atoi(getenv("DOPE_SWEEPG_MUL")) : 1;
+    v->kernel<<<o.K, v->nt, v->smem, s>>>(o, smin, smul);
     return cuda_check(cudaGetLastError(), "general K1");
 }
 
