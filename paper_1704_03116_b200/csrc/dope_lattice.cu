@@ -1029,6 +1029,191 @@ __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
     if (tid == 0) pass_tail(L, agg, cur, best, out);
 }
 
+// Consensus for small blocks (<= 32 x 32, whole x quads): one WARP per block,
+// WPC blocks per CTA in flight, no CTA barrier per block (the per-CTA barrier
+// and the per-CTA aggregate atomics dominated k_consensus_vec on 16^2 / 32^2
+// tilings: thousands of CTAs, each a few blocks).  Lane l owns quads
+// l, l + 32, ...; a row is 1 << lq quads (<= 8), so the quad right of a
+// quad is in the next lane unless the quad ends the row.  Same arithmetic as
+// k_consensus_vec, plus the clean-block pass of k_consensus3d_vec (2D: the 4
+// face neighbours; the iterate is copied into the output buffer).
+template <int WPC>
+__global__ void __launch_bounds__(WPC * 32, 4) k_consensus_warp(Lat2 L, int lq) {
+    constexpr int QB = 2;   // quads per lane per batch
+    if (L.pdl) {
+        griddep_wait();
+        griddep_launch();
+    }
+    if (L.st->stop) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cur = L.st->ycur, best = L.st->ybest, out = other_buffer(cur, best);
+    const ystore_t *__restrict__ y_in = L.y2[cur];
+    ystore_t *__restrict__ y_out = L.y2[out];
+    const astore_t *a_in = L.a;
+    astore_t *a_out = L.fuse ? L.a : nullptr;
+    const int it = L.st->iteration;
+    const bool want_e = L.fuse && it >= 1;
+    const bool clean_ok = L.fuse && L.skip_clean && it >= 2;
+    const uint32_t ep = (uint32_t)it + 1u;
+    const int32_t W = L.W, H = L.ay.dim, q = L.q;
+    const int QR = 1 << lq;
+    CtaAgg agg;   // this warp's blocks (lane 0)
+    const int nwarps = gridDim.x * WPC;
+    for (int k = blockIdx.x * WPC + warp; k < L.K; k += nwarps) {
+        const int by = k / L.ax.k, bx = k - by * L.ax.k;
+        int32_t lo_r, hr, lo_c, wc;
+        L.ay.range(by, lo_r, hr);
+        L.ax.range(bx, lo_c, wc);
+        const bool has_up = lo_r > 0 || L.gup, has_dn = lo_r + hr < H || L.gdn, has_lf = lo_c > 0,
+                   has_rt = lo_c + wc < W;
+        const int nq = hr << lq;
+        if (clean_ok) {
+            const uint32_t *epo = L.dirty + L.K;
+            bool fast = epo[k] != ep;
+            fast = fast && !(has_lf && epo[k - 1] == ep) && !(has_rt && epo[k + 1] == ep);
+            fast = fast && !(lo_r > 0 && epo[k - L.ax.k] == ep) && !(lo_r + hr < H && epo[k + L.ax.k] == ep);
+            fast = fast && !(lo_r == 0 && L.gup) && !(lo_r + hr == H && L.gdn);
+            if (fast) {   // fixed point: only the output buffer needs the iterate
+                for (int t = lane; t < nq; t += 32) {
+                    const int r = t >> lq, c0 = (t & (QR - 1)) << 2;
+                    const int64_t G = (int64_t)(lo_r + r) * W + lo_c + c0;
+                    *reinterpret_cast<unsigned int *>(y_out + G) = *reinterpret_cast<const unsigned int *>(y_in + G);
+                }
+                if (lane == 0) {
+                    L.pu[k] = 0;
+                    L.pr[k] = 0;
+                    agg.add_block(L.pe[k], 0, 0, L.pf[k] & 1);
+                }
+                continue;
+            }
+        }
+        int64_t du = 0;
+        int ss = 0, quad = 0;
+        int clamped = 0, chg_self = 0, chgL = 0, chgR = 0, chgU = 0, chgD = 0;
+        for (int t0 = 0; t0 < nq; t0 += 32 * QB) {
+            uint32_t yh4[QB], up4[QB], dn4[QB], yo[QB], yb[QB];
+            uint2 av[QB];
+            int lf[QB], rt[QB], yr[QB];
+#pragma unroll
+            for (int j = 0; j < QB; ++j) {
+                const int t = t0 + lane + 32 * j;
+                yh4[j] = up4[j] = dn4[j] = yo[j] = yb[j] = 0;
+                av[j] = make_uint2(0, 0);
+                lf[j] = rt[j] = yr[j] = 0;
+                if (t < nq) {
+                    const int r = t >> lq, c0 = (t & (QR - 1)) << 2;
+                    const int64_t G = (int64_t)(lo_r + r) * W + lo_c + c0;
+                    yh4[j] = __ldcs(reinterpret_cast<const unsigned int *>(L.yhat + G));
+                    av[j] = __ldcs(reinterpret_cast<const uint2 *>(a_in + G));
+                    yo[j] = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G));
+                    if (want_e && (lo_r + r + 1 < H || L.gdn))
+                        yb[j] = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G + W));
+                    if (r == 0 && has_up) up4[j] = *reinterpret_cast<const uint32_t *>(L.yhat + G - W);
+                    if (r == hr - 1 && has_dn) dn4[j] = *reinterpret_cast<const uint32_t *>(L.yhat + G + W);
+                    if (c0 == 0 && has_lf) lf[j] = L.yhat[G - 1];
+                    if (c0 + 4 == wc && has_rt) {
+                        rt[j] = L.yhat[G + 4];
+                        if (want_e) yr[j] = y_in[G + 4];
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < QB; ++j) {
+                const int t = t0 + lane + 32 * j;
+                const int r = t >> lq, c0 = (t & (QR - 1)) << 2;
+                const uint32_t ob = (uint32_t)((byte_at(yo[j], 0) >> 1) | ((byte_at(yo[j], 1) >> 1) << 1) |
+                                               ((byte_at(yo[j], 2) >> 1) << 2) | ((byte_at(yo[j], 3) >> 1) << 3));
+                const uint32_t nxt = __shfl_down_sync(FULLMASK, ob, 1);
+                if (t >= nq) continue;
+                const int64_t G = (int64_t)(lo_r + r) * W + lo_c + c0;
+                const bool top = (r == 0 && has_up), bot = (r == hr - 1 && has_dn);
+                const bool lft = (c0 == 0 && has_lf), rgt = (c0 + 4 == wc && has_rt);
+                if (want_e) {
+                    const uint32_t bb = (uint32_t)((byte_at(yb[j], 0) >> 1) | ((byte_at(yb[j], 1) >> 1) << 1) |
+                                                   ((byte_at(yb[j], 2) >> 1) << 2) | ((byte_at(yb[j], 3) >> 1) << 3));
+                    quad += __popc((ob ^ (ob >> 1)) & 0x7u);
+                    if (c0 + 4 < wc) quad += (int)((ob >> 3) ^ (nxt & 1u));
+                    else if (rgt) quad += (int)((ob >> 3) ^ (uint32_t)(yr[j] >> 1));
+                    if (lo_r + r + 1 < H || L.gdn) quad += __popc(ob ^ bb);
+                }
+                int a4[4];
+                unpack_a4(av[j], a4);
+                int y[4], an[4];
+                bool ychg_any = false;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int yh = byte_at(yh4[j], i);
+                    int sx = 0;
+                    if (top) sx += yh - byte_at(up4[j], i);
+                    if (bot) sx += yh - byte_at(dn4[j], i);
+                    if (i == 0 && lft) sx += yh - lf[j];
+                    if (i == 3 && rgt) sx += yh - rt[j];
+                    const int ypre = yh + a4[i] - q * sx;
+                    clamped |= (unsigned)ypre > 1u;
+                    y[i] = ypre < 0 ? 0 : (ypre > 1 ? 1 : ypre);
+                    an[i] = a4[i] + yh - y[i];
+                    ss += yh ^ y[i];
+                    const int yold = byte_at(yo[j], i);
+                    const bool ychg = (2 * y[i] != yold);
+                    if (ychg) du += (int64_t)__ldg(L.u + G + i) * (2 * y[i] - yold);
+                    ychg_any |= ychg;
+                    chg_self |= ychg | (yh != y[i]);
+                }
+                if (a_out) __stcs(reinterpret_cast<uint2 *>(a_out + G), pack_a4(an[0], an[1], an[2], an[3]));
+                __stcg(reinterpret_cast<unsigned int *>(y_out + G), pack_y4(2 * y[0], 2 * y[1], 2 * y[2], 2 * y[3]));
+                if (ychg_any) {
+                    chgU |= top;
+                    chgD |= bot;
+                    chgL |= (lft && (2 * y[0] != byte_at(yo[j], 0)));
+                    chgR |= (rgt && (2 * y[3] != byte_at(yo[j], 3)));
+                }
+            }
+        }
+        // warp reduction; lane 0 publishes the block
+        const int64_t E = (int64_t)L.lamw * (int64_t)__reduce_add_sync(FULLMASK, (unsigned)quad);
+        const int64_t U = warp_sum(du);
+        const int64_t S = (int64_t)__reduce_add_sync(FULLMASK, (unsigned)ss);
+        const unsigned fm = __reduce_or_sync(FULLMASK, (clamped ? 1u : 0u) | (chg_self ? 2u : 0u) | (chgL ? 4u : 0u) |
+                                                           (chgR ? 8u : 0u) | (chgU ? 16u : 0u) | (chgD ? 32u : 0u));
+        if (lane == 0) {
+            L.pe[k] = E;
+            L.pu[k] = U;
+            L.pr[k] = S;
+            L.pf[k] = (int)(fm & 1u);
+            if (fm & 2u) L.dirty[k] = 1u;
+            if (fm & 4u) L.dirty[k - 1] = 1u;
+            if (fm & 8u) L.dirty[k + 1] = 1u;
+            if ((fm & 16u) && k - L.ax.k >= 0) L.dirty[k - L.ax.k] = 1u;
+            if ((fm & 32u) && k + L.ax.k < L.K) L.dirty[k + L.ax.k] = 1u;
+            agg.add_block(E, U, S, (int)(fm & 1u));
+        }
+    }
+    // fold the warps' aggregates, then the CTA's
+    __shared__ int64_t sE[WPC], sU[WPC], sM[WPC], sS[WPC], sX[WPC];
+    __shared__ int sF[WPC];
+    if (lane == 0) {
+        sE[warp] = agg.E;
+        sU[warp] = agg.U;
+        sM[warp] = agg.M;
+        sS[warp] = agg.S;
+        sX[warp] = agg.X;
+        sF[warp] = agg.F;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        CtaAgg c;
+        for (int w = 0; w < WPC; ++w) {
+            c.E += sE[w];
+            c.U += sU[w];
+            c.M = sM[w] > c.M ? sM[w] : c.M;
+            c.S += sS[w];
+            c.X += sX[w];
+            c.F |= sF[w];
+        }
+        pass_tail(L, c, cur, best, out);
+    }
+}
+
 // a += yhat - y for the step-level API (admm.py:241-248), in place.
 __global__ void k_update_multipliers(Lat2 L, int64_t n) {
     astore_t *a = L.a;
@@ -1562,7 +1747,10 @@ static int launch_k2(const Lat2 &o, cudaStream_t s) {
         const int sms = sm_count();
         auto grid = [&](int per_sm) { return o.K < per_sm * sms ? o.K : per_sm * sms; };
         cudaError_t e;
-        if (quads <= 4 * 32) e = launch_pdl(k_consensus_vec<32>, dim3(grid(32)), dim3(32), 0, s, o, lq);
+        static const bool no_warp = getenv("DOPE_NO_K2_WARP") != nullptr;
+        if (!no_warp && lq <= 3 && quads <= 256)   // blocks <= 32 x 32: a warp per block
+            e = launch_pdl(k_consensus_warp<8>, dim3(grid(4)), dim3(256), 0, s, o, lq);
+        else if (quads <= 4 * 32) e = launch_pdl(k_consensus_vec<32>, dim3(grid(32)), dim3(32), 0, s, o, lq);
         else if (quads <= 4 * 64) e = launch_pdl(k_consensus_vec<64>, dim3(grid(24)), dim3(64), 0, s, o, lq);
         else if (quads <= 4 * 256) e = launch_pdl(k_consensus_vec<256>, dim3(grid(8)), dim3(256), 0, s, o, lq);
         else if (quads <= 4 * 1024) e = launch_pdl(k_consensus_vec<1024>, dim3(grid(2)), dim3(1024), 0, s, o, lq);
