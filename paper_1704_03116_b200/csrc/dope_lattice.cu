@@ -1037,9 +1037,8 @@ __global__ void __launch_bounds__(NT) k_consensus_vec(Lat2 L, int lq) {
 // quad is in the next lane unless the quad ends the row.  Same arithmetic as
 // k_consensus_vec, plus the clean-block pass of k_consensus3d_vec (2D: the 4
 // face neighbours; the iterate is copied into the output buffer).
-template <int WPC>
-__global__ void __launch_bounds__(WPC * 32, 4) k_consensus_warp(Lat2 L, int lq) {
-    constexpr int QB = 2;   // quads per lane per batch
+template <int WPC, int QB, int MINB>   // QB: quads per lane per batch
+__global__ void __launch_bounds__(WPC * 32, MINB) k_consensus_warp(Lat2 L, int lq) {
     if (L.pdl) {
         griddep_wait();
         griddep_launch();
@@ -1749,7 +1748,13 @@ static int launch_k2(const Lat2 &o, cudaStream_t s) {
         cudaError_t e;
         static const bool no_warp = getenv("DOPE_NO_K2_WARP") != nullptr;
         if (!no_warp && lq <= 3 && quads <= 256)   // blocks <= 32 x 32: a warp per block
-            e = launch_pdl(k_consensus_warp<8>, dim3(grid(4)), dim3(256), 0, s, o, lq);
+        {
+            static const int wv = getenv("DOPE_K2W_VAR") ? atoi(getenv("DOPE_K2W_VAR")) : -1;
+            const int var = wv >= 0 ? wv : 0;   // 2 quads per batch at 4 CTAs/SM measured best (C5 b16, b32)
+            if (var == 0) e = launch_pdl(k_consensus_warp<8, 2, 4>, dim3(grid(4)), dim3(256), 0, s, o, lq);
+            else if (var == 1) e = launch_pdl(k_consensus_warp<8, 4, 3>, dim3(grid(3)), dim3(256), 0, s, o, lq);
+            else e = launch_pdl(k_consensus_warp<8, 8, 2>, dim3(grid(2)), dim3(256), 0, s, o, lq);
+        }
         else if (quads <= 4 * 32) e = launch_pdl(k_consensus_vec<32>, dim3(grid(32)), dim3(32), 0, s, o, lq);
         else if (quads <= 4 * 64) e = launch_pdl(k_consensus_vec<64>, dim3(grid(24)), dim3(64), 0, s, o, lq);
         else if (quads <= 4 * 256) e = launch_pdl(k_consensus_vec<256>, dim3(grid(8)), dim3(256), 0, s, o, lq);
