@@ -138,6 +138,14 @@ __global__ void __launch_bounds__(NT) k_block_mincut_g(LatG L, int sweep_min, in
     int32_t *gres = L.resid + (size_t)k * NDIR * M;
     const int64_t Wg = L.W;
 
+    // warm start: the copy's residual planes stream into shared memory first;
+    // the stored flow is read back through r(v->w) + r(w->v) = 2 cap(v,w)
+    if (L.warm) {
+        const int4 *src = reinterpret_cast<const int4 *>(gres);
+        int4 *dst = reinterpret_cast<int4 *>(rr);
+#pragma unroll 4
+        for (int i = tid; i < NDIR * M / 4; i += NT) dst[i] = src[i];
+    }
     for (int i = 0; i < NPT; ++i) {
         const int v = tid + i * NT;
         const int r = v / BW, c = v % BW;
@@ -149,7 +157,6 @@ __global__ void __launch_bounds__(NT) k_block_mincut_g(LatG L, int sweep_min, in
             double d, dhat;
             degrees(L, b, R, Cc, qi, d, dhat);
             double cy = (d / qi) * (1.0 - 1.0 / qi) * yi;
-            int32_t f = 0;
 #pragma unroll
             for (int dd = 0; dd < NDIR; ++dd) {
                 const double w = wpair(L, R, Cc, dd);
@@ -161,33 +168,40 @@ __global__ void __launch_bounds__(NT) k_block_mincut_g(LatG L, int sweep_min, in
                     const double qj = (double)L.q[Gn];
                     if (inb) {
                         cy += (-w / qi) * (1.0 - 1.0 / qj) * y[Gn];
-                        capd = (int32_t)rint(L.lam * (w / (qi * qj)) * L.qs);
+                        if (!L.warm) capd = (int32_t)rint(L.lam * (w / (qi * qj)) * L.qs);
                     } else {
                         cy += (-w / qi) * y[Gn];
                     }
                 }
-                if (L.warm) {
-                    if (inb) f += gres[dd * M + v] - capd;
-                } else {
-                    rr[dd * M + v] = capd;
-                }
+                if (!L.warm) rr[dd * M + v] = capd;
             }
             const double rdiag = d / (qi * qi) - dhat;
             const double lin = L.u[G] / qi + L.lam * (cy + rdiag * yi) + mu * ((ak[v] - yi) + 0.5);
             gv = (int32_t)fmax(fmin(rint(lin * L.qs), 1.0e9), -1.0e9);
-            if (L.warm) gv += f;
         } else if (!L.warm) {
 #pragma unroll
             for (int dd = 0; dd < NDIR; ++dd) rr[dd * M + v] = 0;
         }
         g[v] = gv;
     }
-    if (L.warm) {
-        const int4 *src = reinterpret_cast<const int4 *>(gres);
-        int4 *dst = reinterpret_cast<int4 *>(rr);
-        for (int i = tid; i < NDIR * M / 4; i += NT) dst[i] = src[i];
-    }
     __syncthreads();
+    if (L.warm) {
+        // arcs outside the copy's box (or of zero weight) hold 0 in both planes
+        for (int i = 0; i < NPT; ++i) {
+            const int v = tid + i * NT;
+            const int r = v / BW, c = v % BW;
+            if (!(r < b.hr && c < b.wc)) continue;
+            int32_t f2 = 0;
+#pragma unroll
+            for (int dd = 0; dd < NDIR; ++dd) {
+                const int rb = r + dy_of(dd), cb = c + dx_of(dd);
+                if (rb >= 0 && rb < b.hr && cb >= 0 && cb < b.wc)
+                    f2 += rr[dd * M + v] - rr[(dd ^ 1) * M + rb * BW + cb];
+            }
+            g[v] += f2 / 2;
+        }
+        __syncthreads();
+    }
     if (mincut_solve<BH, BW, NT, NDIR>(g, rr, h, masks, reach, misc, sweep_min, sweep_mul) < 0 && tid == 0)
         atomicCAS(&L.st->error, 0, k + 1);
     uint8_t *yk = L.yhat + (size_t)k * M;
