@@ -70,6 +70,14 @@ struct LatG {
 __device__ __forceinline__ int dy_of(int d) { return (d == 2 || d == 4 || d == 6) ? 1 : (d == 3 || d == 5 || d == 7) ? -1 : 0; }
 __device__ __forceinline__ int dx_of(int d) { return (d == 0 || d == 4 || d == 7) ? 1 : (d == 1 || d == 5 || d == 6) ? -1 : 0; }
 
+// x / q for a copy count (or a product of two); q = 2^k -- every box
+// partition of a 2D grid has q in {1, 2, 4} -- is an exact multiplication by
+// 2^-k, so the result is bit-identical to the division at a fraction of its cost
+__device__ __forceinline__ double qdiv(double x, int q) {
+    if ((q & (q - 1)) == 0) return x * __longlong_as_double((long long)(1023 - (31 - __clz(q))) << 52);
+    return x / (double)q;
+}
+
 // weight of the pair (G, G + off_d); 0 outside the grid
 __device__ __forceinline__ double wpair(const LatG &L, int R, int Cc, int d) {
     const int rn = R + dy_of(d), cn = Cc + dx_of(d);
@@ -101,7 +109,7 @@ __device__ __forceinline__ Box box_of(const LatG &L, int k) {
 
 // Per-copy stencil coefficients of pixel (R, C) inside box b:
 //   d = full degree, dhat = in-box scaled degree
-__device__ __forceinline__ void degrees(const LatG &L, const Box &b, int R, int Cc, double qi, double &d,
+__device__ __forceinline__ void degrees(const LatG &L, const Box &b, int R, int Cc, int qi, double &d,
                                         double &dhat) {
     d = 0.0;
     dhat = 0.0;
@@ -110,7 +118,7 @@ __device__ __forceinline__ void degrees(const LatG &L, const Box &b, int R, int 
         if (w == 0.0) continue;
         d += w;
         const int rn = R + dy_of(dd), cn = Cc + dx_of(dd);
-        if (b.holds(rn, cn)) dhat += w / (qi * (double)L.q[(int64_t)rn * L.W + cn]);
+        if (b.holds(rn, cn)) dhat += qdiv(w, qi * (int)L.q[(int64_t)rn * L.W + cn]);
     }
 }
 
@@ -153,10 +161,11 @@ __global__ void __launch_bounds__(NT) k_block_mincut_g(LatG L, int sweep_min, in
         if (r < b.hr && c < b.wc) {
             const int R = b.lo_r + r, Cc = b.lo_c + c;
             const int64_t G = (int64_t)R * Wg + Cc;
-            const double qi = (double)L.q[G], yi = y[G];
+            const int qi = L.q[G];
+            const double yi = y[G];
             double d, dhat;
             degrees(L, b, R, Cc, qi, d, dhat);
-            double cy = (d / qi) * (1.0 - 1.0 / qi) * yi;
+            double cy = qdiv(d, qi) * (1.0 - qdiv(1.0, qi)) * yi;
 #pragma unroll
             for (int dd = 0; dd < NDIR; ++dd) {
                 const double w = wpair(L, R, Cc, dd);
@@ -165,18 +174,18 @@ __global__ void __launch_bounds__(NT) k_block_mincut_g(LatG L, int sweep_min, in
                 int32_t capd = 0;
                 if (w != 0.0) {
                     const int64_t Gn = (int64_t)rn * Wg + cn;
-                    const double qj = (double)L.q[Gn];
+                    const int qj = L.q[Gn];
                     if (inb) {
-                        cy += (-w / qi) * (1.0 - 1.0 / qj) * y[Gn];
-                        if (!L.warm) capd = (int32_t)rint(L.lam * (w / (qi * qj)) * L.qs);
+                        cy += qdiv(-w, qi) * (1.0 - qdiv(1.0, qj)) * y[Gn];
+                        if (!L.warm) capd = (int32_t)rint(L.lam * qdiv(w, qi * qj) * L.qs);
                     } else {
-                        cy += (-w / qi) * y[Gn];
+                        cy += qdiv(-w, qi) * y[Gn];
                     }
                 }
                 if (!L.warm) rr[dd * M + v] = capd;
             }
-            const double rdiag = d / (qi * qi) - dhat;
-            const double lin = L.u[G] / qi + L.lam * (cy + rdiag * yi) + mu * ((ak[v] - yi) + 0.5);
+            const double rdiag = qdiv(d, qi * qi) - dhat;
+            const double lin = qdiv(L.u[G], qi) + L.lam * (cy + rdiag * yi) + mu * ((ak[v] - yi) + 0.5);
             gv = (int32_t)fmax(fmin(rint(lin * L.qs), 1.0e9), -1.0e9);
         } else if (!L.warm) {
 #pragma unroll
@@ -274,14 +283,15 @@ __global__ void __launch_bounds__(256) k_global_g(LatG L, int boxw, int M) {
     int clamped = 0;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
         const int R = (int)(p / L.W), Cc = (int)(p - (int64_t)R * L.W);
-        const double qp = (double)L.q[p];
+        const int qp = L.q[p];
         // the pixel's stencil, loaded once: weights and neighbour block counts
-        double wd[8], qd[8];
+        double wd[8];
+        int qd[8];
         double d = 0.0;
 #pragma unroll
         for (int dd = 0; dd < 8; ++dd) {
             wd[dd] = dd < L.ndir ? wpair(L, R, Cc, dd) : 0.0;
-            qd[dd] = wd[dd] != 0.0 ? (double)L.q[(int64_t)(R + dy_of(dd)) * L.W + Cc + dx_of(dd)] : 1.0;
+            qd[dd] = wd[dd] != 0.0 ? (int)L.q[(int64_t)(R + dy_of(dd)) * L.W + Cc + dx_of(dd)] : 1;
             d += wd[dd];
         }
         // candidate blocks: the base-range owner +-1 on each axis (boxes grow
@@ -310,20 +320,20 @@ __global__ void __launch_bounds__(256) k_global_g(LatG L, int boxw, int M) {
                     const int rn = R + dy_of(dd), cn = Cc + dx_of(dd);
                     if (!b.holds(rn, cn)) continue;
                     const double yi = yk[(rn - lr) * boxw + (cn - lc)];
-                    ct += inb ? (-wd[dd] / qd[dd]) * (1.0 - 1.0 / qp) * yi : (-wd[dd] / qd[dd]) * yi;
-                    dhat += wd[dd] / (qp * qd[dd]);
+                    ct += inb ? qdiv(-wd[dd], qd[dd]) * (1.0 - qdiv(1.0, qp)) * yi : qdiv(-wd[dd], qd[dd]) * yi;
+                    dhat += qdiv(wd[dd], qp * qd[dd]);
                 }
                 if (inb) {
                     const int v = (R - lr) * boxw + (Cc - lc);
                     const double yh = yk[v];
-                    const double rdiag = d / (qp * qp) - dhat;
+                    const double rdiag = qdiv(d, qp * qp) - dhat;
                     acc += mu * (yh + L.a[(size_t)k * M + v]) - L.lam * (rdiag * yh);
-                    ct += (d / qp) * (1.0 - 1.0 / qp) * yh;
+                    ct += qdiv(d, qp) * (1.0 - qdiv(1.0, qp)) * yh;
                 }
                 acc -= L.lam * ct;
             }
         }
-        double yv = acc / (mu * qp);
+        double yv = acc / (mu * (double)qp);
         clamped |= (yv < 0.0 || yv > 1.0);
         yv = yv < 0.0 ? 0.0 : (yv > 1.0 ? 1.0 : yv);
         yo[p] = yv;
