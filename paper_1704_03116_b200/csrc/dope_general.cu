@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+
+#include <type_traits>
 #include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
@@ -288,10 +290,12 @@ __global__ void __launch_bounds__(256) k_global_g(LatG L, int boxw, int M) {
         double wd[8];
         int qd[8];
         double d = 0.0;
+        bool pow2 = (qp & (qp - 1)) == 0;
 #pragma unroll
         for (int dd = 0; dd < 8; ++dd) {
             wd[dd] = dd < L.ndir ? wpair(L, R, Cc, dd) : 0.0;
             qd[dd] = wd[dd] != 0.0 ? (int)L.q[(int64_t)(R + dy_of(dd)) * L.W + Cc + dx_of(dd)] : 1;
+            pow2 &= (qd[dd] & (qd[dd] - 1)) == 0;
             d += wd[dd];
         }
         // candidate blocks: the base-range owner +-1 on each axis (boxes grow
@@ -301,38 +305,54 @@ __global__ void __launch_bounds__(256) k_global_g(LatG L, int boxw, int M) {
         by0 = by0 >= L.KY ? L.KY - 1 : by0;
         bx0 = bx0 >= L.KX ? L.KX - 1 : bx0;
         double acc = 0.0;
-        for (int by = by0 - 1; by <= by0 + 1; ++by) {
-            if (by < 0 || by >= L.KY) continue;
-            const int lr = L.rg[by], hr = L.rg[L.KY + by];
-            if (R < lr - 1 || R > lr + hr) continue;
-            for (int bx = bx0 - 1; bx <= bx0 + 1; ++bx) {
-                if (bx < 0 || bx >= L.KX) continue;
-                const int lc = L.rg[2 * L.KY + bx], wc = L.rg[2 * L.KY + L.KX + bx];
-                if (Cc < lc - 1 || Cc > lc + wc) continue;
-                const int k = by * L.KX + bx;
-                const Box b{lr, hr, lc, wc};
-                const uint8_t *yk = L.yhat + (size_t)k * M;
-                const bool inb = b.holds(R, Cc);
-                double ct = 0.0, dhat = 0.0;
+        // P2: every count here is a power of two -- the divisions become exact
+        // multiplications by per-pixel reciprocals (2^-k, exact in float too)
+        auto candidates = [&](auto P2) {
+            constexpr bool p2 = decltype(P2)::value;
+            float iq[8];
+            float iqp = 1.0f;
+            if (p2) {
+                iqp = 1.0f / (float)qp;
 #pragma unroll
-                for (int dd = 0; dd < 8; ++dd) {
-                    if (wd[dd] == 0.0) continue;
-                    const int rn = R + dy_of(dd), cn = Cc + dx_of(dd);
-                    if (!b.holds(rn, cn)) continue;
-                    const double yi = yk[(rn - lr) * boxw + (cn - lc)];
-                    ct += inb ? qdiv(-wd[dd], qd[dd]) * (1.0 - qdiv(1.0, qp)) * yi : qdiv(-wd[dd], qd[dd]) * yi;
-                    dhat += qdiv(wd[dd], qp * qd[dd]);
-                }
-                if (inb) {
-                    const int v = (R - lr) * boxw + (Cc - lc);
-                    const double yh = yk[v];
-                    const double rdiag = qdiv(d, qp * qp) - dhat;
-                    acc += mu * (yh + L.a[(size_t)k * M + v]) - L.lam * (rdiag * yh);
-                    ct += qdiv(d, qp) * (1.0 - qdiv(1.0, qp)) * yh;
-                }
-                acc -= L.lam * ct;
+                for (int dd = 0; dd < 8; ++dd) iq[dd] = 1.0f / (float)qd[dd];
             }
-        }
+            const double inq = p2 ? 1.0 - (double)iqp : 1.0 - qdiv(1.0, qp);
+            for (int by = by0 - 1; by <= by0 + 1; ++by) {
+                if (by < 0 || by >= L.KY) continue;
+                const int lr = L.rg[by], hr = L.rg[L.KY + by];
+                if (R < lr - 1 || R > lr + hr) continue;
+                for (int bx = bx0 - 1; bx <= bx0 + 1; ++bx) {
+                    if (bx < 0 || bx >= L.KX) continue;
+                    const int lc = L.rg[2 * L.KY + bx], wc = L.rg[2 * L.KY + L.KX + bx];
+                    if (Cc < lc - 1 || Cc > lc + wc) continue;
+                    const int k = by * L.KX + bx;
+                    const Box b{lr, hr, lc, wc};
+                    const uint8_t *yk = L.yhat + (size_t)k * M;
+                    const bool inb = b.holds(R, Cc);
+                    double ct = 0.0, dhat = 0.0;
+#pragma unroll
+                    for (int dd = 0; dd < 8; ++dd) {
+                        if (wd[dd] == 0.0) continue;
+                        const int rn = R + dy_of(dd), cn = Cc + dx_of(dd);
+                        if (!b.holds(rn, cn)) continue;
+                        const double yi = yk[(rn - lr) * boxw + (cn - lc)];
+                        const double wq = p2 ? -wd[dd] * (double)iq[dd] : qdiv(-wd[dd], qd[dd]);
+                        ct += inb ? wq * inq * yi : wq * yi;
+                        dhat += p2 ? wd[dd] * (double)(iqp * iq[dd]) : qdiv(wd[dd], qp * qd[dd]);
+                    }
+                    if (inb) {
+                        const int v = (R - lr) * boxw + (Cc - lc);
+                        const double yh = yk[v];
+                        const double rdiag = (p2 ? d * (double)(iqp * iqp) : qdiv(d, qp * qp)) - dhat;
+                        acc += mu * (yh + L.a[(size_t)k * M + v]) - L.lam * (rdiag * yh);
+                        ct += (p2 ? d * (double)iqp : qdiv(d, qp)) * inq * yh;
+                    }
+                    acc -= L.lam * ct;
+                }
+            }
+        };
+        if (pow2) candidates(std::true_type{});
+        else candidates(std::false_type{});
         double yv = acc / (mu * (double)qp);
         clamped |= (yv < 0.0 || yv > 1.0);
         yv = yv < 0.0 ? 0.0 : (yv > 1.0 ? 1.0 : yv);
