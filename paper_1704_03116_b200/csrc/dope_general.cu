@@ -165,18 +165,32 @@ __global__ void __launch_bounds__(NT) k_block_mincut_g(LatG L, int sweep_min, in
             const int64_t G = (int64_t)R * Wg + Cc;
             const int qi = L.q[G];
             const double yi = y[G];
-            double d, dhat;
-            degrees(L, b, R, Cc, qi, d, dhat);
+            // one pass over the stencil: weights and counts loaded once
+            double wv[NDIR];
+            int qv[NDIR];
+            double d = 0.0, dhat = 0.0;
+#pragma unroll
+            for (int dd = 0; dd < NDIR; ++dd) {
+                wv[dd] = wpair(L, R, Cc, dd);
+                qv[dd] = wv[dd] != 0.0 ? (int)L.q[(int64_t)(R + dy_of(dd)) * Wg + Cc + dx_of(dd)] : 1;
+            }
+            // degrees() in the same order: d over the stencil, dhat over the in-box part
+#pragma unroll
+            for (int dd = 0; dd < NDIR; ++dd) {
+                if (wv[dd] == 0.0) continue;
+                d += wv[dd];
+                if (b.holds(R + dy_of(dd), Cc + dx_of(dd))) dhat += qdiv(wv[dd], qi * qv[dd]);
+            }
             double cy = qdiv(d, qi) * (1.0 - qdiv(1.0, qi)) * yi;
 #pragma unroll
             for (int dd = 0; dd < NDIR; ++dd) {
-                const double w = wpair(L, R, Cc, dd);
+                const double w = wv[dd];
                 const int rn = R + dy_of(dd), cn = Cc + dx_of(dd);
                 const bool inb = w != 0.0 && b.holds(rn, cn);
                 int32_t capd = 0;
                 if (w != 0.0) {
                     const int64_t Gn = (int64_t)rn * Wg + cn;
-                    const int qj = L.q[Gn];
+                    const int qj = qv[dd];
                     if (inb) {
                         cy += qdiv(-w, qi) * (1.0 - qdiv(1.0, qj)) * y[Gn];
                         if (!L.warm) capd = (int32_t)rint(L.lam * qdiv(w, qi * qj) * L.qs);
