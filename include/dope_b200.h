@@ -322,6 +322,8 @@ typedef struct dope_general {
 } dope_general;
 
 int64_t dope_g_copy_stride(const dope_general *L);
+/* Row length of the padded per-copy box (copy_stride = rows * this). */
+int64_t dope_g_box_width(const dope_general *L);
 int64_t dope_g_partials(const dope_general *L);
 int dope_g_check(const dope_general *L);
 const char *dope_g_last_error(void);

@@ -254,7 +254,7 @@ def lib():
     lb.dope_gc_mincut.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_double,
                                   C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
     PG = C.POINTER(General)
-    for name in ("dope_g_copy_stride", "dope_g_partials"):
+    for name in ("dope_g_copy_stride", "dope_g_box_width", "dope_g_partials"):
         f = getattr(lb, name)
         f.restype = C.c_int64
         f.argtypes = [PG]

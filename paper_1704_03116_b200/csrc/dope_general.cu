@@ -542,8 +542,10 @@ static VarG make_varg() {
 
 static const VarG *pick_varg(int conn, int maxh, int maxw) {
     static const VarG table[] = {
-        make_varg<32, 32, 256, 4>(), make_varg<64, 64, 512, 4>(),
-        make_varg<32, 32, 256, 8>(), make_varg<64, 64, 512, 8>(),
+        // 40 x 48: the 32-blocks of a 25 %-overlap partition (boxes <= 40 x 40)
+        // without padding them to 64 x 64 (1920 nodes: 30 BFS words)
+        make_varg<32, 32, 256, 4>(), make_varg<40, 48, 384, 4>(), make_varg<64, 64, 512, 4>(),
+        make_varg<32, 32, 256, 8>(), make_varg<40, 48, 384, 8>(), make_varg<64, 64, 512, 8>(),
     };
     for (const VarG &v : table)
         if (v.ndir == conn && maxh <= v.bh && maxw <= v.bw) return &v;
@@ -653,6 +655,12 @@ int64_t dope_g_copy_stride(const dope_general *L) {
     if (!L) return 0;
     const VarG *v = pick_varg(L->conn, L->box[0], L->box[1]);
     return v ? (int64_t)v->bh * v->bw : 0;
+}
+
+int64_t dope_g_box_width(const dope_general *L) {
+    if (!L) return 0;
+    const VarG *v = pick_varg(L->conn, L->box[0], L->box[1]);
+    return v ? (int64_t)v->bw : 0;
 }
 
 int64_t dope_g_partials(const dope_general *L) {

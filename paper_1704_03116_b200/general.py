@@ -18,7 +18,6 @@ is required; there is no CPU path.
 from __future__ import annotations
 
 import ctypes as C
-import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -187,8 +186,7 @@ class GeneralDevice:
         return out
 
     def _box_w(self) -> int:
-        # variants are square boxes (32^2, 64^2)
-        return int(round(math.sqrt(self.stride)))
+        return int(_lib.lib().dope_g_box_width(C.byref(self.L)))
 
 
 def run_general(model: EnergyModel, partition: Partition, config, use_graph: bool = True):
