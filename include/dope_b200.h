@@ -114,19 +114,23 @@ typedef struct dope_lattice {
                                    current, best, and the next output         */
     uint8_t *yhat;              /* n   block labels (global layout)           */
     uint8_t *resid;             /* K * resid_stride bytes: residual graphs    */
-    uint32_t *dirty;            /* 2K (3D: 6K): [0, K) block needs a re-solve
+    uint32_t *dirty;            /* 9K: [0, K) block needs a re-solve
                                    (init 1); [K, 2K) iteration + 1 of the
-                                   block's last solve; 3D only: [2K, 5K) pass
-                                   + 1 at which y buffer b last received block
-                                   k's iterate, [5K, 6K) pass + 1 of the last
-                                   change of block k's iterate                  */
+                                   block's last solve; [2K, 5K) pass + 1 at
+                                   which y buffer b last received block k's
+                                   iterate, [5K, 6K) pass + 1 of the last
+                                   change of block k's iterate, [6K, 7K) pass
+                                   + 1 whose energy partial of block k is
+                                   current (clean-block consensus passes);
+                                   [7K, 8K) the blocks solved this iteration,
+                                   [8K, 9K) 1 + block k's slot in that list  */
     int64_t *part_energy;       /* K   per-block pair-energy partials          */
     int64_t *part_unary;        /* K   per-block change of sum u*y2           */
     int64_t *part_ressq;        /* K   per-block sum (yhat - y)^2             */
     int32_t *part_flags;        /* K   bit0: clamped                          */
     int64_t *part_cta;          /* DOPE_PART_CTA_LEN: pass-wide aggregates and
-                                   the block claim counter of the persistent
-                                   consensus pass (2D); zeroed by
+                                   the count of the iteration's solved-block
+                                   list (2D); zeroed by
                                    dope_admm_init                              */
     dope_run_state *state;      /* 1                                          */
     int64_t *trace_energy;      /* max_iters                                  */

@@ -296,8 +296,9 @@ class _DeviceState:
         self.agg = torch.zeros(4, dtype=torch.int64, device=dev)
         self.resid = torch.zeros(K * stride, dtype=u8, device=dev)
         # [0, K): re-solve flags; [K, 2K): iteration + 1 of each block's last solve;
-        # 3D also [2K, 6K): y-buffer stamps of the clean-block consensus pass
-        self.dirty = torch.zeros((6 if len(low.dims) == 3 else 2) * K, dtype=torch.int32, device=dev)
+        # [2K, 7K): y-buffer / iterate-change / energy-partial stamps of the
+        # clean-block consensus passes; [7K, 9K): the solved-block list and slots
+        self.dirty = torch.zeros(9 * K, dtype=torch.int32, device=dev)
         self.dirty[:K] = 1
         sstride = int(lb.dope_scratch_stride(C.byref(L)))
         self.scratch = torch.empty(max(K * sstride, 16), dtype=u8, device=dev)
@@ -492,6 +493,8 @@ def update_global(state: AdmmState, problems: BlockProblems, partition: Partitio
     _check_lam(problems, lam)
     dev = state._bind(problems, AdmmConfig())
     dev.call("dope_update_global", fuse=0)
+    # the step kernels do not keep the clean-block stamps: none holds any more
+    dev.dirty[2 * len(problems):].zero_()
     state.clamped_last = bool(dev.pf.any().item())
     return state
 

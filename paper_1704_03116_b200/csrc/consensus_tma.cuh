@@ -20,6 +20,8 @@
 
 struct TmaMaps {
     CUtensorMap a, y[3], yr[3], yhat;
+    CUtensorMap yrow[3];      // y2: one row of TW (ring-only tiles)
+    CUtensorMap h16;          // labels: 16 bytes of one row (ring-only corners)
     CUtensorMap hrow, hcol;   // labels: one row of TW, a 16-byte column of TH rows
     CUtensorMap arow, acol;   // multipliers: one row of TW, an 8-wide column of TH rows
 };
@@ -52,7 +54,6 @@ struct TmaCfg {
     static constexpr int O_H = (O_YR + B_YR + 127) / 128 * 128;
     static constexpr int STAGE = (O_H + B_H + 127) / 128 * 128;
     static constexpr int TX = B_A + B_Y + B_YR + B_H;
-    // clean tiles: neighbour labels in the (unused) multiplier area
     // clean tiles: neighbour labels and the ring multipliers (8-wide
     // columns at both edges, first / last row) in the unused multiplier area
     static constexpr int O_HUP = O_A, O_HDN = O_A + 128, O_HL = O_A + 256, O_HR = O_HL + 16 * TH;
@@ -60,6 +61,13 @@ struct TmaCfg {
     static constexpr int O_AT = O_AR + 16 * TH, O_AB = O_AT + 2 * TW;
     static_assert(O_AB + 2 * TW <= O_Y, "clean boxes fit the multiplier area");
     static constexpr int TX_CLEAN = B_Y + B_YR + 2 * TW + 2 * 16 * TH + 2 * 16 * TH + 2 * 2 * TW;
+    // ring-only tiles (clean block whose energy partial and output-buffer
+    // copy both still hold): the ring's own y2 (16-byte
+    // columns, rows) and the corner labels, in the (unused) y2 / label area
+    static constexpr int RW = (TW + 127) / 128 * 128;
+    static constexpr int O_YCL = O_Y, O_YCR = O_Y + 16 * TH, O_YRT = O_Y + 32 * TH, O_YRB = O_YRT + RW;
+    static constexpr int O_CRN = O_YRB + RW;              // 8 corner label slots of 128 bytes
+    static_assert(O_CRN + 8 * 128 <= STAGE, "ring boxes fit the y2 / label area");
     static constexpr int STAGES = STAGES_;
     static constexpr int SMEM = STAGES * STAGE + 128;
 };
@@ -132,6 +140,62 @@ __device__ __forceinline__ void tma_issue_tile(const Lat2 &L, const TmaMaps &M, 
     }
 }
 
+// Ring-only tile: only the data of the ring groups a re-solved neighbour can
+// move.  ld: sides whose ring quads are loaded (1 L, 2 R, 4 U, 8 D); crn:
+// corners whose labels across both sides are loaded (1 TL, 2 TR, 4 BL, 8 BR).
+template <int TW, int TH>
+__device__ __forceinline__ void tma_issue_ring(const Lat2 &L, const TmaMaps &M, uint8_t *stage,
+                                               uint64_t *bar, int by, int bx, int tile, int cur,
+                                               uint32_t ld, uint32_t crn) {
+    using C = TmaCfg<TW, TH, TW * TH / 4>;
+    const int x0 = bx * TW;
+    const int y0 = by * L.ay.base + tile * C::TH;
+    uint32_t tx = 0;
+    if (ld & 1u) tx += 48 * TH;
+    if (ld & 2u) tx += 48 * TH;
+    if (ld & 4u) tx += 4 * TW;
+    if (ld & 8u) tx += 4 * TW;
+    tx += 32u * (uint32_t)__popc(crn);
+    mbar_expect_tx(bar, tx);
+    if (ld & 1u) {
+        tma_load_2d(stage + C::O_HL, &M.hcol, bar, x0 - 16, y0 + 1);
+        tma_load_2d(stage + C::O_AL, &M.acol, bar, x0, y0);
+        tma_load_2d(stage + C::O_YCL, &M.yr[cur], bar, x0, y0 + 1);
+    }
+    if (ld & 2u) {
+        tma_load_2d(stage + C::O_HR, &M.hcol, bar, x0 + TW, y0 + 1);
+        tma_load_2d(stage + C::O_AR, &M.acol, bar, x0 + TW - 8, y0);
+        tma_load_2d(stage + C::O_YCR, &M.yr[cur], bar, x0 + TW - 16, y0 + 1);
+    }
+    if (ld & 4u) {
+        tma_load_2d(stage + C::O_HUP, &M.hrow, bar, x0, y0);
+        tma_load_2d(stage + C::O_AT, &M.arow, bar, x0, y0);
+        tma_load_2d(stage + C::O_YRT, &M.yrow[cur], bar, x0, y0 + 1);
+    }
+    if (ld & 8u) {
+        tma_load_2d(stage + C::O_HDN, &M.hrow, bar, x0, y0 + C::TH + 1);
+        tma_load_2d(stage + C::O_AB, &M.arow, bar, x0, y0 + C::TH - 1);
+        tma_load_2d(stage + C::O_YRB, &M.yrow[cur], bar, x0, y0 + C::TH);
+    }
+    // corner slots: [side label 16 B][label row across the top / bottom 16 B]
+    if (crn & 1u) {
+        tma_load_2d(stage + C::O_CRN + 0 * 128, &M.h16, bar, x0 - 16, y0 + 1);
+        tma_load_2d(stage + C::O_CRN + 1 * 128, &M.h16, bar, x0, y0);
+    }
+    if (crn & 2u) {
+        tma_load_2d(stage + C::O_CRN + 2 * 128, &M.h16, bar, x0 + TW, y0 + 1);
+        tma_load_2d(stage + C::O_CRN + 3 * 128, &M.h16, bar, x0 + TW - 16, y0);
+    }
+    if (crn & 4u) {
+        tma_load_2d(stage + C::O_CRN + 4 * 128, &M.h16, bar, x0 - 16, y0 + C::TH);
+        tma_load_2d(stage + C::O_CRN + 5 * 128, &M.h16, bar, x0, y0 + C::TH + 1);
+    }
+    if (crn & 8u) {
+        tma_load_2d(stage + C::O_CRN + 6 * 128, &M.h16, bar, x0 + TW, y0 + C::TH);
+        tma_load_2d(stage + C::O_CRN + 7 * 128, &M.h16, bar, x0 + TW - 16, y0 + C::TH + 1);
+    }
+}
+
 // 4 bytes (each 0 or 1) -> 4 bits
 __device__ __forceinline__ uint32_t bits_b01(uint32_t w) { return ((w * 0x01020408u) >> 24) & 0xFu; }
 // 4 bits -> 4 bytes (each 0 or 1)
@@ -169,7 +233,20 @@ struct StageInfo {
     int tile;       // tile index within the block
     int flags;      // bit0 re-solved this iteration, bit1 interior clamp memo, bit2 last tile,
                     // bits 3-6 neighbour across L / R / U / D re-solved this iteration,
-                    // bits 8-15 ring-group clamp memos (see ring_group)
+                    // bits 8-15 ring-group clamp memos (see ring_group),
+                    // bit16 ring-only tile, bits 17-20 its loaded sides (L R U D)
+    int pad_;
+    long long em;   // ring-only: the block's energy partial (it repeats)
+};
+
+// Per-block metadata the producer warp gathers for its next 32 blocks
+// (lane j: block j), so lane 0 never waits on these loads one block at a time.
+struct BlockMeta {
+    int k;
+    int flags;      // StageInfo flags bits 0-1, 3-6, 8-15
+    int mode;       // 0 full tile pass, 1 ring-only, 2 nothing to do (partials repeat)
+    int pad_;
+    long long em;
 };
 
 // Ring groups of a block's boundary quads (clamp memos, part_flags bits
@@ -198,13 +275,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // claims blocks, issues the TMA loads, and drains each finished block's
 // partials -- consumers never wait on a CTA-wide barrier, only on their
 // stage's "full" mbarrier; the producer waits on the stage's "empty" one.
-// Block scheduling is static round-robin by default (dyn = 0) or a
-// pass-wide claim counter (dyn = 1).  Every pass-wide aggregate is an exact
-// integer (the residual sum included, see rsq_excess), so results do not
-// depend on which CTA took a block.
+// Block scheduling is static round-robin (a pass-wide claim counter was
+// measured slower).  Every pass-wide aggregate is an exact integer (the
+// residual sum included, see rsq_excess), so results do not depend on which
+// CTA took a block.
 template <int TW, int TH_, int NT_, int STAGES_>
 __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 1)))
-    k_consensus_tma(Lat2 L, const __grid_constant__ TmaMaps M, uint32_t kx_magic, int dyn) {
+    k_consensus_tma(Lat2 L, const __grid_constant__ TmaMaps M, uint32_t kx_magic, int settle) {
     using C = TmaCfg<TW, TH_, NT_, STAGES_>;
     constexpr int TH = C::TH, NT = C::NT, QPT = C::QPT, QR = TW / 4, LQ = (TW == 64) ? 4 : 5;
     constexpr int ST = C::STAGES;
@@ -255,46 +332,27 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
 
     if (tid >= NT) {
         // ================= producer warp =================
-        if (tid != NT) return;
-        unsigned long long *work = reinterpret_cast<unsigned long long *>(&L.pc[6]);
-        constexpr int CA = 3;                          // blocks claimed ahead
-        int nk[CA] = {};
-        uint32_t nep[CA] = {};
-        int nmemo[CA] = {};
-        uint32_t nside[CA] = {};                       // neighbours re-solved (L R U D bits)
+        // All 32 lanes gather the metadata of the CTA's next 32 blocks (static
+        // round-robin assignment) and settle the blocks with nothing to do;
+        // lane 0 then issues the TMA loads and drains the finished stages.
+        const int plane = tid - NT;
+        __shared__ BlockMeta meta[32];
         const int KY = K / KX;
         const uint32_t ep_now = (uint32_t)(iter + 1);
-        // side bits of block kk: the neighbour's solve epoch is this iteration
-        // (a ghost row from another shard is always treated as moved)
-        auto sides_of = [&](int kk) -> uint32_t {
-            const int by = (int)__umulhi((uint32_t)kk, kx_magic), bx = kk - by * KX;
-            uint32_t sd = 0;
-            if (bx > 0 && L.dirty[K + kk - 1] == ep_now) sd |= 1u;
-            if (bx + 1 < KX && L.dirty[K + kk + 1] == ep_now) sd |= 2u;
-            if (by > 0 ? L.dirty[K + kk - KX] == ep_now : L.gup != 0) sd |= 4u;
-            if (by + 1 < KY ? L.dirty[K + kk + KX] == ep_now : L.gdn != 0) sd |= 8u;
-            return sd;
-        };
-        int nstatic = 0;
-        auto claim = [&]() -> int {
-            if (!dyn) return (int)blockIdx.x + (nstatic++) * (int)gridDim.x;
-            return (int)atomicAdd(work, 1ull);
-        };
-#pragma unroll
-        for (int i = 0; i < CA; ++i) nk[i] = (i == 0 || nk[i - 1] < K) ? claim() : K;
-#pragma unroll
-        for (int i = 0; i + 1 < CA; ++i)
-            if (nk[i] < K) {
-                nep[i] = L.dirty[K + nk[i]];
-                nmemo[i] = L.pf[nk[i]];
-                nside[i] = sides_of(nk[i]);
-            }
-        CtaAgg agg;   // this CTA's pass aggregates (exact integers)
+        // phase A: this iteration's solved blocks, dealt out evenly from K1's
+        // list (they carry the full tile work); phase B: every other block,
+        // static round-robin (clean blocks: mostly ring-only or settled)
+        const int G = (int)gridDim.x, bid = (int)blockIdx.x;
+        const int nsolved = L.skip_clean ? solved_count(L) : 0;
+        const int nA = bid < nsolved ? (nsolved - 1 - bid) / G + 1 : 0;
+        const int nmine = nA + (bid < K ? (K - 1 - bid) / G + 1 : 0);
+        CtaAgg agg;   // this CTA's pass aggregates (exact integers), lane 0
         auto drain = [&](int s) {
             const StageInfo info = sinfo[s];
             if (!(info.flags & 4)) return;
             const int k = info.k;
-            const int64_t e = (int64_t)L.lamw * accE[s];
+            const bool ring = (info.flags & 0x10000) != 0;
+            const int64_t e = ring ? (int64_t)info.em : (int64_t)L.lamw * accE[s];
             const int64_t u2 = (int64_t)accU[s];
             const int64_t sq = accS[s];
             const unsigned f = accF[s];
@@ -321,45 +379,132 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
             if (f & 8u) L.dirty[k + 1] = 1u;
             if ((f & 16u) && k - KX >= 0) L.dirty[k - KX] = 1u;
             if ((f & 32u) && k + KX < K) L.dirty[k + KX] = 1u;
+            // the output buffer now holds the block's whole iterate
+            ybuf_stamp(L, out)[k] = ep_now;
+            if (want_e) pe_stamp(L)[k] = ep_now;
+            if (f & 128u) ychg_stamp(L)[k] = ep_now;
         };
-        int pk = -1, ptile = tpb, pflags = 0;
-        int n = 0;
-        for (;; ++n) {
+        int n = 0;   // stages issued (lane 0)
+        for (int c0 = 0; c0 < nmine; c0 += 32) {
+            const int nc = nmine - c0 < 32 ? nmine - c0 : 32;
+            int64_t eskip = 0;
+            int fskip = 0, nskip = 0;
+            if (plane < nc) {
+                const int j = c0 + plane;
+                const int kk = j < nA ? (int)solved_list(L)[bid + j * G] : bid + (j - nA) * G;
+                const int by = (int)__umulhi((uint32_t)kk, kx_magic), bx = kk - by * KX;
+                const uint32_t epk = L.dirty[K + kk];
+                const int memo = L.pf[kk];
+                // neighbours re-solved this iteration (L R U D bits; a ghost
+                // row from another shard is always treated as moved)
+                uint32_t sd = 0;
+                if (bx > 0 && L.dirty[K + kk - 1] == ep_now) sd |= 1u;
+                if (bx + 1 < KX && L.dirty[K + kk + 1] == ep_now) sd |= 2u;
+                if (by > 0 ? L.dirty[K + kk - KX] == ep_now : L.gup != 0) sd |= 4u;
+                if (by + 1 < KY ? L.dirty[K + kk + KX] == ep_now : L.gdn != 0) sd |= 8u;
+                const bool solved = !L.skip_clean || epk == ep_now;
+                // mode 3: nothing here -- a phase-A entry that is not its
+                // block's latest slot, or a solved block phase A deals with
+                int mode = 0;
+                if (j < nA) {
+                    if (!solved || solved_slot(L)[kk] != (uint32_t)(bid + j * G) + 1u) mode = 3;
+                } else if (L.skip_clean && solved) {
+                    const uint32_t sl = solved_slot(L)[kk];
+                    if (sl >= 1u && sl <= (uint32_t)nsolved && solved_list(L)[sl - 1u] == (uint32_t)kk) mode = 3;
+                }
+                long long em = 0;
+                if (mode == 0 && !solved && iter >= 2 && settle) {
+                    // clean block: its energy partial still holds when it was
+                    // computed last pass and neither the block nor its right /
+                    // lower neighbour (the other ends of its pairs) moved then;
+                    // the output buffer already holds its iterate when it
+                    // received it after the block's last change.  Stamps
+                    // other CTAs may be writing this pass read as "moved".
+                    const uint32_t *ych = ychg_stamp(L);
+                    const uint32_t yk = ych[kk];
+                    bool ok = pe_stamp(L)[kk] == (uint32_t)iter && yk < (uint32_t)iter;
+                    ok = ok && (bx + 1 >= KX || ych[kk + 1] < (uint32_t)iter);
+                    ok = ok && (by + 1 < KY ? ych[kk + KX] < (uint32_t)iter : L.gdn == 0);
+                    const uint32_t so = ybuf_stamp(L, out)[kk];
+                    ok = ok && so != 0u && so >= yk;
+                    if (ok) {
+                        em = L.pe[kk];
+                        mode = sd ? 1 : 2;
+                    }
+                }
+                if (mode == 2) {
+                    // every quad is a fixed point: partials, flags and the
+                    // output buffer's copy all repeat
+                    L.pu[kk] = 0;
+                    L.pr[kk] = 0;
+                    ybuf_stamp(L, out)[kk] = ep_now;
+                    pe_stamp(L)[kk] = ep_now;
+                    eskip = em;
+                    fskip = memo & 1;
+                    nskip = 1;
+                }
+                meta[plane].k = kk;
+                meta[plane].flags = (solved ? 1 : 0) | ((memo & 64) ? 2 : 0) | (int)(sd << 3) | (memo & 0xFF00);
+                meta[plane].mode = mode;
+                meta[plane].em = em;
+            }
+            // fold the settled blocks into lane 0's aggregates
+            eskip = warp_sum(eskip);
+            fskip = __reduce_or_sync(FULLMASK, fskip);
+            nskip = __reduce_add_sync(FULLMASK, nskip);
+            __syncwarp();
+            if (plane == 0) {
+                if (nskip) {
+                    agg.E += eskip;
+                    agg.F |= fskip;
+                    agg.M = agg.M > 0 ? agg.M : 0;
+                }
+                for (int j = 0; j < nc; ++j) {
+                    const BlockMeta bm = meta[j];
+                    if (bm.mode >= 2) continue;
+                    const int by = (int)__umulhi((uint32_t)bm.k, kx_magic), bx = bm.k - by * KX;
+                    const bool hl = bx > 0, hr = bx + 1 < KX, hu = by > 0 || L.gup, hd = by + 1 < KY || L.gdn;
+                    const uint32_t sd = ((uint32_t)bm.flags >> 3) & 0xFu;
+                    for (int tile = 0; tile < tpb; ++tile) {
+                        const int s = n % ST;
+                        if (n >= ST) {
+                            mbar_wait(&empty[s], ((n / ST) - 1) & 1);
+                            drain(s);
+                        }
+                        int fl = bm.flags | (tile == tpb - 1 ? 4 : 0);
+                        uint8_t *stg = base + s * C::STAGE;
+                        sinfo[s].k = bm.k;
+                        sinfo[s].tile = tile;
+                        sinfo[s].em = bm.em;
+                        if (bm.mode == 1) {
+                            const bool tt = tile == 0, tb = tile == tpb - 1;
+                            const uint32_t ld = (sd & 3u) | (tt ? sd & 4u : 0u) | (tb ? sd & 8u : 0u);
+                            uint32_t crn = 0;
+                            if (tt && hu && hl && (sd & 5u)) crn |= 1u;
+                            if (tt && hu && hr && (sd & 6u)) crn |= 2u;
+                            if (tb && hd && hl && (sd & 9u)) crn |= 4u;
+                            if (tb && hd && hr && (sd & 10u)) crn |= 8u;
+                            sinfo[s].flags = fl | 0x10000 | (int)(ld << 17);
+                            tma_issue_ring<TW, TH>(L, M, stg, &full[s], by, bx, tile, cur, ld, crn);
+                        } else {
+                            sinfo[s].flags = fl;
+                            tma_issue_tile<TW, TH>(L, M, stg, &full[s], by, bx, tile, cur, fl & 1);
+                        }
+                        ++n;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        if (plane != 0) return;
+        {   // end marker
             const int s = n % ST;
             if (n >= ST) {
                 mbar_wait(&empty[s], ((n / ST) - 1) & 1);
                 drain(s);
             }
-            if (ptile == tpb) {   // next block
-                if (nk[0] >= K) {
-                    sinfo[s].k = -1;
-                    mbar_arrive(&full[s]);
-                    break;
-                }
-                pk = nk[0];
-                pflags = ((!L.skip_clean || nep[0] == (uint32_t)(iter + 1)) ? 1 : 0) | ((nmemo[0] & 64) ? 2 : 0) |
-                         (int)(nside[0] << 3) | (nmemo[0] & 0xFF00);
-                ptile = 0;
-#pragma unroll
-                for (int i = 0; i + 1 < CA; ++i) {
-                    nk[i] = nk[i + 1];
-                    nep[i] = nep[i + 1];
-                    nmemo[i] = nmemo[i + 1];
-                    nside[i] = nside[i + 1];
-                }
-                if (nk[CA - 2] < K) {   // claimed last time: its claim has returned
-                    nep[CA - 2] = L.dirty[K + nk[CA - 2]];
-                    nmemo[CA - 2] = L.pf[nk[CA - 2]];
-                    nside[CA - 2] = sides_of(nk[CA - 2]);
-                }
-                nk[CA - 1] = nk[CA - 2] < K ? claim() : K;
-            }
-            sinfo[s].k = pk;
-            sinfo[s].tile = ptile;
-            sinfo[s].flags = pflags | (ptile == tpb - 1 ? 4 : 0);
-            const int by = (int)__umulhi((uint32_t)pk, kx_magic), bx = pk - by * KX;
-            tma_issue_tile<TW, TH>(L, M, base + s * C::STAGE, &full[s], by, bx, ptile, cur, pflags & 1);
-            ++ptile;
+            sinfo[s].k = -1;
+            mbar_arrive(&full[s]);
         }
         // drain the stages still in flight when the end marker went out
         for (int m = (n - ST + 1 > 0 ? n - ST + 1 : 0); m < n; ++m) {
@@ -436,6 +581,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
                 const uint32_t yw = bytes_b01(yn) << 1;            // y2 bytes 0/2
                 const uint32_t chg = yw ^ yo;
                 fl |= (chg | (hb ^ yn)) ? 2u : 0u;
+                fl |= chg ? 128u : 0u;   // the block's iterate moved (ychg stamp)
                 __stcs(reinterpret_cast<uint2 *>(a_out + G), an);
                 __stcg(reinterpret_cast<unsigned int *>(y_out + G), yw);
                 if (chg) {
@@ -468,6 +614,65 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
                     if (lft) { cnt += 1u; nb += hrow[-1]; }
                     if (rgt) { cnt += 1u << 24; nb += (uint32_t)hrow[4] << 24; }
                     update(rr, c0, yo, h4, av, cnt, nb, lft, rgt, top, bot, ring_group(lft, rgt, top, bot));
+                }
+            } else if (info.flags & 0x10000) {
+                // ring-only tile: the output buffer already holds the block's
+                // iterate and its energy partial repeats, so only the ring
+                // groups on the sides whose neighbour was re-solved are
+                // recomputed, from the ring boxes the producer loaded
+                const bool tile_top = tile == 0 && has_up, tile_bot = tile == tpb - 1 && has_dn;
+                const uint32_t act = active_groups((uint32_t)(info.flags >> 3) & 0xFu);
+                const uint32_t ld = ((uint32_t)info.flags >> 17) & 0xFu;
+                const int nT = tile_top ? QR : 0, nB = tile_bot ? QR : 0;
+                const int rlo = tile_top ? 1 : 0, rhi = tile_bot ? TH - 1 : TH;
+                const int ncand = nT + nB + 2 * (rhi - rlo);
+                for (int i = tid; i < ncand; i += NT) {
+                    int rr, c0;
+                    if (i < nT) { rr = 0; c0 = 4 * i; }
+                    else if (i < nT + nB) { rr = TH - 1; c0 = 4 * (i - nT); }
+                    else { const int jj = i - nT - nB; rr = rlo + (jj >> 1); c0 = (jj & 1) ? TW - 4 : 0; }
+                    const bool lft = (c0 == 0) && has_lf, rgt = (c0 + 4 == TW) && has_rt;
+                    const bool top = rr == 0 && tile_top, bot = rr == TH - 1 && tile_bot;
+                    const int grp = ring_group(lft, rgt, top, bot);
+                    if (grp < 0 || !((act >> grp) & 1u)) continue;   // fixed point: already in the buffer
+                    uint32_t yo;
+                    uint2 av;
+                    if (lft && (ld & 1u)) {
+                        yo = *reinterpret_cast<const uint32_t *>(sb + C::O_YCL + rr * 16);
+                        av = *reinterpret_cast<const uint2 *>(sb + C::O_AL + rr * 16);
+                    } else if (rgt && (ld & 2u)) {
+                        yo = *reinterpret_cast<const uint32_t *>(sb + C::O_YCR + rr * 16 + 12);
+                        av = *reinterpret_cast<const uint2 *>(sb + C::O_AR + rr * 16 + 8);
+                    } else if (top) {
+                        yo = *reinterpret_cast<const uint32_t *>(sb + C::O_YRT + c0);
+                        av = *reinterpret_cast<const uint2 *>(sb + C::O_AT + 2 * c0);
+                    } else {
+                        yo = *reinterpret_cast<const uint32_t *>(sb + C::O_YRB + c0);
+                        av = *reinterpret_cast<const uint2 *>(sb + C::O_AB + 2 * c0);
+                    }
+                    const uint32_t h4 = yo >> 1;                   // own labels == y2 / 2
+                    uint32_t cnt = 0, nb = 0;
+                    if (top) {
+                        cnt += 0x01010101u;
+                        nb += lft ? *reinterpret_cast<const uint32_t *>(sb + C::O_CRN + 1 * 128)
+                                  : rgt ? *reinterpret_cast<const uint32_t *>(sb + C::O_CRN + 3 * 128 + 12)
+                                        : *reinterpret_cast<const uint32_t *>(sb + C::O_HUP + c0);
+                    }
+                    if (bot) {
+                        cnt += 0x01010101u;
+                        nb += lft ? *reinterpret_cast<const uint32_t *>(sb + C::O_CRN + 5 * 128)
+                                  : rgt ? *reinterpret_cast<const uint32_t *>(sb + C::O_CRN + 7 * 128 + 12)
+                                        : *reinterpret_cast<const uint32_t *>(sb + C::O_HDN + c0);
+                    }
+                    if (lft) {
+                        cnt += 1u;
+                        nb += top ? sb[C::O_CRN + 0 * 128 + 15] : bot ? sb[C::O_CRN + 4 * 128 + 15] : sb[C::O_HL + rr * 16 + 15];
+                    }
+                    if (rgt) {
+                        cnt += 1u << 24;
+                        nb += (uint32_t)(top ? sb[C::O_CRN + 2 * 128] : bot ? sb[C::O_CRN + 6 * 128] : sb[C::O_HR + rr * 16]) << 24;
+                    }
+                    update(rr, c0, yo, h4, av, cnt, nb, lft, rgt, top, bot, grp);
                 }
             } else {
                 // clean block: the interior is a fixed point, so the bulk pass

@@ -61,7 +61,7 @@ struct Lat2 {
     int64_t *pe, *pr, *pu;
     int32_t *pf;
     int64_t *pc;   // [0] E, [1] U, [2] M2 + 1 (max), [3] F (or), [4] sum ss, [5] sum rsq_excess,
-                   // [6] block claim counter of the persistent consensus pass
+                   // [6] count of the solved-block list (solved_list)
     dope_run_state *st;
     int64_t *tr_e;
     double *tr_rs, *tr_mr;
@@ -81,6 +81,16 @@ struct Lat2 {
     int32_t nib3;           // 3D: shared-memory K1 with nibble residual planes (lattice3d_smem.cuh)
     int32_t q3;             // 3D: u / a / y rows can be read as quads (W % 4 == 0, aligned)
 };
+
+// Append block k to the solved-block list (see solved_list); dirty[8K + k] =
+// 1 + the block's latest slot.
+__device__ __forceinline__ void solved_append(const Lat2 &L, int k) {
+    const uint32_t slot = (uint32_t)atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[6]), 1ull);
+    if (slot < (uint32_t)L.K) {
+        L.dirty[(size_t)7 * L.K + slot] = (uint32_t)k;
+        L.dirty[(size_t)8 * L.K + k] = slot + 1u;
+    }
+}
 
 // ---------------------------------------------------------------------------
 // K1: block min-cut (2D, 4-connected)
@@ -146,7 +156,9 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
     __syncthreads();
     if (tid == 0) {
         L.dirty[k] = 0;
-        L.dirty[L.K + k] = (uint32_t)L.st->iteration + 1u;   // solve epoch (consensus fast path)
+        const uint32_t ep = (uint32_t)L.st->iteration + 1u;
+        L.dirty[L.K + k] = ep;   // solve epoch (consensus fast path)
+        solved_append(L, k);
     }
 
     const int by = k / L.ax.k, bx = k % L.ax.k;
@@ -517,8 +529,8 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
             }
         }
     }
-    if (L.ndim == 3)   // solve epochs and the y-buffer stamps of the clean-block pass
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 5 * (int64_t)L.K; i += stride)
+    // solve epochs and the stamps of the clean-block consensus passes
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 6 * (int64_t)L.K; i += stride)
             L.dirty[L.K + i] = 0u;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.K; i += stride) {
         L.dirty[i] = 1u;
@@ -774,7 +786,7 @@ __device__ void pass_tail(const Lat2 &L, const CtaAgg &c, int cur, int best, int
         const int64_t E2 = __ldcg(&L.pc[0]), U2 = __ldcg(&L.pc[1]), M2 = __ldcg(&L.pc[2]) - 1;
         const int F2 = (int)__ldcg(&L.pc[3]);
         const double R2 = rsq_total(__ldcg(&L.pc[4]), __ldcg(&L.pc[5]));
-        for (int i = 0; i < 8; ++i) L.pc[i] = 0;   // incl. the claim counter
+        for (int i = 0; i < 8; ++i) L.pc[i] = 0;   // incl. the solved-list count
         finalize_apply(L, s0, E2, U2, R2, M2, F2, cur, best, out);
         st->done_ctas = 0;
     }
@@ -1320,6 +1332,29 @@ __global__ void k_energy4(Lat2 L, const int32_t *__restrict__ y2, int64_t n,
 }
 
 // ---------------------------------------------------------------------------
+// Stamps of the clean-block consensus passes (dirty[2K, 7K), zeroed by
+// init_state): [2K + b*K + k] = pass + 1 at which y buffer b last received
+// block k's whole iterate, [5K + k] = pass + 1 of the last pass that changed
+// block k's iterate, [6K + k] = pass + 1 of the last pass whose energy
+// partial pe[k] holds E(y_{pass-1}) over block k's pairs (2D TMA pass).
+__device__ __forceinline__ uint32_t *ybuf_stamp(const Lat2 &L, int b) { return L.dirty + (size_t)(2 + b) * L.K; }
+__device__ __forceinline__ uint32_t *ychg_stamp(const Lat2 &L) { return L.dirty + (size_t)5 * L.K; }
+__device__ __forceinline__ uint32_t *pe_stamp(const Lat2 &L) { return L.dirty + (size_t)6 * L.K; }
+
+// Blocks solved since the last consensus pass, for the next pass to deal out
+// evenly: dirty[7K, 8K) lists them, dirty[8K + k] = 1 + block k's latest
+// slot, pc[6] = their count (zeroed by pass_tail and init).  Slot i holds a
+// block for this pass iff i < count, list[i] = k, slot[k] = i + 1 and k's
+// solve epoch is this iteration; the pass deals those out and handles every
+// other solved block like any other block, so a stale list or count costs
+// balance, never results.
+__device__ __forceinline__ uint32_t *solved_list(const Lat2 &L) { return L.dirty + (size_t)7 * L.K; }
+__device__ __forceinline__ uint32_t *solved_slot(const Lat2 &L) { return L.dirty + (size_t)8 * L.K; }
+__device__ __forceinline__ int solved_count(const Lat2 &L) {
+    const unsigned long long v = __ldcg(reinterpret_cast<const unsigned long long *>(&L.pc[6]));
+    return v < (unsigned long long)L.K ? (int)v : L.K;
+}
+
 #include "consensus_tma.cuh"
 #include "lattice3d.cuh"
 #include "lattice3d_smem.cuh"
@@ -1658,7 +1693,9 @@ static int launch_k2_tma(const Lat2 &o, cudaStream_t s, int ctas_per_sm) {
     for (int i = 0; i < 3 && ok; ++i) {
         ok = make_map(&M.y[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.y2[i] - W, W, H + 2, TW, C::TH + 1);
         ok = ok && make_map(&M.yr[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.y2[i] - W, W, H + 2, 16, C::TH);
+        ok = ok && make_map(&M.yrow[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.y2[i] - W, W, H + 2, TW, 1);
     }
+    ok = ok && make_map(&M.h16, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.yhat - W, W, H + 2, 16, 1);
     ok = ok && make_map(&M.yhat, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.yhat - W, W, H + 2, C::YHW, C::TH + 2);
     ok = ok && make_map(&M.hrow, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.yhat - W, W, H + 2, TW, 1);
     ok = ok && make_map(&M.hcol, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.yhat - W, W, H + 2, 16, C::TH);
@@ -1671,9 +1708,10 @@ static int launch_k2_tma(const Lat2 &o, cudaStream_t s, int ctas_per_sm) {
     int grid = ctas_per_sm * sm_count();
     grid = o.K < grid ? o.K : grid;
     const uint32_t magic = (uint32_t)(((1ull << 32) + o.ax.k - 1) / o.ax.k);
-    static const int dyn = getenv("DOPE_K2_DYNAMIC") ? 1 : 0;
+    // DOPE_K2_SETTLE=0: no ring-only / settled clean blocks (A/B diagnostics)
+    static const int settle = getenv("DOPE_K2_SETTLE") ? atoi(getenv("DOPE_K2_SETTLE")) : 1;
     return cuda_check(launch_pdl(k_consensus_tma<TW, TH, NT, ST>, dim3(grid), dim3(C::NT + 32), (size_t)C::SMEM, s,
-                                 o, M, magic, dyn),
+                                 o, M, magic, settle),
                       "launch K2 (tma)");
 }
 

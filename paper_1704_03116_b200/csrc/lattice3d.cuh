@@ -247,12 +247,6 @@ __global__ void k_init_resid3d(Lat2 L, int boxd, int boxh, int boxw) {
     }
 }
 
-// y-buffer stamps of the 3D clean-block pass (dirty[2K, 6K), zeroed by
-// init_state): [2K + b*K + k] = pass + 1 at which buffer b last received
-// block k's iterate, [5K + k] = pass + 1 of the last pass that changed it.
-__device__ __forceinline__ uint32_t *ybuf_stamp(const Lat2 &L, int b) { return L.dirty + (size_t)(2 + b) * L.K; }
-__device__ __forceinline__ uint32_t *ychg_stamp(const Lat2 &L) { return L.dirty + (size_t)5 * L.K; }
-
 // Consensus for 3D (scalar, one CTA per sub-region).  Same semantics as
 // k_consensus: y_t into the free buffer, multipliers, residual partials,
 // energy partials of y_{t-1}, dirty marks for the block and its 6 face
