@@ -393,44 +393,50 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
                 const int j = c0 + plane;
                 const int kk = j < nA ? (int)solved_list(L)[bid + j * G] : bid + (j - nA) * G;
                 const int by = (int)__umulhi((uint32_t)kk, kx_magic), bx = kk - by * KX;
-                const uint32_t epk = L.dirty[K + kk];
-                const int memo = L.pf[kk];
+                // every load of this block's metadata in one independent
+                // round (neighbour indices clamped in range, results masked)
+                const int kl = bx > 0 ? kk - 1 : kk, kr = bx + 1 < KX ? kk + 1 : kk;
+                const int ku = by > 0 ? kk - KX : kk, kd = by + 1 < KY ? kk + KX : kk;
+                const uint32_t *ych = ychg_stamp(L);
+                const uint32_t epk = __ldcg(L.dirty + K + kk);
+                const int memo = __ldcg(L.pf + kk);
+                const uint32_t el = __ldcg(L.dirty + K + kl), er = __ldcg(L.dirty + K + kr);
+                const uint32_t eu = __ldcg(L.dirty + K + ku), ed = __ldcg(L.dirty + K + kd);
+                const uint32_t ps = __ldcg(pe_stamp(L) + kk), yk = __ldcg(ych + kk);
+                const uint32_t yr = __ldcg(ych + kr), yd = __ldcg(ych + kd);
+                const uint32_t so = __ldcg(ybuf_stamp(L, out) + kk);
+                const uint32_t sl = __ldcg(solved_slot(L) + kk);
+                const long long pek = __ldcg(reinterpret_cast<const long long *>(L.pe) + kk);
                 // neighbours re-solved this iteration (L R U D bits; a ghost
                 // row from another shard is always treated as moved)
                 uint32_t sd = 0;
-                if (bx > 0 && L.dirty[K + kk - 1] == ep_now) sd |= 1u;
-                if (bx + 1 < KX && L.dirty[K + kk + 1] == ep_now) sd |= 2u;
-                if (by > 0 ? L.dirty[K + kk - KX] == ep_now : L.gup != 0) sd |= 4u;
-                if (by + 1 < KY ? L.dirty[K + kk + KX] == ep_now : L.gdn != 0) sd |= 8u;
+                if (bx > 0 && el == ep_now) sd |= 1u;
+                if (bx + 1 < KX && er == ep_now) sd |= 2u;
+                if (by > 0 ? eu == ep_now : L.gup != 0) sd |= 4u;
+                if (by + 1 < KY ? ed == ep_now : L.gdn != 0) sd |= 8u;
                 const bool solved = !L.skip_clean || epk == ep_now;
                 // mode 3: nothing here -- a phase-A entry that is not its
                 // block's latest slot, or a solved block phase A deals with
                 int mode = 0;
                 if (j < nA) {
-                    if (!solved || solved_slot(L)[kk] != (uint32_t)(bid + j * G) + 1u) mode = 3;
+                    if (!solved || sl != (uint32_t)(bid + j * G) + 1u) mode = 3;
                 } else if (L.skip_clean && solved) {
-                    const uint32_t sl = solved_slot(L)[kk];
-                    if (sl >= 1u && sl <= (uint32_t)nsolved && solved_list(L)[sl - 1u] == (uint32_t)kk) mode = 3;
+                    if (sl >= 1u && sl <= (uint32_t)nsolved && __ldcg(solved_list(L) + sl - 1u) == (uint32_t)kk) mode = 3;
                 }
                 long long em = 0;
-                if (mode == 0 && !solved && iter >= 2 && settle) {
-                    // clean block: its energy partial still holds when it was
-                    // computed last pass and neither the block nor its right /
-                    // lower neighbour (the other ends of its pairs) moved then;
-                    // the output buffer already holds its iterate when it
-                    // received it after the block's last change.  Stamps
-                    // other CTAs may be writing this pass read as "moved".
-                    const uint32_t *ych = ychg_stamp(L);
-                    const uint32_t yk = ych[kk];
-                    bool ok = pe_stamp(L)[kk] == (uint32_t)iter && yk < (uint32_t)iter;
-                    ok = ok && (bx + 1 >= KX || ych[kk + 1] < (uint32_t)iter);
-                    ok = ok && (by + 1 < KY ? ych[kk + KX] < (uint32_t)iter : L.gdn == 0);
-                    const uint32_t so = ybuf_stamp(L, out)[kk];
-                    ok = ok && so != 0u && so >= yk;
-                    if (ok) {
-                        em = L.pe[kk];
-                        mode = sd ? 1 : 2;
-                    }
+                // clean block: its energy partial still holds when it was
+                // computed last pass and neither the block nor its right /
+                // lower neighbour (the other ends of its pairs) moved then;
+                // the output buffer already holds its iterate when it received
+                // it after the block's last change.  Stamps other CTAs may be
+                // writing this pass read as "moved".
+                const uint32_t it32 = (uint32_t)iter;
+                const bool ok = mode == 0 && !solved && iter >= 2 && settle && ps == it32 && yk < it32 &&
+                                (bx + 1 >= KX || yr < it32) && (by + 1 < KY ? yd < it32 : L.gdn == 0) &&
+                                so != 0u && so >= yk;
+                if (ok) {
+                    em = pek;
+                    mode = sd ? 1 : 2;
                 }
                 if (mode == 2) {
                     // every quad is a fixed point: partials, flags and the
@@ -453,6 +459,11 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
             fskip = __reduce_or_sync(FULLMASK, fskip);
             nskip = __reduce_add_sync(FULLMASK, nskip);
             __syncwarp();
+            if (plane == 0 && c0 == 0 && L.timeline) {   // diagnostics: metadata gathered (slot 0)
+                uint64_t t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                L.timeline[8 * blockIdx.x + 0] = (int64_t)t;
+            }
             if (plane == 0) {
                 if (nskip) {
                     agg.E += eskip;
@@ -497,6 +508,13 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
             __syncwarp();
         }
         if (plane != 0) return;
+        if (L.timeline) {   // diagnostics: last stage issued (slot 1), stages (slot 4), phase-A blocks (slot 5)
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            L.timeline[8 * blockIdx.x + 1] = (int64_t)t;
+            L.timeline[8 * blockIdx.x + 4] = n;
+            L.timeline[8 * blockIdx.x + 5] = nA;
+        }
         {   // end marker
             const int s = n % ST;
             if (n >= ST) {
@@ -516,6 +534,11 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             L.timeline[8 * blockIdx.x + 7] = (int64_t)t;
+        }
+        if (L.timeline) {   // diagnostics: stages drained (slot 2)
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            L.timeline[8 * blockIdx.x + 2] = (int64_t)t;
         }
         pass_tail(L, agg, cur, best, out);
         return;

@@ -45,6 +45,15 @@ def main():
         print(f"it {it+1:3d}: K2 {e1.elapsed_time(e2)*1e3:6.1f} us | ctas {len(st)} start spread "
               f"{(st.max()-t0)/1e3:5.1f} us | end min {(en.min()-t0)/1e3:5.1f} med {(np.median(en)-t0)/1e3:5.1f} "
               f"max {(en.max()-t0)/1e3:5.1f} us | finalize end {(fin-t0)/1e3 if fin else float('nan'):5.1f} us")
+        if it == iters - 1 and (t[: len(st), 0] > 0).any():
+            # per-CTA detail (TMA pass slots: 0 metadata, 1 last issue, 4 stages, 5 phase-A blocks)
+            c = t[: len(st)]
+            meta = (c[:, 0] - c[:, 6]) / 1e3
+            print(f"  metadata gathered after: med {np.median(meta):.1f} max {meta.max():.1f} us")
+            for nst in sorted(set(c[:, 4].tolist())):
+                m = c[:, 4] == nst
+                print(f"  {int(m.sum()):4d} CTAs with {nst:2d} stages: end med {(np.median(c[m, 7]) - t0)/1e3:5.1f} "
+                      f"max {(c[m, 7].max() - t0)/1e3:5.1f} us, phase-A blocks {np.bincount(c[m, 5]).tolist()}")
     dev.raise_on_error()
 
 
