@@ -267,6 +267,16 @@ __device__ __forceinline__ uint32_t active_groups(uint32_t sides) {
     return L | (R << 1) | (U << 2) | (D << 3) | ((L | U) << 4) | ((R | U) << 5) | ((L | D) << 6) | ((R | D) << 7);
 }
 
+// diagnostics (timeline mode, K >= 4 * CTAs): per CTA and stage n < 8,
+// [issue, data arrived (warp 0), consumed (warp 0)] globaltimer stamps after
+// the 8 per-CTA slots
+__device__ __forceinline__ void stage_stamp(const Lat2 &L, int n, int which) {
+    if (!L.timeline || n >= 8 || L.K < 4 * (int)gridDim.x) return;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    L.timeline[8 * gridDim.x + (blockIdx.x * 8 + n) * 3 + which] = (int64_t)t;
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -496,9 +506,11 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
                             if (tb && hd && hl && (sd & 9u)) crn |= 4u;
                             if (tb && hd && hr && (sd & 10u)) crn |= 8u;
                             sinfo[s].flags = fl | 0x10000 | (int)(ld << 17);
+                            stage_stamp(L, n, 0);
                             tma_issue_ring<TW, TH>(L, M, stg, &full[s], by, bx, tile, cur, ld, crn);
                         } else {
                             sinfo[s].flags = fl;
+                            stage_stamp(L, n, 0);
                             tma_issue_tile<TW, TH>(L, M, stg, &full[s], by, bx, tile, cur, fl & 1);
                         }
                         ++n;
@@ -560,6 +572,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
     for (int n = 0;; ++n) {
         const int s = n % ST;
         mbar_wait(&full[s], (n / ST) & 1);
+        if (tid == 0) stage_stamp(L, n, 1);
         const StageInfo info = sinfo[s];
         if (info.k < 0) break;
         const int k = info.k, tile = info.tile;
@@ -591,6 +604,14 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
             };
             // consensus update of one quad given its multipliers, own labels
             // and cross-block neighbour labels (count / sum per pixel)
+            // running unary term u * (y2_new - y2_old) of one quad
+            auto unary = [&](int64_t G, uint32_t yw, uint32_t yo) {
+                const int4 uv = __ldg(reinterpret_cast<const int4 *>(L.u + G));
+                du += (int64_t)uv.x * ((int)(yw & 0xFFu) - (int)(yo & 0xFFu)) +
+                      (int64_t)uv.y * ((int)((yw >> 8) & 0xFFu) - (int)((yo >> 8) & 0xFFu)) +
+                      (int64_t)uv.z * ((int)((yw >> 16) & 0xFFu) - (int)((yo >> 16) & 0xFFu)) +
+                      (int64_t)uv.w * ((int)(yw >> 24) - (int)(yo >> 24));
+            };
             auto update = [&](int rr, int c0, uint32_t yo, uint32_t h4, uint2 av, uint32_t cnt, uint32_t nb,
                               bool lft, bool rgt, bool top, bool bot, int grp) {
                 const int64_t G = gt + (int64_t)rr * W + c0;
@@ -608,12 +629,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
                 __stcs(reinterpret_cast<uint2 *>(a_out + G), an);
                 __stcg(reinterpret_cast<unsigned int *>(y_out + G), yw);
                 if (chg) {
-                    // running unary term u * (y2_new - y2_old) where y moved
-                    const int4 uv = __ldg(reinterpret_cast<const int4 *>(L.u + G));
-                    du += (int64_t)uv.x * ((int)(yw & 0xFFu) - (int)(yo & 0xFFu)) +
-                          (int64_t)uv.y * ((int)((yw >> 8) & 0xFFu) - (int)((yo >> 8) & 0xFFu)) +
-                          (int64_t)uv.z * ((int)((yw >> 16) & 0xFFu) - (int)((yo >> 16) & 0xFFu)) +
-                          (int64_t)uv.w * ((int)(yw >> 24) - (int)(yo >> 24));
+                    unary(G, yw, yo);   // only where y moved
                     const uint32_t em = (lft ? 4u : 0u) | (rgt ? 8u : 0u) | (top ? 16u : 0u) | (bot ? 32u : 0u);
                     const uint32_t mk = 0x30u | ((chg & 0xFFu) ? 4u : 0u) | ((chg >> 24) ? 8u : 0u);
                     fl |= em & mk;
@@ -638,6 +654,8 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
                     if (rgt) { cnt += 1u << 24; nb += (uint32_t)hrow[4] << 24; }
                     update(rr, c0, yo, h4, av, cnt, nb, lft, rgt, top, bot, ring_group(lft, rgt, top, bot));
                 }
+                // the unary term of the quads whose y moved: their u loads
+                // all in flight together instead of one latency per quad
             } else if (info.flags & 0x10000) {
                 // ring-only tile: the output buffer already holds the block's
                 // iterate and its energy partial repeats, so only the ring
@@ -802,6 +820,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
         }
         // this warp is done with stage s
         __syncwarp();
+        if (tid == 0) stage_stamp(L, n, 2);
         if (lane == 0) mbar_arrive(&empty[s]);
     }
 }
