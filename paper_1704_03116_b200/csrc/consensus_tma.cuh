@@ -267,14 +267,15 @@ __device__ __forceinline__ uint32_t active_groups(uint32_t sides) {
     return L | (R << 1) | (U << 2) | (D << 3) | ((L | U) << 4) | ((R | U) << 5) | ((L | D) << 6) | ((R | D) << 7);
 }
 
-// diagnostics (timeline mode, K >= 4 * CTAs): per CTA and stage n < 8,
-// [issue, data arrived (warp 0), consumed (warp 0)] globaltimer stamps after
+// diagnostics (timeline mode, K >= 5 * CTAs): per CTA and stage n < 8,
+// [issue, data arrived (warp 0), consumed (warp 0), tile loop done (warp 0)]
+// globaltimer stamps after
 // the 8 per-CTA slots
 __device__ __forceinline__ void stage_stamp(const Lat2 &L, int n, int which) {
-    if (!L.timeline || n >= 8 || L.K < 4 * (int)gridDim.x) return;
+    if (!L.timeline || n >= 8 || L.K < 5 * (int)gridDim.x) return;
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    L.timeline[8 * gridDim.x + (blockIdx.x * 8 + n) * 3 + which] = (int64_t)t;
+    L.timeline[8 * gridDim.x + (blockIdx.x * 8 + n) * 4 + which] = (int64_t)t;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -798,6 +799,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
                 }
             }
         }
+        if (tid == 0) stage_stamp(L, n, 3);
         if (info.flags & 4) {
             // block done in this warp: one shared atomic per quantity
             const unsigned e = __reduce_add_sync(FULLMASK, (unsigned)quad_acc);

@@ -56,13 +56,13 @@ def main():
                 print(f"  {int(m.sum()):4d} CTAs with {nst:2d} stages: end med {(np.median(c[m, 7]) - t0)/1e3:5.1f} "
                       f"max {(c[m, 7].max() - t0)/1e3:5.1f} us, phase-A blocks {np.bincount(c[m, 5]).tolist()}")
             G = len(st)
-            sg = tl.cpu().numpy()[8 * G: 8 * G + 24 * G].reshape(G, 8, 3)
+            sg = tl.cpu().numpy()[8 * G: 8 * G + 32 * G].reshape(G, 8, 4)
             for b in np.argsort(c[:, 7])[-3:].tolist() + [int(np.argsort(c[:, 7])[G // 2])]:
                 ns = int(c[b, 4])
-                rows = [f"({(sg[b, i, 0] - t0)/1e3:.1f},{(sg[b, i, 1] - t0)/1e3:.1f},{(sg[b, i, 2] - t0)/1e3:.1f})"
+                rows = [f"({(sg[b, i, 0] - t0)/1e3:.1f},{(sg[b, i, 1] - t0)/1e3:.1f},{(sg[b, i, 3] - t0)/1e3:.1f},{(sg[b, i, 2] - t0)/1e3:.1f})"
                         for i in range(min(ns, 8))]
                 print(f"  CTA {b}: start {(c[b, 6] - t0)/1e3:.1f} meta {(c[b, 0] - t0)/1e3:.1f} stages "
-                      f"[issue,data,done] {' '.join(rows)} drained {(c[b, 2] - t0)/1e3:.1f} end {(c[b, 7] - t0)/1e3:.1f}")
+                      f"[issue,data,loop,done] {' '.join(rows)} drained {(c[b, 2] - t0)/1e3:.1f} end {(c[b, 7] - t0)/1e3:.1f}")
     dev.raise_on_error()
 
 
