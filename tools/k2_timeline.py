@@ -56,6 +56,8 @@ def main():
                 print(f"  {int(m.sum()):4d} CTAs with {nst:2d} stages: end med {(np.median(c[m, 7]) - t0)/1e3:5.1f} "
                       f"max {(c[m, 7].max() - t0)/1e3:5.1f} us, phase-A blocks {np.bincount(c[m, 5]).tolist()}")
             G = len(st)
+            if K < 5 * G:   # no room for the per-stage stamps
+                continue
             sg = tl.cpu().numpy()[8 * G: 8 * G + 32 * G].reshape(G, 8, 4)
             for b in np.argsort(c[:, 7])[-3:].tolist() + [int(np.argsort(c[:, 7])[G // 2])]:
                 ns = int(c[b, 4])
