@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
         const int G = (int)gridDim.x, bid = (int)blockIdx.x;
         // (a CTA with at most two blocks has nothing to balance: skip phase A
         // and the dependent list read it costs)
-        const int nsolved = (L.skip_clean && K > 2 * G) ? solved_count(L) : 0;
+        const int nsolved = (L.skip_clean && L.slist && K > 2 * G) ? solved_count(L) : 0;
         const int nA = bid < nsolved ? (nsolved - 1 - bid) / G + 1 : 0;
         const int nmine = nA + (bid < K ? (K - 1 - bid) / G + 1 : 0);
         CtaAgg agg;   // this CTA's pass aggregates (exact integers), lane 0

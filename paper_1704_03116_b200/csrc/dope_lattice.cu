@@ -80,6 +80,7 @@ struct Lat2 {
     int32_t pdl;            // launched with programmatic dependent launch (DOPE_PDL=1)
     int32_t nib3;           // 3D: shared-memory K1 with nibble residual planes (lattice3d_smem.cuh)
     int32_t q3;             // 3D: u / a / y rows can be read as quads (W % 4 == 0, aligned)
+    int32_t slist;          // K1 lists its solved blocks for the TMA consensus pass (solved_list)
 };
 
 // Append block k to the solved-block list (see solved_list); dirty[8K + k] =
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
         L.dirty[k] = 0;
         const uint32_t ep = (uint32_t)L.st->iteration + 1u;
         L.dirty[L.K + k] = ep;   // solve epoch (consensus fast path)
-        solved_append(L, k);
+        if (L.slist) solved_append(L, k);
     }
 
     const int by = k / L.ax.k, bx = k % L.ax.k;
@@ -1407,6 +1408,10 @@ static const Variant3 *pick_variant3(int maxd, int maxh, int maxw) {
     return nullptr;
 }
 
+static int k2_tma_width(const Lat2 &o);
+static int sm_count();
+constexpr int K2_CPS_FWD = 4;
+
 static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
                       const Variant3 **var3 = nullptr) {
     if (!L || !L->u || !L->a || !L->y2[0] || !L->y2[1] || !L->y2[2] || !L->yhat || !L->resid ||
@@ -1500,6 +1505,9 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
                          ((uintptr_t)o.a >> 1) | ((uintptr_t)o.u >> 2);
     o.pdl = getenv("DOPE_PDL") != nullptr;
     o.vec4 = !is3 && (o.W % 4 == 0) && (o.ax.rem == 0) && (o.ax.base % 4 == 0) && (al % 4 == 0);
+    // the TMA consensus pass deals out the solved blocks when its CTAs hold
+    // more than two blocks each
+    o.slist = k2_tma_width(o) != 0 && o.K > 2 * K2_CPS_FWD * sm_count();
     o.q3 = is3 && (o.W % 4 == 0) && (al % 4 == 0);
     // 32^3 boxes with 2*cap <= 15 run the shared-memory K1 (nibble residuals);
     // DOPE_K1_3D=l2 forces the HBM-scratch kernel (diagnostics)
@@ -1710,13 +1718,15 @@ static int launch_k2_tma(const Lat2 &o, cudaStream_t s, int ctas_per_sm) {
     const uint32_t magic = (uint32_t)(((1ull << 32) + o.ax.k - 1) / o.ax.k);
     // DOPE_K2_SETTLE=0: no ring-only / settled clean blocks (A/B diagnostics)
     static const int settle = getenv("DOPE_K2_SETTLE") ? atoi(getenv("DOPE_K2_SETTLE")) : 1;
+    // (measured: with at most two blocks per CTA the settled / ring-only
+    // modes do not pay for their metadata -- C5 b64 / b128)
     return cuda_check(launch_pdl(k_consensus_tma<TW, TH, NT, ST>, dim3(grid), dim3(C::NT + 32), (size_t)C::SMEM, s,
-                                 o, M, magic, settle),
+                                 o, M, magic, settle && o.K > 2 * grid ? 1 : 0),
                       "launch K2 (tma)");
 }
 
 // measured on C3 (tools/k2_variants.sh)
-constexpr int K2_TH = 64, K2_NT = 128, K2_STAGES = 2, K2_CPS = 4;
+constexpr int K2_TH = 64, K2_NT = 128, K2_STAGES = 2, K2_CPS = K2_CPS_FWD;
 
 static int k2_tma_width(const Lat2 &o) {
     // eligible: run-loop mode, uniform tiling, 64/128-wide blocks, TMA-friendly strides
