@@ -121,8 +121,11 @@ def test_bk_maxflow_reference_known_answers():
     assert flow == 0.0 and len(set(labels.tolist())) == 1
 
 
-@pytest.mark.parametrize("size,block,iters", [(1024, 64, 8), (512, 32, 8), (512, 128, 6)])
+@pytest.mark.parametrize("size,block,iters", [(1024, 64, 8), (512, 32, 8), (512, 128, 6),
+                                               (2560, 64, 10)])
 def test_larger_grids_match_oracle(size, block, iters):
+    """(2560, 64): 1600 blocks, more than two per consensus CTA, so the TMA pass
+    deals out K1's solved-block list and takes its settled / ring-only paths."""
     import oracle as orc
     wl = W.disks_workload(f"t{size}", size, 16, block, 2, iters, rmin=10, rmax=150, seed=11)
     rows, cols, vals = wl.pair_arrays()
@@ -152,10 +155,11 @@ def _c3_model():
 
 
 def test_c3_full_size_first_iterations_match_oracle():
-    """BASELINE's 4096^2 grid at full size: first 3 iterations bit-exact vs the oracle."""
+    """BASELINE's 4096^2 grid at full size: first 6 iterations bit-exact vs the oracle
+    (from the third on, the consensus pass settles clean blocks from its stamps)."""
     import oracle as orc
     wl, model, part = _c3_model()
-    iters = 3
+    iters = 6
     cfg = dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=iters)
     labels, state = dope.run(model, part, cfg)
     spec = orc.LatticeSpec(wl.dims, wl.kpa, wl.offsets, [1.0, 1.0], wl.u.astype(np.float64), wl.lam)
@@ -177,6 +181,12 @@ def test_c3_full_run_properties():
                                                          skip_clean=False, warm_start=False))
     assert np.array_equal(labels1, labels2)
     assert [t.energy for t in s1.trace] == [t.energy for t in s2.trace]
+    assert [t.max_block_residual for t in s1.trace] == [t.max_block_residual for t in s2.trace]
+    assert np.allclose([t.residual_sq for t in s1.trace], [t.residual_sq for t in s2.trace], rtol=1e-12, atol=0)
+    assert [t.clamped for t in s1.trace] == [t.clamped for t in s2.trace]
+    assert np.array_equal(s1.y, s2.y)
+    assert np.array_equal(s1.labels_global(), s2.labels_global())
+    assert np.array_equal(s1.multipliers_global(), s2.multipliers_global())
     e = [t.energy for t in s1.trace]
     assert s1.best_iteration == int(np.argmin(e)) + 1
     # the returned state.y is the best iterate (binary on the int path): its energy is the min
