@@ -141,7 +141,9 @@ typedef struct dope_lattice {
                                    the last K1 launch (2D): globaltimer stamps,
                                    rounds, sweeps (diagnostics only)          */
     uint8_t *scratch;           /* 3D only: K * dope_scratch_stride bytes of
-                                   per-sub-region node state (may be NULL in 2D) */
+                                   per-sub-region node state and the int8 u
+                                   bricks dope_admm_init fills (may be NULL in
+                                   2D)                                          */
     /* Sharding: this lattice is a slab of whole block rows (2D) or whole
      * block planes (3D, along the depth axis) of a larger grid.  y2[i] and
      * yhat must then point one row (2D) / one plane (3D) INTO allocations

@@ -47,6 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
            f"-I{ROOT / 'include'}", f"-I{CSRC}", "-o", str(LIB)]
     if verbose:
         cmd += ["-Xptxas", "-v"]
+    cmd += os.environ.get("DOPE_NVCC_EXTRA", "").split()   # diagnostics builds (e.g. -DK1S_DIAG)
     cmd += [str(s) for s in sources()]
     subprocess.run(cmd, check=True)
     return LIB

@@ -1853,9 +1853,11 @@ int64_t dope_resid_stride(const dope_lattice *L) {
 
 int64_t dope_scratch_stride(const dope_lattice *L) {
     // 3D: excess (int32) + heights (uint16) per box node, 6 bytes (the
-    // residual planes' 6 bytes give the same figure); 2D keeps them in SMEM
+    // residual planes' 6 bytes give the same figure), then the int8 u brick
+    // of the shared-memory K1 (box + 128-byte header); 2D keeps them in SMEM
     if (!L || L->ndim != 3) return 0;
-    return dope_resid_stride(L);
+    const int64_t six = dope_resid_stride(L);
+    return six + six / 6 + 128;
 }
 
 int dope_lattice_check(const dope_lattice *L) {
@@ -1888,6 +1890,11 @@ int dope_admm_init(const dope_lattice *L, void *stream) {
     k_init_unary<<<grid_for(P.n), 256, 0, s>>>(P.o, P.n);
     rc = cuda_check(cudaGetLastError(), "init_unary");
     if (rc) return rc;
+    if (P.v3 && P.o.nib3) {
+        k_init_ubrick<<<P.o.K, 256, 0, s>>>(P.o);
+        rc = cuda_check(cudaGetLastError(), "init_ubrick");
+        if (rc) return rc;
+    }
     if (P.v3 && P.o.nib3) k_init_resid3d_nib<<<P.o.K, 256, 0, s>>>(P.o);
     else if (P.v3) k_init_resid3d<<<P.o.K, 256, 0, s>>>(P.o, P.o.boxd, P.o.boxh, P.o.boxw);
     else k_init_resid<<<P.o.K, 256, 0, s>>>(P.o);

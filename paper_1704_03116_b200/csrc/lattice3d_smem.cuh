@@ -21,9 +21,6 @@
 // y*32 + x with z the loop index, y the warp and x the lane (conflict-free).
 // Labels, flows and the exactness argument are those of DESIGN.md §2.
 
-#ifndef K1S_QB
-#define K1S_QB 2
-#endif
 namespace k1s {
 constexpr int B = 32, M = B * B * B, NT = 1024, PLANE = B * B;
 constexpr int NIBW = M / 8;                                // nibble words per plane
@@ -36,6 +33,7 @@ constexpr size_t OFF_SLOT = OFF_K + 2 * 4 * 1024;           // uint16[32 warps][
 constexpr size_t OFF_FLAG = OFF_SLOT + 2 * 32 * 32;          // uint32[2][32] row-activity flags
 constexpr size_t OFF_MISC = OFF_FLAG + 2 * 4 * 32;
 constexpr size_t SMEM = OFF_MISC + 64;
+constexpr int UBR = M + 128;                               // int8 u brick: 128-byte header + box
 constexpr int BIAS = 32768;
 constexpr int GMAX = 32000;
 static_assert(SMEM <= 227 * 1024, "shared memory");
@@ -161,6 +159,14 @@ __device__ __forceinline__ int s3_relabel(uint16_t *h, const uint32_t *FE, const
     return nh != HINF;
 }
 
+// int8 copy of u in box order, one brick per sub-region after the fallback
+// scratch (L.scratch + K*6M, stride UBR): the shared-memory K1 bulk-copies it
+// in one piece instead of gathering 32-byte rows of int32.  Header byte 0 != 0:
+// some |u| of the block exceeds int8 (that block runs the HBM-scratch body).
+__device__ __forceinline__ int8_t *u_brick(const Lat2 &L, int k) {
+    return reinterpret_cast<int8_t *>(L.scratch + (size_t)L.K * 6 * k1s::M + (size_t)k * k1s::UBR);
+}
+
 // out of line so that its registers do not count against the fast path
 __device__ __noinline__ void mincut3d_l2_fallback(const Lat2 &L, const K1Tune &T, int k, uint8_t *smem) {
     mincut3d_l2<k1s::B, k1s::B, k1s::B, k1s::NT>(L, T, k, smem);
@@ -225,9 +231,13 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
     // (1) the persistent E/S/D nibble planes (48 KB) stream in by one bulk copy
     //     while (2) 2*linear is computed from u, a, y; (3) then the excess adds
     //     the stored flow: excess = 2*linear + sum over the 6 arcs of (r - cap).
-    if (L.warm) {
-        if (tid == 0) {
-            mbar_expect_tx(bar, 3 * NIBW * 4);
+    const bool quads = L.q3 && (gb.lo_c % 4 == 0) && (gb.wc % 4 == 0);
+    // the int8 u brick (quad path) lands in the height array, unused until the
+    // first relabel
+    const int8_t *ubs = reinterpret_cast<const int8_t *>(sm3 + OFF_H);
+    if ((L.warm || quads) && tid == 0) {
+        mbar_expect_tx(bar, (L.warm ? 3 * NIBW * 4 : 0) + (quads ? UBR : 0));
+        if (L.warm) {
 #pragma unroll
             for (int p = 0; p < 3; ++p)
                 asm volatile(
@@ -235,45 +245,89 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
                     ::"r"(smem_u32(FE + p * NIBW)), "l"(gF + p * NIBW), "r"(NIBW * 4), "r"(smem_u32(bar))
                     : "memory");
         }
+        if (quads)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                ::"r"(smem_u32(ubs)), "l"(u_brick(L, k)), "r"(UBR), "r"(smem_u32(bar))
+                : "memory");
     }
     int over = 0;
     const int32_t lim = GMAX - 6 * cap;
-    const bool quads = L.q3 && (gb.lo_c % 4 == 0) && (gb.wc % 4 == 0);
     if (quads) {
         // thread -> 4 consecutive x of one row; 128 rows per pass, 8 passes.
-        // Every load of a pass (incl. the cross-block neighbour rows) is
-        // issued before any is used.
         const int x0 = (tid & 7) * 4;
-        const int xs = (x0 & 7) * 4;   // bit offset of the quad in its nibble word
-        constexpr int QB = K1S_QB;     // rows per thread in flight
-#pragma unroll 1
-        for (int p0 = 0; p0 < 8; p0 += QB) {
-            int4 u4[QB];
-            uint2 a4[QB];
-            uint32_t y4[QB], ny[QB], nz[QB], nx[QB];
-#pragma unroll
-            for (int j = 0; j < QB; ++j) {
-                const int row = (p0 + j) * 128 + (tid >> 3), z = row >> 5, y = row & 31;
-                u4[j] = make_int4(0, 0, 0, 0);
-                a4[j] = make_uint2(0, 0);
-                y4[j] = ny[j] = nz[j] = nx[j] = 0;
-                if (z < gb.dz && y < gb.hr && x0 < gb.wc) {
-                    const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + y) * W + gb.lo_c + x0;
-                    u4[j] = __ldg(reinterpret_cast<const int4 *>(L.u + G));
-                    a4[j] = *reinterpret_cast<const uint2 *>(a_cur + G);
-                    y4[j] = *reinterpret_cast<const uint32_t *>(y_cur + G);
-                    // one cross-block row per axis (both sides only when the block is 1 thick: below)
-                    if (y == 0 && up_r) ny[j] = *reinterpret_cast<const uint32_t *>(y_cur + G - W);
-                    else if (y == gb.hr - 1 && dn_r) ny[j] = *reinterpret_cast<const uint32_t *>(y_cur + G + W);
-                    if (z == 0 && up_z) nz[j] = *reinterpret_cast<const uint32_t *>(y_cur + G - HW);
-                    else if (z == gb.dz - 1 && dn_z) nz[j] = *reinterpret_cast<const uint32_t *>(y_cur + G + HW);
-                    if (x0 == 0 && lf_c) nx[j] = y_cur[G - 1];
-                    if (x0 + 4 == gb.wc && rt_c) nx[j] |= (uint32_t)y_cur[G + 4] << 8;
-                }
+        // u comes from the int8 brick; a, y of a pass (4 planes: 12 KB)
+        // stream into a double-buffered staging area in the (not yet used)
+        // height array by per-thread cp.async, two passes ahead; the cross-block neighbour words of the
+        // next pass are register loads one pass ahead.  No register holds
+        // in-flight data.  The stored flow's net inflow is added in the same
+        // pass (the nibble planes arrive with pass 0).
+        uint2 *stA = reinterpret_cast<uint2 *>(sm3 + OFF_H + UBR);   // [2][1024]
+        uint32_t *stY = reinterpret_cast<uint32_t *>(stA + 2 * NT);  // [2][1024]
+        static_assert(UBR + 2 * NT * 12 <= 2 * M, "u brick + staging fit the height array");
+        auto gidx = [&](int p, bool &ok, int &z, int &y) -> int64_t {
+            const int row = p * 128 + (tid >> 3);
+            z = row >> 5;
+            y = row & 31;
+            ok = z < gb.dz && y < gb.hr && x0 < gb.wc;
+            return ((int64_t)(gb.lo_z + z) * H + gb.lo_r + y) * W + gb.lo_c + x0;
+        };
+        auto issue = [&](int p) {
+            bool ok;
+            int z, y;
+            const int64_t G = gidx(p, ok, z, y);
+            const int b = p & 1;
+            if (ok) {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(stA + b * NT + tid)),
+                             "l"(a_cur + G) : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(stY + b * NT + tid)),
+                             "l"(y_cur + G) : "memory");
             }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        // cross-block neighbour words of pass p (one row per axis; the
+        // 1-thick-block second side is read in the compute step)
+        auto nbr = [&](int p, uint32_t &ny, uint32_t &nz, uint32_t &nx) {
+            bool ok;
+            int z, y;
+            const int64_t G = gidx(p, ok, z, y);
+            ny = nz = nx = 0;
+            if (!ok) return;
+            if (y == 0 && up_r) ny = *reinterpret_cast<const uint32_t *>(y_cur + G - W);
+            else if (y == gb.hr - 1 && dn_r) ny = *reinterpret_cast<const uint32_t *>(y_cur + G + W);
+            if (z == 0 && up_z) nz = *reinterpret_cast<const uint32_t *>(y_cur + G - HW);
+            else if (z == gb.dz - 1 && dn_z) nz = *reinterpret_cast<const uint32_t *>(y_cur + G + HW);
+            if (x0 == 0 && lf_c) nx = y_cur[G - 1];
+            if (x0 + 4 == gb.wc && rt_c) nx |= (uint32_t)y_cur[G + 4] << 8;
+        };
+        issue(0);
+        issue(1);
+        uint32_t ny, nz, nx;
+        nbr(0, ny, nz, nx);
+        mbar_wait(bar, 0);   // u brick (+ the nibble planes: flow terms are added in the same passes)
+#ifdef K1S_DIAG
+        if (tl) L.timeline[8 * k + 7] = gtimer();
+#endif
+        if (ubs[0]) over = 1;  // some |u| exceeds int8: the HBM-scratch body solves this block
+        // fully unrolled: a register move of a pending load result would
+        // wait for it, exposing one DRAM latency per pass
 #pragma unroll
-            for (int j = 0; j < QB; ++j) {
-                const int row = (p0 + j) * 128 + (tid >> 3), z = row >> 5, y = row & 31;
+        for (int pp = 0; pp < 8; ++pp) {
+            uint32_t ny1 = 0, nz1 = 0, nx1 = 0;
+            if (pp + 1 < 8) nbr(pp + 1, ny1, nz1, nx1);   // in flight during this pass
+            if (pp + 1 < 8) asm volatile("cp.async.wait_group 1;" ::: "memory");
+            else asm volatile("cp.async.wait_group 0;" ::: "memory");
+            const int row = pp * 128 + (tid >> 3), z = row >> 5, y = row & 31;
+            const int bsel = pp & 1;
+            uint32_t uw = 0;
+            uint2 a4 = make_uint2(0, 0);
+            uint32_t y4 = 0;
+            if (z < gb.dz && y < gb.hr && x0 < gb.wc) {
+                uw = *reinterpret_cast<const uint32_t *>(ubs + 128 + z * PLANE + y * B + x0);
+                a4 = stA[bsel * NT + tid];
+                y4 = stY[bsel * NT + tid];
+            }
+            {
                 const int v0 = z * PLANE + y * B + x0;
                 const bool valid = z < gb.dz && y < gb.hr && x0 < gb.wc;
                 int32_t g[4] = {0, 0, 0, 0};
@@ -283,9 +337,9 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
                     int32_t yv[4], sx[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        yv[e] = (int32_t)((y4[j] >> (8 * e)) & 0xffu);
-                        const int32_t by = (int32_t)((ny[j] >> (8 * e)) & 0xffu);
-                        const int32_t bz = (int32_t)((nz[j] >> (8 * e)) & 0xffu);
+                        yv[e] = (int32_t)((y4 >> (8 * e)) & 0xffu);
+                        const int32_t by = (int32_t)((ny >> (8 * e)) & 0xffu);
+                        const int32_t bz = (int32_t)((nz >> (8 * e)) & 0xffu);
                         sx[e] = ((yb || yt) ? yv[e] - by : 0) + ((zb || zt) ? yv[e] - bz : 0);
                     }
                     if (yb && yt) {   // 1-row block with neighbours on both sides
@@ -300,15 +354,48 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
 #pragma unroll
                         for (int e = 0; e < 4; ++e) sx[e] += yv[e] - (int32_t)((o >> (8 * e)) & 0xffu);
                     }
-                    if (x0 == 0 && lf_c) sx[0] += yv[0] - (int32_t)(nx[j] & 0xffu);
-                    if (x0 + 4 == gb.wc && rt_c) sx[3] += yv[3] - (int32_t)((nx[j] >> 8) & 0xffu);
-                    const int32_t uu[4] = {u4[j].x, u4[j].y, u4[j].z, u4[j].w};
-                    const uint32_t aw[2] = {a4[j].x, a4[j].y};
+                    if (x0 == 0 && lf_c) sx[0] += yv[0] - (int32_t)(nx & 0xffu);
+                    if (x0 + 4 == gb.wc && rt_c) sx[3] += yv[3] - (int32_t)((nx >> 8) & 0xffu);
+                    const int32_t uu[4] = {(int32_t)(int8_t)(uw & 0xffu), (int32_t)(int8_t)((uw >> 8) & 0xffu),
+                                           (int32_t)(int8_t)((uw >> 16) & 0xffu), (int32_t)(int8_t)(uw >> 24)};
+                    const uint32_t aw[2] = {a4.x, a4.y};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int32_t av = (int32_t)(int16_t)((aw[e >> 1] >> (16 * (e & 1))) & 0xffffu);
                         g[e] = 2 * uu[e] + L.lamw * sx[e] + L.mu * (2 * av - yv[e]) + L.mu;
                         over |= (g[e] > lim) | (g[e] < -lim);
+                    }
+                    if (L.warm) {
+                        // excess += sum over the node's arcs of (r - cap), four
+                        // nodes at once on bytes: per direction the forward
+                        // arc's r minus the backward arc's (= 2cap - r of the
+                        // neighbour's forward arc, the caps cancel).  A missing
+                        // backward arc reads as cap, a missing forward arc
+                        // (stored 0) gets cap added back: both terms vanish.
+                        const int xs = (x0 & 7) * 4;   // bit offset of the quad in its nibble word
+                        const int wi = v0 >> 3;
+                        const uint32_t cw = (uint32_t)cap * 0x1111u;
+                        const uint32_t wEc = FE[wi];
+                        const uint32_t E4 = (wEc >> xs) & 0xFFFFu;
+                        const uint32_t pn = x0 == 0 ? (uint32_t)cap
+                                                    : (xs ? (wEc >> (xs - 4)) & 0xFu : FE[wi - 1] >> 28);
+                        const uint32_t Ep4 = ((E4 << 4) | pn) & 0xFFFFu;
+                        const uint32_t S4 = (FS[wi] >> xs) & 0xFFFFu;
+                        const uint32_t N4 = y > 0 ? (FS[wi - B / 8] >> xs) & 0xFFFFu : cw;
+                        const uint32_t D4 = (FD[wi] >> xs) & 0xFFFFu;
+                        const uint32_t U4 = z > 0 ? (FD[wi - PLANE / 8] >> xs) & 0xFFFFu : cw;
+                        uint32_t corr = x0 + 4 == gb.wc ? (uint32_t)cap << 24 : 0u;
+                        if (y + 1 == gb.hr) corr += (uint32_t)cap * 0x01010101u;
+                        if (z + 1 == gb.dz) corr += (uint32_t)cap * 0x01010101u;
+                        auto spread4 = [](uint32_t x) -> uint32_t {   // 4 nibbles -> 4 bytes
+                            uint32_t t = (x | (x << 8)) & 0x00FF00FFu;
+                            return (t | (t << 4)) & 0x0F0F0F0Fu;
+                        };
+                        // bytes: flow + 48 (no carry / borrow: 0 < . < 256)
+                        const uint32_t t4 = (spread4(E4) + spread4(S4) + spread4(D4) + corr + 0x30303030u) -
+                                            (spread4(Ep4) + spread4(N4) + spread4(U4));
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) g[e] += (int32_t)((t4 >> (8 * e)) & 0xffu) - 48;
                     }
                 }
                 if (!L.warm) {   // cold residual graph: every existing arc at cap
@@ -330,41 +417,14 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
                 gw.y = ((uint32_t)(g[2] + BIAS) & 0xffffu) | ((uint32_t)(g[3] + BIAS) << 16);
                 *reinterpret_cast<uint2 *>(G2 + (v0 >> 1)) = gw;
             }
+            if (pp + 2 < 8) issue(pp + 2);   // this thread's own slots: no barrier
+            ny = ny1;
+            nz = nz1;
+            nx = nx1;
         }
-        if (L.warm) {
-            mbar_wait(bar, 0);
-            // excess += sum over arcs of (r - cap); one nibble word per plane
-            // and direction covers the quad
-#pragma unroll 2
-            for (int p = 0; p < 8; ++p) {
-                const int row = p * 128 + (tid >> 3), z = row >> 5, y = row & 31;
-                const int v0 = z * PLANE + y * B + x0;
-                if (!(z < gb.dz && y < gb.hr && x0 < gb.wc)) continue;
-                const uint32_t wE = FE[v0 >> 3] >> xs;
-                const uint32_t wS = FS[v0 >> 3] >> xs;
-                const uint32_t wD = FD[v0 >> 3] >> xs;
-                const uint32_t wW = x0 > 0 ? FE[(v0 - 1) >> 3] >> (((v0 - 1) & 7) * 4) : 0u;
-                const uint32_t wN = y > 0 ? FS[(v0 - B) >> 3] >> xs : 0u;
-                const uint32_t wU = z > 0 ? FD[(v0 - PLANE) >> 3] >> xs : 0u;
-                int32_t f[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int x = x0 + e;
-                    int32_t t = 0;
-                    if (x + 1 < gb.wc) t += (int32_t)((wE >> (4 * e)) & 0xfu) - cap;
-                    if (x > 0) t += cap - (int32_t)((e == 0 ? wW : (wE >> (4 * (e - 1)))) & 0xfu);
-                    if (y + 1 < gb.hr) t += (int32_t)((wS >> (4 * e)) & 0xfu) - cap;
-                    if (y > 0) t += cap - (int32_t)((wN >> (4 * e)) & 0xfu);
-                    if (z + 1 < gb.dz) t += (int32_t)((wD >> (4 * e)) & 0xfu) - cap;
-                    if (z > 0) t += cap - (int32_t)((wU >> (4 * e)) & 0xfu);
-                    f[e] = t;
-                }
-                uint2 gw = *reinterpret_cast<const uint2 *>(G2 + (v0 >> 1));
-                gw.x += (uint32_t)f[0] + ((uint32_t)f[1] << 16);
-                gw.y += (uint32_t)f[2] + ((uint32_t)f[3] << 16);
-                *reinterpret_cast<uint2 *>(G2 + (v0 >> 1)) = gw;
-            }
-        }
+#ifdef K1S_DIAG
+        if (tl) L.timeline[8 * k + 6] = gtimer();
+#endif
     } else {
         // scalar prologue (blocks whose x range is not quad-aligned): lane = x
 #pragma unroll 2
@@ -552,7 +612,9 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
             t_bfs += t1 - t0;
             if (rounds == 0) {
                 L.timeline[8 * k + 5] = t1;
+#ifndef K1S_DIAG
                 L.timeline[8 * k + 6] = level;
+#endif
             }
         }
         if (!hit) break;
@@ -629,7 +691,9 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
         L.timeline[8 * k + 1] = gtimer();
         L.timeline[8 * k + 2] = rounds;
         L.timeline[8 * k + 3] = sweeps_done;
+#ifndef K1S_DIAG
         L.timeline[8 * k + 7] = t_bfs;
+#endif
     }
     if (tid == 0) {
         atomicAdd((unsigned long long *)&L.st->solves, 1ull);
@@ -639,6 +703,27 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
 }
 
 // cold residual graph in the nibble layout: every existing E/S/D arc at cap
+// fills the u bricks (dope_admm_init)
+__global__ void k_init_ubrick(Lat2 L) {
+    using namespace k1s;
+    const int k = blockIdx.x;
+    int bz, by, bx;
+    const Geo3 gb = block_geo3(L, k, bz, by, bx);
+    int8_t *ub = u_brick(L, k);
+    const int64_t HW = (int64_t)L.ay.dim * L.W;
+    int bad = 0;
+    for (int v = threadIdx.x; v < M; v += blockDim.x) {
+        const int z = v / PLANE, r = (v / B) % B, c = v % B;
+        int32_t uv = 0;
+        if (z < gb.dz && r < gb.hr && c < gb.wc)
+            uv = L.u[(int64_t)(gb.lo_z + z) * HW + (int64_t)(gb.lo_r + r) * L.W + gb.lo_c + c];
+        bad |= (uv < -128) | (uv > 127);
+        ub[128 + v] = (int8_t)uv;
+    }
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) ub[0] = (int8_t)(bad ? 1 : 0);
+}
+
 __global__ void k_init_resid3d_nib(Lat2 L) {
     using namespace k1s;
     const int k = blockIdx.x;

@@ -49,6 +49,11 @@ def main():
               f"| relabel med {np.median(bfs):6.1f} max {bfs.max():6.1f} lev1 med {np.median(t[:,6]):.0f} max {t[:,6].max()} "
               f"| sweeps-part med {np.median(swp):6.1f} | slowest: rounds {t[j,2]} sweeps {t[j,3]} relabel {bfs[j]:.1f} "
               f"sweeps-part {swp[j]:.1f}")
+        if len(sys.argv) > 3 and sys.argv[3] == "diag":   # build with -DK1S_DIAG: [6] passes done [7] bulk copies in
+            ps = (t[:, 6] - t[:, 0]) / 1e3
+            pl = (t[:, 7] - t[:, 0]) / 1e3
+            print(f"        passes done med {np.median(ps):5.1f} max {ps.max():5.1f} | bulk copies in med {np.median(pl):5.1f} "
+                  f"max {pl.max():5.1f} | prologue end med {np.median(pro):5.1f}")
     dev.raise_on_error()
 
 
