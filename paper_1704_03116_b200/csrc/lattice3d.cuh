@@ -545,6 +545,24 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_consensus3d_vec(Lat2 L, int l
     if (tid == 0) pass_tail(L, agg, cur, best, out);
 }
 
+// Quad groups of a 3D block for the clamp memos (part_flags bits 1-27):
+// 3 * 3 * 3 classes by the block side(s) a quad touches per axis (none / low /
+// high, only sides with a neighbour); group 0 is the interior.
+__device__ __forceinline__ int quad_group3(bool lf, bool rt, bool tp, bool bt, bool zb, bool zt) {
+    return (lf ? 1 : (rt ? 2 : 0)) + 3 * (tp ? 1 : (bt ? 2 : 0)) + 9 * (zb ? 1 : (zt ? 2 : 0));
+}
+// groups touching a side in sd (bit0 -x, 1 +x, 2 -y, 3 +y, 4 -z, 5 +z)
+__device__ __forceinline__ unsigned active_groups3(uint32_t sd) {
+    unsigned m = 0;
+    for (int g = 0; g < 27; ++g) {
+        const int xs = g % 3, ys = (g / 3) % 3, zs = g / 9;
+        if ((xs == 1 && (sd & 1u)) || (xs == 2 && (sd & 2u)) || (ys == 1 && (sd & 4u)) || (ys == 2 && (sd & 8u)) ||
+            (zs == 1 && (sd & 16u)) || (zs == 2 && (sd & 32u)))
+            m |= 1u << g;
+    }
+    return m;
+}
+
 // 3D consensus for blocks whose (y, x) face is 32 x 32 (C4's 32^3 tiling):
 // thread t owns the quad (r = t / 8, c0 = 4 * (t % 8)) of every z-plane of
 // the block, so the per-quad geometry is fixed and planes are visited in
@@ -581,7 +599,7 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
     const int32_t W = L.W, H = L.ay.dim, D = L.az.dim, q = L.q;
     const int64_t HW = (int64_t)H * W;
     __shared__ int64_t red_e[NT / 32], red_s[NT / 32], red_u[NT / 32];
-    __shared__ unsigned red_f[NT / 32];
+    __shared__ unsigned red_f[NT / 32], red_g[NT / 32];
     for (int k = blockIdx.x; k < L.K; k += gridDim.x) {
         int bz, by, bx;
         const Geo3 gb = block_geo3(L, k, bz, by, bx);
@@ -589,36 +607,157 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
         const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
         const bool lf_c = gb.lo_c > 0, rt_c = gb.lo_c + gb.wc < W;
         const int64_t G0 = ((int64_t)gb.lo_z * H + gb.lo_r + r) * W + gb.lo_c + c0;
-        if (clean_ok) {   // clean-block pass (k_consensus3d_vec)
+        // Clean block (not re-solved): it was left with y == yhat and no
+        // moving neighbour face in the last pass, so every quad is a fixed
+        // point except those on a face whose neighbour was re-solved now, and
+        // its energy partial of y_{t-1} equals the one the last pass stored
+        // (DESIGN.md §4).  Ghost planes of another shard count as moved.
+        if (clean_ok && L.dirty[L.K + k] != ep && pe_stamp(L)[k] == (uint32_t)it && !(gb.lo_z == 0 && L.gzu) &&
+            !(gb.lo_z + gb.dz == D && L.gzd)) {
             const int KX = L.ax.k, KYX = L.ay.k * L.ax.k;
             const uint32_t *epo = L.dirty + L.K;
-            bool fast = epo[k] != ep;
-            fast = fast && !(lf_c && epo[k - 1] == ep) && !(rt_c && epo[k + 1] == ep);
-            fast = fast && !(up_r && epo[k - KX] == ep) && !(dn_r && epo[k + KX] == ep);
-            fast = fast && !(gb.lo_z > 0 && epo[k - KYX] == ep) && !(gb.lo_z + gb.dz < D && epo[k + KYX] == ep);
-            fast = fast && !(gb.lo_z == 0 && L.gzu) && !(gb.lo_z + gb.dz == D && L.gzd);   // other rank's solves unknown
-            if (fast) {
-                const uint32_t st_out = ybuf_stamp(L, out)[k];
-                if (st_out == 0u || st_out < ychg_stamp(L)[k]) {
-                    for (int z0 = 0; z0 < gb.dz; z0 += 8) {   // 8 planes of loads in flight
-                        uint32_t v[8];
+            // re-solved neighbours: bit0 -x, 1 +x, 2 -y, 3 +y, 4 -z, 5 +z
+            uint32_t sd = 0;
+            if (lf_c && epo[k - 1] == ep) sd |= 1u;
+            if (rt_c && epo[k + 1] == ep) sd |= 2u;
+            if (up_r && epo[k - KX] == ep) sd |= 4u;
+            if (dn_r && epo[k + KX] == ep) sd |= 8u;
+            if (gb.lo_z > 0 && epo[k - KYX] == ep) sd |= 16u;
+            if (gb.lo_z + gb.dz < D && epo[k + KYX] == ep) sd |= 32u;
+            const uint32_t st_out = ybuf_stamp(L, out)[k];
+            if (st_out == 0u || st_out < ychg_stamp(L)[k]) {   // the output buffer lacks the block's iterate
+                for (int z0 = 0; z0 < gb.dz; z0 += 8) {   // 8 planes of loads in flight
+                    uint32_t v[8];
 #pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            v[j] = z0 + j < gb.dz ? *reinterpret_cast<const unsigned int *>(y_in + G0 + (z0 + j) * HW) : 0u;
+                    for (int j = 0; j < 8; ++j)
+                        v[j] = z0 + j < gb.dz ? *reinterpret_cast<const unsigned int *>(y_in + G0 + (z0 + j) * HW) : 0u;
 #pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            if (z0 + j < gb.dz) *reinterpret_cast<unsigned int *>(y_out + G0 + (z0 + j) * HW) = v[j];
-                    }
+                    for (int j = 0; j < 8; ++j)
+                        if (z0 + j < gb.dz) *reinterpret_cast<unsigned int *>(y_out + G0 + (z0 + j) * HW) = v[j];
                 }
+            }
+            if (sd == 0) {   // settled: partials, flags and the buffer copy all repeat
                 __syncthreads();
                 if (tid == 0) {
                     ybuf_stamp(L, out)[k] = ep;
+                    pe_stamp(L)[k] = ep;
                     L.pu[k] = 0;
                     L.pr[k] = 0;
-                    agg.add_block(L.pe[k], 0, 0, L.pf[k]);
+                    agg.add_block(L.pe[k], 0, 0, L.pf[k] & 1);
                 }
                 continue;
             }
+            __syncthreads();   // the copy lands before the ring quads overwrite it
+            // ring quads: those on a face whose neighbour was re-solved, each
+            // once (faces in the order -z +z -y +y -x +x; a quad on an earlier
+            // active face is skipped)
+            const bool zl_ = (sd & 16u) != 0, zh_ = (sd & 32u) != 0, yl_ = (sd & 4u) != 0, yh_ = (sd & 8u) != 0;
+            int64_t du_r = 0;
+            int ss_r = 0;
+            unsigned marks_r = 0, gfresh = 0;
+            auto ring_quad = [&](int rr, int cc, int z) {
+                const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + rr) * W + gb.lo_c + cc;
+                const bool tp = rr == 0 && up_r, bt = rr == 31 && dn_r, lf = cc == 0 && lf_c, rt = cc == 28 && rt_c;
+                const bool zb = z == 0 && up_z, zt = z == gb.dz - 1 && dn_z;
+                const uint32_t yo = __ldcg(reinterpret_cast<const unsigned int *>(y_in + G));
+                const uint32_t h4 = __ldcg(reinterpret_cast<const unsigned int *>(L.yhat + G));
+                const uint2 av = __ldcg(reinterpret_cast<const uint2 *>(a_in + G));
+                uint32_t cnt = 0, nb = 0;
+                if (tp) { cnt += 0x01010101u; nb += *reinterpret_cast<const uint32_t *>(L.yhat + G - W); }
+                if (bt) { cnt += 0x01010101u; nb += *reinterpret_cast<const uint32_t *>(L.yhat + G + W); }
+                if (zb) { cnt += 0x01010101u; nb += *reinterpret_cast<const uint32_t *>(L.yhat + G - HW); }
+                if (zt) { cnt += 0x01010101u; nb += *reinterpret_cast<const uint32_t *>(L.yhat + G + HW); }
+                if (lf) { cnt += 1u; nb += L.yhat[G - 1]; }
+                if (rt) { cnt += 1u << 24; nb += (uint32_t)L.yhat[G + 4] << 24; }
+                const uint32_t sb = ((cnt & (h4 * 0xFFu)) | 0x04040404u) - nb;
+                int a4[4];
+                unpack_a4(av, a4);
+                int y[4], an[4];
+                uint32_t yw = 0, qc = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int h = (int)((h4 >> (8 * i)) & 0xFFu);
+                    const int p = a4[i] + h + 4 * q - q * (int)((sb >> (8 * i)) & 0xFFu);
+                    qc |= (uint32_t)p;
+                    y[i] = p > 0 ? 1 : 0;
+                    an[i] = a4[i] + h - y[i];
+                    ss_r += h ^ y[i];
+                    yw |= (uint32_t)(2 * y[i]) << (8 * i);
+                }
+                gfresh |= (qc > 1u ? 1u : 0u) << quad_group3(lf, rt, tp, bt, zb, zt);
+                __stcs(reinterpret_cast<uint2 *>(a_out + G), pack_a4(an[0], an[1], an[2], an[3]));
+                __stcg(reinterpret_cast<unsigned int *>(y_out + G), yw);
+                const uint32_t chg = yw ^ yo;
+                const uint32_t hb = ((h4 * 0x01020408u) >> 24) & 0xFu;
+                const uint32_t yb4 = (uint32_t)(y[0] | (y[1] << 1) | (y[2] << 2) | (y[3] << 3));
+                if (chg | (hb ^ yb4)) marks_r |= 1u;
+                if (chg) {
+                    marks_r |= 256u;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int dy = (int)((yw >> (8 * i)) & 0xFFu) - (int)((yo >> (8 * i)) & 0xFFu);
+                        if (dy) du_r += (int64_t)__ldg(L.u + G + i) * dy;
+                    }
+                    if (lf && (chg & 0xFFu)) marks_r |= 2u;
+                    if (rt && (chg >> 24)) marks_r |= 4u;
+                    if (tp) marks_r |= 8u;
+                    if (bt) marks_r |= 16u;
+                    if (zb) marks_r |= 32u;
+                    if (zt) marks_r |= 64u;
+                }
+            };
+            {
+                const int rr = tid >> 3, cc = (tid & 7) << 2;
+                if (zl_) ring_quad(rr, cc, 0);
+                if (zh_ && gb.dz > 1) ring_quad(rr, cc, gb.dz - 1);
+            }
+            {
+                const int z = tid >> 3, cc = (tid & 7) << 2;
+                const bool zdone = (z == 0 && zl_) || (z == gb.dz - 1 && zh_);
+                if (z < gb.dz && !zdone) {
+                    if (yl_) ring_quad(0, cc, z);
+                    if (yh_) ring_quad(31, cc, z);
+                }
+            }
+#pragma unroll 1
+            for (int j = 0; j < 4; ++j) {
+                const int rr = tid & 31, z = (tid >> 5) + 8 * j;
+                const bool done = (z == 0 && zl_) || (z == gb.dz - 1 && zh_) || (rr == 0 && yl_) || (rr == 31 && yh_);
+                if (z < gb.dz && !done) {
+                    if (sd & 1u) ring_quad(rr, 0, z);
+                    if (sd & 2u) ring_quad(rr, 28, z);
+                }
+            }
+            du_r = warp_sum(du_r);
+            const int sq_r = (int)__reduce_add_sync(FULLMASK, (unsigned)ss_r);
+            const unsigned fm_r = __reduce_or_sync(FULLMASK, marks_r);
+            const unsigned gf_r = __reduce_or_sync(FULLMASK, gfresh);
+            if (lane == 0) { red_e[warp] = gf_r; red_s[warp] = sq_r; red_u[warp] = du_r; red_f[warp] = fm_r; }
+            __syncthreads();
+            if (tid == 0) {
+                int64_t S = 0, U = 0;
+                unsigned Fm = 0, gf = 0;
+                for (int w = 0; w < NT / 32; ++w) { gf |= (unsigned)red_e[w]; S += red_s[w]; U += red_u[w]; Fm |= red_f[w]; }
+                // clamp memo: recomputed groups take this pass's bits, the others keep theirs
+                const unsigned act = active_groups3(sd);
+                const unsigned gbits = (gf & act) | (((unsigned)L.pf[k] >> 1) & ~act);
+                L.pu[k] = U;
+                L.pr[k] = S;
+                L.pf[k] = (gbits ? 1 : 0) | (int)(gbits << 1);
+                if (Fm & 1u) L.dirty[k] = 1u;
+                if (Fm & 2u) L.dirty[k - 1] = 1u;
+                if (Fm & 4u) L.dirty[k + 1] = 1u;
+                if (Fm & 8u) L.dirty[k - KX] = 1u;
+                if (Fm & 16u) L.dirty[k + KX] = 1u;
+                if ((Fm & 32u) && k - KYX >= 0) L.dirty[k - KYX] = 1u;
+                if ((Fm & 64u) && k + KYX < L.K) L.dirty[k + KYX] = 1u;
+                ybuf_stamp(L, out)[k] = ep;
+                pe_stamp(L)[k] = ep;
+                if (Fm & 256u) ychg_stamp(L)[k] = ep;
+                agg.add_block(L.pe[k], U, S, gbits ? 1 : 0);
+            }
+            __syncthreads();
+            continue;
         }
         const bool top = r == 0 && up_r, bot = r == 31 && dn_r;
         const bool lft = c0 == 0 && lf_c, rgt = c0 == 28 && rt_c;
@@ -627,7 +766,7 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
         const bool xnx = gb.lo_c + c0 + 4 < W;             // the +x partner of the quad's last voxel
         int64_t e_acc = 0, du = 0;
         int ss = 0;
-        unsigned marks = 0, clamp_or = 0;
+        unsigned marks = 0, clamp_or = 0, gcl = 0;
         for (int z0 = 0; z0 < gb.dz; z0 += ZB) {
             const int zl = min(z0 + ZB, gb.dz) - 1;        // last plane of the batch
             uint32_t yh4[ZB], yo[ZB], nb[ZB], cnt[ZB], yb[ZB];
@@ -679,16 +818,19 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
                 unpack_a4(av[j], a4);
                 int y[4], an[4];
                 uint32_t yw = 0;
+                uint32_t qc = 0;
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int h = (int)((h4 >> (8 * i)) & 0xFFu);
                     const int p = a4[i] + h + 4 * q - q * (int)((sb >> (8 * i)) & 0xFFu);
-                    clamp_or |= (uint32_t)p;
+                    qc |= (uint32_t)p;
                     y[i] = p > 0 ? 1 : 0;
                     an[i] = a4[i] + h - y[i];
                     ss += h ^ y[i];
                     yw |= (uint32_t)(2 * y[i]) << (8 * i);
                 }
+                clamp_or |= qc;
+                gcl |= (qc > 1u ? 1u : 0u) << quad_group3(lft, rgt, top, bot, z == 0 && up_z, z == gb.dz - 1 && dn_z);
                 if (a_out) __stcs(reinterpret_cast<uint2 *>(a_out + G), pack_a4(an[0], an[1], an[2], an[3]));
                 __stcg(reinterpret_cast<unsigned int *>(y_out + G), yw);
                 const uint32_t chg = yw ^ yo[j];
@@ -715,16 +857,18 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
         du = warp_sum(du);
         const int sq = (int)__reduce_add_sync(FULLMASK, (unsigned)ss);
         const unsigned fm = __reduce_or_sync(FULLMASK, marks | (clamp_or > 1u ? 128u : 0u));
-        if (lane == 0) { red_e[warp] = e_acc; red_s[warp] = sq; red_u[warp] = du; red_f[warp] = fm; }
+        const unsigned gall = __reduce_or_sync(FULLMASK, gcl);
+        if (lane == 0) { red_e[warp] = e_acc; red_s[warp] = sq; red_u[warp] = du; red_f[warp] = fm; red_g[warp] = gall; }
         __syncthreads();
         if (tid == 0) {
             int64_t E = 0, S = 0, U = 0;
             unsigned Fm = 0;
-            for (int w = 0; w < NT / 32; ++w) { E += red_e[w]; S += red_s[w]; U += red_u[w]; Fm |= red_f[w]; }
+            unsigned gb_ = 0;
+            for (int w = 0; w < NT / 32; ++w) { E += red_e[w]; S += red_s[w]; U += red_u[w]; Fm |= red_f[w]; gb_ |= red_g[w]; }
             L.pe[k] = E;
             L.pu[k] = U;
             L.pr[k] = S;
-            L.pf[k] = (Fm & 128u) ? 1 : 0;
+            L.pf[k] = ((Fm & 128u) ? 1 : 0) | (int)(gb_ << 1);   // bit 0 clamped, bits 1-27 quad-group clamp memos
             const int KX = L.ax.k, KYX = L.ay.k * L.ax.k;
             if (Fm & 1u) L.dirty[k] = 1u;
             if (Fm & 2u) L.dirty[k - 1] = 1u;
@@ -734,6 +878,7 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
             if ((Fm & 32u) && k - KYX >= 0) L.dirty[k - KYX] = 1u;
             if ((Fm & 64u) && k + KYX < L.K) L.dirty[k + KYX] = 1u;
             ybuf_stamp(L, out)[k] = ep;
+            if (want_e) pe_stamp(L)[k] = ep;
             if (Fm & 256u) ychg_stamp(L)[k] = ep;
             agg.add_block(E, U, S, (Fm & 128u) ? 1 : 0);
         }

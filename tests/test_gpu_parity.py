@@ -240,17 +240,42 @@ def test_3d_k1_paths_match_oracle(size, kpa, lam, uscale, iters):
 
 
 def test_c4_full_size_first_iterations_match_oracle():
+    """C4 at full size, 5 iterations bit-exact vs the oracle (from the third on the
+    consensus pass settles clean blocks and recomputes only re-solved-neighbour faces)."""
     import oracle as orc
-    wl = W.c4(iters=3)
+    iters = 5
+    wl = W.c4(iters=iters)
     rows, cols, vals = wl.pair_arrays()
     model = dope.EnergyModel(wl.u.astype(np.float64), dope.SparseWeights(wl.n, rows, cols, vals), wl.lam)
     part = dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0, materialize=False)
-    labels, state = dope.run(model, part, dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=3))
+    labels, state = dope.run(model, part, dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=iters))
     spec = orc.LatticeSpec(wl.dims, wl.kpa, wl.offsets, [1.0, 1.0, 1.0], wl.u.astype(np.float64), wl.lam)
-    ref = orc.run(spec, 1.0, 1.0, 0.0, 3, threads=os.cpu_count() or 16)
+    ref = orc.run(spec, 1.0, 1.0, 0.0, iters, threads=os.cpu_count() or 16)
     assert np.array_equal([t.energy for t in state.trace], ref["energy"])
+    assert np.array_equal([t.max_block_residual for t in state.trace], ref["max_block_residual"])
     assert np.array_equal(state.labels_global(), ref["yhat"])
     assert np.array_equal(labels, ref["labels"])
+
+
+def test_c4_clean_block_paths_match_plain_run():
+    """C4, 30 iterations: the clean-block consensus paths (settled / face-only
+    recompute, memoised energies and clamp groups) against a run that re-solves and
+    recomputes every block every iteration -- identical traces, iterates, labels."""
+    iters = 30
+    wl = W.c4(iters=iters)
+    rows, cols, vals = wl.pair_arrays()
+    model = dope.EnergyModel(wl.u.astype(np.float64), dope.SparseWeights(wl.n, rows, cols, vals), wl.lam)
+    part = dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0, materialize=False)
+    l1, s1 = dope.run(model, part, dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=iters))
+    l2, s2 = dope.run(model, part, dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=iters,
+                                                   skip_clean=False))
+    assert [t.energy for t in s1.trace] == [t.energy for t in s2.trace]
+    assert [t.max_block_residual for t in s1.trace] == [t.max_block_residual for t in s2.trace]
+    assert [t.clamped for t in s1.trace] == [t.clamped for t in s2.trace]
+    assert np.allclose([t.residual_sq for t in s1.trace], [t.residual_sq for t in s2.trace], rtol=1e-12, atol=0)
+    assert np.array_equal(s1.y, s2.y) and np.array_equal(l1, l2)
+    assert np.array_equal(s1.labels_global(), s2.labels_global())
+    assert np.array_equal(s1.multipliers_global(), s2.multipliers_global())
 
 
 def _float_model(wl):
