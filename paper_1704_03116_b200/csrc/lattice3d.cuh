@@ -812,38 +812,34 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
                     if (gb.lo_z + z + 1 < D || L.gzd) qd += __popc(yo[j] ^ (z < zl ? yo[j + 1 < ZB ? j + 1 : j] : yz));
                     e_acc += (int64_t)L.lamw * qd;
                 }
+                // the quad's update on packed bytes / int16 pairs (quad_update, 2D K2)
                 const uint32_t h4 = yh4[j];
-                const uint32_t sb = ((cnt[j] & (h4 * 0xFFu)) | 0x04040404u) - nb[j];
-                int a4[4];
-                unpack_a4(av[j], a4);
-                int y[4], an[4];
-                uint32_t yw = 0;
+                uint2 an2;
                 uint32_t qc = 0;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int h = (int)((h4 >> (8 * i)) & 0xFFu);
-                    const int p = a4[i] + h + 4 * q - q * (int)((sb >> (8 * i)) & 0xFFu);
-                    qc |= (uint32_t)p;
-                    y[i] = p > 0 ? 1 : 0;
-                    an[i] = a4[i] + h - y[i];
-                    ss += h ^ y[i];
-                    yw |= (uint32_t)(2 * y[i]) << (8 * i);
-                }
+                const uint32_t yn = quad_update(h4, av[j], cnt[j], nb[j], q, 4 * q, an2, qc);
                 clamp_or |= qc;
                 gcl |= (qc > 1u ? 1u : 0u) << quad_group3(lft, rgt, top, bot, z == 0 && up_z, z == gb.dz - 1 && dn_z);
-                if (a_out) __stcs(reinterpret_cast<uint2 *>(a_out + G), pack_a4(an[0], an[1], an[2], an[3]));
+                const uint32_t hb = bits_b01(h4);
+                ss += __popc(hb ^ yn);
+                const uint32_t yw = bytes_b01(yn) << 1;   // y2 bytes 0/2
+                if (a_out) __stcs(reinterpret_cast<uint2 *>(a_out + G), an2);
                 __stcg(reinterpret_cast<unsigned int *>(y_out + G), yw);
                 const uint32_t chg = yw ^ yo[j];
-                const uint32_t hb = ((h4 * 0x01020408u) >> 24) & 0xFu;
-                const uint32_t yb4 = (uint32_t)(y[0] | (y[1] << 1) | (y[2] << 2) | (y[3] << 3));
-                if (chg | (hb ^ yb4)) marks |= 1u;
+                if (chg | (hb ^ yn)) marks |= 1u;
                 if (chg) {
                     marks |= 256u;
+                    const uint32_t yoj = yo[j];
+                    int32_t uq[4];
+                    if (L.q3) {
+                        const int4 uv = __ldg(reinterpret_cast<const int4 *>(L.u + G));
+                        uq[0] = uv.x; uq[1] = uv.y; uq[2] = uv.z; uq[3] = uv.w;
+                    } else {
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int dy = (int)((yw >> (8 * i)) & 0xFFu) - (int)((yo[j] >> (8 * i)) & 0xFFu);
-                        if (dy) du += (int64_t)__ldg(L.u + G + i) * dy;
+                        for (int i = 0; i < 4; ++i) uq[i] = __ldg(L.u + G + i);
                     }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        du += (int64_t)uq[i] * ((int)((yw >> (8 * i)) & 0xFFu) - (int)((yoj >> (8 * i)) & 0xFFu));
                     if (lft && (chg & 0xFFu)) marks |= 2u;
                     if (rgt && (chg >> 24)) marks |= 4u;
                     if (top) marks |= 8u;
