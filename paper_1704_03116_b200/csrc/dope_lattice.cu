@@ -530,6 +530,11 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
             }
         }
     }
+    if (L.ndim == 3 && L.scratch) {   // slab accumulators of the 3D consensus pass (slab_acc3)
+        const size_t M = (size_t)L.boxd * L.boxh * L.boxw;
+        unsigned long long *acc = reinterpret_cast<unsigned long long *>(L.scratch + (size_t)L.K * (7 * M + 128));
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 8 * (int64_t)L.K; i += stride) acc[i] = 0ull;
+    }
     // solve epochs and the stamps of the clean-block consensus passes
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 6 * (int64_t)L.K; i += stride)
             L.dirty[L.K + i] = 0u;
@@ -1751,7 +1756,8 @@ static int launch_k2(const Lat2 &o, cudaStream_t s) {
         if (!getenv("DOPE_NO_VEC3") && !getenv("DOPE_NO_PLANE3") && lq == 3 && o.ax.rem == 0 &&
             o.ay.base == 32 && o.ay.rem == 0 && o.W % 4 == 0 && al % 8 == 0) {
             const int sms = sm_count();
-            return cuda_check(launch_pdl(k_consensus3d_plane, dim3(o.K < 4 * sms ? o.K : 4 * sms), dim3(256), 0, s,
+            const int units = o.K * ((o.az.base + K2P_SLAB - 1) / K2P_SLAB);   // (block, slab) work units
+            return cuda_check(launch_pdl(k_consensus3d_plane, dim3(units < 4 * sms ? units : 4 * sms), dim3(256), 0, s,
                                          o),
                               "launch K2-3D (plane)");
         }
@@ -1854,10 +1860,11 @@ int64_t dope_resid_stride(const dope_lattice *L) {
 int64_t dope_scratch_stride(const dope_lattice *L) {
     // 3D: excess (int32) + heights (uint16) per box node, 6 bytes (the
     // residual planes' 6 bytes give the same figure), then the int8 u brick
-    // of the shared-memory K1 (box + 128-byte header); 2D keeps them in SMEM
+    // of the shared-memory K1 (box + 128-byte header) and 64 bytes of slab
+    // accumulators for the 3D consensus pass; 2D keeps them in SMEM
     if (!L || L->ndim != 3) return 0;
     const int64_t six = dope_resid_stride(L);
-    return six + six / 6 + 128;
+    return six + six / 6 + 128 + 64;   // + the consensus pass's slab accumulators
 }
 
 int dope_lattice_check(const dope_lattice *L) {

@@ -545,6 +545,14 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_consensus3d_vec(Lat2 L, int l
     if (tid == 0) pass_tail(L, agg, cur, best, out);
 }
 
+// Per-block slab accumulators of the 3D plane consensus pass: E, U, S,
+// marks | group bits << 32, arrival count (5 x 8 bytes in a 64-byte slot after
+// the u bricks in L.scratch; zero at allocation, left zeroed after each pass).
+__device__ __forceinline__ unsigned long long *slab_acc3(const Lat2 &L, int k) {
+    const size_t M = (size_t)L.boxd * L.boxh * L.boxw;
+    return reinterpret_cast<unsigned long long *>(L.scratch + (size_t)L.K * (7 * M + 128) + (size_t)k * 64);
+}
+
 // Quad groups of a 3D block for the clamp memos (part_flags bits 1-27):
 // 3 * 3 * 3 classes by the block side(s) a quad touches per axis (none / low /
 // high, only sides with a neighbour); group 0 is the interior.
@@ -574,6 +582,9 @@ __device__ __forceinline__ unsigned active_groups3(uint32_t sd) {
 #ifndef K2P_ZB
 #define K2P_ZB 4
 #endif
+#ifndef K2P_SLAB
+#define K2P_SLAB 8   // planes per work unit of the full update
+#endif
 #ifndef K2P_MINB
 #define K2P_MINB 4
 #endif
@@ -600,9 +611,15 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
     const int64_t HW = (int64_t)H * W;
     __shared__ int64_t red_e[NT / 32], red_s[NT / 32], red_u[NT / 32];
     __shared__ unsigned red_f[NT / 32], red_g[NT / 32];
-    for (int k = blockIdx.x; k < L.K; k += gridDim.x) {
+    // work units: (block, slab of K2P_SLAB planes); a block's clean-block
+    // pass runs in its slab-0 unit, its full update is split over its slabs
+    // (per-block accumulators, the last slab to finish publishes)
+    const int nsl = (L.az.base + K2P_SLAB - 1) / K2P_SLAB;
+    for (int u = blockIdx.x; u < L.K * nsl; u += gridDim.x) {
+        const int k = u / nsl, slab = u - k * nsl;
         int bz, by, bx;
         const Geo3 gb = block_geo3(L, k, bz, by, bx);
+        if (slab * K2P_SLAB >= gb.dz) continue;   // ragged last block plane
         const bool up_z = gb.lo_z > 0 || L.gzu, dn_z = gb.lo_z + gb.dz < D || L.gzd;   // ghost planes: shards
         const bool up_r = gb.lo_r > 0, dn_r = gb.lo_r + gb.hr < H;
         const bool lf_c = gb.lo_c > 0, rt_c = gb.lo_c + gb.wc < W;
@@ -612,8 +629,12 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
         // point except those on a face whose neighbour was re-solved now, and
         // its energy partial of y_{t-1} equals the one the last pass stored
         // (DESIGN.md §4).  Ghost planes of another shard count as moved.
-        if (clean_ok && L.dirty[L.K + k] != ep && pe_stamp(L)[k] == (uint32_t)it && !(gb.lo_z == 0 && L.gzu) &&
+        // (a stamp already at ep was written in this pass by the block's
+        // clean path -- a full-path block publishes only after all its slabs)
+        const uint32_t pst = pe_stamp(L)[k];
+        if (clean_ok && L.dirty[L.K + k] != ep && (pst == (uint32_t)it || pst == ep) && !(gb.lo_z == 0 && L.gzu) &&
             !(gb.lo_z + gb.dz == D && L.gzd)) {
+            if (slab != 0) continue;
             const int KX = L.ax.k, KYX = L.ay.k * L.ax.k;
             const uint32_t *epo = L.dirty + L.K;
             // re-solved neighbours: bit0 -x, 1 +x, 2 -y, 3 +y, 4 -z, 5 +z
@@ -767,8 +788,9 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
         int64_t e_acc = 0, du = 0;
         int ss = 0;
         unsigned marks = 0, clamp_or = 0, gcl = 0;
-        for (int z0 = 0; z0 < gb.dz; z0 += ZB) {
-            const int zl = min(z0 + ZB, gb.dz) - 1;        // last plane of the batch
+        const int zend = min((slab + 1) * K2P_SLAB, gb.dz);
+        for (int z0 = slab * K2P_SLAB; z0 < zend; z0 += ZB) {
+            const int zl = min(z0 + ZB, zend) - 1;        // last plane of the batch
             uint32_t yh4[ZB], yo[ZB], nb[ZB], cnt[ZB], yb[ZB];
             uint2 av[ZB];
             int yr[ZB];
@@ -861,6 +883,30 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
             unsigned Fm = 0;
             unsigned gb_ = 0;
             for (int w = 0; w < NT / 32; ++w) { E += red_e[w]; S += red_s[w]; U += red_u[w]; Fm |= red_f[w]; gb_ |= red_g[w]; }
+            const int nsk = (gb.dz + K2P_SLAB - 1) / K2P_SLAB;   // this block's slabs
+            bool last = true;
+            if (nsk > 1) {
+                // fold into the block's accumulators; the last slab takes the totals
+                // and leaves them zeroed for the next pass
+                unsigned long long *acc = slab_acc3(L, k);
+                if (E) atomicAdd(&acc[0], (unsigned long long)E);
+                if (U) atomicAdd(&acc[1], (unsigned long long)U);
+                if (S) atomicAdd(&acc[2], (unsigned long long)S);
+                if (Fm | gb_) atomicOr(&acc[3], (unsigned long long)Fm | ((unsigned long long)gb_ << 32));
+                __threadfence();
+                last = atomicAdd(reinterpret_cast<unsigned int *>(&acc[4]), 1u) == (unsigned)nsk - 1u;
+                if (last) {
+                    __threadfence();
+                    E = (int64_t)__ldcg(&acc[0]);
+                    U = (int64_t)__ldcg(&acc[1]);
+                    S = (int64_t)__ldcg(&acc[2]);
+                    const unsigned long long fg = __ldcg(&acc[3]);
+                    Fm = (unsigned)fg;
+                    gb_ = (unsigned)(fg >> 32);
+                    acc[0] = acc[1] = acc[2] = acc[3] = acc[4] = 0ull;
+                }
+            }
+            if (last) {
             L.pe[k] = E;
             L.pu[k] = U;
             L.pr[k] = S;
@@ -877,6 +923,7 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
             if (want_e) pe_stamp(L)[k] = ep;
             if (Fm & 256u) ychg_stamp(L)[k] = ep;
             agg.add_block(E, U, S, (Fm & 128u) ? 1 : 0);
+            }
         }
         __syncthreads();
     }
