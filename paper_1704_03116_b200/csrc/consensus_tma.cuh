@@ -416,7 +416,6 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
                 const uint32_t el = __ldcg(L.dirty + K + kl), er = __ldcg(L.dirty + K + kr);
                 const uint32_t eu = __ldcg(L.dirty + K + ku), ed = __ldcg(L.dirty + K + kd);
                 const uint32_t ps = __ldcg(pe_stamp(L) + kk), yk = __ldcg(ych + kk);
-                const uint32_t yr = __ldcg(ych + kr), yd = __ldcg(ych + kd);
                 const uint32_t so = __ldcg(ybuf_stamp(L, out) + kk);
                 const uint32_t sl = __ldcg(solved_slot(L) + kk);
                 const long long pek = __ldcg(reinterpret_cast<const long long *>(L.pe) + kk);
@@ -437,16 +436,14 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 
                     if (sl >= 1u && sl <= (uint32_t)nsolved && __ldcg(solved_list(L) + sl - 1u) == (uint32_t)kk) mode = 3;
                 }
                 long long em = 0;
-                // clean block: its energy partial still holds when it was
-                // computed last pass and neither the block nor its right /
-                // lower neighbour (the other ends of its pairs) moved then;
-                // the output buffer already holds its iterate when it received
-                // it after the block's last change.  Stamps other CTAs may be
-                // writing this pass read as "moved".
+                // clean block: neither it nor the facing pixels
+                // of its right / lower neighbour (the other ends of its pairs)
+                // moved in the last pass -- a move there would have marked it
+                // dirty -- so its energy partial repeats when the last pass
+                // stored one (energy stamp); the output buffer already holds
+                // its iterate when it received it after the block's last change
                 const uint32_t it32 = (uint32_t)iter;
-                const bool ok = mode == 0 && !solved && iter >= 2 && settle && ps == it32 && yk < it32 &&
-                                (bx + 1 >= KX || yr < it32) && (by + 1 < KY ? yd < it32 : L.gdn == 0) &&
-                                so != 0u && so >= yk;
+                const bool ok = mode == 0 && !solved && iter >= 2 && settle && ps == it32 && so != 0u && so >= yk;
                 if (ok) {
                     em = pek;
                     mode = sd ? 1 : 2;

@@ -40,7 +40,7 @@ for it in range(iters):
     okd = np.ones((KY, KX), bool)
     okd[:-1, :] = ych[1:, :] < it
     so = d[(2 + out) * K:(3 + out) * K].reshape(KY, KX)
-    ok &= okr & okd & (so != 0) & (so >= ych) & ~epg & (it >= 2)
+    ok = (d[6 * K:7 * K].reshape(KY, KX) == it) & (so != 0) & (so >= ych) & ~epg & (it >= 2)
     ev[0].record()
     dev.call("dope_update_global", fuse=1)
     ev[1].record()
