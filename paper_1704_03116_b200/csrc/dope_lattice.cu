@@ -1380,13 +1380,24 @@ static Variant make_variant() {
     return Variant{BH, BW, NT, K1Cfg<BH, BW, NT>::SMEM, &k_block_mincut<BH, BW, NT>};
 }
 
-static const Variant *pick_variant(int maxh, int maxw) {
+static int sm_count();
+
+static const Variant *pick_variant(int maxh, int maxw, int nblocks) {
     static const Variant table[] = {
         make_variant<16, 16, 64>(),
         make_variant<32, 32, 128>(),
         make_variant<64, 64, 256>(),
         make_variant<128, 128, 512>(),
     };
+    // With few blocks per SM the K1 time is the slowest solve, not throughput:
+    // twice the threads per block then pay (measured: C5 b64, K = 1024, K1
+    // 23.0 -> 18.9 us; C3, K = 4096, 29.2 -> 31.0 us).  DOPE_K1_WIDE=0/1 forces.
+    static const Variant wide64 = make_variant<64, 64, 512>();
+    static const Variant wide128 = make_variant<128, 128, 1024>();
+    static const int force = getenv("DOPE_K1_WIDE") ? atoi(getenv("DOPE_K1_WIDE")) : -1;
+    const bool wide = force >= 0 ? force != 0 : nblocks <= 8 * sm_count();
+    if (wide && maxh > 32 && maxw > 32 && maxh <= 64 && maxw <= 64) return &wide64;
+    if (wide && maxh > 64 && maxw > 64 && maxh <= 128 && maxw <= 128) return &wide128;
     for (const Variant &v : table)
         if (maxh <= v.bh && maxw <= v.bw) return &v;
     return nullptr;
@@ -1497,7 +1508,7 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
         if (var3) *var3 = v3;
         if (var) *var = nullptr;
     } else {
-        const Variant *v = pick_variant(maxh, maxw);
+        const Variant *v = pick_variant(maxh, maxw, o.K);
         if (!v) return DOPE_E_GEOMETRY;
         o.boxd = 1;
         o.boxh = v->bh;
@@ -1852,7 +1863,7 @@ int64_t dope_resid_stride(const dope_lattice *L) {
     }
     if (L->ndim != 2 || L->kpa[0] < 1 || L->kpa[1] < 1) return 0;
     Axis ay = make_axis(L->dims[0], L->kpa[0]), ax = make_axis(L->dims[1], L->kpa[1]);
-    const Variant *v = pick_variant(ay.base + (ay.rem ? 1 : 0), ax.base + (ax.rem ? 1 : 0));
+    const Variant *v = pick_variant(ay.base + (ay.rem ? 1 : 0), ax.base + (ax.rem ? 1 : 0), 0);
     if (!v) return 0;
     return (int64_t)2 * v->bh * v->bw;   // E and S residual planes
 }
