@@ -596,11 +596,24 @@ static VarF make_varf() {
     return VarF{BH, BW, NT, ND, K1FCfg<BH, BW, NT, ND>::SMEM, &k_block_mincut_f<BH, BW, NT, ND>};
 }
 
-static const VarF *pick_varf(int conn, int maxh, int maxw) {
+static const VarF *pick_varf(int conn, int maxh, int maxw, int nblocks) {
     static const VarF table[] = {
         make_varf<32, 32, 256, 4>(), make_varf<64, 64, 512, 4>(),
         make_varf<32, 32, 256, 8>(), make_varf<64, 64, 512, 8>(),
     };
+    // few blocks per SM: the slowest solve sets K1, twice the threads pay
+    // (as in the integer path); DOPE_K1_WIDE=0/1 forces
+    static const VarF wide[] = {make_varf<64, 64, 1024, 4>(), make_varf<64, 64, 1024, 8>()};
+    static const int force = getenv("DOPE_K1_WIDE") ? atoi(getenv("DOPE_K1_WIDE")) : -1;
+    static const int sms = [] {
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n > 0 ? n : 148;
+    }();
+    if ((force >= 0 ? force != 0 : (nblocks > 0 && nblocks <= 8 * sms)) && maxh > 32 && maxw > 32 && maxh <= 64 &&
+        maxw <= 64)
+        return &wide[conn == 8 ? 1 : 0];
     for (const VarF &v : table)
         if (v.ndir == conn && maxh <= v.bh && maxw <= v.bw) return &v;
     return nullptr;
@@ -658,7 +671,7 @@ static int build(const dope_lattice_f *L, LatF &o, const VarF **var) {
     o.tr_rs = L->trace_residual_sq;
     o.tr_mr = L->trace_max_residual;
     o.tr_cl = L->trace_clamped;
-    const VarF *v = pick_varf(L->conn, o.ay.base + (o.ay.rem ? 1 : 0), o.ax.base + (o.ax.rem ? 1 : 0));
+    const VarF *v = pick_varf(L->conn, o.ay.base + (o.ay.rem ? 1 : 0), o.ax.base + (o.ax.rem ? 1 : 0), L->kpa[0] * L->kpa[1]);
     if (!v) return DOPE_E_GEOMETRY;
     o.boxh = v->bh;
     o.boxw = v->bw;
@@ -712,7 +725,7 @@ const char *dope_f_last_error(void) { return g_err; }
 int64_t dope_f_resid_stride(const dope_lattice_f *L) {
     if (!L || (L->conn != 4 && L->conn != 8) || L->kpa[0] < 1 || L->kpa[1] < 1) return 0;
     Axis ay = make_axis(L->dims[0], L->kpa[0]), ax = make_axis(L->dims[1], L->kpa[1]);
-    const VarF *v = pick_varf(L->conn, ay.base + (ay.rem ? 1 : 0), ax.base + (ax.rem ? 1 : 0));
+    const VarF *v = pick_varf(L->conn, ay.base + (ay.rem ? 1 : 0), ax.base + (ax.rem ? 1 : 0), 0);
     return v ? (int64_t)4 * v->ndir * v->bh * v->bw : 0;
 }
 
