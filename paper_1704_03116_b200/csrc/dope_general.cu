@@ -540,14 +540,28 @@ static VarG make_varg() {
     return VarG{BH, BW, NT, ND, K1FCfg<BH, BW, NT, ND>::SMEM, &k_block_mincut_g<BH, BW, NT, ND>};
 }
 
-static const VarG *pick_varg(int conn, int maxh, int maxw) {
+static const VarG *pick_varg(int conn, int maxh, int maxw, int ncopies) {
     static const VarG table[] = {
         // 40 x 48: the 32-blocks of a 25 %-overlap partition (boxes <= 40 x 40)
         // without padding them to 64 x 64 (1920 nodes: 30 BFS words)
         make_varg<32, 32, 256, 4>(), make_varg<40, 48, 384, 4>(), make_varg<64, 64, 512, 4>(),
         make_varg<32, 32, 256, 8>(), make_varg<40, 48, 384, 8>(), make_varg<64, 64, 512, 8>(),
     };
-    for (const VarG &v : table)
+    // few block copies per SM: the slowest solve sets K1g, more threads per
+    // copy pay (as in the integer and float paths); DOPE_K1_WIDE=0/1 forces
+    static const VarG wide[] = {
+        make_varg<32, 32, 512, 4>(), make_varg<40, 48, 960, 4>(), make_varg<64, 64, 1024, 4>(),
+        make_varg<32, 32, 512, 8>(), make_varg<40, 48, 960, 8>(), make_varg<64, 64, 1024, 8>(),
+    };
+    static const int force = getenv("DOPE_K1_WIDE") ? atoi(getenv("DOPE_K1_WIDE")) : -1;
+    static const int sms = [] {
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n > 0 ? n : 148;
+    }();
+    const bool use_wide = force >= 0 ? force != 0 : (ncopies > 0 && ncopies <= 8 * sms);
+    for (const VarG &v : (use_wide ? wide : table))
         if (v.ndir == conn && maxh <= v.bh && maxw <= v.bw) return &v;
     return nullptr;
 }
@@ -603,7 +617,7 @@ static int build(const dope_general *L, LatG &o, const VarG **var) {
     o.tr_mu = L->trace_mu;
     o.tr_cl = L->trace_clamped;
     o.npe = npe_for((int64_t)o.H * o.W);
-    const VarG *v = pick_varg(L->conn, L->box[0], L->box[1]);
+    const VarG *v = pick_varg(L->conn, L->box[0], L->box[1], o.K);
     if (!v) return DOPE_E_GEOMETRY;
     o.boxh = v->bh;
     o.boxw = v->bw;
@@ -653,13 +667,13 @@ const char *dope_g_last_error(void) { return g_err; }
 
 int64_t dope_g_copy_stride(const dope_general *L) {
     if (!L) return 0;
-    const VarG *v = pick_varg(L->conn, L->box[0], L->box[1]);
+    const VarG *v = pick_varg(L->conn, L->box[0], L->box[1], 0);
     return v ? (int64_t)v->bh * v->bw : 0;
 }
 
 int64_t dope_g_box_width(const dope_general *L) {
     if (!L) return 0;
-    const VarG *v = pick_varg(L->conn, L->box[0], L->box[1]);
+    const VarG *v = pick_varg(L->conn, L->box[0], L->box[1], 0);
     return v ? (int64_t)v->bw : 0;
 }
 
