@@ -287,7 +287,10 @@ __global__ void k_init_state_g(LatG L, int64_t n, int64_t ncopy) {
 // ---------------------------------------------------------------------------
 // K2g: global step (admm.py:136-151, 172-180), one thread per pixel
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_global_g(LatG L, int boxw, int M) {
+#ifndef KG_MINB
+#define KG_MINB 3
+#endif
+__global__ void __launch_bounds__(256, KG_MINB) k_global_g(LatG L, int boxw, int M) {
     const dope_run_state *st = L.st;
     if (st->stop) return;
     const int cur = st->ycur, best = st->ybest;
@@ -305,10 +308,20 @@ __global__ void __launch_bounds__(256) k_global_g(LatG L, int boxw, int M) {
         int qd[8];
         double d = 0.0;
         bool pow2 = (qp & (qp - 1)) == 0;
+        // the neighbours' counts are loaded with the weights, not after them
+        // (clamped into the grid; a pair outside has weight 0 and count 1)
+        int qraw[8];
 #pragma unroll
         for (int dd = 0; dd < 8; ++dd) {
+            int rn = R + dy_of(dd), cn = Cc + dx_of(dd);
+            rn = rn < 0 ? 0 : (rn >= L.H ? L.H - 1 : rn);
+            cn = cn < 0 ? 0 : (cn >= L.W ? L.W - 1 : cn);
+            qraw[dd] = dd < L.ndir ? (int)L.q[(int64_t)rn * L.W + cn] : 1;
             wd[dd] = dd < L.ndir ? wpair(L, R, Cc, dd) : 0.0;
-            qd[dd] = wd[dd] != 0.0 ? (int)L.q[(int64_t)(R + dy_of(dd)) * L.W + Cc + dx_of(dd)] : 1;
+        }
+#pragma unroll
+        for (int dd = 0; dd < 8; ++dd) {
+            qd[dd] = wd[dd] != 0.0 ? qraw[dd] : 1;
             pow2 &= (qd[dd] & (qd[dd] - 1)) == 0;
             d += wd[dd];
         }
