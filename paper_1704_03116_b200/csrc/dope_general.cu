@@ -288,7 +288,7 @@ __global__ void k_init_state_g(LatG L, int64_t n, int64_t ncopy) {
 // K2g: global step (admm.py:136-151, 172-180), one thread per pixel
 // ---------------------------------------------------------------------------
 #ifndef KG_MINB
-#define KG_MINB 3
+#define KG_MINB 4
 #endif
 __global__ void __launch_bounds__(256, KG_MINB) k_global_g(LatG L, int boxw, int M) {
     const dope_run_state *st = L.st;
