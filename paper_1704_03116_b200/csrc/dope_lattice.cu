@@ -118,8 +118,15 @@ struct K1Tune {
     int32_t max_rounds;
 };
 
+// resident CTAs per SM the register allocation must allow for the 256-thread
+// 64x64 kernel: 5 (= its shared-memory limit; 48 registers, measured on C3
+// against 4 and unbounded)
+#ifndef K1_MINB
+#define K1_MINB 5
+#endif
+#define K1_MINB_OF(nt) ((nt) == 256 ? K1_MINB : 1)
 template <int BH, int BW, int NT>
-__global__ void __launch_bounds__(NT) k_block_mincut(Lat2 L, K1Tune T) {
+__global__ void __launch_bounds__(NT, (K1_MINB_OF(NT))) k_block_mincut(Lat2 L, K1Tune T) {
     using C = K1Cfg<BH, BW, NT>;
     constexpr int M = C::M, NPT = C::NPT, NW = C::NW;
     extern __shared__ __align__(16) uint8_t smem[];
