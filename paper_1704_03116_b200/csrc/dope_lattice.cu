@@ -124,7 +124,13 @@ struct K1Tune {
 #ifndef K1_MINB
 #define K1_MINB 5
 #endif
-#define K1_MINB_OF(nt) ((nt) == 256 ? K1_MINB : 1)
+#ifndef K1_MINB128
+#define K1_MINB128 1
+#endif
+#ifndef K1_MINB64
+#define K1_MINB64 1
+#endif
+#define K1_MINB_OF(nt) ((nt) == 256 ? K1_MINB : ((nt) == 128 ? K1_MINB128 : ((nt) == 64 ? K1_MINB64 : 1)))
 template <int BH, int BW, int NT>
 __global__ void __launch_bounds__(NT, (K1_MINB_OF(NT))) k_block_mincut(Lat2 L, K1Tune T) {
     using C = K1Cfg<BH, BW, NT>;
