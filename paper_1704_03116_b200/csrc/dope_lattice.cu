@@ -130,9 +130,13 @@ struct K1Tune {
 #ifndef K1_MINB64
 #define K1_MINB64 1
 #endif
-#define K1_MINB_OF(nt) ((nt) == 256 ? K1_MINB : ((nt) == 128 ? K1_MINB128 : ((nt) == 64 ? K1_MINB64 : 1)))
+// 64x64 with 512 threads (the wide variant): 2 CTAs/SM (68 registers would
+// leave one -- C5 b64 K1 18.9 vs 21.3 us)
+#define K1_MINB_OF(bh, nt)                                                                                \
+    ((bh) == 64 && (nt) == 512 ? 2                                                                        \
+                               : ((nt) == 256 ? K1_MINB : ((nt) == 128 ? K1_MINB128 : ((nt) == 64 ? K1_MINB64 : 1))))
 template <int BH, int BW, int NT>
-__global__ void __launch_bounds__(NT, (K1_MINB_OF(NT))) k_block_mincut(Lat2 L, K1Tune T) {
+__global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 L, K1Tune T) {
     using C = K1Cfg<BH, BW, NT>;
     constexpr int M = C::M, NPT = C::NPT, NW = C::NW;
     extern __shared__ __align__(16) uint8_t smem[];
