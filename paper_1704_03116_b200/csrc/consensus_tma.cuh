@@ -291,7 +291,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // residual sum included, see rsq_excess), so results do not depend on which
 // CTA took a block.
 template <int TW, int TH_, int NT_, int STAGES_>
-__global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? 4 : (NT_ <= 256 ? 2 : 1)))
+#ifndef K2T_CPS
+#define K2T_CPS 4
+#endif
+__global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 ? 2 : 1)))
     k_consensus_tma(Lat2 L, const __grid_constant__ TmaMaps M, uint32_t kx_magic, int settle) {
     using C = TmaCfg<TW, TH_, NT_, STAGES_>;
     constexpr int TH = C::TH, NT = C::NT, QPT = C::QPT, QR = TW / 4, LQ = (TW == 64) ? 4 : 5;

@@ -1443,7 +1443,10 @@ static const Variant3 *pick_variant3(int maxd, int maxh, int maxw) {
 
 static int k2_tma_width(const Lat2 &o);
 static int sm_count();
-constexpr int K2_CPS_FWD = 4;
+#ifndef K2T_CPS
+#define K2T_CPS 4   // persistent TMA consensus CTAs per SM
+#endif
+constexpr int K2_CPS_FWD = K2T_CPS;
 
 static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
                       const Variant3 **var3 = nullptr) {
