@@ -151,13 +151,29 @@ typedef struct dope_lattice {
      * 3D ones only need them on a side whose ghost flag is set). */
     int32_t ghost_up;           /* a neighbour shard exists above / before     */
     int32_t ghost_dn;           /* a neighbour shard exists below / after      */
-    int32_t sharded;            /* run-loop consensus publishes agg[] instead
-                                   of deciding; call dope_decide after the
-                                   cross-rank all-reduce                       */
-    int64_t *agg;               /* 4: [E (sum), R2 as double bits (sum),
-                                   max block residual^2 (max), clamped (max)] */
-    void *halo;                 /* sharded: 16 * U bytes of halo staging, U = W
-                                   (2D) or dims[1] * dims[2] (3D)              */
+    int32_t sharded;            /* run-loop consensus publishes its slot of
+                                   agg[] instead of deciding; dope_decide
+                                   reduces the gathered table                  */
+    int64_t *agg;               /* sharded: 8 * shard_count int64, one slot per
+                                   shard: [energy of y_{t-1}, sum of block
+                                   ||yhat - y||^2, sum of their rounding
+                                   excesses x 2^53, max block ||.||^2, clamped,
+                                   end-of-run energy, 0, 0] -- exact integers,
+                                   reduced in shard order by dope_decide      */
+    void *halo;                 /* sharded: dope_halo_bytes(L) bytes: boundary
+                                   rows out / in (U bytes each, U = W in 2D,
+                                   dims[1] * dims[2] in 3D) and the int16
+                                   multipliers of the two ghost rows / planes */
+    /* Audit mode (optional, NULL = off): after every iteration of the run
+     * loop the device adds the iteration's state digest -- position-weighted
+     * sums of yhat, 2y and a, oracle/dope_oracle.c state_digest -- into
+     * trace_hash[3 (t - 1) .. 3 (t - 1) + 2]; the buffer holds 3 * max_iters
+     * + 2 words and must be zeroed before the run.  hash_base = global index
+     * of this lattice's first pixel (a shard of a larger grid), else 0.     */
+    uint64_t *trace_hash;
+    int64_t hash_base;
+    int32_t shard_index;        /* sharded: this shard's slot in agg[]          */
+    int32_t shard_count;        /* sharded: number of shards (slots in agg[])   */
 } dope_lattice;
 
 /* Library / ABI identification; "b200-sm100a". */
@@ -195,8 +211,20 @@ int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void 
 /* End of run (admm.py:300-310): energy + best check of the last iterate;
  * the current iterate becomes the best one unless converged. */
 int dope_finish_run(const dope_lattice *L, void *stream);
-/* Sharded run loop: apply the all-reduced agg[] (trace, best, stop). */
+/* Sharded run loop: reduce the gathered agg[] table in shard order and apply
+ * it (trace, best, stop) -- identical on every shard. */
 int dope_decide(const dope_lattice *L, void *stream);
+/* Sharded run loop, after the consensus pass (before dope_decide): new
+ * iterate and multipliers of the ghost rows / planes computed locally from
+ * the exchanged labels (replaces a y-halo exchange); marks the adjacent local
+ * blocks dirty where the ghost iterate moved.  Blocks must be >= 2 rows /
+ * planes deep along the sharded axis (else DOPE_E_GEOMETRY). */
+int dope_ghost_consensus(const dope_lattice *L, void *stream);
+/* Bytes of the sharded halo buffer (L->halo) for this geometry. */
+int64_t dope_halo_bytes(const dope_lattice *L);
+/* Audit mode: add this iteration's state digest into L->trace_hash (no-op
+ * when trace_hash is NULL or the iteration was already digested). */
+int dope_trace_digest(const dope_lattice *L, void *stream);
 /* Sharded run loop: install the neighbour shards' boundary rows (2D) /
  * planes (3D) into the ghost rows / planes; which = 0: labels (uint8[U]),
  * 1: current y2 (uint8[U], marks the adjacent local blocks dirty where it
@@ -209,23 +237,41 @@ int dope_ghost_update(const dope_lattice *L, int32_t which, const void *up_row,
 int dope_pack_rows(const dope_lattice *L, int32_t which, void *first_row, void *last_row,
                    void *stream);
 /* dope_finish_run in two halves for sharded runs: the local energy of the
- * current iterate into state.energy_acc (all-reduce it across shards), then
- * the final decision. */
+ * current iterate into this shard's agg slot (gather the table across
+ * shards), then the final decision on the summed energy. */
 int dope_energy_local(const dope_lattice *L, void *stream);
 int dope_finish_decide(const dope_lattice *L, void *stream);
 /* Multi-GPU (NCCL over NVLink / NVSwitch), one rank per GPU, 2D and 3D
- * lattices (slabs of block rows / block planes).
+ * lattices (slabs of block rows / block planes).  Per iteration: K1, ONE
+ * grouped send/recv of the boundary label rows, the consensus pass,
+ * dope_ghost_consensus, ONE all-gather of the 64-byte agg slots, dope_decide.
  * dope_comm_unique_id on rank 0, broadcast the 128 bytes, dope_comm_init on
- * every rank.  dope_sharded_run runs `iters` iterations of the sharded loop
- * (K1, label halo, consensus, all-reduce of agg[], dope_decide, y halo) --
+ * every rank.  dope_sharded_run runs `iters` iterations of that loop --
  * captured in one CUDA graph when use_graph; dope_sharded_finish ends the
- * run (energy of the last iterate all-reduced, final decision). */
+ * run (energy of the last iterate gathered, final decision). */
 int dope_comm_unique_id(uint8_t *out128);
 int dope_comm_init(int32_t rank, int32_t world, const uint8_t *id128, void **comm_out);
+/* Loopback communicator: all `world` shards of one grid held by THIS process
+ * on one device -- the single-GPU stand-in for `world` ranks.  It runs the
+ * same iteration (and graph capture) as the NCCL communicator: each boundary
+ * row travels by one cudaMemcpyAsync into the receiver's halo slot, each agg
+ * slot by one copy into every peer's table; no kernel waits on another. */
+int dope_comm_loopback(int32_t world, void **comm_out);
 int dope_comm_destroy(void *comm);
+/* One shard (NCCL communicator: this rank's slab). */
 int dope_sharded_run(const dope_lattice *L, void *comm, int32_t iters, int32_t use_graph,
                      void *stream);
 int dope_sharded_finish(const dope_lattice *L, void *comm, void *stream);
+/* All shards a communicator holds in this process: 1 for NCCL, `world` for
+ * loopback (shards[r].shard_index == r). */
+int dope_sharded_run_group(const dope_lattice *const *shards, int32_t nshards, void *comm,
+                           int32_t iters, int32_t use_graph, void *stream);
+int dope_sharded_finish_group(const dope_lattice *const *shards, int32_t nshards, void *comm,
+                              void *stream);
+/* Instantiated run-loop graphs held by the library (bounded LRU per loop
+ * kind, DOPE_GRAPH_CACHE entries each) and a way to drop them all. */
+int64_t dope_graph_cache_entries(void);
+void dope_graph_cache_clear(void);
 /* binarize (admm.py:260-262) of the current iterate into out[n] (0/1). */
 int dope_binarize(const dope_lattice *L, uint8_t *out, void *stream);
 /* evaluate_energy of an arbitrary doubled labeling y2 (int path):
@@ -277,6 +323,8 @@ typedef struct dope_lattice_f {
     dope_run_state *state;
     double *trace_energy, *trace_residual_sq, *trace_max_residual;
     int32_t *trace_clamped;
+    uint64_t *trace_hash;       /* optional audit digests (labels only), as in
+                                   dope_lattice                                */
 } dope_lattice_f;
 
 int64_t dope_f_resid_stride(const dope_lattice_f *L);

@@ -820,15 +820,47 @@ typedef struct {
     double mu_final;
 } oracle_run_info;
 
+/* Per-iteration state digest (test fixtures only; no reference counterpart).
+ * H_k = sum over pixels g of v_k(g) * mix64(3 g + k) mod 2^64 for
+ * v_0 = yhat, v_1 = 2 y (an integer on the q == 1 integer configs), v_2 = a
+ * (integer there): an order-independent position-weighted sum, so a GPU
+ * reduction in any order -- or per-shard partial sums with a global index
+ * base -- gives the same three words.  mix64 = the splitmix64 finaliser. */
+static inline uint64_t mix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+static void state_digest(int64_t n, const uint8_t *yhat, const double *y, const double *a,
+                         uint64_t *out3) {
+    uint64_t h0 = 0, h1 = 0, h2 = 0;
+    for (int64_t g = 0; g < n; g++) {
+        const uint64_t b = 3 * (uint64_t)g;
+        h0 += (uint64_t)yhat[g] * mix64(b);
+        h1 += (uint64_t)(int64_t)llround(2.0 * y[g]) * mix64(b + 1);
+        h2 += (uint64_t)(int64_t)llround(a[g]) * mix64(b + 2);
+    }
+    out3[0] = h0; out3[1] = h1; out3[2] = h2;
+}
+
+int oracle_state_digest(int64_t n, const uint8_t *yhat, const double *y, const double *a,
+                        uint64_t *out3) {
+    state_digest(n, yhat, y, a, out3);
+    return 0;
+}
+
 /* run (admm.py:265-310) with the trace of admm.py:291-299.
- * trace_* arrays have max_iters entries; yhat_hist (optional) max_iters*n.
+ * trace_* arrays have max_iters entries; yhat_hist (optional) max_iters*n;
+ * digests (optional) 3*max_iters words of state_digest per iteration.
  * y (in: ignored, out: state.y after run, i.e. best iterate when not
  * converged), a (out: final multipliers, global layout), yhat (out: final
  * block labels, global layout), labels (out: binarize(state.y)). */
 int oracle_run(const oracle_lattice *L, double mu0, double mu_fact, double eps, int32_t max_iters,
                int threads, double *y, double *a, uint8_t *yhat, int8_t *labels,
                double *tr_mu, double *tr_energy, double *tr_ressq, double *tr_maxres,
-               int32_t *tr_clamped, uint8_t *yhat_hist, oracle_run_info *info) {
+               int32_t *tr_clamped, uint8_t *yhat_hist, uint64_t *digests, oracle_run_info *info) {
     lattice_ctx c;
     if (ctx_init(&c, L)) { ctx_free(&c); return -1; }
     int64_t n = c.n, K = c.K;
@@ -856,6 +888,9 @@ int oracle_run(const oracle_lattice *L, double mu0, double mu_fact, double eps, 
         if (e < best_e) { best_e = e; memcpy(best_y, y, sizeof(double) * n); info->best_iteration = it; }
         for (int64_t g = 0; g < n; g++) a[g] = a[g] + ((double)yhat[g] - y[g]);
         mu *= mu_fact;
+        /* digest of (yhat_t, y_t, a_t) after the multiplier update -- what the
+         * device state holds at the end of iteration t */
+        if (digests) state_digest(n, yhat, y, a, digests + 3 * (int64_t)(it - 1));
         if (K == 0 || maxres <= eps) { info->converged = 1; break; }
     }
     if (!rc && !info->converged) memcpy(y, best_y, sizeof(double) * n);

@@ -62,7 +62,9 @@ def lib():
                                            C.POINTER(C.c_double)]
         _lib.oracle_run.restype = C.c_int
         _lib.oracle_run.argtypes = [C.POINTER(_Lattice), C.c_double, C.c_double, C.c_double,
-                                    C.c_int32, C.c_int] + [C.c_void_p] * 10 + [C.POINTER(_RunInfo)]
+                                    C.c_int32, C.c_int] + [C.c_void_p] * 11 + [C.POINTER(_RunInfo)]
+        _lib.oracle_state_digest.restype = C.c_int
+        _lib.oracle_state_digest.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.oracle_update_blocks.restype = C.c_int
         _lib.oracle_update_blocks.argtypes = [C.POINTER(_Lattice), C.c_void_p, C.c_void_p,
                                               C.c_double, C.c_void_p, C.c_int]
@@ -153,7 +155,7 @@ class LatticeSpec:
 
 
 def run(spec: LatticeSpec, mu0: float, mu_fact: float, eps: float, max_iters: int,
-        threads: int = 1, keep_history: bool = False) -> dict:
+        threads: int = 1, keep_history: bool = False, digests: bool = False) -> dict:
     s, keep = spec._struct()
     n = spec.n
     y = np.empty(n)
@@ -163,11 +165,13 @@ def run(spec: LatticeSpec, mu0: float, mu_fact: float, eps: float, max_iters: in
     tr = {k: np.zeros(max_iters) for k in ("mu", "energy", "residual_sq", "max_block_residual")}
     clamped = np.zeros(max_iters, dtype=np.int32)
     hist = np.zeros((max_iters, n), dtype=np.uint8) if keep_history else None
+    dig = np.zeros((max_iters, 3), dtype=np.uint64) if digests else None
     info = _RunInfo()
     rc = lib().oracle_run(C.byref(s), mu0, mu_fact, eps, max_iters, threads, _ptr(y), _ptr(a),
                           _ptr(yhat), _ptr(labels), _ptr(tr["mu"]), _ptr(tr["energy"]),
                           _ptr(tr["residual_sq"]), _ptr(tr["max_block_residual"]), _ptr(clamped),
-                          _ptr(hist) if hist is not None else None, C.byref(info))
+                          _ptr(hist) if hist is not None else None,
+                          _ptr(dig) if dig is not None else None, C.byref(info))
     if rc:
         raise RuntimeError(f"oracle_run failed ({rc})")
     it = info.iterations
@@ -177,6 +181,18 @@ def run(spec: LatticeSpec, mu0: float, mu_fact: float, eps: float, max_iters: in
                best_iteration=int(info.best_iteration), mu_final=info.mu_final)
     if hist is not None:
         out["yhat_history"] = hist[:it].copy()
+    if dig is not None:
+        out["digests"] = dig[:it].copy()
+    return out
+
+
+def state_digest(yhat, y, a) -> np.ndarray:
+    """(yhat, 2y, a) position-weighted digest of one state (dope_oracle.c state_digest)."""
+    yhat = np.ascontiguousarray(yhat, dtype=np.uint8)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    out = np.zeros(3, dtype=np.uint64)
+    lib().oracle_state_digest(yhat.size, _ptr(yhat), _ptr(y), _ptr(a), _ptr(out))
     return out
 
 

@@ -82,6 +82,10 @@ class Lattice(C.Structure):
         ("sharded", C.c_int32),
         ("agg", C.c_void_p),
         ("halo", C.c_void_p),
+        ("trace_hash", C.c_void_p),
+        ("hash_base", C.c_int64),
+        ("shard_index", C.c_int32),
+        ("shard_count", C.c_int32),
     ]
 
 
@@ -116,6 +120,7 @@ class LatticeF(C.Structure):
         ("trace_residual_sq", C.c_void_p),
         ("trace_max_residual", C.c_void_p),
         ("trace_clamped", C.c_void_p),
+        ("trace_hash", C.c_void_p),
     ]
 
 
@@ -183,7 +188,7 @@ def lib():
     lb.dope_lattice_check.argtypes = [P]
     for name in ("dope_admm_init", "dope_update_blocks", "dope_update_global",
                  "dope_update_multipliers", "dope_finish_run", "dope_energy_local",
-                 "dope_finish_decide"):
+                 "dope_finish_decide", "dope_ghost_consensus", "dope_trace_digest"):
         f = getattr(lb, name)
         f.restype = C.c_int
         f.argtypes = [P, C.c_void_p]
@@ -201,6 +206,19 @@ def lib():
     lb.dope_sharded_run.argtypes = [P, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
     lb.dope_sharded_finish.restype = C.c_int
     lb.dope_sharded_finish.argtypes = [P, C.c_void_p, C.c_void_p]
+    lb.dope_comm_loopback.restype = C.c_int
+    lb.dope_comm_loopback.argtypes = [C.c_int32, C.POINTER(C.c_void_p)]
+    PP = C.POINTER(P)
+    lb.dope_sharded_run_group.restype = C.c_int
+    lb.dope_sharded_run_group.argtypes = [PP, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+    lb.dope_sharded_finish_group.restype = C.c_int
+    lb.dope_sharded_finish_group.argtypes = [PP, C.c_int32, C.c_void_p, C.c_void_p]
+    lb.dope_halo_bytes.restype = C.c_int64
+    lb.dope_halo_bytes.argtypes = [P]
+    lb.dope_graph_cache_entries.restype = C.c_int64
+    lb.dope_graph_cache_entries.argtypes = []
+    lb.dope_graph_cache_clear.restype = None
+    lb.dope_graph_cache_clear.argtypes = []
     lb.dope_pack_rows.restype = C.c_int
     lb.dope_pack_rows.argtypes = [P, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
     lb.dope_decide.restype = C.c_int
@@ -285,15 +303,3 @@ def check(rc: int, what: str) -> None:
         msg = "CUDA error: " + (lib().dope_last_cuda_error().decode() or
                                 lib().dope_f_last_error().decode())
     raise DopeError(f"{what} failed ({rc}): {msg}")
-
-
-def exported_symbols() -> list[str]:
-    return ["dope_backend_name", "dope_abi_version", "dope_last_cuda_error", "dope_resid_stride",
-            "dope_scratch_stride",
-            "dope_lattice_check", "dope_admm_init", "dope_update_blocks", "dope_update_global",
-            "dope_update_multipliers", "dope_admm_run", "dope_finish_run", "dope_binarize", "dope_decide", "dope_ghost_update",
-            "dope_pack_rows", "dope_energy_local", "dope_finish_decide", "dope_prepare_kernels",
-            "dope_comm_unique_id", "dope_comm_init", "dope_comm_destroy", "dope_sharded_run",
-            "dope_sharded_finish", "dope_f_resid_stride", "dope_f_check", "dope_f_last_error",
-            "dope_f_admm_init", "dope_f_update_blocks", "dope_f_update_global",
-            "dope_f_update_multipliers", "dope_f_admm_run", "dope_f_finish_run", "dope_f_binarize", "dope_energy4", "dope_bk_maxflow", "dope_bk_workspace_bytes"]

@@ -77,6 +77,7 @@ class AdmmConfig:
     warm_start: bool = True
     skip_clean: bool = True
     use_graph: bool = True
+    digests: bool = False       # audit mode: AdmmState.digests[t] = state digest of iteration t
 
     def __post_init__(self):
         if self.mu0 is not None and self.mu0 <= 0:
@@ -147,7 +148,7 @@ class _FloatDeviceState:
     """Caller-owned device buffers of one float-weight run (dope_lattice_f)."""
 
     def __init__(self, problems: BlockProblems, mu: float, eps: float, max_iters: int,
-                 warm_start: bool, skip_clean: bool):
+                 warm_start: bool, skip_clean: bool, digests: bool = False):
         import torch
         low: FloatLowering = problems.lowering
         dev = problems.device
@@ -199,6 +200,10 @@ class _FloatDeviceState:
         L.state = self.state.data_ptr()
         L.trace_energy, L.trace_residual_sq = self.tr_e.data_ptr(), self.tr_rs.data_ptr()
         L.trace_max_residual, L.trace_clamped = self.tr_mr.data_ptr(), self.tr_cl.data_ptr()
+        self.trace_hash = (torch.zeros(3 * max_iters + 2, dtype=torch.int64, device=dev)
+                           if digests else None)
+        if digests:
+            L.trace_hash = self.trace_hash.data_ptr()
         _lib.check(lb.dope_f_check(C.byref(L)), "dope_f_check")
 
     _NAMES = {"dope_admm_init": "dope_f_admm_init", "dope_update_blocks": "dope_f_update_blocks",
@@ -241,11 +246,12 @@ class _FloatDeviceState:
 
 
 def make_device_state(problems: BlockProblems, mu: float, eps: float, max_iters: int,
-                      warm_start: bool = True, skip_clean: bool = True):
-    """Device buffers of one run for the lowering kind (int or float lattice)."""
+                      warm_start: bool = True, skip_clean: bool = True, digests: bool = False):
+    """Device buffers of one run for the lowering kind (int or float lattice).
+    digests: audit mode, per-iteration state digests in .trace_hash."""
     if problems.kind == "float":
-        return _FloatDeviceState(problems, mu, eps, max_iters, warm_start, skip_clean)
-    return _DeviceState(problems, int(mu), eps, max_iters, warm_start, skip_clean)
+        return _FloatDeviceState(problems, mu, eps, max_iters, warm_start, skip_clean, digests)
+    return _DeviceState(problems, int(mu), eps, max_iters, warm_start, skip_clean, digests)
 
 
 def assemble_block_problems(model: EnergyModel, partition: Partition) -> BlockProblems:
@@ -256,7 +262,7 @@ class _DeviceState:
     """Caller-owned device buffers of one run (include/dope_b200.h)."""
 
     def __init__(self, problems: BlockProblems, mu: int, eps: float, max_iters: int,
-                 warm_start: bool, skip_clean: bool):
+                 warm_start: bool, skip_clean: bool, digests: bool = False):
         import torch
         low = problems.lowering
         dev = problems.device
@@ -331,6 +337,11 @@ class _DeviceState:
         L.trace_max_residual = self.tr_mr.data_ptr()
         L.trace_clamped = self.tr_cl.data_ptr()
         L.agg = self.agg.data_ptr()
+        # audit mode: per-iteration (yhat, 2y, a) digests (dope_lattice.trace_hash)
+        self.trace_hash = (torch.zeros(3 * max_iters + 2, dtype=torch.int64, device=dev)
+                           if digests else None)
+        if digests:
+            L.trace_hash = self.trace_hash.data_ptr()
         _lib.check(lb.dope_lattice_check(C.byref(L)), "dope_lattice_check")
 
     def stream(self):
@@ -388,6 +399,7 @@ class AdmmState:
         self.best_iteration = 0
         self.clamped_last = False
         self.trace: list = []
+        self.digests = None     # (iterations, 3) uint64 when AdmmConfig.digests
         self._dev: _DeviceState | None = None
         self._n = partition.shape.n
 
@@ -399,7 +411,7 @@ class AdmmState:
         mu = self.mu
         if problems.kind == "float":
             self._dev = _FloatDeviceState(problems, mu, eps, max_iters or config.max_iters,
-                                          config.warm_start, config.skip_clean)
+                                          config.warm_start, config.skip_clean, config.digests)
             self._dev.call("dope_admm_init")
             return self._dev
         if mu != round(mu) or mu <= 0:
@@ -407,7 +419,7 @@ class AdmmState:
         if problems.lowering.lamw % int(mu) != 0:
             raise NotImplementedError("the integer lattice path needs lambda*w divisible by mu")
         self._dev = _DeviceState(problems, int(mu), eps, max_iters or config.max_iters,
-                                 config.warm_start, config.skip_clean)
+                                 config.warm_start, config.skip_clean, config.digests)
         self._dev.call("dope_admm_init")
         return self._dev
 
@@ -574,5 +586,7 @@ def run(model: EnergyModel, partition: Partition, config: AdmmConfig,
     state.converged = bool(rs.converged)
     state.best_iteration = int(rs.best_iteration)
     state.clamped_last = bool(cl[it - 1]) if it else False
+    if dev.trace_hash is not None:
+        state.digests = dev.trace_hash[:3 * it].cpu().numpy().view(np.uint64).reshape(it, 3)
     labels = dev.binarize().to(torch.int8).cpu().numpy()
     return labels, state

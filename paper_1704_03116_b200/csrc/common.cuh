@@ -214,4 +214,67 @@ __device__ int bfs_relabel(const uint64_t *__restrict__ masks, uint64_t *__restr
     return __any_sync(FULLMASK, hit);
 }
 
+// ---------------------------------------------------------------------------
+// Per-iteration state digest (test / audit mode: dope_lattice.trace_hash).
+// H_k = sum_g v_k(g) * mix64(3 (base + g) + k) mod 2^64 over the iteration's
+// labels (k = 0), 2y (k = 1) and multipliers (k = 2): order-independent, so
+// any reduction order -- and per-shard sums with a global index base -- give
+// the words the CPU oracle computes (oracle/dope_oracle.c state_digest).
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+// One thread: open iteration st.iteration's digest slot unless it was already
+// taken (a launch after the run stopped is a no-op).  h holds 3 * max_iters
+// digest words followed by two control words: [last digested iteration, active].
+template <typename State>
+__global__ void k_digest_begin(const State *st, uint64_t *h, int max_iters) {
+    const int it = st->iteration;
+    uint64_t *ctl = h + 3 * (size_t)max_iters;
+    if (it >= 1 && it <= max_iters && (int64_t)ctl[0] != it) {
+        ctl[0] = (uint64_t)it;
+        ctl[1] = 1;
+        h[3 * (size_t)(it - 1)] = 0;
+        h[3 * (size_t)(it - 1) + 1] = 0;
+        h[3 * (size_t)(it - 1) + 2] = 0;
+    } else {
+        ctl[1] = 0;
+    }
+}
+
+// y (k = 1) and a (k = 2) may be null (float path: only the labels are integers).
+template <typename State, typename YT, typename AT>
+__global__ void __launch_bounds__(256) k_digest(const State *st, uint64_t *h, int max_iters, int64_t n,
+                                                int64_t base, const uint8_t *__restrict__ yhat,
+                                                const YT *y0, const YT *y1, const YT *y2,
+                                                const AT *__restrict__ a) {
+    const uint64_t *ctl = h + 3 * (size_t)max_iters;
+    if (!ctl[1]) return;
+    const int64_t it = (int64_t)ctl[0];
+    const int cur = st->ycur;
+    const YT *__restrict__ y = cur == 0 ? y0 : (cur == 1 ? y1 : y2);
+    uint64_t s0 = 0, s1 = 0, s2 = 0;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = 3 * (uint64_t)(base + g);
+        s0 += (uint64_t)yhat[g] * mix64(b);
+        if (y) s1 += (uint64_t)(int64_t)y[g] * mix64(b + 1);
+        if (a) s2 += (uint64_t)(int64_t)a[g] * mix64(b + 2);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_down_sync(FULLMASK, s0, o);
+        s1 += __shfl_down_sync(FULLMASK, s1, o);
+        s2 += __shfl_down_sync(FULLMASK, s2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        unsigned long long *slot = reinterpret_cast<unsigned long long *>(h + 3 * (size_t)(it - 1));
+        atomicAdd(slot, (unsigned long long)s0);
+        atomicAdd(slot + 1, (unsigned long long)s1);
+        atomicAdd(slot + 2, (unsigned long long)s2);
+    }
+}
+
 }  // namespace dope

@@ -1,12 +1,25 @@
-// dope_comm.cu -- multi-GPU sharded ADMM loop over NCCL (NVLink / NVSwitch).
+// dope_comm.cu -- the sharded ADMM loop: slabs of whole block rows (2D) /
+// block planes (3D) over several GPUs (NCCL over NVLink / NVSwitch), or over
+// several shards held by one process (loopback: the single-GPU stand-in).
 //
-// One rank per GPU owns a slab of whole block rows (paper_1704_03116_b200/
-// sharded.py describes the protocol).  Per iteration the only cross-rank
-// traffic is two one-row halos (labels after K1, the new iterate after the
-// consensus pass) -- grouped ncclSend/ncclRecv with the slab neighbours -- and
-// an all-reduce of four scalars.  The whole iteration, NCCL calls included,
-// is captured into one CUDA graph.
+// The reference parallelises only update_blocks, with a thread pool inside one
+// process (admm.py:128-132); the cross-block coupling is a one-pixel halo
+// (SURVEY.md §8(e)).  Per iteration, on every shard:
 //
+//   1. K1 (dope_update_blocks) on the slab;
+//   2. label halo: the first / last local row of yhat to the slab neighbours
+//      (one grouped ncclSend/ncclRecv; loopback: one cudaMemcpyAsync per row)
+//      and into the ghost rows (dope_ghost_update);
+//   3. the consensus pass (dope_update_global), which writes this shard's
+//      64-byte slot of the agg table (exact integers);
+//   4. dope_ghost_consensus: the ghost rows' new iterate and multipliers,
+//      recomputed locally from the labels of step 2 (no y halo);
+//   5. one all-gather of the agg slots (loopback: one copy per peer table);
+//   6. dope_decide: the table reduced in shard order -- the same trace entry,
+//      best iterate and stop decision on every shard, bit-identical to the
+//      single-GPU run.
+//
+// The whole iteration, NCCL calls included, is captured into one CUDA graph.
 // NCCL is loaded at run time (dlopen of libnccl.so.2: the copy PyTorch has
 // already loaded is reused), so single-GPU users never need it.
 #include <cuda_runtime.h>
@@ -15,13 +28,16 @@
 #include <stdio.h>
 #include <string.h>
 
-#include <map>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "dope_b200.h"
+#include "graph_cache.cuh"
 
 namespace dope_comm {
+
+using dope::GraphCache;
 
 // --- minimal NCCL ABI (nccl.h 2.x) ----------------------------------------
 typedef struct ncclComm *ncclComm_t;
@@ -30,7 +46,6 @@ typedef struct {
 } ncclUniqueId;
 typedef enum { ncclSuccess = 0 } ncclResult_t;
 typedef enum { ncclInt8 = 0, ncclChar = 0, ncclInt32 = 2, ncclInt64 = 4, ncclFloat64 = 8 } ncclDataType_t;
-typedef enum { ncclSum = 0, ncclMax = 2 } ncclRedOp_t;
 
 struct Nccl {
     ncclResult_t (*GetUniqueId)(ncclUniqueId *);
@@ -40,8 +55,7 @@ struct Nccl {
     ncclResult_t (*GroupEnd)();
     ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
     ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
-    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
-                              cudaStream_t);
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
     const char *(*GetErrorString)(ncclResult_t);
     bool ok = false;
 };
@@ -61,64 +75,155 @@ static Nccl &nccl() {
         LOAD(GroupEnd, "ncclGroupEnd");
         LOAD(Send, "ncclSend");
         LOAD(Recv, "ncclRecv");
-        LOAD(AllReduce, "ncclAllReduce");
+        LOAD(AllGather, "ncclAllGather");
         LOAD(GetErrorString, "ncclGetErrorString");
 #undef LOAD
         n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.GroupStart && n.GroupEnd &&
-               n.Send && n.Recv && n.AllReduce;
+               n.Send && n.Recv && n.AllGather;
     });
     return n;
 }
 
-struct Comm {
-    ncclComm_t comm;
-    int rank, world;
+static int nc(ncclResult_t r) { return r == ncclSuccess ? DOPE_OK : DOPE_E_CUDA; }
+static int cu(cudaError_t e) { return e == cudaSuccess ? DOPE_OK : DOPE_E_CUDA; }
+
+constexpr int AGG_SLOT = 8;   // int64 per shard in the agg table (dope_lattice.cu)
+
+// exchanged unit: a row (2D) or a plane (3D), one byte per pixel (labels)
+static size_t unit_bytes(const dope_lattice *L) {
+    return L->ndim == 3 ? (size_t)L->dims[1] * L->dims[2] : (size_t)L->dims[1];
+}
+
+// halo buffer slots (dope_halo_bytes): first row out, last row out, from above, from below
+struct Halo {
+    uint8_t *first, *last, *up, *dn;
+    explicit Halo(const dope_lattice *L) {
+        const size_t U = unit_bytes(L);
+        uint8_t *h = static_cast<uint8_t *>(L->halo);
+        first = h;
+        last = h + U;
+        up = h + 2 * U;
+        dn = h + 3 * U;
+    }
 };
 
-static int nc(ncclResult_t r) { return r == ncclSuccess ? DOPE_OK : DOPE_E_CUDA; }
+// How the shards of one grid talk.  `S` are the shards this process holds.
+struct Transport {
+    int world = 1;
+    virtual ~Transport() {}
+    // boundary label rows -> the neighbours' "from above / below" halo slots
+    virtual int move_rows(const dope_lattice *const *S, int nloc, cudaStream_t s) = 0;
+    // every shard's agg slot -> every table
+    virtual int gather_agg(const dope_lattice *const *S, int nloc, cudaStream_t s) = 0;
+    // the shard with this index is held here
+    virtual int check_group(const dope_lattice *const *S, int nloc) const = 0;
+};
 
-// halo buffer layout (caller-owned, 4 slots of W * 4 bytes; each row uses W bytes):
-//   [0] send first row, [1] send last row, [2] recv from above, [3] recv from below
-static int exchange(const dope_lattice *L, const Comm &C, int which, cudaStream_t s) {
-    Nccl &N = nccl();
-    // the exchanged unit: a row (2D, slabs of block rows) or a plane (3D, slabs
-    // of block planes); labels and y2 are both one byte per pixel
-    const size_t W = L->ndim == 3 ? (size_t)L->dims[1] * L->dims[2] : (size_t)L->dims[1];
-    const size_t bytes = W;
-    uint8_t *h = static_cast<uint8_t *>(L->halo);
-    uint8_t *first = h, *last = h + 4 * W, *up = h + 8 * W, *dn = h + 12 * W;
-    int rc = dope_pack_rows(L, which, first, last, s);
-    if (rc) return rc;
-    if ((rc = nc(N.GroupStart()))) return rc;
-    if (C.rank > 0) {
-        if ((rc = nc(N.Send(first, bytes, ncclChar, C.rank - 1, C.comm, s)))) return rc;
-        if ((rc = nc(N.Recv(up, bytes, ncclChar, C.rank - 1, C.comm, s)))) return rc;
+struct NcclTransport : Transport {
+    ncclComm_t comm = nullptr;
+    int rank = 0;
+    int check_group(const dope_lattice *const *S, int nloc) const override {
+        return nloc == 1 && S[0]->shard_index == rank && S[0]->shard_count == world ? DOPE_OK : DOPE_E_ARGS;
     }
-    if (C.rank + 1 < C.world) {
-        if ((rc = nc(N.Send(last, bytes, ncclChar, C.rank + 1, C.comm, s)))) return rc;
-        if ((rc = nc(N.Recv(dn, bytes, ncclChar, C.rank + 1, C.comm, s)))) return rc;
+    int move_rows(const dope_lattice *const *S, int, cudaStream_t s) override {
+        Nccl &N = nccl();
+        const dope_lattice *L = S[0];
+        const Halo h(L);
+        const size_t U = unit_bytes(L);
+        int rc;
+        if ((rc = nc(N.GroupStart()))) return rc;
+        if (rank > 0) {
+            if ((rc = nc(N.Send(h.first, U, ncclChar, rank - 1, comm, s)))) return rc;
+            if ((rc = nc(N.Recv(h.up, U, ncclChar, rank - 1, comm, s)))) return rc;
+        }
+        if (rank + 1 < world) {
+            if ((rc = nc(N.Send(h.last, U, ncclChar, rank + 1, comm, s)))) return rc;
+            if ((rc = nc(N.Recv(h.dn, U, ncclChar, rank + 1, comm, s)))) return rc;
+        }
+        return nc(N.GroupEnd());
     }
-    if ((rc = nc(N.GroupEnd()))) return rc;
-    return dope_ghost_update(L, which, C.rank > 0 ? up : nullptr, C.rank + 1 < C.world ? dn : nullptr, s);
+    int gather_agg(const dope_lattice *const *S, int, cudaStream_t s) override {
+        // in place: this rank's slot is already at agg + AGG_SLOT * rank
+        int64_t *t = S[0]->agg;
+        return nc(nccl().AllGather(t + (size_t)AGG_SLOT * rank, t, AGG_SLOT, ncclInt64, comm, s));
+    }
+};
+
+struct LoopbackTransport : Transport {
+    int check_group(const dope_lattice *const *S, int nloc) const override {
+        if (nloc != world) return DOPE_E_ARGS;
+        for (int r = 0; r < nloc; ++r)
+            if (S[r]->shard_index != r || S[r]->shard_count != world) return DOPE_E_ARGS;
+        return DOPE_OK;
+    }
+    int move_rows(const dope_lattice *const *S, int nloc, cudaStream_t s) override {
+        int rc;
+        for (int r = 0; r < nloc; ++r) {
+            const Halo h(S[r]);
+            const size_t U = unit_bytes(S[r]);
+            if (r > 0 && (rc = cu(cudaMemcpyAsync(h.up, Halo(S[r - 1]).last, U, cudaMemcpyDeviceToDevice, s))))
+                return rc;
+            if (r + 1 < nloc &&
+                (rc = cu(cudaMemcpyAsync(h.dn, Halo(S[r + 1]).first, U, cudaMemcpyDeviceToDevice, s))))
+                return rc;
+        }
+        return DOPE_OK;
+    }
+    int gather_agg(const dope_lattice *const *S, int nloc, cudaStream_t s) override {
+        int rc;
+        for (int src = 0; src < nloc; ++src)
+            for (int dst = 0; dst < nloc; ++dst) {
+                if (dst == src) continue;
+                const size_t off = (size_t)AGG_SLOT * src;
+                if ((rc = cu(cudaMemcpyAsync(S[dst]->agg + off, S[src]->agg + off, AGG_SLOT * sizeof(int64_t),
+                                             cudaMemcpyDeviceToDevice, s))))
+                    return rc;
+            }
+        return DOPE_OK;
+    }
+};
+
+static int one_iteration(const dope_lattice *const *S, int nloc, Transport &T, cudaStream_t s) {
+    int rc;
+    for (int r = 0; r < nloc; ++r)
+        if ((rc = dope_update_blocks(S[r], s))) return rc;
+    for (int r = 0; r < nloc; ++r) {
+        const Halo h(S[r]);
+        if ((rc = dope_pack_rows(S[r], 0, h.first, h.last, s))) return rc;
+    }
+    if ((rc = T.move_rows(S, nloc, s))) return rc;
+    for (int r = 0; r < nloc; ++r) {
+        const Halo h(S[r]);
+        if ((rc = dope_ghost_update(S[r], 0, S[r]->ghost_up ? h.up : nullptr, S[r]->ghost_dn ? h.dn : nullptr,
+                                    s)))
+            return rc;
+    }
+    for (int r = 0; r < nloc; ++r)
+        if ((rc = dope_update_global(S[r], s))) return rc;
+    for (int r = 0; r < nloc; ++r)
+        if ((rc = dope_ghost_consensus(S[r], s))) return rc;
+    if ((rc = T.gather_agg(S, nloc, s))) return rc;
+    for (int r = 0; r < nloc; ++r)
+        if ((rc = dope_decide(S[r], s))) return rc;
+    for (int r = 0; r < nloc; ++r)
+        if ((rc = dope_trace_digest(S[r], s))) return rc;
+    return DOPE_OK;
 }
 
-static int allreduce_agg(const dope_lattice *L, const Comm &C, cudaStream_t s) {
-    Nccl &N = nccl();
-    int64_t *a = L->agg;
-    int rc;
-    if ((rc = nc(N.AllReduce(a, a, 1, ncclInt64, ncclSum, C.comm, s)))) return rc;
-    if ((rc = nc(N.AllReduce(a + 1, a + 1, 1, ncclFloat64, ncclSum, C.comm, s)))) return rc;
-    return nc(N.AllReduce(a + 2, a + 2, 2, ncclInt64, ncclMax, C.comm, s));
+static GraphCache &sharded_graphs() {
+    static GraphCache c;
+    return c;
 }
 
-static int one_iteration(const dope_lattice *L, const Comm &C, cudaStream_t s) {
-    int rc;
-    if ((rc = dope_update_blocks(L, s))) return rc;
-    if ((rc = exchange(L, C, 0, s))) return rc;
-    if ((rc = dope_update_global(L, s))) return rc;
-    if ((rc = allreduce_agg(L, C, s))) return rc;
-    if ((rc = dope_decide(L, s))) return rc;
-    return exchange(L, C, 1, s);
+static int check_shards(const dope_lattice *const *S, int nloc, const Transport &T) {
+    if (!S || nloc < 1) return DOPE_E_ARGS;
+    for (int r = 0; r < nloc; ++r) {
+        const dope_lattice *L = S[r];
+        if (!L || !L->halo || !L->agg || !L->sharded || !L->fuse_multipliers) return DOPE_E_ARGS;
+        int rc = dope_lattice_check(L);
+        if (rc) return rc;
+    }
+    return T.check_group(S, nloc);
 }
 
 }  // namespace dope_comm
@@ -142,84 +247,104 @@ int dope_comm_init(int32_t rank, int32_t world, const uint8_t *id128, void **com
     if (!N.ok || !id128 || !comm_out || world < 1 || rank < 0 || rank >= world) return DOPE_E_ARGS;
     ncclUniqueId id;
     memcpy(id.internal, id128, 128);
-    Comm *c = new Comm{nullptr, rank, world};
+    NcclTransport *c = new NcclTransport();
+    c->rank = rank;
+    c->world = world;
     int rc = nc(N.CommInitRank(&c->comm, world, id, rank));
     if (rc) {
         delete c;
         return rc;
     }
-    *comm_out = c;
+    *comm_out = static_cast<Transport *>(c);
+    return DOPE_OK;
+}
+
+int dope_comm_loopback(int32_t world, void **comm_out) {
+    if (world < 1 || !comm_out) return DOPE_E_ARGS;
+    LoopbackTransport *c = new LoopbackTransport();
+    c->world = world;
+    *comm_out = static_cast<Transport *>(c);
     return DOPE_OK;
 }
 
 int dope_comm_destroy(void *comm) {
     if (!comm) return DOPE_OK;
-    Comm *c = static_cast<Comm *>(comm);
-    int rc = nc(nccl().CommDestroy(c->comm));
-    delete c;
+    Transport *t = static_cast<Transport *>(comm);
+    sharded_graphs().erase_owner(comm);   // graphs captured against this communicator
+    int rc = DOPE_OK;
+    if (NcclTransport *n = dynamic_cast<NcclTransport *>(t)) rc = nc(nccl().CommDestroy(n->comm));
+    delete t;
     return rc;
 }
 
-int dope_sharded_run(const dope_lattice *L, void *comm, int32_t iters, int32_t use_graph,
-                     void *stream) {
-    if (!L || !comm || !L->halo || !L->sharded || !L->fuse_multipliers) return DOPE_E_ARGS;
-    const Comm &C = *static_cast<Comm *>(comm);
+int dope_sharded_run_group(const dope_lattice *const *S, int32_t nloc, void *comm, int32_t iters,
+                           int32_t use_graph, void *stream) {
+    if (!comm) return DOPE_E_ARGS;
+    Transport &T = *static_cast<Transport *>(comm);
     cudaStream_t s = (cudaStream_t)stream;
-    int rc = dope_lattice_check(L);
+    int rc = check_shards(S, nloc, T);
     if (rc) return rc;
     if (iters <= 0) return DOPE_OK;
     if (!use_graph) {
         for (int i = 0; i < iters; ++i)
-            if ((rc = one_iteration(L, C, s))) return rc;
+            if ((rc = one_iteration(S, nloc, T, s))) return rc;
         return DOPE_OK;
     }
-    static std::mutex mu;
-    static std::map<std::string, cudaGraphExec_t> cache;
-    std::string key((const char *)L, sizeof(*L));
+    std::string key;
+    for (int r = 0; r < nloc; ++r) key.append((const char *)S[r], sizeof(dope_lattice));
     key.append((const char *)&iters, sizeof(iters));
     key.append((const char *)&comm, sizeof(comm));
-    cudaGraphExec_t exec = nullptr;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        auto it = cache.find(key);
-        if (it != cache.end()) exec = it->second;
-    }
+    cudaGraphExec_t exec = sharded_graphs().find(key);
     if (!exec) {
         // outside capture: kernel attributes, and NCCL peer connections (the
-        // first send/recv / all-reduce on a communicator sets them up).  The
-        // warm-up exchange re-installs the neighbours' current boundary rows
-        // (a no-op on the state), the all-reduce only touches agg[], which the
-        // first consensus pass overwrites.
-        if ((rc = dope_prepare_kernels(L))) return rc;
-        if ((rc = exchange(L, C, 0, s))) return rc;
-        if ((rc = exchange(L, C, 1, s))) return rc;
-        if ((rc = allreduce_agg(L, C, s))) return rc;
+        // first send/recv / all-gather on a communicator sets them up).  The
+        // warm-up moves the current halo slots and agg tables, which the
+        // first iteration overwrites before reading.
+        for (int r = 0; r < nloc; ++r)
+            if ((rc = dope_prepare_kernels(S[r]))) return rc;
+        if ((rc = T.move_rows(S, nloc, s))) return rc;
+        if ((rc = T.gather_agg(S, nloc, s))) return rc;
         cudaStream_t cs;
-        if ((rc = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess ? DOPE_OK : DOPE_E_CUDA)) return rc;
+        if ((rc = cu(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)))) return rc;
         cudaGraph_t graph;
-        if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return DOPE_E_CUDA;
-        for (int i = 0; i < iters && !rc; ++i) rc = one_iteration(L, C, cs);
+        if ((rc = cu(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal)))) {
+            cudaStreamDestroy(cs);
+            return rc;
+        }
+        for (int i = 0; i < iters && !rc; ++i) rc = one_iteration(S, nloc, T, cs);
         cudaError_t e = cudaStreamEndCapture(cs, &graph);
-        if (rc) return rc;
-        if (e != cudaSuccess) return DOPE_E_CUDA;
-        if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) return DOPE_E_CUDA;
-        cudaGraphDestroy(graph);
         cudaStreamDestroy(cs);
-        std::lock_guard<std::mutex> lk(mu);
-        cache[key] = exec;
+        if (!rc && e != cudaSuccess) rc = DOPE_E_CUDA;
+        if (!rc) {
+            rc = cu(cudaGraphInstantiate(&exec, graph, 0));
+        }
+        if (e == cudaSuccess) cudaGraphDestroy(graph);
+        if (rc) return rc;
+        sharded_graphs().put(key, exec, comm);
     }
-    return cudaGraphLaunch(exec, s) == cudaSuccess ? DOPE_OK : DOPE_E_CUDA;
+    return cu(cudaGraphLaunch(exec, s));
+}
+
+int dope_sharded_finish_group(const dope_lattice *const *S, int32_t nloc, void *comm, void *stream) {
+    if (!comm) return DOPE_E_ARGS;
+    Transport &T = *static_cast<Transport *>(comm);
+    cudaStream_t s = (cudaStream_t)stream;
+    int rc = check_shards(S, nloc, T);
+    if (rc) return rc;
+    for (int r = 0; r < nloc; ++r)
+        if ((rc = dope_energy_local(S[r], s))) return rc;   // -> agg slot [5]
+    if ((rc = T.gather_agg(S, nloc, s))) return rc;
+    for (int r = 0; r < nloc; ++r)
+        if ((rc = dope_finish_decide(S[r], s))) return rc;
+    return DOPE_OK;
+}
+
+int dope_sharded_run(const dope_lattice *L, void *comm, int32_t iters, int32_t use_graph, void *stream) {
+    return dope_sharded_run_group(&L, 1, comm, iters, use_graph, stream);
 }
 
 int dope_sharded_finish(const dope_lattice *L, void *comm, void *stream) {
-    if (!L || !comm) return DOPE_E_ARGS;
-    const Comm &C = *static_cast<Comm *>(comm);
-    cudaStream_t s = (cudaStream_t)stream;
-    int rc;
-    if ((rc = dope_energy_local(L, s))) return rc;
-    int64_t *acc = &L->state->energy_acc;
-    if ((rc = nc(nccl().AllReduce(acc, acc, 1, ncclInt64, ncclSum, C.comm, s)))) return rc;
-    return dope_finish_decide(L, s);
+    return dope_sharded_finish_group(&L, 1, comm, stream);
 }
 
 }  // extern "C"

@@ -26,6 +26,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "graph_cache.cuh"
 #include "dope_b200.h"
 #include "mincut_core.cuh"
 
@@ -58,6 +59,7 @@ struct LatF {
     dope_run_state *st;
     double *tr_e, *tr_rs, *tr_mr;
     int32_t *tr_cl;
+    uint64_t *trace_hash;        // audit mode: per-iteration label digests (may be null)
 };
 
 // neighbour directions: E W S N SE NW SW NE (opposites d ^ 1)
@@ -667,6 +669,7 @@ static int build(const dope_lattice_f *L, LatF &o, const VarF **var) {
     o.pr = L->part_ressq;
     o.pf = L->part_flags;
     o.st = L->state;
+    o.trace_hash = L->trace_hash;
     o.tr_e = L->trace_energy;
     o.tr_rs = L->trace_residual_sq;
     o.tr_mr = L->trace_max_residual;
@@ -771,6 +774,15 @@ int dope_f_update_multipliers(const dope_lattice_f *L, void *stream) {
     return cuda_check(cudaGetLastError(), "update_multipliers_f");
 }
 
+// Audit mode: digest of the iteration's labels (y and a are not integers here).
+static int launch_digest_f(const LatF &o, cudaStream_t s) {
+    if (!o.trace_hash) return DOPE_OK;
+    k_digest_begin<<<1, 1, 0, s>>>(o.st, o.trace_hash, o.max_iters);
+    k_digest<dope_run_state, uint8_t, int16_t><<<2 * 148, 256, 0, s>>>(
+        o.st, o.trace_hash, o.max_iters, (int64_t)o.ay.dim * o.W, 0, o.yhat, nullptr, nullptr, nullptr, nullptr);
+    return cuda_check(cudaGetLastError(), "state digest");
+}
+
 int dope_f_admm_run(const dope_lattice_f *L, int32_t iters, int32_t use_graph, void *stream) {
     LatF o;
     const VarF *v;
@@ -782,19 +794,14 @@ int dope_f_admm_run(const dope_lattice_f *L, int32_t iters, int32_t use_graph, v
         for (int i = 0; i < iters; ++i) {
             if ((rc = launch_k1(o, v, s))) return rc;
             if ((rc = launch_k2(o, s))) return rc;
+            if ((rc = launch_digest_f(o, s))) return rc;
         }
         return DOPE_OK;
     }
-    static std::mutex mu;
-    static std::map<std::string, cudaGraphExec_t> cache;
+    static GraphCache cache;
     std::string key((const char *)L, sizeof(*L));
     key.append((const char *)&iters, sizeof(iters));
-    cudaGraphExec_t exec = nullptr;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        auto it = cache.find(key);
-        if (it != cache.end()) exec = it->second;
-    }
+    cudaGraphExec_t exec = cache.find(key);
     if (!exec) {
         if ((rc = configure(v))) return rc;
         cudaStream_t cs;
@@ -804,6 +811,7 @@ int dope_f_admm_run(const dope_lattice_f *L, int32_t iters, int32_t use_graph, v
         for (int i = 0; i < iters && !rc; ++i) {
             rc = launch_k1(o, v, cs);
             if (!rc) rc = launch_k2(o, cs);
+            if (!rc) rc = launch_digest_f(o, cs);
         }
         cudaError_t e = cudaStreamEndCapture(cs, &graph);
         if (rc) return rc;
@@ -812,8 +820,7 @@ int dope_f_admm_run(const dope_lattice_f *L, int32_t iters, int32_t use_graph, v
         cudaGraphDestroy(graph);
         cudaStreamDestroy(cs);
         if (rc) return rc;
-        std::lock_guard<std::mutex> lk(mu);
-        cache[key] = exec;
+        cache.put(key, exec);
     }
     return cuda_check(cudaGraphLaunch(exec, s), "graph launch");
 }

@@ -34,6 +34,7 @@
 
 #include "common.cuh"
 #include "dope_b200.h"
+#include "graph_cache.cuh"
 #include "mincut_core.cuh"
 
 namespace dope_g {
@@ -728,16 +729,10 @@ int dope_g_admm_run(const dope_general *L, int32_t iters, int32_t use_graph, voi
             if ((rc = one_iteration(o, v, s))) return rc;
         return DOPE_OK;
     }
-    static std::mutex mu;
-    static std::map<std::string, cudaGraphExec_t> cache;
+    static GraphCache cache;
     std::string key((const char *)L, sizeof(*L));
     key.append((const char *)&iters, sizeof(iters));
-    cudaGraphExec_t exec = nullptr;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        auto it = cache.find(key);
-        if (it != cache.end()) exec = it->second;
-    }
+    cudaGraphExec_t exec = cache.find(key);
     if (!exec) {
         cudaStream_t cs;
         if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return DOPE_E_CUDA;
@@ -750,8 +745,7 @@ int dope_g_admm_run(const dope_general *L, int32_t iters, int32_t use_graph, voi
         if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) return DOPE_E_CUDA;
         cudaGraphDestroy(graph);
         cudaStreamDestroy(cs);
-        std::lock_guard<std::mutex> lk(mu);
-        cache[key] = exec;
+        cache.put(key, exec);
     }
     return cuda_check(cudaGraphLaunch(exec, s), "graph launch");
 }

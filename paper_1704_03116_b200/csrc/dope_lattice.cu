@@ -33,6 +33,7 @@
 
 #include "dope_b200.h"
 #include "common.cuh"
+#include "graph_cache.cuh"
 
 
 namespace dope {
@@ -81,7 +82,25 @@ struct Lat2 {
     int32_t nib3;           // 3D: shared-memory K1 with nibble residual planes (lattice3d_smem.cuh)
     int32_t q3;             // 3D: u / a / y rows can be read as quads (W % 4 == 0, aligned)
     int32_t slist;          // K1 lists its solved blocks for the TMA consensus pass (solved_list)
+    uint64_t *trace_hash;   // audit mode: per-iteration state digests (may be null)
+    int64_t hash_base;      // global index of the first pixel (shards)
+    int32_t shard_index, shard_count;   // sharded: this shard's slot in the agg table
+    astore_t *ga_up, *ga_dn;            // sharded: multipliers of the ghost rows / planes
 };
+
+// Sharded mode: layout of the caller's halo buffer (dope_halo_bytes), U bytes
+// per exchanged row (2D) / plane (3D): [0, U) first local row out, [U, 2U) last
+// local row out, [2U, 3U) row received from above, [3U, 4U) from below, then
+// (8-byte aligned) the int16 multipliers of the ghost row above and below.
+__host__ __device__ inline int64_t halo_ga_offset(int64_t U) { return (4 * U + 7) / 8 * 8; }
+__host__ __device__ inline int64_t halo_bytes(int64_t U) { return halo_ga_offset(U) + 4 * U; }
+
+// agg table of the sharded run loop: AGG_SLOT int64 per shard, filled by each
+// shard's consensus pass (and end-of-run energy), gathered across shards
+// before dope_decide: [0] energy of y_{t-1}, [1] sum of block ss, [2] sum of
+// the residual excesses (rsq_excess), [3] max block ss, [4] clamp flag,
+// [5] end-of-run energy of the last iterate.
+constexpr int AGG_SLOT = 8;
 
 // Append block k to the solved-block list (see solved_list); dirty[8K + k] =
 // 1 + the block's latest slot.
@@ -547,6 +566,19 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
             }
         }
     }
+    if (L.ga_up) {   // sharded: multipliers of the ghost rows / planes
+        const int64_t U = L.ndim == 3 ? (int64_t)L.ay.dim * L.W : (int64_t)L.W;
+        for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < U; c += stride) {
+            L.ga_up[c] = 0;
+            L.ga_dn[c] = 0;
+            if (L.ndim == 2) {   // every rotating buffer's ghost rows start at y = 1/2
+                for (int b = 1; b < 3; ++b) {
+                    L.y2[b][-L.W + c] = 1;
+                    L.y2[b][(int64_t)L.ay.dim * L.W + c] = 1;
+                }
+            }
+        }
+    }
     if (L.ndim == 3 && L.scratch) {   // slab accumulators of the 3D consensus pass (slab_acc3)
         const size_t M = (size_t)L.boxd * L.boxh * L.boxw;
         unsigned long long *acc = reinterpret_cast<unsigned long long *>(L.scratch + (size_t)L.K * (7 * M + 128));
@@ -666,30 +698,6 @@ __device__ void apply_iteration(const Lat2 &L, const dope_run_state &s0, int64_t
     st->ycur = out;
 }
 
-// Apply one consensus pass's global aggregates (pair energy E of y_{t-1},
-// unary change U, residual sum R2, max block residual^2 M2, clamp flag F):
-// run-loop decision, or -- when sharded -- publish them for the cross-rank
-// all-reduce and leave the decision to dope_decide.  Always advances the
-// running unary term.  One thread.
-__device__ void finalize_apply(const Lat2 &L, dope_run_state s0, int64_t E2, int64_t U2, double R2,
-                               int64_t M2, int F2, int cur, int best_idx, int out) {
-    dope_run_state *st = L.st;
-    E2 += s0.unary2 / 2;             // E(y_{t-1}) = u.y_{t-1} + pair terms
-    st->unary2 = s0.unary2 + U2;     // now sum u*y2_t
-    if (L.fuse) st->a_bound = ++s0.a_bound;   // this pass updated the multipliers
-    if (!L.fuse) {                   // step-level API: rotate only
-        st->ybest = best_idx;
-        st->ycur = out;
-    } else if (L.sharded) {
-        L.agg[0] = E2;
-        L.agg[1] = __double_as_longlong(R2);
-        L.agg[2] = M2;
-        L.agg[3] = F2;
-    } else {
-        apply_iteration(L, s0, E2, R2, M2, F2, cur, best_idx, out);
-    }
-}
-
 // Residual sum of squares, admm.py:295: sum over blocks of fl(fl(sqrt(ss))^2).
 // Each term is ss + e with e an exact multiple of 2^-53 (|e| <= 4 ulp(ss)), so
 // the sum is kept exactly as two integers (sum ss, sum e * 2^53) and rounded
@@ -703,14 +711,111 @@ __device__ __forceinline__ double rsq_total(int64_t sum_ss, int64_t sum_excess) 
     return (double)sum_ss + (double)sum_excess * 0x1p-53;
 }
 
-// Sharded mode: apply the all-reduced aggregates (identical on every rank).
+// Apply one consensus pass's global aggregates (pair energy E of y_{t-1},
+// unary change U, residual sum R2, max block residual^2 M2, clamp flag F):
+// run-loop decision, or -- when sharded -- publish them for the cross-rank
+// all-reduce and leave the decision to dope_decide.  Always advances the
+// running unary term.  One thread.
+__device__ void finalize_apply(const Lat2 &L, dope_run_state s0, int64_t E2, int64_t U2, int64_t S2,
+                               int64_t X2, int64_t M2, int F2, int cur, int best_idx, int out) {
+    dope_run_state *st = L.st;
+    E2 += s0.unary2 / 2;             // E(y_{t-1}) = u.y_{t-1} + pair terms
+    st->unary2 = s0.unary2 + U2;     // now sum u*y2_t
+    if (L.fuse) st->a_bound = ++s0.a_bound;   // this pass updated the multipliers
+    if (!L.fuse) {                   // step-level API: rotate only
+        st->ybest = best_idx;
+        st->ycur = out;
+    } else if (L.sharded) {          // this shard's slot of the agg table; dope_decide reduces
+        int64_t *slot = L.agg + (size_t)AGG_SLOT * L.shard_index;
+        slot[0] = E2;
+        slot[1] = S2;
+        slot[2] = X2;
+        slot[3] = M2;
+        slot[4] = F2;
+    } else {
+        apply_iteration(L, s0, E2, rsq_total(S2, X2), M2, F2, cur, best_idx, out);
+    }
+}
+
+
+// Sharded mode: reduce the gathered agg table in shard order -- exact
+// integers throughout, so every shard (and the single-GPU run) reaches the
+// same trace entry, best iterate and stop decision -- and apply it.
 __global__ void k_decide(Lat2 L) {
     dope_run_state *st = L.st;
     if (st->stop) return;
     const int cur = st->ycur, best = st->ybest;
     const dope_run_state s0 = *st;
-    apply_iteration(L, s0, L.agg[0], __longlong_as_double(L.agg[1]), L.agg[2], (int)L.agg[3], cur, best,
-                    other_buffer(cur, best));
+    int64_t E = 0, S = 0, X = 0, M = -1;
+    int F = 0;
+    for (int r = 0; r < L.shard_count; ++r) {
+        const int64_t *slot = L.agg + (size_t)AGG_SLOT * r;
+        E += slot[0];
+        S += slot[1];
+        X += slot[2];
+        M = slot[3] > M ? slot[3] : M;
+        F |= (int)slot[4];
+    }
+    apply_iteration(L, s0, E, rsq_total(S, X), M, F, cur, best, other_buffer(cur, best));
+}
+
+// Sharded mode: the new iterate and multipliers of the ghost rows (2D) /
+// planes (3D) -- the neighbour shards' boundary pixels -- recomputed here
+// instead of exchanged.  A ghost pixel's update (admm.py:136-151 on the q == 1
+// stencil, like the consensus pass) needs its own label and multiplier, the
+// labels of its cross-block neighbours: in-row (in-plane) ones across block
+// seams, the facing local boundary pixel, and -- never, with blocks at least
+// two rows / planes deep -- the pixel beyond; all are in hand after the label
+// halo.  The ghost multipliers are kept redundantly (a += yhat - y, exactly
+// the owner's update), so the values equal the owner's bit for bit.  Runs
+// after the consensus pass and before dope_decide: writes y into the output
+// buffer's ghost rows and marks the adjacent local block dirty where the
+// ghost iterate moved (it enters that block's objective, blockform.py:103).
+__global__ void k_ghost_consensus(Lat2 L) {
+    dope_run_state *st = L.st;
+    if (st->stop) return;
+    const int cur = st->ycur, best = st->ybest, out = other_buffer(cur, best);
+    const ystore_t *__restrict__ y_in = L.y2[cur];
+    ystore_t *__restrict__ y_out = L.y2[out];
+    const bool is3 = L.ndim == 3;
+    const int64_t P = is3 ? (int64_t)L.ay.dim * L.W : (int64_t)L.W;   // pixels per ghost unit
+    const int64_t below = (is3 ? (int64_t)L.az.dim : (int64_t)L.ay.dim) * P;
+    const bool has_up = is3 ? L.gzu : L.gup, has_dn = is3 ? L.gzd : L.gdn;
+    const int kplane = is3 ? L.ay.k * L.ax.k : L.ax.k;   // blocks per block row / plane
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < P; c += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = is3 ? (int32_t)(c / L.W) : 0, x = (int32_t)(c - (int64_t)r * L.W);
+        const int bx = L.ax.owner(x), by = is3 ? L.ay.owner(r) : 0;
+        const int kin = by * L.ax.k + bx;   // local block facing this column, within its block row / plane
+        for (int side = 0; side < 2; ++side) {
+            if (side == 0 ? !has_up : !has_dn) continue;
+            const int64_t G = side == 0 ? c - P : below + c;          // ghost pixel
+            const int64_t I = side == 0 ? c : below - P + c;          // facing local pixel
+            const int32_t yh = L.yhat[G];
+            int32_t s = yh - L.yhat[I];
+            if (x > 0 && L.ax.owner(x - 1) != bx) s += yh - L.yhat[G - 1];
+            if (x + 1 < L.W && L.ax.owner(x + 1) != bx) s += yh - L.yhat[G + 1];
+            if (is3) {
+                if (r > 0 && L.ay.owner(r - 1) != by) s += yh - L.yhat[G - L.W];
+                if (r + 1 < L.ay.dim && L.ay.owner(r + 1) != by) s += yh - L.yhat[G + L.W];
+            }
+            astore_t *ga = side == 0 ? L.ga_up : L.ga_dn;
+            const int32_t aold = ga[c];
+            const int32_t ypre = yh + aold - L.q * s;
+            const int32_t y = ypre < 0 ? 0 : (ypre > 1 ? 1 : ypre);
+            ga[c] = (astore_t)(aold + yh - y);
+            y_out[G] = (ystore_t)(2 * y);
+            if (2 * y != (int32_t)y_in[G])
+                L.dirty[side == 0 ? kin : (size_t)(L.K - kplane) + kin] = 1u;
+        }
+    }
+}
+
+// Sharded mode, end of run: move this shard's energy of the last iterate into
+// its agg slot (the cross-shard sum happens in k_finish_decide).
+__global__ void k_publish_energy(Lat2 L) {
+    dope_run_state *st = L.st;
+    L.agg[(size_t)AGG_SLOT * L.shard_index + 5] = st->energy_acc;
+    st->energy_acc = 0;
 }
 
 // Sharded mode: copy this shard's first and last local rows (labels or the
@@ -808,9 +913,9 @@ __device__ void pass_tail(const Lat2 &L, const CtaAgg &c, int cur, int best, int
         const dope_run_state s0 = *st;
         const int64_t E2 = __ldcg(&L.pc[0]), U2 = __ldcg(&L.pc[1]), M2 = __ldcg(&L.pc[2]) - 1;
         const int F2 = (int)__ldcg(&L.pc[3]);
-        const double R2 = rsq_total(__ldcg(&L.pc[4]), __ldcg(&L.pc[5]));
+        const int64_t S2 = __ldcg(&L.pc[4]), X2 = __ldcg(&L.pc[5]);
         for (int i = 0; i < 8; ++i) L.pc[i] = 0;   // incl. the solved-list count
-        finalize_apply(L, s0, E2, U2, R2, M2, F2, cur, best, out);
+        finalize_apply(L, s0, E2, U2, S2, X2, M2, F2, cur, best, out);
         st->done_ctas = 0;
     }
 }
@@ -1313,7 +1418,11 @@ __global__ void k_finish_decide(Lat2 L) {
     dope_run_state *st = L.st;
     const int T = st->iteration;
     if (T >= 1 && !st->error) {
-        const int64_t E = st->energy_acc;
+        int64_t E = st->energy_acc;
+        if (L.sharded) {   // the gathered end-of-run energies of every shard
+            E = 0;
+            for (int r = 0; r < L.shard_count; ++r) E += L.agg[(size_t)AGG_SLOT * r + 5];
+        }
         if (T - 1 < L.max_iters) L.tr_e[T - 1] = E;
         if (E < st->best_energy) {
             st->best_energy = E;
@@ -1515,6 +1624,18 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
     o.gzd = is3 ? L->ghost_dn : 0;
     o.sharded = L->sharded;
     o.agg = L->agg;
+    o.trace_hash = L->trace_hash;
+    o.hash_base = L->hash_base;
+    o.shard_index = L->sharded ? L->shard_index : 0;
+    o.shard_count = L->sharded ? L->shard_count : 1;
+    if (L->sharded && (L->shard_count < 1 || L->shard_index < 0 || L->shard_index >= L->shard_count))
+        return DOPE_E_ARGS;
+    if (L->sharded && L->halo) {
+        const int64_t U = is3 ? L->dims[1] * L->dims[2] : L->dims[1];
+        uint8_t *h = static_cast<uint8_t *>(L->halo);
+        o.ga_up = reinterpret_cast<astore_t *>(h + halo_ga_offset(U));
+        o.ga_dn = o.ga_up + U;
+    }
     if (o.sharded && (!o.agg || (is3 ? o.az.rem != 0 : o.ay.rem != 0))) return DOPE_E_ARGS;
     const int maxd = o.az.base + (o.az.rem ? 1 : 0);
     const int maxh = o.ay.base + (o.ay.rem ? 1 : 0);
@@ -1655,6 +1776,16 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     cfg.attrs = attr;
     cfg.numAttrs = off ? 0 : 1;
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// Audit mode: digest of (yhat, 2y, a) after the iteration (dope_lattice.trace_hash).
+static int launch_digest(const Plan &P, cudaStream_t s) {
+    if (!P.o.trace_hash) return DOPE_OK;
+    const Lat2 &o = P.o;
+    k_digest_begin<<<1, 1, 0, s>>>(o.st, o.trace_hash, o.max_iters);
+    k_digest<dope_run_state, ystore_t, astore_t><<<2 * 148, 256, 0, s>>>(
+        o.st, o.trace_hash, o.max_iters, P.n, o.hash_base, o.yhat, o.y2[0], o.y2[1], o.y2[2], o.a);
+    return cuda_check(cudaGetLastError(), "state digest");
 }
 
 static int launch_k1(const Plan &P, cudaStream_t s) {
@@ -1971,20 +2102,15 @@ int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void 
         for (int i = 0; i < iters; ++i) {
             if ((rc = launch_k1(P, s))) return rc;
             if ((rc = launch_k2(P.o, s))) return rc;
+            if ((rc = launch_digest(P, s))) return rc;
         }
         return DOPE_OK;
     }
     // CUDA graph of `iters` iterations, cached by the lattice description
-    static std::mutex mu;
-    static std::map<std::string, cudaGraphExec_t> cache;
+    static GraphCache cache;
     std::string key((const char *)L, sizeof(*L));
     key.append((const char *)&iters, sizeof(iters));
-    cudaGraphExec_t exec = nullptr;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        auto it = cache.find(key);
-        if (it != cache.end()) exec = it->second;
-    }
+    cudaGraphExec_t exec = cache.find(key);
     if (!exec) {
         // kernel attributes must be set outside stream capture
         if ((rc = dope_prepare_kernels(L))) return rc;
@@ -1995,6 +2121,7 @@ int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void 
         for (int i = 0; i < iters && !rc; ++i) {
             rc = launch_k1(P, cs);
             if (!rc) rc = launch_k2(P.o, cs);
+            if (!rc) rc = launch_digest(P, cs);
         }
         cudaError_t e = cudaStreamEndCapture(cs, &graph);
         if (rc) return rc;
@@ -2003,11 +2130,14 @@ int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void 
         cudaGraphDestroy(graph);
         cudaStreamDestroy(cs);
         if (rc) return rc;
-        std::lock_guard<std::mutex> lk(mu);
-        cache[key] = exec;
+        cache.put(key, exec);
     }
     return cuda_check(cudaGraphLaunch(exec, s), "graph launch");
 }
+
+int64_t dope_graph_cache_entries(void) { return graph_cache_entries_all(); }
+
+void dope_graph_cache_clear(void) { graph_cache_clear_all(); }
 
 static int launch_energy_current(const Lat2 &o, int64_t n, cudaStream_t s) {
     const uintptr_t al = (uintptr_t)o.y2[0] | (uintptr_t)o.y2[1] | (uintptr_t)o.y2[2];
@@ -2063,7 +2193,35 @@ int dope_energy_local(const dope_lattice *L, void *stream) {
     Plan P;
     int rc = build_plan(L, P);
     if (rc) return rc;
-    return launch_energy_current(P.o, P.n, (cudaStream_t)stream);
+    if ((rc = launch_energy_current(P.o, P.n, (cudaStream_t)stream))) return rc;
+    if (!P.o.sharded) return DOPE_OK;
+    k_publish_energy<<<1, 1, 0, (cudaStream_t)stream>>>(P.o);
+    return cuda_check(cudaGetLastError(), "publish_energy");
+}
+
+int64_t dope_halo_bytes(const dope_lattice *L) {
+    if (!L || (L->ndim != 2 && L->ndim != 3)) return 0;
+    return halo_bytes(L->ndim == 3 ? L->dims[1] * L->dims[2] : L->dims[1]);
+}
+
+int dope_ghost_consensus(const dope_lattice *L, void *stream) {
+    Plan P;
+    int rc = build_plan(L, P);
+    if (rc) return rc;
+    if (!P.o.sharded || !P.o.ga_up) return DOPE_E_ARGS;
+    // the ghost unit's far-side neighbour must lie in its own block (blocks at
+    // least two rows / planes deep along the sharded axis)
+    if ((L->ghost_up || L->ghost_dn) && (P.o.ndim == 3 ? P.o.az.base : P.o.ay.base) < 2) return DOPE_E_GEOMETRY;
+    const int64_t unit = P.o.ndim == 3 ? (int64_t)P.o.ay.dim * P.o.W : (int64_t)P.o.W;
+    k_ghost_consensus<<<grid_for(unit), 256, 0, (cudaStream_t)stream>>>(P.o);
+    return cuda_check(cudaGetLastError(), "ghost_consensus");
+}
+
+int dope_trace_digest(const dope_lattice *L, void *stream) {
+    Plan P;
+    int rc = build_plan(L, P);
+    if (rc) return rc;
+    return launch_digest(P, (cudaStream_t)stream);
 }
 
 int dope_finish_decide(const dope_lattice *L, void *stream) {

@@ -1,27 +1,31 @@
-"""Multi-GPU sharding of the ADMM loop: slabs of block rows (2D) or block
-planes (3D, along the depth axis), halo exchange.
+"""Sharding of the ADMM loop over GPUs: slabs of block rows (2D) or block
+planes (3D, along the depth axis) with one ghost row / plane on each side.
 
 The reference parallelises `update_blocks` over sub-regions with a thread
-pool (admm.py:186-190) and keeps everything else global.  Here the
-sub-regions are sharded across GPUs as contiguous slabs of block rows.  Within
-an iteration the only cross-shard data are one-pixel halos:
+pool inside one process (admm.py:128-132) and keeps everything else global.
+Here the sub-regions are sharded across GPUs as contiguous slabs; within an
+iteration the only cross-shard data are:
 
-  1. K1 on every shard (the block objective reads y of the row / plane
-     above and below the slab from the ghost rows / planes);
-  2. exchange of the label (yhat) boundary rows -> ghost rows;
-  3. consensus pass on every shard -> local aggregates
-     [energy of y_{t-1}, sum of block residuals^2, max block residual^2, clamp];
-  4. all-reduce of the aggregates (sum, sum, max, max);
-  5. `dope_decide` applies the identical trace / best-iterate / stop rule on
-     every shard;
-  6. exchange of the new y boundary rows -> ghost rows (a changed ghost marks
-     the adjacent local block row dirty).
+  1. K1 on every shard (the block objective reads y of the row / plane above
+     and below the slab from the ghost rows / planes);
+  2. the label (yhat) boundary rows -> the neighbours' ghost rows;
+  3. the consensus pass on every shard -> this shard's slot of the agg table
+     [energy of y_{t-1}, sum ss, sum of rounding excesses, max ss, clamp] --
+     exact integers;
+  4. `dope_ghost_consensus`: the ghost rows' new y and multipliers recomputed
+     locally from the labels of step 2 (no y halo: the values equal the
+     owner's bit for bit);
+  5. one all-gather of the agg slots;
+  6. `dope_decide`: the table reduced in shard order -> the same trace,
+     best iterate and stop rule on every shard.
 
-Integer energies, max residuals and labels are therefore bit-identical to the
-single-GPU run; the float trace field residual_sq is summed per shard first
-(rtol 1e-12).  Communicators: `VirtualComm` runs G shards inside one process
-(single-GPU emulation used by the tests), `DistComm` uses torch.distributed
-(NCCL on B200s, gloo on CPU) with one shard per rank.
+Every trace field, label and iterate is therefore bit-identical to the
+single-GPU run (and the reference).  Communicators (csrc/dope_comm.cu): NCCL,
+one shard per rank (`NcclComm`, `NcclShard`), and loopback, all shards in one
+process on one GPU (`LoopbackGroup`, the single-GPU stand-in for G ranks that
+drives the same C++ iteration and graph capture).  `run_shards` + `DistComm`
+restate the protocol step by step over torch.distributed for executors that
+implement the shard interface (the gloo CPU protocol test).
 """
 from __future__ import annotations
 
@@ -35,6 +39,8 @@ from .energy import EnergyModel
 from .lowering import LatticeLowering, lower_lattice
 from .partition import Partition
 
+AGG_SLOT = 8   # int64 per shard in the agg table (dope_b200.h)
+
 
 def shard_block_rows(ky: int, world: int) -> list:
     """Contiguous near-equal slabs of block rows, one per rank."""
@@ -47,6 +53,19 @@ def shard_block_rows(ky: int, world: int) -> list:
         out.append((lo, lo + n))
         lo += n
     return out
+
+
+def _check_config(full: LatticeLowering, config: AdmmConfig) -> int:
+    """The integer sharded path's limits (the same as admm._bind): a fixed,
+    integer mu dividing lambda*w.  Raises instead of truncating."""
+    if config.mu_fact != 1.0:
+        raise NotImplementedError("the sharded integer path keeps mu fixed (mu_fact == 1)")
+    mu0 = config.resolved_mu0(len(full.dims))
+    if mu0 != round(mu0) or mu0 <= 0:
+        raise NotImplementedError("the sharded integer path needs an integer mu0")
+    if full.lamw % int(round(mu0)) != 0:
+        raise NotImplementedError("the sharded integer path needs lambda*w divisible by mu0")
+    return int(round(mu0))
 
 
 class _Problems:
@@ -68,31 +87,42 @@ class GpuShard:
     CUDA device (product executor)."""
 
     def __init__(self, full: LatticeLowering, kb0: int, kb1: int, mu: int, eps: float,
-                 max_iters: int, warm_start: bool = True, skip_clean: bool = True):
+                 max_iters: int, warm_start: bool = True, skip_clean: bool = True,
+                 index: int = 0, count: int = 1, digests: bool = False):
         import torch
         dims, kpa = tuple(full.dims), tuple(full.kpa)
         n0, k0 = dims[0], kpa[0]   # the sharded axis: rows (2D) / planes (3D)
         if n0 % k0:
             raise NotImplementedError("sharding needs a uniform tiling along the sharded axis")
         bh = n0 // k0
+        if count > 1 and bh < 2:
+            raise NotImplementedError("sharding needs blocks at least two rows / planes deep")
         self.kb0, self.kb1, self.bh = kb0, kb1, bh
         self.r0, self.r1 = kb0 * bh, kb1 * bh
+        self.index, self.count = index, count
         u = full.u.reshape(dims)[self.r0:self.r1].ravel()
         low = LatticeLowering((self.r1 - self.r0,) + dims[1:], (kb1 - kb0,) + kpa[1:], full.conn,
                               full.lamw, np.ascontiguousarray(u), full.lam)
         dev = _device()
         self.problems = _Problems(low, dev)
-        self.dev = _DeviceState(self.problems, mu, eps, max_iters, warm_start, skip_clean)
+        self.dev = _DeviceState(self.problems, mu, eps, max_iters, warm_start, skip_clean,
+                                digests=digests)
         L = self.dev.L
         L.ghost_up = int(kb0 > 0)
         L.ghost_dn = int(kb1 < k0)
         L.sharded = 1
         L.fuse_multipliers = 1
-        _lib.check(_lib.lib().dope_lattice_check(C.byref(L)), "dope_lattice_check (shard)")
-        self.W = int(np.prod(dims[1:]))   # exchanged unit: one row (2D) / plane (3D), bytes
-        self.rows_u8 = [torch.zeros(self.W, dtype=torch.uint8, device=dev) for _ in range(4)]
+        L.shard_index, L.shard_count = index, count
+        self.unit = int(np.prod(dims[1:]))   # pixels per row (2D) / plane (3D)
+        L.hash_base = self.r0 * self.unit
+        self.agg = torch.zeros(AGG_SLOT * count, dtype=torch.int64, device=dev)
+        L.agg = self.agg.data_ptr()
+        lb = _lib.lib()
+        self.halo = torch.zeros(int(lb.dope_halo_bytes(C.byref(L))), dtype=torch.uint8, device=dev)
+        L.halo = self.halo.data_ptr()
+        _lib.check(lb.dope_lattice_check(C.byref(L)), "dope_lattice_check (shard)")
 
-    # -- kernels ------------------------------------------------------------
+    # -- step interface (run_shards) -----------------------------------------
     def call(self, name, *args):
         self.dev.call(name, *args)
 
@@ -105,6 +135,9 @@ class GpuShard:
     def update_global(self):
         self.call("dope_update_global")
 
+    def ghost_consensus(self):
+        self.call("dope_ghost_consensus")
+
     def decide(self):
         self.call("dope_decide")
 
@@ -114,61 +147,30 @@ class GpuShard:
     def finish_decide(self):
         self.call("dope_finish_decide")
 
-    def staging(self, which):
-        """(send_first, send_last, recv_up, recv_dn) buffers for labels / y."""
-        return self.rows_u8   # labels and y2 are both one byte per pixel
+    def halo_slots(self):
+        """(first row out, last row out, from above, from below) views of the halo buffer."""
+        U = self.unit
+        return tuple(self.halo[i * U:(i + 1) * U] for i in range(4))
 
-    def pack_rows(self, which):
-        first, last, _, _ = self.staging(which)
-        lb = _lib.lib()
-        _lib.check(lb.dope_pack_rows(C.byref(self.dev.L), which, first.data_ptr(), last.data_ptr(),
-                                     self.dev.stream()), "dope_pack_rows")
-        return first, last
+    def pack_rows(self):
+        first, last, _, _ = self.halo_slots()
+        _lib.check(_lib.lib().dope_pack_rows(C.byref(self.dev.L), 0, first.data_ptr(), last.data_ptr(),
+                                             self.dev.stream()), "dope_pack_rows")
 
-    def ghost_update(self, which, up, dn):
-        lb = _lib.lib()
-        _lib.check(lb.dope_ghost_update(C.byref(self.dev.L), which,
-                                        up.data_ptr() if up is not None else None,
-                                        dn.data_ptr() if dn is not None else None,
-                                        self.dev.stream()), "dope_ghost_update")
-
-    # -- aggregates ---------------------------------------------------------
-    @property
-    def agg(self):
-        return self.dev.agg
-
-    @property
-    def energy_acc(self):
-        import torch
-        return self.dev.state.view(torch.int64)[8:9]     # dope_run_state.energy_acc
+    def install_rows(self):
+        _, _, up, dn = self.halo_slots()
+        L = self.dev.L
+        _lib.check(_lib.lib().dope_ghost_update(C.byref(L), 0, up.data_ptr() if L.ghost_up else None,
+                                                dn.data_ptr() if L.ghost_dn else None,
+                                                self.dev.stream()), "dope_ghost_update")
 
     def labels(self):
         return self.dev.binarize()
 
-
-class VirtualComm:
-    """All shards in this process (single-GPU emulation of G ranks)."""
-
-    def exchange(self, shards, which):
-        packed = [s.pack_rows(which) for s in shards]
-        for i, s in enumerate(shards):
-            up = packed[i - 1][1] if i > 0 else None
-            dn = packed[i + 1][0] if i + 1 < len(shards) else None
-            s.ghost_update(which, up, dn)
-
-    def allreduce_agg(self, shards):
-        import torch
-        a = torch.stack([s.agg for s in shards])
-        r2 = a[:, 1].contiguous().view(torch.float64)
-        out = torch.stack([a[:, 0].sum(), r2.sum().view(torch.int64), a[:, 2].max(), a[:, 3].max()])
-        for s in shards:
-            s.agg.copy_(out)
-
-    def allreduce_energy(self, shards):
-        import torch
-        tot = torch.stack([s.energy_acc for s in shards]).sum(dim=0)
-        for s in shards:
-            s.energy_acc.copy_(tot)
+    def digests(self):
+        """Per-iteration (yhat, 2y, a) digests of this slab (global index base)."""
+        it = self.dev.run_state().iteration
+        return self.dev.trace_hash[:3 * it].cpu().numpy().view(np.uint64).reshape(it, 3)
 
 
 class DistComm:
@@ -181,74 +183,115 @@ class DistComm:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
 
-    def exchange(self, shards, which):
+    def move_rows(self, shards):
         (s,) = shards
-        first, last = s.pack_rows(which)
-        _, _, recv_up, recv_dn = s.staging(which)
+        first, last, up, dn = s.halo_slots()
         dist = self.dist
         ops = []
         if self.rank > 0:
             ops.append(dist.P2POp(dist.isend, first, self.rank - 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, recv_up, self.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, up, self.rank - 1, self.group))
         if self.rank + 1 < self.world:
             ops.append(dist.P2POp(dist.isend, last, self.rank + 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, recv_dn, self.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, dn, self.rank + 1, self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
-        s.ghost_update(which, recv_up if self.rank > 0 else None,
-                       recv_dn if self.rank + 1 < self.world else None)
 
-    def allreduce_agg(self, shards):
+    def gather_agg(self, shards):
         import torch
         (s,) = shards
-        a = s.agg
-        dist = self.dist
-        dist.all_reduce(a[0:1], op=dist.ReduceOp.SUM, group=self.group)
-        r2 = a[1:2].view(torch.float64)
-        dist.all_reduce(r2, op=dist.ReduceOp.SUM, group=self.group)
-        dist.all_reduce(a[2:4], op=dist.ReduceOp.MAX, group=self.group)
-
-    def allreduce_energy(self, shards):
-        (s,) = shards
-        self.dist.all_reduce(s.energy_acc, op=self.dist.ReduceOp.SUM, group=self.group)
+        table = s.agg.view(self.world, AGG_SLOT)
+        mine = table[self.rank].clone()
+        parts = [torch.empty_like(mine) for _ in range(self.world)]
+        self.dist.all_gather(parts, mine, group=self.group)
+        table.copy_(torch.stack(parts))
 
 
 def run_shards(shards, comm, max_iters: int):
-    """The sharded run loop (admm.py:283-310 distributed by slabs)."""
+    """The sharded run loop step by step (csrc/dope_comm.cu one_iteration)."""
     for s in shards:
         s.init()
     for _ in range(max_iters):
         for s in shards:
             s.update_blocks()
-        comm.exchange(shards, 0)
+        for s in shards:
+            s.pack_rows()
+        comm.move_rows(shards)
+        for s in shards:
+            s.install_rows()
         for s in shards:
             s.update_global()
-        comm.allreduce_agg(shards)
+        for s in shards:
+            s.ghost_consensus()
+        comm.gather_agg(shards)
         for s in shards:
             s.decide()
-        comm.exchange(shards, 1)
     for s in shards:
         s.energy_local()
-    comm.allreduce_energy(shards)
+    comm.gather_agg(shards)
     for s in shards:
         s.finish_decide()
 
 
-def run_virtual(model: EnergyModel, partition: Partition, config: AdmmConfig, shards: int):
-    """`run` with the sub-regions sharded over `shards` virtual ranks on this GPU.
+class LoopbackGroup:
+    """All G shards of one grid in this process, on this GPU, run by the C++
+    loopback communicator: the same iteration and graph capture as NCCL, each
+    halo row moved by one cudaMemcpyAsync, each agg slot copied into every
+    peer table."""
+
+    def __init__(self, shards):
+        self.shards = list(shards)
+        self.handle = C.c_void_p()
+        _lib.check(_lib.lib().dope_comm_loopback(len(self.shards), C.byref(self.handle)),
+                   "dope_comm_loopback")
+        self._arr = (C.POINTER(_lib.Lattice) * len(self.shards))(
+            *[C.pointer(s.dev.L) for s in self.shards])
+
+    def run(self, iters: int, use_graph: bool = True):
+        lb = _lib.lib()
+        for s in self.shards:
+            s.init()
+        st = self.shards[0].dev.stream()
+        _lib.check(lb.dope_sharded_run_group(self._arr, len(self.shards), self.handle, iters,
+                                             int(use_graph), st), "dope_sharded_run_group")
+        _lib.check(lb.dope_sharded_finish_group(self._arr, len(self.shards), self.handle, st),
+                   "dope_sharded_finish_group")
+
+    def close(self):
+        if self.handle:
+            _lib.lib().dope_comm_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+
+def _make_shards(model: EnergyModel, partition: Partition, config: AdmmConfig, world: int,
+                 ranks, digests: bool = False):
+    full = lower_lattice(model, partition)
+    mu = _check_config(full, config)
+    eps = config.resolved_eps(partition)
+    slabs = shard_block_rows(full.kpa[0], world)
+    return [GpuShard(full, slabs[r][0], slabs[r][1], mu, eps, config.max_iters, config.warm_start,
+                     config.skip_clean, index=r, count=world, digests=digests) for r in ranks]
+
+
+def run_virtual(model: EnergyModel, partition: Partition, config: AdmmConfig, shards: int,
+                use_graph: bool = True, digests: bool = False):
+    """`run` with the sub-regions sharded over `shards` loopback ranks on this GPU.
 
     Returns (labels, trace, state_fields) assembled from the shards."""
-    full = lower_lattice(model, partition)
-    if config.mu_fact != 1.0:
-        raise NotImplementedError("the integer lattice path keeps mu fixed (mu_fact == 1)")
-    mu0 = config.resolved_mu0(len(full.dims))
-    eps = config.resolved_eps(partition)
-    slabs = shard_block_rows(full.kpa[0], shards)
-    sh = [GpuShard(full, a, b, int(mu0), eps, config.max_iters, config.warm_start,
-                   config.skip_clean) for a, b in slabs]
-    run_shards(sh, VirtualComm(), config.max_iters)
-    return collect(sh, mu0, config)
+    sh = _make_shards(model, partition, config, shards, range(shards), digests)
+    group = LoopbackGroup(sh)
+    try:
+        group.run(config.max_iters, use_graph)
+        out = collect(sh, config.resolved_mu0(partition.shape.ndim), config)
+    finally:
+        group.close()
+    if digests:
+        tot = sh[0].digests().copy()
+        for s in sh[1:]:
+            tot += s.digests()
+        out[2]["digests"] = tot
+    return out
 
 
 def collect(shards, mu0, config):
@@ -266,16 +309,17 @@ def collect(shards, mu0, config):
              for t in range(it)]
     y = torch.cat([s.dev.y2_current() for s in shards]).double().div_(2.0).cpu().numpy()
     yhat = torch.cat([s.dev.yhat for s in shards]).cpu().numpy()
+    a = torch.cat([s.dev.a for s in shards]).double().cpu().numpy()
     return labels, trace, {"iterations": it, "converged": bool(rs.converged),
-                           "best_iteration": int(rs.best_iteration), "y": y, "yhat": yhat}
+                           "best_iteration": int(rs.best_iteration), "y": y, "yhat": yhat, "a": a}
 
 
 class NcclComm:
     """NCCL communicator owned by libdope_b200 (one rank per GPU).
 
     The 128-byte unique id is created on rank 0 and broadcast with
-    torch.distributed (any backend); the halo exchanges and all-reduces then
-    run inside dope_sharded_run's CUDA graph."""
+    torch.distributed (any backend); the halo exchange and the agg all-gather
+    then run inside dope_sharded_run's CUDA graph."""
 
     def __init__(self, rank: int, world: int, group=None):
         import torch
@@ -302,13 +346,7 @@ class NcclComm:
 
 
 class NcclShard(GpuShard):
-    """A GpuShard whose whole run loop (NCCL halos included) is one CUDA graph."""
-
-    def __init__(self, *args, **kw):
-        import torch
-        super().__init__(*args, **kw)
-        self.halo = torch.zeros(16 * self.W, dtype=torch.uint8, device=self.problems.device)
-        self.dev.L.halo = self.halo.data_ptr()
+    """A GpuShard whose whole run loop (NCCL halo and gather included) is one CUDA graph."""
 
     def run(self, comm: NcclComm, iters: int, use_graph: bool = True):
         lb = _lib.lib()
@@ -322,7 +360,7 @@ class NcclShard(GpuShard):
 def shard_for_rank(model: EnergyModel, partition: Partition, config: AdmmConfig, rank: int,
                    world: int, cls=NcclShard):
     full = lower_lattice(model, partition)
-    mu0 = config.resolved_mu0(len(full.dims))
+    mu = _check_config(full, config)
     kb0, kb1 = shard_block_rows(full.kpa[0], world)[rank]
-    return cls(full, kb0, kb1, int(mu0), config.resolved_eps(partition), config.max_iters,
-               config.warm_start, config.skip_clean)
+    return cls(full, kb0, kb1, mu, config.resolved_eps(partition), config.max_iters,
+               config.warm_start, config.skip_clean, index=rank, count=world)
