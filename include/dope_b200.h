@@ -427,6 +427,75 @@ int dope_gc_mincut(int64_t H, int64_t W, int32_t conn, const double *tcap, const
                    double lam, double qscale, uint8_t *labels, int64_t *stats, void *workspace,
                    int64_t ws_bytes, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * General graph path (dope_gstep.cu): the step functions of admm.py:113-199 and
+ * evaluate_energy (energy.py:187-194) for ANY SparseWeights pair set on ANY
+ * box partition (2D / 3D, overlap 0 / 10 / 25), float64 -- what the lattice
+ * kernels above do not cover.  Block-local data are "entries": block k's
+ * pixels (ascending, partition.py:52-59) at [blk_ptr[k], blk_ptr[k + 1]).
+ * The block operators of blockform.py:48-105 are evaluated on the fly from
+ * the symmetric CSR of W.  All pointers are device pointers.
+ * ------------------------------------------------------------------------- */
+typedef struct dope_gstep {
+    int64_t n;                  /* pixels                                      */
+    int32_t K;                  /* blocks                                      */
+    int64_t M;                  /* entries: sum of block sizes                 */
+    const int64_t *adj_ptr;     /* n + 1: symmetric CSR of W (both triangles,
+                                   columns ascending)                          */
+    const int32_t *adj_idx;
+    const double *adj_w;
+    const double *deg;          /* n: row sums d of W                          */
+    const double *u;            /* n: unary                                    */
+    const double *q;            /* n: block counts (partition.counts)          */
+    const int64_t *blk_ptr;     /* K + 1                                       */
+    const int32_t *ent_pix;     /* M: global pixel of each entry               */
+    const int32_t *ent_blk;     /* M: block of each entry                      */
+    const int64_t *mem_ptr;     /* n + 1: entries holding each pixel           */
+    const int64_t *mem_ent;     /* sum q: those entries, blocks ascending      */
+    const double *r;            /* M: remainder d/q^2 - dhat (dope_gs_prepare) */
+} dope_gstep;
+
+const char *dope_gs_last_error(void);
+/* r[e] = d_g / q_g^2 - dhat_e (blockform.py:75) for every entry. */
+int dope_gs_prepare(const dope_gstep *G, double *r, void *stream);
+/* block_objective (blockform.py:89-105) of entries [e0, e1):
+ * linear = u/q + lam (C y + r S y) + mu ((a - S y) + 1/2). */
+int dope_gs_objective(const dope_gstep *G, int64_t e0, int64_t e1, const double *y, const double *a,
+                      double mu, double lam, double *linear, void *stream);
+/* solve_global (admm.py:136-151) -> y; clamp != 0: update_global's clip to
+ * [0, 1] and *clamped |= any value outside (admm.py:172-180; zero it first).
+ * mu <= 0 -> DOPE_E_ARGS (the reference's ValueError). */
+int dope_gs_solve_global(const dope_gstep *G, const uint8_t *yhat, const double *a, double mu, double lam,
+                         double *y, int32_t clamp, int32_t *clamped, void *stream);
+/* ss[k] = ||yhat_k - S_k y||^2 (block_residuals, admm.py:193-199). */
+int dope_gs_residuals(const dope_gstep *G, const uint8_t *yhat, const double *y, double *ss, void *stream);
+/* a += yhat - S y per entry (update_multipliers, admm.py:183-190). */
+int dope_gs_update_multipliers(const dope_gstep *G, const uint8_t *yhat, const double *y, double *a,
+                               void *stream);
+/* consensus_objective (admm.py:154-169) per block: out[2k] = yhat_k . (C_k y +
+ * r_k S_k y), out[2k + 1] = ||S_k y - (yhat_k + a_k)||^2. */
+int dope_gs_consensus_objective(const dope_gstep *G, const uint8_t *yhat, const double *a, const double *y,
+                                double *out2k, void *stream);
+/* evaluate_energy (energy.py:187-194) over a pair list: out3 = [u.y + lam q,
+ * q = sum w (y_i - y_j)^2, u.y]; deterministic (fixed-order reduction);
+ * scratch holds dope_gs_energy_scratch() doubles. */
+int64_t dope_gs_energy_scratch(void);
+int dope_gs_energy(int64_t n, const double *u, int64_t npairs, const int32_t *pair_i, const int32_t *pair_j,
+                   const double *w, double lam, const double *y, double *scratch, double *out3, void *stream);
+/* A batch of B graphs, one CTA each, with seam 1's semantics (labels = nodes
+ * reaching the sink; flows[b]); graph b: nodes [node_off[b], node_off[b+1]),
+ * pairs [pair_off[b], pair_off[b+1]) with graph-local ends, workspace at
+ * ws_off[b] (dope_bk_workspace_bytes of that graph).  Offsets are device
+ * arrays. */
+int dope_bk_maxflow_batch(int32_t B, const int64_t *node_off, const int64_t *pair_off, const int64_t *ws_off,
+                          const double *tcap, const int32_t *pair_i, const int32_t *pair_j, const double *cap_ij,
+                          const double *cap_ji, uint8_t *labels, double *flows, void *workspace, void *stream);
+/* exhaustive_minimize (solvers.py:53-82) of a batch of graphs of <= 24 nodes:
+ * variable 0 is the most significant bit, ties to the smallest code. */
+int dope_exhaustive_batch(int32_t B, const int64_t *node_off, const int64_t *pair_off, const double *linear,
+                          const int32_t *pair_i, const int32_t *pair_j, const double *w, double lam,
+                          uint8_t *labels, double *energy, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -159,6 +159,27 @@ class General(C.Structure):
     ]
 
 
+class GStep(C.Structure):
+    """Mirror of dope_gstep (general graph path)."""
+    _fields_ = [
+        ("n", C.c_int64),
+        ("K", C.c_int32),
+        ("M", C.c_int64),
+        ("adj_ptr", C.c_void_p),
+        ("adj_idx", C.c_void_p),
+        ("adj_w", C.c_void_p),
+        ("deg", C.c_void_p),
+        ("u", C.c_void_p),
+        ("q", C.c_void_p),
+        ("blk_ptr", C.c_void_p),
+        ("ent_pix", C.c_void_p),
+        ("ent_blk", C.c_void_p),
+        ("mem_ptr", C.c_void_p),
+        ("mem_ent", C.c_void_p),
+        ("r", C.c_void_p),
+    ]
+
+
 class DopeError(RuntimeError):
     pass
 
@@ -287,6 +308,30 @@ def lib():
     lb.dope_g_admm_run.argtypes = [PG, C.c_int32, C.c_int32, C.c_void_p]
     lb.dope_g_binarize.restype = C.c_int
     lb.dope_g_binarize.argtypes = [PG, C.c_void_p, C.c_void_p]
+    PS = C.POINTER(GStep)
+    V = C.c_void_p
+    lb.dope_gs_last_error.restype = C.c_char_p
+    lb.dope_gs_prepare.restype = C.c_int
+    lb.dope_gs_prepare.argtypes = [PS, V, V]
+    lb.dope_gs_objective.restype = C.c_int
+    lb.dope_gs_objective.argtypes = [PS, C.c_int64, C.c_int64, V, V, C.c_double, C.c_double, V, V]
+    lb.dope_gs_solve_global.restype = C.c_int
+    lb.dope_gs_solve_global.argtypes = [PS, V, V, C.c_double, C.c_double, V, C.c_int32, V, V]
+    lb.dope_gs_residuals.restype = C.c_int
+    lb.dope_gs_residuals.argtypes = [PS, V, V, V, V]
+    lb.dope_gs_update_multipliers.restype = C.c_int
+    lb.dope_gs_update_multipliers.argtypes = [PS, V, V, V, V]
+    lb.dope_gs_consensus_objective.restype = C.c_int
+    lb.dope_gs_consensus_objective.argtypes = [PS, V, V, V, V, V]
+    lb.dope_gs_energy_scratch.restype = C.c_int64
+    lb.dope_gs_energy_scratch.argtypes = []
+    lb.dope_gs_energy.restype = C.c_int
+    lb.dope_gs_energy.argtypes = [C.c_int64, V, C.c_int64, V, V, V, C.c_double, V, V, V, V]
+    lb.dope_bk_maxflow_batch.restype = C.c_int
+    lb.dope_bk_maxflow_batch.argtypes = [C.c_int32, V, V, V, V, V, V, V, V, V, V, V, V]
+    lb.dope_exhaustive_batch.restype = C.c_int
+    lb.dope_exhaustive_batch.argtypes = [C.c_int32, V, V, V, V, V, V, C.c_double, V, V, V]
+    lb.dope_trace_digest.restype = C.c_int
     if lb.dope_abi_version() != ABI_VERSION:
         raise DopeError(f"libdope_b200 ABI {lb.dope_abi_version()} != {ABI_VERSION}")
     _lib = lb
@@ -300,6 +345,7 @@ def check(rc: int, what: str) -> None:
            DOPE_E_CAPACITY: "capacities exceed the int8 residual range",
            DOPE_E_NONSUBMODULAR: "negative pairwise weights"}.get(rc)
     if rc == DOPE_E_CUDA:
-        msg = "CUDA error: " + (lib().dope_last_cuda_error().decode() or
-                                lib().dope_f_last_error().decode())
+        lb = lib()
+        msg = "CUDA error: " + (lb.dope_last_cuda_error().decode() or lb.dope_f_last_error().decode()
+                                or lb.dope_gs_last_error().decode())
     raise DopeError(f"{what} failed ({rc}): {msg}")

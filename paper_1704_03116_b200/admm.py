@@ -1,20 +1,20 @@
-"""Consensus (ADMM) loop on the B200: API mirror of reference admm.py:27-310.
+"""Consensus (ADMM) loop on the B200: API mirror of reference admm.py:27-252.
 
 Same names, arguments, side effects on AdmmState and error types as the
-reference; the work runs in libdope_b200.so through the C ABI
-(include/dope_b200.h):
+reference.  run() keeps the whole loop on the device (no host sync inside):
 
-  update_blocks      -> dope_update_blocks     (K1, one CTA per sub-region)
-  update_global      -> dope_update_global     (K2: y, clamp, residual and
-                                                energy partials)
-  update_multipliers -> dope_update_multipliers
-  block_residuals    <- K2's per-block partials
-  run                -> dope_admm_init + dope_admm_run (K1, K2+multipliers,
-                        K3 per iteration, CUDA graph, no host sync inside the
-                        loop) + dope_finish_run
+  integer lattices (q == 1)   libdope_b200 dope_admm_run: K1 block min cuts,
+                              K2 consensus + multipliers + trace/best/stop in
+                              one CUDA graph (dope_lattice.cu)
+  float 2D lattices (q == 1)  dope_f_admm_run (dope_float.cu)
+  2D lattices with overlap /  dope_g_admm_run (dope_general.cu)
+  a mu schedule
+  anything else               graphstep.run_graph: the general graph path
+                              (dope_gstep.cu + batched block min cuts)
 
-State lives on the device; AdmmState.y / block_labels / multipliers
-materialize host arrays on access.
+The step-level functions (update_blocks, solve_global, consensus_objective,
+update_global, update_multipliers, block_residuals) run on the general graph
+path's device kernels with the reference's host-visible state semantics.
 """
 from __future__ import annotations
 
@@ -25,9 +25,10 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .energy import EnergyModel
+from .energy import EnergyModel, NonSubmodularError
 from .lowering import FloatLowering, LatticeLowering, lower_float, lower_lattice
 from .partition import Partition
+from .solvers import EXHAUSTIVE, ICM, MAXFLOW, BlockSolverKind  # noqa: F401  (re-exported)
 
 
 class BlockSolveError(RuntimeError):
@@ -43,24 +44,6 @@ def _device():
     if not torch.cuda.is_available():
         raise RuntimeError("the DOPE B200 path needs a CUDA device (there is no CPU fallback)")
     return torch.device("cuda", torch.cuda.current_device())
-
-
-@dataclass(frozen=True)
-class BlockSolverKind:
-    kind: str
-    max_sweeps: int = 100
-    restarts: int = 1
-
-    def __post_init__(self):
-        if self.kind not in ("maxflow", "exhaustive", "icm"):
-            raise ValueError(f"unknown solver kind {self.kind!r}")
-        if self.max_sweeps < 1 or self.restarts < 1:
-            raise ValueError("max_sweeps and restarts must be positive")
-
-
-MAXFLOW = BlockSolverKind("maxflow")
-EXHAUSTIVE = BlockSolverKind("exhaustive")
-ICM = BlockSolverKind("icm")
 
 
 @dataclass
@@ -114,34 +97,55 @@ class TraceRecord:
 
 
 class BlockProblems:
-    """Device-lowered block problems: what assemble_block_problems returns here.
+    """What assemble_block_problems (blockform.py:48-86) returns here.
 
-    The reference materializes per-block operators (blockform.py:216-254);
-    on the q == 1 lattice they reduce to the unary, lambda*w and the block
-    geometry, kept resident in HBM.
+    The reference materialises per-block operators.  On a q == 1 lattice they
+    reduce to the unary, lambda*w (or weight planes) and the block geometry,
+    kept resident in HBM for the run loop's kernels (kind "int" / "float").
+    Any other model / partition has kind "graph".  Indexing gives the
+    reference's BlockProblem fields per block (u_hat, w_hat, d_hat, r_diag,
+    c_rows, computed on demand) and the step-level API runs on the general
+    graph path's device data (graph(), built on first use).
     """
 
     def __init__(self, model: EnergyModel, partition: Partition):
         import torch
-        try:
-            self.lowering = lower_lattice(model, partition)
-            self.kind = "int"
-        except NotImplementedError:
-            # not an integer 4/6-connected constant-weight lattice: the float path (2D,
-            # 4/8-connected, any non-negative weights); it raises if that fails too
-            self.lowering = lower_float(model, partition)
-            self.kind = "float"
+        if model.n != partition.shape.n:
+            raise ValueError("model and partition sizes differ")
         self.partition = partition
         self.model = model
         self.device = _device()
-        self.u = torch.as_tensor(self.lowering.u, device=self.device)
+        self.lowering, self.kind, self.u = None, "graph", None
+        for kind, lower in (("int", lower_lattice), ("float", lower_float)):
+            try:
+                self.lowering = lower(model, partition)
+                self.kind = kind
+                break
+            except (NotImplementedError, NonSubmodularError):
+                continue
+        if self.lowering is not None:
+            self.u = torch.as_tensor(self.lowering.u, device=self.device)
+        self._graph = None
+
+    def graph(self):
+        """The general graph path's device data (graphstep.GraphProblems)."""
+        if self._graph is None:
+            from .graphstep import GraphProblems
+            self._graph = GraphProblems(self.model, self.partition)
+        return self._graph
 
     def __len__(self) -> int:
-        return self.lowering.K
+        return self.partition.k
+
+    def __getitem__(self, k: int):
+        return self.graph()[k]
+
+    def __iter__(self):
+        return iter(self.graph())
 
     @property
     def lam(self) -> float:
-        return self.lowering.lam
+        return float(self.model.lam)
 
 
 class _FloatDeviceState:
@@ -389,181 +393,249 @@ class _DeviceState:
 
 
 class AdmmState:
-    """Mutable state of one run (admm.py:145-157), resident on the device."""
+    """Mutable state of one run (admm.py:87-99), with the reference's fields.
 
-    def __init__(self, partition: Partition, mu: float):
-        self.partition = partition
+    y, block_labels and multipliers are host numpy arrays (lists of per-block
+    arrays) exactly like the reference's dataclass: in-place edits such as
+    ``state.multipliers[k] += d`` or ``state.y = v`` are what the next step
+    call sees -- every step function uploads the state it reads and downloads
+    what it writes (the step API's device kernels are csrc/dope_gstep.cu).  A
+    state returned by run() keeps them on the device and materialises each one
+    on first access (a 4096^2 run never copies 4096 block lists otherwise).
+    """
+
+    def __init__(self, y=None, block_labels=None, multipliers=None, mu: float = 0.0,
+                 iteration: int = 0, converged: bool = False, best_iteration: int = 0,
+                 trace=None, clamped_last: bool = False, partition: Partition | None = None):
+        self._y, self._block_labels, self._multipliers = y, block_labels, multipliers
         self.mu = float(mu)
-        self.iteration = 0
-        self.converged = False
-        self.best_iteration = 0
-        self.clamped_last = False
-        self.trace: list = []
-        self.digests = None     # (iterations, 3) uint64 when AdmmConfig.digests
-        self._dev: _DeviceState | None = None
-        self._n = partition.shape.n
+        self.iteration = iteration
+        self.converged = converged
+        self.best_iteration = best_iteration
+        self.trace: list = [] if trace is None else trace
+        self.clamped_last = clamped_last
+        self.partition = partition
+        self.digests = None        # (iterations, 3) uint64 when AdmmConfig.digests
+        self._src = None           # device source of the fields not yet materialised
 
-    # -- device binding ---------------------------------------------------
-    def _bind(self, problems: BlockProblems, config: AdmmConfig, max_iters: int | None = None,
-              eps: float = 0.0) -> _DeviceState:
-        if self._dev is not None and self._dev.problems is problems:
-            return self._dev
-        mu = self.mu
-        if problems.kind == "float":
-            self._dev = _FloatDeviceState(problems, mu, eps, max_iters or config.max_iters,
-                                          config.warm_start, config.skip_clean, config.digests)
-            self._dev.call("dope_admm_init")
-            return self._dev
-        if mu != round(mu) or mu <= 0:
-            raise NotImplementedError("the integer lattice path needs an integer mu")
-        if problems.lowering.lamw % int(mu) != 0:
-            raise NotImplementedError("the integer lattice path needs lambda*w divisible by mu")
-        self._dev = _DeviceState(problems, int(mu), eps, max_iters or config.max_iters,
-                                 config.warm_start, config.skip_clean, config.digests)
-        self._dev.call("dope_admm_init")
-        return self._dev
+    # -- construction from a finished device run --------------------------------
+    @classmethod
+    def from_lattice(cls, partition: Partition, dev, mu: float) -> "AdmmState":
+        """Fields live in a lattice run's device buffers (global layout, q == 1)."""
+        st = cls(mu=mu, partition=partition)
+        st._src = ("lattice", dev)
+        return st
 
-    # -- host views (reference attribute names) ---------------------------
+    @classmethod
+    def from_device(cls, partition: Partition, y, yhat_cat, a_cat, layout, mu: float) -> "AdmmState":
+        """Fields live in the general graph path's entry-indexed device buffers."""
+        st = cls(mu=mu, partition=partition)
+        st._src = ("entries", (y, yhat_cat, a_cat, layout))
+        return st
+
+    def _entries(self):
+        from .graphstep import layout
+        return layout(self.partition)
+
+    def _fetch(self, what: str):
+        kind, src = self._src
+        if kind == "lattice":
+            dev = src
+            if what == "y":
+                return dev.y2_current().double().div_(2.0).cpu().numpy()
+            lay = self._entries()
+            if what == "block_labels":
+                return lay.split(dev.yhat.cpu().numpy()[lay.ent_pix].astype(np.int8))
+            return lay.split(dev.multipliers().double().cpu().numpy()[lay.ent_pix])
+        y, yhat, a, lay = src
+        if what == "y":
+            return y.cpu().numpy().copy()
+        if what == "block_labels":
+            return lay.split(yhat[:lay.M].cpu().numpy().astype(np.int8))
+        return lay.split(a[:lay.M].cpu().numpy().copy())
+
     @property
     def y(self) -> np.ndarray:
-        if self._dev is None:
-            return np.full(self._n, 0.5)
-        return self._dev.y2_current().double().div_(2.0).cpu().numpy()
+        if self._y is None and self._src is not None:
+            self._y = self._fetch("y")
+        return self._y
 
     @y.setter
     def y(self, value):
-        if self._dev is None:
-            raise RuntimeError("bind the state to problems before assigning y")
-        import torch
-        v = np.asarray(value, dtype=np.float64)
-        if v.shape != (self._n,) or (not isinstance(self._dev, _FloatDeviceState)
-                                     and not np.all(np.isin(v, (0.0, 0.5, 1.0)))):
-            raise NotImplementedError("the integer lattice path holds y in {0, 1/2, 1}")
-        if isinstance(self._dev, _FloatDeviceState):
-            self._dev.y2[self._dev.run_state().ycur].copy_(torch.as_tensor(v))
-        else:
-            self._dev.y2_current().copy_(torch.as_tensor((2 * v).astype(np.uint8)))
-            self._dev.reset_unary()
-        K = self._dev.problems.lowering.K
-        self._dev.dirty[:K].fill_(1)
-        if self._dev.dirty.numel() > 2 * K:   # y buffers rewritten: no stamp holds
-            self._dev.dirty[2 * K:].zero_()
-
-    def _global_to_blocks(self, vec: np.ndarray, dtype) -> list:
-        out = []
-        for b in self.partition.blocks:
-            sl = tuple(slice(lo, hi) for lo, hi in b.extent)
-            out.append(vec.reshape(self.partition.shape.dims)[sl].ravel().astype(dtype))
-        return out
+        self._y = np.asarray(value, dtype=np.float64)
 
     @property
     def block_labels(self) -> list:
-        if self._dev is None:
-            return [np.zeros(b.size if b.pixels.size else int(np.prod([h - l for l, h in b.extent])),
-                             dtype=np.int8) for b in self.partition.blocks]
-        return self._global_to_blocks(self._dev.yhat.cpu().numpy(), np.int8)
+        if self._block_labels is None and self._src is not None:
+            self._block_labels = self._fetch("block_labels")
+        return self._block_labels
+
+    @block_labels.setter
+    def block_labels(self, value):
+        self._block_labels = list(value)
 
     @property
     def multipliers(self) -> list:
-        return self._global_to_blocks(self.multipliers_global(), np.float64)
+        if self._multipliers is None and self._src is not None:
+            self._multipliers = self._fetch("multipliers")
+        return self._multipliers
 
-    def multipliers_global(self) -> np.ndarray:
-        if self._dev is None:
-            return np.zeros(self._n)
-        return self._dev.multipliers().double().cpu().numpy()
+    @multipliers.setter
+    def multipliers(self, value):
+        self._multipliers = list(value)
+
+    # -- global-layout helpers (non-overlapping partitions) -----------------------
+    def _to_global(self, per_block, dtype) -> np.ndarray:
+        lay = self._entries()
+        if lay.M != lay.n:
+            raise ValueError("global layout needs a non-overlapping partition")
+        out = np.empty(lay.n, dtype=dtype)
+        out[lay.ent_pix] = lay.join(per_block, dtype, "vectors")
+        return out
 
     def labels_global(self) -> np.ndarray:
-        """Current block labels (yhat) in global layout."""
-        return self._dev.yhat.cpu().numpy().astype(np.int8)
+        """Current block labels (yhat) scattered to global layout."""
+        if self._block_labels is None and self._src is not None and self._src[0] == "lattice":
+            return self._src[1].yhat.cpu().numpy().astype(np.int8)
+        return self._to_global(self.block_labels, np.int8)
+
+    def multipliers_global(self) -> np.ndarray:
+        if self._multipliers is None and self._src is not None and self._src[0] == "lattice":
+            return self._src[1].multipliers().double().cpu().numpy()
+        return self._to_global(self.multipliers, np.float64)
 
 
 def init_state(partition: Partition, mu0: float) -> AdmmState:
-    """y = 1/2, zero multipliers, zero block labels (admm.py:160-168)."""
-    return AdmmState(partition, mu0)
+    """y = 1/2, zero multipliers, zero block labels (admm.py:100-110)."""
+    n = partition.shape.n
+    return AdmmState(np.full(n, 0.5), [np.zeros(b.size, dtype=np.int8) for b in partition.blocks],
+                     [np.zeros(b.size) for b in partition.blocks], float(mu0), partition=partition)
 
 
-def _check_lam(problems: BlockProblems, lam: float):
-    if float(lam) != problems.lam:
-        raise ValueError("lam differs from the lowered model's lambda")
+# ---------------------------------------------------------------------------
+# Step-level API (admm.py:113-204) on the general graph path
+# ---------------------------------------------------------------------------
+
+def _graph(problems):
+    from .graphstep import GraphProblems
+    if isinstance(problems, GraphProblems):
+        return problems
+    if isinstance(problems, BlockProblems):
+        return problems.graph()
+    raise TypeError("problems must come from assemble_block_problems")
 
 
-def update_blocks(state: AdmmState, problems: BlockProblems, lam: float,
-                  config: AdmmConfig) -> AdmmState:
-    """Re-solve every (dirty) block on the GPU (admm.py:171-191)."""
-    if config.solver.kind != "maxflow":
-        raise NotImplementedError("only the max-flow block solver has a B200 kernel")
-    _check_lam(problems, lam)
-    dev = state._bind(problems, config)
-    dev.call("dope_update_blocks")
-    dev.raise_on_error()
+def _dev_vec(v, dtype, dev):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(v, dtype=dtype), device=dev)
+
+
+def _dev_entries(gp_layout, per_block, dtype, what):
+    import torch
+    cat = gp_layout.join(per_block, dtype, what)
+    t = torch.zeros(max(gp_layout.M, 1), dtype=torch.uint8 if dtype == np.uint8 else torch.float64,
+                    device=gp_layout.device)
+    if gp_layout.M:
+        t[:gp_layout.M] = torch.as_tensor(cat, device=gp_layout.device)
+    return t
+
+
+def update_blocks(state: AdmmState, problems, lam: float, config: AdmmConfig) -> AdmmState:
+    """Re-solve every block against the current y (admm.py:113-133): block
+    objectives and block min cuts (one CTA per block) on the device."""
+    gp = _graph(problems)
+    lay = gp.layout
+    y = _dev_vec(state.y, np.float64, gp.device)
+    if y.shape != (lay.n,):
+        raise ValueError(f"y has shape {tuple(y.shape)}, expected ({lay.n},)")
+    a = _dev_entries(lay, state.multipliers, np.float64, "multipliers")
+    lin = gp.objective(y, a, state.mu, lam)
+    labels = gp.solve(lin, lam, config.solver.kind)
+    state.block_labels = lay.split(labels[:lay.M].cpu().numpy().astype(np.int8))
     return state
 
 
-def update_global(state: AdmmState, problems: BlockProblems, partition: Partition,
-                  lam: float) -> AdmmState:
-    """Closed-form global step, clamped into [0, 1] (admm.py:230-238)."""
-    _check_lam(problems, lam)
-    dev = state._bind(problems, AdmmConfig())
-    dev.call("dope_update_global", fuse=0)
-    # the step kernels do not keep the clean-block stamps: none holds any more
-    dev.dirty[2 * len(problems):].zero_()
-    state.clamped_last = bool(dev.pf.any().item())
+def solve_global(problems, partition: Partition, block_labels: list, multipliers: list, mu: float,
+                 lam: float) -> np.ndarray:
+    """Unclamped closed-form global minimiser (admm.py:136-151) on the device."""
+    gp = _graph(problems)
+    lay = gp.layout
+    yhat = _dev_entries(lay, [np.asarray(b) for b in block_labels], np.uint8, "labels")
+    a = _dev_entries(lay, multipliers, np.float64, "multipliers")
+    y, _ = gp.solve_global(yhat, a, mu, lam, clamp=False)
+    return y.cpu().numpy()
+
+
+def consensus_objective(problems, partition: Partition, block_labels: list, multipliers: list,
+                        mu: float, lam: float, y) -> float:
+    """lam sum_k yhat_k' (C_k + R_k S_k) y + mu/2 sum_k ||S_k y - (yhat_k + a_k)||^2
+    (admm.py:154-169): per-block terms on the device, summed in block order."""
+    gp = _graph(problems)
+    lay = gp.layout
+    yhat = _dev_entries(lay, [np.asarray(b) for b in block_labels], np.uint8, "labels")
+    a = _dev_entries(lay, multipliers, np.float64, "multipliers")
+    parts = gp.consensus_parts(yhat, a, _dev_vec(y, np.float64, gp.device))
+    total = 0.0
+    for c, p in parts:
+        total += lam * float(c)
+        total += 0.5 * mu * float(p)
+    return total
+
+
+def update_global(state: AdmmState, problems, partition: Partition, lam: float) -> AdmmState:
+    """Closed-form global step, clamped into [0, 1] (admm.py:172-180)."""
+    gp = _graph(problems)
+    lay = gp.layout
+    yhat = _dev_entries(lay, [np.asarray(b) for b in state.block_labels], np.uint8, "labels")
+    a = _dev_entries(lay, state.multipliers, np.float64, "multipliers")
+    y, flag = gp.solve_global(yhat, a, state.mu, lam, clamp=True)
+    state.clamped_last = bool(flag.item())
+    state.y = y.cpu().numpy()
     return state
 
 
 def update_multipliers(state: AdmmState, partition: Partition, mu_fact: float) -> AdmmState:
-    """a_k += yhat_k - S_k y, then mu *= mu_fact (admm.py:241-248)."""
-    if state._dev is None:
-        raise RuntimeError("state is not bound to device problems")
-    if mu_fact != 1.0:
-        raise NotImplementedError("the B200 path keeps mu fixed (mu_fact == 1)")
-    state._dev.call("dope_update_multipliers")
+    """a_k += yhat_k - S_k y, then mu *= mu_fact (admm.py:183-190), on the device."""
+    from .graphstep import layout, update_multipliers_dev
+    lay = layout(partition)
+    yhat = _dev_entries(lay, [np.asarray(b) for b in state.block_labels], np.uint8, "labels")
+    a = _dev_entries(lay, state.multipliers, np.float64, "multipliers")
+    update_multipliers_dev(lay, yhat, _dev_vec(state.y, np.float64, lay.device), a)
+    state.multipliers = lay.split(a[:lay.M].cpu().numpy())
     state.mu *= mu_fact
     return state
 
 
 def block_residuals(state: AdmmState, partition: Partition) -> np.ndarray:
-    """Per-block ||yhat_k - S_k y|| (admm.py:251-257), from the consensus partials."""
-    if state._dev is None:
-        raise RuntimeError("state is not bound to device problems")
-    ss = state._dev.pr.cpu().numpy()
-    return np.sqrt(ss.astype(np.float64))
+    """Per-block ||yhat_k - S_k y|| (admm.py:193-199), on the device."""
+    from .graphstep import layout, residuals_sq
+    lay = layout(partition)
+    yhat = _dev_entries(lay, [np.asarray(b) for b in state.block_labels], np.uint8, "labels")
+    ss = residuals_sq(lay, yhat, _dev_vec(state.y, np.float64, lay.device))
+    return np.sqrt(ss.cpu().numpy())
 
 
 def binarize(y) -> np.ndarray:
+    """y >= 1/2 -> 1, exact ties to 1 (admm.py:202-204)."""
     return (np.asarray(y) >= 0.5).astype(np.int8)
 
 
-def run(model: EnergyModel, partition: Partition, config: AdmmConfig,
-        problems: BlockProblems | None = None):
-    """Full distributed minimization on the GPU (admm.py:265-310).
+# ---------------------------------------------------------------------------
+# run
+# ---------------------------------------------------------------------------
 
-    Returns (y_binary, state) with the reference's semantics: best relaxed
-    energy iterate when max_iters runs out (state.y is then that iterate),
-    the final iterate when converged.
-    """
+def _run_lattice(model, partition, config, problems) -> tuple:
     import torch
-    if config.solver.kind != "maxflow":
-        raise NotImplementedError("only the max-flow block solver has a B200 kernel")
-    overlap = partition.overlap_pct != 0 or bool(partition.counts.size and int(partition.counts.max()) > 1)
-    if overlap or config.mu_fact != 1.0:
-        # overlapping partitions / growing mu: the general path (SURVEY §8(f) row 1)
-        from .general import run_general
-        return run_general(model, partition, config, use_graph=config.use_graph)
-    if problems is None:
-        problems = assemble_block_problems(model, partition)
     mu0 = config.resolved_mu0(partition.shape.ndim)
     eps = config.resolved_eps(partition)
-    if problems.kind != "float" and partition.shape.ndim == 2 and (
-            mu0 != round(mu0) or problems.lowering.lamw % int(round(mu0)) != 0):
-        # the exact integer path needs mu | lambda*w; otherwise the general path
-        from .general import run_general
-        return run_general(model, partition, config, use_graph=config.use_graph)
-    state = init_state(partition, mu0)
-    dev = state._bind(problems, config, config.max_iters, eps)
+    if problems.kind == "int" and (mu0 != round(mu0) or problems.lowering.lamw % int(round(mu0)) != 0):
+        raise NotImplementedError("the integer lattice path needs an integer mu dividing lambda*w")
+    dev = make_device_state(problems, mu0, eps, config.max_iters, config.warm_start, config.skip_clean,
+                            config.digests)
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     start.record()
+    dev.call("dope_admm_init")
     dev.call("dope_admm_run", config.max_iters, int(config.use_graph), fuse=1)
     dev.call("dope_finish_run")
     end.record()
@@ -575,11 +647,11 @@ def run(model: EnergyModel, partition: Partition, config: AdmmConfig,
     r2 = dev.tr_rs[:it].cpu().numpy()
     mr = dev.tr_mr[:it].cpu().numpy()
     cl = dev.tr_cl[:it].cpu().numpy()
-    per = total_ms / max(it, 1)
+    per = total_ms / max(it, 1)   # one graph launch: the per-iteration average
+    state = AdmmState.from_lattice(partition, dev, mu0)
     mu = mu0
     for t in range(it):
-        state.trace.append(TraceRecord(t + 1, mu, float(e[t]), float(r2[t]), float(mr[t]),
-                                       per, bool(cl[t])))
+        state.trace.append(TraceRecord(t + 1, mu, float(e[t]), float(r2[t]), float(mr[t]), per, bool(cl[t])))
         mu *= config.mu_fact
     state.mu = mu
     state.iteration = it
@@ -590,3 +662,45 @@ def run(model: EnergyModel, partition: Partition, config: AdmmConfig,
         state.digests = dev.trace_hash[:3 * it].cpu().numpy().view(np.uint64).reshape(it, 3)
     labels = dev.binarize().to(torch.int8).cpu().numpy()
     return labels, state
+
+
+def run(model: EnergyModel, partition: Partition, config: AdmmConfig,
+        problems: BlockProblems | None = None):
+    """Full distributed minimisation on the GPU (admm.py:207-252).
+
+    Returns (y_binary, state) with the reference's semantics: the best
+    relaxed-energy iterate when max_iters runs out (state.y is then that
+    iterate), the final iterate when converged.  Dispatch, fastest first:
+    the exact integer lattice kernels (q == 1, integer u and lambda*w, integer
+    mu dividing it, mu_fact == 1), the float lattice kernels (2D 4/8-connected,
+    q == 1, mu_fact == 1), the 2D lattice overlap / mu-schedule kernels
+    (dope_general), and the general graph path for everything else (any pair
+    set, 3D overlap, any schedule).  All of them run on the device.
+    """
+    if config.solver.kind == "icm":
+        raise NotImplementedError("the ICM block solver has no B200 kernel (out of scope)")
+    if problems is not None and not isinstance(problems, BlockProblems):
+        from .graphstep import GraphProblems, run_graph
+        if isinstance(problems, GraphProblems):
+            return run_graph(model, partition, config, problems)
+        raise TypeError("problems must come from assemble_block_problems")
+    overlap = partition.overlap_pct != 0 or bool(partition.counts.size and int(partition.counts.max()) > 1)
+    lattice_ok = config.solver.kind == "maxflow"
+    if lattice_ok and not overlap and config.mu_fact == 1.0:
+        if problems is None:
+            problems = assemble_block_problems(model, partition)
+        if problems.kind in ("int", "float"):
+            try:
+                return _run_lattice(model, partition, config, problems)
+            except NotImplementedError:
+                pass
+    if lattice_ok and partition.shape.ndim == 2:
+        from .general import lower_general, run_general
+        try:
+            lower_general(model, partition)
+        except NotImplementedError:
+            pass
+        else:
+            return run_general(model, partition, config, use_graph=config.use_graph)
+    from .graphstep import run_graph
+    return run_graph(model, partition, config, problems.graph() if problems is not None else None)

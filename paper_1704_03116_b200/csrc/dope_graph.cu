@@ -99,13 +99,10 @@ __device__ void bfs_from_sink(const Ws &w, int m, int tid) {
     }
 }
 
-__global__ void __launch_bounds__(NT) k_graph_maxflow(int32_t m, const double *__restrict__ tcap,
-                                                      int64_t P, const int32_t *__restrict__ pi,
-                                                      const int32_t *__restrict__ pj,
-                                                      const double *__restrict__ cij,
-                                                      const double *__restrict__ cji,
-                                                      uint8_t *__restrict__ labels,
-                                                      double *__restrict__ flow, char *wsbase) {
+__device__ void solve_graph(int32_t m, const double *__restrict__ tcap, int64_t P, const int32_t *__restrict__ pi,
+                            const int32_t *__restrict__ pj, const double *__restrict__ cij,
+                            const double *__restrict__ cji, uint8_t *__restrict__ labels,
+                            double *__restrict__ flow, char *wsbase) {
     Ws w;
     ws_layout(m, P, &w, wsbase);
     const int tid = threadIdx.x;
@@ -210,6 +207,36 @@ __global__ void __launch_bounds__(NT) k_graph_maxflow(int32_t m, const double *_
     }
 }
 
+__global__ void __launch_bounds__(NT) k_graph_maxflow(int32_t m, const double *__restrict__ tcap,
+                                                      int64_t P, const int32_t *__restrict__ pi,
+                                                      const int32_t *__restrict__ pj,
+                                                      const double *__restrict__ cij,
+                                                      const double *__restrict__ cji,
+                                                      uint8_t *__restrict__ labels,
+                                                      double *__restrict__ flow, char *wsbase) {
+    solve_graph(m, tcap, P, pi, pj, cij, cji, labels, flow, wsbase);
+}
+
+// A batch of independent graphs, one CTA each (the step-level update_blocks of
+// the general graph path): graph b has nodes [node_off[b], node_off[b+1]) and
+// pairs [pair_off[b], pair_off[b+1]) of the concatenated arrays (pair ends are
+// graph-local) and the workspace at ws_off[b].
+__global__ void __launch_bounds__(NT) k_graph_maxflow_batch(const int64_t *node_off, const int64_t *pair_off,
+                                                            const int64_t *ws_off, const double *tcap,
+                                                            const int32_t *pi, const int32_t *pj, const double *cij,
+                                                            const double *cji, uint8_t *labels, double *flow,
+                                                            char *wsbase) {
+    const int b = blockIdx.x;
+    const int64_t n0 = node_off[b], p0 = pair_off[b];
+    const int32_t m = (int32_t)(node_off[b + 1] - n0);
+    const int64_t P = pair_off[b + 1] - p0;
+    if (m == 0) {
+        if (threadIdx.x == 0) flow[b] = 0.0;
+        return;
+    }
+    solve_graph(m, tcap + n0, P, pi + p0, pj + p0, cij + p0, cji + p0, labels + n0, flow + b, wsbase + ws_off[b]);
+}
+
 }  // namespace dope_graph
 
 extern "C" {
@@ -235,6 +262,16 @@ int dope_bk_maxflow(int32_t m, const double *tcap, int64_t npairs, const int32_t
     dope_graph::k_graph_maxflow<<<1, dope_graph::NT, 0, s>>>(m, tcap, npairs, pair_i, pair_j,
                                                              cap_ij, cap_ji, labels, flow,
                                                              (char *)workspace);
+    return cudaGetLastError() == cudaSuccess ? DOPE_OK : DOPE_E_CUDA;
+}
+
+int dope_bk_maxflow_batch(int32_t B, const int64_t *node_off, const int64_t *pair_off, const int64_t *ws_off,
+                          const double *tcap, const int32_t *pair_i, const int32_t *pair_j, const double *cap_ij,
+                          const double *cap_ji, uint8_t *labels, double *flows, void *workspace, void *stream) {
+    if (B < 0 || (B && (!node_off || !pair_off || !ws_off || !flows || !workspace))) return DOPE_E_ARGS;
+    if (B == 0) return DOPE_OK;
+    dope_graph::k_graph_maxflow_batch<<<B, dope_graph::NT, 0, (cudaStream_t)stream>>>(
+        node_off, pair_off, ws_off, tcap, pair_i, pair_j, cap_ij, cap_ji, labels, flows, (char *)workspace);
     return cudaGetLastError() == cudaSuccess ? DOPE_OK : DOPE_E_CUDA;
 }
 

@@ -1,7 +1,12 @@
-"""Energy containers and evaluation (mirror of reference energy.py:19-121, 187-194).
+"""Pairwise binary energies: containers and evaluation (reference energy.py:19-121, 187-194).
 
-The objective over binary labels is  u.y + lam * sum_{i<j} w_ij (y_i - y_j)^2,
-each unordered pair stored once (i < j).
+    E(y) = u . y + lam * sum over stored pairs (i < j) of w_ij (y_i - y_j)^2
+
+A SparseWeights holds every unordered pair once, canonicalised to i < j.
+Negative weights make the model non-submodular: they are refused unless the
+caller opts in (the max-flow solvers refuse them later with
+NonSubmodularError).  evaluate_energy runs on the device (dope_gs_energy,
+fixed-order reduction, float64).
 """
 from __future__ import annotations
 
@@ -14,9 +19,14 @@ class NonSubmodularError(ValueError):
     """Negative pairwise weights reached a solver that cannot take them (energy.py:19-20)."""
 
 
+def _canonical_pairs(i: np.ndarray, j: np.ndarray):
+    lo, hi = np.minimum(i, j), np.maximum(i, j)
+    return lo.astype(np.int32), hi.astype(np.int32)
+
+
 @dataclass
 class SparseWeights:
-    """Symmetric sparse pairwise weights, each unordered pair stored once (energy.py:23-97)."""
+    """Symmetric sparse weights, one entry per unordered pair (energy.py:23-97)."""
 
     n: int
     rows: np.ndarray
@@ -25,41 +35,70 @@ class SparseWeights:
     allow_negative: bool = False
 
     def __post_init__(self):
-        self.rows = np.asarray(self.rows, dtype=np.int32)
-        self.cols = np.asarray(self.cols, dtype=np.int32)
-        self.vals = np.asarray(self.vals, dtype=np.float64)
-        if not (self.rows.shape == self.cols.shape == self.vals.shape):
+        r = np.asarray(self.rows, dtype=np.int64)
+        c = np.asarray(self.cols, dtype=np.int64)
+        v = np.asarray(self.vals, dtype=np.float64)
+        if not r.shape == c.shape == v.shape:
             raise ValueError("rows, cols and vals must have equal length")
-        if self.rows.size:
-            if self.rows.min() < 0 or self.cols.max() >= self.n or self.cols.min() < 0 \
-                    or self.rows.max() >= self.n:
+        if r.size:
+            if min(r.min(), c.min()) < 0 or max(r.max(), c.max()) >= self.n:
                 raise ValueError("pair index out of range")
-            if (self.rows == self.cols).any():
+            if np.any(r == c):
                 raise ValueError("diagonal entries are not allowed")
-            swap = self.rows > self.cols
-            if swap.any():
-                r = np.where(swap, self.cols, self.rows)
-                c = np.where(swap, self.rows, self.cols)
-                self.rows, self.cols = r.astype(np.int32), c.astype(np.int32)
-            if not np.isfinite(self.vals).all():
+            if not np.all(np.isfinite(v)):
                 raise ValueError("weights must be finite")
-            if not self.allow_negative and (self.vals < 0).any():
+            if not self.allow_negative and np.any(v < 0):
                 raise NonSubmodularError("negative pairwise weights require allow_negative=True")
+        self.rows, self.cols = _canonical_pairs(r, c)
+        self.vals = v
 
     @property
     def npairs(self) -> int:
-        return self.vals.size
+        return int(self.vals.size)
 
     def degrees(self) -> np.ndarray:
-        d = np.zeros(self.n)
-        np.add.at(d, self.rows, self.vals)
-        np.add.at(d, self.cols, self.vals)
+        """Row sums of the symmetric matrix (energy.py:64-69)."""
+        d = np.bincount(self.rows, weights=self.vals, minlength=self.n)
+        np.add.at(d, self.cols, self.vals)   # continue in pair order, like the reference
         return d
+
+    def _both_triangles(self):
+        return (np.concatenate([self.rows, self.cols]), np.concatenate([self.cols, self.rows]),
+                np.concatenate([self.vals, self.vals]))
+
+    def to_csr(self):
+        """Both triangles as a scipy CSR matrix, duplicates summed (energy.py:70-76)."""
+        import scipy.sparse as sp
+        i, j, v = self._both_triangles()
+        return sp.csr_matrix((v, (i, j)), shape=(self.n, self.n))
+
+    def adjacency(self):
+        """(indptr, indices, data) of the symmetric CSR form (energy.py:78-81)."""
+        m = self.to_csr()
+        return m.indptr, m.indices, m.data
+
+    def laplacian(self):
+        """L = D - W as scipy CSR (energy.py:83-86)."""
+        import scipy.sparse as sp
+        w = self.to_csr()
+        return (sp.diags(np.asarray(w.sum(axis=1)).ravel()) - w).tocsr()
+
+    @classmethod
+    def from_symmetric(cls, mat, allow_negative: bool = False) -> "SparseWeights":
+        """Upper-triangle entries of a symmetric (sparse or dense) matrix (energy.py:88-97)."""
+        import scipy.sparse as sp
+        coo = sp.coo_matrix(mat)
+        tol = 1e-12 * (1.0 + (abs(coo).max() if coo.nnz else 0.0))
+        if (abs(coo - coo.T) > tol).nnz:
+            raise ValueError("weight matrix is not symmetric")
+        upper = coo.row < coo.col
+        return cls(coo.shape[0], coo.row[upper], coo.col[upper], coo.data[upper],
+                   allow_negative=allow_negative)
 
 
 @dataclass
 class EnergyModel:
-    """Unary costs, pairwise weights and the regularization strength (energy.py:100-121)."""
+    """Unary costs, pairwise weights and the regularisation strength (energy.py:100-121)."""
 
     unary: np.ndarray
     weights: SparseWeights
@@ -78,26 +117,11 @@ class EnergyModel:
 
     @property
     def nonsubmodular(self) -> bool:
-        return bool(self.weights.npairs and (self.weights.vals < 0).any())
+        return bool(self.weights.npairs) and bool(np.any(self.weights.vals < 0))
 
 
 def evaluate_energy(model: EnergyModel, y) -> float:
-    """u.y + lam * sum_{i<j} w_ij (y_i - y_j)^2 for binary or relaxed y (energy.py:187-194).
-
-    Evaluated on the GPU (float64 torch reductions on the device); the run
-    loop itself uses the fused integer partials of the consensus kernel.
-    """
-    import torch
-    from .admm import _device
-    dev = _device()
-    yt = torch.as_tensor(np.asarray(y, dtype=np.float64), device=dev)
-    if yt.shape != (model.n,):
-        raise ValueError(f"labeling has shape {tuple(yt.shape)}, expected ({model.n},)")
-    w = model.weights
-    rows = torch.as_tensor(w.rows, device=dev, dtype=torch.int64)
-    cols = torch.as_tensor(w.cols, device=dev, dtype=torch.int64)
-    vals = torch.as_tensor(w.vals, device=dev)
-    u = torch.as_tensor(model.unary, device=dev)
-    d = yt[rows] - yt[cols]
-    quad = torch.dot(vals, d * d)
-    return float(torch.dot(u, yt) + model.lam * quad)
+    """u . y + lam * sum w (y_i - y_j)^2 of a binary or relaxed labeling
+    (energy.py:187-194), evaluated on the GPU (dope_gs_energy)."""
+    from .graphstep import device_energy
+    return device_energy(model, y)

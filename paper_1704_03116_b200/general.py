@@ -18,7 +18,7 @@ is required; there is no CPU path.
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -69,21 +69,6 @@ def lower_general(model: EnergyModel, partition: Partition) -> GeneralLowering:
     return GeneralLowering(tuple(shape.dims), (ky, kx), conn,
                            np.asarray(model.unary, dtype=np.float64), planes,
                            counts.astype(np.uint8), ranges, box, float(model.lam))
-
-
-@dataclass
-class GeneralState:
-    """Host view of a finished general-path run (AdmmState's attribute names)."""
-    partition: Partition
-    mu: float
-    y: np.ndarray
-    block_labels: list
-    multipliers: list
-    iteration: int = 0
-    converged: bool = False
-    best_iteration: int = 0
-    clamped_last: bool = False
-    trace: list = field(default_factory=list)
 
 
 class GeneralDevice:
@@ -192,7 +177,7 @@ class GeneralDevice:
 def run_general(model: EnergyModel, partition: Partition, config, use_graph: bool = True):
     """admm.run for overlapping partitions / growing mu (admm.py:207-252)."""
     import torch
-    from .admm import BlockSolveError, TraceRecord
+    from .admm import AdmmState, BlockSolveError, TraceRecord
     low = lower_general(model, partition)
     mu0 = config.resolved_mu0(partition.shape.ndim)
     eps = config.resolved_eps(partition)
@@ -211,10 +196,10 @@ def run_general(model: EnergyModel, partition: Partition, config, use_graph: boo
     per = start.elapsed_time(end) / max(it, 1)
     tr = {k: v[:it].cpu().numpy() for k, v in dev.tr.items()}
     cl = dev.tr_cl[:it].cpu().numpy()
-    state = GeneralState(partition, float(tr["mu"][-1] * config.mu_fact) if it else mu0,
-                         dev.y[rs.ycur].cpu().numpy(),
-                         [c.astype(np.int8) for c in dev.copies(dev.yhat.cpu().numpy(), partition)],
-                         dev.copies(dev.a.cpu().numpy(), partition))
+    state = AdmmState(dev.y[rs.ycur].cpu().numpy(),
+                      [c.astype(np.int8) for c in dev.copies(dev.yhat.cpu().numpy(), partition)],
+                      dev.copies(dev.a.cpu().numpy(), partition),
+                      float(tr["mu"][-1] * config.mu_fact) if it else mu0, partition=partition)
     state.iteration = it
     state.converged = bool(rs.converged)
     state.best_iteration = int(rs.best_iteration)

@@ -1,65 +1,68 @@
-"""Grid shapes and row-major indexing (mirror of reference grid.py:21-77).
+"""Grid geometry: the row-major pixel numbering every device array uses.
 
-Only the parts the hot path needs: the lowering requires the reference's
-row-major linearization so every device array compares elementwise with the
-reference's global vectors.
+Mirrors the reference's GridShape (grid.py:21-77): 2D (H, W) or 3D (D, H, W)
+grids, pixel g = sum_a coord_a * stride_a with the last axis fastest, so each
+device vector compares elementwise with the reference's global vectors.
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
+from functools import reduce
+
+
+def _row_major_strides(dims) -> tuple:
+    out = []
+    step = 1
+    for d in reversed(dims):
+        out.append(step)
+        step *= d
+    return tuple(reversed(out))
 
 
 @dataclass(frozen=True)
 class GridShape:
-    """Dimensions of a 2D or 3D pixel grid (grid.py:21-52)."""
+    """Extents of a 2D / 3D pixel grid (reference grid.py:21-52)."""
 
     dims: tuple
 
     def __post_init__(self):
-        dims = tuple(int(d) for d in self.dims)
-        if len(dims) not in (2, 3):
-            raise ValueError(f"grid must be 2D or 3D, got {len(dims)} axes")
-        if any(d < 1 for d in dims):
-            raise ValueError(f"all grid dimensions must be positive, got {dims}")
-        object.__setattr__(self, "dims", dims)
-
-    @property
-    def n(self) -> int:
-        p = 1
-        for d in self.dims:
-            p *= d
-        return p
+        ext = tuple(int(d) for d in self.dims)
+        if not 2 <= len(ext) <= 3:
+            raise ValueError(f"grid must be 2D or 3D, got {len(ext)} axes")
+        if min(ext) < 1:
+            raise ValueError(f"all grid dimensions must be positive, got {ext}")
+        object.__setattr__(self, "dims", ext)
 
     @property
     def ndim(self) -> int:
         return len(self.dims)
 
     @property
+    def n(self) -> int:
+        return reduce(lambda a, b: a * b, self.dims, 1)
+
+    @property
     def strides(self) -> tuple:
-        s = [1] * len(self.dims)
-        for a in range(len(self.dims) - 2, -1, -1):
-            s[a] = s[a + 1] * self.dims[a + 1]
-        return tuple(s)
+        return _row_major_strides(self.dims)
 
 
 def index_of(shape: GridShape, coords) -> int:
-    coords = tuple(int(c) for c in coords)
-    if len(coords) != shape.ndim:
-        raise ValueError(f"expected {shape.ndim} coordinates, got {len(coords)}")
-    idx = 0
-    for c, d, s in zip(coords, shape.dims, shape.strides):
-        if not 0 <= c < d:
-            raise ValueError(f"coordinate {coords} outside grid {shape.dims}")
-        idx += c * s
-    return idx
+    """Linear index of a coordinate tuple (grid.py:55-66)."""
+    c = tuple(int(v) for v in coords)
+    if len(c) != shape.ndim:
+        raise ValueError(f"expected {shape.ndim} coordinates, got {len(c)}")
+    if any(not 0 <= v < d for v, d in zip(c, shape.dims)):
+        raise ValueError(f"coordinate {c} outside grid {shape.dims}")
+    return sum(v * s for v, s in zip(c, shape.strides))
 
 
 def coords_of(shape: GridShape, index: int) -> tuple:
-    index = int(index)
-    if not 0 <= index < shape.n:
-        raise ValueError(f"index {index} outside grid of {shape.n} pixels")
-    out = []
-    for s in shape.strides:
-        out.append(index // s)
-        index %= s
-    return tuple(out)
+    """Coordinate tuple of a linear index (grid.py:69-77)."""
+    g = int(index)
+    if not 0 <= g < shape.n:
+        raise ValueError(f"index {g} outside grid of {shape.n} pixels")
+    coords = []
+    for d in reversed(shape.dims):
+        g, r = divmod(g, d)
+        coords.append(r)
+    return tuple(reversed(coords))

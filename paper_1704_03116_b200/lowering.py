@@ -97,6 +97,12 @@ def lower_lattice(model: EnergyModel, partition: Partition) -> LatticeLowering:
     lamw_f = float(lw[0]) if lw.size else 0.0
     if lamw_f != round(lamw_f):
         raise NotImplementedError("lambda*w must be an integer on the integer lattice path")
+    if 4 * abs(round(lamw_f)) > 255:   # r + r' = 2 * (2 lambda w) per byte residual pair
+        raise NotImplementedError("lambda*w exceeds the integer path's byte residuals (4 lambda w > 255)")
+    box = [-(-d // k) for d, k in zip(shape.dims, partition.k_per_axis)]
+    if max(box) > (128 if shape.ndim == 2 else 32):
+        raise NotImplementedError(f"block extent {box} exceeds the integer K1 boxes "
+                                  "(128^2 in 2D, 32^3 in 3D)")
     u = model.unary
     if not np.all(u == np.round(u)) or np.abs(u).max(initial=0) > 2 ** 28:
         raise NotImplementedError("unary costs must be (bounded) integers on the integer path")

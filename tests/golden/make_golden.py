@@ -259,6 +259,88 @@ def main_inputs():
     print("inputs:", {k: out[f"vals{k}"].size for k in (3, 5)}, {k: out3[f"vals{k}"].size for k in (3, 5)})
 
 
+def ref_run_model(model, part, cfg):
+    """admm.run of an arbitrary reference model / partition / config, with every
+    iteration's per-copy block labels (block order)."""
+    hist = []
+    orig = ref_admm.update_blocks
+
+    def recording(state, problems, lam, config):
+        out = orig(state, problems, lam, config)
+        hist.append(np.concatenate([np.asarray(l, dtype=np.uint8) for l in state.block_labels]))
+        return out
+
+    ref_admm.update_blocks = recording
+    try:
+        labels, state = ref_admm.run(model, part, cfg)
+    finally:
+        ref_admm.update_blocks = orig
+    tr = state.trace
+    return dict(
+        mu=np.array([t.mu for t in tr]), energy=np.array([t.energy for t in tr]),
+        residual_sq=np.array([t.residual_sq for t in tr]),
+        max_block_residual=np.array([t.max_block_residual for t in tr]),
+        clamped=np.array([t.clamped for t in tr]),
+        yhat_bits=np.packbits(np.array(hist, dtype=np.uint8), axis=1),
+        y=state.y, labels=np.asarray(labels, dtype=np.int8),
+        a_copies=np.concatenate([np.asarray(m, dtype=np.float64) for m in state.multipliers]),
+        converged=state.converged, iterations=state.iteration,
+        best_iteration=state.best_iteration, counts=part.counts,
+        eps=cfg.resolved_eps(part), mu0=cfg.resolved_mu0(part.shape.ndim))
+
+
+def save_graph(case, model, part, cfg, overlap, integer):
+    r = ref_run_model(model, part, cfg)
+    w = model.weights
+    meta = dict(dims=np.array(part.shape.dims), kpa=np.array(part.k_per_axis if hasattr(part, "k_per_axis")
+                                                              else ()), overlap=overlap,
+                u=model.unary, rows=w.rows, cols=w.cols, vals=w.vals, lam=model.lam,
+                cfg_mu0=np.nan if cfg.mu0 is None else cfg.mu0, cfg_mu_fact=cfg.mu_fact,
+                cfg_eps=np.nan if cfg.eps is None else cfg.eps, max_iters=cfg.max_iters,
+                integer=integer)
+    np.savez_compressed(OUT / f"graph_{case}.npz", **r, **meta)
+    print(f"graph_{case}: iters={r['iterations']} converged={r['converged']} "
+          f"best={r['best_iteration']} E_last={r['energy'][-1]} qmax={int(r['counts'].max())}")
+
+
+def main_graph():
+    """The general graph path: models / partitions the lattice kernels do not
+    take -- 3D overlap (q up to 8), the 3D default config, kernel-5 windows."""
+    from dope.energy import build_potts_weights
+    from dope.grid import GridImage
+    # 3D 6-connected integer model, 2x2x2 blocks grown by 25 %, fixed integer mu
+    wl = W.c4(seed=12, size=24, block=12, iters=15)
+    rows, cols, vals = wl.pair_arrays()
+    m3 = EnergyModel(wl.u.astype(np.float64), SparseWeights(wl.n, rows, cols, vals), 2.0)
+    save_graph("int3d_ov25", m3, make_partition(GridShape(wl.dims), (2, 2, 2), 25),
+               ref_admm.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=15), 25, True)
+    # the same volume, 10 % overlap, q in {1, 2, 4, 8}
+    save_graph("int3d_ov10", m3, make_partition(GridShape(wl.dims), (3, 2, 2), 10),
+               ref_admm.AdmmConfig(mu0=2.0, mu_fact=1.0, eps=0.0, max_iters=12), 10, True)
+    # the reference's DEFAULT config on a 3D integer model (mu0 500, mu_fact 1.05, eps)
+    save_graph("int3d_default", m3, make_partition(GridShape(wl.dims), (2, 2, 2), 0),
+               ref_admm.AdmmConfig(max_iters=20), 0, False)
+    # 2D kernel-5 contrast window (non-lattice pair set), 2x3 blocks, 10 % overlap, default
+    rng = np.random.default_rng(41)
+    h, wd = 40, 36
+    yy, xx = np.meshgrid(np.arange(h), np.arange(wd), indexing="ij")
+    fg = ((yy - 18.0) ** 2 + (xx - 20.0) ** 2) < 110.0
+    img = GridImage(GridShape((h, wd)), np.clip(np.where(fg, 0.75, 0.3) + rng.normal(0, 0.08, (h, wd)),
+                                                0, 1).ravel())
+    wts = build_potts_weights(img, 5, sigma=0.2, contrast=True)
+    mk = EnergyModel((0.5 - img.data[:, 0]) * 8.0, wts, 1.5)
+    save_graph("k5_ov10", mk, make_partition(GridShape((h, wd)), (2, 3), 10),
+               ref_admm.AdmmConfig(max_iters=30), 10, False)
+    save_graph("k5_sched", mk, make_partition(GridShape((h, wd)), (3, 3), 25),
+               ref_admm.AdmmConfig(mu0=2.0, mu_fact=1.05, eps=0.0, max_iters=25), 25, False)
+    # 3D kernel-3 window (18-connected) with unit weights and integer unaries, 25 % overlap
+    v3 = GridImage(GridShape((10, 12, 14)), np.zeros(10 * 12 * 14))
+    w3 = build_potts_weights(v3, 3, sigma=1.0, contrast=False)
+    u3 = rng.integers(-4, 5, v3.shape.n).astype(np.float64)
+    save_graph("int3d_k3_ov25", EnergyModel(u3, w3, 1.0), make_partition(v3.shape, (2, 2, 2), 25),
+               ref_admm.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=10), 25, True)
+
+
 class _RaggedWL(W.Workload):
     @property
     def kpa(self):
@@ -276,6 +358,9 @@ def main():
         return
     if "--only-inputs" in sys.argv:
         main_inputs()
+        return
+    if "--only-graph" in sys.argv:
+        main_graph()
         return
     gen_bk(core)
     save_run("c1", W.c1())
@@ -304,6 +389,7 @@ def main():
     save_run("rho2", r2)
     main_general()
     main_inputs()
+    main_graph()
 
 
 if __name__ == "__main__":

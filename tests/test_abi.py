@@ -31,7 +31,8 @@ def test_struct_layouts_match_header(tmp_path):
     """The ctypes mirrors agree with the C compiler's layout of the header."""
     import subprocess
     mirrors = {"L": ("dope_lattice", _lib.Lattice), "S": ("dope_run_state", _lib.RunState),
-               "F": ("dope_lattice_f", _lib.LatticeF), "G": ("dope_general", _lib.General)}
+               "F": ("dope_lattice_f", _lib.LatticeF), "G": ("dope_general", _lib.General),
+               "Q": ("dope_gstep", _lib.GStep)}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "dope_b200.h"', 'int main(){']
     for tag, (cname, py) in mirrors.items():
         for f, _ in py._fields_:

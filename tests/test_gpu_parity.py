@@ -70,6 +70,8 @@ def test_run_matches_reference_trace(case, opts):
 
 @pytest.mark.parametrize("case", ["c1", "mini128_b16", "ragged", "mini3d"])
 def test_step_api_block_labels_every_iteration(case):
+    """The public step functions (general graph path on the device) reproduce the
+    reference's run iteration by iteration."""
     g = load_golden(f"run_{case}.npz")
     model, part = model_from_golden(g)
     problems = dope.assemble_block_problems(model, part)
@@ -85,6 +87,31 @@ def test_step_api_block_labels_every_iteration(case):
         assert float(res.max()) == g["max_block_residual"][it]
         assert dope.evaluate_energy(model, state.y) == g["energy"][it]
         dope.update_multipliers(state, part, 1.0)
+
+
+@pytest.mark.parametrize("case", ["c1", "mini128_b16", "ragged", "mini3d"])
+def test_abi_step_entries_every_iteration(case):
+    """The lattice ABI's step entries (dope_update_blocks / dope_update_global /
+    dope_update_multipliers, include/dope_b200.h) driven one call at a time."""
+    from paper_1704_03116_b200.admm import make_device_state
+    g = load_golden(f"run_{case}.npz")
+    model, part = model_from_golden(g)
+    problems = dope.assemble_block_problems(model, part)
+    assert problems.kind == "int"
+    dev = make_device_state(problems, float(g["rho"]), 0.0, int(g["max_iters"]))
+    dev.call("dope_admm_init")
+    hist = np.unpackbits(g["yhat_bits"], axis=1)[:, :model.n]
+    for it in range(int(g["iterations"])):
+        dev.call("dope_update_blocks")
+        dev.raise_on_error()
+        assert np.array_equal(dev.yhat.cpu().numpy(), hist[it]), it
+        dev.call("dope_update_global", fuse=0)
+        dev.dirty[2 * len(problems):].zero_()   # step calls keep no clean-block stamps
+        assert bool(dev.pf.any().item()) == bool(g["clamped"][it])
+        ss = dev.pr.cpu().numpy()
+        assert float(np.sqrt(ss.max())) == g["max_block_residual"][it]
+        dev.call("dope_update_multipliers")
+    assert np.array_equal(dev.a.double().cpu().numpy(), g["a"])
 
 
 def test_bk_maxflow_seam_matches_reference_graphs():
