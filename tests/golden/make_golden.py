@@ -289,11 +289,11 @@ def ref_run_model(model, part, cfg):
         eps=cfg.resolved_eps(part), mu0=cfg.resolved_mu0(part.shape.ndim))
 
 
-def save_graph(case, model, part, cfg, overlap, integer):
+def save_graph(case, model, shape, kpa, overlap, cfg, integer):
+    part = make_partition(shape, kpa, overlap)
     r = ref_run_model(model, part, cfg)
     w = model.weights
-    meta = dict(dims=np.array(part.shape.dims), kpa=np.array(part.k_per_axis if hasattr(part, "k_per_axis")
-                                                              else ()), overlap=overlap,
+    meta = dict(dims=np.array(shape.dims), kpa=np.array(kpa), overlap=overlap,
                 u=model.unary, rows=w.rows, cols=w.cols, vals=w.vals, lam=model.lam,
                 cfg_mu0=np.nan if cfg.mu0 is None else cfg.mu0, cfg_mu_fact=cfg.mu_fact,
                 cfg_eps=np.nan if cfg.eps is None else cfg.eps, max_iters=cfg.max_iters,
@@ -312,14 +312,14 @@ def main_graph():
     wl = W.c4(seed=12, size=24, block=12, iters=15)
     rows, cols, vals = wl.pair_arrays()
     m3 = EnergyModel(wl.u.astype(np.float64), SparseWeights(wl.n, rows, cols, vals), 2.0)
-    save_graph("int3d_ov25", m3, make_partition(GridShape(wl.dims), (2, 2, 2), 25),
-               ref_admm.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=15), 25, True)
+    save_graph("int3d_ov25", m3, GridShape(wl.dims), (2, 2, 2), 25,
+               ref_admm.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=15), True)
     # the same volume, 10 % overlap, q in {1, 2, 4, 8}
-    save_graph("int3d_ov10", m3, make_partition(GridShape(wl.dims), (3, 2, 2), 10),
-               ref_admm.AdmmConfig(mu0=2.0, mu_fact=1.0, eps=0.0, max_iters=12), 10, True)
+    save_graph("int3d_ov10", m3, GridShape(wl.dims), (3, 2, 2), 10,
+               ref_admm.AdmmConfig(mu0=2.0, mu_fact=1.0, eps=0.0, max_iters=12), True)
     # the reference's DEFAULT config on a 3D integer model (mu0 500, mu_fact 1.05, eps)
-    save_graph("int3d_default", m3, make_partition(GridShape(wl.dims), (2, 2, 2), 0),
-               ref_admm.AdmmConfig(max_iters=20), 0, False)
+    save_graph("int3d_default", m3, GridShape(wl.dims), (2, 2, 2), 0,
+               ref_admm.AdmmConfig(max_iters=20), False)
     # 2D kernel-5 contrast window (non-lattice pair set), 2x3 blocks, 10 % overlap, default
     rng = np.random.default_rng(41)
     h, wd = 40, 36
@@ -329,16 +329,15 @@ def main_graph():
                                                 0, 1).ravel())
     wts = build_potts_weights(img, 5, sigma=0.2, contrast=True)
     mk = EnergyModel((0.5 - img.data[:, 0]) * 8.0, wts, 1.5)
-    save_graph("k5_ov10", mk, make_partition(GridShape((h, wd)), (2, 3), 10),
-               ref_admm.AdmmConfig(max_iters=30), 10, False)
-    save_graph("k5_sched", mk, make_partition(GridShape((h, wd)), (3, 3), 25),
-               ref_admm.AdmmConfig(mu0=2.0, mu_fact=1.05, eps=0.0, max_iters=25), 25, False)
+    save_graph("k5_ov10", mk, GridShape((h, wd)), (2, 3), 10, ref_admm.AdmmConfig(max_iters=30), False)
+    save_graph("k5_sched", mk, GridShape((h, wd)), (3, 3), 25,
+               ref_admm.AdmmConfig(mu0=2.0, mu_fact=1.05, eps=0.0, max_iters=25), False)
     # 3D kernel-3 window (18-connected) with unit weights and integer unaries, 25 % overlap
     v3 = GridImage(GridShape((10, 12, 14)), np.zeros(10 * 12 * 14))
     w3 = build_potts_weights(v3, 3, sigma=1.0, contrast=False)
     u3 = rng.integers(-4, 5, v3.shape.n).astype(np.float64)
-    save_graph("int3d_k3_ov25", EnergyModel(u3, w3, 1.0), make_partition(v3.shape, (2, 2, 2), 25),
-               ref_admm.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=10), 25, True)
+    save_graph("int3d_k3_ov25", EnergyModel(u3, w3, 1.0), v3.shape, (2, 2, 2), 25,
+               ref_admm.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=10), True)
 
 
 class _RaggedWL(W.Workload):
