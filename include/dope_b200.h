@@ -272,7 +272,11 @@ int dope_sharded_finish_group(const dope_lattice *const *shards, int32_t nshards
  * kind, DOPE_GRAPH_CACHE entries each) and a way to drop them all. */
 int64_t dope_graph_cache_entries(void);
 void dope_graph_cache_clear(void);
-/* binarize (admm.py:260-262) of the current iterate into out[n] (0/1). */
+/* The integer path's unary from a float64 vector (EnergyModel.unary): out[i]
+ * = u[i] when every u[i] is an integer within +-2^28, else *bad |= 1 (zero
+ * it first) -- the device side of re-running a lowered model on new unaries. */
+int dope_unary_i32(const double *u, int64_t n, int32_t *out, int32_t *bad, void *stream);
+/* binarize (admm.py:202-204) of the current iterate into out[n] (0/1). */
 int dope_binarize(const dope_lattice *L, uint8_t *out, void *stream);
 /* evaluate_energy of an arbitrary doubled labeling y2 (int path):
  * out[0] = sum u*y2 * 2 + lamw * sum (y2_i - y2_j)^2, i.e. 4*E (exact). */

@@ -127,6 +127,44 @@ class BlockProblems:
             self.u = torch.as_tensor(self.lowering.u, device=self.device)
         self._graph = None
 
+    def refresh_unary(self, model: EnergyModel) -> bool:
+        """Take a new model that shares this one's weights, partition and lambda:
+        upload its unary (the integer path converts and checks it on the device).
+        False when the new unary does not fit this lowering."""
+        import torch
+        if model.weights is not self.model.weights or float(model.lam) != float(self.model.lam):
+            return False
+        if model is self.model:
+            return True
+        u64 = torch.as_tensor(model.unary, device=self.device)
+        if self.kind == "int":
+            bad = torch.zeros(1, dtype=torch.int32, device=self.device)
+            _lib.check(_lib.lib().dope_unary_i32(u64.data_ptr(), u64.numel(), self.u.data_ptr(), bad.data_ptr(),
+                                                 C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)),
+                       "dope_unary_i32")
+            if bad.item():
+                return False
+        elif self.kind == "float":
+            self.u.copy_(u64)
+        self.model = model
+        self._graph = None
+        return True
+
+    def run_state(self, mu, eps: float, config: "AdmmConfig"):
+        """Device buffers for a run of this lowering, reused across runs with the
+        same parameters (so the cached CUDA graph of the loop is reused too)."""
+        key = (float(mu), float(eps), config.max_iters, config.warm_start, config.skip_clean, config.digests)
+        last = getattr(self, "_run_owner", None)
+        if last is not None and last() is not None:
+            last()._detach()      # a live state of the previous run keeps its own copy
+        if getattr(self, "_run_key", None) != key:
+            self._run_dev = make_device_state(self, mu, eps, config.max_iters, config.warm_start,
+                                              config.skip_clean, config.digests)
+            self._run_key = key
+        elif self._run_dev.trace_hash is not None:
+            self._run_dev.trace_hash.zero_()
+        return self._run_dev
+
     def graph(self):
         """The general graph path's device data (graphstep.GraphProblems)."""
         if self._graph is None:
@@ -259,7 +297,27 @@ def make_device_state(problems: BlockProblems, mu: float, eps: float, max_iters:
 
 
 def assemble_block_problems(model: EnergyModel, partition: Partition) -> BlockProblems:
+    """blockform.assemble_block_problems (blockform.py:48-86): the device lowering."""
     return BlockProblems(model, partition)
+
+
+_lowered: dict = {}
+
+
+def _problems_for(model: EnergyModel, partition: Partition) -> BlockProblems:
+    """assemble_block_problems, reused when the same weights / partition come
+    back with new unaries (the serving loop of run(): the lattice checks and
+    device buffers are kept, only the unary is uploaded)."""
+    import weakref
+    key = (id(model.weights), id(partition))
+    hit = _lowered.get(key)
+    if hit is not None and hit[0]() is model.weights and hit[1]() is partition:
+        if hit[2].refresh_unary(model):
+            return hit[2]
+    problems = BlockProblems(model, partition)
+    drop = lambda _r, k=key: _lowered.pop(k, None)
+    _lowered[key] = (weakref.ref(model.weights, drop), weakref.ref(partition, drop), problems)
+    return problems
 
 
 class _DeviceState:
@@ -426,6 +484,14 @@ class AdmmState:
         st._src = ("lattice", dev)
         return st
 
+    def _detach(self):
+        """Copy a lattice run's fields off the device buffers (they are about to
+        be reused by the next run of the same problems)."""
+        if self._src is not None and self._src[0] == "lattice":
+            dev = self._src[1]
+            self._src = ("lattice_host", (dev.y2_current().double().div_(2.0).cpu().numpy(),
+                                          dev.yhat.cpu().numpy(), dev.multipliers().double().cpu().numpy()))
+
     @classmethod
     def from_device(cls, partition: Partition, y, yhat_cat, a_cat, layout, mu: float) -> "AdmmState":
         """Fields live in the general graph path's entry-indexed device buffers."""
@@ -439,6 +505,12 @@ class AdmmState:
 
     def _fetch(self, what: str):
         kind, src = self._src
+        if kind == "lattice_host":
+            y, yhat, a = src
+            if what == "y":
+                return y
+            lay = self._entries()
+            return lay.split((yhat.astype(np.int8) if what == "block_labels" else a)[lay.ent_pix])
         if kind == "lattice":
             dev = src
             if what == "y":
@@ -497,11 +569,15 @@ class AdmmState:
         """Current block labels (yhat) scattered to global layout."""
         if self._block_labels is None and self._src is not None and self._src[0] == "lattice":
             return self._src[1].yhat.cpu().numpy().astype(np.int8)
+        if self._block_labels is None and self._src is not None and self._src[0] == "lattice_host":
+            return self._src[1][1].astype(np.int8)
         return self._to_global(self.block_labels, np.int8)
 
     def multipliers_global(self) -> np.ndarray:
         if self._multipliers is None and self._src is not None and self._src[0] == "lattice":
             return self._src[1].multipliers().double().cpu().numpy()
+        if self._multipliers is None and self._src is not None and self._src[0] == "lattice_host":
+            return self._src[1][2]
         return self._to_global(self.multipliers, np.float64)
 
 
@@ -540,9 +616,49 @@ def _dev_entries(gp_layout, per_block, dtype, what):
     return t
 
 
+def _lattice_blocks(state: AdmmState, problems: BlockProblems, lam: float, config: AdmmConfig):
+    """update_blocks on the integer lattice K1 (dope_update_blocks) when the
+    state is one the kernel represents exactly: y in {0, 1/2, 1}, integer
+    multipliers within int16, an integer mu dividing lambda*w (q == 1).
+    Returns the per-block labels, or None when the state does not qualify."""
+    import torch
+    low = problems.lowering
+    mu = state.mu
+    if (problems.kind != "int" or config.solver.kind != "maxflow" or float(lam) != problems.lam
+            or not mu > 0 or mu != round(mu) or low.lamw % int(round(mu))):
+        return None
+    y2 = 2.0 * np.asarray(state.y, dtype=np.float64)
+    if y2.shape != (low.n,) or not np.all(np.isin(y2, (0.0, 1.0, 2.0))):
+        return None
+    from .graphstep import layout
+    lay = layout(problems.partition)
+    a = np.empty(low.n)
+    a[lay.ent_pix] = lay.join(state.multipliers, np.float64, "multipliers")
+    if not np.all(a == np.round(a)) or np.abs(a).max(initial=0) > 32000:
+        return None
+    dev = getattr(problems, "_step_dev", None)
+    if dev is None:
+        dev = problems._step_dev = _DeviceState(problems, int(round(mu)), 0.0, 1, True, False)
+        dev.call("dope_admm_init")
+    dev.L.mu = int(round(mu))
+    dev.y2_current().copy_(torch.as_tensor(y2.astype(np.uint8), device=problems.device))
+    dev.a.copy_(torch.as_tensor(a.astype(np.int16), device=problems.device))
+    dev.dirty[:low.K].fill_(1)
+    dev.call("dope_update_blocks")
+    dev.raise_on_error()
+    return lay.split(dev.yhat.cpu().numpy()[lay.ent_pix].astype(np.int8))
+
+
 def update_blocks(state: AdmmState, problems, lam: float, config: AdmmConfig) -> AdmmState:
     """Re-solve every block against the current y (admm.py:113-133): block
-    objectives and block min cuts (one CTA per block) on the device."""
+    objectives and block min cuts (one CTA per block) on the device -- the
+    integer lattice K1 when the state is one it represents exactly, else the
+    general graph path."""
+    if isinstance(problems, BlockProblems):
+        labels = _lattice_blocks(state, problems, lam, config)
+        if labels is not None:
+            state.block_labels = labels
+            return state
     gp = _graph(problems)
     lay = gp.layout
     y = _dev_vec(state.y, np.float64, gp.device)
@@ -630,8 +746,7 @@ def _run_lattice(model, partition, config, problems) -> tuple:
     eps = config.resolved_eps(partition)
     if problems.kind == "int" and (mu0 != round(mu0) or problems.lowering.lamw % int(round(mu0)) != 0):
         raise NotImplementedError("the integer lattice path needs an integer mu dividing lambda*w")
-    dev = make_device_state(problems, mu0, eps, config.max_iters, config.warm_start, config.skip_clean,
-                            config.digests)
+    dev = problems.run_state(mu0, eps, config)
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     start.record()
@@ -649,6 +764,8 @@ def _run_lattice(model, partition, config, problems) -> tuple:
     cl = dev.tr_cl[:it].cpu().numpy()
     per = total_ms / max(it, 1)   # one graph launch: the per-iteration average
     state = AdmmState.from_lattice(partition, dev, mu0)
+    import weakref
+    problems._run_owner = weakref.ref(state)
     mu = mu0
     for t in range(it):
         state.trace.append(TraceRecord(t + 1, mu, float(e[t]), float(r2[t]), float(mr[t]), per, bool(cl[t])))
@@ -688,7 +805,7 @@ def run(model: EnergyModel, partition: Partition, config: AdmmConfig,
     lattice_ok = config.solver.kind == "maxflow"
     if lattice_ok and not overlap and config.mu_fact == 1.0:
         if problems is None:
-            problems = assemble_block_problems(model, partition)
+            problems = _problems_for(model, partition)
         if problems.kind in ("int", "float"):
             try:
                 return _run_lattice(model, partition, config, problems)

@@ -810,6 +810,19 @@ __global__ void k_ghost_consensus(Lat2 L) {
     }
 }
 
+// The integer path's unary from the caller's float64 vector (the reference's
+// EnergyModel.unary): exact integers within +-2^28, else *bad = 1.
+__global__ void k_unary_i32(const double *__restrict__ u, int64_t n, int32_t *__restrict__ out, int32_t *bad) {
+    int b = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = u[i];
+        const bool ok = v == rint(v) && fabs(v) <= 268435456.0;
+        b |= !ok;
+        out[i] = ok ? (int32_t)v : 0;
+    }
+    if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
 // Sharded mode, end of run: move this shard's energy of the last iterate into
 // its agg slot (the cross-shard sum happens in k_finish_decide).
 __global__ void k_publish_energy(Lat2 L) {
@@ -2215,6 +2228,13 @@ int dope_ghost_consensus(const dope_lattice *L, void *stream) {
     const int64_t unit = P.o.ndim == 3 ? (int64_t)P.o.ay.dim * P.o.W : (int64_t)P.o.W;
     k_ghost_consensus<<<grid_for(unit), 256, 0, (cudaStream_t)stream>>>(P.o);
     return cuda_check(cudaGetLastError(), "ghost_consensus");
+}
+
+int dope_unary_i32(const double *u, int64_t n, int32_t *out, int32_t *bad, void *stream) {
+    if (n < 0 || (n && (!u || !out || !bad))) return DOPE_E_ARGS;
+    if (n == 0) return DOPE_OK;
+    k_unary_i32<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(u, n, out, bad);
+    return cuda_check(cudaGetLastError(), "unary_i32");
 }
 
 int dope_trace_digest(const dope_lattice *L, void *stream) {

@@ -28,8 +28,10 @@ def write_trace(path, trace) -> None:
 
 
 def write_report(path, report: dict) -> None:
+    """Sorted-key JSON with a trailing newline, byte for byte the reference's format."""
     with open(path, "w", encoding="utf-8") as f:
         json.dump(report, f, sort_keys=True, indent=2)
+        f.write("\n")
 
 
 def write_labels(path_base, labels, shape: GridShape) -> str:

@@ -22,6 +22,8 @@ def test_trace_csv_schema(tmp_path):
 def test_report_and_labels(tmp_path):
     dio.write_report(tmp_path / "r.json", {"b": 1, "a": [1, 2]})
     assert list(json.load(open(tmp_path / "r.json")).keys()) == ["a", "b"]
+    # byte-identical to the reference writer (io.py:227-231: json.dump then "\n")
+    assert open(tmp_path / "r.json", "rb").read() == b'{\n  "a": [\n    1,\n    2\n  ],\n  "b": 1\n}\n'
     lab = np.array([0, 1, 1, 0, 1, 0], dtype=np.int8)
     path = dio.write_labels(tmp_path / "lab", lab, dope.GridShape((2, 3)))
     data = open(path, "rb").read()

@@ -129,14 +129,3 @@ def test_nccl_single_rank_graph_matches_single_gpu(three_d):
     finally:
         comm.close()
     _same_run(trace, st, labels, s1, labels1)
-
-
-def test_shard_for_rank_refuses_what_it_cannot_run_exactly():
-    wl = W.mini_disks(256, 64, 8, 2, 5, seed=1)
-    model, part = _model(wl)
-    with pytest.raises(NotImplementedError):
-        sharded.shard_for_rank(model, part, dope.AdmmConfig(mu0=1.0, max_iters=5), 0, 1)  # mu_fact 1.05
-    with pytest.raises(NotImplementedError):
-        sharded.shard_for_rank(model, part, dope.AdmmConfig(mu0=1.5, mu_fact=1.0, max_iters=5), 0, 1)
-    with pytest.raises(NotImplementedError):
-        sharded.shard_for_rank(model, part, dope.AdmmConfig(mu0=3.0, mu_fact=1.0, max_iters=5), 0, 1)

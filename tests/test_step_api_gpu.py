@@ -237,3 +237,39 @@ def test_run_state_fields_materialise_from_the_device():
     dope.update_blocks(state, problems, model.lam, dope.AdmmConfig(mu0=1.0, mu_fact=1.0))
     dope.update_global(state, problems, part, model.lam)
     assert state.y.shape == (wl.n,)
+
+
+def test_repeated_runs_reuse_the_lowering_and_keep_the_graph_cache_bounded():
+    """The serving loop of run(): the same weights / partition with new unaries
+    reuse the lowering, the device buffers and the captured CUDA graph; 50 runs
+    leave the library's graph cache at a constant size; a state that outlives
+    the next run keeps its own fields."""
+    from paper_1704_03116_b200 import _lib, workloads as W
+    wl = W.mini_disks(256, 64, 8, 2, 12, seed=4)
+    rows, cols, vals = wl.pair_arrays()
+    weights = dope.SparseWeights(wl.n, rows, cols, vals)
+    part = dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0, materialize=False)
+    cfg = dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=wl.iters)
+    rng = np.random.default_rng(5)
+    lb = _lib.lib()
+    sizes, first = [], None
+    for i in range(50):
+        u = wl.u.astype(np.float64) + rng.integers(-1, 2, wl.n)
+        labels, state = dope.run(dope.EnergyModel(u, weights, wl.lam), part, cfg)
+        if i == 0:
+            first = (u, labels, state, state.y.copy())
+        sizes.append(int(lb.dope_graph_cache_entries()))
+        if i in (1, 37):   # fresh lowering of the same model: identical results
+            fresh = dope.run(dope.EnergyModel(u, dope.SparseWeights(wl.n, rows, cols, vals), wl.lam),
+                             dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0), cfg)
+            assert np.array_equal(fresh[0], labels)
+            assert [t.energy for t in fresh[1].trace] == [t.energy for t in state.trace]
+    assert len(set(sizes[5:])) == 1, sizes
+    u0, labels0, state0, y0 = first
+    assert np.array_equal(state0.y, y0)                     # survived 49 later runs
+    assert np.array_equal(dope.binarize(state0.y), labels0)
+    # half-integer unaries leave the integer path: the run falls through to the float kernels
+    half = dope.run(dope.EnergyModel(u0 + 0.5, weights, wl.lam), part, cfg)
+    ref = dope.run(dope.EnergyModel(u0 + 0.5, dope.SparseWeights(wl.n, rows, cols, vals), wl.lam),
+                   dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0), cfg)
+    assert np.array_equal(half[0], ref[0])
