@@ -136,7 +136,15 @@ class BlockProblems:
             return False
         if model is self.model:
             return True
-        u64 = torch.as_tensor(model.unary, device=self.device)
+        # stage through a pinned buffer: the host copy runs on all cores, the
+        # DMA at full link speed (a pageable H2D of 134 MB at 4096^2 is slower)
+        src = torch.from_numpy(np.ascontiguousarray(model.unary, dtype=np.float64))
+        if getattr(self, "_u_pinned", None) is None or self._u_pinned.shape != src.shape:
+            self._u_pinned = torch.empty(src.shape, dtype=torch.float64).pin_memory()
+            self._u_dev64 = torch.empty(src.shape, dtype=torch.float64, device=self.device)
+        self._u_pinned.copy_(src)
+        u64 = self._u_dev64
+        u64.copy_(self._u_pinned, non_blocking=True)
         if self.kind == "int":
             bad = torch.zeros(1, dtype=torch.int32, device=self.device)
             _lib.check(_lib.lib().dope_unary_i32(u64.data_ptr(), u64.numel(), self.u.data_ptr(), bad.data_ptr(),
@@ -485,12 +493,13 @@ class AdmmState:
         return st
 
     def _detach(self):
-        """Copy a lattice run's fields off the device buffers (they are about to
-        be reused by the next run of the same problems)."""
+        """Snapshot a lattice run's fields before its device buffers are reused by
+        the next run of the same problems: device-to-device copies of the
+        compressed state (2y bytes, labels, multipliers), still materialised
+        lazily."""
         if self._src is not None and self._src[0] == "lattice":
             dev = self._src[1]
-            self._src = ("lattice_host", (dev.y2_current().double().div_(2.0).cpu().numpy(),
-                                          dev.yhat.cpu().numpy(), dev.multipliers().double().cpu().numpy()))
+            self._src = ("lattice_copy", (dev.y2_current().clone(), dev.yhat.clone(), dev.multipliers().clone()))
 
     @classmethod
     def from_device(cls, partition: Partition, y, yhat_cat, a_cat, layout, mu: float) -> "AdmmState":
@@ -505,12 +514,14 @@ class AdmmState:
 
     def _fetch(self, what: str):
         kind, src = self._src
-        if kind == "lattice_host":
-            y, yhat, a = src
+        if kind == "lattice_copy":
+            y2, yhat, a = src
             if what == "y":
-                return y
+                return y2.double().div_(2.0).cpu().numpy()
             lay = self._entries()
-            return lay.split((yhat.astype(np.int8) if what == "block_labels" else a)[lay.ent_pix])
+            if what == "block_labels":
+                return lay.split(yhat.cpu().numpy()[lay.ent_pix].astype(np.int8))
+            return lay.split(a.double().cpu().numpy()[lay.ent_pix])
         if kind == "lattice":
             dev = src
             if what == "y":
@@ -569,15 +580,15 @@ class AdmmState:
         """Current block labels (yhat) scattered to global layout."""
         if self._block_labels is None and self._src is not None and self._src[0] == "lattice":
             return self._src[1].yhat.cpu().numpy().astype(np.int8)
-        if self._block_labels is None and self._src is not None and self._src[0] == "lattice_host":
-            return self._src[1][1].astype(np.int8)
+        if self._block_labels is None and self._src is not None and self._src[0] == "lattice_copy":
+            return self._src[1][1].cpu().numpy().astype(np.int8)
         return self._to_global(self.block_labels, np.int8)
 
     def multipliers_global(self) -> np.ndarray:
         if self._multipliers is None and self._src is not None and self._src[0] == "lattice":
             return self._src[1].multipliers().double().cpu().numpy()
-        if self._multipliers is None and self._src is not None and self._src[0] == "lattice_host":
-            return self._src[1][2]
+        if self._multipliers is None and self._src is not None and self._src[0] == "lattice_copy":
+            return self._src[1][2].double().cpu().numpy()
         return self._to_global(self.multipliers, np.float64)
 
 
