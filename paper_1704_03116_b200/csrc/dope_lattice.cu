@@ -183,10 +183,13 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         griddep_wait();     // the previous consensus pass (PDL launch)
         griddep_launch();   // all K1 CTAs are resident: the consensus pass may launch
     }
+    int ycur;
     {
-        // both flags in one round trip: a clean CTA must leave its slot fast
-        // (4096 CTAs churn through ~5 slots per SM)
+        // the flags and the current buffer in one round trip: a clean CTA must
+        // leave its slot fast (4096 CTAs churn through ~5 slots per SM), a
+        // dirty one needs ycur before its first data load
         const int stop = L.st->stop;
+        ycur = L.st->ycur;
         const uint32_t dk = L.skip_clean ? L.dirty[k] : 1u;
         if (stop || dk == 0) return;
     }
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
     const int32_t Wg = L.W;
     const int32_t cap = L.cap;
     const astore_t *__restrict__ a_cur = L.a;
-    const ystore_t *__restrict__ y_cur = L.y2[L.st->ycur];
+    const ystore_t *__restrict__ y_cur = L.y2[ycur];
     // stored residual graph: E and S planes only (the W / N residual of an
     // arc pair is 2*cap minus the forward one: r(v->w) + r(w->v) = 2*cap)
     uint8_t *gres = L.resid + (size_t)k * 2 * M;
@@ -491,7 +494,7 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
             }
         }
     }
-    if (L.warm) {   // E and S planes back
+    if (L.warm && sweeps_done > 0) {   // E and S planes back (unchanged when nothing was pushed)
         uint4 *dst = reinterpret_cast<uint4 *>(gres);
         for (int i = tid; i < M * 2 / 16; i += NT) {
             const int so = (i < M / 16) ? 16 * i : 2 * M + 16 * (i - M / 16);

@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
         const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + warp) * W + gb.lo_c + lane;
         L.yhat[G] = (uint8_t)((Rb[z * B + warp] >> lane) & 1u);
     }
-    if (L.warm) {   // E/S/D nibble planes back (48 KB, 16-byte stores)
+    if (L.warm && sweeps_done > 0) {   // E/S/D nibble planes back (48 KB; unchanged without a sweep)
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
             const int w = (j * NT + tid) * 4;
