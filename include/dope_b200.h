@@ -316,11 +316,15 @@ typedef struct dope_lattice_f {
                                    stored at i (SE/SW only when conn == 8)     */
     const double *rdiag;        /* n: r = d - dhat (blockform.py:242-243)      */
     const int32_t *capq[4];     /* rint(lam * w * qscale), same layout          */
-    double *a[2];               /* n, ping-pong                                */
+    double *a[2];               /* n; a[0] updated in place (a[1] unused by the
+                                   run loop, kept for the ABI)                 */
     double *y[3];               /* n, rotating iterates                        */
     uint8_t *yhat;              /* n                                           */
     int32_t *resid;             /* K * dope_f_resid_stride bytes               */
-    uint32_t *dirty;            /* K                                           */
+    uint32_t *dirty;            /* 6K: [0, K) re-solve flags, [K, 2K) solve
+                                   epochs, [2K, 5K) y-buffer stamps, [5K, 6K)
+                                   last change of each block's iterate (the
+                                   clean-block consensus pass)                 */
     double *part_energy;        /* K                                           */
     double *part_ressq;         /* K                                           */
     int32_t *part_flags;        /* K                                           */

@@ -225,7 +225,10 @@ class _FloatDeviceState:
         self.y2 = [torch.full((n,), 0.5, dtype=f64, device=dev) for _ in range(3)]
         self.yhat = torch.zeros(n, dtype=torch.uint8, device=dev)
         self.resid = torch.zeros(K * stride // 4, dtype=torch.int32, device=dev)
-        self.dirty = torch.ones(K, dtype=torch.int32, device=dev)
+        # [0, K) re-solve flags, [K, 2K) solve epochs, [2K, 5K) y-buffer stamps,
+        # [5K, 6K) last change of each block's iterate (clean-block pass)
+        self.dirty = torch.zeros(6 * K, dtype=torch.int32, device=dev)
+        self.dirty[:K] = 1
         self.pe = torch.zeros(K, dtype=f64, device=dev)
         self.pr = torch.zeros(K, dtype=f64, device=dev)
         self.pf = torch.zeros(K, dtype=torch.int32, device=dev)

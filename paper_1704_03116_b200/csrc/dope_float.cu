@@ -101,7 +101,10 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
     if (L.st->stop) return;
     if (L.skip_clean && L.dirty[k] == 0) return;
     __syncthreads();
-    if (tid == 0) L.dirty[k] = 0;
+    if (tid == 0) {
+        L.dirty[k] = 0;
+        L.dirty[L.K + k] = (uint32_t)L.st->iteration + 1u;   // solve epoch (K2f's clean-block pass)
+    }
     const int by = k / L.ax.k, bx = k - by * L.ax.k;
     int32_t lo_r, hr, lo_c, wc;
     L.ay.range(by, lo_r, hr);
@@ -233,6 +236,11 @@ __global__ void k_init_state_f(LatF L, int64_t n) {
     }
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.K; i += stride) {
         L.dirty[i] = 1u;
+        L.dirty[L.K + i] = 0u;                 // solve epochs
+        L.dirty[2 * L.K + i] = 0u;             // y buffer 0 holds the initial iterate ...
+        L.dirty[3 * L.K + i] = 0xFFFFFFFFu;    // ... buffers 1, 2 nothing yet
+        L.dirty[4 * L.K + i] = 0xFFFFFFFFu;
+        L.dirty[5 * L.K + i] = 0u;             // pass of the last change of the block's iterate
         L.pe[i] = 0.0;
         L.pr[i] = 0.0;
         L.pf[i] = 0;
@@ -274,7 +282,6 @@ __device__ void apply_f(const LatF &L, double E2, double R2, double M2, int F2, 
         L.tr_mr[t] = maxres;
         L.tr_cl[t] = F2;
     }
-    st->parity ^= 1;
     st->iteration = t + 1;
     if (L.K == 0 || maxres <= L.eps) {
         st->converged = 1;
@@ -292,7 +299,53 @@ __device__ void apply_f(const LatF &L, double E2, double R2, double M2, int F2, 
 #endif
 constexpr int K2F_NT = K2F_THREADS;
 
-__global__ void __launch_bounds__(K2F_NT) k_consensus_f(LatF L) {
+// The last consensus CTA of a pass: fold every block's partials (fixed order)
+// and apply the iteration (admm.py:226-249), or -- step-level API -- rotate.
+__device__ __forceinline__ void k2f_finalize(const LatF &L, int cur, int best, int out) {
+    constexpr int NWARP = K2F_NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __threadfence();
+    __shared__ double sE[NWARP], sR[NWARP], sM[NWARP];
+    __shared__ int sF[NWARP];
+    if (!L.fuse) {
+        if (tid == 0) {
+            L.st->ybest = best;
+            L.st->ycur = out;
+            L.st->done_ctas = 0;
+        }
+        return;
+    }
+    double E = 0.0, R2 = 0.0, M2 = -1.0;
+    int F = 0;
+    for (int b = tid; b < L.K; b += blockDim.x) {
+        E += __ldcg(&L.pe[b]);
+        const double sq = __ldcg(&L.pr[b]);
+        const double rr = sqrt(sq);
+        R2 += rr * rr;
+        M2 = sq > M2 ? sq : M2;
+        F |= __ldcg(&L.pf[b]) & 1;
+    }
+    E = warp_sum(E);
+    R2 = warp_sum(R2);
+    for (int o = 16; o > 0; o >>= 1) {
+        const double t = __shfl_xor_sync(FULLMASK, M2, o);
+        M2 = t > M2 ? t : M2;
+    }
+    F = __any_sync(FULLMASK, F);
+    if (lane == 0) { sE[warp] = E; sR[warp] = R2; sM[warp] = M2; sF[warp] = F; }
+    __syncthreads();
+    if (tid == 0) {
+        double E2 = 0.0, RR = 0.0, MM = -1.0;
+        int FF = 0;
+        for (int w = 0; w < NWARP; ++w) {
+            E2 += sE[w]; RR += sR[w]; MM = sM[w] > MM ? sM[w] : MM; FF |= sF[w];
+        }
+        apply_f(L, E2, RR, MM, FF, cur, best, out);
+        L.st->done_ctas = 0;
+    }
+}
+
+__global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
     if (L.st->stop) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int k = blockIdx.x;
@@ -305,12 +358,67 @@ __global__ void __launch_bounds__(K2F_NT) k_consensus_f(LatF L) {
     const double *__restrict__ y_in = L.y[cur];
     double *__restrict__ y_out = L.y[out];
     const int p = L.st->parity;
-    const double *__restrict__ a_in = p ? L.a1 : L.a0;
-    double *__restrict__ a_out = L.fuse ? (p ? L.a0 : L.a1) : nullptr;
-    const bool want_e = L.fuse && L.st->iteration >= 1;
+    // multipliers in place: a_{t+1}[g] depends on a_t[g] only
+    const double *a_in = p ? L.a1 : L.a0;
+    double *a_out = L.fuse ? (p ? L.a1 : L.a0) : nullptr;
+    const int iteration = L.st->iteration;
+    const bool want_e = L.fuse && iteration >= 1;
+    const int32_t pass = iteration + 1;    // this pass (= this iteration's K1 solve epoch)
+    int32_t *ybuf = reinterpret_cast<int32_t *>(L.dirty + 2 * L.K);    // [3][K] buffer stamps
+    int32_t *lastchg = reinterpret_cast<int32_t *>(L.dirty + 5 * L.K);
     __shared__ unsigned nbmark;            // bit (dy+1)*3 + (dx+1): neighbour block dirty
-    if (tid == 0) nbmark = 0;
+    // 0 full update; clean block (not re-solved now, unmoved in the last pass):
+    // 1 fixed point, nothing to do; 2 fixed point, copy y into the output
+    // buffer; 3 ring only (a neighbour was re-solved), 4 ring only + copy
+    __shared__ int mode;
+    __shared__ int last;
+    if (tid == 0) {
+        nbmark = 0;
+        // Clean-block fixed point: a block K1 did not re-solve
+        // had y and a unmoved (so y == yhat) in the previous pass, and no
+        // border pixel next to it moved either; if none of its 8 neighbours
+        // was re-solved now, every input of this pass equals the last one's,
+        // so y, a, the residual (0), the clamp flags and the energy partial of
+        // the unmoved iterate are all the previous pass's -- bit for bit.
+        // With a re-solved neighbour only the ring pixels (those with a
+        // cross-block neighbour) see new inputs: the interior (r = 0 there:
+        // y = clamp(yhat + a)) is still a fixed point, its clamp flags are the
+        // memo in part_flags bit 1.
+        int m = 0;
+        if (L.skip_clean && L.fuse && iteration >= 2 && L.dirty[L.K + k] != (uint32_t)pass) {
+            bool nb = false;
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int nby = by + dy, nbx = bx + dx;
+                    if ((dy || dx) && nby >= 0 && nby < L.ay.k && nbx >= 0 && nbx < L.ax.k &&
+                        L.dirty[L.K + nby * L.ax.k + nbx] == (uint32_t)pass)
+                        nb = true;
+                }
+            const bool stale = ybuf[out * L.K + k] < lastchg[k];
+            m = nb ? (stale ? 4 : 3) : (stale ? 2 : 1);
+        }
+        mode = m;
+    }
     __syncthreads();
+    if (mode == 2 || mode == 4) {   // the output buffer holds an older iterate of this block: copy
+        for (int v = tid; v < hr * wc; v += K2F_NT) {
+            const int r = v / wc, c = v - r * wc;
+            const int64_t G = (int64_t)(lo_r + r) * W + lo_c + c;
+            y_out[G] = y_in[G];   // ring pixels are rewritten below in mode 4
+        }
+        if (mode == 4) __syncthreads();
+    }
+    if (mode == 1 || mode == 2) {
+        __syncthreads();
+        if (tid == 0) {
+            if (mode == 2) ybuf[out * L.K + k] = pass;
+            __threadfence();
+            last = (atomicAdd(&L.st->done_ctas, 1) == L.K - 1);
+        }
+        __syncthreads();
+        if (last) k2f_finalize(L, cur, best, out);
+        return;
+    }
 
     // read-only planes through restrict-qualified pointers: the loads of
     // the next pixels may be issued ahead of this pixel's stores
@@ -385,7 +493,7 @@ __global__ void __launch_bounds__(K2F_NT) k_consensus_f(LatF L) {
         y_out[G] = y;
         const double dlt = yh - y;
         ss += dlt * dlt;
-        if (want_e) {
+        if (want_e && mode == 0) {
             double q = 0.0;
             // pairs owned by this pixel: E S SE SW (forward planes)
             if (Cc + 1 < W) { const double d = yold - y_in[G + 1]; q += w0[G] * (d * d); }
@@ -401,6 +509,7 @@ __global__ void __launch_bounds__(K2F_NT) k_consensus_f(LatF L) {
         }
         const bool ychg = (y != yold);
         if (ychg || (av + (yh - y)) != av) marks |= 1u;
+        if (ychg) marks |= 1u << 10;
         if (ychg && border) {
             for (int d = 0; d < L.ndir; ++d) {
                 const int rn = R + dy_of(d), cn = Cc + dx_of(d);
@@ -411,14 +520,15 @@ __global__ void __launch_bounds__(K2F_NT) k_consensus_f(LatF L) {
             }
         }
     };
-    // interior pixels
+    // interior pixels (a fixed point in the ring-only modes)
     const int iw = wc - 2, ih = hr - 2;
-    const int mi = (iw > 0 && ih > 0) ? iw * ih : 0;
+    const int mi = (iw > 0 && ih > 0 && mode == 0) ? iw * ih : 0;
 #pragma unroll 4
     for (int v = tid; v < mi; v += K2F_NT) {
         const int r = v / iw, c = v - r * iw;
         pixel(r + 1, c + 1, false);
     }
+    const int clamped_int = clamped;
     // the ring of border pixels: top row, bottom row, then left / right columns
     const int nring = (hr <= 2 || wc <= 2) ? hr * wc : 2 * wc + 2 * (hr - 2);
     for (int t = tid; t < nring; t += K2F_NT) {
@@ -432,11 +542,10 @@ __global__ void __launch_bounds__(K2F_NT) k_consensus_f(LatF L) {
     constexpr int NWARP = K2F_NT / 32;
     __shared__ double red_e[NWARP], red_s[NWARP];
     __shared__ int red_f[NWARP];
-    __shared__ int last;
     e_acc = warp_sum(e_acc);
     ss = warp_sum(ss);
     for (int o = 16; o > 0; o >>= 1) marks |= __shfl_xor_sync(FULLMASK, marks, o);
-    const int fl = __any_sync(FULLMASK, clamped);
+    const int fl = (__any_sync(FULLMASK, clamped) ? 1 : 0) | (__any_sync(FULLMASK, clamped_int) ? 2 : 0);
     if (lane == 0) {
         red_e[warp] = e_acc;
         red_s[warp] = ss;
@@ -448,11 +557,18 @@ __global__ void __launch_bounds__(K2F_NT) k_consensus_f(LatF L) {
         double E = 0.0, S = 0.0;
         int F = 0;
         for (int w = 0; w < NWARP; ++w) { E += red_e[w]; S += red_s[w]; F |= red_f[w]; }
-        L.pe[k] = E;
+        if (mode == 0) {
+            L.pe[k] = E;
+            L.pf[k] = F;   // bit 0 any pixel clamped, bit 1 an interior pixel clamped
+        } else {           // ring only: the energy partial and the interior clamp memo hold
+            const int memo = L.pf[k] & 2;
+            L.pf[k] = memo | ((F & 1) | (memo >> 1));
+        }
         L.pr[k] = S;
-        L.pf[k] = F;
         const unsigned mk = nbmark;
         if (mk & 1u) L.dirty[k] = 1u;
+        ybuf[out * L.K + k] = pass;             // the output buffer holds the new iterate
+        if (mk & (1u << 10)) lastchg[k] = pass;
         for (int dy = -1; dy <= 1; ++dy)
             for (int dx = -1; dx <= 1; ++dx)
                 if ((dy || dx) && (mk & (1u << (1 + (dy + 1) * 3 + (dx + 1)))))
@@ -461,47 +577,7 @@ __global__ void __launch_bounds__(K2F_NT) k_consensus_f(LatF L) {
         last = (atomicAdd(&L.st->done_ctas, 1) == L.K - 1);
     }
     __syncthreads();
-    if (last) {
-        __threadfence();
-        __shared__ double sE[NWARP], sR[NWARP], sM[NWARP];
-        __shared__ int sF[NWARP];
-        if (!L.fuse) {
-            if (tid == 0) {
-                L.st->ybest = best;
-                L.st->ycur = out;
-                L.st->done_ctas = 0;
-            }
-            return;
-        }
-        double E = 0.0, R2 = 0.0, M2 = -1.0;
-        int F = 0;
-        for (int b = tid; b < L.K; b += blockDim.x) {
-            E += __ldcg(&L.pe[b]);
-            const double sq = __ldcg(&L.pr[b]);
-            const double rr = sqrt(sq);
-            R2 += rr * rr;
-            M2 = sq > M2 ? sq : M2;
-            F |= __ldcg(&L.pf[b]);
-        }
-        E = warp_sum(E);
-        R2 = warp_sum(R2);
-        for (int o = 16; o > 0; o >>= 1) {
-            const double t = __shfl_xor_sync(FULLMASK, M2, o);
-            M2 = t > M2 ? t : M2;
-        }
-        F = __any_sync(FULLMASK, F);
-        if (lane == 0) { sE[warp] = E; sR[warp] = R2; sM[warp] = M2; sF[warp] = F; }
-        __syncthreads();
-        if (tid == 0) {
-            double E2 = 0.0, RR = 0.0, MM = -1.0;
-            int FF = 0;
-            for (int w = 0; w < NWARP; ++w) {
-                E2 += sE[w]; RR += sR[w]; MM = sM[w] > MM ? sM[w] : MM; FF |= sF[w];
-            }
-            apply_f(L, E2, RR, MM, FF, cur, best, out);
-            L.st->done_ctas = 0;
-        }
-    }
+    if (last) k2f_finalize(L, cur, best, out);
 }
 
 __global__ void k_update_multipliers_f(LatF L, int64_t n) {
