@@ -11,18 +11,18 @@
  *
  *   Seam 2 (batched, one CTA per sub-region) replaces the per-iteration step
  *   functions of admm.py:
- *     update_blocks      admm.py:171-191  (+ blockform.block_objective
- *                        blockform.py:257-273, maxflow.solve_binary
- *                        maxflow.py:423-425)            -> dope_update_blocks()
- *     update_global      admm.py:230-238  (solve_global admm.py:194-209)
- *     update_multipliers admm.py:241-248
- *     block_residuals    admm.py:251-257
+ *     update_blocks      admm.py:113-133  (+ blockform.block_objective
+ *                        blockform.py:89-105, maxflow.solve_binary
+ *                        maxflow.py:111-113)            -> dope_update_blocks()
+ *     update_global      admm.py:172-180  (solve_global admm.py:136-151)
+ *     update_multipliers admm.py:183-190
+ *     block_residuals    admm.py:193-199
  *     evaluate_energy    energy.py:187-194              -> dope_update_global()
- *     run bookkeeping    admm.py:283-310 (trace, best, stop) -> last CTA of
+ *     run bookkeeping    admm.py:225-252 (trace, best, stop) -> last CTA of
  *                                                          dope_update_global
- *     run                admm.py:265-310                -> dope_admm_run(),
+ *     run                admm.py:207-252                -> dope_admm_run(),
  *                                                          dope_finish_run()
- *     binarize           admm.py:260-262                -> dope_binarize()
+ *     binarize           admm.py:202-204                -> dope_binarize()
  *
  * Conventions
  *   - Plain pointers and sizes; no framework types.  Device pointers are
@@ -32,7 +32,7 @@
  *   - Return codes: 0 ok; < 0 invalid arguments / unsupported geometry
  *     (see DOPE_E_*); > 0 never returned by launch calls -- solver failures
  *     are reported on the device in dope_run_state.error as 1 + block id
- *     (the reference's BlockSolveError(block_id), admm.py:85-90).
+ *     (the reference's BlockSolveError(block_id), admm.py:27-32).
  *   - Integer lattice path: grid coordinates row-major (GridShape.strides,
  *     grid.py:46-52), block ids row-major over the block lattice
  *     (partition.py:103), non-overlapping near-equal box tiling
@@ -62,8 +62,8 @@ extern "C" {
 typedef struct dope_run_state {
     int64_t best_energy;        /* energy of the best iterate so far           */
     int32_t iteration;          /* iterations completed                        */
-    int32_t best_iteration;     /* admm.py:300-303 (strict <)                  */
-    int32_t converged;          /* admm.py:305-307                             */
+    int32_t best_iteration;     /* admm.py:242-245 (strict <)                  */
+    int32_t converged;          /* admm.py:247-249                             */
     int32_t stop;               /* converged, error or finished: later
                                    iteration launches are no-ops               */
     int32_t ycur;               /* y buffer (0..2) holding the current iterate */
@@ -190,7 +190,7 @@ int dope_lattice_check(const dope_lattice *L);
 /* Set kernel attributes ahead of CUDA-graph capture (called internally). */
 int dope_prepare_kernels(const dope_lattice *L);
 
-/* init_state (admm.py:160-168): y = 1/2, a = 0, yhat = 0, every block dirty,
+/* init_state (admm.py:102-110): y = 1/2, a = 0, yhat = 0, every block dirty,
  * cold residual graphs, run state reset. */
 int dope_admm_init(const dope_lattice *L, void *stream);
 /* update_blocks: one CTA per sub-region computes 2*linear from (u, a, y,
@@ -208,7 +208,7 @@ int dope_update_multipliers(const dope_lattice *L, void *stream);
  * become no-ops once converged.  use_graph: capture one iteration in a CUDA
  * graph and replay it. */
 int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void *stream);
-/* End of run (admm.py:300-310): energy + best check of the last iterate;
+/* End of run (admm.py:242-252): energy + best check of the last iterate;
  * the current iterate becomes the best one unless converged. */
 int dope_finish_run(const dope_lattice *L, void *stream);
 /* Sharded run loop: reduce the gathered agg[] table in shard order and apply
@@ -220,6 +220,9 @@ int dope_decide(const dope_lattice *L, void *stream);
  * blocks dirty where the ghost iterate moved.  Blocks must be >= 2 rows /
  * planes deep along the sharded axis (else DOPE_E_GEOMETRY). */
 int dope_ghost_consensus(const dope_lattice *L, void *stream);
+/* dope_ghost_consensus and dope_decide in one launch (the last CTA decides
+ * once every ghost pixel is in): the run loop's step after the agg gather. */
+int dope_ghost_decide(const dope_lattice *L, void *stream);
 /* Bytes of the sharded halo buffer (L->halo) for this geometry. */
 int64_t dope_halo_bytes(const dope_lattice *L);
 /* Audit mode: add this iteration's state digest into L->trace_hash (no-op
@@ -243,8 +246,9 @@ int dope_energy_local(const dope_lattice *L, void *stream);
 int dope_finish_decide(const dope_lattice *L, void *stream);
 /* Multi-GPU (NCCL over NVLink / NVSwitch), one rank per GPU, 2D and 3D
  * lattices (slabs of block rows / block planes).  Per iteration: K1, ONE
- * grouped send/recv of the boundary label rows, the consensus pass,
- * dope_ghost_consensus, ONE all-gather of the 64-byte agg slots, dope_decide.
+ * grouped send/recv of the boundary label rows, the consensus pass, ONE
+ * all-gather of the 64-byte agg slots, dope_ghost_decide (at world size 1:
+ * K1, the consensus pass, dope_ghost_decide -- nothing to exchange).
  * dope_comm_unique_id on rank 0, broadcast the 128 bytes, dope_comm_init on
  * every rank.  dope_sharded_run runs `iters` iterations of that loop --
  * captured in one CUDA graph when use_graph; dope_sharded_finish ends the
@@ -314,7 +318,7 @@ typedef struct dope_lattice_f {
     const double *u;            /* n                                           */
     const double *w[4];         /* E S SE SW weight planes: w of pair (i, i+off)
                                    stored at i (SE/SW only when conn == 8)     */
-    const double *rdiag;        /* n: r = d - dhat (blockform.py:242-243)      */
+    const double *rdiag;        /* n: r = d - dhat (blockform.py:75)      */
     const int32_t *capq[4];     /* rint(lam * w * qscale), same layout          */
     double *a[2];               /* n; a[0] updated in place (a[1] unused by the
                                    run loop, kept for the ABI)                 */

@@ -16,23 +16,23 @@
  *     the flow value are bit-identical to the reference on identical inputs.
  *     Labels: 1 iff the node ends in the sink tree (_core.pyx:257-259).
  *
- *  2. The consensus (ADMM) loop of admm.py:265-310 for a lattice stencil
+ *  2. The consensus (ADMM) loop of admm.py:207-252 for a lattice stencil
  *     model on a NON-OVERLAPPING box partition (q == 1 everywhere), where the
- *     coupling operators of blockform.py:216-254 collapse to a one-pixel
+ *     coupling operators of blockform.py:48-86 collapse to a one-pixel
  *     cross-block stencil:
- *       block_objective (blockform.py:257-273):
+ *       block_objective (blockform.py:89-105):
  *         linear_g = u_g + lam*(sum_{j~g, out} -w_gj y_j + r_g y_g)
  *                        + mu*((a_g - y_g) + 0.5),  r_g = sum_{j~g,out} w_gj
- *       solve_global (admm.py:194-209) + clamp (admm.py:230-238):
+ *       solve_global (admm.py:136-151) + clamp (admm.py:172-180):
  *         acc_g = mu*(yh_g + a_g) - lam*(r_g*yh_g);  then per neighbouring
  *         block in id order acc_g -= lam*(sum_i -w_ig yh_i);  y = acc/mu
- *       block_residuals (admm.py:251-257), evaluate_energy (energy.py:187-194),
- *       update_multipliers (admm.py:241-248), best-iterate / stop rule
- *       (admm.py:300-310).
+ *       block_residuals (admm.py:193-199), evaluate_energy (energy.py:187-194),
+ *       update_multipliers (admm.py:183-190), best-iterate / stop rule
+ *       (admm.py:242-252).
  *     Floating-point order follows SURVEY.md Appendix C where it matters.
  *
  * Block solves may run on several host threads (the reference's
- * ThreadPoolExecutor over blocks, admm.py:186-190); results do not depend on
+ * ThreadPoolExecutor over blocks, admm.py:128-132); results do not depend on
  * the thread count.
  */
 #include <math.h>
@@ -413,7 +413,7 @@ static inline int inside_ext(const lattice_ctx *c, int64_t j, const int64_t *ext
     return 1;
 }
 
-/* r_diag = d/q^2 - dhat with q == 1 (blockform.py:226, 242-243): d is the row
+/* r_diag = d/q^2 - dhat with q == 1 (blockform.py:58, 75): d is the row
  * sum of the symmetric weight matrix built from (rows,cols)+(cols,rows)
  * (energy.py:71-76), i.e. forward partners in direction order then backward
  * partners in direction order; dhat accumulates the in-block pairs with
@@ -524,10 +524,10 @@ static void scratch_free(block_scratch *s) {
     bk_ws_free(&s->ws);
 }
 
-/* Solve one block: block_objective (blockform.py:257-273) + solve_binary
- * (maxflow.py:385-425).  Pairs are listed in CSR order of the block-local
+/* Solve one block: block_objective (blockform.py:89-105) + solve_binary
+ * (maxflow.py:73-113).  Pairs are listed in CSR order of the block-local
  * weight matrix (row ascending, then column ascending), as the reference's
- * w_scaled[p][:, p].tocoo() row<col selection yields (blockform.py:238-241). */
+ * w_scaled[p][:, p].tocoo() row<col selection yields (blockform.py:64-67). */
 static int solve_one_block(const lattice_ctx *c, int64_t k, const double *y, const double *a,
                            double mu, uint8_t *yhat, block_scratch *s) {
     const oracle_lattice *L = c->L;
@@ -546,7 +546,7 @@ static int solve_one_block(const lattice_ctx *c, int64_t k, const double *y, con
         coords_of(c, g, x);
         /* linear term */
         double cy = 0.0, r = 0.0;
-        /* c_rows @ y: CSR row sum over global columns ascending (blockform.py:271).
+        /* c_rows @ y: CSR row sum over global columns ascending (blockform.py:103).
          * Cross-block neighbours: backward partners have lower index than
          * forward ones; within each group directions are visited so that
          * indices ascend. */
@@ -601,7 +601,7 @@ static int solve_one_block(const lattice_ctx *c, int64_t k, const double *y, con
         }
         for (int p2 = 0; p2 < nc; p2++) {
             if (cw[p2] == 0.0) continue;    /* structural zeros are not stored */
-            if (cw[p2] < 0.0) return -3;     /* NonSubmodularError (maxflow.py:398-401) */
+            if (cw[p2] < 0.0) return -3;     /* NonSubmodularError (maxflow.py:86-89) */
             s->pi[np] = (int32_t)i;
             s->pj[np] = (int32_t)cand[p2];
             s->cij[np] = L->lam * cw[p2];
@@ -658,7 +658,7 @@ static int update_blocks(const lattice_ctx *c, const double *y, const double *a,
 
 /* --------------------------- global update -------------------------------- */
 
-/* solve_global (admm.py:194-209) + clamp (admm.py:230-238), q == 1. */
+/* solve_global (admm.py:136-151) + clamp (admm.py:172-180), q == 1. */
 static int update_global(const lattice_ctx *c, const uint8_t *yhat, const double *a, double mu,
                          double *y, int *clamped) {
     const oracle_lattice *L = c->L;
@@ -851,7 +851,7 @@ int oracle_state_digest(int64_t n, const uint8_t *yhat, const double *y, const d
     return 0;
 }
 
-/* run (admm.py:265-310) with the trace of admm.py:291-299.
+/* run (admm.py:207-252) with the trace of admm.py:233-241.
  * trace_* arrays have max_iters entries; yhat_hist (optional) max_iters*n;
  * digests (optional) 3*max_iters words of state_digest per iteration.
  * y (in: ignored, out: state.y after run, i.e. best iterate when not

@@ -7,7 +7,7 @@ this module, and only as the checker.  The product package
 Functions restate the reference hot path (see dope_oracle.c for file:line
 citations):
   bk_maxflow      -- _core.bk_maxflow contract (_core.pyx:263-333)
-  run             -- admm.run (admm.py:265-310) on a q == 1 lattice partition
+  run             -- admm.run (admm.py:207-252) on a q == 1 lattice partition
   update_blocks / update_global / block_residuals / energy -- step functions
   reference_core() -- the reference's own compiled _core (oracle/_ref), if built
 """

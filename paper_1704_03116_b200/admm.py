@@ -32,7 +32,7 @@ from .solvers import EXHAUSTIVE, ICM, MAXFLOW, BlockSolverKind  # noqa: F401  (r
 
 
 class BlockSolveError(RuntimeError):
-    """A block solver failed; carries the block id (admm.py:85-90)."""
+    """A block solver failed; carries the block id (admm.py:27-32)."""
 
     def __init__(self, block_id: int, cause):
         super().__init__(f"solver failed on block {block_id}: {cause}")
@@ -48,7 +48,7 @@ def _device():
 
 @dataclass
 class AdmmConfig:
-    """Loop parameters (admm.py:93-129) plus B200 execution options."""
+    """Loop parameters (admm.py:35-71) plus B200 execution options."""
 
     mu0: float | None = None
     mu_fact: float = 1.05

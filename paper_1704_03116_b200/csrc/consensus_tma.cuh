@@ -2,8 +2,8 @@
 // uniform tilings with 64- or 128-wide blocks.  Included by dope_lattice.cu
 // inside namespace dope (uses Lat2, CtaAgg, pass_tail, other_buffer).
 //
-// Same arithmetic as k_consensus_vec (solve_global + clamp admm.py:194-238,
-// update_multipliers admm.py:241-248, block residuals admm.py:251-257, energy
+// Same arithmetic as k_consensus_vec (solve_global + clamp admm.py:136-180,
+// update_multipliers admm.py:183-190, block residuals admm.py:193-199, energy
 // of the previous iterate energy.py:187-194), organised for HBM:
 //   * persistent grid (a few CTAs per SM); each CTA walks its blocks as tiles
 //     of TH x TW pixels (64x64, or 32 rows of a 128-wide block);
@@ -206,7 +206,7 @@ __device__ __forceinline__ uint32_t bytes_b01(uint32_t b) { return (b * 0x002040
 //   cnt : per-pixel count of cross-block neighbours (bytes)
 //   nb  : per-pixel sum of their labels (bytes)
 // y = clamp(h + a - q * sx) with sx = cnt*h - nb (the solve_global stencil,
-// admm.py:194-238); sx enters biased by 4 so the bytewise subtraction never
+// admm.py:136-180); sx enters biased by 4 so the bytewise subtraction never
 // borrows.  Returns the new y as bits; writes the new multipliers.
 __device__ __forceinline__ uint32_t quad_update(uint32_t h4, uint2 a2, uint32_t cnt, uint32_t nb, int q,
                                                 int q4, uint2 &an, uint32_t &clp) {

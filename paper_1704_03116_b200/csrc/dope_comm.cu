@@ -12,12 +12,12 @@
 //      and into the ghost rows (dope_ghost_update);
 //   3. the consensus pass (dope_update_global), which writes this shard's
 //      64-byte slot of the agg table (exact integers);
-//   4. dope_ghost_consensus: the ghost rows' new iterate and multipliers,
-//      recomputed locally from the labels of step 2 (no y halo);
-//   5. one all-gather of the agg slots (loopback: one copy per peer table);
-//   6. dope_decide: the table reduced in shard order -- the same trace entry,
-//      best iterate and stop decision on every shard, bit-identical to the
-//      single-GPU run.
+//   4. one all-gather of the agg slots (loopback: one copy per peer table);
+//   5. dope_ghost_decide: the ghost rows' new iterate and multipliers,
+//      recomputed locally from the labels of step 2 (no y halo), then the
+//      table reduced in shard order -- the same trace entry, best iterate
+//      and stop decision on every shard, bit-identical to the single-GPU run.
+// At world size 1 steps 2 and 4 vanish.
 //
 // The whole iteration, NCCL calls included, is captured into one CUDA graph.
 // NCCL is loaded at run time (dlopen of libnccl.so.2: the copy PyTorch has
@@ -185,26 +185,29 @@ struct LoopbackTransport : Transport {
 
 static int one_iteration(const dope_lattice *const *S, int nloc, Transport &T, cudaStream_t s) {
     int rc;
+    const bool exchange = T.world > 1;   // world size 1: no halo, no gather
     for (int r = 0; r < nloc; ++r)
         if ((rc = dope_update_blocks(S[r], s))) return rc;
-    for (int r = 0; r < nloc; ++r) {
-        const Halo h(S[r]);
-        if ((rc = dope_pack_rows(S[r], 0, h.first, h.last, s))) return rc;
-    }
-    if ((rc = T.move_rows(S, nloc, s))) return rc;
-    for (int r = 0; r < nloc; ++r) {
-        const Halo h(S[r]);
-        if ((rc = dope_ghost_update(S[r], 0, S[r]->ghost_up ? h.up : nullptr, S[r]->ghost_dn ? h.dn : nullptr,
-                                    s)))
-            return rc;
+    if (exchange) {
+        for (int r = 0; r < nloc; ++r) {
+            const Halo h(S[r]);
+            if ((rc = dope_pack_rows(S[r], 0, S[r]->ghost_up ? h.first : nullptr, S[r]->ghost_dn ? h.last : nullptr,
+                                     s)))
+                return rc;
+        }
+        if ((rc = T.move_rows(S, nloc, s))) return rc;
+        for (int r = 0; r < nloc; ++r) {
+            const Halo h(S[r]);
+            if ((rc = dope_ghost_update(S[r], 0, S[r]->ghost_up ? h.up : nullptr, S[r]->ghost_dn ? h.dn : nullptr,
+                                        s)))
+                return rc;
+        }
     }
     for (int r = 0; r < nloc; ++r)
         if ((rc = dope_update_global(S[r], s))) return rc;
-    for (int r = 0; r < nloc; ++r)
-        if ((rc = dope_ghost_consensus(S[r], s))) return rc;
-    if ((rc = T.gather_agg(S, nloc, s))) return rc;
-    for (int r = 0; r < nloc; ++r)
-        if ((rc = dope_decide(S[r], s))) return rc;
+    if (exchange && (rc = T.gather_agg(S, nloc, s))) return rc;
+    for (int r = 0; r < nloc; ++r)   // ghost rows' iterate + the decision, one launch
+        if ((rc = dope_ghost_decide(S[r], s))) return rc;
     for (int r = 0; r < nloc; ++r)
         if ((rc = dope_trace_digest(S[r], s))) return rc;
     return DOPE_OK;

@@ -3,15 +3,15 @@
 //
 // Exactness strategy:
 //   * the block objective is evaluated in float64 in the reference's
-//     operation order (blockform.py:271-272; cross terms in ascending global
-//     index, r = d - dhat precomputed on the host as blockform.py:242-243 does);
+//     operation order (blockform.py:103-104; cross terms in ascending global
+//     index, r = d - dhat precomputed on the host as blockform.py:75 does);
 //   * capacities are quantised once to int32 at scale S (default 2^16):
 //     terminal rint(linear*S), pair rint(lam*w*S) -- the block min cut is then
 //     solved EXACTLY (integer push-relabel, labels = sink-reachable set) for
 //     the quantised energy; the survey's probe found identical traces to the
 //     reference at S >= 2^16 on a C2-like instance;
 //   * the consensus update replays solve_global's float64 accumulation order
-//     (admm.py:203-209: own-block term and per-neighbour-block coupling sums in
+//     (admm.py:145-151: own-block term and per-neighbour-block coupling sums in
 //     block-id order).
 // Parity bar (BASELINE): final energy within 1e-5 relative, <= 0.01 % labels.
 #include <cuda_runtime.h>
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
     const double *__restrict__ y_cur = L.y[L.st->ycur];
     int32_t *gres = L.resid + (size_t)k * NDIR * M;
 
-    // ---- prologue: linear in float64 (blockform.py:271-272), quantised ----
+    // ---- prologue: linear in float64 (blockform.py:103-104), quantised ----
     // Warm start: the kept residual planes stream into shared memory first
     // (all 16-byte loads in flight); the stored flow is then read back from
     // them through the arc-pair invariant r(v->w) + r(w->v) = 2 cap(v,w), so
@@ -229,7 +229,7 @@ __global__ void k_init_resid_f(LatF L, int M, int bw) {
 __global__ void k_init_state_f(LatF L, int64_t n) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        L.y[0][i] = 0.5;             // admm.py:163-164; best_y = copy
+        L.y[0][i] = 0.5;             // admm.py:102-110; best_y = copy
         L.a0[i] = 0.0;
         L.a1[i] = 0.0;
         L.yhat[i] = 0;
@@ -259,9 +259,9 @@ __device__ __forceinline__ int other_buffer_f(int cur, int best) {
 }
 
 // ---------------------------------------------------------------------------
-// K2f: consensus (solve_global admm.py:194-209 float order, clamp, multipliers,
+// K2f: consensus (solve_global admm.py:136-151 float order, clamp, multipliers,
 // residual and energy partials, dirty marks), one CTA per block; the last CTA
-// finalizes the iteration (admm.py:289-307).
+// finalizes the iteration (admm.py:231-249).
 // ---------------------------------------------------------------------------
 __device__ void apply_f(const LatF &L, double E2, double R2, double M2, int F2, int cur, int best,
                         int out) {
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
     double e_acc = 0.0, ss = 0.0;
     int clamped = 0;
     unsigned marks = 0;
-    // One pixel of solve_global (admm.py:203-209) + clamp, multipliers,
+    // One pixel of solve_global (admm.py:145-151) + clamp, multipliers,
     // residual, energy of the previous iterate and dirty marks.  Block-border
     // pixels sum their cross-block terms in block-id order; they are handled
     // by a second pass so that no warp of the interior pass diverges into it.

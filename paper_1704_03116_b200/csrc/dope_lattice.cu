@@ -2,7 +2,7 @@
 // integer lattice models, behind the C ABI of include/dope_b200.h.
 //
 //   K1 k_block_mincut   one CTA per sub-region.  Prologue computes the block
-//                       objective (blockform.py:257-273 collapsed to the q==1
+//                       objective (blockform.py:89-105 collapsed to the q==1
 //                       stencil) straight from u, a, y and the y-halo; the
 //                       block's residual graph lives in shared memory; exact
 //                       integer push-relabel with a warp-level bit-parallel
@@ -12,13 +12,13 @@
 //                       _core.pyx:257-259; see DESIGN.md for the proof that
 //                       this set is unique, hence bit-exact).
 //   K2 k_consensus      one CTA per sub-region: solve_global + clamp
-//                       (admm.py:194-238), update_multipliers (admm.py:241-248),
-//                       block residual partials (admm.py:251-257), energy
+//                       (admm.py:136-180), update_multipliers (admm.py:183-190),
+//                       block residual partials (admm.py:193-199), energy
 //                       partials (energy.py:187-194), next-iteration dirty
 //                       blocks, best-iterate copy.
 //   K3 k_finalize       one CTA: deterministic reduction of the partials, trace
 //                       record, best iterate (strict <), stop rule
-//                       (admm.py:283-307).
+//                       (admm.py:225-249).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
     // arc pair is 2*cap minus the forward one: r(v->w) + r(w->v) = 2*cap)
     uint8_t *gres = L.resid + (size_t)k * 2 * M;
 
-    // ---- prologue: 2*linear (blockform.py:271-272 on the q==1 stencil) ----
+    // ---- prologue: 2*linear (blockform.py:103-104 on the q==1 stencil) ----
     // lin2 = 2u + lamw * sum_cross (y2_g - y2_j) + mu*(2a - y2_g) + mu
     if (L.warm) {
         // E and S residual planes (block-major, 2*M bytes): asynchronous
@@ -543,7 +543,7 @@ __global__ void k_init_resid(Lat2 L) {
 __global__ void k_init_state(Lat2 L, int64_t n) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        L.y2[0][i] = 1;              // y = 1/2 (admm.py:163-164); best_y = copy
+        L.y2[0][i] = 1;              // y = 1/2 (admm.py:102-110); best_y = copy
         L.a[i] = 0;
         L.yhat[i] = 0;
     }
@@ -650,7 +650,7 @@ __global__ void k_init_unary(Lat2 L, int64_t n) {
 // trace entry.  The unary part u.y is kept incrementally in st.unary2
 // (= sum u*y2): each pass adds u*(y2_t - y2_{t-1}) where y moved, so u is only
 // read where the labeling changed.  The best iterate is tracked by buffer
-// index: no copies (admm.py:300-303).  The last iterate's energy is taken by
+// index: no copies (admm.py:242-245).  The last iterate's energy is taken by
 // dope_finish_run.
 
 __device__ __forceinline__ int other_buffer(int cur, int best) {
@@ -659,7 +659,7 @@ __device__ __forceinline__ int other_buffer(int cur, int best) {
     return 3 - cur - best;
 }
 
-// Apply one iteration's global aggregates to the run state (admm.py:289-307):
+// Apply one iteration's global aggregates to the run state (admm.py:231-249):
 // trace entry, best iterate by buffer index (strict <), parity, stop rule,
 // y-buffer rotation.  E2 is the energy of the previous iterate (y_{t}),
 // R2/M2/F2 the residual sum, max block residual^2 and clamp flag of this one.
@@ -701,7 +701,7 @@ __device__ void apply_iteration(const Lat2 &L, const dope_run_state &s0, int64_t
     st->ycur = out;
 }
 
-// Residual sum of squares, admm.py:295: sum over blocks of fl(fl(sqrt(ss))^2).
+// Residual sum of squares, admm.py:237: sum over blocks of fl(fl(sqrt(ss))^2).
 // Each term is ss + e with e an exact multiple of 2^-53 (|e| <= 4 ulp(ss)), so
 // the sum is kept exactly as two integers (sum ss, sum e * 2^53) and rounded
 // once: deterministic whatever order the blocks are visited in.
@@ -744,9 +744,8 @@ __device__ void finalize_apply(const Lat2 &L, dope_run_state s0, int64_t E2, int
 // Sharded mode: reduce the gathered agg table in shard order -- exact
 // integers throughout, so every shard (and the single-GPU run) reaches the
 // same trace entry, best iterate and stop decision -- and apply it.
-__global__ void k_decide(Lat2 L) {
+__device__ void decide_apply(const Lat2 &L) {
     dope_run_state *st = L.st;
-    if (st->stop) return;
     const int cur = st->ycur, best = st->ybest;
     const dope_run_state s0 = *st;
     int64_t E = 0, S = 0, X = 0, M = -1;
@@ -762,6 +761,11 @@ __global__ void k_decide(Lat2 L) {
     apply_iteration(L, s0, E, rsq_total(S, X), M, F, cur, best, other_buffer(cur, best));
 }
 
+__global__ void k_decide(Lat2 L) {
+    if (L.st->stop) return;
+    decide_apply(L);
+}
+
 // Sharded mode: the new iterate and multipliers of the ghost rows (2D) /
 // planes (3D) -- the neighbour shards' boundary pixels -- recomputed here
 // instead of exchanged.  A ghost pixel's update (admm.py:136-151 on the q == 1
@@ -774,10 +778,7 @@ __global__ void k_decide(Lat2 L) {
 // after the consensus pass and before dope_decide: writes y into the output
 // buffer's ghost rows and marks the adjacent local block dirty where the
 // ghost iterate moved (it enters that block's objective, blockform.py:103).
-__global__ void k_ghost_consensus(Lat2 L) {
-    dope_run_state *st = L.st;
-    if (st->stop) return;
-    const int cur = st->ycur, best = st->ybest, out = other_buffer(cur, best);
+__device__ void ghost_pixels(const Lat2 &L, int cur, int out) {
     const ystore_t *__restrict__ y_in = L.y2[cur];
     ystore_t *__restrict__ y_out = L.y2[out];
     const bool is3 = L.ndim == 3;
@@ -810,6 +811,35 @@ __global__ void k_ghost_consensus(Lat2 L) {
             if (2 * y != (int32_t)y_in[G])
                 L.dirty[side == 0 ? kin : (size_t)(L.K - kplane) + kin] = 1u;
         }
+    }
+}
+
+__global__ void k_ghost_consensus(Lat2 L) {
+    dope_run_state *st = L.st;
+    if (st->stop) return;
+    const int cur = st->ycur, best = st->ybest;
+    ghost_pixels(L, cur, other_buffer(cur, best));
+}
+
+// The sharded loop's step after the agg gather, in one launch: the ghost rows'
+// new iterate (every CTA, as k_ghost_consensus) and -- in the last CTA to
+// finish, once every ghost pixel is in -- the decision (as k_decide).
+__global__ void k_ghost_decide(Lat2 L) {
+    dope_run_state *st = L.st;
+    if (st->stop) return;   // read before any CTA can be last: uniform over the grid
+    const int cur = st->ycur, best = st->ybest;
+    if (L.ga_up) ghost_pixels(L, cur, other_buffer(cur, best));
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&st->done_ctas, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        st->done_ctas = 0;
+        decide_apply(L);
     }
 }
 
@@ -850,7 +880,7 @@ __global__ void k_pack_rows(Lat2 L, int which, void *first, void *last) {
 // Sharded mode: install the neighbour shards' boundary rows into the ghost
 // rows.  which == 0: labels; which == 1: current iterate y2, marking the local
 // boundary block row dirty where the neighbour's y changed (it enters this
-// shard's block objectives, blockform.py:271).
+// shard's block objectives, blockform.py:103).
 __global__ void k_ghost_update(Lat2 L, int which, const void *up_new, const void *dn_new) {
     if (L.ndim == 3) {   // ghost planes; a changed ghost y marks the adjacent local block
         const int64_t HW = (int64_t)L.ay.dim * L.W, below = (int64_t)L.az.dim * HW;
@@ -1369,7 +1399,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB) k_consensus_warp(Lat2 L, int l
     }
 }
 
-// a += yhat - y for the step-level API (admm.py:241-248), in place.
+// a += yhat - y for the step-level API (admm.py:183-190), in place.
 __global__ void k_update_multipliers(Lat2 L, int64_t n) {
     astore_t *a = L.a;
     const ystore_t *y2 = L.y2[L.st->ycur];
@@ -1428,7 +1458,7 @@ __global__ void k_energy_current_vec(Lat2 L, uint32_t nwords) {
     cta_atomic_add(acc, &L.st->energy_acc);
 }
 
-// End of run (admm.py:300-310): trace energy + best check of the last
+// End of run (admm.py:242-252): trace energy + best check of the last
 // iterate, then state.y = best iterate unless converged.
 __global__ void k_finish_decide(Lat2 L) {
     dope_run_state *st = L.st;
@@ -1451,7 +1481,7 @@ __global__ void k_finish_decide(Lat2 L) {
     st->stop = 1;
 }
 
-// binarize (admm.py:260-262) of the current iterate: y >= 1/2 -> 1
+// binarize (admm.py:202-204) of the current iterate: y >= 1/2 -> 1
 __global__ void k_binarize(Lat2 L, int64_t n, uint8_t *out) {
     const ystore_t *y2 = L.y2[L.st->ycur];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -2238,6 +2268,18 @@ int dope_unary_i32(const double *u, int64_t n, int32_t *out, int32_t *bad, void 
     if (n == 0) return DOPE_OK;
     k_unary_i32<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(u, n, out, bad);
     return cuda_check(cudaGetLastError(), "unary_i32");
+}
+
+int dope_ghost_decide(const dope_lattice *L, void *stream) {
+    Plan P;
+    int rc = build_plan(L, P);
+    if (rc) return rc;
+    if (!P.o.sharded) return DOPE_E_ARGS;
+    const bool ghosts = P.o.ga_up && (L->ghost_up || L->ghost_dn);
+    if (ghosts && (P.o.ndim == 3 ? P.o.az.base : P.o.ay.base) < 2) return DOPE_E_GEOMETRY;
+    const int64_t unit = P.o.ndim == 3 ? (int64_t)P.o.ay.dim * P.o.W : (int64_t)P.o.W;
+    k_ghost_decide<<<ghosts ? grid_for(unit) : 1, 256, 0, (cudaStream_t)stream>>>(P.o);
+    return cuda_check(cudaGetLastError(), "ghost_decide");
 }
 
 int dope_trace_digest(const dope_lattice *L, void *stream) {

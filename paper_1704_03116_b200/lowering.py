@@ -1,6 +1,6 @@
 """Lowering of (EnergyModel, Partition) onto the integer lattice kernels.
 
-The reference assembles generic per-block operators (blockform.py:216-254).
+The reference assembles generic per-block operators (blockform.py:48-86).
 For a lattice stencil model on a non-overlapping box tiling (q == 1) those
 operators collapse to a one-pixel cross-block stencil, which is
 what the B200 kernels implement.  This module checks that the model really is
@@ -211,7 +211,7 @@ def lower_float(model: EnergyModel, partition: Partition, qscale: float = QSCALE
         fwd, bwd = [wE, wS], [wW, wN]
         fin = [("E", wE), ("S", wS)]
         bin_ = [("N", wN), ("W", wW)]
-    # r = d - dhat in dope_oracle.c's order (blockform.py:242-243 / energy.py:64-76)
+    # r = d - dhat in dope_oracle.c's order (blockform.py:75 / energy.py:64-76)
     dsum = np.zeros((H, W))
     for p in fwd + bwd:
         dsum = dsum + p

@@ -376,7 +376,7 @@ def main():
                         kpa=np.array((3, 4)), conn=4, lam=2.0, rho=1.0, max_iters=12,
                         name=rag.name, u=rag.u)
     print("run_ragged:", r["iterations"], r["energy"][-1])
-    # early convergence (stop rule admm.py:305-307): one block converges at it 1
+    # early convergence (stop rule admm.py:247-249): one block converges at it 1
     one = W.mini_disks(64, 64, 2, 1, 10, seed=5, rmax=20.0)
     save_run("single_block", one)
     # float config C2 (8-conn contrast weights, rho = 0.5) at 128^2 with 16 blocks

@@ -2,7 +2,7 @@
 
 Integer configs must be bit-exact every iteration: block labels, energies,
 max block residual, clamped flag, final y / labels / multipliers.
-residual_sq is a float sum of sqrt(int)^2 (admm.py:295) whose summation order
+residual_sq is a float sum of sqrt(int)^2 (admm.py:237) whose summation order
 is BLAS-specific in the reference, so it is compared at rtol 1e-12.
 """
 import os
