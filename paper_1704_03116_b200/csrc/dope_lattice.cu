@@ -785,6 +785,7 @@ __device__ void ghost_pixels(const Lat2 &L, int cur, int out) {
     const int64_t P = is3 ? (int64_t)L.ay.dim * L.W : (int64_t)L.W;   // pixels per ghost unit
     const int64_t below = (is3 ? (int64_t)L.az.dim : (int64_t)L.ay.dim) * P;
     const bool has_up = is3 ? L.gzu : L.gup, has_dn = is3 ? L.gzd : L.gdn;
+    if (!has_up && !has_dn) return;
     const int kplane = is3 ? L.ay.k * L.ax.k : L.ax.k;   // blocks per block row / plane
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < P; c += (int64_t)gridDim.x * blockDim.x) {
         const int32_t r = is3 ? (int32_t)(c / L.W) : 0, x = (int32_t)(c - (int64_t)r * L.W);
