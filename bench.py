@@ -151,8 +151,21 @@ def build_problem(wl, device, lower=True):
     return model, part, problems
 
 
-def cpu_baseline(wl, iters: int):
-    """Oracle C port of the reference loop on the host cores (bounded sample)."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(wl, iters: int, extras: bool = True):
+    """Oracle C port of the reference loop on the host cores (bounded sample):
+    `iters` iterations from init_state on all host threads; with extras, one
+    iteration on ONE thread and the block solves of the first iteration alone
+    (threads = 1 vs nproc, block-solve-only rate)."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle as orc
     threads = os.cpu_count() or 1
@@ -160,10 +173,22 @@ def cpu_baseline(wl, iters: int):
     t0 = time.perf_counter()
     out = orc.run(spec, wl.rho, 1.0, 0.0, iters, threads=threads)
     dt = time.perf_counter() - t0
-    return {"value": out["iterations"] / dt, "unit": "iterations/s", "cores": threads,
-            "kind": "port",
-            "sample": f"{wl.name}: first {out['iterations']} ADMM iterations from init_state "
-                      f"(oracle C port of admm.run + BK, {threads} threads), {dt:.1f} s"}
+    res = {"value": out["iterations"] / dt, "unit": "iterations/s", "cores": threads,
+           "kind": "port", "cpu_model": cpu_model(),
+           "sample": f"{wl.name}: first {out['iterations']} ADMM iterations from init_state "
+                     f"(oracle C port of admm.run + BK, {threads} threads), {dt:.1f} s"}
+    if extras:
+        t0 = time.perf_counter()
+        one = orc.run(spec, wl.rho, 1.0, 0.0, 1, threads=1)
+        res["threads_1"] = {"value": one["iterations"] / (time.perf_counter() - t0), "unit": "iterations/s",
+                            "sample": "first ADMM iteration, 1 thread"}
+        y = np.full(wl.n, 0.5)
+        a = np.zeros(wl.n)
+        t0 = time.perf_counter()
+        orc.update_blocks(spec, y, a, wl.rho, threads=threads)
+        res["block_solves_only"] = {"value": 1.0 / (time.perf_counter() - t0), "unit": "update_blocks/s",
+                                    "sample": f"first iteration's {wl.num_blocks} block solves, {threads} threads"}
+    return res
 
 
 def is_general(wl) -> bool:
@@ -320,7 +345,7 @@ def run_reference(args):
     iters = max(1, args.cpu_sample_iters)
     vals = []
     for s in range(args.warmup + args.steps):
-        r = cpu_baseline_general(wl, iters) if is_general(wl) else cpu_baseline(wl, iters)
+        r = cpu_baseline_general(wl, iters) if is_general(wl) else cpu_baseline(wl, iters, extras=False)
         if s >= args.warmup:
             vals.append(r["value"])
     v = statistics.mean(vals)
