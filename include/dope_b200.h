@@ -123,7 +123,9 @@ typedef struct dope_lattice {
                                    + 1 whose energy partial of block k is
                                    current (clean-block consensus passes);
                                    [7K, 8K) the blocks solved this iteration,
-                                   [8K, 9K) 1 + block k's slot in that list  */
+                                   [8K, 9K) 1 + block k's slot in that list,
+                                   [9K, 11K + 2) the run loop's two dirty-block
+                                   worklists [count, K entries]: 11K + 2 in all */
     int64_t *part_energy;       /* K   per-block pair-energy partials          */
     int64_t *part_unary;        /* K   per-block change of sum u*y2           */
     int64_t *part_ressq;        /* K   per-block sum (yhat - y)^2             */
@@ -208,6 +210,9 @@ int dope_update_multipliers(const dope_lattice *L, void *stream);
  * become no-ops once converged.  use_graph: capture one iteration in a CUDA
  * graph and replay it. */
 int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void *stream);
+/* Run-loop entry (dope_admm_run / dope_sharded_run call it): the current
+ * iteration's dirty-block worklist rebuilt from the re-solve flags. */
+int dope_rebuild_dirty_list(const dope_lattice *L, void *stream);
 /* End of run (admm.py:242-252): energy + best check of the last iterate;
  * the current iterate becomes the best one unless converged. */
 int dope_finish_run(const dope_lattice *L, void *stream);

@@ -209,7 +209,8 @@ def lib():
     lb.dope_lattice_check.argtypes = [P]
     for name in ("dope_admm_init", "dope_update_blocks", "dope_update_global",
                  "dope_update_multipliers", "dope_finish_run", "dope_energy_local",
-                 "dope_finish_decide", "dope_ghost_consensus", "dope_trace_digest", "dope_ghost_decide"):
+                 "dope_finish_decide", "dope_ghost_consensus", "dope_trace_digest", "dope_ghost_decide",
+                 "dope_rebuild_dirty_list"):
         f = getattr(lb, name)
         f.restype = C.c_int
         f.argtypes = [P, C.c_void_p]

@@ -376,8 +376,9 @@ class _DeviceState:
         self.resid = torch.zeros(K * stride, dtype=u8, device=dev)
         # [0, K): re-solve flags; [K, 2K): iteration + 1 of each block's last solve;
         # [2K, 7K): y-buffer / iterate-change / energy-partial stamps of the
-        # clean-block consensus passes; [7K, 9K): the solved-block list and slots
-        self.dirty = torch.zeros(9 * K, dtype=torch.int32, device=dev)
+        # clean-block consensus passes; [7K, 9K): the solved-block list and slots;
+        # [9K, 11K + 2): the run loop's dirty-block worklists
+        self.dirty = torch.zeros(11 * K + 2, dtype=torch.int32, device=dev)
         self.dirty[:K] = 1
         sstride = int(lb.dope_scratch_stride(C.byref(L)))
         self.scratch = torch.empty(max(K * sstride, 16), dtype=u8, device=dev)

@@ -390,11 +390,11 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
             L.pr[k] = sq;
             L.pf[k] = clamped | (memo ? 64 : 0) | (int)(gbits << 8);
             agg.add_block(e, u2, sq, clamped);
-            if (f & 2u) L.dirty[k] = 1u;
-            if (f & 4u) L.dirty[k - 1] = 1u;
-            if (f & 8u) L.dirty[k + 1] = 1u;
-            if ((f & 16u) && k - KX >= 0) L.dirty[k - KX] = 1u;
-            if ((f & 32u) && k + KX < K) L.dirty[k + KX] = 1u;
+            if (f & 2u) mark_dirty(L, k);
+            if (f & 4u) mark_dirty(L, k - 1);
+            if (f & 8u) mark_dirty(L, k + 1);
+            if ((f & 16u) && k - KX >= 0) mark_dirty(L, k - KX);
+            if ((f & 32u) && k + KX < K) mark_dirty(L, k + KX);
             // the output buffer now holds the block's whole iterate
             ybuf_stamp(L, out)[k] = ep_now;
             if (want_e) pe_stamp(L)[k] = ep_now;

@@ -288,6 +288,8 @@ int dope_sharded_run_group(const dope_lattice *const *S, int32_t nloc, void *com
     int rc = check_shards(S, nloc, T);
     if (rc) return rc;
     if (iters <= 0) return DOPE_OK;
+    for (int r = 0; r < nloc; ++r)
+        if ((rc = dope_rebuild_dirty_list(S[r], s))) return rc;
     if (!use_graph) {
         for (int i = 0; i < iters; ++i)
             if ((rc = one_iteration(S, nloc, T, s))) return rc;

@@ -86,7 +86,31 @@ struct Lat2 {
     int64_t hash_base;      // global index of the first pixel (shards)
     int32_t shard_index, shard_count;   // sharded: this shard's slot in the agg table
     astore_t *ga_up, *ga_dn;            // sharded: multipliers of the ghost rows / planes
+    uint32_t *dlist;        // run loop: two dirty-block worklists (dirty_list), else null
 };
+
+// Dirty-block worklists of the run loop (dirty[9K, 11K + 2)): list p = [count,
+// K entries]; the consensus pass of iteration t appends every block it marks
+// dirty (first mark only) to list (t + 1) & 1, which K1 of iteration t + 1
+// deals out first-come: CTA i solves entry i, so every block that needs a
+// solve starts in the first wave instead of wherever its id puts it among the
+// K mostly-clean CTAs.  K1 resets the other list for the next pass.
+__device__ __forceinline__ uint32_t *dirty_list(const Lat2 &L, int parity) {
+    return L.dlist + (size_t)(parity & 1) * (L.K + 1);
+}
+
+// Mark block k dirty for the next iteration (and list it, run loop).
+__device__ __forceinline__ void mark_dirty(const Lat2 &L, int64_t k) {
+    if (!L.dlist) {
+        L.dirty[k] = 1u;
+        return;
+    }
+    if (atomicExch(&L.dirty[k], 1u) == 0u) {
+        uint32_t *lst = dirty_list(L, L.st->iteration + 1);
+        const uint32_t slot = atomicAdd(lst, 1u);
+        if (slot < (uint32_t)L.K) lst[1 + slot] = (uint32_t)k;
+    }
+}
 
 // Sharded mode: layout of the caller's halo buffer (dope_halo_bytes), U bytes
 // per exchanged row (2D) / plane (3D): [0, U) first local row out, [U, 2U) last
@@ -168,7 +192,7 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
     uint32_t *masks32 = reinterpret_cast<uint32_t *>(masks);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int k = blockIdx.x;
+    int k = blockIdx.x;
     uint64_t t_begin = 0;
     if (L.timeline && tid == 0) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
@@ -184,7 +208,17 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         griddep_launch();   // all K1 CTAs are resident: the consensus pass may launch
     }
     int ycur;
-    {
+    if (L.dlist) {
+        // run loop: CTA i takes entry i of this iteration's dirty-block list
+        const int stop = L.st->stop;
+        ycur = L.st->ycur;
+        const int it = L.st->iteration;
+        const uint32_t *lst = dirty_list(L, it);
+        if (blockIdx.x == 0 && tid == 0) dirty_list(L, it + 1)[0] = 0u;   // the next pass fills it
+        const uint32_t cnt = lst[0], ent = lst[1 + (blockIdx.x < (unsigned)L.K ? blockIdx.x : 0)];
+        if (stop || blockIdx.x >= cnt) return;
+        k = (int)ent;
+    } else {
         // the flags and the current buffer in one round trip: a clean CTA must
         // leave its slot fast (4096 CTAs churn through ~5 slots per SM), a
         // dirty one needs ycur before its first data load
@@ -590,6 +624,14 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
     // solve epochs and the stamps of the clean-block consensus passes
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 6 * (int64_t)L.K; i += stride)
             L.dirty[L.K + i] = 0u;
+    if (L.dlist) {   // iteration 0 solves every block: list 0 = all, list 1 empty
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.K; i += stride)
+            L.dlist[1 + i] = (uint32_t)i;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            L.dlist[0] = (uint32_t)L.K;
+            L.dlist[L.K + 1] = 0u;
+        }
+    }
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.K; i += stride) {
         L.dirty[i] = 1u;
         L.pe[i] = 0;
@@ -810,7 +852,7 @@ __device__ void ghost_pixels(const Lat2 &L, int cur, int out) {
             ga[c] = (astore_t)(aold + yh - y);
             y_out[G] = (ystore_t)(2 * y);
             if (2 * y != (int32_t)y_in[G])
-                L.dirty[side == 0 ? kin : (size_t)(L.K - kplane) + kin] = 1u;
+                mark_dirty(L, side == 0 ? kin : (size_t)(L.K - kplane) + kin);
         }
     }
 }
@@ -842,6 +884,21 @@ __global__ void k_ghost_decide(Lat2 L) {
         st->done_ctas = 0;
         decide_apply(L);
     }
+}
+
+// Run-loop entry: this iteration's dirty-block list from the flags (they may
+// have been set by step-level calls or the host since the last pass), the
+// other list emptied.  One CTA.
+__global__ void k_rebuild_dlist(Lat2 L) {
+    const int it = L.st->iteration;
+    uint32_t *cur = dirty_list(L, it);
+    if (threadIdx.x == 0) {
+        cur[0] = 0u;
+        dirty_list(L, it + 1)[0] = 0u;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < L.K; k += blockDim.x)
+        if (L.dirty[k]) cur[1 + atomicAdd(cur, 1u)] = (uint32_t)k;
 }
 
 // The integer path's unary from the caller's float64 vector (the reference's
@@ -895,11 +952,11 @@ __global__ void k_ghost_update(Lat2 L, int which, const void *up_new, const void
                 const int r = (int)(c / L.W), col = (int)(c - (int64_t)r * L.W);
                 const int kyx = L.ay.owner(r) * L.ax.k + L.ax.owner(col);
                 if (L.gzu && up && y[-HW + c] != up[c]) {
-                    L.dirty[kyx] = 1u;
+                    mark_dirty(L, kyx);
                     y[-HW + c] = up[c];
                 }
                 if (L.gzd && dn && y[below + c] != dn[c]) {
-                    L.dirty[(L.az.k - 1) * L.ay.k * L.ax.k + kyx] = 1u;
+                    mark_dirty(L, (L.az.k - 1) * L.ay.k * L.ax.k + kyx);
                     y[below + c] = dn[c];
                 }
             }
@@ -917,11 +974,11 @@ __global__ void k_ghost_update(Lat2 L, int which, const void *up_new, const void
             uint8_t *y = L.y2[L.st->ycur];
             const int bx = L.ax.owner(c);
             if (L.gup && up && y[-W + c] != up[c]) {
-                L.dirty[bx] = 1u;
+                mark_dirty(L, bx);
                 y[-W + c] = up[c];
             }
             if (L.gdn && dn && y[below + c] != dn[c]) {
-                L.dirty[(L.ay.k - 1) * L.ax.k + bx] = 1u;
+                mark_dirty(L, (L.ay.k - 1) * L.ax.k + bx);
                 y[below + c] = dn[c];
             }
         }
@@ -1006,11 +1063,11 @@ __device__ __forceinline__ void block_epilogue(const Lat2 &L, int k, int64_t e_a
         L.pu[k] = U;
         L.pr[k] = S;
         L.pf[k] = Fm & 1;
-        if (Fm & 2) L.dirty[k] = 1u;
-        if (Fm & 4) L.dirty[k - 1] = 1u;
-        if (Fm & 8) L.dirty[k + 1] = 1u;
-        if ((Fm & 16) && k - L.ax.k >= 0) L.dirty[k - L.ax.k] = 1u;
-        if ((Fm & 32) && k + L.ax.k < L.K) L.dirty[k + L.ax.k] = 1u;
+        if (Fm & 2) mark_dirty(L, k);
+        if (Fm & 4) mark_dirty(L, k - 1);
+        if (Fm & 8) mark_dirty(L, k + 1);
+        if ((Fm & 16) && k - L.ax.k >= 0) mark_dirty(L, k - L.ax.k);
+        if ((Fm & 32) && k + L.ax.k < L.K) mark_dirty(L, k + L.ax.k);
         agg.add_block(E, U, S, Fm & 1);
     }
     __syncthreads();
@@ -1366,11 +1423,11 @@ __global__ void __launch_bounds__(WPC * 32, MINB) k_consensus_warp(Lat2 L, int l
             L.pu[k] = U;
             L.pr[k] = S;
             L.pf[k] = (int)(fm & 1u);
-            if (fm & 2u) L.dirty[k] = 1u;
-            if (fm & 4u) L.dirty[k - 1] = 1u;
-            if (fm & 8u) L.dirty[k + 1] = 1u;
-            if ((fm & 16u) && k - L.ax.k >= 0) L.dirty[k - L.ax.k] = 1u;
-            if ((fm & 32u) && k + L.ax.k < L.K) L.dirty[k + L.ax.k] = 1u;
+            if (fm & 2u) mark_dirty(L, k);
+            if (fm & 4u) mark_dirty(L, k - 1);
+            if (fm & 8u) mark_dirty(L, k + 1);
+            if ((fm & 16u) && k - L.ax.k >= 0) mark_dirty(L, k - L.ax.k);
+            if ((fm & 32u) && k + L.ax.k < L.K) mark_dirty(L, k + L.ax.k);
             agg.add_block(E, U, S, (int)(fm & 1u));
         }
     }
@@ -1677,6 +1734,10 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
     o.shard_count = L->sharded ? L->shard_count : 1;
     if (L->sharded && (L->shard_count < 1 || L->shard_index < 0 || L->shard_index >= L->shard_count))
         return DOPE_E_ARGS;
+    // dirty-block worklists: run loop (fused pass, clean-block skipping) with a
+    // K1 that deals them out (2D integer K1, shared-memory K1-3D)
+    if (L->fuse_multipliers && L->skip_clean && !L->timeline && !getenv("DOPE_NO_DLIST"))
+        o.dlist = L->dirty + (size_t)9 * o.K;
     if (L->sharded && L->halo) {
         const int64_t U = is3 ? L->dims[1] * L->dims[2] : L->dims[1];
         uint8_t *h = static_cast<uint8_t *>(L->halo);
@@ -1720,6 +1781,7 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
         return e && strcmp(e, "l2") == 0;
     }();
     o.nib3 = is3 && !k1_3d_l2 && o.boxd == 32 && o.boxh == 32 && o.boxw == 32 && 2 * o.cap <= 15;
+    if (is3 && !o.nib3) o.dlist = nullptr;   // the HBM-scratch K1-3D scans the flags
     return DOPE_OK;
 }
 
@@ -2145,6 +2207,7 @@ int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void 
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     if (iters <= 0) return DOPE_OK;
+    if ((rc = dope_rebuild_dirty_list(L, stream))) return rc;
     if (!use_graph) {
         for (int i = 0; i < iters; ++i) {
             if ((rc = launch_k1(P, s))) return rc;
@@ -2262,6 +2325,15 @@ int dope_ghost_consensus(const dope_lattice *L, void *stream) {
     const int64_t unit = P.o.ndim == 3 ? (int64_t)P.o.ay.dim * P.o.W : (int64_t)P.o.W;
     k_ghost_consensus<<<grid_for(unit), 256, 0, (cudaStream_t)stream>>>(P.o);
     return cuda_check(cudaGetLastError(), "ghost_consensus");
+}
+
+int dope_rebuild_dirty_list(const dope_lattice *L, void *stream) {
+    Plan P;
+    int rc = build_plan(L, P);
+    if (rc) return rc;
+    if (!P.o.dlist) return DOPE_OK;
+    k_rebuild_dlist<<<1, 1024, 0, (cudaStream_t)stream>>>(P.o);
+    return cuda_check(cudaGetLastError(), "rebuild_dlist");
 }
 
 int dope_unary_i32(const double *u, int64_t n, int32_t *out, int32_t *bad, void *stream) {

@@ -333,13 +333,13 @@ __global__ void __launch_bounds__(512) k_consensus3d(Lat2 L) {
         L.pr[k] = S;
         L.pf[k] = (Fm & 128u) ? 1 : 0;
         const int KX = L.ax.k, KYX = L.ay.k * L.ax.k;
-        if (Fm & 1u) L.dirty[k] = 1u;
-        if (Fm & 2u) L.dirty[k - 1] = 1u;
-        if (Fm & 4u) L.dirty[k + 1] = 1u;
-        if (Fm & 8u) L.dirty[k - KX] = 1u;
-        if (Fm & 16u) L.dirty[k + KX] = 1u;
-        if ((Fm & 32u) && k - KYX >= 0) L.dirty[k - KYX] = 1u;
-        if ((Fm & 64u) && k + KYX < L.K) L.dirty[k + KYX] = 1u;
+        if (Fm & 1u) mark_dirty(L, k);
+        if (Fm & 2u) mark_dirty(L, k - 1);
+        if (Fm & 4u) mark_dirty(L, k + 1);
+        if (Fm & 8u) mark_dirty(L, k - KX);
+        if (Fm & 16u) mark_dirty(L, k + KX);
+        if ((Fm & 32u) && k - KYX >= 0) mark_dirty(L, k - KYX);
+        if ((Fm & 64u) && k + KYX < L.K) mark_dirty(L, k + KYX);
         ybuf_stamp(L, out)[k] = (uint32_t)L.st->iteration + 1u;
         if (Fm & 256u) ychg_stamp(L)[k] = (uint32_t)L.st->iteration + 1u;
         CtaAgg agg;
@@ -529,13 +529,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_consensus3d_vec(Lat2 L, int l
             L.pr[k] = S;
             L.pf[k] = (Fm & 128u) ? 1 : 0;
             const int KX = L.ax.k, KYX = L.ay.k * L.ax.k;
-            if (Fm & 1u) L.dirty[k] = 1u;
-            if (Fm & 2u) L.dirty[k - 1] = 1u;
-            if (Fm & 4u) L.dirty[k + 1] = 1u;
-            if (Fm & 8u) L.dirty[k - KX] = 1u;
-            if (Fm & 16u) L.dirty[k + KX] = 1u;
-            if ((Fm & 32u) && k - KYX >= 0) L.dirty[k - KYX] = 1u;
-            if ((Fm & 64u) && k + KYX < L.K) L.dirty[k + KYX] = 1u;
+            if (Fm & 1u) mark_dirty(L, k);
+            if (Fm & 2u) mark_dirty(L, k - 1);
+            if (Fm & 4u) mark_dirty(L, k + 1);
+            if (Fm & 8u) mark_dirty(L, k - KX);
+            if (Fm & 16u) mark_dirty(L, k + KX);
+            if ((Fm & 32u) && k - KYX >= 0) mark_dirty(L, k - KYX);
+            if ((Fm & 64u) && k + KYX < L.K) mark_dirty(L, k + KYX);
             ybuf_stamp(L, out)[k] = (uint32_t)it + 1u;
             if (Fm & 256u) ychg_stamp(L)[k] = (uint32_t)it + 1u;
             agg.add_block(E, U, S, (Fm & 128u) ? 1 : 0);
@@ -765,13 +765,13 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
                 L.pu[k] = U;
                 L.pr[k] = S;
                 L.pf[k] = (gbits ? 1 : 0) | (int)(gbits << 1);
-                if (Fm & 1u) L.dirty[k] = 1u;
-                if (Fm & 2u) L.dirty[k - 1] = 1u;
-                if (Fm & 4u) L.dirty[k + 1] = 1u;
-                if (Fm & 8u) L.dirty[k - KX] = 1u;
-                if (Fm & 16u) L.dirty[k + KX] = 1u;
-                if ((Fm & 32u) && k - KYX >= 0) L.dirty[k - KYX] = 1u;
-                if ((Fm & 64u) && k + KYX < L.K) L.dirty[k + KYX] = 1u;
+                if (Fm & 1u) mark_dirty(L, k);
+                if (Fm & 2u) mark_dirty(L, k - 1);
+                if (Fm & 4u) mark_dirty(L, k + 1);
+                if (Fm & 8u) mark_dirty(L, k - KX);
+                if (Fm & 16u) mark_dirty(L, k + KX);
+                if ((Fm & 32u) && k - KYX >= 0) mark_dirty(L, k - KYX);
+                if ((Fm & 64u) && k + KYX < L.K) mark_dirty(L, k + KYX);
                 ybuf_stamp(L, out)[k] = ep;
                 pe_stamp(L)[k] = ep;
                 if (Fm & 256u) ychg_stamp(L)[k] = ep;
@@ -912,13 +912,13 @@ __global__ void __launch_bounds__(256, K2P_MINB) k_consensus3d_plane(Lat2 L) {
             L.pr[k] = S;
             L.pf[k] = ((Fm & 128u) ? 1 : 0) | (int)(gb_ << 1);   // bit 0 clamped, bits 1-27 quad-group clamp memos
             const int KX = L.ax.k, KYX = L.ay.k * L.ax.k;
-            if (Fm & 1u) L.dirty[k] = 1u;
-            if (Fm & 2u) L.dirty[k - 1] = 1u;
-            if (Fm & 4u) L.dirty[k + 1] = 1u;
-            if (Fm & 8u) L.dirty[k - KX] = 1u;
-            if (Fm & 16u) L.dirty[k + KX] = 1u;
-            if ((Fm & 32u) && k - KYX >= 0) L.dirty[k - KYX] = 1u;
-            if ((Fm & 64u) && k + KYX < L.K) L.dirty[k + KYX] = 1u;
+            if (Fm & 1u) mark_dirty(L, k);
+            if (Fm & 2u) mark_dirty(L, k - 1);
+            if (Fm & 4u) mark_dirty(L, k + 1);
+            if (Fm & 8u) mark_dirty(L, k - KX);
+            if (Fm & 16u) mark_dirty(L, k + KX);
+            if ((Fm & 32u) && k - KYX >= 0) mark_dirty(L, k - KYX);
+            if ((Fm & 64u) && k + KYX < L.K) mark_dirty(L, k + KYX);
             ybuf_stamp(L, out)[k] = ep;
             if (want_e) pe_stamp(L)[k] = ep;
             if (Fm & 256u) ychg_stamp(L)[k] = ep;

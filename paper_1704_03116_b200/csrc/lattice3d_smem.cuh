@@ -187,10 +187,19 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
     // row-activity flags: word y, bit z <=> row (z, y) may hold a node to push
     // (Fp) / to relabel (Fr); warp w scans the rows of word w
     uint32_t *Fp = reinterpret_cast<uint32_t *>(sm3 + OFF_FLAG), *Fr = Fp + 32;
-    const int k = blockIdx.x;
+    int k = blockIdx.x;
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm3 + OFF_MISC + 32);
-    if (L.st->stop) return;
-    if (L.skip_clean && L.dirty[k] == 0) return;
+    if (L.dlist) {   // run loop: CTA i takes entry i of this iteration's dirty-block list
+        const int stop = L.st->stop, it = L.st->iteration;
+        const uint32_t *lst = dirty_list(L, it);
+        if (blockIdx.x == 0 && tid == 0) dirty_list(L, it + 1)[0] = 0u;   // the next pass fills it
+        const uint32_t cnt = lst[0], ent = lst[1 + blockIdx.x];
+        if (stop || blockIdx.x >= cnt) return;
+        k = (int)ent;
+    } else {
+        if (L.st->stop) return;
+        if (L.skip_clean && L.dirty[k] == 0) return;
+    }
     if (tid == 0) {
         mbar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
