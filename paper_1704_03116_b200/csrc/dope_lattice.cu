@@ -1736,7 +1736,9 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
         return DOPE_E_ARGS;
     // dirty-block worklists: run loop (fused pass, clean-block skipping) with a
     // K1 that deals them out (2D integer K1, shared-memory K1-3D)
-    if (L->fuse_multipliers && L->skip_clean && !L->timeline && !getenv("DOPE_NO_DLIST"))
+    // (only with more blocks than the first K1 wave holds: with fewer, every
+    // CTA starts at once and the list's extra round trip is pure cost -- C1)
+    if (L->fuse_multipliers && L->skip_clean && !L->timeline && !getenv("DOPE_NO_DLIST") && o.K > 2 * sm_count())
         o.dlist = L->dirty + (size_t)9 * o.K;
     if (L->sharded && L->halo) {
         const int64_t U = is3 ? L->dims[1] * L->dims[2] : L->dims[1];
