@@ -8,7 +8,11 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libdope_b200.so"
+import os
+
+# DOPE_LIB: load another build of the library (e.g. the bounds-checked
+# libdope_b200_checked.so of `python -m paper_1704_03116_b200.build --checked`)
+LIB_PATH = Path(os.environ.get("DOPE_LIB") or Path(__file__).resolve().parent / "libdope_b200.so")
 ABI_VERSION = 1
 
 DOPE_OK = 0

@@ -39,19 +39,27 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+CHECKED_LIB = PKG / "libdope_b200_checked.so"
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> Path:
+    """checked: the bounds / invariant-checked variant (-DDOPE_BOUNDS) as
+    libdope_b200_checked.so -- load it with DOPE_LIB=<path> (diagnostics)."""
+    out = CHECKED_LIB if checked else LIB
+    if not force and not checked and not _stale():
         return LIB
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
            "-Xcompiler", "-O2", "-shared", "-cudart", "static",
-           f"-I{ROOT / 'include'}", f"-I{CSRC}", "-o", str(LIB)]
+           f"-I{ROOT / 'include'}", f"-I{CSRC}", "-o", str(out)]
+    if checked:
+        cmd += ["-DDOPE_BOUNDS"]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     cmd += os.environ.get("DOPE_NVCC_EXTRA", "").split()   # diagnostics builds (e.g. -DK1S_DIAG)
     cmd += [str(s) for s in sources()]
     subprocess.run(cmd, check=True)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

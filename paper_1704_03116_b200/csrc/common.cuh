@@ -4,8 +4,25 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #define FULLMASK 0xffffffffu
+
+// Checked builds (-DDOPE_BOUNDS, `python -m paper_1704_03116_b200.build --checked`):
+// device-side bounds / invariant checks that trap with the failing condition
+// -- the stand-in for compute-sanitizer, which this GPU pool does not allow.
+#ifdef DOPE_BOUNDS
+#define DOPE_ASSERT(c)                                                                           \
+    do {                                                                                         \
+        if (!(c)) {                                                                              \
+            printf("DOPE_ASSERT %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, blockIdx.x, \
+                   threadIdx.x, #c);                                                             \
+            __trap();                                                                            \
+        }                                                                                        \
+    } while (0)
+#else
+#define DOPE_ASSERT(c) ((void)0)
+#endif
 
 namespace dope {
 

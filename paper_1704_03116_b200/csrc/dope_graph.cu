@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "common.cuh"
 #include "dope_b200.h"
 
 namespace dope_graph {
@@ -109,6 +110,7 @@ __device__ void solve_graph(int32_t m, const double *__restrict__ tcap, int64_t 
     __shared__ int s_any;
     for (int i = tid; i < m; i += NT) w.g[i] = tcap[i];
     for (int64_t p = tid; p < P; p += NT) {
+        DOPE_ASSERT(pi[p] >= 0 && pi[p] < m && pj[p] >= 0 && pj[p] < m);
         w.rc[2 * p] = cij[p];
         w.rc[2 * p + 1] = cji[p];
         w.head[2 * p] = pj[p];

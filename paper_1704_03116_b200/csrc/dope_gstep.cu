@@ -26,6 +26,7 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include "common.cuh"
 #include "dope_b200.h"
 
 namespace dope_gs {
@@ -46,6 +47,7 @@ static int grid_for(int64_t n, int nt = 256) {
 
 // entry of block k holding pixel j, or -1
 __device__ __forceinline__ int64_t entry_of(const dope_gstep &G, int64_t j, int32_t k) {
+    DOPE_ASSERT(j >= 0 && j < G.n && k >= 0 && k < G.K);
     for (int64_t t = G.mem_ptr[j]; t < G.mem_ptr[j + 1]; ++t) {
         const int64_t e = G.mem_ent[t];
         if (G.ent_blk[e] == k) return e;

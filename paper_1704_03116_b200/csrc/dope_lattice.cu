@@ -101,6 +101,7 @@ __device__ __forceinline__ uint32_t *dirty_list(const Lat2 &L, int parity) {
 
 // Mark block k dirty for the next iteration (and list it, run loop).
 __device__ __forceinline__ void mark_dirty(const Lat2 &L, int64_t k) {
+    DOPE_ASSERT(k >= 0 && k < L.K);
     if (!L.dlist) {
         L.dirty[k] = 1u;
         return;
@@ -218,6 +219,7 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         const uint32_t cnt = lst[0], ent = lst[1 + (blockIdx.x < (unsigned)L.K ? blockIdx.x : 0)];
         if (stop || blockIdx.x >= cnt) return;
         k = (int)ent;
+        DOPE_ASSERT(cnt <= (uint32_t)L.K && k >= 0 && k < L.K);
     } else {
         // the flags and the current buffer in one round trip: a clean CTA must
         // leave its slot fast (4096 CTAs churn through ~5 slots per SM), a
@@ -285,6 +287,7 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
                 yl[j] = yrr[j] = 0;
                 if (ok[j]) {
                     const int64_t G = (int64_t)(lo_r + r) * Wg + lo_c + c0;
+                    DOPE_ASSERT(G >= 0 && G + 4 <= (int64_t)L.ay.dim * Wg);
                     uq[j] = __ldg(reinterpret_cast<const int4 *>(L.u + G));
                     aq[j] = *reinterpret_cast<const uint2 *>(a_cur + G);
                     yq[j] = *reinterpret_cast<const uint32_t *>(y_cur + G);
@@ -475,6 +478,8 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
                     const int w = v + off;
                     if (h[w] != ht) continue;
                     const int32_t delta = left < rv ? left : rv;
+                    DOPE_ASSERT(w >= 0 && w < M && delta > 0 && rv <= 2 * cap &&
+                                rr[(d ^ 1) * M + w] + delta <= 2 * cap);   // r + r' = 2 cap per arc pair
                     rr[d * M + v] = (uint8_t)(rv - delta);
                     rr[(d ^ 1) * M + w] = (uint8_t)(rr[(d ^ 1) * M + w] + delta);
                     atomicAdd(&g[w], delta);
@@ -515,6 +520,7 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
             if (r < hr && c0 < wc) {
                 const uint32_t b = (uint32_t)(reach[v0 >> 6] >> (v0 & 63)) & 0xFu;
                 const int64_t G = (int64_t)(lo_r + r) * Wg + lo_c + c0;
+                DOPE_ASSERT(G >= 0 && G + 4 <= (int64_t)L.ay.dim * Wg);
                 *reinterpret_cast<uint32_t *>(L.yhat + G) = (b * 0x00204081u) & 0x01010101u;
             }
         }
@@ -837,6 +843,7 @@ __device__ void ghost_pixels(const Lat2 &L, int cur, int out) {
             if (side == 0 ? !has_up : !has_dn) continue;
             const int64_t G = side == 0 ? c - P : below + c;          // ghost pixel
             const int64_t I = side == 0 ? c : below - P + c;          // facing local pixel
+            DOPE_ASSERT(G >= -P && G < below + P && I >= 0 && I < below);
             const int32_t yh = L.yhat[G];
             int32_t s = yh - L.yhat[I];
             if (x > 0 && L.ax.owner(x - 1) != bx) s += yh - L.yhat[G - 1];
