@@ -503,10 +503,14 @@ int dope_gs_energy(int64_t n, const double *u, int64_t npairs, const int32_t *pa
  * reaching the sink; flows[b]); graph b: nodes [node_off[b], node_off[b+1]),
  * pairs [pair_off[b], pair_off[b+1]) with graph-local ends, workspace at
  * ws_off[b] (dope_bk_workspace_bytes of that graph).  Offsets are device
- * arrays. */
+ * arrays.  adj_off / adj (optional, NULL: built per solve): each graph's
+ * tail-grouped arc lists in pair order (arc 2p: i->j, 2p+1: j->i), graph b's
+ * m_b + 1 offsets at adj_off + node_off[b] + b, its 2 P_b arcs at
+ * adj + 2 pair_off[b]. */
 int dope_bk_maxflow_batch(int32_t B, const int64_t *node_off, const int64_t *pair_off, const int64_t *ws_off,
                           const double *tcap, const int32_t *pair_i, const int32_t *pair_j, const double *cap_ij,
-                          const double *cap_ji, uint8_t *labels, double *flows, void *workspace, void *stream);
+                          const double *cap_ji, uint8_t *labels, double *flows, void *workspace,
+                          const int32_t *adj_off, const int32_t *adj, void *stream);
 /* exhaustive_minimize (solvers.py:53-82) of a batch of graphs of <= 24 nodes:
  * variable 0 is the most significant bit, ties to the smallest code. */
 int dope_exhaustive_batch(int32_t B, const int64_t *node_off, const int64_t *pair_off, const double *linear,

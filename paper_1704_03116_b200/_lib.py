@@ -333,7 +333,7 @@ def lib():
     lb.dope_gs_energy.restype = C.c_int
     lb.dope_gs_energy.argtypes = [C.c_int64, V, C.c_int64, V, V, V, C.c_double, V, V, V, V]
     lb.dope_bk_maxflow_batch.restype = C.c_int
-    lb.dope_bk_maxflow_batch.argtypes = [C.c_int32, V, V, V, V, V, V, V, V, V, V, V, V]
+    lb.dope_bk_maxflow_batch.argtypes = [C.c_int32, V, V, V, V, V, V, V, V, V, V, V, V, V, V]
     lb.dope_exhaustive_batch.restype = C.c_int
     lb.dope_exhaustive_batch.argtypes = [C.c_int32, V, V, V, V, V, V, C.c_double, V, V, V]
     lb.dope_trace_digest.restype = C.c_int

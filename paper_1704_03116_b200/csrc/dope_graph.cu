@@ -100,10 +100,14 @@ __device__ void bfs_from_sink(const Ws &w, int m, int tid) {
     }
 }
 
+// pre_off / pre_adj (optional): the graph's tail-grouped adjacency, built once
+// by the caller (the batched step-level solves reuse one structure per block
+// every iteration instead of a serial per-solve build).
 __device__ void solve_graph(int32_t m, const double *__restrict__ tcap, int64_t P, const int32_t *__restrict__ pi,
                             const int32_t *__restrict__ pj, const double *__restrict__ cij,
                             const double *__restrict__ cji, uint8_t *__restrict__ labels,
-                            double *__restrict__ flow, char *wsbase) {
+                            double *__restrict__ flow, char *wsbase, const int32_t *pre_off = nullptr,
+                            const int32_t *pre_adj = nullptr) {
     Ws w;
     ws_layout(m, P, &w, wsbase);
     const int tid = threadIdx.x;
@@ -116,7 +120,10 @@ __device__ void solve_graph(int32_t m, const double *__restrict__ tcap, int64_t 
         w.head[2 * p] = pj[p];
         w.head[2 * p + 1] = pi[p];
     }
-    if (tid == 0) {
+    if (pre_off) {
+        for (int i = tid; i <= m; i += NT) w.off[i] = pre_off[i];
+        for (int64_t a = tid; a < 2 * P; a += NT) w.adj[a] = pre_adj[a];
+    } else if (tid == 0) {
         // tail-grouped adjacency in pair order (deterministic, serial)
         for (int i = 0; i <= m; ++i) w.off[i] = 0;
         for (int64_t p = 0; p < P; ++p) { w.off[pi[p] + 1] += 1; w.off[pj[p] + 1] += 1; }
@@ -227,7 +234,8 @@ __global__ void __launch_bounds__(NT) k_graph_maxflow_batch(const int64_t *node_
                                                             const int64_t *ws_off, const double *tcap,
                                                             const int32_t *pi, const int32_t *pj, const double *cij,
                                                             const double *cji, uint8_t *labels, double *flow,
-                                                            char *wsbase) {
+                                                            char *wsbase, const int32_t *adj_off,
+                                                            const int32_t *adj) {
     const int b = blockIdx.x;
     const int64_t n0 = node_off[b], p0 = pair_off[b];
     const int32_t m = (int32_t)(node_off[b + 1] - n0);
@@ -236,7 +244,8 @@ __global__ void __launch_bounds__(NT) k_graph_maxflow_batch(const int64_t *node_
         if (threadIdx.x == 0) flow[b] = 0.0;
         return;
     }
-    solve_graph(m, tcap + n0, P, pi + p0, pj + p0, cij + p0, cji + p0, labels + n0, flow + b, wsbase + ws_off[b]);
+    solve_graph(m, tcap + n0, P, pi + p0, pj + p0, cij + p0, cji + p0, labels + n0, flow + b, wsbase + ws_off[b],
+                adj_off ? adj_off + n0 + b : nullptr, adj ? adj + 2 * p0 : nullptr);
 }
 
 }  // namespace dope_graph
@@ -269,11 +278,13 @@ int dope_bk_maxflow(int32_t m, const double *tcap, int64_t npairs, const int32_t
 
 int dope_bk_maxflow_batch(int32_t B, const int64_t *node_off, const int64_t *pair_off, const int64_t *ws_off,
                           const double *tcap, const int32_t *pair_i, const int32_t *pair_j, const double *cap_ij,
-                          const double *cap_ji, uint8_t *labels, double *flows, void *workspace, void *stream) {
+                          const double *cap_ji, uint8_t *labels, double *flows, void *workspace,
+                          const int32_t *adj_off, const int32_t *adj, void *stream) {
     if (B < 0 || (B && (!node_off || !pair_off || !ws_off || !flows || !workspace))) return DOPE_E_ARGS;
     if (B == 0) return DOPE_OK;
     dope_graph::k_graph_maxflow_batch<<<B, dope_graph::NT, 0, (cudaStream_t)stream>>>(
-        node_off, pair_off, ws_off, tcap, pair_i, pair_j, cap_ij, cap_ji, labels, flows, (char *)workspace);
+        node_off, pair_off, ws_off, tcap, pair_i, pair_j, cap_ij, cap_ji, labels, flows, (char *)workspace, adj_off,
+        adj);
     return cudaGetLastError() == cudaSuccess ? DOPE_OK : DOPE_E_CUDA;
 }
 

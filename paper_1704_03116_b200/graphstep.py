@@ -317,11 +317,32 @@ class GraphProblems:
         self.bp_ptr = np.zeros(lay.K + 1, dtype=np.int64)
         np.cumsum(np.bincount(kb, minlength=lay.K), out=self.bp_ptr[1:])
         self.bp_i, self.bp_j, self.bp_w = li.astype(np.int32), lj.astype(np.int32), vals
+        # every block's tail-grouped arc lists in pair order (built once here,
+        # not per solve): arc 2p leaves i, arc 2p + 1 leaves j
+        m_b = lay.sizes
+        P_b = np.diff(self.bp_ptr)
+        arc_tail = np.empty(2 * li.size, dtype=np.int64)
+        arc_tail[0::2] = li
+        arc_tail[1::2] = lj
+        arc_blk = np.repeat(kb, 2)
+        arc_local = np.arange(2 * li.size, dtype=np.int64) - 2 * np.repeat(self.bp_ptr[:-1], 2 * P_b)
+        order = np.lexsort((arc_local, arc_tail, arc_blk))
+        adj = arc_local[order].astype(np.int32)
+        counts = np.zeros(lay.M + lay.K, dtype=np.int64)   # per block m_b + 1 slots, slot 0 stays 0
+        ent_slot = arc_tail + lay.blk_ptr[arc_blk] + arc_blk + 1
+        np.add.at(counts, ent_slot, 1)
+        adj_off = np.zeros(lay.M + lay.K, dtype=np.int64)
+        for b in range(lay.K):   # per-block prefix sums (K small Python steps)
+            a0 = int(lay.blk_ptr[b]) + b
+            adj_off[a0:a0 + m_b[b] + 1] = np.cumsum(counts[a0:a0 + m_b[b] + 1])
+        self.adj_off_h, self.adj_h = adj_off.astype(np.int32), adj
         neg = np.flatnonzero(vals < 0)
         self.first_nonsubmodular = int(kb[neg[0]]) if neg.size else -1
         t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=self.device)
         self.d_bp_ptr, self.d_bp_i, self.d_bp_j, self.d_bp_w = (t(self.bp_ptr), t(self.bp_i), t(self.bp_j),
                                                                 t(vals))
+        self.d_adj_off = t(self.adj_off_h)
+        self.d_adj = t(self.adj_h) if self.adj_h.size else t(np.zeros(1, np.int32))
         self._ws = None
 
     def __len__(self) -> int:
@@ -382,7 +403,8 @@ class GraphProblems:
             _lib.check(lb.dope_bk_maxflow_batch(lay.K, lay.d_blk_ptr.data_ptr(), self.d_bp_ptr.data_ptr(),
                                                 ws_off.data_ptr(), lin.data_ptr(), pp(self.d_bp_i), pp(self.d_bp_j),
                                                 pp(caps), pp(caps), labels.data_ptr(), out.data_ptr(),
-                                                ws.data_ptr(), st), "dope_bk_maxflow_batch")
+                                                ws.data_ptr(), self.d_adj_off.data_ptr(), self.d_adj.data_ptr(),
+                                                st), "dope_bk_maxflow_batch")
         elif kind == "exhaustive":
             big = np.flatnonzero(lay.sizes > EXHAUSTIVE_MAX_VARS)
             if big.size:
