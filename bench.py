@@ -632,6 +632,19 @@ def main():
                       "call": "paper_1704_03116_b200.run(EnergyModel(u_host_f64, weights, lam), partition, "
                               "AdmmConfig(...)) -> (labels numpy, AdmmState with trace), synchronous"}
 
+    # quality of the answer (BASELINE configs[4]: final energy vs block size):
+    # the returned labeling's energy (best iterate) against the whole-grid
+    # serial min cut of compare mode (cli.py:95-100), both on the device
+    quality = None
+    if rank == 0 and ws == 1 and not args.sharded and len(wl.dims) == 2 and wl.integer:
+        import paper_1704_03116_b200 as dope
+        from paper_1704_03116_b200 import compare
+        e_best = float(rs.best_energy)
+        _, e_serial, _ = compare.run_serial(model, dope.GridShape(wl.dims))
+        quality = {"energy_returned": e_best, "best_iteration": int(rs.best_iteration),
+                   "serial_cut_energy": e_serial,
+                   "relative_energy_diff_pct": compare.relative_energy_diff(e_serial, e_best)}
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(wl, args.cpu_sample_iters)
@@ -663,6 +676,8 @@ def main():
             line["e2e"] = e2e
         if e2e_public:
             line["e2e_public_api"] = e2e_public
+        if quality:
+            line["config"]["quality"] = quality
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
