@@ -81,7 +81,8 @@ typedef struct dope_run_state {
     int32_t a_bound;            /* multiplier passes so far: an upper bound on
                                    |a| (int16 storage; the run loop stops with
                                    error -1 at 32000)                          */
-    int32_t reserved_;
+    int32_t generation;         /* runs begun on this state (dope_admm_init): the
+                                   peer-exchange epochs are generation-tagged */
 } dope_run_state;
 
 /* Length (int64 elements) of dope_lattice.part_cta. */
@@ -176,7 +177,30 @@ typedef struct dope_lattice {
     int64_t hash_base;
     int32_t shard_index;        /* sharded: this shard's slot in agg[]          */
     int32_t shard_count;        /* sharded: number of shards (slots in agg[])   */
+    const struct dope_peers *peers; /* peer-memory exchange (device pointer to a
+                                   dope_peers, see below), or NULL            */
 } dope_lattice;
+
+/* Peer-memory exchange of the sharded loop (no NCCL inside the run loop):
+ * the kernel that produces a halo row or an agg slot stores it straight into
+ * the neighbour / peer shards' memory (NVLink P2P stores across GPUs, plain
+ * stores between loopback shards) and raises an epoch flag there; the
+ * consumer waits on the flag.  K1's last CTA pushes the shard's boundary label
+ * rows, the consensus pass's last CTA pushes the agg slot (table halves
+ * alternate by iteration parity), dope_peer_install / dope_ghost_decide wait.
+ * Layout in each shard's halo buffer after the ghost multipliers: uint32
+ * flags [row from above, row from below, K1 done-counter, pad, agg-slot flag
+ * of every shard] (dope_halo_bytes counts them); agg[] holds 2 x 8 x
+ * shard_count int64 in peer mode. */
+#define DOPE_MAX_SHARDS 64
+typedef struct dope_peers {
+    uint8_t *row_to_up;         /* upper neighbour's "from below" halo slot, or NULL */
+    uint8_t *row_to_dn;         /* lower neighbour's "from above" halo slot, or NULL */
+    uint32_t *flag_to_up;       /* its row flag for that slot                  */
+    uint32_t *flag_to_dn;
+    int64_t *agg_of[DOPE_MAX_SHARDS];    /* every shard's agg table            */
+    uint32_t *aflag_of[DOPE_MAX_SHARDS]; /* every shard's agg-slot flags       */
+} dope_peers;
 
 /* Library / ABI identification; "b200-sm100a". */
 const char *dope_backend_name(void);
@@ -266,6 +290,23 @@ int dope_comm_init(int32_t rank, int32_t world, const uint8_t *id128, void **com
  * row travels by one cudaMemcpyAsync into the receiver's halo slot, each agg
  * slot by one copy into every peer's table; no kernel waits on another. */
 int dope_comm_loopback(int32_t world, void **comm_out);
+/* Loopback shards with the peer-memory exchange: builds each shard's
+ * dope_peers (device memory owned by the communicator) from the shards'
+ * halo / agg buffers and returns their device pointers in peers_out[world]
+ * (set shards[r]->peers = peers_out[r] before running). */
+int dope_comm_loopback_peer(int32_t world, const dope_lattice *const *shards, void **comm_out,
+                            void **peers_out);
+/* Multi-GPU peer-memory exchange over CUDA IPC: each rank allocates its halo
+ * and agg buffers with dope_peer_alloc (IPC needs allocation bases), exports
+ * their handles (dope_peer_export, 128 bytes), all-gathers them out of band
+ * (e.g. torch.distributed), and opens the others' (dope_comm_peer_init). */
+int dope_peer_alloc(int64_t bytes, void **ptr);
+int dope_peer_free(void *ptr);
+int dope_peer_export(const dope_lattice *L, uint8_t *out128);
+int dope_comm_peer_init(const dope_lattice *L, const uint8_t *all128, void **comm_out, void **peers_out);
+/* Peer mode, after K1: wait for the neighbours' boundary rows, install them
+ * in the ghost rows. */
+int dope_peer_install(const dope_lattice *L, void *stream);
 int dope_comm_destroy(void *comm);
 /* One shard (NCCL communicator: this rank's slab). */
 int dope_sharded_run(const dope_lattice *L, void *comm, int32_t iters, int32_t use_graph,

@@ -45,7 +45,7 @@ class RunState(C.Structure):
         ("energy_acc", C.c_int64),
         ("unary2", C.c_int64),
         ("a_bound", C.c_int32),
-        ("reserved_", C.c_int32),
+        ("generation", C.c_int32),
     ]
 
 
@@ -90,6 +90,7 @@ class Lattice(C.Structure):
         ("hash_base", C.c_int64),
         ("shard_index", C.c_int32),
         ("shard_count", C.c_int32),
+        ("peers", C.c_void_p),
     ]
 
 
@@ -239,6 +240,18 @@ def lib():
     lb.dope_sharded_run_group.argtypes = [PP, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
     lb.dope_sharded_finish_group.restype = C.c_int
     lb.dope_sharded_finish_group.argtypes = [PP, C.c_int32, C.c_void_p, C.c_void_p]
+    lb.dope_comm_loopback_peer.restype = C.c_int
+    lb.dope_comm_loopback_peer.argtypes = [C.c_int32, PP, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
+    lb.dope_peer_install.restype = C.c_int
+    lb.dope_peer_install.argtypes = [P, C.c_void_p]
+    lb.dope_peer_alloc.restype = C.c_int
+    lb.dope_peer_alloc.argtypes = [C.c_int64, C.POINTER(C.c_void_p)]
+    lb.dope_peer_free.restype = C.c_int
+    lb.dope_peer_free.argtypes = [C.c_void_p]
+    lb.dope_peer_export.restype = C.c_int
+    lb.dope_peer_export.argtypes = [P, C.c_void_p]
+    lb.dope_comm_peer_init.restype = C.c_int
+    lb.dope_comm_peer_init.argtypes = [P, C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
     lb.dope_halo_bytes.restype = C.c_int64
     lb.dope_halo_bytes.argtypes = [P]
     lb.dope_graph_cache_entries.restype = C.c_int64

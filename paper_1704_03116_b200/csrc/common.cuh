@@ -232,6 +232,20 @@ __device__ int bfs_relabel(const uint64_t *__restrict__ masks, uint64_t *__restr
 }
 
 // ---------------------------------------------------------------------------
+// Sharded mode: layout of a shard's halo buffer (dope_halo_bytes), U bytes per
+// exchanged row (2D) / plane (3D): [0, U) first local row out, [U, 2U) last
+// local row out, [2U, 3U) row received from above, [3U, 4U) from below, then
+// (8-byte aligned) the int16 multipliers of the ghost row above and below,
+// then (16-byte aligned) the peer-exchange flags: uint32 [row from above, row
+// from below, K1 done-counter, pad, agg-slot flag of every shard].
+// ---------------------------------------------------------------------------
+__host__ __device__ inline int64_t halo_ga_offset(int64_t U) { return (4 * U + 7) / 8 * 8; }
+__host__ __device__ inline int64_t halo_flag_offset(int64_t U) { return (halo_ga_offset(U) + 4 * U + 15) / 16 * 16; }
+__host__ __device__ inline int64_t halo_bytes(int64_t U, int64_t count) {
+    return halo_flag_offset(U) + 4 * (4 + (count > 0 ? count : 1));
+}
+
+// ---------------------------------------------------------------------------
 // Per-iteration state digest (test / audit mode: dope_lattice.trace_hash).
 // H_k = sum_g v_k(g) * mix64(3 (base + g) + k) mod 2^64 over the iteration's
 // labels (k = 0), 2y (k = 1) and multipliers (k = 2): order-independent, so

@@ -32,6 +32,7 @@
 #include <string>
 #include <vector>
 
+#include "common.cuh"
 #include "dope_b200.h"
 #include "graph_cache.cuh"
 
@@ -107,10 +108,23 @@ struct Halo {
     }
 };
 
+static uint32_t *halo_flags(const dope_lattice *L) {
+    return reinterpret_cast<uint32_t *>(static_cast<uint8_t *>(L->halo) + dope::halo_flag_offset((int64_t)unit_bytes(L)));
+}
+
 // How the shards of one grid talk.  `S` are the shards this process holds.
+// peer: the kernels move the halo rows and agg slots themselves through the
+// shards' dope_peers (K1's last CTA, the consensus pass's last CTA), the
+// consumers wait on flags -- move_rows / gather_agg are not called.
 struct Transport {
     int world = 1;
-    virtual ~Transport() {}
+    bool peer = false;
+    std::vector<void *> device_mem;   // dope_peers copies owned by this communicator
+    std::vector<void *> ipc_mem;      // opened IPC mappings
+    virtual ~Transport() {
+        for (void *p : device_mem) cudaFree(p);
+        for (void *p : ipc_mem) cudaIpcCloseMemHandle(p);
+    }
     // boundary label rows -> the neighbours' "from above / below" halo slots
     virtual int move_rows(const dope_lattice *const *S, int nloc, cudaStream_t s) = 0;
     // every shard's agg slot -> every table
@@ -183,8 +197,68 @@ struct LoopbackTransport : Transport {
     }
 };
 
+// The ranks of a multi-GPU run with the peer-memory exchange over CUDA IPC.
+struct PeerTransport : Transport {
+    int rank = 0;
+    int check_group(const dope_lattice *const *S, int nloc) const override {
+        return nloc == 1 && S[0]->shard_index == rank && S[0]->shard_count == world ? DOPE_OK : DOPE_E_ARGS;
+    }
+    int move_rows(const dope_lattice *const *, int, cudaStream_t) override { return DOPE_OK; }
+    int gather_agg(const dope_lattice *const *, int, cudaStream_t) override { return DOPE_OK; }
+};
+
+// dope_peers of shard r from the other shards' halo / agg base pointers
+static dope_peers peers_of(int r, int world, const std::vector<uint8_t *> &halo, const std::vector<int64_t *> &agg,
+                           size_t U) {
+    dope_peers p;
+    memset(&p, 0, sizeof(p));
+    const int64_t fo = dope::halo_flag_offset((int64_t)U);
+    auto flags = [&](int q) { return reinterpret_cast<uint32_t *>(halo[q] + fo); };
+    if (r > 0) {
+        p.row_to_up = halo[r - 1] + 3 * U;   // its "from below" slot
+        p.flag_to_up = flags(r - 1) + 1;
+    }
+    if (r + 1 < world) {
+        p.row_to_dn = halo[r + 1] + 2 * U;   // its "from above" slot
+        p.flag_to_dn = flags(r + 1) + 0;
+    }
+    for (int q = 0; q < world; ++q) {
+        p.agg_of[q] = agg[q];
+        p.aflag_of[q] = flags(q) + 4;
+    }
+    return p;
+}
+
+static int upload_peers(Transport &T, const dope_peers &p, void **out) {
+    void *d = nullptr;
+    if (cudaMalloc(&d, sizeof(dope_peers)) != cudaSuccess) return DOPE_E_CUDA;
+    if (cudaMemcpy(d, &p, sizeof(p), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        return DOPE_E_CUDA;
+    }
+    T.device_mem.push_back(d);
+    *out = d;
+    return DOPE_OK;
+}
+
 static int one_iteration(const dope_lattice *const *S, int nloc, Transport &T, cudaStream_t s) {
     int rc;
+    if (T.peer) {
+        // K1 pushes its boundary rows (last CTA), install waits for the
+        // neighbours', the consensus pass pushes its agg slot (last CTA),
+        // dope_ghost_decide waits for every slot -- no collective launches
+        for (int r = 0; r < nloc; ++r)
+            if ((rc = dope_update_blocks(S[r], s))) return rc;
+        for (int r = 0; r < nloc; ++r)
+            if ((rc = dope_peer_install(S[r], s))) return rc;
+        for (int r = 0; r < nloc; ++r)
+            if ((rc = dope_update_global(S[r], s))) return rc;
+        for (int r = 0; r < nloc; ++r)
+            if ((rc = dope_ghost_decide(S[r], s))) return rc;
+        for (int r = 0; r < nloc; ++r)
+            if ((rc = dope_trace_digest(S[r], s))) return rc;
+        return DOPE_OK;
+    }
     const bool exchange = T.world > 1;   // world size 1: no halo, no gather
     for (int r = 0; r < nloc; ++r)
         if ((rc = dope_update_blocks(S[r], s))) return rc;
@@ -223,6 +297,7 @@ static int check_shards(const dope_lattice *const *S, int nloc, const Transport 
     for (int r = 0; r < nloc; ++r) {
         const dope_lattice *L = S[r];
         if (!L || !L->halo || !L->agg || !L->sharded || !L->fuse_multipliers) return DOPE_E_ARGS;
+        if (T.peer != (L->peers != nullptr)) return DOPE_E_ARGS;
         int rc = dope_lattice_check(L);
         if (rc) return rc;
     }
@@ -270,6 +345,87 @@ int dope_comm_loopback(int32_t world, void **comm_out) {
     return DOPE_OK;
 }
 
+int dope_comm_loopback_peer(int32_t world, const dope_lattice *const *S, void **comm_out, void **peers_out) {
+    if (world < 1 || world > DOPE_MAX_SHARDS || !S || !comm_out || !peers_out) return DOPE_E_ARGS;
+    std::vector<uint8_t *> halo(world);
+    std::vector<int64_t *> agg(world);
+    for (int r = 0; r < world; ++r) {
+        if (!S[r] || !S[r]->halo || !S[r]->agg || S[r]->shard_index != r || S[r]->shard_count != world)
+            return DOPE_E_ARGS;
+        halo[r] = static_cast<uint8_t *>(S[r]->halo);
+        agg[r] = S[r]->agg;
+    }
+    LoopbackTransport *c = new LoopbackTransport();
+    c->world = world;
+    c->peer = true;
+    for (int r = 0; r < world; ++r) {
+        int rc = upload_peers(*c, peers_of(r, world, halo, agg, unit_bytes(S[r])), &peers_out[r]);
+        if (rc) {
+            delete c;
+            return rc;
+        }
+    }
+    *comm_out = static_cast<Transport *>(c);
+    return DOPE_OK;
+}
+
+int dope_peer_alloc(int64_t bytes, void **ptr) {
+    if (bytes <= 0 || !ptr) return DOPE_E_ARGS;
+    if (cudaMalloc(ptr, (size_t)bytes) != cudaSuccess) return DOPE_E_CUDA;
+    return cudaMemset(*ptr, 0, (size_t)bytes) == cudaSuccess ? DOPE_OK : DOPE_E_CUDA;
+}
+
+int dope_peer_free(void *ptr) { return cudaFree(ptr) == cudaSuccess ? DOPE_OK : DOPE_E_CUDA; }
+
+int dope_peer_export(const dope_lattice *L, uint8_t *out128) {
+    if (!L || !L->halo || !L->agg || !out128) return DOPE_E_ARGS;
+    cudaIpcMemHandle_t h[2];
+    if (cudaIpcGetMemHandle(&h[0], L->halo) != cudaSuccess) return DOPE_E_CUDA;
+    if (cudaIpcGetMemHandle(&h[1], L->agg) != cudaSuccess) return DOPE_E_CUDA;
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    memcpy(out128, h, 128);
+    return DOPE_OK;
+}
+
+int dope_comm_peer_init(const dope_lattice *L, const uint8_t *all128, void **comm_out, void **peers_out) {
+    if (!L || !all128 || !comm_out || !peers_out || !L->halo || !L->agg) return DOPE_E_ARGS;
+    const int world = L->shard_count, rank = L->shard_index;
+    if (world < 1 || world > DOPE_MAX_SHARDS || rank < 0 || rank >= world) return DOPE_E_ARGS;
+    PeerTransport *c = new PeerTransport();
+    c->world = world;
+    c->rank = rank;
+    c->peer = true;
+    std::vector<uint8_t *> halo(world);
+    std::vector<int64_t *> agg(world);
+    for (int q = 0; q < world; ++q) {
+        if (q == rank) {
+            halo[q] = static_cast<uint8_t *>(L->halo);
+            agg[q] = L->agg;
+            continue;
+        }
+        cudaIpcMemHandle_t h[2];
+        memcpy(h, all128 + (size_t)128 * q, 128);
+        void *ph = nullptr, *pa = nullptr;
+        if (cudaIpcOpenMemHandle(&ph, h[0], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+            cudaIpcOpenMemHandle(&pa, h[1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            if (ph) cudaIpcCloseMemHandle(ph);
+            delete c;
+            return DOPE_E_CUDA;
+        }
+        c->ipc_mem.push_back(ph);
+        c->ipc_mem.push_back(pa);
+        halo[q] = static_cast<uint8_t *>(ph);
+        agg[q] = static_cast<int64_t *>(pa);
+    }
+    int rc = upload_peers(*c, peers_of(rank, world, halo, agg, unit_bytes(L)), peers_out);
+    if (rc) {
+        delete c;
+        return rc;
+    }
+    *comm_out = static_cast<Transport *>(c);
+    return DOPE_OK;
+}
+
 int dope_comm_destroy(void *comm) {
     if (!comm) return DOPE_OK;
     Transport *t = static_cast<Transport *>(comm);
@@ -307,8 +463,10 @@ int dope_sharded_run_group(const dope_lattice *const *S, int32_t nloc, void *com
         // first iteration overwrites before reading.
         for (int r = 0; r < nloc; ++r)
             if ((rc = dope_prepare_kernels(S[r]))) return rc;
-        if ((rc = T.move_rows(S, nloc, s))) return rc;
-        if ((rc = T.gather_agg(S, nloc, s))) return rc;
+        if (!T.peer) {
+            if ((rc = T.move_rows(S, nloc, s))) return rc;
+            if ((rc = T.gather_agg(S, nloc, s))) return rc;
+        }
         cudaStream_t cs;
         if ((rc = cu(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)))) return rc;
         cudaGraph_t graph;
@@ -337,8 +495,8 @@ int dope_sharded_finish_group(const dope_lattice *const *S, int32_t nloc, void *
     int rc = check_shards(S, nloc, T);
     if (rc) return rc;
     for (int r = 0; r < nloc; ++r)
-        if ((rc = dope_energy_local(S[r], s))) return rc;   // -> agg slot [5]
-    if ((rc = T.gather_agg(S, nloc, s))) return rc;
+        if ((rc = dope_energy_local(S[r], s))) return rc;   // -> agg slot [5] (peer mode: pushed)
+    if (!T.peer && (rc = T.gather_agg(S, nloc, s))) return rc;
     for (int r = 0; r < nloc; ++r)
         if ((rc = dope_finish_decide(S[r], s))) return rc;
     return DOPE_OK;

@@ -87,7 +87,29 @@ struct Lat2 {
     int32_t shard_index, shard_count;   // sharded: this shard's slot in the agg table
     astore_t *ga_up, *ga_dn;            // sharded: multipliers of the ghost rows / planes
     uint32_t *dlist;        // run loop: two dirty-block worklists (dirty_list), else null
+    const dope_peers *peers;  // peer-memory exchange (sharded), else null
+    uint32_t *pflags;       // peer mode: this shard's flags [row from above, row from below,
+                            // K1 done-counter, pad, agg-slot flag per shard]
 };
+
+// ---------------------------------------------------------------------------
+// Peer-memory exchange (dope_peers): system-scope release / acquire flags.
+// Epochs carry the run generation so flags left by an earlier run never match.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_flag(const uint32_t *p, uint32_t v) {
+    while (ld_acquire_sys(p) != v) __nanosleep(100);
+}
+__device__ __forceinline__ uint32_t peer_epoch(const dope_run_state *st, uint32_t step) {
+    return ((uint32_t)st->generation << 16) + step;
+}
 
 // Dirty-block worklists of the run loop (dirty[9K, 11K + 2)): list p = [count,
 // K entries]; the consensus pass of iteration t appends every block it marks
@@ -113,12 +135,8 @@ __device__ __forceinline__ void mark_dirty(const Lat2 &L, int64_t k) {
     }
 }
 
-// Sharded mode: layout of the caller's halo buffer (dope_halo_bytes), U bytes
-// per exchanged row (2D) / plane (3D): [0, U) first local row out, [U, 2U) last
-// local row out, [2U, 3U) row received from above, [3U, 4U) from below, then
-// (8-byte aligned) the int16 multipliers of the ghost row above and below.
-__host__ __device__ inline int64_t halo_ga_offset(int64_t U) { return (4 * U + 7) / 8 * 8; }
-__host__ __device__ inline int64_t halo_bytes(int64_t U) { return halo_ga_offset(U) + 4 * U; }
+// Sharded mode: the halo buffer's layout is in common.cuh (halo_bytes).
+
 
 // agg table of the sharded run loop: AGG_SLOT int64 per shard, filled by each
 // shard's consensus pass (and end-of-run energy), gathered across shards
@@ -126,6 +144,37 @@ __host__ __device__ inline int64_t halo_bytes(int64_t U) { return halo_ga_offset
 // the residual excesses (rsq_excess), [3] max block ss, [4] clamp flag,
 // [5] end-of-run energy of the last iterate.
 constexpr int AGG_SLOT = 8;
+
+// Peer mode, every K1 CTA on its way out (CTA-uniform call): the last CTA of
+// the grid pushes this shard's first / last row of labels into the
+// neighbours' halo slots and raises their row flags (epoch = this iteration).
+__device__ __noinline__ void k1_peer_exit(const Lat2 &L) {
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&L.pflags[2], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const dope_peers *pr = L.peers;
+    uint8_t *up = pr->row_to_up, *dn = pr->row_to_dn;
+    const int64_t P = L.ndim == 3 ? (int64_t)L.ay.dim * L.W : (int64_t)L.W;
+    const int64_t lastoff = ((L.ndim == 3 ? (int64_t)L.az.dim : (int64_t)L.ay.dim) - 1) * P;
+    for (int64_t c = threadIdx.x; c < P; c += blockDim.x) {
+        if (up) up[c] = L.yhat[c];
+        if (dn) dn[c] = L.yhat[lastoff + c];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const uint32_t ep = peer_epoch(L.st, (uint32_t)L.st->iteration + 1u);
+        if (up) st_release_sys(pr->flag_to_up, ep);
+        if (dn) st_release_sys(pr->flag_to_dn, ep);
+        L.pflags[2] = 0u;
+    }
+}
 
 // Append block k to the solved-block list (see solved_list); dirty[8K + k] =
 // 1 + the block's latest slot.
@@ -217,7 +266,10 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         const uint32_t *lst = dirty_list(L, it);
         if (blockIdx.x == 0 && tid == 0) dirty_list(L, it + 1)[0] = 0u;   // the next pass fills it
         const uint32_t cnt = lst[0], ent = lst[1 + (blockIdx.x < (unsigned)L.K ? blockIdx.x : 0)];
-        if (stop || blockIdx.x >= cnt) return;
+        if (stop || blockIdx.x >= cnt) {
+            if (L.peers) k1_peer_exit(L);
+            return;
+        }
         k = (int)ent;
         DOPE_ASSERT(cnt <= (uint32_t)L.K && k >= 0 && k < L.K);
     } else {
@@ -227,7 +279,10 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         const int stop = L.st->stop;
         ycur = L.st->ycur;
         const uint32_t dk = L.skip_clean ? L.dirty[k] : 1u;
-        if (stop || dk == 0) return;
+        if (stop || dk == 0) {
+            if (L.peers) k1_peer_exit(L);
+            return;
+        }
     }
     __syncthreads();
     if (tid == 0) {
@@ -553,6 +608,7 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         atomicAdd((unsigned long long *)&L.st->sweeps, (unsigned long long)sweeps_done);
         atomicMax(&L.st->max_rounds_seen, rounds);
     }
+    if (L.peers) k1_peer_exit(L);
 }
 
 // cold residual graphs for every block (warm-start initial state)
@@ -649,6 +705,7 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
         dope_run_state s;
         memset(&s, 0, sizeof(s));
         s.best_energy = INT64_MAX;
+        s.generation = L.st->generation + 1;   // tags this run's peer-exchange epochs
         *L.st = s;
     }
 }
@@ -762,6 +819,34 @@ __device__ __forceinline__ double rsq_total(int64_t sum_ss, int64_t sum_excess) 
     return (double)sum_ss + (double)sum_excess * 0x1p-53;
 }
 
+// The agg table the sharded loop uses for iteration `it`: peer mode alternates
+// two halves by parity (a shard can be one iteration ahead of another and
+// already pushing its next slot), the gather modes use the first.
+__device__ __forceinline__ int64_t *agg_table(const Lat2 &L, int it) {
+    return L.agg + (L.peers ? (size_t)(it & 1) * AGG_SLOT * L.shard_count : 0);
+}
+
+// Peer mode: this shard's slot into every other shard's table (same half),
+// then their flags for it.  One thread.
+__device__ void push_agg_slot(const Lat2 &L, int it, const int64_t *slot, uint32_t ep) {
+    const dope_peers *pr = L.peers;
+    const size_t off = (size_t)(it & 1) * AGG_SLOT * L.shard_count + (size_t)AGG_SLOT * L.shard_index;
+    for (int r = 0; r < L.shard_count; ++r) {
+        if (r == L.shard_index) continue;
+        int64_t *dst = pr->agg_of[r] + off;
+        for (int i = 0; i < AGG_SLOT; ++i) dst[i] = slot[i];
+    }
+    __threadfence_system();
+    for (int r = 0; r < L.shard_count; ++r)
+        if (r != L.shard_index) st_release_sys(pr->aflag_of[r] + L.shard_index, ep);
+}
+
+// Peer mode: wait until every other shard's slot for this epoch has arrived.
+__device__ void wait_agg_slots(const Lat2 &L, uint32_t ep) {
+    for (int r = 0; r < L.shard_count; ++r)
+        if (r != L.shard_index) wait_flag(L.pflags + 4 + r, ep);
+}
+
 // Apply one consensus pass's global aggregates (pair energy E of y_{t-1},
 // unary change U, residual sum R2, max block residual^2 M2, clamp flag F):
 // run-loop decision, or -- when sharded -- publish them for the cross-rank
@@ -777,12 +862,13 @@ __device__ void finalize_apply(const Lat2 &L, dope_run_state s0, int64_t E2, int
         st->ybest = best_idx;
         st->ycur = out;
     } else if (L.sharded) {          // this shard's slot of the agg table; dope_decide reduces
-        int64_t *slot = L.agg + (size_t)AGG_SLOT * L.shard_index;
+        int64_t *slot = agg_table(L, s0.iteration) + (size_t)AGG_SLOT * L.shard_index;
         slot[0] = E2;
         slot[1] = S2;
         slot[2] = X2;
         slot[3] = M2;
         slot[4] = F2;
+        if (L.peers) push_agg_slot(L, s0.iteration, slot, peer_epoch(L.st, (uint32_t)s0.iteration + 1u));
     } else {
         apply_iteration(L, s0, E2, rsq_total(S2, X2), M2, F2, cur, best_idx, out);
     }
@@ -796,10 +882,12 @@ __device__ void decide_apply(const Lat2 &L) {
     dope_run_state *st = L.st;
     const int cur = st->ycur, best = st->ybest;
     const dope_run_state s0 = *st;
+    if (L.peers) wait_agg_slots(L, peer_epoch(st, (uint32_t)s0.iteration + 1u));
+    const int64_t *table = agg_table(L, s0.iteration);
     int64_t E = 0, S = 0, X = 0, M = -1;
     int F = 0;
     for (int r = 0; r < L.shard_count; ++r) {
-        const int64_t *slot = L.agg + (size_t)AGG_SLOT * r;
+        const int64_t *slot = table + (size_t)AGG_SLOT * r;
         E += slot[0];
         S += slot[1];
         X += slot[2];
@@ -908,6 +996,31 @@ __global__ void k_rebuild_dlist(Lat2 L) {
         if (L.dirty[k]) cur[1 + atomicAdd(cur, 1u)] = (uint32_t)k;
 }
 
+// Peer mode, after K1: wait for the neighbours' boundary rows of this
+// iteration (their K1's last CTA raised the flags) and install them in the
+// ghost rows / planes.  One CTA.
+__global__ void k_peer_install(Lat2 L) {
+    dope_run_state *st = L.st;
+    if (st->stop) return;
+    const bool is3 = L.ndim == 3;
+    const bool up = is3 ? L.gzu : L.gup, dn = is3 ? L.gzd : L.gdn;
+    const int64_t P = is3 ? (int64_t)L.ay.dim * L.W : (int64_t)L.W;
+    const int64_t below = (is3 ? (int64_t)L.az.dim : (int64_t)L.ay.dim) * P;
+    if (threadIdx.x == 0) {
+        const uint32_t ep = peer_epoch(st, (uint32_t)st->iteration + 1u);
+        if (up) wait_flag(L.pflags + 0, ep);
+        if (dn) wait_flag(L.pflags + 1, ep);
+    }
+    __syncthreads();
+    // halo slots: [2U, 3U) from above, [3U, 4U) from below (dope_halo_bytes)
+    const uint8_t *from_up = reinterpret_cast<const uint8_t *>(L.ga_up) - halo_ga_offset(P) + 2 * P;
+    const uint8_t *from_dn = from_up + P;
+    for (int64_t c = threadIdx.x; c < P; c += blockDim.x) {
+        if (up) L.yhat[c - P] = from_up[c];
+        if (dn) L.yhat[below + c] = from_dn[c];
+    }
+}
+
 // The integer path's unary from the caller's float64 vector (the reference's
 // EnergyModel.unary): exact integers within +-2^28, else *bad = 1.
 __global__ void k_unary_i32(const double *__restrict__ u, int64_t n, int32_t *__restrict__ out, int32_t *bad) {
@@ -925,8 +1038,10 @@ __global__ void k_unary_i32(const double *__restrict__ u, int64_t n, int32_t *__
 // its agg slot (the cross-shard sum happens in k_finish_decide).
 __global__ void k_publish_energy(Lat2 L) {
     dope_run_state *st = L.st;
-    L.agg[(size_t)AGG_SLOT * L.shard_index + 5] = st->energy_acc;
+    int64_t *slot = agg_table(L, st->iteration) + (size_t)AGG_SLOT * L.shard_index;
+    slot[5] = st->energy_acc;
     st->energy_acc = 0;
+    if (L.peers) push_agg_slot(L, st->iteration, slot, peer_epoch(st, 0x8000u + (uint32_t)st->iteration));
 }
 
 // Sharded mode: copy this shard's first and last local rows (labels or the
@@ -1531,8 +1646,10 @@ __global__ void k_finish_decide(Lat2 L) {
     if (T >= 1 && !st->error) {
         int64_t E = st->energy_acc;
         if (L.sharded) {   // the gathered end-of-run energies of every shard
+            if (L.peers) wait_agg_slots(L, peer_epoch(st, 0x8000u + (uint32_t)T));
+            const int64_t *table = agg_table(L, T);
             E = 0;
-            for (int r = 0; r < L.shard_count; ++r) E += L.agg[(size_t)AGG_SLOT * r + 5];
+            for (int r = 0; r < L.shard_count; ++r) E += table[(size_t)AGG_SLOT * r + 5];
         }
         if (T - 1 < L.max_iters) L.tr_e[T - 1] = E;
         if (E < st->best_energy) {
@@ -1752,6 +1869,11 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
         uint8_t *h = static_cast<uint8_t *>(L->halo);
         o.ga_up = reinterpret_cast<astore_t *>(h + halo_ga_offset(U));
         o.ga_dn = o.ga_up + U;
+        o.pflags = reinterpret_cast<uint32_t *>(h + halo_flag_offset(U));
+        if (L->peers) {
+            if (L->shard_count > DOPE_MAX_SHARDS) return DOPE_E_ARGS;
+            o.peers = L->peers;
+        }
     }
     if (o.sharded && (!o.agg || (is3 ? o.az.rem != 0 : o.ay.rem != 0))) return DOPE_E_ARGS;
     const int maxd = o.az.base + (o.az.rem ? 1 : 0);
@@ -2320,7 +2442,7 @@ int dope_energy_local(const dope_lattice *L, void *stream) {
 
 int64_t dope_halo_bytes(const dope_lattice *L) {
     if (!L || (L->ndim != 2 && L->ndim != 3)) return 0;
-    return halo_bytes(L->ndim == 3 ? L->dims[1] * L->dims[2] : L->dims[1]);
+    return halo_bytes(L->ndim == 3 ? L->dims[1] * L->dims[2] : L->dims[1], L->shard_count);
 }
 
 int dope_ghost_consensus(const dope_lattice *L, void *stream) {
@@ -2362,6 +2484,15 @@ int dope_ghost_decide(const dope_lattice *L, void *stream) {
     const int64_t unit = P.o.ndim == 3 ? (int64_t)P.o.ay.dim * P.o.W : (int64_t)P.o.W;
     k_ghost_decide<<<ghosts ? grid_for(unit) : 1, 256, 0, (cudaStream_t)stream>>>(P.o);
     return cuda_check(cudaGetLastError(), "ghost_decide");
+}
+
+int dope_peer_install(const dope_lattice *L, void *stream) {
+    Plan P;
+    int rc = build_plan(L, P);
+    if (rc) return rc;
+    if (!P.o.peers || !P.o.ga_up) return DOPE_E_ARGS;
+    k_peer_install<<<1, 256, 0, (cudaStream_t)stream>>>(P.o);
+    return cuda_check(cudaGetLastError(), "peer_install");
 }
 
 int dope_trace_digest(const dope_lattice *L, void *stream) {

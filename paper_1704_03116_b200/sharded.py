@@ -88,7 +88,7 @@ class GpuShard:
 
     def __init__(self, full: LatticeLowering, kb0: int, kb1: int, mu: int, eps: float,
                  max_iters: int, warm_start: bool = True, skip_clean: bool = True,
-                 index: int = 0, count: int = 1, digests: bool = False):
+                 index: int = 0, count: int = 1, digests: bool = False, ipc: bool = False):
         import torch
         dims, kpa = tuple(full.dims), tuple(full.kpa)
         n0, k0 = dims[0], kpa[0]   # the sharded axis: rows (2D) / planes (3D)
@@ -115,11 +115,22 @@ class GpuShard:
         L.shard_index, L.shard_count = index, count
         self.unit = int(np.prod(dims[1:]))   # pixels per row (2D) / plane (3D)
         L.hash_base = self.r0 * self.unit
-        self.agg = torch.zeros(AGG_SLOT * count, dtype=torch.int64, device=dev)
-        L.agg = self.agg.data_ptr()
         lb = _lib.lib()
-        self.halo = torch.zeros(int(lb.dope_halo_bytes(C.byref(L))), dtype=torch.uint8, device=dev)
-        L.halo = self.halo.data_ptr()
+        halo_bytes = int(lb.dope_halo_bytes(C.byref(L)))
+        agg_bytes = 2 * AGG_SLOT * count * 8     # two parity halves (peer mode alternates them)
+        self._raw = []
+        if ipc:   # CUDA IPC needs allocation bases: the library allocates them
+            self.halo = self.agg = None
+            for nbytes, field in ((halo_bytes, "halo"), (agg_bytes, "agg")):
+                ptr = C.c_void_p()
+                _lib.check(lb.dope_peer_alloc(nbytes, C.byref(ptr)), "dope_peer_alloc")
+                self._raw.append(ptr)
+                setattr(L, field, ptr.value)
+        else:
+            self.agg = torch.zeros(2 * AGG_SLOT * count, dtype=torch.int64, device=dev)
+            L.agg = self.agg.data_ptr()
+            self.halo = torch.zeros(halo_bytes, dtype=torch.uint8, device=dev)
+            L.halo = self.halo.data_ptr()
         _lib.check(lb.dope_lattice_check(C.byref(L)), "dope_lattice_check (shard)")
 
     # -- step interface (run_shards) -----------------------------------------
@@ -167,6 +178,10 @@ class GpuShard:
     def labels(self):
         return self.dev.binarize()
 
+    def __del__(self):
+        for ptr in getattr(self, "_raw", []):
+            _lib.lib().dope_peer_free(ptr)
+
     def digests(self):
         """Per-iteration (yhat, 2y, a) digests of this slab (global index base)."""
         it = self.dev.run_state().iteration
@@ -201,7 +216,7 @@ class DistComm:
     def gather_agg(self, shards):
         import torch
         (s,) = shards
-        table = s.agg.view(self.world, AGG_SLOT)
+        table = s.agg[:AGG_SLOT * self.world].view(self.world, AGG_SLOT)   # the first half
         mine = table[self.rank].clone()
         parts = [torch.empty_like(mine) for _ in range(self.world)]
         self.dist.all_gather(parts, mine, group=self.group)
@@ -238,15 +253,24 @@ class LoopbackGroup:
     """All G shards of one grid in this process, on this GPU, run by the C++
     loopback communicator: the same iteration and graph capture as NCCL, each
     halo row moved by one cudaMemcpyAsync, each agg slot copied into every
-    peer table."""
+    peer table -- or, with peer=True, the peer-memory exchange: the kernels
+    store the rows and slots into the other shards' buffers themselves and
+    wait on epoch flags (the multi-GPU IPC design, on one device)."""
 
-    def __init__(self, shards):
+    def __init__(self, shards, peer: bool = False):
         self.shards = list(shards)
         self.handle = C.c_void_p()
-        _lib.check(_lib.lib().dope_comm_loopback(len(self.shards), C.byref(self.handle)),
-                   "dope_comm_loopback")
         self._arr = (C.POINTER(_lib.Lattice) * len(self.shards))(
             *[C.pointer(s.dev.L) for s in self.shards])
+        if peer:
+            peers = (C.c_void_p * len(self.shards))()
+            _lib.check(_lib.lib().dope_comm_loopback_peer(len(self.shards), self._arr, C.byref(self.handle),
+                                                          peers), "dope_comm_loopback_peer")
+            for s, p in zip(self.shards, peers):
+                s.dev.L.peers = p
+        else:
+            _lib.check(_lib.lib().dope_comm_loopback(len(self.shards), C.byref(self.handle)),
+                       "dope_comm_loopback")
 
     def run(self, iters: int, use_graph: bool = True):
         lb = _lib.lib()
@@ -275,12 +299,13 @@ def _make_shards(model: EnergyModel, partition: Partition, config: AdmmConfig, w
 
 
 def run_virtual(model: EnergyModel, partition: Partition, config: AdmmConfig, shards: int,
-                use_graph: bool = True, digests: bool = False):
-    """`run` with the sub-regions sharded over `shards` loopback ranks on this GPU.
+                use_graph: bool = True, digests: bool = False, peer: bool = False):
+    """`run` with the sub-regions sharded over `shards` loopback ranks on this GPU
+    (peer: the peer-memory exchange instead of copies between kernels).
 
     Returns (labels, trace, state_fields) assembled from the shards."""
     sh = _make_shards(model, partition, config, shards, range(shards), digests)
-    group = LoopbackGroup(sh)
+    group = LoopbackGroup(sh, peer=peer)
     try:
         group.run(config.max_iters, use_graph)
         out = collect(sh, config.resolved_mu0(partition.shape.ndim), config)
@@ -345,6 +370,37 @@ class NcclComm:
             self.handle = C.c_void_p()
 
 
+class IpcPeerComm:
+    """Peer-memory exchange across GPUs (one shard per rank): the shard's halo
+    and agg buffers come from dope_peer_alloc, their CUDA IPC handles are
+    all-gathered over torch.distributed, every rank opens the others' and the
+    run loop's kernels store halo rows / agg slots into peer memory directly
+    (DESIGN.md §7).  Use with shard_for_rank(..., cls=NcclShard, ipc=True)."""
+
+    def __init__(self, shard: "GpuShard", group=None):
+        import torch.distributed as dist
+        lb = _lib.lib()
+        L = shard.dev.L
+        mine = (C.c_uint8 * 128)()
+        _lib.check(lb.dope_peer_export(C.byref(L), mine), "dope_peer_export")
+        world = L.shard_count
+        allh = [bytes(mine)]
+        if world > 1:
+            allh = [None] * world
+            dist.all_gather_object(allh, bytes(mine), group=group)
+        buf = (C.c_uint8 * (128 * world))(*b"".join(allh))
+        self.handle = C.c_void_p()
+        peers = C.c_void_p()
+        _lib.check(lb.dope_comm_peer_init(C.byref(L), buf, C.byref(self.handle), C.byref(peers)),
+                   "dope_comm_peer_init")
+        L.peers = peers.value
+
+    def close(self):
+        if self.handle:
+            _lib.lib().dope_comm_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+
 class NcclShard(GpuShard):
     """A GpuShard whose whole run loop (NCCL halo and gather included) is one CUDA graph."""
 
@@ -358,9 +414,9 @@ class NcclShard(GpuShard):
 
 
 def shard_for_rank(model: EnergyModel, partition: Partition, config: AdmmConfig, rank: int,
-                   world: int, cls=NcclShard):
+                   world: int, cls=NcclShard, ipc: bool = False):
     full = lower_lattice(model, partition)
     mu = _check_config(full, config)
     kb0, kb1 = shard_block_rows(full.kpa[0], world)[rank]
     return cls(full, kb0, kb1, mu, config.resolved_eps(partition), config.max_iters,
-               config.warm_start, config.skip_clean, index=rank, count=world)
+               config.warm_start, config.skip_clean, index=rank, count=world, ipc=ipc)

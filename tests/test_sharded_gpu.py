@@ -59,27 +59,31 @@ def test_loopback_shards_match_reference_c1(shards):
     assert np.array_equal(st["a"], g["a"])
 
 
-@pytest.mark.parametrize("size,block,shards,graph", [(1024, 64, 4, True), (1024, 64, 16, True),
-                                                      (512, 128, 4, True), (1024, 64, 8, False)])
-def test_loopback_shards_match_single_gpu(size, block, shards, graph):
+@pytest.mark.parametrize("size,block,shards,graph,peer", [(1024, 64, 4, True, False), (1024, 64, 16, True, False),
+                                                           (512, 128, 4, True, False), (1024, 64, 8, False, False),
+                                                           (1024, 64, 4, True, True), (1024, 64, 16, True, True),
+                                                           (512, 128, 4, False, True)])
+def test_loopback_shards_match_single_gpu(size, block, shards, graph, peer):
     wl = W.disks_workload("s", size, 16, block, 2, 30, rmin=10, rmax=150, seed=3)
     model, part = _model(wl)
     cfg = dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=wl.iters)
     labels1, s1 = dope.run(model, part, cfg)
-    labels, trace, st = sharded.run_virtual(model, part, cfg, shards, use_graph=graph)
+    labels, trace, st = sharded.run_virtual(model, part, cfg, shards, use_graph=graph, peer=peer)
     _same_run(trace, st, labels, s1, labels1)
 
 
-@pytest.mark.parametrize("name,shards", [("C3", 2), ("C3", 4), ("C3", 8), ("C5-B64", 8),
-                                         ("C4", 2), ("C4", 4), ("C4", 8)])
-def test_loopback_full_size_matches_fixture_every_iteration(name, shards):
-    """BASELINE configs at full size and full length, sharded G ways: the summed
-    per-shard digests equal the oracle's every iteration."""
+@pytest.mark.parametrize("name,shards,peer", [("C3", 2, False), ("C3", 4, False), ("C3", 8, False),
+                                              ("C5-B64", 8, False), ("C4", 2, False), ("C4", 4, False),
+                                              ("C4", 8, False), ("C3", 8, True), ("C4", 8, True)])
+def test_loopback_full_size_matches_fixture_every_iteration(name, shards, peer):
+    """BASELINE configs at full size and full length, sharded G ways (copies
+    between kernels, or the peer-memory exchange): the summed per-shard digests
+    equal the oracle's every iteration."""
     g = load_golden(f"full_{name.lower()}.npz")
     wl = W.by_name(name)
     model, part = _model(wl)
     cfg = dope.AdmmConfig(mu0=wl.rho, mu_fact=1.0, eps=0.0, max_iters=wl.iters)
-    labels, trace, st = sharded.run_virtual(model, part, cfg, shards, digests=True)
+    labels, trace, st = sharded.run_virtual(model, part, cfg, shards, digests=True, peer=peer)
     it = int(g["iterations"])
     assert st["iterations"] == it
     assert st["best_iteration"] == int(g["best_iteration"])
@@ -91,14 +95,15 @@ def test_loopback_full_size_matches_fixture_every_iteration(name, shards):
     assert not bad, f"digests differ at iterations {bad[:10]}"
 
 
-@pytest.mark.parametrize("size,block,shards", [(96, 32, 3), (128, 32, 2), (64, 16, 4)])
-def test_loopback_3d_shards_match_single_gpu(size, block, shards):
+@pytest.mark.parametrize("size,block,shards,peer", [(96, 32, 3, False), (128, 32, 2, False), (64, 16, 4, False),
+                                                    (96, 32, 3, True), (64, 16, 4, True)])
+def test_loopback_3d_shards_match_single_gpu(size, block, shards, peer):
     """3D: slabs of block planes with ghost planes (C4's multi-GPU layout)."""
     wl = W.c4(seed=4, size=size, block=block, iters=20)
     model, part = _model(wl)
     cfg = dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=wl.iters)
     labels1, s1 = dope.run(model, part, cfg)
-    labels, trace, st = sharded.run_virtual(model, part, cfg, shards)
+    labels, trace, st = sharded.run_virtual(model, part, cfg, shards, peer=peer)
     _same_run(trace, st, labels, s1, labels1)
 
 
@@ -124,6 +129,23 @@ def test_nccl_single_rank_graph_matches_single_gpu(three_d):
     comm = sharded.NcclComm(0, 1)
     try:
         sh = sharded.shard_for_rank(model, part, cfg, 0, 1)
+        sh.run(comm, cfg.max_iters, use_graph=True)
+        labels, trace, st = sharded.collect([sh], 1.0, cfg)
+    finally:
+        comm.close()
+    _same_run(trace, st, labels, s1, labels1)
+
+
+def test_ipc_peer_comm_single_rank_matches_single_gpu():
+    """The multi-GPU peer-memory transport (CUDA IPC handles, library-owned
+    buffers) at world size 1: export / init path and the peer-mode loop."""
+    wl = W.mini_disks(256, 64, 8, 2, 20, seed=5)
+    model, part = _model(wl)
+    cfg = dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=wl.iters)
+    labels1, s1 = dope.run(model, part, cfg)
+    sh = sharded.shard_for_rank(model, part, cfg, 0, 1, ipc=True)
+    comm = sharded.IpcPeerComm(sh)
+    try:
         sh.run(comm, cfg.max_iters, use_graph=True)
         labels, trace, st = sharded.collect([sh], 1.0, cfg)
     finally:
