@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-graph", action="store_true")
     p.add_argument("--sharded", action="store_true",
                    help="use the NCCL-sharded run loop even on one GPU (path check)")
+    p.add_argument("--peer", action="store_true",
+                   help="sharded loop with the peer-memory exchange (CUDA IPC) instead of NCCL")
     return p.parse_args()
 
 
@@ -382,6 +384,8 @@ def main():
         return run_general_bench(args, wl)
     iters = args.iters or wl.iters
     use_graph = int(not args.no_graph)
+    if args.peer:
+        args.sharded = True
     if ws == 1 and not args.sharded:
         model, part, problems = build_problem(wl, torch.device("cuda", local))
         dev = make_device_state(problems, wl.rho, 0.0, iters, True, True)
@@ -401,8 +405,12 @@ def main():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29533")
             dist.init_process_group("nccl", rank=0, world_size=1)
-        comm = sharded.NcclComm(rank, ws)
-        shard = sharded.shard_for_rank(model, part, cfg, rank, ws)
+        if args.peer:
+            shard = sharded.shard_for_rank(model, part, cfg, rank, ws, ipc=True)
+            comm = sharded.IpcPeerComm(shard)
+        else:
+            comm = sharded.NcclComm(rank, ws)
+            shard = sharded.shard_for_rank(model, part, cfg, rank, ws)
         dev = shard.dev
         problems = shard.problems
 
@@ -663,9 +671,12 @@ def main():
                        "pixel_edges_per_s": value * wl.num_pairs,
                        "l2": ("inputs larger than L2 (state > 126 MB)" if wl.n * 21 > 126e6 else
                               "state fits in the 126 MB L2 (small config; no flush between steps)"),
-                       "parallelism": (f"{ws} GPUs: block {'planes' if len(wl.dims) == 3 else 'rows'} "
-                                       f"sharded in slabs, NCCL halo {'planes' if len(wl.dims) == 3 else 'rows'}"
-                                       f" + 4-scalar all-reduce per iteration" if ws > 1 else "1 GPU"),
+                       "parallelism": (f"{ws} GPU(s): block {'planes' if len(wl.dims) == 3 else 'rows'} "
+                                       f"sharded in slabs; per iteration one label-halo exchange and one "
+                                       f"64-byte agg gather "
+                                       + ("by peer-memory stores inside the kernels (CUDA IPC)" if args.peer
+                                          else "over NCCL") + ", captured in one CUDA graph"
+                                       if (ws > 1 or args.sharded) else "1 GPU"),
                        "block_solves_per_run": solves_per_run,
                        "push_relabel_sweeps_per_run": sweeps_per_run,
                        "kernels": kstat},

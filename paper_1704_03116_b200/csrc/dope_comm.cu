@@ -108,9 +108,6 @@ struct Halo {
     }
 };
 
-static uint32_t *halo_flags(const dope_lattice *L) {
-    return reinterpret_cast<uint32_t *>(static_cast<uint8_t *>(L->halo) + dope::halo_flag_offset((int64_t)unit_bytes(L)));
-}
 
 // How the shards of one grid talk.  `S` are the shards this process holds.
 // peer: the kernels move the halo rows and agg slots themselves through the
@@ -250,7 +247,7 @@ static int one_iteration(const dope_lattice *const *S, int nloc, Transport &T, c
         for (int r = 0; r < nloc; ++r)
             if ((rc = dope_update_blocks(S[r], s))) return rc;
         for (int r = 0; r < nloc; ++r)
-            if ((rc = dope_peer_install(S[r], s))) return rc;
+            if ((S[r]->ghost_up || S[r]->ghost_dn) && (rc = dope_peer_install(S[r], s))) return rc;
         for (int r = 0; r < nloc; ++r)
             if ((rc = dope_update_global(S[r], s))) return rc;
         for (int r = 0; r < nloc; ++r)

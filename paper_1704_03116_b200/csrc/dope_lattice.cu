@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         if (blockIdx.x == 0 && tid == 0) dirty_list(L, it + 1)[0] = 0u;   // the next pass fills it
         const uint32_t cnt = lst[0], ent = lst[1 + (blockIdx.x < (unsigned)L.K ? blockIdx.x : 0)];
         if (stop || blockIdx.x >= cnt) {
-            if (L.peers) k1_peer_exit(L);
+            if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
             return;
         }
         k = (int)ent;
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         ycur = L.st->ycur;
         const uint32_t dk = L.skip_clean ? L.dirty[k] : 1u;
         if (stop || dk == 0) {
-            if (L.peers) k1_peer_exit(L);
+            if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
             return;
         }
     }
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         atomicAdd((unsigned long long *)&L.st->sweeps, (unsigned long long)sweeps_done);
         atomicMax(&L.st->max_rounds_seen, rounds);
     }
-    if (L.peers) k1_peer_exit(L);
+    if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
 }
 
 // cold residual graphs for every block (warm-start initial state)

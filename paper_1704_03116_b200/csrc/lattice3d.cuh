@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut3d(Lat2 L, K1Tune T) {
     extern __shared__ __align__(16) uint8_t smem3[];
     const int k = blockIdx.x;
     if (L.st->stop || (L.skip_clean && L.dirty[k] == 0)) {
-        if (L.peers) k1_peer_exit(L);
+        if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
         return;
     }
     __syncthreads();
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut3d(Lat2 L, K1Tune T) {
         L.dirty[L.K + k] = (uint32_t)L.st->iteration + 1u;   // solve epoch
     }
     mincut3d_l2<BD, BH, BW, NT>(L, T, k, smem3);
-    if (L.peers) k1_peer_exit(L);
+    if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
 }
 
 __global__ void k_init_resid3d(Lat2 L, int boxd, int boxh, int boxw) {

@@ -195,12 +195,12 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
         if (blockIdx.x == 0 && tid == 0) dirty_list(L, it + 1)[0] = 0u;   // the next pass fills it
         const uint32_t cnt = lst[0], ent = lst[1 + blockIdx.x];
         if (stop || blockIdx.x >= cnt) {
-            if (L.peers) k1_peer_exit(L);
+            if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
             return;
         }
         k = (int)ent;
     } else if (L.st->stop || (L.skip_clean && L.dirty[k] == 0)) {
-        if (L.peers) k1_peer_exit(L);
+        if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
         return;
     }
     if (tid == 0) {
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
             __syncthreads();
             for (int w = tid; w < 3 * NIBW; w += NT) gF[w] = FE[w];
         }
-        if (L.peers) k1_peer_exit(L);
+        if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
         return;
     }
 
@@ -713,7 +713,7 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
         atomicAdd((unsigned long long *)&L.st->sweeps, (unsigned long long)sweeps_done);
         atomicMax(&L.st->max_rounds_seen, rounds);
     }
-    if (L.peers) k1_peer_exit(L);
+    if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
 }
 
 // cold residual graph in the nibble layout: every existing E/S/D arc at cap
