@@ -148,32 +148,37 @@ constexpr int AGG_SLOT = 8;
 // Peer mode, every K1 CTA on its way out (CTA-uniform call): the last CTA of
 // the grid pushes this shard's first / last row of labels into the
 // neighbours' halo slots and raises their row flags (epoch = this iteration).
-__device__ __noinline__ void k1_peer_exit(const Lat2 &L) {
+__device__ __noinline__ void k1_peer_exit_impl(uint32_t *pflags, const dope_peers *pr, const uint8_t *yhat,
+                                               const dope_run_state *st, int64_t P, int64_t lastoff) {
+    // (plain arguments: a `const Lat2 &` would force the caller's whole
+    // parameter block into local memory)
     __shared__ int last;
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        last = atomicAdd(&L.pflags[2], 1u) == gridDim.x - 1;
+        last = atomicAdd(&pflags[2], 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (!last) return;
     __threadfence();
-    const dope_peers *pr = L.peers;
     uint8_t *up = pr->row_to_up, *dn = pr->row_to_dn;
-    const int64_t P = L.ndim == 3 ? (int64_t)L.ay.dim * L.W : (int64_t)L.W;
-    const int64_t lastoff = ((L.ndim == 3 ? (int64_t)L.az.dim : (int64_t)L.ay.dim) - 1) * P;
     for (int64_t c = threadIdx.x; c < P; c += blockDim.x) {
-        if (up) up[c] = L.yhat[c];
-        if (dn) dn[c] = L.yhat[lastoff + c];
+        if (up) up[c] = yhat[c];
+        if (dn) dn[c] = yhat[lastoff + c];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence_system();
-        const uint32_t ep = peer_epoch(L.st, (uint32_t)L.st->iteration + 1u);
+        const uint32_t ep = peer_epoch(st, (uint32_t)st->iteration + 1u);
         if (up) st_release_sys(pr->flag_to_up, ep);
         if (dn) st_release_sys(pr->flag_to_dn, ep);
-        L.pflags[2] = 0u;
+        pflags[2] = 0u;
     }
+}
+__device__ __forceinline__ void k1_peer_exit(const Lat2 &L) {
+    const int64_t P = L.ndim == 3 ? (int64_t)L.ay.dim * L.W : (int64_t)L.W;
+    const int64_t lastoff = ((L.ndim == 3 ? (int64_t)L.az.dim : (int64_t)L.ay.dim) - 1) * P;
+    k1_peer_exit_impl(L.pflags, L.peers, L.yhat, L.st, P, lastoff);
 }
 
 // Append block k to the solved-block list (see solved_list); dirty[8K + k] =
