@@ -326,6 +326,11 @@ void dope_graph_cache_clear(void);
  * = u[i] when every u[i] is an integer within +-2^28, else *bad |= 1 (zero
  * it first) -- the device side of re-running a lowered model on new unaries. */
 int dope_unary_i32(const double *u, int64_t n, int32_t *out, int32_t *bad, void *stream);
+/* Page-lock / release a caller's host buffer in place (cudaHostRegister),
+ * so the unary of run()'s serving loop is DMA'd without a staging copy.
+ * Returns DOPE_OK, or DOPE_E_CUDA with the runtime error cleared. */
+int dope_host_register(void *ptr, int64_t bytes);
+int dope_host_unregister(void *ptr);
 /* binarize (admm.py:202-204) of the current iterate into out[n] (0/1). */
 int dope_binarize(const dope_lattice *L, uint8_t *out, void *stream);
 /* evaluate_energy of an arbitrary doubled labeling y2 (int path):

@@ -350,6 +350,10 @@ def lib():
     lb.dope_exhaustive_batch.restype = C.c_int
     lb.dope_exhaustive_batch.argtypes = [C.c_int32, V, V, V, V, V, V, C.c_double, V, V, V]
     lb.dope_trace_digest.restype = C.c_int
+    lb.dope_host_register.restype = C.c_int
+    lb.dope_host_register.argtypes = [V, C.c_int64]
+    lb.dope_host_unregister.restype = C.c_int
+    lb.dope_host_unregister.argtypes = [V]
     lb.dope_unary_i32.restype = C.c_int
     lb.dope_unary_i32.argtypes = [V, C.c_int64, V, V, V]
     if lb.dope_abi_version() != ABI_VERSION:

@@ -136,15 +136,12 @@ class BlockProblems:
             return False
         if model is self.model:
             return True
-        # stage through a pinned buffer: the host copy runs on all cores, the
-        # DMA at full link speed (a pageable H2D of 134 MB at 4096^2 is slower)
-        src = torch.from_numpy(np.ascontiguousarray(model.unary, dtype=np.float64))
-        if getattr(self, "_u_pinned", None) is None or self._u_pinned.shape != src.shape:
-            self._u_pinned = torch.empty(src.shape, dtype=torch.float64).pin_memory()
-            self._u_dev64 = torch.empty(src.shape, dtype=torch.float64, device=self.device)
-        self._u_pinned.copy_(src)
-        u64 = self._u_dev64
-        u64.copy_(self._u_pinned, non_blocking=True)
+        # pipelined pinned staging, or a direct DMA once the caller's buffer
+        # repeats (hostio.UnaryUploader)
+        if getattr(self, "_uploader", None) is None:
+            from .hostio import UnaryUploader
+            self._uploader = UnaryUploader(self.lowering.n, self.device)
+        u64 = self._uploader.upload(model.unary)
         if self.kind == "int":
             bad = torch.zeros(1, dtype=torch.int32, device=self.device)
             _lib.check(_lib.lib().dope_unary_i32(u64.data_ptr(), u64.numel(), self.u.data_ptr(), bad.data_ptr(),
@@ -792,8 +789,27 @@ def _run_lattice(model, partition, config, problems) -> tuple:
     state.clamped_last = bool(cl[it - 1]) if it else False
     if dev.trace_hash is not None:
         state.digests = dev.trace_hash[:3 * it].cpu().numpy().view(np.uint64).reshape(it, 3)
-    labels = dev.binarize().to(torch.int8).cpu().numpy()
+    if getattr(problems, "_downloader", None) is None:
+        from .hostio import LabelDownloader
+        problems._downloader = LabelDownloader(problems.lowering.n)
+    labels = problems._downloader.fetch(dev.binarize())
     return labels, state
+
+
+_max_counts: dict = {}
+
+
+def _max_count(partition: Partition) -> int:
+    """max q over pixels, computed once per partition object (an O(n) scan of
+    partition.counts would otherwise cost ~3.5 ms per run() at 4096^2)."""
+    import weakref
+    key = id(partition)
+    hit = _max_counts.get(key)
+    if hit is not None and hit[0]() is partition:
+        return hit[1]
+    q = int(partition.counts.max()) if partition.counts.size else 1
+    _max_counts[key] = (weakref.ref(partition, lambda _r, k=key: _max_counts.pop(k, None)), q)
+    return q
 
 
 def run(model: EnergyModel, partition: Partition, config: AdmmConfig,
@@ -816,7 +832,7 @@ def run(model: EnergyModel, partition: Partition, config: AdmmConfig,
         if isinstance(problems, GraphProblems):
             return run_graph(model, partition, config, problems)
         raise TypeError("problems must come from assemble_block_problems")
-    overlap = partition.overlap_pct != 0 or bool(partition.counts.size and int(partition.counts.max()) > 1)
+    overlap = partition.overlap_pct != 0 or _max_count(partition) > 1
     lattice_ok = config.solver.kind == "maxflow"
     if lattice_ok and not overlap and config.mu_fact == 1.0:
         if problems is None:

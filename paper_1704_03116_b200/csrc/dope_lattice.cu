@@ -2479,6 +2479,26 @@ int dope_unary_i32(const double *u, int64_t n, int32_t *out, int32_t *bad, void 
     return cuda_check(cudaGetLastError(), "unary_i32");
 }
 
+int dope_host_register(void *ptr, int64_t bytes) {
+    if (!ptr || bytes <= 0) return DOPE_E_ARGS;
+    const cudaError_t e = cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();   // not sticky: the caller falls back to staging
+        return DOPE_E_CUDA;
+    }
+    return DOPE_OK;
+}
+
+int dope_host_unregister(void *ptr) {
+    if (!ptr) return DOPE_E_ARGS;
+    const cudaError_t e = cudaHostUnregister(ptr);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        return DOPE_E_CUDA;
+    }
+    return DOPE_OK;
+}
+
 int dope_ghost_decide(const dope_lattice *L, void *stream) {
     Plan P;
     int rc = build_plan(L, P);

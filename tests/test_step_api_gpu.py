@@ -275,3 +275,32 @@ def test_repeated_runs_reuse_the_lowering_and_keep_the_graph_cache_bounded():
     ref = dope.run(dope.EnergyModel(u0 + 0.5, dope.SparseWeights(wl.n, rows, cols, vals), wl.lam),
                    dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0), cfg)
     assert np.array_equal(half[0], ref[0])
+
+
+def test_serving_loop_refilling_one_host_buffer():
+    """run() on one host unary buffer refilled in place between calls: from the
+    second call the buffer is DMA'd directly (page-locked once), and every
+    call sees the new contents -- identical to a fresh lowering each time.
+    Switching to another array releases the registration."""
+    from paper_1704_03116_b200 import admm as A, workloads as W
+    wl = W.mini_disks(256, 64, 8, 2, 10, seed=6)
+    rows, cols, vals = wl.pair_arrays()
+    weights = dope.SparseWeights(wl.n, rows, cols, vals)
+    part = dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0, materialize=False)
+    cfg = dope.AdmmConfig(mu0=1.0, mu_fact=1.0, eps=0.0, max_iters=wl.iters)
+    rng = np.random.default_rng(9)
+    buf = np.empty(wl.n, dtype=np.float64)
+    problems = None
+    for i in range(5):
+        buf[:] = wl.u + rng.integers(-2, 3, wl.n)
+        labels, state = dope.run(dope.EnergyModel(buf, weights, wl.lam), part, cfg)
+        fresh = dope.run(dope.EnergyModel(buf.copy(), dope.SparseWeights(wl.n, rows, cols, vals), wl.lam),
+                         dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0), cfg)
+        assert labels.dtype == np.int8 and np.array_equal(labels, fresh[0])
+        assert [t.energy for t in state.trace] == [t.energy for t in fresh[1].trace]
+        problems = A._problems_for(dope.EnergyModel(buf, weights, wl.lam), part)
+    up = problems._uploader
+    assert up.registered_uploads >= 3 and up._registered is not None
+    other = buf.copy()
+    dope.run(dope.EnergyModel(other, weights, wl.lam), part, cfg)
+    assert up._registered is None
