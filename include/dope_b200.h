@@ -115,7 +115,7 @@ typedef struct dope_lattice {
                                    current, best, and the next output         */
     uint8_t *yhat;              /* n   block labels (global layout)           */
     uint8_t *resid;             /* K * resid_stride bytes: residual graphs    */
-    uint32_t *dirty;            /* 9K: [0, K) block needs a re-solve
+    uint32_t *dirty;            /* 12K + 2: [0, K) block needs a re-solve
                                    (init 1); [K, 2K) iteration + 1 of the
                                    block's last solve; [2K, 5K) pass + 1 at
                                    which y buffer b last received block k's
@@ -126,7 +126,10 @@ typedef struct dope_lattice {
                                    [7K, 8K) the blocks solved this iteration,
                                    [8K, 9K) 1 + block k's slot in that list,
                                    [9K, 11K + 2) the run loop's two dirty-block
-                                   worklists [count, K entries]: 11K + 2 in all */
+                                   worklists [count, K entries], [11K + 2,
+                                   12K + 2) iteration + 1 of the block's last
+                                   finished solve (K1 / consensus overlap):
+                                   12K + 2 in all */
     int64_t *part_energy;       /* K   per-block pair-energy partials          */
     int64_t *part_unary;        /* K   per-block change of sum u*y2           */
     int64_t *part_ressq;        /* K   per-block sum (yhat - y)^2             */

@@ -374,8 +374,9 @@ class _DeviceState:
         # [0, K): re-solve flags; [K, 2K): iteration + 1 of each block's last solve;
         # [2K, 7K): y-buffer / iterate-change / energy-partial stamps of the
         # clean-block consensus passes; [7K, 9K): the solved-block list and slots;
-        # [9K, 11K + 2): the run loop's dirty-block worklists
-        self.dirty = torch.zeros(11 * K + 2, dtype=torch.int32, device=dev)
+        # [9K, 11K + 2): the run loop's dirty-block worklists; [11K + 2, 12K + 2):
+        # finished-solve epochs (K1 / consensus overlap)
+        self.dirty = torch.zeros(12 * K + 2, dtype=torch.int32, device=dev)
         self.dirty[:K] = 1
         sstride = int(lb.dope_scratch_stride(C.byref(L)))
         self.scratch = torch.empty(max(K * sstride, 16), dtype=u8, device=dev)

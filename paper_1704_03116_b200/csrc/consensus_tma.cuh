@@ -18,6 +18,14 @@
 //     K1 clears them); each CTA then folds its own blocks into pass-wide
 //     aggregates, so the last CTA only adds up one residual sum per CTA.
 
+// work items per claim of the overlapped pass (dynamic distribution)
+#ifndef K2_CHUNK
+#define K2_CHUNK 4
+#endif
+#ifndef K2_DYN
+#define K2_DYN 0
+#endif
+
 struct TmaMaps {
     CUtensorMap a, y[3], yr[3], yhat;
     CUtensorMap yrow[3];      // y2: one row of TW (ring-only tiles)
@@ -267,6 +275,12 @@ __device__ __forceinline__ uint32_t active_groups(uint32_t sides) {
     return L | (R << 1) | (U << 2) | (D << 3) | ((L | U) << 4) | ((R | U) << 5) | ((L | D) << 6) | ((R | D) << 7);
 }
 
+// the pass's diagnostics slots: after K1's per-block ones in overlap mode
+// (both kernels are live at once)
+__device__ __forceinline__ int64_t *k2_timeline(const Lat2 &L) {
+    return L.timeline + (L.ovl ? 8 * (size_t)L.K : 0);
+}
+
 // diagnostics (timeline mode, K >= 5 * CTAs): per CTA and stage n < 8,
 // [issue, data arrived (warp 0), consumed (warp 0), tile loop done (warp 0)]
 // globaltimer stamps after
@@ -275,7 +289,7 @@ __device__ __forceinline__ void stage_stamp(const Lat2 &L, int n, int which) {
     if (!L.timeline || n >= 8 || L.K < 5 * (int)gridDim.x) return;
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    L.timeline[8 * gridDim.x + (blockIdx.x * 8 + n) * 4 + which] = (int64_t)t;
+    k2_timeline(L)[8 * gridDim.x + (blockIdx.x * 8 + n) * 4 + which] = (int64_t)t;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -330,7 +344,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
         if (L.timeline) {   // diagnostics: CTA start (slot 6 of entry blockIdx)
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            L.timeline[8 * blockIdx.x + 6] = (int64_t)t;
+            k2_timeline(L)[8 * blockIdx.x + 6] = (int64_t)t;
         }
         for (int i = 0; i < ST; ++i) {
             mbar_init(&full[i], 1);
@@ -401,13 +415,50 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
             if (f & 128u) ychg_stamp(L)[k] = ep_now;
         };
         int n = 0;   // stages issued (lane 0)
-        for (int c0 = 0; c0 < nmine; c0 += 32) {
-            const int nc = nmine - c0 < 32 ? nmine - c0 : 32;
+        // Overlap mode: the CTAs start staggered behind K1's solves (a CTA
+        // becomes resident when K1 CTAs leave its SM), so the work items --
+        // every block (phase B) then the solved list (phase A) -- are claimed
+        // in chunks of K2_CHUNK: chunk bid first, then from a pass-wide counter
+        // (pc[7], zeroed by the last CTA).  Otherwise static round-robin.
+        // Phase-B chunks hold K2_CHUNK blocks, phase-A chunks one solved
+        // block each (a full tile pass: the heavy items, spread thin).
+        // (measured on C3: slower than the static deal -- each chunk pays a
+        // metadata round trip the static gather shares over all of a CTA's
+        // blocks; kept behind -DK2_DYN=1)
+        const bool dyn = K2_DYN && L.ovl != 0;
+        const int NB = (K + K2_CHUNK - 1) / K2_CHUNK, NCH = NB + nsolved;
+        int chunk = bid;
+        for (int c0 = 0;; c0 += 32) {
+            int nc, ibase = 0;
+            if (dyn) {
+                if (chunk >= NCH) break;
+                ibase = chunk < NB ? chunk * K2_CHUNK : K + (chunk - NB);
+                nc = chunk < NB ? (K - ibase < K2_CHUNK ? K - ibase : K2_CHUNK) : 1;
+            } else {
+                if (c0 >= nmine) break;
+                nc = nmine - c0 < 32 ? nmine - c0 : 32;
+            }
+            // the next chunk's claim goes out now; its index is needed only
+            // after this chunk's stages are issued
+            unsigned long long claim = 0;
+            if (dyn && plane == 0)
+                claim = atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[7]), 1ull);
             int64_t eskip = 0;
             int fskip = 0, nskip = 0;
             if (plane < nc) {
                 const int j = c0 + plane;
-                const int kk = j < nA ? (int)solved_list(L)[bid + j * G] : bid + (j - nA) * G;
+                bool isA;
+                int aslot, kk;
+                if (dyn) {
+                    const int item = ibase + plane;
+                    isA = item >= K;
+                    aslot = item - K;
+                    kk = isA ? (int)solved_list(L)[aslot] : item;
+                } else {
+                    isA = j < nA;
+                    aslot = bid + j * G;
+                    kk = isA ? (int)solved_list(L)[aslot] : bid + (j - nA) * G;
+                }
                 const int by = (int)__umulhi((uint32_t)kk, kx_magic), bx = kk - by * KX;
                 // every load of this block's metadata in one independent
                 // round (neighbour indices clamped in range, results masked)
@@ -433,8 +484,8 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
                 // mode 3: nothing here -- a phase-A entry that is not its
                 // block's latest slot, or a solved block phase A deals with
                 int mode = 0;
-                if (j < nA) {
-                    if (!solved || sl != (uint32_t)(bid + j * G) + 1u) mode = 3;
+                if (isA) {
+                    if (!solved || sl != (uint32_t)aslot + 1u) mode = 3;
                 } else if (L.skip_clean && solved) {
                     if (sl >= 1u && sl <= (uint32_t)nsolved && __ldcg(solved_list(L) + sl - 1u) == (uint32_t)kk) mode = 3;
                 }
@@ -475,7 +526,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
             if (plane == 0 && c0 == 0 && L.timeline) {   // diagnostics: metadata gathered (slot 0)
                 uint64_t t;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                L.timeline[8 * blockIdx.x + 0] = (int64_t)t;
+                k2_timeline(L)[8 * blockIdx.x + 0] = (int64_t)t;
             }
             if (plane == 0) {
                 if (nskip) {
@@ -483,9 +534,36 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
                     agg.F |= fskip;
                     agg.M = agg.M > 0 ? agg.M : 0;
                 }
+                // overlap mode: a block whose labels (or a re-solved
+                // neighbour's) K1 has not published yet is deferred behind
+                // the CTA's ready blocks, then awaited in order
+                auto ready = [&](const BlockMeta &bm) {
+                    const uint32_t sd = ((uint32_t)bm.flags >> 3) & 0xFu;
+                    const uint32_t *kd = L.kdone;
+                    bool r = !(bm.flags & 1) || ld_acquire_gpu(kd + bm.k) == ep_now;
+                    if (r && (sd & 1u)) r = ld_acquire_gpu(kd + bm.k - 1) == ep_now;
+                    if (r && (sd & 2u)) r = ld_acquire_gpu(kd + bm.k + 1) == ep_now;
+                    if (r && (sd & 4u)) r = ld_acquire_gpu(kd + bm.k - KX) == ep_now;
+                    if (r && (sd & 8u)) r = ld_acquire_gpu(kd + bm.k + KX) == ep_now;
+                    return r;
+                };
+                uint32_t deferred = 0;
+                for (int pass = 0; pass < (L.ovl ? 2 : 1); ++pass)
                 for (int j = 0; j < nc; ++j) {
                     const BlockMeta bm = meta[j];
                     if (bm.mode >= 2) continue;
+                    if (L.ovl) {
+                        if (pass == 0 && !ready(bm)) {
+                            deferred |= 1u << j;
+                            continue;
+                        }
+                        if (pass == 1) {
+                            if (!(deferred >> j & 1u)) continue;
+                            while (!ready(bm)) __nanosleep(128);
+                        }
+                        // labels written by other CTAs (generic proxy) before the TMA reads them
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                    }
                     const int by = (int)__umulhi((uint32_t)bm.k, kx_magic), bx = bm.k - by * KX;
                     const bool hl = bx > 0, hr = bx + 1 < KX, hu = by > 0 || L.gup, hd = by + 1 < KY || L.gdn;
                     const uint32_t sd = ((uint32_t)bm.flags >> 3) & 0xFu;
@@ -521,14 +599,15 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
                 }
             }
             __syncwarp();
+            if (dyn) chunk = G + __shfl_sync(FULLMASK, (int)claim, 0);
         }
         if (plane != 0) return;
         if (L.timeline) {   // diagnostics: last stage issued (slot 1), stages (slot 4), phase-A blocks (slot 5)
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            L.timeline[8 * blockIdx.x + 1] = (int64_t)t;
-            L.timeline[8 * blockIdx.x + 4] = n;
-            L.timeline[8 * blockIdx.x + 5] = nA;
+            k2_timeline(L)[8 * blockIdx.x + 1] = (int64_t)t;
+            k2_timeline(L)[8 * blockIdx.x + 4] = n;
+            k2_timeline(L)[8 * blockIdx.x + 5] = nA;
         }
         {   // end marker
             const int s = n % ST;
@@ -548,12 +627,12 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
         if (L.timeline) {   // diagnostics: CTA end (slot 7)
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            L.timeline[8 * blockIdx.x + 7] = (int64_t)t;
+            k2_timeline(L)[8 * blockIdx.x + 7] = (int64_t)t;
         }
         if (L.timeline) {   // diagnostics: stages drained (slot 2)
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            L.timeline[8 * blockIdx.x + 2] = (int64_t)t;
+            k2_timeline(L)[8 * blockIdx.x + 2] = (int64_t)t;
         }
         pass_tail(L, agg, cur, best, out);
         return;

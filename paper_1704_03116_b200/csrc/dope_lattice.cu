@@ -90,7 +90,32 @@ struct Lat2 {
     const dope_peers *peers;  // peer-memory exchange (sharded), else null
     uint32_t *pflags;       // peer mode: this shard's flags [row from above, row from below,
                             // K1 done-counter, pad, agg-slot flag per shard]
+    int32_t ovl;            // run loop: the consensus pass overlaps K1 (k1_publish_done, PDL launch)
+    uint32_t *kdone;        // overlap mode: iteration + 1 of each block's last FINISHED solve
 };
+
+// ---------------------------------------------------------------------------
+// K1 -> consensus overlap (run loop, TMA consensus pass): K1 CTAs write their
+// block's dirty-flag clear, solve epoch and solved-list slot, fence, and only
+// then trigger the dependent launch, so the consensus pass starts with the
+// iteration's solved set fixed; each solving CTA publishes its labels with a
+// release store of the block's done epoch, which the consensus producer
+// acquires before it streams the block's (or a neighbour's) labels.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// K1 epilogue: every thread's label / residual stores precede the flag (the
+// barrier orders them before thread 0's cumulative release)
+__device__ __forceinline__ void k1_publish_done(const Lat2 &L, int k) {
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_gpu(L.kdone + k, (uint32_t)L.st->iteration + 1u);
+}
 
 // ---------------------------------------------------------------------------
 // Peer-memory exchange (dope_peers): system-scope release / acquire flags.
@@ -248,16 +273,8 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int k = blockIdx.x;
-    uint64_t t_begin = 0;
-    if (L.timeline && tid == 0) {
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
-        L.timeline[8 * k + 0] = (int64_t)t_begin;
-        L.timeline[8 * k + 1] = (int64_t)t_begin;
-        L.timeline[8 * k + 2] = -1;
-        L.timeline[8 * k + 3] = 0;
-        L.timeline[8 * k + 4] = (int64_t)t_begin;
-        L.timeline[8 * k + 5] = (int64_t)t_begin;
-    }
+    uint64_t t_begin = 0;   // diagnostics: CTA start (recorded once the block is known)
+    if (L.timeline && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
     if (L.pdl) {
         griddep_wait();     // the previous consensus pass (PDL launch)
         griddep_launch();   // all K1 CTAs are resident: the consensus pass may launch
@@ -265,12 +282,19 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
     int ycur;
     if (L.dlist) {
         // run loop: CTA i takes entry i of this iteration's dirty-block list
+        // (both lists' count and entry i are read with the run state, one
+        // round trip: most CTAs find nothing to do and must leave fast)
         const int stop = L.st->stop;
         ycur = L.st->ycur;
         const int it = L.st->iteration;
-        const uint32_t *lst = dirty_list(L, it);
-        if (blockIdx.x == 0 && tid == 0) dirty_list(L, it + 1)[0] = 0u;   // the next pass fills it
-        const uint32_t cnt = lst[0], ent = lst[1 + (blockIdx.x < (unsigned)L.K ? blockIdx.x : 0)];
+        const uint32_t bi = blockIdx.x < (unsigned)L.K ? blockIdx.x : 0u;
+        const uint32_t c0 = __ldcg(L.dlist), c1 = __ldcg(L.dlist + L.K + 1);
+        const uint32_t e0 = __ldcg(L.dlist + 1 + bi), e1 = __ldcg(L.dlist + L.K + 2 + bi);
+        if (blockIdx.x == 0 && tid == 0) {
+            dirty_list(L, it + 1)[0] = 0u;   // the next pass fills it
+            if (L.ovl) __threadfence();      // before this CTA's trigger (or exit)
+        }
+        const uint32_t cnt = (it & 1) ? c1 : c0, ent = (it & 1) ? e1 : e0;
         if (stop || blockIdx.x >= cnt) {
             if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
             return;
@@ -290,12 +314,22 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         }
     }
     __syncthreads();
+    if (L.timeline && tid == 0) {
+        L.timeline[8 * k + 0] = (int64_t)t_begin;
+        L.timeline[8 * k + 1] = (int64_t)t_begin;
+        L.timeline[8 * k + 2] = -1;
+        L.timeline[8 * k + 3] = 0;
+        L.timeline[8 * k + 4] = (int64_t)t_begin;
+        L.timeline[8 * k + 5] = (int64_t)t_begin;
+    }
     if (tid == 0) {
         L.dirty[k] = 0;
         const uint32_t ep = (uint32_t)L.st->iteration + 1u;
         L.dirty[L.K + k] = ep;   // solve epoch (consensus fast path)
         if (L.slist) solved_append(L, k);
+        if (L.ovl) __threadfence();   // the consensus pass may start once every CTA triggered
     }
+    if (L.ovl) griddep_launch();      // (a CTA triggers when all its threads did: thread 0 after its fence)
 
     const int by = k / L.ax.k, bx = k % L.ax.k;
     int32_t lo_r, hr, lo_c, wc;
@@ -613,6 +647,7 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         atomicAdd((unsigned long long *)&L.st->sweeps, (unsigned long long)sweeps_done);
         atomicMax(&L.st->max_rounds_seen, rounds);
     }
+    if (L.ovl) k1_publish_done(L, k);
     if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
 }
 
@@ -691,6 +726,9 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
     // solve epochs and the stamps of the clean-block consensus passes
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 6 * (int64_t)L.K; i += stride)
             L.dirty[L.K + i] = 0u;
+    // finished-solve epochs of the overlap mode (dirty[11K + 2, 12K + 2))
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.K; i += stride)
+        L.dirty[(size_t)11 * L.K + 2 + i] = 0u;
     if (L.dlist) {   // iteration 0 solves every block: list 0 = all, list 1 empty
         for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.K; i += stride)
             L.dlist[1 + i] = (uint32_t)i;
@@ -1141,6 +1179,9 @@ __device__ void pass_tail(const Lat2 &L, const CtaAgg &c, int cur, int best, int
     dope_run_state *st = L.st;
     if (atomicAdd(&st->done_ctas, 1) == (int)(gridDim.x * gridDim.y * gridDim.z) - 1) {
         __threadfence();
+        // overlap mode: K1 (error flag, statistics) complete before the decision;
+        // the grid cannot complete before K1 either
+        if (L.ovl) griddep_wait();
         const dope_run_state s0 = *st;
         const int64_t E2 = __ldcg(&L.pc[0]), U2 = __ldcg(&L.pc[1]), M2 = __ldcg(&L.pc[2]) - 1;
         const int F2 = (int)__ldcg(&L.pc[3]);
@@ -1867,7 +1908,7 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
     // K1 that deals them out (2D integer K1, shared-memory K1-3D)
     // (only with more blocks than the first K1 wave holds: with fewer, every
     // CTA starts at once and the list's extra round trip is pure cost -- C1)
-    if (L->fuse_multipliers && L->skip_clean && !L->timeline && !getenv("DOPE_NO_DLIST") && o.K > 2 * sm_count())
+    if (L->fuse_multipliers && L->skip_clean && !getenv("DOPE_NO_DLIST") && o.K > 2 * sm_count())
         o.dlist = L->dirty + (size_t)9 * o.K;
     if (L->sharded && L->halo) {
         const int64_t U = is3 ? L->dims[1] * L->dims[2] : L->dims[1];
@@ -2007,6 +2048,22 @@ static int configure_plan(const Plan &P) {
 // griddep_wait().  Off by default: measured neutral on C3 and 5-10 % slower on
 // C5 (early-launched CTAs hold SM slots); same results either way.
 template <typename... KArgs, typename... Args>
+static cudaError_t launch_attr(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                               Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args... args) {
     static const bool off = getenv("DOPE_PDL") == nullptr;
@@ -2132,8 +2189,13 @@ static int launch_k2_tma(const Lat2 &o, cudaStream_t s, int ctas_per_sm) {
     static const int settle = getenv("DOPE_K2_SETTLE") ? atoi(getenv("DOPE_K2_SETTLE")) : 1;
     // (measured: with at most two blocks per CTA the settled / ring-only
     // modes do not pay for their metadata -- C5 b64 / b128)
+    const int st_mode = settle && o.K > 2 * grid ? 1 : 0;
+    if (o.ovl)   // overlap mode: a programmatic dependent of K1 (see k1_publish_done)
+        return cuda_check(launch_attr(true, k_consensus_tma<TW, TH, NT, ST>, dim3(grid), dim3(C::NT + 32),
+                                      (size_t)C::SMEM, s, o, M, magic, st_mode),
+                          "launch K2 (tma, overlapped)");
     return cuda_check(launch_pdl(k_consensus_tma<TW, TH, NT, ST>, dim3(grid), dim3(C::NT + 32), (size_t)C::SMEM, s,
-                                 o, M, magic, settle && o.K > 2 * grid ? 1 : 0),
+                                 o, M, magic, st_mode),
                       "launch K2 (tma)");
 }
 
@@ -2337,10 +2399,22 @@ int dope_update_multipliers(const dope_lattice *L, void *stream) {
     return cuda_check(cudaGetLastError(), "update_multipliers");
 }
 
+// Overlap mode (run loop only: K1 and the consensus pass are adjacent in the
+// stream): 2D integer K1 + the TMA consensus pass on one GPU.
+static void enable_overlap(Plan &P) {
+    static const bool off = getenv("DOPE_NO_OVL") != nullptr || getenv("DOPE_NO_TMA") != nullptr ||
+                            getenv("DOPE_K2_VARIANT") != nullptr;
+    if (off || !P.v || P.v3 || P.o.sharded || !P.o.skip_clean || !P.o.fuse || !k2_tma_width(P.o)) return;
+    P.o.ovl = 1;
+    P.o.pdl = 0;   // K1 itself is an ordinary launch (the previous pass complete)
+    P.o.kdone = P.o.dirty + (size_t)11 * P.o.K + 2;
+}
+
 int dope_admm_run(const dope_lattice *L, int32_t iters, int32_t use_graph, void *stream) {
     Plan P;
     int rc = build_plan(L, P);
     if (rc) return rc;
+    enable_overlap(P);
     cudaStream_t s = (cudaStream_t)stream;
     if (iters <= 0) return DOPE_OK;
     if ((rc = dope_rebuild_dirty_list(L, stream))) return rc;
