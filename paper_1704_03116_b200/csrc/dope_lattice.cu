@@ -220,6 +220,35 @@ __device__ __forceinline__ void solved_append(const Lat2 &L, int k) {
 // K1: block min-cut (2D, 4-connected)
 // ---------------------------------------------------------------------------
 
+// Warp-level compaction (K1 sweeps): the lanes whose bit is set in `word`
+// (node v of lane i) join the warp's batch slots[0..cnt); every full batch of
+// 32 runs work(node), one node per lane.  Returns the new batch fill.
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+template <class F>
+__device__ __forceinline__ int warp_enqueue(uint16_t *slots, uint32_t word, int cnt, int lane, int v, F &&work) {
+    while (word) {
+        const bool mine = (word >> lane) & 1u;
+        const int rank = __popc(word & lanemask_lt());
+        const int room = 32 - cnt;
+        if (mine && rank < room) slots[cnt + rank] = (uint16_t)v;
+        const int n = __popc(word);
+        word = __ballot_sync(FULLMASK, mine && rank >= room);
+        if (n >= room) {
+            __syncwarp();
+            work((int)slots[lane]);
+            __syncwarp();
+            cnt = 0;
+        } else {
+            cnt += n;
+        }
+    }
+    return cnt;
+}
+
 template <int BH, int BW, int NT>
 struct K1Cfg {
     static constexpr int M = BH * BW;
@@ -279,6 +308,17 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         griddep_wait();     // the previous consensus pass (PDL launch)
         griddep_launch();   // all K1 CTAs are resident: the consensus pass may launch
     }
+#ifdef K1_DIAG2
+    // per-SM count of resident K1 CTAs at [16K, 16K + 256) of the timeline
+    uint32_t smid_;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));
+    int *sm_cnt = L.timeline ? reinterpret_cast<int *>(L.timeline + 16 * (size_t)L.K) : nullptr;
+    if (sm_cnt && tid == 0) atomicAdd(sm_cnt + smid_, 1);
+    struct SmLeave {
+        int *c; uint32_t s; int t;
+        __device__ ~SmLeave() { if (c && t == 0) atomicSub(c + s, 1); }
+    } sm_leave_{sm_cnt, smid_, tid};
+#endif
     int ycur;
     if (L.dlist) {
         // run loop: CTA i takes entry i of this iteration's dirty-block list
@@ -506,9 +546,19 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         L.timeline[8 * k + 4] = (int64_t)t;
     }
     // ---- solve: rounds of (global relabel BFS, push/relabel sweeps) ----
+#ifdef K1_DIAG2
+    __shared__ long long dclk[3][5];   // per sweep of round 1: start, push done, barrier, relabel done, end
+    __shared__ int dnp[3];
+    if (tid == 0)
+        for (int i = 0; i < 15; ++i) dclk[i / 5][i % 5] = 0;
+#endif
+    uint64_t t_bfs = 0;   // diagnostics (timeline mode, thread 0): last BFS start and levels
+    int lev_last = 0;
     int rounds = 0;
     long long sweeps_done = 0;
     for (;;) {
+        if (L.timeline && tid == 0)   // diagnostics: this round's BFS start
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_bfs));
         // masks via ballots: warp covers 32 consecutive nodes per step
 #pragma unroll 2
         for (int i = 0; i < NPT; ++i) {
@@ -544,65 +594,148 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             L.timeline[8 * k + 5] = (int64_t)t;
-            L.timeline[8 * k + 6] = levels;
+            int nact = 0;   // active nodes at the first BFS
+            for (int w = 0; w < 2 * NW; ++w) nact += __popc(masks32[5 * 2 * NW + w]);
+            L.timeline[8 * k + 6] = levels | ((int64_t)nact << 16);
         }
+        if (L.timeline && tid == 0) lev_last = levels;
         if (!hit) break;
         if (++rounds > T.max_rounds) {
             if (tid == 0) atomicCAS(&L.st->error, 0, k + 1);
             break;
         }
         const int cap_sweeps = T.sweep_min + T.sweep_mul * levels;
+        // The sweeps visit only candidate nodes, kept as bitmasks in the BFS
+        // scratch (both rebuilt by the next BFS): C = nodes to push from
+        // (initially the active nodes the BFS reached: reach & active), N =
+        // nodes to relabel (pushers left with excess, nodes that received
+        // some).  A warp owns the 32-node groups of its lanes (the BFS mask
+        // layout: group i of warp w = 32-bit word i * NT / 32 + w); it reads
+        // its group words in one load per lane and compacts the set bits
+        // into batches of 32, one node per lane, in a slot row.  Warm solves
+        // move little excess: a straggler's sweeps typically push from a
+        // handful of nodes, where a scan of every node's g and h cost
+        // ~1000-3000 cycles per phase (tools/mb_scan.cu, tools/k1_stragglers.py).
+        uint32_t *candC = reinterpret_cast<uint32_t *>(reach);          // 2 * NW words
+        uint32_t *candN = masks32;                                       // 2 * NW words
+        uint16_t *slots = reinterpret_cast<uint16_t *>(masks32 + 2 * NW) + warp * 32;
+        static_assert(8 * NW + (NT / 32) * 64 <= 6 * 8 * NW, "candidate masks and slots fit the BFS masks");
+        for (int w = tid; w < 2 * NW; w += NT) candC[w] &= masks32[5 * 2 * NW + w];   // reach & active
+        __syncthreads();
+        for (int w = tid; w < 2 * NW; w += NT) candN[w] = 0u;
+        __syncthreads();
         for (int sw = 0; sw < cap_sweeps; ++sw) {
             ++sweeps_done;
-            // push phase: admissible arcs h(w) == h(v) - 1
-#pragma unroll 2
-            for (int i = 0; i < NPT; ++i) {
-                const int v = tid + i * NT;
-                const int32_t e = g[v];
-                if (e <= 0) continue;
-                const uint16_t hv = h[v];
-                if (hv == HINF || hv == 0) continue;
-                const uint16_t ht = hv - 1;
-                int32_t left = e;
-#pragma unroll
-                for (int d = 0; d < 4; ++d) {
-                    const int off = (d == 0) ? 1 : (d == 1) ? -1 : (d == 2) ? BW : -BW;
-                    const int32_t rv = rr[d * M + v];
-                    if (rv == 0) continue;
-                    const int w = v + off;
-                    if (h[w] != ht) continue;
-                    const int32_t delta = left < rv ? left : rv;
-                    DOPE_ASSERT(w >= 0 && w < M && delta > 0 && rv <= 2 * cap &&
-                                rr[(d ^ 1) * M + w] + delta <= 2 * cap);   // r + r' = 2 cap per arc pair
-                    rr[d * M + v] = (uint8_t)(rv - delta);
-                    rr[(d ^ 1) * M + w] = (uint8_t)(rr[(d ^ 1) * M + w] + delta);
-                    atomicAdd(&g[w], delta);
-                    left -= delta;
-                    if (left == 0) break;
-                }
-                if (left != e) atomicSub(&g[v], e - left);
-            }
-            __syncthreads();
-            // relabel phase: h(v) = 1 + min over residual arcs (monotone)
+#ifdef K1_DIAG2
+            int npush = 0;
+            if (tid == 0 && rounds == 1 && sw < 3) dclk[sw][0] = clock64();
+#endif
             int act = 0;
-#pragma unroll 2
-            for (int i = 0; i < NPT; ++i) {
-                const int v = tid + i * NT;
-                if (g[v] <= 0) continue;
-                const uint16_t hv = h[v];
-                if (hv == HINF) continue;
-                uint32_t mn = HINF;
-#pragma unroll
-                for (int d = 0; d < 4; ++d) {
-                    const int off = (d == 0) ? 1 : (d == 1) ? -1 : (d == 2) ? BW : -BW;
-                    if (rr[d * M + v] == 0) continue;
-                    const uint32_t hw = h[v + off];
-                    mn = hw < mn ? hw : mn;
+#pragma unroll 1
+            for (int phase = 0; phase < 2; ++phase) {   // 0: push from C, 1: relabel N
+                uint32_t *cand = phase == 0 ? candC : candN;
+                // this warp's group words (lane j: group j), taken and cleared
+                uint32_t gw = 0;
+                if (lane < NPT) {
+                    const int wi = lane * (NT / 32) + warp;
+                    gw = cand[wi];
+                    if (gw) cand[wi] = 0u;
                 }
-                const uint32_t nh = (mn + 1 >= (uint32_t)M) ? HINF : mn + 1;
-                if (nh != hv) h[v] = (uint16_t)nh;
-                act |= (nh != HINF);
+                uint32_t groups = __ballot_sync(FULLMASK, gw != 0u);
+                int cnt = 0;
+                while (groups || cnt) {
+                    const int i = groups ? __ffs(groups) - 1 : 0;
+                    uint32_t word = groups ? __shfl_sync(FULLMASK, gw, i) : 0u;
+                    if (groups) groups &= groups - 1;
+                    const int v = i * NT + warp * 32 + lane;
+                    const bool tail = groups == 0u;
+                    while (word || (tail && cnt)) {
+                        const bool mine = (word >> lane) & 1u;
+                        const int rank = __popc(word & lanemask_lt());
+                        const int room = 32 - cnt;
+                        if (mine && rank < room) slots[cnt + rank] = (uint16_t)v;
+                        const int nw = __popc(word);
+                        word = __ballot_sync(FULLMASK, mine && rank >= room);
+                        const int fill = cnt + (nw < room ? nw : room);
+                        if (fill < 32 && !(tail && word == 0u)) {
+                            cnt = fill;
+                            continue;
+                        }
+                        // a full batch (or the last one): one node per lane
+                        __syncwarp();
+                        if (lane < fill) {
+                            const int u = slots[lane];
+                            const int32_t e = g[u];
+                            const uint16_t hu = h[u];
+                            if (phase == 0) {
+                                if (e > 0 && hu != HINF) {
+#ifdef K1_DIAG2
+                                    ++npush;
+#endif
+                                    int32_t left = e;
+                                    if (hu != 0) {
+                                        // push along the admissible arcs h(w) == h(u) - 1
+                                        const uint16_t ht = hu - 1;
+#pragma unroll
+                                        for (int d = 0; d < 4; ++d) {
+                                            const int off = (d == 0) ? 1 : (d == 1) ? -1 : (d == 2) ? BW : -BW;
+                                            const int32_t rv = rr[d * M + u];
+                                            if (rv == 0) continue;
+                                            const int w = u + off;
+                                            if (h[w] != ht) continue;
+                                            const int32_t delta = left < rv ? left : rv;
+                                            DOPE_ASSERT(w >= 0 && w < M && delta > 0 && rv <= 2 * cap &&
+                                                        rr[(d ^ 1) * M + w] + delta <= 2 * cap);   // r + r' = 2 cap
+                                            rr[d * M + u] = (uint8_t)(rv - delta);
+                                            rr[(d ^ 1) * M + w] = (uint8_t)(rr[(d ^ 1) * M + w] + delta);
+                                            atomicAdd(&g[w], delta);
+                                            atomicOr(&candN[w >> 5], 1u << (w & 31));   // w may turn active
+                                            left -= delta;
+                                            if (left == 0) break;
+                                        }
+                                        if (left != e) atomicSub(&g[u], e - left);
+                                    }
+                                    if (left > 0) atomicOr(&candN[u >> 5], 1u << (u & 31));
+                                }
+                            } else if (e > 0 && hu != HINF) {
+                                // h(u) = 1 + min over residual arcs (monotone)
+                                uint32_t mn = HINF;
+#pragma unroll
+                                for (int d = 0; d < 4; ++d) {
+                                    const int off = (d == 0) ? 1 : (d == 1) ? -1 : (d == 2) ? BW : -BW;
+                                    if (rr[d * M + u] == 0) continue;
+                                    const uint32_t hw = h[u + off];
+                                    mn = hw < mn ? hw : mn;
+                                }
+                                const uint32_t nh = (mn + 1 >= (uint32_t)M) ? HINF : mn + 1;
+                                if (nh != hu) h[u] = (uint16_t)nh;
+                                if (nh != HINF) {   // pushes next sweep
+                                    act = 1;
+                                    atomicOr(&candC[u >> 5], 1u << (u & 31));
+                                }
+                            }
+                        }
+                        __syncwarp();
+                        cnt = 0;
+                    }
+                }
+#ifdef K1_DIAG2
+                if (tid == 0 && rounds == 1 && sw < 3) dclk[sw][1 + 2 * phase] = clock64();
+#endif
+                if (phase == 0) {
+                    __syncthreads();
+#ifdef K1_DIAG2
+                    if (tid == 0 && rounds == 1 && sw < 3) dclk[sw][2] = clock64();
+                    {
+                        const int np = __syncthreads_count(npush);
+                        if (tid == 0 && rounds == 1 && sw < 3) dnp[sw] = np;
+                    }
+#endif
+                }
             }
+#ifdef K1_DIAG2
+            if (tid == 0 && rounds == 1 && sw < 3) dclk[sw][4] = clock64();
+#endif
             if (!__syncthreads_or(act)) break;
         }
     }
@@ -639,9 +772,22 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         uint64_t t_end;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
         L.timeline[8 * k + 1] = (int64_t)t_end;
-        L.timeline[8 * k + 2] = rounds;
-        L.timeline[8 * k + 3] = sweeps_done;
+        // rounds | levels of the last BFS << 16; sweeps | (last BFS start - CTA start, ns) << 24
+        L.timeline[8 * k + 2] = rounds | ((int64_t)lev_last << 16);
+        L.timeline[8 * k + 3] = sweeps_done | ((int64_t)(t_bfs - t_begin) << 24);
     }
+#ifdef K1_DIAG2
+    // [8K + 8k + j]: sweep j < 3 of round 1: (push scan+work, barrier, relabel, end) cycles in 16-bit
+    // fields, pushers in bits 48..63
+    if (tid == 0 && L.timeline)
+        for (int j = 0; j < 3; ++j) {
+            const long long c0 = dclk[j][0];
+            const auto f = [&](int i) { return (long long)((dclk[j][i] - dclk[j][i - 1]) & 0xFFFF); };
+            L.timeline[8 * (size_t)L.K + 8 * k + j] =
+                c0 ? (f(1) | f(2) << 16 | f(3) << 32 | (long long)(dnp[j] & 0x7FFF) << 48) : 0;
+            L.timeline[8 * (size_t)L.K + 8 * k + 3 + j] = c0 ? (dclk[j][4] - dclk[j][3]) : 0;
+        }
+#endif
     if (tid == 0) {
         atomicAdd((unsigned long long *)&L.st->solves, 1ull);
         atomicAdd((unsigned long long *)&L.st->sweeps, (unsigned long long)sweeps_done);

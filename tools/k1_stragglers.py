@@ -24,19 +24,22 @@ def main():
     _, _, problems = build_problem(wl, torch.device("cuda", 0))
     dev = _DeviceState(problems, int(wl.rho), 0.0, iters, True, True)
     K = wl.num_blocks
-    t1 = torch.zeros(8 * K, dtype=torch.int64, device="cuda")
+    # [8K, 16K): per-sweep stamps of a -DK1_DIAG2 build (DOPE_LIB=...)
+    t1 = torch.zeros(16 * K + 256, dtype=torch.int64, device="cuda")
     t2 = torch.zeros(8 * K + 64 * K, dtype=torch.int64, device="cuda")
     dev.L.fuse_multipliers = 1
     dev.call("dope_admm_init")
     agg = []
     for it in range(iters):
-        t1.view(K, 8)[:, 2] = -2
+        t1[: 16 * K].zero_()
+        t1[: 8 * K].view(K, 8)[:, 2] = -2
         dev.L.timeline = t1.data_ptr()
         dev.call("dope_update_blocks")
         dev.L.timeline = t2.data_ptr()
         dev.call("dope_update_global", fuse=1)
         torch.cuda.synchronize()
-        a = t1.view(K, 8).cpu().numpy()
+        a = t1[: 8 * K].view(K, 8).cpu().numpy()
+        d2 = t1[8 * K: 16 * K].view(K, 8).cpu().numpy()
         solved = np.nonzero(a[:, 2] >= -1)[0]
         if it < 5 or solved.size == 0:
             continue
@@ -51,14 +54,25 @@ def main():
             pro = (r[4] - r[0]) / 1e3
             bfs = (r[5] - r[4]) / 1e3
             rest = (r[1] - r[5]) / 1e3
-            parts.append(f"{tot:5.1f}us(ld {ld:4.1f} pro {pro:4.1f} bfs1 {bfs:4.1f} lev {r[6]:3d} rest {rest:5.1f} "
-                         f"rounds {r[2]} sweeps {r[3]})")
-            agg.append((tot, ld, pro, bfs, r[6], rest, r[2], r[3]))
+            rounds, lev_last = r[2] & 0xFFFF, r[2] >> 16
+            sweeps, t_last = r[3] & 0xFFFFFF, (r[3] >> 24) / 1e3
+            tail = tot - t_last   # last BFS + epilogue
+            sw = d2[k]
+            if sw[0]:
+                cyc = []
+                for j in range(3):
+                    v = int(sw[j])
+                    cyc.append(f"{v & 0xFFFF}/{(v >> 16) & 0xFFFF}/{(v >> 32) & 0xFFFF}/{sw[3 + j]}p{v >> 48}")
+                parts.append("[sweep cycles push/bar/relabel/end " + " ".join(cyc) + "]")
+            lev1, nact = r[6] & 0xFFFF, r[6] >> 16
+            parts.append(f"{tot:5.1f}us(ld {ld:4.1f} pro {pro:4.1f} bfs1 {bfs:4.1f} lev {lev1:3d} act {nact:4d} rest {rest:5.1f} "
+                         f"rounds {rounds} sweeps {sweeps} last-bfs+epi {tail:4.1f} lev {lev_last})")
+            agg.append((tot, ld, pro, bfs, lev1, rest, rounds, sweeps, tail, lev_last, nact))
         print(f"it {it + 1:3d} solved {solved.size:4d} med {med:5.1f} | " + " ".join(parts[:2]))
     A = np.array(agg, dtype=np.float64)
     if A.size:
         print("slowest-block means: total %.1f loads %.1f prologue %.1f bfs1 %.1f levels %.0f rest %.1f rounds %.1f "
-              "sweeps %.1f" % tuple(A.mean(axis=0)))
+              "sweeps %.1f last-bfs+epilogue %.1f last levels %.0f active %.0f" % tuple(A.mean(axis=0)))
         # all solved blocks of the last iteration: rounds / sweeps histogram
     dev.raise_on_error()
 

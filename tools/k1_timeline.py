@@ -50,7 +50,7 @@ def main():
             ld = (t[solved, 7] - t[solved, 0]) / 1e3
             bfs = (t[solved, 5] - t[solved, 4]) / 1e3
             rest = (t[solved, 1] - t[solved, 5]) / 1e3
-            lev = t[solved, 6]
+            lev = t[solved, 6] & 0xFFFF
             print(f"        loads med {np.median(ld):5.1f} max {ld.max():5.1f} | prologue med {np.median(pro):5.1f} max {pro.max():5.1f} | bfs1 med {np.median(bfs):5.1f} "
                   f"max {bfs.max():5.1f} levels med {np.median(lev):.0f} max {lev.max()} | rest med {np.median(rest):5.1f} "
                   f"max {rest.max():5.1f}")
