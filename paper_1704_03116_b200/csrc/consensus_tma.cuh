@@ -377,19 +377,80 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
         const int nA = bid < nsolved ? (nsolved - 1 - bid) / G + 1 : 0;
         const int nmine = nA + (bid < K ? (K - 1 - bid) / G + 1 : 0);
         CtaAgg agg;   // this CTA's pass aggregates (exact integers), lane 0
-        auto drain = [&](int s) {
-            const StageInfo info = sinfo[s];
-            if (!(info.flags & 4)) return;
-            const int k = info.k;
-            const bool ring = (info.flags & 0x10000) != 0;
-            const int64_t e = ring ? (int64_t)info.em : (int64_t)L.lamw * accE[s];
-            const int64_t u2 = (int64_t)accU[s];
-            const int64_t sq = accS[s];
-            const unsigned f = accF[s];
+        // Draining a stage is split: `take` reads the stage's descriptor and
+        // accumulators (shared memory) and resets them before the stage is
+        // refilled; `finish` then does the global writes -- per-block
+        // partials, stamps and the dirty marks -- while the refill's TMA loads
+        // are in flight.  The marks' atomics go out together, not one round
+        // trip after another (they used to stall the producer ~3 us per
+        // re-solved block).
+        struct Taken {
+            StageInfo info;
+            unsigned long long u;
+            unsigned int e, sq, f;
+        };
+        auto take = [&](int s, Taken &t) {
+            t.info = sinfo[s];
+            if (!(t.info.flags & 4)) return false;
+            t.e = accE[s];
+            t.u = accU[s];
+            t.sq = accS[s];
+            t.f = accF[s];
             accE[s] = 0;
             accS[s] = 0;
             accF[s] = 0;
             accU[s] = 0;
+            return true;
+        };
+        uint32_t *const next_list = L.dlist ? dirty_list(L, iter + 1) : nullptr;
+        // Worklist marks, software-pipelined over the CTA's drains so the
+        // producer never waits on an atomic's return value: a drain issues
+        // the exchanges of its block's marks (first marks join the worklist),
+        // turns the previous drain's exchange results into one slot
+        // reservation, and writes the entries of the reservation before that.
+        int p1k[5], p2k[5];
+        uint32_t p1old[5], p1m = 0u, p2new = 0u, p2slot = 0u;
+        auto mark_pipe = [&](const int (&kk)[5], uint32_t mm) {
+            if (p2new) {   // stage 3: entries of the reservation issued two drains ago
+                uint32_t slot = p2slot;
+#pragma unroll
+                for (int i = 0; i < 5; ++i)
+                    if (p2new >> i & 1u) {
+                        if (slot < (uint32_t)K) next_list[1 + slot] = (uint32_t)p2k[i];
+                        ++slot;
+                    }
+                p2new = 0u;
+            }
+            if (p1m) {     // stage 2: reserve slots for the first marks of the last drain
+                uint32_t nm = 0u;
+#pragma unroll
+                for (int i = 0; i < 5; ++i)
+                    if ((p1m >> i & 1u) && p1old[i] == 0u) nm |= 1u << i;
+                if (nm) {
+                    p2slot = atomicAdd(next_list, (uint32_t)__popc(nm));
+                    p2new = nm;
+#pragma unroll
+                    for (int i = 0; i < 5; ++i) p2k[i] = p1k[i];
+                }
+                p1m = 0u;
+            }
+            if (mm) {      // stage 1: the exchanges of this drain
+#pragma unroll
+                for (int i = 0; i < 5; ++i) {
+                    p1k[i] = kk[i];
+                    p1old[i] = (mm >> i & 1u) ? atomicExch(&L.dirty[kk[i]], 1u) : 1u;
+                }
+                p1m = mm;
+            }
+        };
+        auto finish = [&](const Taken &t) {
+            const StageInfo &info = t.info;
+            const int k = info.k;
+            const bool ring = (info.flags & 0x10000) != 0;
+            const int64_t e = ring ? (int64_t)info.em : (int64_t)L.lamw * t.e;
+            const int64_t u2 = (int64_t)t.u;
+            const int64_t sq = t.sq;
+            const unsigned f = t.f;
             const bool solved = info.flags & 1;
             const bool memo = solved ? (f & 64u) != 0 : (info.flags & 2) != 0;
             // ring groups: recomputed ones take this pass's clamp bits, the
@@ -404,15 +465,25 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
             L.pr[k] = sq;
             L.pf[k] = clamped | (memo ? 64 : 0) | (int)(gbits << 8);
             agg.add_block(e, u2, sq, clamped);
-            if (f & 2u) mark_dirty(L, k);
-            if (f & 4u) mark_dirty(L, k - 1);
-            if (f & 8u) mark_dirty(L, k + 1);
-            if ((f & 16u) && k - KX >= 0) mark_dirty(L, k - KX);
-            if ((f & 32u) && k + KX < K) mark_dirty(L, k + KX);
+            // dirty marks for the next iteration: self, L, R, U, D
+            const int kk[5] = {k, k - 1, k + 1, k - KX, k + KX};
+            const uint32_t mm = ((f >> 1) & 7u) | ((f & 16u) && k - KX >= 0 ? 8u : 0u) |
+                                ((f & 32u) && k + KX < K ? 16u : 0u);
+            if (!next_list) {
+#pragma unroll
+                for (int i = 0; i < 5; ++i)
+                    if (mm >> i & 1u) L.dirty[kk[i]] = 1u;
+            } else {
+                mark_pipe(kk, mm);
+            }
             // the output buffer now holds the block's whole iterate
             ybuf_stamp(L, out)[k] = ep_now;
             if (want_e) pe_stamp(L)[k] = ep_now;
             if (f & 128u) ychg_stamp(L)[k] = ep_now;
+        };
+        auto drain = [&](int s) {
+            Taken t;
+            if (take(s, t)) finish(t);
         };
         int n = 0;   // stages issued (lane 0)
         // Overlap mode: the CTAs start staggered behind K1's solves (a CTA
@@ -569,9 +640,11 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
                     const uint32_t sd = ((uint32_t)bm.flags >> 3) & 0xFu;
                     for (int tile = 0; tile < tpb; ++tile) {
                         const int s = n % ST;
+                        Taken pend;
+                        bool has_pend = false;
                         if (n >= ST) {
                             mbar_wait(&empty[s], ((n / ST) - 1) & 1);
-                            drain(s);
+                            has_pend = take(s, pend);
                         }
                         int fl = bm.flags | (tile == tpb - 1 ? 4 : 0);
                         uint8_t *stg = base + s * C::STAGE;
@@ -594,6 +667,7 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
                             stage_stamp(L, n, 0);
                             tma_issue_tile<TW, TH>(L, M, stg, &full[s], by, bx, tile, cur, fl & 1);
                         }
+                        if (has_pend) finish(pend);   // while the refill is in flight
                         ++n;
                     }
                 }
@@ -623,6 +697,11 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
             const int s = m % ST;
             mbar_wait(&empty[s], (m / ST) & 1);
             drain(s);
+        }
+        if (next_list) {   // flush the mark pipeline
+            const int none[5] = {0, 0, 0, 0, 0};
+            mark_pipe(none, 0u);
+            mark_pipe(none, 0u);
         }
         if (L.timeline) {   // diagnostics: CTA end (slot 7)
             uint64_t t;
