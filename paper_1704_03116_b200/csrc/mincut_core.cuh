@@ -18,7 +18,11 @@ struct K1FCfg {
     static constexpr size_t OFF_R = OFF_G + 4 * (size_t)M;
     static constexpr size_t OFF_H = OFF_R + 4 * (size_t)NDIR * M;
     static constexpr size_t OFF_MASK = OFF_H + 2 * (size_t)M;
-    static constexpr size_t OFF_REACH = OFF_MASK + 8 * (size_t)(NDIR + 2) * NW;
+    // BFS masks; during the sweeps the relabel candidates + one 32-slot row per warp
+    static constexpr size_t MASKB = 8 * (size_t)(NDIR + 2) * NW > 8 * (size_t)NW + (NT / 32) * 64
+                                        ? 8 * (size_t)(NDIR + 2) * NW
+                                        : 8 * (size_t)NW + (NT / 32) * 64;
+    static constexpr size_t OFF_REACH = OFF_MASK + MASKB;
     static constexpr size_t OFF_MISC = OFF_REACH + 8 * (size_t)NW;
     static constexpr size_t SMEM = OFF_MISC + 64;
 };
@@ -65,47 +69,101 @@ __device__ int mincut_solve(int32_t *g, int32_t *rr, uint16_t *h, uint64_t *mask
         if (!hit) break;
         if (++rounds > (1 << 16)) return -1;
         const int cap_sweeps = sweep_min + sweep_mul * levels;
+        // Sweeps over candidate bitmasks, as in the integer K1
+        // (dope_lattice.cu): C = nodes to push from (reach & active after the
+        // BFS), N = nodes to relabel; each warp compacts the set bits of its
+        // 32-node groups into batches of 32, one node per lane.
+        uint32_t *candC = reinterpret_cast<uint32_t *>(reach);
+        uint32_t *candN = masks32;
+        uint16_t *slots = reinterpret_cast<uint16_t *>(masks32 + 2 * NW) + warp * 32;
+        static_assert(8 * NW + (NT / 32) * 64 <= Cf::MASKB, "candidate masks and slots fit");
+        static_assert(NPT <= 32, "one group word per lane");
+        for (int w = tid; w < 2 * NW; w += NT) candC[w] &= masks32[(NDIR + 1) * 2 * NW + w];
+        __syncthreads();
+        for (int w = tid; w < 2 * NW; w += NT) candN[w] = 0u;
+        __syncthreads();
         for (int sw = 0; sw < cap_sweeps; ++sw) {
-            for (int i = 0; i < NPT; ++i) {
-                const int v = tid + i * NT;
-                const int32_t e = g[v];
-                if (e <= 0) continue;
-                const uint16_t hv = h[v];
-                if (hv == HINF || hv == 0) continue;
-                const uint16_t ht = hv - 1;
-                int32_t left = e;
-#pragma unroll
-                for (int d = 0; d < NDIR; ++d) {
-                    const int32_t rv = rr[d * M + v];
-                    if (rv == 0) continue;
-                    const int w = v + OFFS[d];
-                    if (h[w] != ht) continue;
-                    const int32_t delta = left < rv ? left : rv;
-                    rr[d * M + v] = rv - delta;
-                    rr[(d ^ 1) * M + w] += delta;
-                    atomicAdd(&g[w], delta);
-                    left -= delta;
-                    if (left == 0) break;
-                }
-                if (left != e) atomicSub(&g[v], e - left);
-            }
-            __syncthreads();
             int act = 0;
-            for (int i = 0; i < NPT; ++i) {
-                const int v = tid + i * NT;
-                if (g[v] <= 0) continue;
-                const uint16_t hv = h[v];
-                if (hv == HINF) continue;
-                uint32_t mn = HINF;
-#pragma unroll
-                for (int d = 0; d < NDIR; ++d) {
-                    if (rr[d * M + v] == 0) continue;
-                    const uint32_t hw = h[v + OFFS[d]];
-                    mn = hw < mn ? hw : mn;
+#pragma unroll 1
+            for (int phase = 0; phase < 2; ++phase) {   // 0: push from C, 1: relabel N
+                uint32_t *cand = phase == 0 ? candC : candN;
+                uint32_t gw = 0;
+                if (lane < NPT) {
+                    const int wi = lane * (NT / 32) + warp;
+                    gw = cand[wi];
+                    if (gw) cand[wi] = 0u;
                 }
-                const uint32_t nh = (mn + 1 >= (uint32_t)M) ? HINF : mn + 1;
-                if (nh != hv) h[v] = (uint16_t)nh;
-                act |= (nh != HINF);
+                uint32_t groups = __ballot_sync(FULLMASK, gw != 0u);
+                int cnt = 0;
+                while (groups || cnt) {
+                    const int i = groups ? __ffs(groups) - 1 : 0;
+                    uint32_t word = groups ? __shfl_sync(FULLMASK, gw, i) : 0u;
+                    if (groups) groups &= groups - 1;
+                    const int v = i * NT + warp * 32 + lane;
+                    const bool tail = groups == 0u;
+                    while (word || (tail && cnt)) {
+                        const bool mine = (word >> lane) & 1u;
+                        uint32_t lt;
+                        asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+                        const int rank = __popc(word & lt);
+                        const int room = 32 - cnt;
+                        if (mine && rank < room) slots[cnt + rank] = (uint16_t)v;
+                        const int nw = __popc(word);
+                        word = __ballot_sync(FULLMASK, mine && rank >= room);
+                        const int fill = cnt + (nw < room ? nw : room);
+                        if (fill < 32 && !(tail && word == 0u)) {
+                            cnt = fill;
+                            continue;
+                        }
+                        __syncwarp();
+                        if (lane < fill) {
+                            const int u = slots[lane];
+                            const int32_t e = g[u];
+                            const uint16_t hu = h[u];
+                            if (phase == 0) {
+                                if (e > 0 && hu != HINF) {
+                                    int32_t left = e;
+                                    if (hu != 0) {
+                                        const uint16_t ht = hu - 1;
+#pragma unroll
+                                        for (int d = 0; d < NDIR; ++d) {
+                                            const int32_t rv = rr[d * M + u];
+                                            if (rv == 0) continue;
+                                            const int w = u + OFFS[d];
+                                            if (h[w] != ht) continue;
+                                            const int32_t delta = left < rv ? left : rv;
+                                            rr[d * M + u] = rv - delta;
+                                            rr[(d ^ 1) * M + w] += delta;
+                                            atomicAdd(&g[w], delta);
+                                            atomicOr(&candN[w >> 5], 1u << (w & 31));
+                                            left -= delta;
+                                            if (left == 0) break;
+                                        }
+                                        if (left != e) atomicSub(&g[u], e - left);
+                                    }
+                                    if (left > 0) atomicOr(&candN[u >> 5], 1u << (u & 31));
+                                }
+                            } else if (e > 0 && hu != HINF) {
+                                uint32_t mn = HINF;
+#pragma unroll
+                                for (int d = 0; d < NDIR; ++d) {
+                                    if (rr[d * M + u] == 0) continue;
+                                    const uint32_t hw = h[u + OFFS[d]];
+                                    mn = hw < mn ? hw : mn;
+                                }
+                                const uint32_t nh = (mn + 1 >= (uint32_t)M) ? HINF : mn + 1;
+                                if (nh != hu) h[u] = (uint16_t)nh;
+                                if (nh != HINF) {
+                                    act = 1;
+                                    atomicOr(&candC[u >> 5], 1u << (u & 31));
+                                }
+                            }
+                        }
+                        __syncwarp();
+                        cnt = 0;
+                    }
+                }
+                if (phase == 0) __syncthreads();
             }
             if (!__syncthreads_or(act)) break;
         }
