@@ -115,7 +115,7 @@ typedef struct dope_lattice {
                                    current, best, and the next output         */
     uint8_t *yhat;              /* n   block labels (global layout)           */
     uint8_t *resid;             /* K * resid_stride bytes: residual graphs    */
-    uint32_t *dirty;            /* 12K + 2: [0, K) block needs a re-solve
+    uint32_t *dirty;            /* 16K + 8: [0, K) block needs a re-solve
                                    (init 1); [K, 2K) iteration + 1 of the
                                    block's last solve; [2K, 5K) pass + 1 at
                                    which y buffer b last received block k's
@@ -128,8 +128,10 @@ typedef struct dope_lattice {
                                    [9K, 11K + 2) the run loop's two dirty-block
                                    worklists [count, K entries], [11K + 2,
                                    12K + 2) iteration + 1 of the block's last
-                                   finished solve (K1 / consensus overlap):
-                                   12K + 2 in all */
+                                   finished solve (K1 / consensus overlap),
+                                   [12K + 2, 16K + 8) the consensus pass's
+                                   tile-work queue (4 words per entry, then
+                                   length, claims, CTAs done): 16K + 8 in all */
     int64_t *part_energy;       /* K   per-block pair-energy partials          */
     int64_t *part_unary;        /* K   per-block change of sum u*y2           */
     int64_t *part_ressq;        /* K   per-block sum (yhat - y)^2             */

@@ -375,8 +375,9 @@ class _DeviceState:
         # [2K, 7K): y-buffer / iterate-change / energy-partial stamps of the
         # clean-block consensus passes; [7K, 9K): the solved-block list and slots;
         # [9K, 11K + 2): the run loop's dirty-block worklists; [11K + 2, 12K + 2):
-        # finished-solve epochs (K1 / consensus overlap)
-        self.dirty = torch.zeros(12 * K + 2, dtype=torch.int32, device=dev)
+        # finished-solve epochs (K1 / consensus overlap); [12K + 2, 16K + 8): the
+        # consensus pass's tile-work queue
+        self.dirty = torch.zeros(16 * K + 8, dtype=torch.int32, device=dev)
         self.dirty[:K] = 1
         sstride = int(lb.dope_scratch_stride(C.byref(L)))
         self.scratch = torch.empty(max(K * sstride, 16), dtype=u8, device=dev)

@@ -18,14 +18,6 @@
 //     K1 clears them); each CTA then folds its own blocks into pass-wide
 //     aggregates, so the last CTA only adds up one residual sum per CTA.
 
-// work items per claim of the overlapped pass (dynamic distribution)
-#ifndef K2_CHUNK
-#define K2_CHUNK 4
-#endif
-#ifndef K2_DYN
-#define K2_DYN 0
-#endif
-
 struct TmaMaps {
     CUtensorMap a, y[3], yr[3], yhat;
     CUtensorMap yrow[3];      // y2: one row of TW (ring-only tiles)
@@ -232,6 +224,12 @@ __device__ __forceinline__ uint32_t quad_update(uint32_t h4, uint2 a2, uint32_t 
     an.x = __byte_perm((uint32_t)(a0 + h0 - y0), (uint32_t)(a1 + h1 - y1), 0x5410);
     an.y = __byte_perm((uint32_t)(a2_ + h2 - y2), (uint32_t)(a3_ + h3 - y3), 0x5410);
     return (uint32_t)(y0 | (y1 << 1) | (y2 << 2) | (y3 << 3));
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt_() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
 }
 
 // Stage descriptor written by the producer before it arms the stage's barrier
@@ -486,50 +484,73 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
             if (take(s, t)) finish(t);
         };
         int n = 0;   // stages issued (lane 0)
-        // Overlap mode: the CTAs start staggered behind K1's solves (a CTA
-        // becomes resident when K1 CTAs leave its SM), so the work items --
-        // every block (phase B) then the solved list (phase A) -- are claimed
-        // in chunks of K2_CHUNK: chunk bid first, then from a pass-wide counter
-        // (pc[7], zeroed by the last CTA).  Otherwise static round-robin.
-        // Phase-B chunks hold K2_CHUNK blocks, phase-A chunks one solved
-        // block each (a full tile pass: the heavy items, spread thin).
-        // (measured on C3: slower than the static deal -- each chunk pays a
-        // metadata round trip the static gather shares over all of a CTA's
-        // blocks; kept behind -DK2_DYN=1)
-        const bool dyn = K2_DYN && L.ovl != 0;
-        const int NB = (K + K2_CHUNK - 1) / K2_CHUNK, NCH = NB + nsolved;
-        int chunk = bid;
-        for (int c0 = 0;; c0 += 32) {
-            int nc, ibase = 0;
-            if (dyn) {
-                if (chunk >= NCH) break;
-                ibase = chunk < NB ? chunk * K2_CHUNK : K + (chunk - NB);
-                nc = chunk < NB ? (K - ibase < K2_CHUNK ? K - ibase : K2_CHUNK) : 1;
-            } else {
-                if (c0 >= nmine) break;
-                nc = nmine - c0 < 32 ? nmine - c0 : 32;
+        // Queue mode (the TMA pass with a solved list): phase B's blocks with
+        // tile work (clean full passes, ring-only) go to a pass-wide queue
+        // (L.kq) that every CTA drains once its own phase-A / phase-B work is
+        // issued, so the stage chain of a CTA no longer depends on how many
+        // such blocks its static share held (measured: 1..7 stages per CTA).
+        const bool qmode = L.kq != nullptr;
+        // overlap mode: a block whose labels (or a re-solved neighbour's) K1
+        // has not published yet is deferred behind the CTA's ready blocks,
+        // then awaited in order
+        auto ready = [&](const BlockMeta &bm) {
+            const uint32_t sd = ((uint32_t)bm.flags >> 3) & 0xFu;
+            const uint32_t *kd = L.kdone;
+            bool r = !(bm.flags & 1) || ld_acquire_gpu(kd + bm.k) == ep_now;
+            if (r && (sd & 1u)) r = ld_acquire_gpu(kd + bm.k - 1) == ep_now;
+            if (r && (sd & 2u)) r = ld_acquire_gpu(kd + bm.k + 1) == ep_now;
+            if (r && (sd & 4u)) r = ld_acquire_gpu(kd + bm.k - KX) == ep_now;
+            if (r && (sd & 8u)) r = ld_acquire_gpu(kd + bm.k + KX) == ep_now;
+            return r;
+        };
+        // the stages of one block (lane 0)
+        auto issue_block = [&](const BlockMeta &bm) {
+            const int by = (int)__umulhi((uint32_t)bm.k, kx_magic), bx = bm.k - by * KX;
+            const bool hl = bx > 0, hr = bx + 1 < KX, hu = by > 0 || L.gup, hd = by + 1 < KY || L.gdn;
+            const uint32_t sd = ((uint32_t)bm.flags >> 3) & 0xFu;
+            for (int tile = 0; tile < tpb; ++tile) {
+                const int s = n % ST;
+                Taken pend;
+                bool has_pend = false;
+                if (n >= ST) {
+                    mbar_wait(&empty[s], ((n / ST) - 1) & 1);
+                    has_pend = take(s, pend);
+                }
+                int fl = bm.flags | (tile == tpb - 1 ? 4 : 0);
+                uint8_t *stg = base + s * C::STAGE;
+                sinfo[s].k = bm.k;
+                sinfo[s].tile = tile;
+                sinfo[s].em = bm.em;
+                if (bm.mode == 1) {
+                    const bool tt = tile == 0, tb = tile == tpb - 1;
+                    const uint32_t ld = (sd & 3u) | (tt ? sd & 4u : 0u) | (tb ? sd & 8u : 0u);
+                    uint32_t crn = 0;
+                    if (tt && hu && hl && (sd & 5u)) crn |= 1u;
+                    if (tt && hu && hr && (sd & 6u)) crn |= 2u;
+                    if (tb && hd && hl && (sd & 9u)) crn |= 4u;
+                    if (tb && hd && hr && (sd & 10u)) crn |= 8u;
+                    sinfo[s].flags = fl | 0x10000 | (int)(ld << 17);
+                    stage_stamp(L, n, 0);
+                    tma_issue_ring<TW, TH>(L, M, stg, &full[s], by, bx, tile, cur, ld, crn);
+                } else {
+                    sinfo[s].flags = fl;
+                    stage_stamp(L, n, 0);
+                    tma_issue_tile<TW, TH>(L, M, stg, &full[s], by, bx, tile, cur, fl & 1);
+                }
+                if (has_pend) finish(pend);   // while the refill is in flight
+                ++n;
             }
-            // the next chunk's claim goes out now; its index is needed only
-            // after this chunk's stages are issued
-            unsigned long long claim = 0;
-            if (dyn && plane == 0)
-                claim = atomicAdd(reinterpret_cast<unsigned long long *>(&L.pc[7]), 1ull);
+        };
+        for (int c0 = 0; c0 < nmine; c0 += 32) {
+            const int nc = nmine - c0 < 32 ? nmine - c0 : 32;
             int64_t eskip = 0;
             int fskip = 0, nskip = 0;
+            bool qpush = false, qmode1 = false;
             if (plane < nc) {
                 const int j = c0 + plane;
-                bool isA;
-                int aslot, kk;
-                if (dyn) {
-                    const int item = ibase + plane;
-                    isA = item >= K;
-                    aslot = item - K;
-                    kk = isA ? (int)solved_list(L)[aslot] : item;
-                } else {
-                    isA = j < nA;
-                    aslot = bid + j * G;
-                    kk = isA ? (int)solved_list(L)[aslot] : bid + (j - nA) * G;
-                }
+                const bool isA = j < nA;
+                const int aslot = bid + j * G;
+                const int kk = isA ? (int)solved_list(L)[aslot] : bid + (j - nA) * G;
                 const int by = (int)__umulhi((uint32_t)kk, kx_magic), bx = kk - by * KX;
                 // every load of this block's metadata in one independent
                 // round (neighbour indices clamped in range, results masked)
@@ -586,8 +607,28 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
                 }
                 meta[plane].k = kk;
                 meta[plane].flags = (solved ? 1 : 0) | ((memo & 64) ? 2 : 0) | (int)(sd << 3) | (memo & 0xFF00);
-                meta[plane].mode = mode;
+                // queue mode: a phase-B block with tile work joins the pass's
+                // queue (any CTA may take it) instead of this CTA's stages
+                qpush = qmode && !isA && mode <= 1;
+                qmode1 = mode == 1;
+                meta[plane].mode = qpush ? 3 : mode;
                 meta[plane].em = em;
+            }
+            if (qmode) {   // warp-aggregated append: entry = {k + 1, flags | mode << 29, em}
+                const uint32_t qm = __ballot_sync(FULLMASK, qpush);
+                if (qm) {
+                    uint32_t slot = 0;
+                    if (plane == 0) slot = atomicAdd(L.kq + 4 * (size_t)K, (uint32_t)__popc(qm));
+                    slot = __shfl_sync(FULLMASK, slot, 0) + __popc(qm & lanemask_lt_());
+                    if (qpush) {
+                        const BlockMeta &bm = meta[plane];
+                        uint32_t *e = L.kq + 4 * (size_t)slot;
+                        e[1] = (uint32_t)bm.flags | (qmode1 ? (1u << 29) : 0u);
+                        e[2] = (uint32_t)(unsigned long long)bm.em;
+                        e[3] = (uint32_t)((unsigned long long)bm.em >> 32);
+                        st_release_gpu(e, (uint32_t)bm.k + 1u);
+                    }
+                }
             }
             // fold the settled blocks into lane 0's aggregates
             eskip = warp_sum(eskip);
@@ -605,19 +646,6 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
                     agg.F |= fskip;
                     agg.M = agg.M > 0 ? agg.M : 0;
                 }
-                // overlap mode: a block whose labels (or a re-solved
-                // neighbour's) K1 has not published yet is deferred behind
-                // the CTA's ready blocks, then awaited in order
-                auto ready = [&](const BlockMeta &bm) {
-                    const uint32_t sd = ((uint32_t)bm.flags >> 3) & 0xFu;
-                    const uint32_t *kd = L.kdone;
-                    bool r = !(bm.flags & 1) || ld_acquire_gpu(kd + bm.k) == ep_now;
-                    if (r && (sd & 1u)) r = ld_acquire_gpu(kd + bm.k - 1) == ep_now;
-                    if (r && (sd & 2u)) r = ld_acquire_gpu(kd + bm.k + 1) == ep_now;
-                    if (r && (sd & 4u)) r = ld_acquire_gpu(kd + bm.k - KX) == ep_now;
-                    if (r && (sd & 8u)) r = ld_acquire_gpu(kd + bm.k + KX) == ep_now;
-                    return r;
-                };
                 uint32_t deferred = 0;
                 for (int pass = 0; pass < (L.ovl ? 2 : 1); ++pass)
                 for (int j = 0; j < nc; ++j) {
@@ -635,45 +663,44 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
                         // labels written by other CTAs (generic proxy) before the TMA reads them
                         asm volatile("fence.proxy.async.global;" ::: "memory");
                     }
-                    const int by = (int)__umulhi((uint32_t)bm.k, kx_magic), bx = bm.k - by * KX;
-                    const bool hl = bx > 0, hr = bx + 1 < KX, hu = by > 0 || L.gup, hd = by + 1 < KY || L.gdn;
-                    const uint32_t sd = ((uint32_t)bm.flags >> 3) & 0xFu;
-                    for (int tile = 0; tile < tpb; ++tile) {
-                        const int s = n % ST;
-                        Taken pend;
-                        bool has_pend = false;
-                        if (n >= ST) {
-                            mbar_wait(&empty[s], ((n / ST) - 1) & 1);
-                            has_pend = take(s, pend);
-                        }
-                        int fl = bm.flags | (tile == tpb - 1 ? 4 : 0);
-                        uint8_t *stg = base + s * C::STAGE;
-                        sinfo[s].k = bm.k;
-                        sinfo[s].tile = tile;
-                        sinfo[s].em = bm.em;
-                        if (bm.mode == 1) {
-                            const bool tt = tile == 0, tb = tile == tpb - 1;
-                            const uint32_t ld = (sd & 3u) | (tt ? sd & 4u : 0u) | (tb ? sd & 8u : 0u);
-                            uint32_t crn = 0;
-                            if (tt && hu && hl && (sd & 5u)) crn |= 1u;
-                            if (tt && hu && hr && (sd & 6u)) crn |= 2u;
-                            if (tb && hd && hl && (sd & 9u)) crn |= 4u;
-                            if (tb && hd && hr && (sd & 10u)) crn |= 8u;
-                            sinfo[s].flags = fl | 0x10000 | (int)(ld << 17);
-                            stage_stamp(L, n, 0);
-                            tma_issue_ring<TW, TH>(L, M, stg, &full[s], by, bx, tile, cur, ld, crn);
-                        } else {
-                            sinfo[s].flags = fl;
-                            stage_stamp(L, n, 0);
-                            tma_issue_tile<TW, TH>(L, M, stg, &full[s], by, bx, tile, cur, fl & 1);
-                        }
-                        if (has_pend) finish(pend);   // while the refill is in flight
-                        ++n;
-                    }
+                    issue_block(bm);
                 }
             }
             __syncwarp();
-            if (dyn) chunk = G + __shfl_sync(FULLMASK, (int)claim, 0);
+        }
+        if (qmode) {
+            // this CTA's appends are out: count it done, then take queue
+            // entries until every CTA is done and the queue is exhausted
+            uint32_t *qlen = L.kq + 4 * (size_t)K, *qclaim = qlen + 1, *qdone = qlen + 2;
+            if (plane == 0) {
+                __threadfence();
+                atomicAdd(qdone, 1u);
+                for (;;) {
+                    const uint32_t idx = atomicAdd(qclaim, 1u);
+                    uint32_t *e = L.kq + 4 * (size_t)idx;
+                    uint32_t k1 = 0;
+                    for (;;) {
+                        if (idx < (uint32_t)K) k1 = ld_acquire_gpu(e);
+                        if (k1) break;
+                        if (ld_acquire_gpu(qdone) == (uint32_t)G && idx >= ld_acquire_gpu(qlen)) break;
+                        __nanosleep(64);
+                    }
+                    if (!k1) break;
+                    BlockMeta bm;
+                    bm.k = (int)k1 - 1;
+                    const uint32_t fw = __ldcg(e + 1);
+                    bm.flags = (int)(fw & ~(1u << 29));
+                    bm.mode = (fw >> 29) & 1u;
+                    bm.em = (long long)(((unsigned long long)__ldcg(e + 3) << 32) | __ldcg(e + 2));
+                    e[0] = 0u;   // consumed (the queue is empty again when the pass ends)
+                    if (L.ovl) {
+                        while (!ready(bm)) __nanosleep(128);
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                    }
+                    issue_block(bm);
+                }
+            }
+            __syncwarp();
         }
         if (plane != 0) return;
         if (L.timeline) {   // diagnostics: last stage issued (slot 1), stages (slot 4), phase-A blocks (slot 5)

@@ -92,6 +92,8 @@ struct Lat2 {
                             // K1 done-counter, pad, agg-slot flag per shard]
     int32_t ovl;            // run loop: the consensus pass overlaps K1 (k1_publish_done, PDL launch)
     uint32_t *kdone;        // overlap mode: iteration + 1 of each block's last FINISHED solve
+    uint32_t *kq;           // TMA consensus pass: queue of tile-work blocks (4 words each, K
+                            // entries) + [length, claims, CTAs done], or null
 };
 
 // ---------------------------------------------------------------------------
@@ -872,8 +874,9 @@ __global__ void k_init_state(Lat2 L, int64_t n) {
     // solve epochs and the stamps of the clean-block consensus passes
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 6 * (int64_t)L.K; i += stride)
             L.dirty[L.K + i] = 0u;
-    // finished-solve epochs of the overlap mode (dirty[11K + 2, 12K + 2))
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.K; i += stride)
+    // finished-solve epochs of the overlap mode (dirty[11K + 2, 12K + 2)) and
+    // the consensus pass's tile-work queue (dirty[12K + 2, 16K + 8))
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 5 * (int64_t)L.K + 6; i += stride)
         L.dirty[(size_t)11 * L.K + 2 + i] = 0u;
     if (L.dlist) {   // iteration 0 solves every block: list 0 = all, list 1 empty
         for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.K; i += stride)
@@ -1333,6 +1336,11 @@ __device__ void pass_tail(const Lat2 &L, const CtaAgg &c, int cur, int best, int
         const int F2 = (int)__ldcg(&L.pc[3]);
         const int64_t S2 = __ldcg(&L.pc[4]), X2 = __ldcg(&L.pc[5]);
         for (int i = 0; i < 8; ++i) L.pc[i] = 0;   // incl. the solved-list count
+        if (L.kq) {   // the tile-work queue's counters (its entries were cleared as taken)
+            L.kq[4 * (size_t)L.K] = 0u;
+            L.kq[4 * (size_t)L.K + 1] = 0u;
+            L.kq[4 * (size_t)L.K + 2] = 0u;
+        }
         finalize_apply(L, s0, E2, U2, S2, X2, M2, F2, cur, best, out);
         st->done_ctas = 0;
     }
@@ -2096,6 +2104,8 @@ static int build_lat2(const dope_lattice *L, Lat2 &o, const Variant **var,
     // the TMA consensus pass deals out the solved blocks when its CTAs hold
     // more than two blocks each
     o.slist = k2_tma_width(o) != 0 && o.K > 2 * K2_CPS_FWD * sm_count();
+    // ... and shares phase B's tile-work blocks through a pass-wide queue
+    if (o.slist && !getenv("DOPE_NO_K2Q")) o.kq = L->dirty + (size_t)12 * o.K + 2;
     o.q3 = is3 && (o.W % 4 == 0) && (al % 4 == 0);
     // 32^3 boxes with 2*cap <= 15 run the shared-memory K1 (nibble residuals);
     // DOPE_K1_3D=l2 forces the HBM-scratch kernel (diagnostics)
@@ -2328,7 +2338,14 @@ static int launch_k2_tma(const Lat2 &o, cudaStream_t s, int ctas_per_sm) {
         snprintf(g_last_err, sizeof(g_last_err), "cuTensorMapEncodeTiled failed");
         return DOPE_E_CUDA;
     }
-    int grid = ctas_per_sm * sm_count();
+    // every CTA must be resident at once: with the tile-work queue a CTA
+    // waits for all others to publish theirs (never more CTAs than fit)
+    static int occ = -1;
+    if (occ < 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_consensus_tma<TW, TH, NT, ST>, C::NT + 32,
+                                                                  (size_t)C::SMEM) != cudaSuccess)
+        occ = 1;
+    const int per_sm = ctas_per_sm < occ ? ctas_per_sm : (occ < 1 ? 1 : occ);
+    int grid = per_sm * sm_count();
     grid = o.K < grid ? o.K : grid;
     const uint32_t magic = (uint32_t)(((1ull << 32) + o.ax.k - 1) / o.ax.k);
     // DOPE_K2_SETTLE=0: no ring-only / settled clean blocks (A/B diagnostics)
