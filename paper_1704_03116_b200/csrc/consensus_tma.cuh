@@ -800,8 +800,9 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
                       (int64_t)uv.z * ((int)((yw >> 16) & 0xFFu) - (int)((yo >> 16) & 0xFFu)) +
                       (int64_t)uv.w * ((int)(yw >> 24) - (int)(yo >> 24));
             };
+            // defer: 0 = gather u now (ring quads), else the caller batches it
             auto update = [&](int rr, int c0, uint32_t yo, uint32_t h4, uint2 av, uint32_t cnt, uint32_t nb,
-                              bool lft, bool rgt, bool top, bool bot, int grp) {
+                              bool lft, bool rgt, bool top, bool bot, int grp, uint32_t *yw_out = nullptr) {
                 const int64_t G = gt + (int64_t)rr * W + c0;
                 uint2 an;
                 uint32_t cq = 0;
@@ -816,14 +817,16 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
                 fl |= chg ? 128u : 0u;   // the block's iterate moved (ychg stamp)
                 __stcs(reinterpret_cast<uint2 *>(a_out + G), an);
                 __stcg(reinterpret_cast<unsigned int *>(y_out + G), yw);
+                if (yw_out) *yw_out = yw;
                 if (chg) {
-                    unary(G, yw, yo);   // only where y moved
+                    if (!yw_out) unary(G, yw, yo);   // only where y moved
                     const uint32_t em = (lft ? 4u : 0u) | (rgt ? 8u : 0u) | (top ? 16u : 0u) | (bot ? 32u : 0u);
                     const uint32_t mk = 0x30u | ((chg & 0xFFu) ? 4u : 0u) | ((chg >> 24) ? 8u : 0u);
                     fl |= em & mk;
                 }
             };
             if (solved) {
+                uint32_t ywq[QPT], yoq[QPT];
 #pragma unroll
                 for (int j = 0; j < QPT; ++j) {
                     const int rr = rr_[j], c0 = c0_[j];
@@ -840,10 +843,25 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
                     if (bot) { cnt += 0x01010101u; nb += *reinterpret_cast<const uint32_t *>(hrow + C::YHW); }
                     if (lft) { cnt += 1u; nb += hrow[-1]; }
                     if (rgt) { cnt += 1u << 24; nb += (uint32_t)hrow[4] << 24; }
-                    update(rr, c0, yo, h4, av, cnt, nb, lft, rgt, top, bot, ring_group(lft, rgt, top, bot));
+                    update(rr, c0, yo, h4, av, cnt, nb, lft, rgt, top, bot, ring_group(lft, rgt, top, bot), &ywq[j]);
+                    yoq[j] = yo;
                 }
                 // the unary term of the quads whose y moved: their u loads
                 // all in flight together instead of one latency per quad
+                int4 uq[QPT];
+#pragma unroll
+                for (int j = 0; j < QPT; ++j) {
+                    const int64_t G = gt + (int64_t)rr_[j] * W + c0_[j];
+                    uq[j] = ywq[j] != yoq[j] ? __ldg(reinterpret_cast<const int4 *>(L.u + G)) : make_int4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int j = 0; j < QPT; ++j) {
+                    const uint32_t yw = ywq[j], yo = yoq[j];
+                    du += (int64_t)uq[j].x * ((int)(yw & 0xFFu) - (int)(yo & 0xFFu)) +
+                          (int64_t)uq[j].y * ((int)((yw >> 8) & 0xFFu) - (int)((yo >> 8) & 0xFFu)) +
+                          (int64_t)uq[j].z * ((int)((yw >> 16) & 0xFFu) - (int)((yo >> 16) & 0xFFu)) +
+                          (int64_t)uq[j].w * ((int)(yw >> 24) - (int)(yo >> 24));
+                }
             } else if (info.flags & 0x10000) {
                 // ring-only tile: the output buffer already holds the block's
                 // iterate and its energy partial repeats, so only the ring

@@ -622,8 +622,76 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         uint32_t *candN = masks32;                                       // 2 * NW words
         uint16_t *slots = reinterpret_cast<uint16_t *>(masks32 + 2 * NW) + warp * 32;
         static_assert(8 * NW + (NT / 32) * 64 <= 6 * 8 * NW, "candidate masks and slots fit the BFS masks");
-        for (int w = tid; w < 2 * NW; w += NT) candC[w] &= masks32[5 * 2 * NW + w];   // reach & active
+        // Dense rounds (cold solves: most nodes active) sweep every node as
+        // plain loops -- the candidate bookkeeping would only add atomics.
+        if (tid == 0) misc[2] = 0;
         __syncthreads();
+        {
+            int myc = 0;
+            for (int w = tid; w < 2 * NW; w += NT) {   // reach & active
+                const uint32_t c = candC[w] & masks32[5 * 2 * NW + w];
+                candC[w] = c;
+                myc += __popc(c);
+            }
+            if (myc) atomicAdd(&misc[2], myc);
+        }
+        __syncthreads();
+        if (misc[2] > M / 16) {
+            for (int sw = 0; sw < cap_sweeps; ++sw) {
+                ++sweeps_done;
+                // push phase: admissible arcs h(w) == h(v) - 1
+#pragma unroll 2
+                for (int i = 0; i < NPT; ++i) {
+                    const int v = tid + i * NT;
+                    const int32_t e = g[v];
+                    if (e <= 0) continue;
+                    const uint16_t hv = h[v];
+                    if (hv == HINF || hv == 0) continue;
+                    const uint16_t ht = hv - 1;
+                    int32_t left = e;
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) {
+                        const int off = (d == 0) ? 1 : (d == 1) ? -1 : (d == 2) ? BW : -BW;
+                        const int32_t rv = rr[d * M + v];
+                        if (rv == 0) continue;
+                        const int w = v + off;
+                        if (h[w] != ht) continue;
+                        const int32_t delta = left < rv ? left : rv;
+                        DOPE_ASSERT(w >= 0 && w < M && delta > 0 && rv <= 2 * cap &&
+                                    rr[(d ^ 1) * M + w] + delta <= 2 * cap);   // r + r' = 2 cap per arc pair
+                        rr[d * M + v] = (uint8_t)(rv - delta);
+                        rr[(d ^ 1) * M + w] = (uint8_t)(rr[(d ^ 1) * M + w] + delta);
+                        atomicAdd(&g[w], delta);
+                        left -= delta;
+                        if (left == 0) break;
+                    }
+                    if (left != e) atomicSub(&g[v], e - left);
+                }
+                __syncthreads();
+                // relabel phase: h(v) = 1 + min over residual arcs (monotone)
+                int act = 0;
+#pragma unroll 2
+                for (int i = 0; i < NPT; ++i) {
+                    const int v = tid + i * NT;
+                    if (g[v] <= 0) continue;
+                    const uint16_t hv = h[v];
+                    if (hv == HINF) continue;
+                    uint32_t mn = HINF;
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) {
+                        const int off = (d == 0) ? 1 : (d == 1) ? -1 : (d == 2) ? BW : -BW;
+                        if (rr[d * M + v] == 0) continue;
+                        const uint32_t hw = h[v + off];
+                        mn = hw < mn ? hw : mn;
+                    }
+                    const uint32_t nh = (mn + 1 >= (uint32_t)M) ? HINF : mn + 1;
+                    if (nh != hv) h[v] = (uint16_t)nh;
+                    act |= (nh != HINF);
+                }
+                if (!__syncthreads_or(act)) break;
+            }
+            continue;   // next round: global relabel
+        }
         for (int w = tid; w < 2 * NW; w += NT) candN[w] = 0u;
         __syncthreads();
         for (int sw = 0; sw < cap_sweeps; ++sw) {
