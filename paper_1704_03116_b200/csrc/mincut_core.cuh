@@ -78,8 +78,66 @@ __device__ int mincut_solve(int32_t *g, int32_t *rr, uint16_t *h, uint64_t *mask
         uint16_t *slots = reinterpret_cast<uint16_t *>(masks32 + 2 * NW) + warp * 32;
         static_assert(8 * NW + (NT / 32) * 64 <= Cf::MASKB, "candidate masks and slots fit");
         static_assert(NPT <= 32, "one group word per lane");
-        for (int w = tid; w < 2 * NW; w += NT) candC[w] &= masks32[(NDIR + 1) * 2 * NW + w];
+        // dense rounds (most nodes active) sweep every node as plain loops
+        if (tid == 0) misc[2] = 0;
         __syncthreads();
+        {
+            int myc = 0;
+            for (int w = tid; w < 2 * NW; w += NT) {
+                const uint32_t c = candC[w] & masks32[(NDIR + 1) * 2 * NW + w];
+                candC[w] = c;
+                myc += __popc(c);
+            }
+            if (myc) atomicAdd(&misc[2], myc);
+        }
+        __syncthreads();
+        if (misc[2] > M / 16) {
+            for (int sw = 0; sw < cap_sweeps; ++sw) {
+                for (int i = 0; i < NPT; ++i) {
+                    const int v = tid + i * NT;
+                    const int32_t e = g[v];
+                    if (e <= 0) continue;
+                    const uint16_t hv = h[v];
+                    if (hv == HINF || hv == 0) continue;
+                    const uint16_t ht = hv - 1;
+                    int32_t left = e;
+#pragma unroll
+                    for (int d = 0; d < NDIR; ++d) {
+                        const int32_t rv = rr[d * M + v];
+                        if (rv == 0) continue;
+                        const int w = v + OFFS[d];
+                        if (h[w] != ht) continue;
+                        const int32_t delta = left < rv ? left : rv;
+                        rr[d * M + v] = rv - delta;
+                        rr[(d ^ 1) * M + w] += delta;
+                        atomicAdd(&g[w], delta);
+                        left -= delta;
+                        if (left == 0) break;
+                    }
+                    if (left != e) atomicSub(&g[v], e - left);
+                }
+                __syncthreads();
+                int act = 0;
+                for (int i = 0; i < NPT; ++i) {
+                    const int v = tid + i * NT;
+                    if (g[v] <= 0) continue;
+                    const uint16_t hv = h[v];
+                    if (hv == HINF) continue;
+                    uint32_t mn = HINF;
+#pragma unroll
+                    for (int d = 0; d < NDIR; ++d) {
+                        if (rr[d * M + v] == 0) continue;
+                        const uint32_t hw = h[v + OFFS[d]];
+                        mn = hw < mn ? hw : mn;
+                    }
+                    const uint32_t nh = (mn + 1 >= (uint32_t)M) ? HINF : mn + 1;
+                    if (nh != hv) h[v] = (uint16_t)nh;
+                    act |= (nh != HINF);
+                }
+                if (!__syncthreads_or(act)) break;
+            }
+            continue;
+        }
         for (int w = tid; w < 2 * NW; w += NT) candN[w] = 0u;
         __syncthreads();
         for (int sw = 0; sw < cap_sweeps; ++sw) {
