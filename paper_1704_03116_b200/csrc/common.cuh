@@ -212,7 +212,9 @@ __device__ int bfs_relabel(const uint64_t *__restrict__ masks, uint64_t *__restr
 #pragma unroll
         for (int k = 0; k < WPL; ++k) {
             R[k] |= NEW[k];
-            uint64_t nb = NEW[k];
+            // heights only steer a following sweep: a BFS without active
+            // nodes ends the solve (hit = false), its heights are never read
+            uint64_t nb = have_active ? NEW[k] : 0ull;
             const int base = (lane * WPL + k) * 64;
             while (nb) {
                 const int b = __ffsll((long long)nb) - 1;

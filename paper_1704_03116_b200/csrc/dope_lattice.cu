@@ -251,6 +251,12 @@ __device__ __forceinline__ int warp_enqueue(uint16_t *slots, uint32_t word, int 
     return cnt;
 }
 
+// 4 bytes -> 4 bits: bit j set iff byte j is nonzero
+__device__ __forceinline__ uint32_t nz_bits4(uint32_t x) {
+    const uint32_t t = (((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;
+    return ((t >> 7) * 0x00204081u) >> 21 & 0xFu;
+}
+
 template <int BH, int BW, int NT>
 struct K1Cfg {
     static constexpr int M = BH * BW;
@@ -561,29 +567,36 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
     for (;;) {
         if (L.timeline && tid == 0)   // diagnostics: this round's BFS start
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_bfs));
-        // masks via ballots: warp covers 32 consecutive nodes per step
+#ifdef K1_DIAG2
+        long long c_r0 = clock64(), c_r1 = 0;
+#endif
+        // residual masks: one (direction, 32-node group) word per thread
+        // step, from the group's 32 residual bytes (nonzero bytes -> bits)
+        for (int p = tid; p < 4 * 2 * NW; p += NT) {
+            const int d = p / (2 * NW), w = p - d * (2 * NW);
+            const uint4 *src = reinterpret_cast<const uint4 *>(rr + d * M + 32 * w);
+            const uint4 x0 = src[0], x1 = src[1];
+            masks32[p] = nz_bits4(x0.x) | nz_bits4(x0.y) << 4 | nz_bits4(x0.z) << 8 | nz_bits4(x0.w) << 12 |
+                         nz_bits4(x1.x) << 16 | nz_bits4(x1.y) << 20 | nz_bits4(x1.z) << 24 | nz_bits4(x1.w) << 28;
+        }
+        // sink / active masks (ballots: warp covers 32 consecutive nodes per step)
 #pragma unroll 2
         for (int i = 0; i < NPT; ++i) {
             const int v = tid + i * NT;
             const int32_t gv = g[v];
-            const uint32_t bE = __ballot_sync(FULLMASK, rr[0 * M + v] != 0);
-            const uint32_t bW = __ballot_sync(FULLMASK, rr[1 * M + v] != 0);
-            const uint32_t bS = __ballot_sync(FULLMASK, rr[2 * M + v] != 0);
-            const uint32_t bN = __ballot_sync(FULLMASK, rr[3 * M + v] != 0);
             const uint32_t bK = __ballot_sync(FULLMASK, gv < 0);
             const uint32_t bA = __ballot_sync(FULLMASK, gv > 0);
             h[v] = gv < 0 ? 0 : HINF;          // sink set: level 0 (BFS skips them)
             if (lane == 0) {
                 const int w32 = (i * NT + warp * 32) >> 5;
-                masks32[0 * 2 * NW + w32] = bE;
-                masks32[1 * 2 * NW + w32] = bW;
-                masks32[2 * 2 * NW + w32] = bS;
-                masks32[3 * 2 * NW + w32] = bN;
                 masks32[4 * 2 * NW + w32] = bK;
                 masks32[5 * 2 * NW + w32] = bA;
             }
         }
         __syncthreads();
+#ifdef K1_DIAG2
+        c_r1 = clock64();
+#endif
         if (warp == 0) {
             int levels = 0;
             const int hit = bfs_relabel<NW, BW, 0>(masks, reach, h, lane, &levels);
@@ -592,6 +605,13 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         __syncthreads();
         const int hit = misc[0];
         const int levels = misc[1];
+#ifdef K1_DIAG2
+        if (tid == 0) {   // [8K + 8k + 6 / 7]: first / last round's (mask build, BFS) cycles
+            const long long c_r2 = clock64();
+            const long long v = ((c_r1 - c_r0) & 0xFFFFF) | (((c_r2 - c_r1) & 0xFFFFF) << 20) | ((long long)levels << 40);
+            if (L.timeline) L.timeline[8 * (size_t)L.K + 8 * k + (rounds == 0 ? 6 : 7)] = v;
+        }
+#endif
         if (L.timeline && tid == 0 && rounds == 0) {
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -64,6 +64,10 @@ def main():
                     v = int(sw[j])
                     cyc.append(f"{v & 0xFFFF}/{(v >> 16) & 0xFFFF}/{(v >> 32) & 0xFFFF}/{sw[3 + j]}p{v >> 48}")
                 parts.append("[sweep cycles push/bar/relabel/end " + " ".join(cyc) + "]")
+            for j, nm in ((6, "bfs1"), (7, "bfs-last")):
+                v = int(sw[j])
+                if v:
+                    parts.append(f"[{nm} masks {v & 0xFFFFF} bfs {(v >> 20) & 0xFFFFF} lev {v >> 40}]")
             lev1, nact = r[6] & 0xFFFF, r[6] >> 16
             parts.append(f"{tot:5.1f}us(ld {ld:4.1f} pro {pro:4.1f} bfs1 {bfs:4.1f} lev {lev1:3d} act {nact:4d} rest {rest:5.1f} "
                          f"rounds {rounds} sweeps {sweeps} last-bfs+epi {tail:4.1f} lev {lev_last})")
