@@ -295,8 +295,10 @@ struct K1Tune {
 #define K1_MINB_OF(bh, nt)                                                                                \
     ((bh) == 64 && (nt) == 512 ? 2                                                                        \
                                : ((nt) == 256 ? K1_MINB : ((nt) == 128 ? K1_MINB128 : ((nt) == 64 ? K1_MINB64 : 1))))
+// One block's solve (K1 body): prologue, rounds of (BFS, sweeps), epilogue.
 template <int BH, int BW, int NT>
-__global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 L, K1Tune T) {
+__device__ __forceinline__ void k1_body(const Lat2 &L, const K1Tune &T, int k, int ycur, bool last,
+                                        uint64_t t_begin) {
     using C = K1Cfg<BH, BW, NT>;
     constexpr int M = C::M, NPT = C::NPT, NW = C::NW;
     extern __shared__ __align__(16) uint8_t smem[];
@@ -307,60 +309,7 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
     uint64_t *reach = reinterpret_cast<uint64_t *>(smem + C::OFF_REACH);
     int *misc = reinterpret_cast<int *>(smem + C::OFF_MISC);
     uint32_t *masks32 = reinterpret_cast<uint32_t *>(masks);
-
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    int k = blockIdx.x;
-    uint64_t t_begin = 0;   // diagnostics: CTA start (recorded once the block is known)
-    if (L.timeline && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
-    if (L.pdl) {
-        griddep_wait();     // the previous consensus pass (PDL launch)
-        griddep_launch();   // all K1 CTAs are resident: the consensus pass may launch
-    }
-#ifdef K1_DIAG2
-    // per-SM count of resident K1 CTAs at [16K, 16K + 256) of the timeline
-    uint32_t smid_;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));
-    int *sm_cnt = L.timeline ? reinterpret_cast<int *>(L.timeline + 16 * (size_t)L.K) : nullptr;
-    if (sm_cnt && tid == 0) atomicAdd(sm_cnt + smid_, 1);
-    struct SmLeave {
-        int *c; uint32_t s; int t;
-        __device__ ~SmLeave() { if (c && t == 0) atomicSub(c + s, 1); }
-    } sm_leave_{sm_cnt, smid_, tid};
-#endif
-    int ycur;
-    if (L.dlist) {
-        // run loop: CTA i takes entry i of this iteration's dirty-block list
-        // (both lists' count and entry i are read with the run state, one
-        // round trip: most CTAs find nothing to do and must leave fast)
-        const int stop = L.st->stop;
-        ycur = L.st->ycur;
-        const int it = L.st->iteration;
-        const uint32_t bi = blockIdx.x < (unsigned)L.K ? blockIdx.x : 0u;
-        const uint32_t c0 = __ldcg(L.dlist), c1 = __ldcg(L.dlist + L.K + 1);
-        const uint32_t e0 = __ldcg(L.dlist + 1 + bi), e1 = __ldcg(L.dlist + L.K + 2 + bi);
-        if (blockIdx.x == 0 && tid == 0) {
-            dirty_list(L, it + 1)[0] = 0u;   // the next pass fills it
-            if (L.ovl) __threadfence();      // before this CTA's trigger (or exit)
-        }
-        const uint32_t cnt = (it & 1) ? c1 : c0, ent = (it & 1) ? e1 : e0;
-        if (stop || blockIdx.x >= cnt) {
-            if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
-            return;
-        }
-        k = (int)ent;
-        DOPE_ASSERT(cnt <= (uint32_t)L.K && k >= 0 && k < L.K);
-    } else {
-        // the flags and the current buffer in one round trip: a clean CTA must
-        // leave its slot fast (4096 CTAs churn through ~5 slots per SM), a
-        // dirty one needs ycur before its first data load
-        const int stop = L.st->stop;
-        ycur = L.st->ycur;
-        const uint32_t dk = L.skip_clean ? L.dirty[k] : 1u;
-        if (stop || dk == 0) {
-            if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
-            return;
-        }
-    }
     __syncthreads();
     if (L.timeline && tid == 0) {
         L.timeline[8 * k + 0] = (int64_t)t_begin;
@@ -375,9 +324,11 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         const uint32_t ep = (uint32_t)L.st->iteration + 1u;
         L.dirty[L.K + k] = ep;   // solve epoch (consensus fast path)
         if (L.slist) solved_append(L, k);
-        if (L.ovl) __threadfence();   // the consensus pass may start once every CTA triggered
+        if (L.ovl && last) __threadfence();   // the consensus pass may start once every CTA triggered
     }
-    if (L.ovl) griddep_launch();      // (a CTA triggers when all its threads did: thread 0 after its fence)
+    // (a CTA triggers when all its threads did: thread 0 after its fence; a
+    // worklist CTA at its last block)
+    if (L.ovl && last) griddep_launch();
 
     const int by = k / L.ax.k, bx = k % L.ax.k;
     int32_t lo_r, hr, lo_c, wc;
@@ -884,6 +835,115 @@ __global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 
         atomicMax(&L.st->max_rounds_seen, rounds);
     }
     if (L.ovl) k1_publish_done(L, k);
+}
+
+
+template <int BH, int BW, int NT>
+__global__ void __launch_bounds__(NT, (K1_MINB_OF(BH, NT))) k_block_mincut(Lat2 L, K1Tune T) {
+    using C = K1Cfg<BH, BW, NT>;
+    constexpr int M = C::M, NPT = C::NPT, NW = C::NW;
+    extern __shared__ __align__(16) uint8_t smem[];
+    int32_t *g = reinterpret_cast<int32_t *>(smem + C::OFF_G);
+    uint8_t *rr = smem + C::OFF_R;
+    uint16_t *h = reinterpret_cast<uint16_t *>(smem + C::OFF_H);
+    uint64_t *masks = reinterpret_cast<uint64_t *>(smem + C::OFF_MASK);
+    uint64_t *reach = reinterpret_cast<uint64_t *>(smem + C::OFF_REACH);
+    int *misc = reinterpret_cast<int *>(smem + C::OFF_MISC);
+    uint32_t *masks32 = reinterpret_cast<uint32_t *>(masks);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int k = blockIdx.x;
+    uint64_t t_begin = 0;   // diagnostics: CTA start (recorded once the block is known)
+    if (L.timeline && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+    if (L.pdl) {
+        griddep_wait();     // the previous consensus pass (PDL launch)
+        griddep_launch();   // all K1 CTAs are resident: the consensus pass may launch
+    }
+#ifdef K1_DIAG2
+    // per-SM count of resident K1 CTAs at [16K, 16K + 256) of the timeline
+    uint32_t smid_;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));
+    int *sm_cnt = L.timeline ? reinterpret_cast<int *>(L.timeline + 16 * (size_t)L.K) : nullptr;
+    if (sm_cnt && tid == 0) atomicAdd(sm_cnt + smid_, 1);
+    struct SmLeave {
+        int *c; uint32_t s; int t;
+        __device__ ~SmLeave() { if (c && t == 0) atomicSub(c + s, 1); }
+    } sm_leave_{sm_cnt, smid_, tid};
+#endif
+    int ycur;
+    if (L.dlist) {
+        // run loop: CTA i takes entry i of this iteration's dirty-block list
+        // (both lists' count and entry i are read with the run state, one
+        // round trip: most CTAs find nothing to do and must leave fast)
+        const int stop = L.st->stop;
+        ycur = L.st->ycur;
+        const int it = L.st->iteration;
+        const uint32_t bi = blockIdx.x < (unsigned)L.K ? blockIdx.x : 0u;
+        const uint32_t c0 = __ldcg(L.dlist), c1 = __ldcg(L.dlist + L.K + 1);
+        const uint32_t e0 = __ldcg(L.dlist + 1 + bi), e1 = __ldcg(L.dlist + L.K + 2 + bi);
+        if (blockIdx.x == 0 && tid == 0) {
+            dirty_list(L, it + 1)[0] = 0u;   // the next pass fills it
+            if (L.ovl) __threadfence();      // before this CTA's trigger (or exit)
+        }
+        const uint32_t cnt = (it & 1) ? c1 : c0, ent = (it & 1) ? e1 : e0;
+        if (stop || blockIdx.x >= cnt) {
+            if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
+            return;
+        }
+        k = (int)ent;
+        DOPE_ASSERT(cnt <= (uint32_t)L.K && k >= 0 && k < L.K);
+    } else {
+        // the flags and the current buffer in one round trip: a clean CTA must
+        // leave its slot fast (4096 CTAs churn through ~5 slots per SM), a
+        // dirty one needs ycur before its first data load
+        const int stop = L.st->stop;
+        ycur = L.st->ycur;
+        const uint32_t dk = L.skip_clean ? L.dirty[k] : 1u;
+        if (stop || dk == 0) {
+            if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
+            return;
+        }
+    }
+    k1_body<BH, BW, NT>(L, T, k, ycur, true, t_begin);
+    if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
+}
+
+// K1, worklist mode (run loop with dirty-block worklists): one wave of
+// resident CTAs walks the iteration's list -- CTA i takes entries i, i +
+// grid, ... -- so clean blocks cost no CTA launches (a 4096-CTA grid of
+// mostly-exiting CTAs finished dispatching ~15 us into the iteration, which
+// is when the overlapped consensus pass could start).
+#ifndef K1WL_MINB
+#define K1WL_MINB 5
+#endif
+template <int BH, int BW, int NT>
+__global__ void __launch_bounds__(NT, (BH == 64 && NT == 256 ? K1WL_MINB : K1_MINB_OF(BH, NT)))
+    k_block_mincut_wl(const __grid_constant__ Lat2 L, const __grid_constant__ K1Tune T) {
+    const int tid = threadIdx.x;
+    uint64_t t_begin = 0;
+    if (L.timeline && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+    const int stop = L.st->stop;
+    const int ycur = L.st->ycur;
+    const int it = L.st->iteration;
+    const uint32_t bi = blockIdx.x < (unsigned)L.K ? blockIdx.x : 0u;
+    const uint32_t c0 = __ldcg(L.dlist), c1 = __ldcg(L.dlist + L.K + 1);
+    const uint32_t e0 = __ldcg(L.dlist + 1 + bi), e1 = __ldcg(L.dlist + L.K + 2 + bi);
+    if (blockIdx.x == 0 && tid == 0) {
+        dirty_list(L, it + 1)[0] = 0u;   // the next pass fills it
+        if (L.ovl) __threadfence();      // before this CTA's trigger (or exit)
+    }
+    const uint32_t cnt = (it & 1) ? c1 : c0, ent = (it & 1) ? e1 : e0;
+    if (!stop) {
+        const uint32_t *lst = dirty_list(L, it);
+        DOPE_ASSERT(cnt <= (uint32_t)L.K);
+        for (uint32_t e = blockIdx.x; e < cnt; e += gridDim.x) {
+            const int k = (int)(e == blockIdx.x ? ent : __ldcg(lst + 1 + e));
+            DOPE_ASSERT(k >= 0 && k < L.K);
+            k1_body<BH, BW, NT>(L, T, k, ycur, e + gridDim.x >= cnt, t_begin);
+            __syncthreads();   // shared memory reused by the next block
+            if (L.timeline && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+        }
+    }
     if (L.peers && (L.gup | L.gdn | L.gzu | L.gzd)) k1_peer_exit(L);
 }
 
@@ -2015,11 +2075,12 @@ struct Variant {
     int bh, bw, nt;
     size_t smem;
     void (*kernel)(Lat2, K1Tune);
+    void (*kernel_wl)(Lat2, K1Tune);   // worklist mode (k_block_mincut_wl)
 };
 
 template <int BH, int BW, int NT>
 static Variant make_variant() {
-    return Variant{BH, BW, NT, K1Cfg<BH, BW, NT>::SMEM, &k_block_mincut<BH, BW, NT>};
+    return Variant{BH, BW, NT, K1Cfg<BH, BW, NT>::SMEM, &k_block_mincut<BH, BW, NT>, &k_block_mincut_wl<BH, BW, NT>};
 }
 
 static int sm_count();
@@ -2246,6 +2307,9 @@ static int configure_k1(const Variant *v) {
         int rc = cuda_check(cudaFuncSetAttribute(v->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)v->smem), "cudaFuncSetAttribute(K1)");
         if (rc) return rc;
+        rc = cuda_check(cudaFuncSetAttribute(v->kernel_wl, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)v->smem), "cudaFuncSetAttribute(K1 worklist)");
+        if (rc) return rc;
         configured[(void *)v->kernel] = true;
     }
     return DOPE_OK;
@@ -2334,13 +2398,36 @@ static int launch_digest(const Plan &P, cudaStream_t s) {
     return cuda_check(cudaGetLastError(), "state digest");
 }
 
+// resident CTAs of a 2D K1 worklist kernel per SM (its grid is one wave)
+static int k1_wave(const Variant *v) {
+    static std::mutex mu;
+    static std::map<void *, int> occ;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = occ.find((void *)v->kernel_wl);
+    if (it != occ.end()) return it->second;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, v->kernel_wl, v->nt, v->smem) != cudaSuccess || n < 1) n = 1;
+    occ[(void *)v->kernel_wl] = n;
+    return n;
+}
+
 static int launch_k1(const Plan &P, cudaStream_t s) {
     int rc = configure_plan(P);
     if (rc) return rc;
     if (P.v3 && P.o.nib3) k_block_mincut3d_s<<<P.o.K, k1s::NT, k1s::SMEM, s>>>(P.o, tune_3d());
     else if (P.v3) P.v3->kernel<<<P.o.K, P.v3->nt, P.v3->smem, s>>>(P.o, default_tune());
-    else return cuda_check(launch_pdl(P.v->kernel, dim3(P.o.K), dim3(P.v->nt), P.v->smem, s, P.o, default_tune()),
-                           "launch K1");
+    else {
+        // worklist mode: one wave walks the list (DOPE_K1_FULLGRID=1: one CTA per block)
+        static const bool full = getenv("DOPE_K1_FULLGRID") != nullptr;
+        if (P.o.dlist && !full) {
+            const int wave = k1_wave(P.v) * sm_count();
+            return cuda_check(launch_pdl(P.v->kernel_wl, dim3(wave < P.o.K ? wave : P.o.K), dim3(P.v->nt),
+                                         P.v->smem, s, P.o, default_tune()),
+                              "launch K1 (worklist)");
+        }
+        return cuda_check(launch_pdl(P.v->kernel, dim3(P.o.K), dim3(P.v->nt), P.v->smem, s, P.o, default_tune()),
+                          "launch K1");
+    }
     return cuda_check(cudaGetLastError(), "launch K1");
 }
 
@@ -2432,6 +2519,8 @@ static int launch_k2_tma(const Lat2 &o, cudaStream_t s, int ctas_per_sm) {
     if (occ < 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_consensus_tma<TW, TH, NT, ST>, C::NT + 32,
                                                                   (size_t)C::SMEM) != cudaSuccess)
         occ = 1;
+    static const int cps_env = getenv("DOPE_K2_CPS") ? atoi(getenv("DOPE_K2_CPS")) : 0;
+    if (cps_env > 0) ctas_per_sm = cps_env;
     const int per_sm = ctas_per_sm < occ ? ctas_per_sm : (occ < 1 ? 1 : occ);
     int grid = per_sm * sm_count();
     grid = o.K < grid ? o.K : grid;
