@@ -2417,9 +2417,11 @@ static int launch_k1(const Plan &P, cudaStream_t s) {
     if (P.v3 && P.o.nib3) k_block_mincut3d_s<<<P.o.K, k1s::NT, k1s::SMEM, s>>>(P.o, tune_3d());
     else if (P.v3) P.v3->kernel<<<P.o.K, P.v3->nt, P.v3->smem, s>>>(P.o, default_tune());
     else {
-        // worklist mode: one wave walks the list (DOPE_K1_FULLGRID=1: one CTA per block)
-        static const bool full = getenv("DOPE_K1_FULLGRID") != nullptr;
-        if (P.o.dlist && !full) {
+        // worklist mode, DOPE_K1_WL=1: one wave walks the list (measured on C3:
+        // the overlapped pass starts ~6 us earlier but ends no earlier, and the
+        // cold iterations are slower); default: one CTA per block
+        static const bool wl = getenv("DOPE_K1_WL") != nullptr;
+        if (P.o.dlist && wl) {
             const int wave = k1_wave(P.v) * sm_count();
             return cuda_check(launch_pdl(P.v->kernel_wl, dim3(wave < P.o.K ? wave : P.o.K), dim3(P.v->nt),
                                          P.v->smem, s, P.o, default_tune()),
