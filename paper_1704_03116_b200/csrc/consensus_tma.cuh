@@ -579,7 +579,9 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
                 if (isA) {
                     if (!solved || sl != (uint32_t)aslot + 1u) mode = 3;
                 } else if (L.skip_clean && solved) {
-                    if (sl >= 1u && sl <= (uint32_t)nsolved && __ldcg(solved_list(L) + sl - 1u) == (uint32_t)kk) mode = 3;
+                    // a block K1 solved this iteration sits in the solved list
+                    // exactly once (phase A): its slot is this iteration's
+                    if (nsolved > 0 ? (sl >= 1u && sl <= (uint32_t)nsolved) : false) mode = 3;
                 }
                 long long em = 0;
                 // clean block: neither it nor the facing pixels
@@ -614,21 +616,12 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
                 meta[plane].mode = qpush ? 3 : mode;
                 meta[plane].em = em;
             }
-            if (qmode) {   // warp-aggregated append: entry = {k + 1, flags | mode << 29, em}
-                const uint32_t qm = __ballot_sync(FULLMASK, qpush);
-                if (qm) {
-                    uint32_t slot = 0;
-                    if (plane == 0) slot = atomicAdd(L.kq + 4 * (size_t)K, (uint32_t)__popc(qm));
-                    slot = __shfl_sync(FULLMASK, slot, 0) + __popc(qm & lanemask_lt_());
-                    if (qpush) {
-                        const BlockMeta &bm = meta[plane];
-                        uint32_t *e = L.kq + 4 * (size_t)slot;
-                        e[1] = (uint32_t)bm.flags | (qmode1 ? (1u << 29) : 0u);
-                        e[2] = (uint32_t)(unsigned long long)bm.em;
-                        e[3] = (uint32_t)((unsigned long long)bm.em >> 32);
-                        st_release_gpu(e, (uint32_t)bm.k + 1u);
-                    }
-                }
+            // queue mode: this batch's appends, reserved now (lane 0), written
+            // once the CTA's own stages are issued
+            uint32_t qm = 0u, qslot = 0u;
+            if (qmode) {
+                qm = __ballot_sync(FULLMASK, qpush);
+                if (qm && plane == 0) qslot = atomicAdd(L.kq + 4 * (size_t)K, (uint32_t)__popc(qm));
             }
             // fold the settled blocks into lane 0's aggregates
             eskip = warp_sum(eskip);
@@ -667,6 +660,18 @@ __global__ void __launch_bounds__(NT_ + 32, (NT_ <= 128 ? K2T_CPS : (NT_ <= 256 
                 }
             }
             __syncwarp();
+            if (qm) {   // warp-aggregated append: entry = {k + 1, flags | mode << 29, em}
+                const uint32_t slot = __shfl_sync(FULLMASK, qslot, 0) + __popc(qm & lanemask_lt_());
+                if (qpush) {
+                    const BlockMeta &bm = meta[plane];
+                    uint32_t *e = L.kq + 4 * (size_t)slot;
+                    e[1] = (uint32_t)bm.flags | (qmode1 ? (1u << 29) : 0u);
+                    e[2] = (uint32_t)(unsigned long long)bm.em;
+                    e[3] = (uint32_t)((unsigned long long)bm.em >> 32);
+                    st_release_gpu(e, (uint32_t)bm.k + 1u);
+                }
+                __syncwarp();
+            }
         }
         if (qmode) {
             // this CTA's appends are out: count it done, then take queue
