@@ -127,10 +127,13 @@ class BlockProblems:
             self.u = torch.as_tensor(self.lowering.u, device=self.device)
         self._graph = None
 
-    def refresh_unary(self, model: EnergyModel) -> bool:
+    def refresh_unary(self, model: EnergyModel, defer_check: bool = False) -> bool:
         """Take a new model that shares this one's weights, partition and lambda:
         upload its unary (the integer path converts and checks it on the device).
-        False when the new unary does not fit this lowering."""
+        False when the new unary does not fit this lowering.  With defer_check
+        the integer check's verdict is read later (unary_confirmed), so the
+        caller can enqueue the run behind the upload without a synchronisation;
+        a lowering whose check then fails must be discarded."""
         import torch
         if model.weights is not self.model.weights or float(model.lam) != float(self.model.lam):
             return False
@@ -147,13 +150,20 @@ class BlockProblems:
             _lib.check(_lib.lib().dope_unary_i32(u64.data_ptr(), u64.numel(), self.u.data_ptr(), bad.data_ptr(),
                                                  C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)),
                        "dope_unary_i32")
-            if bad.item():
+            self._pending_bad = bad
+            if not defer_check and not self.unary_confirmed():
                 return False
         elif self.kind == "float":
             self.u.copy_(u64)
         self.model = model
         self._graph = None
         return True
+
+    def unary_confirmed(self) -> bool:
+        """The device verdict of the last deferred unary check (synchronises)."""
+        bad = getattr(self, "_pending_bad", None)
+        self._pending_bad = None
+        return bad is None or not bad.item()
 
     def run_state(self, mu, eps: float, config: "AdmmConfig"):
         """Device buffers for a run of this lowering, reused across runs with the
@@ -274,12 +284,12 @@ class _FloatDeviceState:
     def run_state(self) -> _lib.RunState:
         return _lib.RunState.from_buffer_copy(self.state.cpu().numpy().tobytes())
 
-    def y2_current(self):
+    def y2_current(self, rs=None):
         # float path stores y itself; expose 2*y for a uniform host view
-        return self.y2[self.run_state().ycur] * 2.0
+        return self.y2[(self.run_state() if rs is None else rs).ycur] * 2.0
 
-    def multipliers(self):
-        return self.a[self.run_state().parity]
+    def multipliers(self, rs=None):
+        return self.a[(self.run_state() if rs is None else rs).parity]
 
     def binarize(self):
         import torch
@@ -288,8 +298,8 @@ class _FloatDeviceState:
                    "dope_f_binarize")
         return out
 
-    def raise_on_error(self):
-        rs = self.run_state()
+    def raise_on_error(self, rs=None):
+        rs = self.run_state() if rs is None else rs
         if rs.error:
             raise BlockSolveError(rs.error - 1, "push-relabel round limit exceeded")
         return rs
@@ -312,7 +322,7 @@ def assemble_block_problems(model: EnergyModel, partition: Partition) -> BlockPr
 _lowered: dict = {}
 
 
-def _problems_for(model: EnergyModel, partition: Partition) -> BlockProblems:
+def _problems_for(model: EnergyModel, partition: Partition, defer_check: bool = False) -> BlockProblems:
     """assemble_block_problems, reused when the same weights / partition come
     back with new unaries (the serving loop of run(): the lattice checks and
     device buffers are kept, only the unary is uploaded)."""
@@ -320,12 +330,18 @@ def _problems_for(model: EnergyModel, partition: Partition) -> BlockProblems:
     key = (id(model.weights), id(partition))
     hit = _lowered.get(key)
     if hit is not None and hit[0]() is model.weights and hit[1]() is partition:
-        if hit[2].refresh_unary(model):
+        if hit[2].refresh_unary(model, defer_check):
             return hit[2]
     problems = BlockProblems(model, partition)
     drop = lambda _r, k=key: _lowered.pop(k, None)
     _lowered[key] = (weakref.ref(model.weights, drop), weakref.ref(partition, drop), problems)
     return problems
+
+
+def _forget(problems: BlockProblems):
+    for key, hit in list(_lowered.items()):
+        if hit[2] is problems:
+            _lowered.pop(key, None)
 
 
 class _DeviceState:
@@ -431,10 +447,10 @@ class _DeviceState:
         raw = self.state.cpu().numpy().tobytes()
         return _lib.RunState.from_buffer_copy(raw)
 
-    def y2_current(self):
-        return self.y2[self.run_state().ycur]
+    def y2_current(self, rs=None):
+        return self.y2[(self.run_state() if rs is None else rs).ycur]
 
-    def multipliers(self):
+    def multipliers(self, rs=None):
         return self.a
 
     def binarize(self):
@@ -444,8 +460,8 @@ class _DeviceState:
         _lib.check(lb.dope_binarize(C.byref(self.L), out.data_ptr(), self.stream()), "dope_binarize")
         return out
 
-    def raise_on_error(self):
-        rs = self.run_state()
+    def raise_on_error(self, rs=None):
+        rs = self.run_state() if rs is None else rs
         if rs.error == -1:
             raise OverflowError("a multiplier left the int16 range (|a| > 32000); "
                                 "the run exceeded the iteration range the compressed state holds")
@@ -489,20 +505,24 @@ class AdmmState:
 
     # -- construction from a finished device run --------------------------------
     @classmethod
-    def from_lattice(cls, partition: Partition, dev, mu: float) -> "AdmmState":
-        """Fields live in a lattice run's device buffers (global layout, q == 1)."""
+    def from_lattice(cls, partition: Partition, dev, mu: float, rs=None) -> "AdmmState":
+        """Fields live in a lattice run's device buffers (global layout, q == 1);
+        rs = the run state read back at the end of the run."""
         st = cls(mu=mu, partition=partition)
         st._src = ("lattice", dev)
+        st._rs = rs
         return st
 
     def _detach(self):
         """Snapshot a lattice run's fields before its device buffers are reused by
         the next run of the same problems: device-to-device copies of the
         compressed state (2y bytes, labels, multipliers), still materialised
-        lazily."""
+        lazily.  Enqueued without a synchronisation (the buffer indices come
+        from the run state read back when the run ended)."""
         if self._src is not None and self._src[0] == "lattice":
-            dev = self._src[1]
-            self._src = ("lattice_copy", (dev.y2_current().clone(), dev.yhat.clone(), dev.multipliers().clone()))
+            dev, rs = self._src[1], getattr(self, "_rs", None)
+            self._src = ("lattice_copy", (dev.y2_current(rs).clone(), dev.yhat.clone(),
+                                          dev.multipliers(rs).clone()))
 
     @classmethod
     def from_device(cls, partition: Partition, y, yhat_cat, a_cat, layout, mu: float) -> "AdmmState":
@@ -754,11 +774,18 @@ def binarize(y) -> np.ndarray:
 # run
 # ---------------------------------------------------------------------------
 
+class _StaleUnary(Exception):
+    """A deferred unary check failed: the cached integer lowering cannot take
+    this model's unary (run() re-lowers it from scratch)."""
+
+
 def _run_lattice(model, partition, config, problems) -> tuple:
     import torch
     mu0 = config.resolved_mu0(partition.shape.ndim)
     eps = config.resolved_eps(partition)
     if problems.kind == "int" and (mu0 != round(mu0) or problems.lowering.lamw % int(round(mu0)) != 0):
+        if not problems.unary_confirmed():
+            raise _StaleUnary()
         raise NotImplementedError("the integer lattice path needs an integer mu dividing lambda*w")
     dev = problems.run_state(mu0, eps, config)
     start = torch.cuda.Event(enable_timing=True)
@@ -768,16 +795,25 @@ def _run_lattice(model, partition, config, problems) -> tuple:
     dev.call("dope_admm_run", config.max_iters, int(config.use_graph), fuse=1)
     dev.call("dope_finish_run")
     end.record()
-    end.synchronize()
+    # one batch of D2H copies (labels of the best / final iterate, run state,
+    # trace) and one synchronisation
+    if getattr(problems, "_downloader", None) is None:
+        from .hostio import LabelDownloader
+        problems._downloader = LabelDownloader(problems.lowering.n)
+    small = {"state": dev.state, "e": dev.tr_e, "rs": dev.tr_rs, "mr": dev.tr_mr, "cl": dev.tr_cl}
+    if dev.trace_hash is not None:
+        small["hash"] = dev.trace_hash
+    problems._downloader.enqueue(dev.binarize(), small)
+    labels, host = problems._downloader.wait()
+    if not problems.unary_confirmed():
+        raise _StaleUnary()
     total_ms = start.elapsed_time(end)
-    rs = dev.raise_on_error()
+    rs = _lib.RunState.from_buffer_copy(host["state"].tobytes())
+    dev.raise_on_error(rs)
     it = rs.iteration
-    e = dev.tr_e[:it].cpu().numpy()
-    r2 = dev.tr_rs[:it].cpu().numpy()
-    mr = dev.tr_mr[:it].cpu().numpy()
-    cl = dev.tr_cl[:it].cpu().numpy()
+    e, r2, mr, cl = host["e"][:it], host["rs"][:it], host["mr"][:it], host["cl"][:it]
     per = total_ms / max(it, 1)   # one graph launch: the per-iteration average
-    state = AdmmState.from_lattice(partition, dev, mu0)
+    state = AdmmState.from_lattice(partition, dev, mu0, rs)
     import weakref
     problems._run_owner = weakref.ref(state)
     mu = mu0
@@ -790,11 +826,7 @@ def _run_lattice(model, partition, config, problems) -> tuple:
     state.best_iteration = int(rs.best_iteration)
     state.clamped_last = bool(cl[it - 1]) if it else False
     if dev.trace_hash is not None:
-        state.digests = dev.trace_hash[:3 * it].cpu().numpy().view(np.uint64).reshape(it, 3)
-    if getattr(problems, "_downloader", None) is None:
-        from .hostio import LabelDownloader
-        problems._downloader = LabelDownloader(problems.lowering.n)
-    labels = problems._downloader.fetch(dev.binarize())
+        state.digests = host["hash"][:3 * it].view(np.uint64).reshape(it, 3)
     return labels, state
 
 
@@ -837,13 +869,18 @@ def run(model: EnergyModel, partition: Partition, config: AdmmConfig,
     overlap = partition.overlap_pct != 0 or _max_count(partition) > 1
     lattice_ok = config.solver.kind == "maxflow"
     if lattice_ok and not overlap and config.mu_fact == 1.0:
-        if problems is None:
-            problems = _problems_for(model, partition)
+        cached = problems is None
+        if cached:
+            problems = _problems_for(model, partition, defer_check=True)
         if problems.kind in ("int", "float"):
             try:
                 return _run_lattice(model, partition, config, problems)
             except NotImplementedError:
                 pass
+            except _StaleUnary:
+                # the reused integer lowering cannot hold this unary: lower anew
+                _forget(problems)
+                return run(model, partition, config)
     if lattice_ok and partition.shape.ndim == 2:
         from .general import lower_general, run_general
         try:

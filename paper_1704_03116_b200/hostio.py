@@ -10,8 +10,10 @@ host numpy arrays).
   The uploader keeps a reference to that array so its memory cannot be
   reused while registered; a different array unregisters it.  The contents
   are read fresh on every call, so in-place edits between calls are seen.
-* Labels download.  The device labels go to a cached pinned buffer, then a
-  multi-threaded host copy fills a fresh numpy array the caller owns.
+* Labels download.  The device labels are DMA'd straight into a pooled
+  page-locked array that is handed to the caller (reused only after the
+  caller dropped it), batched with the trace / run-state reads: one
+  synchronisation per call.
 """
 from __future__ import annotations
 
@@ -92,17 +94,73 @@ class UnaryUploader:
 
 
 class LabelDownloader:
+    """Device labels -> host numpy, and the run's small results in the same
+    DMA batch (one synchronisation per run() call).
+
+    The labels land directly in page-locked memory that is handed to the
+    caller: a pool of at most POOL pinned arrays, one reused only once the
+    caller has dropped every reference to it (CPython reference count), so a
+    serving loop that keeps at most a few label arrays alive never copies
+    them on the host.  When every pooled array is still held, the labels go
+    through a pinned staging buffer into a fresh array (the copying path)."""
+
+    POOL = 4
+
     def __init__(self, n: int):
         self.n = n
-        self._pin = None
+        self._tensors = []           # pinned torch tensors backing self._arrays
+        self._arrays = []            # their numpy views (the pool)
+        self._stage = None
+        self._small = {}             # name -> pinned mirror of a small device tensor
+        self._pending = None
+
+    def _free_slot(self):
+        import sys
+        import torch
+        for k in range(len(self._arrays)):
+            if sys.getrefcount(self._arrays[k]) <= 2:   # only the pool list holds it
+                return k
+        if len(self._arrays) < self.POOL:
+            t = torch.empty(self.n, dtype=torch.int8).pin_memory()
+            self._tensors.append(t)
+            self._arrays.append(t.numpy())
+            return len(self._arrays) - 1
+        return None
+
+    def enqueue(self, labels_dev, small: dict | None = None):
+        """Enqueue the D2H copies on the labels' stream; wait() returns them."""
+        import torch
+        k = self._free_slot()
+        if k is None:
+            if self._stage is None:
+                self._stage = torch.empty(self.n, dtype=torch.int8).pin_memory()
+            dst = self._stage
+        else:
+            dst = self._tensors[k]
+        dst.copy_(labels_dev.view(torch.int8), non_blocking=True)
+        host = {}
+        for name, t in (small or {}).items():
+            pin = self._small.get(name)
+            if pin is None or pin.shape != t.shape or pin.dtype != t.dtype:
+                pin = self._small[name] = torch.empty(t.shape, dtype=t.dtype).pin_memory()
+            pin.copy_(t, non_blocking=True)
+            host[name] = pin
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(labels_dev.device))
+        self._pending = (ev, k, host)
+
+    def wait(self):
+        """(labels int8 numpy the caller owns, {name: numpy copy of each small tensor})."""
+        ev, k, host = self._pending
+        self._pending = None
+        ev.synchronize()
+        if k is None:
+            labels = self._stage.numpy().copy()
+        else:
+            labels = self._arrays[k]
+        return labels, {name: pin.numpy().copy() for name, pin in host.items()}
 
     def fetch(self, labels_dev) -> np.ndarray:
-        """uint8/int8[n] device labels -> a fresh int8 numpy array (synchronises)."""
-        import torch
-        if self._pin is None:
-            self._pin = torch.empty(self.n, dtype=torch.int8).pin_memory()
-        self._pin.copy_(labels_dev.view(torch.int8), non_blocking=True)
-        torch.cuda.current_stream(labels_dev.device).synchronize()
-        out = torch.empty(self.n, dtype=torch.int8)
-        out.copy_(self._pin)
-        return out.numpy()
+        """uint8/int8[n] device labels -> int8 numpy array (synchronises)."""
+        self.enqueue(labels_dev)
+        return self.wait()[0]

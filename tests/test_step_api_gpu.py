@@ -291,14 +291,18 @@ def test_serving_loop_refilling_one_host_buffer():
     rng = np.random.default_rng(9)
     buf = np.empty(wl.n, dtype=np.float64)
     problems = None
-    for i in range(5):
+    kept = []      # every returned label array stays alive: the pinned pool must not reuse them
+    for i in range(7):
         buf[:] = wl.u + rng.integers(-2, 3, wl.n)
         labels, state = dope.run(dope.EnergyModel(buf, weights, wl.lam), part, cfg)
         fresh = dope.run(dope.EnergyModel(buf.copy(), dope.SparseWeights(wl.n, rows, cols, vals), wl.lam),
                          dope.make_partition(dope.GridShape(wl.dims), wl.kpa, 0), cfg)
         assert labels.dtype == np.int8 and np.array_equal(labels, fresh[0])
         assert [t.energy for t in state.trace] == [t.energy for t in fresh[1].trace]
+        kept.append((labels, fresh[0].copy()))
         problems = A._problems_for(dope.EnergyModel(buf, weights, wl.lam), part)
+    for got, want in kept:
+        assert np.array_equal(got, want)
     up = problems._uploader
     assert up.registered_uploads >= 3 and up._registered is not None
     other = buf.copy()
