@@ -276,6 +276,7 @@ struct K1Cfg {
 struct K1Tune {
     int32_t sweep_min, sweep_mul;   // sweeps per round = sweep_min + sweep_mul*levels
     int32_t max_rounds;
+    int32_t dense_min, dense_mul;   // the same for dense rounds (most nodes active: cold solves)
 };
 
 // resident CTAs per SM the register allocation must allow for the 256-thread
@@ -577,7 +578,7 @@ __device__ __forceinline__ void k1_body(const Lat2 &L, const K1Tune &T, int k, i
             if (tid == 0) atomicCAS(&L.st->error, 0, k + 1);
             break;
         }
-        const int cap_sweeps = T.sweep_min + T.sweep_mul * levels;
+        int cap_sweeps = T.sweep_min + T.sweep_mul * levels;
         // The sweeps visit only candidate nodes, kept as bitmasks in the BFS
         // scratch (both rebuilt by the next BFS): C = nodes to push from
         // (initially the active nodes the BFS reached: reach & active), N =
@@ -608,6 +609,7 @@ __device__ __forceinline__ void k1_body(const Lat2 &L, const K1Tune &T, int k, i
         }
         __syncthreads();
         if (misc[2] > M / 16) {
+            cap_sweeps = T.dense_min + T.dense_mul * levels;
             for (int sw = 0; sw < cap_sweeps; ++sw) {
                 ++sweeps_done;
                 // push phase: admissible arcs h(w) == h(v) - 1
@@ -2279,6 +2281,10 @@ static K1Tune tune_3d() {
         x.max_rounds = 1 << 16;
         if (const char *e = getenv("DOPE_SWEEP3_MIN")) x.sweep_min = atoi(e);
         if (const char *e = getenv("DOPE_SWEEP3_MUL")) x.sweep_mul = atoi(e);
+        x.dense_min = x.sweep_min;
+        x.dense_mul = x.sweep_mul;
+        if (const char *e = getenv("DOPE_SWEEP3D_MIN")) x.dense_min = atoi(e);
+        if (const char *e = getenv("DOPE_SWEEP3D_MUL")) x.dense_mul = atoi(e);
         return x;
     }();
     return t;
@@ -2294,9 +2300,27 @@ static K1Tune default_tune() {
         x.max_rounds = 1 << 16;
         if (const char *e = getenv("DOPE_SWEEP_MIN")) x.sweep_min = atoi(e);
         if (const char *e = getenv("DOPE_SWEEP_MUL")) x.sweep_mul = atoi(e);
+        x.dense_min = x.sweep_min;
+        x.dense_mul = x.sweep_mul;
+        if (const char *e = getenv("DOPE_SWEEPD_MIN")) x.dense_min = atoi(e);
+        if (const char *e = getenv("DOPE_SWEEPD_MUL")) x.dense_mul = atoi(e);
         return x;
     }();
     return t;
+}
+
+// Dense rounds (cold solves) with one block per SM at most: the solve's
+// latency is K1's time and the one-warp BFS sits on the critical path, so
+// a round sweeps 1 + levels times (C1, K = 16: 40.7k -> 48.2k it/s);
+// with several waves of blocks, throughput counts and 3 sweeps per round
+// stay best (C3 / C5 b32-b128, 1 / 2 / 6 / 12 / 24 / 1 + levels measured).
+static K1Tune tune_2d(int nblocks) {
+    K1Tune x = default_tune();
+    if (!getenv("DOPE_SWEEPD_MIN") && !getenv("DOPE_SWEEPD_MUL") && nblocks <= sm_count()) {
+        x.dense_min = 1;
+        x.dense_mul = 1;
+    }
+    return x;
 }
 
 static int configure_k1(const Variant *v) {
@@ -2424,10 +2448,10 @@ static int launch_k1(const Plan &P, cudaStream_t s) {
         if (P.o.dlist && wl) {
             const int wave = k1_wave(P.v) * sm_count();
             return cuda_check(launch_pdl(P.v->kernel_wl, dim3(wave < P.o.K ? wave : P.o.K), dim3(P.v->nt),
-                                         P.v->smem, s, P.o, default_tune()),
+                                         P.v->smem, s, P.o, tune_2d(P.o.K)),
                               "launch K1 (worklist)");
         }
-        return cuda_check(launch_pdl(P.v->kernel, dim3(P.o.K), dim3(P.v->nt), P.v->smem, s, P.o, default_tune()),
+        return cuda_check(launch_pdl(P.v->kernel, dim3(P.o.K), dim3(P.v->nt), P.v->smem, s, P.o, tune_2d(P.o.K)),
                           "launch K1");
     }
     return cuda_check(cudaGetLastError(), "launch K1");
