@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
     out = CHECKED_LIB if checked else LIB
     if not force and not checked and not _stale():
         return LIB
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+    cmd = [nvcc(), "-t", "0", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
            "-Xcompiler", "-O2", "-shared", "-cudart", "static",
            f"-I{ROOT / 'include'}", f"-I{CSRC}", "-o", str(out)]
     if checked:

@@ -168,6 +168,34 @@ struct Expand<NW, WPL, LANES, BW, PL, DIAG, 0> {
                                                const uint64_t *__restrict__, int) {}
 };
 
+// Expand for 2D boxes whose rows are exactly one 64-bit word (BW == 64): the
+// row above / below is the neighbouring word (one 64-bit shuffle per lane
+// boundary), the diagonals are its 1-bit shifts -- about half the
+// instructions of the generic shifted() form, which matters because one warp
+// runs the BFS alone (its issue latency is the level time).
+template <int NW, int WPL, bool DIAG>
+__device__ __forceinline__ void expand_rows64(const uint64_t (&R)[WPL], uint64_t (&NEW)[WPL],
+                                              const uint64_t *__restrict__ m, int lane) {
+    static_assert(NW == 32 * WPL, "one lane owns WPL consecutive rows");
+    uint64_t above = __shfl_up_sync(FULLMASK, R[WPL - 1], 1);
+    uint64_t below = __shfl_down_sync(FULLMASK, R[0], 1);
+    if (lane == 0) above = 0;
+    if (lane == 31) below = 0;
+#pragma unroll
+    for (int k = 0; k < WPL; ++k) {
+        const int idx = lane * WPL + k;
+        const uint64_t own = R[k];
+        const uint64_t up = k > 0 ? R[k - 1] : above;
+        const uint64_t dn = k < WPL - 1 ? R[k + 1] : below;
+        uint64_t x = (m[0 * NW + idx] & (own >> 1)) | (m[1 * NW + idx] & (own << 1)) |
+                     (m[2 * NW + idx] & dn) | (m[3 * NW + idx] & up);
+        if constexpr (DIAG)   // SE(+BW+1) NW(-BW-1) SW(+BW-1) NE(-BW+1)
+            x |= (m[4 * NW + idx] & (dn >> 1)) | (m[5 * NW + idx] & (up << 1)) |
+                 (m[6 * NW + idx] & (dn << 1)) | (m[7 * NW + idx] & (up >> 1));
+        NEW[k] = x & ~own;
+    }
+}
+
 // Global relabel: exact BFS distances to the sink set (g < 0) over residual
 // arcs, written to h[] for nodes beyond the sink set (the caller has set
 // h = 0 on the sink set and HINF elsewhere).  `masks` holds NDIR direction
@@ -203,7 +231,10 @@ __device__ int bfs_relabel(const uint64_t *__restrict__ masks, uint64_t *__restr
             for (int k = 0; k < WPL; ++k) missing |= (A[k] & ~R[k]) != 0;
             if (!__any_sync(FULLMASK, missing)) break;
         }
-        Expand<NW, WPL, LANES, BW, PL, DIAG, WPL>::run(R, NEW, masks, lane);
+        if constexpr (PL == 0 && BW == 64 && NW >= 32)
+            expand_rows64<NW, WPL, DIAG>(R, NEW, masks, lane);
+        else
+            Expand<NW, WPL, LANES, BW, PL, DIAG, WPL>::run(R, NEW, masks, lane);
         bool grew = false;
 #pragma unroll
         for (int k = 0; k < WPL; ++k) grew |= (NEW[k] != 0);
@@ -231,6 +262,94 @@ __device__ int bfs_relabel(const uint64_t *__restrict__ masks, uint64_t *__restr
     }
     *levels_out = level;
     return __any_sync(FULLMASK, hit);
+}
+
+// Global relabel with bit-sliced levels: as bfs_relabel, but the level of a
+// newly reached node is not stored per node by its owning lane (a serial loop
+// over the frontier bits of a word: 8-connected wavefronts are squares whose
+// top / bottom edges fill whole words) -- bit b of the level is OR-ed into
+// plane b (planes[b * NW + word], zeroed by the caller) for the whole word at
+// once.  levels_to_heights() then decodes the planes with every thread of the
+// CTA.  Planes may alias the height array (decode stages through registers).
+template <int NW, int BW, int PL, bool DIAG = false>
+__device__ int bfs_relabel_planes(const uint64_t *__restrict__ masks, uint64_t *__restrict__ reach,
+                                  uint64_t *__restrict__ planes, int lane, int *levels_out) {
+    constexpr int NDIR = PL > 0 ? 6 : (DIAG ? 8 : 4);
+    constexpr int LANES = NW < 32 ? NW : 32;
+    constexpr int WPL = NW < 32 ? 1 : NW / 32;
+    static_assert(NW % LANES == 0, "word layout");
+    const uint64_t *mSink = masks + NDIR * NW, *mAct = masks + (NDIR + 1) * NW;
+    const bool on = lane < LANES;
+    uint64_t R[WPL], A[WPL], NEW[WPL];
+    bool any_act = false;
+#pragma unroll
+    for (int k = 0; k < WPL; ++k) {
+        const int idx = lane * WPL + k;
+        R[k] = on ? mSink[idx] : 0;
+        A[k] = on ? mAct[idx] : 0;
+        any_act |= (A[k] != 0);
+    }
+    const bool have_active = __any_sync(FULLMASK, any_act);
+    int level = 0;
+    for (;;) {
+        if (have_active) {
+            bool missing = false;
+#pragma unroll
+            for (int k = 0; k < WPL; ++k) missing |= (A[k] & ~R[k]) != 0;
+            if (!__any_sync(FULLMASK, missing)) break;
+        }
+        if constexpr (PL == 0 && BW == 64 && NW >= 32)
+            expand_rows64<NW, WPL, DIAG>(R, NEW, masks, lane);
+        else
+            Expand<NW, WPL, LANES, BW, PL, DIAG, WPL>::run(R, NEW, masks, lane);
+        bool grew = false;
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) grew |= (NEW[k] != 0);
+        if (!__any_sync(FULLMASK, grew)) break;
+        ++level;
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) R[k] |= NEW[k];
+        if (have_active) {
+            // heights only steer a following sweep (see bfs_relabel)
+            for (int lv = level, b = 0; lv; lv >>= 1, ++b) {
+                if (!(lv & 1)) continue;
+#pragma unroll
+                for (int k = 0; k < WPL; ++k)
+                    if (on && NEW[k]) planes[b * NW + lane * WPL + k] |= NEW[k];
+            }
+        }
+    }
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < WPL; ++k) {
+        if (on) reach[lane * WPL + k] = R[k];
+        hit |= (A[k] & R[k]) != 0;
+    }
+    *levels_out = level;
+    return __any_sync(FULLMASK, hit);
+}
+
+// Every thread of the CTA: heights from the level planes of a BFS that ran
+// `levels` levels (h = level for reached nodes -- 0 on the sink set -- HINF
+// otherwise).  planes may alias h: the bits are gathered into registers,
+// then -- behind a barrier -- the heights are written.
+template <int M, int NT>
+__device__ __forceinline__ void levels_to_heights(const uint64_t *planes, const uint64_t *__restrict__ reach,
+                                                  uint16_t *h, int levels) {
+    constexpr int NPT = M / NT, NW = M / 64;
+    const int np = 32 - __clz(levels);
+    uint16_t hv[NPT];
+#pragma unroll
+    for (int i = 0; i < NPT; ++i) {
+        const int v = threadIdx.x + i * NT;
+        const int word = v >> 6, bit = v & 63;
+        uint32_t x = 0;
+        for (int b = 0; b < np; ++b) x |= (uint32_t)((planes[b * NW + word] >> bit) & 1ull) << b;
+        hv[i] = ((reach[word] >> bit) & 1ull) ? (uint16_t)x : HINF;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NPT; ++i) h[threadIdx.x + i * NT] = hv[i];
 }
 
 // ---------------------------------------------------------------------------

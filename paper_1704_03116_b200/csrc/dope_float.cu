@@ -100,6 +100,8 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
     const int k = blockIdx.x;
     if (L.st->stop) return;
     if (L.skip_clean && L.dirty[k] == 0) return;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(misc + 8);
+    if (tid == 0) mc_bar_init(bar);
     __syncthreads();
     if (tid == 0) {
         L.dirty[k] = 0;
@@ -109,6 +111,12 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
     int32_t lo_r, hr, lo_c, wc;
     L.ay.range(by, lo_r, hr);
     L.ax.range(bx, lo_c, wc);
+#ifdef K1F_DIAG
+    if (tid == 0 && k < 4096) {
+        for (int i = 0; i < 16; ++i) g_k1f_diag[16 * k + i] = 0;
+        g_k1f_diag[16 * k + 0] = k1f_now();
+    }
+#endif
     const int32_t Wg = L.W, H = L.ay.dim;
     const double *__restrict__ a_cur = L.st->parity ? L.a1 : L.a0;
     const double *__restrict__ y_cur = L.y[L.st->ycur];
@@ -119,11 +127,12 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
     // (all 16-byte loads in flight); the stored flow is then read back from
     // them through the arc-pair invariant r(v->w) + r(w->v) = 2 cap(v,w), so
     // no capacity plane is re-read: net inflow on arc d = (r_d(v) - r_d'(w)) / 2.
-    if (L.warm) {
-        const int4 *src = reinterpret_cast<const int4 *>(gres);
-        int4 *dst = reinterpret_cast<int4 *>(rr);
-#pragma unroll 4
-        for (int i = tid; i < NDIR * M / 4; i += NT) dst[i] = src[i];
+    if (L.warm && tid == 0) {
+        // one bulk copy per plane (16-byte loads by the threads took 8 dependent
+        // round trips: 9 us of prologue per solve)
+        mc_bar_expect(bar, NDIR * M * 4);
+#pragma unroll
+        for (int d = 0; d < NDIR; ++d) mc_bulk_load(rr + d * M, gres + d * M, M * 4, bar);
     }
     for (int i = 0; i < NPT; ++i) {
         const int v = tid + i * NT;
@@ -170,6 +179,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
         }
         g[v] = gv;
     }
+    if (L.warm) mc_bar_wait(bar, 0);
     __syncthreads();
     if (L.warm) {
         for (int i = 0; i < NPT; ++i) {
@@ -188,20 +198,32 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
         __syncthreads();
     }
 
-    if (mincut_solve<BH, BW, NT, NDIR>(g, rr, h, masks, reach, misc, sweep_min, sweep_mul) < 0 && tid == 0)
-        atomicCAS(&L.st->error, 0, k + 1);
+    K1F_D(1, = k1f_now());
+    {
+        const int rounds_ = mincut_solve<BH, BW, NT, NDIR>(g, rr, h, masks, reach, misc, sweep_min, sweep_mul);
+        if (rounds_ < 0 && tid == 0) atomicCAS(&L.st->error, 0, k + 1);
+        K1F_D(3, = rounds_);
+        K1F_D(2, = k1f_now());
+    }
+    if (L.warm) {
+        // the residual planes go back by bulk stores while the labels are written
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll
+            for (int d = 0; d < NDIR; ++d) mc_bulk_store(gres + d * M, rr + d * M, M * 4);
+        }
+    }
     for (int i = 0; i < NPT; ++i) {
         const int v = tid + i * NT;
         const int r = v / BW, c = v % BW;
         if (r < hr && c < wc)
             L.yhat[(int64_t)(lo_r + r) * Wg + lo_c + c] = (uint8_t)((reach[v >> 6] >> (v & 63)) & 1ull);
     }
-    if (L.warm) {
-        int4 *dst = reinterpret_cast<int4 *>(gres);
-        const int4 *src = reinterpret_cast<const int4 *>(rr);
-        for (int i = tid; i < NDIR * M / 4; i += NT) dst[i] = src[i];
-    }
+    if (L.warm && tid == 0) mc_bulk_store_wait();
     if (tid == 0) atomicAdd((unsigned long long *)&L.st->solves, 1ull);
+    __syncthreads();
+    K1F_D(7, = k1f_now());
 }
 
 // cold residual planes (quantised capacities of in-block arcs)
@@ -851,6 +873,11 @@ int dope_f_update_multipliers(const dope_lattice_f *L, void *stream) {
 }
 
 // Audit mode: digest of the iteration's labels (y and a are not integers here).
+#ifdef K1F_DIAG
+extern "C" int dope_f_diag_read(long long *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, dope_f::g_k1f_diag, sizeof(long long) * n);
+}
+#endif
 static int launch_digest_f(const LatF &o, cudaStream_t s) {
     if (!o.trace_hash) return DOPE_OK;
     k_digest_begin<<<1, 1, 0, s>>>(o.st, o.trace_hash, o.max_iters);

@@ -31,6 +31,49 @@ struct K1FCfg {
 // rr[d*M + v] = residual of arc v -> v + off(d) (directions E W S N SE NW SW NE,
 // opposite = d ^ 1).  Leaves the sink-reachable set in reach[].  Returns the
 // number of global-relabel rounds, or -1 past the round limit.
+// ---- bulk (TMA) copies of a block's residual planes, one issuing thread ----
+__device__ __forceinline__ uint32_t mc_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mc_bar_init(uint64_t *bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mc_smem(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mc_bar_expect(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mc_smem(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mc_bar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "MCWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra MCWAIT_%=;\n"
+        "}\n" ::"r"(mc_smem(bar)), "r"(parity), "r"(0x989680) : "memory");
+}
+__device__ __forceinline__ void mc_bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(mc_smem(dst)), "l"(src), "r"(bytes), "r"(mc_smem(bar)) : "memory");
+}
+__device__ __forceinline__ void mc_bulk_store(void *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(dst), "r"(mc_smem(src)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mc_bulk_store_wait() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+#ifdef K1F_DIAG
+static __device__ long long g_k1f_diag[16 * 4096];
+__device__ __forceinline__ long long k1f_now() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define K1F_D(slot, expr) do { if (threadIdx.x == 0 && blockIdx.x < 4096) g_k1f_diag[16 * blockIdx.x + (slot)] expr; } while (0)
+#else
+#define K1F_D(slot, expr) do { } while (0)
+#endif
+
 template <int BH, int BW, int NT, int NDIR>
 __device__ int mincut_solve(int32_t *g, int32_t *rr, uint16_t *h, uint64_t *masks, uint64_t *reach, int *misc,
                             int sweep_min, int sweep_mul) {
@@ -49,7 +92,6 @@ __device__ int mincut_solve(int32_t *g, int32_t *rr, uint16_t *h, uint64_t *mask
             for (int d = 0; d < NDIR; ++d) b[d] = __ballot_sync(FULLMASK, rr[d * M + v] != 0);
             const uint32_t bK = __ballot_sync(FULLMASK, gvv < 0);
             const uint32_t bA = __ballot_sync(FULLMASK, gvv > 0);
-            h[v] = gvv < 0 ? 0 : HINF;
             if (lane == 0) {
                 const int w32 = (i * NT + warp * 32) >> 5;
 #pragma unroll
@@ -58,16 +100,22 @@ __device__ int mincut_solve(int32_t *g, int32_t *rr, uint16_t *h, uint64_t *mask
                 masks32[(NDIR + 1) * 2 * NW + w32] = bA;
             }
         }
+        // level planes of the BFS live in the height array until they are decoded
+        uint64_t *planes = reinterpret_cast<uint64_t *>(h);
+        for (int w = tid; w < M / 4; w += NT) planes[w] = 0ull;
         __syncthreads();
         if (warp == 0) {
             int levels = 0;
-            const int hit = bfs_relabel<NW, BW, 0, NDIR == 8>(masks, reach, h, lane, &levels);
+            const int hit = bfs_relabel_planes<NW, BW, 0, NDIR == 8>(masks, reach, planes, lane, &levels);
             if (lane == 0) { misc[0] = hit; misc[1] = levels; }
         }
         __syncthreads();
         const int hit = misc[0], levels = misc[1];
+        K1F_D(4, += levels);
+        K1F_D(8, = rounds == 0 ? k1f_now() : g_k1f_diag[16 * blockIdx.x + 8]);
         if (!hit) break;
         if (++rounds > (1 << 16)) return -1;
+        levels_to_heights<M, NT>(planes, reach, h, levels);   // published by the barriers below
         const int cap_sweeps = sweep_min + sweep_mul * levels;
         // Sweeps over candidate bitmasks, as in the integer K1
         // (dope_lattice.cu): C = nodes to push from (reach & active after the
@@ -91,8 +139,11 @@ __device__ int mincut_solve(int32_t *g, int32_t *rr, uint16_t *h, uint64_t *mask
             if (myc) atomicAdd(&misc[2], myc);
         }
         __syncthreads();
+        K1F_D(9, += misc[2]);
         if (misc[2] > M / 16) {
+            K1F_D(6, += 1);
             for (int sw = 0; sw < cap_sweeps; ++sw) {
+                K1F_D(5, += 1);
                 for (int i = 0; i < NPT; ++i) {
                     const int v = tid + i * NT;
                     const int32_t e = g[v];
@@ -142,6 +193,7 @@ __device__ int mincut_solve(int32_t *g, int32_t *rr, uint16_t *h, uint64_t *mask
         __syncthreads();
         for (int sw = 0; sw < cap_sweeps; ++sw) {
             int act = 0;
+            K1F_D(5, += 1);
 #pragma unroll 1
             for (int phase = 0; phase < 2; ++phase) {   // 0: push from C, 1: relabel N
                 uint32_t *cand = phase == 0 ? candC : candN;
@@ -183,12 +235,22 @@ __device__ int mincut_solve(int32_t *g, int32_t *rr, uint16_t *h, uint64_t *mask
                                     int32_t left = e;
                                     if (hu != 0) {
                                         const uint16_t ht = hu - 1;
+                                        // every arc's residual and head height first (independent
+                                        // loads), then the sequential split of the excess
+                                        int32_t rvs[NDIR];
+                                        uint16_t hws[NDIR];
 #pragma unroll
                                         for (int d = 0; d < NDIR; ++d) {
-                                            const int32_t rv = rr[d * M + u];
+                                            rvs[d] = rr[d * M + u];
+                                            const int w = u + OFFS[d];
+                                            hws[d] = h[w < 0 ? 0 : (w >= M ? M - 1 : w)];
+                                        }
+#pragma unroll
+                                        for (int d = 0; d < NDIR; ++d) {
+                                            const int32_t rv = rvs[d];
                                             if (rv == 0) continue;
                                             const int w = u + OFFS[d];
-                                            if (h[w] != ht) continue;
+                                            if (hws[d] != ht) continue;
                                             const int32_t delta = left < rv ? left : rv;
                                             rr[d * M + u] = rv - delta;
                                             rr[(d ^ 1) * M + w] += delta;
