@@ -134,53 +134,97 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
 #pragma unroll
         for (int d = 0; d < NDIR; ++d) mc_bulk_load(rr + d * M, gres + d * M, M * 4, bar);
     }
-    for (int i = 0; i < NPT; ++i) {
-        const int v = tid + i * NT;
-        const int r = v / BW, c = v % BW;
-        const bool valid = r < hr && c < wc;
-        int32_t gv = 0;
-        if (valid) {
+    // (a) the ring of border nodes, one per thread (its cross-block sum needs
+    //     up to 2 * NDIR more operands: all loads of a node in flight together,
+    //     and no interior warp diverges into it); (b) the interior nodes, the
+    //     four operands of a batch of nodes in flight together.
+    {
+        const int nring = (hr <= 2 || wc <= 2) ? hr * wc : 2 * wc + 2 * (hr - 2);
+        for (int t = tid; t < nring; t += NT) {
+            int r, c;
+            if (hr <= 2 || wc <= 2) { r = t / wc; c = t - r * wc; }
+            else if (t < wc) { r = 0; c = t; }
+            else if (t < 2 * wc) { r = hr - 1; c = t - wc; }
+            else { const int q = t - 2 * wc; r = 1 + (q >> 1); c = (q & 1) ? wc - 1 : 0; }
             const int32_t R = lo_r + r, Cc = lo_c + c;
             const int64_t G = (int64_t)R * Wg + Cc;
             // cross-block neighbours in ascending global index: NW N NE W E SW S SE
             constexpr int ORD8[8] = {5, 3, 7, 1, 0, 6, 2, 4};
             constexpr int ORD4[4] = {3, 1, 0, 2};
-            double cy = 0.0;
-            const bool border = r == 0 || c == 0 || r == hr - 1 || c == wc - 1;
-            if (border) {
+            double tw[NDIR], ty[NDIR];
 #pragma unroll
-                for (int t = 0; t < NDIR; ++t) {
-                    const int d = NDIR == 8 ? ORD8[t] : ORD4[t];
-                    const int rn = R + dy_of(d), cn = Cc + dx_of(d);
-                    if (rn < 0 || rn >= H || cn < 0 || cn >= Wg) continue;
-                    if (rn >= lo_r && rn < lo_r + hr && cn >= lo_c && cn < lo_c + wc) continue;
-                    int pl;
-                    const int64_t low = pair_low(L, G, d, pl);
-                    cy += (-L.w[pl][low]) * y_cur[(int64_t)rn * Wg + cn];
-                }
+            for (int t2 = 0; t2 < NDIR; ++t2) {
+                const int d = NDIR == 8 ? ORD8[t2] : ORD4[t2];
+                const int rn = R + dy_of(d), cn = Cc + dx_of(d);
+                const bool cross = !(rn < 0 || rn >= H || cn < 0 || cn >= Wg) &&
+                                   !(rn >= lo_r && rn < lo_r + hr && cn >= lo_c && cn < lo_c + wc);
+                int pl;
+                const int64_t low = pair_low(L, G, d, pl);
+                tw[t2] = cross ? L.w[pl][low] : 0.0;
+                ty[t2] = cross ? y_cur[(int64_t)rn * Wg + cn] : 0.0;
             }
-            const double sy = y_cur[G];
-            const double lin = L.u[G] + L.lam * (cy + L.rdiag[G] * sy) + L.mu * ((a_cur[G] - sy) + 0.5);
+            const double sy = y_cur[G], uu = L.u[G], rd = L.rdiag[G], av = a_cur[G];
+            double cy = 0.0;
+#pragma unroll
+            for (int t2 = 0; t2 < NDIR; ++t2) {
+                const int d = NDIR == 8 ? ORD8[t2] : ORD4[t2];
+                const int rn = R + dy_of(d), cn = Cc + dx_of(d);
+                if (rn < 0 || rn >= H || cn < 0 || cn >= Wg) continue;
+                if (rn >= lo_r && rn < lo_r + hr && cn >= lo_c && cn < lo_c + wc) continue;
+                cy += (-tw[t2]) * ty[t2];
+            }
+            const double lin = uu + L.lam * (cy + rd * sy) + L.mu * ((av - sy) + 0.5);
             const double qv = rint(lin * L.qs);
-            gv = (int32_t)fmax(fmin(qv, 1.0e9), -1.0e9);
+            g[r * BW + c] = (int32_t)fmax(fmin(qv, 1.0e9), -1.0e9);
+        }
+    }
+    constexpr int GRP = NPT < 4 ? NPT : 4;   // nodes per batch of loads (register budget)
+#pragma unroll 1
+    for (int i0 = 0; i0 < NPT; i0 += GRP) {
+        double p_u[GRP], p_y[GRP], p_rd[GRP], p_a[GRP];
+#pragma unroll
+        for (int i = 0; i < GRP; ++i) {
+            const int v = tid + (i0 + i) * NT;
+            const int r = v / BW, c = v % BW;
+            const bool inner = r > 0 && c > 0 && r < hr - 1 && c < wc - 1;
+            const int64_t G = (int64_t)(lo_r + r) * Wg + lo_c + c;
+            p_u[i] = inner ? L.u[G] : 0.0;
+            p_y[i] = inner ? y_cur[G] : 0.0;
+            p_rd[i] = inner ? L.rdiag[G] : 0.0;
+            p_a[i] = inner ? a_cur[G] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < GRP; ++i) {
+            const int v = tid + (i0 + i) * NT;
+            const int r = v / BW, c = v % BW;
+            const bool valid = r < hr && c < wc;
+            const bool inner = r > 0 && c > 0 && r < hr - 1 && c < wc - 1;
+            if (inner) {
+                const double sy = p_y[i];
+                const double lin = p_u[i] + L.lam * (0.0 + p_rd[i] * sy) + L.mu * ((p_a[i] - sy) + 0.5);
+                const double qv = rint(lin * L.qs);
+                g[v] = (int32_t)fmax(fmin(qv, 1.0e9), -1.0e9);
+            } else if (!valid) {
+                g[v] = 0;
+            }
             if (!L.warm) {
+                const int64_t G = (int64_t)(lo_r + r) * Wg + lo_c + c;
 #pragma unroll
                 for (int d = 0; d < NDIR; ++d) {
                     const int rb = r + dy_of(d), cb = c + dx_of(d);
-                    const bool has = rb >= 0 && rb < hr && cb >= 0 && cb < wc;
+                    const bool has = valid && rb >= 0 && rb < hr && cb >= 0 && cb < wc;
                     int pl;
                     const int64_t low = pair_low(L, G, d, pl);
                     rr[d * M + v] = has ? L.cq[pl][low] : 0;
                 }
             }
-        } else if (!L.warm) {
-#pragma unroll
-            for (int d = 0; d < NDIR; ++d) rr[d * M + v] = 0;
         }
-        g[v] = gv;
     }
+    K1F_D(10, = k1f_now());
     if (L.warm) mc_bar_wait(bar, 0);
+    K1F_D(11, = k1f_now());
     __syncthreads();
+    K1F_D(12, = k1f_now());
     if (L.warm) {
         for (int i = 0; i < NPT; ++i) {
             const int v = tid + i * NT;

@@ -54,7 +54,7 @@ def main():
         parts = []
         for j in order:
             x = r[j]
-            parts.append(f"[{(x[7]-x[0])/1e3:.1f}us pro {(x[1]-x[0])/1e3:.1f} bfs1 {(x[8]-x[1])/1e3:.1f} "
+            parts.append(f"[{(x[7]-x[0])/1e3:.1f}us pro {(x[1]-x[0])/1e3:.1f} (lin {(x[10]-x[0])/1e3:.1f} bulk {(x[11]-x[10])/1e3:.1f} sync {(x[12]-x[11])/1e3:.1f}) bfs1 {(x[8]-x[1])/1e3:.1f} "
                          f"solve {(x[2]-x[1])/1e3:.1f} epi {(x[7]-x[2])/1e3:.1f} rounds {x[3]} dense {x[6]} "
                          f"lev {x[4]} sw {x[5]} cand {x[9]}]")
         span = (r[:, 7].max() - r[:, 0].min()) / 1e3
