@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
         y_out[G] = y;
         const double dlt = yh - y;
         ss += dlt * dlt;
-        if (want_e && mode == 0) {
+        if (want_e && mode == 0 && border) {   // interior pixels: the energy pass below
             double q = 0.0;
             // pairs owned by this pixel: E S SE SW (forward planes)
             if (Cc + 1 < W) { const double d = yold - y_in[G + 1]; q += w0[G] * (d * d); }
@@ -589,10 +589,67 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
     // interior pixels (a fixed point in the ring-only modes)
     const int iw = wc - 2, ih = hr - 2;
     const int mi = (iw > 0 && ih > 0 && mode == 0) ? iw * ih : 0;
+    // The energy of the previous iterate reads only planes nothing writes in
+    // this pass: its own loop, so the loads of several pixels are in flight
+    // together (inside pixel() every pixel's loads waited behind the previous
+    // pixel's in-place multiplier store).  Same per-thread summation order.
+    if (want_e) {
 #pragma unroll 4
-    for (int v = tid; v < mi; v += K2F_NT) {
-        const int r = v / iw, c = v - r * iw;
-        pixel(r + 1, c + 1, false);
+        for (int v = tid; v < mi; v += K2F_NT) {
+            const int r = v / iw + 1, c = v % iw + 1;
+            const int32_t R = lo_r + r, Cc = lo_c + c;
+            const int64_t G = (int64_t)R * W + Cc;
+            const double yold = y_in[G];
+            double q = 0.0;
+            if (Cc + 1 < W) { const double d = yold - y_in[G + 1]; q += w0[G] * (d * d); }
+            if (R + 1 < H) {
+                const double d = yold - y_in[G + W];
+                q += w1[G] * (d * d);
+                if (L.ndir == 8) {
+                    if (Cc + 1 < W) { const double d2 = yold - y_in[G + W + 1]; q += w2[G] * (d2 * d2); }
+                    if (Cc > 0) { const double d3 = yold - y_in[G + W - 1]; q += w3[G] * (d3 * d3); }
+                }
+            }
+            e_acc += uu[G] * yold + L.lam * q;
+        }
+    }
+    // interior update (no cross-block term): the operands of a batch of pixels
+    // first, then the in-place stores
+    constexpr int KB = 4;
+    for (int v0 = tid; v0 < mi; v0 += KB * K2F_NT) {
+        double b_a[KB], b_rd[KB], b_yo[KB], b_yh[KB];
+        int64_t b_G[KB];
+#pragma unroll
+        for (int j = 0; j < KB; ++j) {
+            const int v = v0 + j * K2F_NT;
+            const bool ok = v < mi;
+            const int r = ok ? v / iw + 1 : 1, c = ok ? v % iw + 1 : 1;
+            const int64_t G = (int64_t)(lo_r + r) * W + lo_c + c;
+            b_G[j] = ok ? G : -1;
+            b_yh[j] = (double)yhp[G];
+            b_a[j] = a_in[G];
+            b_rd[j] = rdg[G];
+            b_yo[j] = y_in[G];
+        }
+#pragma unroll
+        for (int j = 0; j < KB; ++j) {
+            const int64_t G = b_G[j];
+            if (G < 0) continue;
+            const double yh = b_yh[j], av = b_a[j];
+            const double own = L.mu * (yh + av) - L.lam * (b_rd[j] * yh);
+            const double acc = 0.0 + own;
+            const double yp = L.inv_mu != 0.0 ? acc * L.inv_mu : acc / (L.mu * 1.0);
+            clamped |= (yp < 0.0 || yp > 1.0);
+            const double y = yp < 0.0 ? 0.0 : (yp > 1.0 ? 1.0 : yp);
+            const double yold = b_yo[j];
+            if (a_out) a_out[G] = av + (yh - y);
+            y_out[G] = y;
+            const double dlt = yh - y;
+            ss += dlt * dlt;
+            const bool ychg = (y != yold);
+            if (ychg || (av + (yh - y)) != av) marks |= 1u;
+            if (ychg) marks |= 1u << 10;
+        }
     }
     const int clamped_int = clamped;
     // the ring of border pixels: top row, bottom row, then left / right columns

@@ -266,10 +266,11 @@ __device__ int mincut_solve(int32_t *g, int32_t *rr, uint16_t *h, uint64_t *mask
                             } else if (e > 0 && hu != HINF) {
                                 uint32_t mn = HINF;
 #pragma unroll
-                                for (int d = 0; d < NDIR; ++d) {
-                                    if (rr[d * M + u] == 0) continue;
-                                    const uint32_t hw = h[u + OFFS[d]];
-                                    mn = hw < mn ? hw : mn;
+                                for (int d = 0; d < NDIR; ++d) {   // independent loads (clamped index)
+                                    const int w = u + OFFS[d];
+                                    const uint32_t hw = h[w < 0 ? 0 : (w >= M ? M - 1 : w)];
+                                    const uint32_t cand = rr[d * M + u] != 0 ? hw : (uint32_t)HINF;
+                                    mn = cand < mn ? cand : mn;
                                 }
                                 const uint32_t nh = (mn + 1 >= (uint32_t)M) ? HINF : mn + 1;
                                 if (nh != hu) h[u] = (uint16_t)nh;
