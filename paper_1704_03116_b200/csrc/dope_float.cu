@@ -411,7 +411,14 @@ __device__ __forceinline__ void k2f_finalize(const LatF &L, int cur, int best, i
     }
 }
 
+#ifdef K1F_DIAG
+static __device__ long long g_k2f_diag[16 * 4096];
+#define K2F_D(slot) do { if (threadIdx.x == 0 && blockIdx.x < 4096) g_k2f_diag[16 * blockIdx.x + (slot)] = k1f_now(); } while (0)
+#else
+#define K2F_D(slot) do { } while (0)
+#endif
 __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
+    K2F_D(0);
     if (L.st->stop) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int k = blockIdx.x;
@@ -466,6 +473,10 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
         mode = m;
     }
     __syncthreads();
+    K2F_D(1);
+#ifdef K1F_DIAG
+    if (threadIdx.x == 0) g_k2f_diag[16 * blockIdx.x + 15] = mode;
+#endif
     if (mode == 2 || mode == 4) {   // the output buffer holds an older iterate of this block: copy
         for (int v = tid; v < hr * wc; v += K2F_NT) {
             const int r = v / wc, c = v - r * wc;
@@ -515,15 +526,29 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
             double nb_term[8];
             int64_t nb_idx[8];
             int nn = 0;
-            for (int d = 0; d < L.ndir; ++d) {
+            // every cross-block neighbour's weight and label first (independent
+            // loads), then the block-id ordering on registers
+            double p_w[8];
+            uint8_t p_yh[8];
+#pragma unroll
+            for (int d = 0; d < 8; ++d) {
+                const int rn = R + dy_of(d), cn = Cc + dx_of(d);
+                const bool in = d < L.ndir && !(rn < 0 || rn >= H || cn < 0 || cn >= W);
+                const bool cross = in && !(rn >= lo_r && rn < lo_r + hr && cn >= lo_c && cn < lo_c + wc);
+                int pl;
+                const int64_t low = pair_low(L, G, d, pl);
+                p_w[d] = cross ? L.w[pl][low] : 0.0;
+                p_yh[d] = cross ? L.yhat[(int64_t)rn * W + cn] : (uint8_t)0;
+            }
+#pragma unroll
+            for (int d = 0; d < 8; ++d) {
+                if (d >= L.ndir) break;
                 const int rn = R + dy_of(d), cn = Cc + dx_of(d);
                 if (rn < 0 || rn >= H || cn < 0 || cn >= W) continue;
                 // neighbour at distance 1: its block is this one or the adjacent one
                 const int br = by + (rn < lo_r ? -1 : (rn >= lo_r + hr ? 1 : 0));
                 const int bc = bx + (cn < lo_c ? -1 : (cn >= lo_c + wc ? 1 : 0));
                 if (br == by && bc == bx) continue;
-                int pl;
-                const int64_t low = pair_low(L, G, d, pl);
                 const int64_t J = (int64_t)rn * W + cn;
                 int q = nn++;
                 const int bid = br * L.ax.k + bc;
@@ -533,7 +558,7 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
                 }
                 nb_blk[q] = bid;
                 nb_idx[q] = J;
-                nb_term[q] = (-L.w[pl][low]) * (double)L.yhat[J];
+                nb_term[q] = (-p_w[d]) * (double)p_yh[d];
             }
             bool own_done = false;
             int t2 = 0;
@@ -613,6 +638,7 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
             e_acc += uu[G] * yold + L.lam * q;
         }
     }
+    K2F_D(2);
     // interior update (no cross-block term): the operands of a batch of pixels
     // first, then the in-place stores
     constexpr int KB = 4;
@@ -651,6 +677,7 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
             if (ychg) marks |= 1u << 10;
         }
     }
+    K2F_D(3);
     const int clamped_int = clamped;
     // the ring of border pixels: top row, bottom row, then left / right columns
     const int nring = (hr <= 2 || wc <= 2) ? hr * wc : 2 * wc + 2 * (hr - 2);
@@ -662,6 +689,7 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
         else { const int u = t - 2 * wc; r = 1 + (u >> 1); c = (u & 1) ? wc - 1 : 0; }
         pixel(r, c, true);
     }
+    K2F_D(4);
     constexpr int NWARP = K2F_NT / 32;
     __shared__ double red_e[NWARP], red_s[NWARP];
     __shared__ int red_f[NWARP];
@@ -676,6 +704,7 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
         atomicOr(&nbmark, marks);
     }
     __syncthreads();
+    K2F_D(5);
     if (tid == 0) {
         double E = 0.0, S = 0.0;
         int F = 0;
@@ -700,7 +729,9 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
         last = (atomicAdd(&L.st->done_ctas, 1) == L.K - 1);
     }
     __syncthreads();
+    K2F_D(6);
     if (last) k2f_finalize(L, cur, best, out);
+    K2F_D(7);
 }
 
 __global__ void k_update_multipliers_f(LatF L, int64_t n) {
@@ -977,6 +1008,9 @@ int dope_f_update_multipliers(const dope_lattice_f *L, void *stream) {
 #ifdef K1F_DIAG
 extern "C" int dope_f_diag_read(long long *host, int n) {
     return (int)cudaMemcpyFromSymbol(host, dope_f::g_k1f_diag, sizeof(long long) * n);
+}
+extern "C" int dope_f_diag_read_k2(long long *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, dope_f::g_k2f_diag, sizeof(long long) * n);
 }
 #endif
 static int launch_digest_f(const LatF &o, cudaStream_t s) {

@@ -38,6 +38,21 @@ def main():
         e2.record()
         torch.cuda.synchronize()
         lb.dope_f_diag_read(host.ctypes.data_as(C.c_void_p), C.c_int(16 * K))
+        h2 = np.zeros(16 * K, dtype=np.int64)
+        lb.dope_f_diag_read_k2(h2.ctypes.data_as(C.c_void_p), C.c_int(16 * K))
+        b = h2.reshape(K, 16)
+        if it >= 12:
+            t0k = b[:, 0].min()
+            end = np.where(b[:, 7] > 0, b[:, 7], b[:, 1])
+            slow = np.argsort(end)[::-1][:3]
+            msg = []
+            for k in slow:
+                x = b[k]
+                msg.append(f"[blk {k} mode {x[15]} start {(x[0]-t0k)/1e3:.1f} mode@ {(x[1]-t0k)/1e3:.1f} E {(x[2]-t0k)/1e3:.1f} "
+                           f"int {(x[3]-t0k)/1e3:.1f} ring {(x[4]-t0k)/1e3:.1f} red {(x[5]-t0k)/1e3:.1f} "
+                           f"tail {(x[6]-t0k)/1e3:.1f} end {(x[7]-t0k)/1e3:.1f}]")
+            modes = np.bincount(b[:, 15].astype(int), minlength=5)
+            print(f"   K2f modes {modes.tolist()} " + " ".join(msg))
         a = host.reshape(K, 16)
         solved = np.nonzero(a[:, 2] >= a[:, 0] + 1)[0]
         solved = solved[a[solved, 0] > 0]
