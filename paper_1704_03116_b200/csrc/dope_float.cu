@@ -518,6 +518,24 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
         const int64_t G = (int64_t)R * W + Cc;
         const double yh = (double)yhp[G];
         const double av = a_in[G];
+        const double yold = y_in[G];
+        // ring pixels: the energy term of the previous iterate first, so that its
+        // loads travel with the pixel's other operands (one round trip less)
+        double e_term = 0.0;
+        if (want_e && mode == 0 && border) {
+            double q = 0.0;
+            // pairs owned by this pixel: E S SE SW (forward planes)
+            if (Cc + 1 < W) { const double d = yold - y_in[G + 1]; q += w0[G] * (d * d); }
+            if (R + 1 < H) {
+                const double d = yold - y_in[G + W];
+                q += w1[G] * (d * d);
+                if (L.ndir == 8) {
+                    if (Cc + 1 < W) { const double d2 = yold - y_in[G + W + 1]; q += w2[G] * (d2 * d2); }
+                    if (Cc > 0) { const double d3 = yold - y_in[G + W - 1]; q += w3[G] * (d3 * d3); }
+                }
+            }
+            e_term = uu[G] * yold + L.lam * q;
+        }
         // own-block term and cross-block coupling sums, in block-id order
         const double own = L.mu * (yh + av) - L.lam * (rdg[G] * yh);
         double acc = 0.0;
@@ -579,25 +597,11 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
         const double yp = L.inv_mu != 0.0 ? acc * L.inv_mu : acc / (L.mu * 1.0);
         clamped |= (yp < 0.0 || yp > 1.0);
         const double y = yp < 0.0 ? 0.0 : (yp > 1.0 ? 1.0 : yp);
-        const double yold = y_in[G];
         if (a_out) a_out[G] = av + (yh - y);
         y_out[G] = y;
         const double dlt = yh - y;
         ss += dlt * dlt;
-        if (want_e && mode == 0 && border) {   // interior pixels: the energy pass below
-            double q = 0.0;
-            // pairs owned by this pixel: E S SE SW (forward planes)
-            if (Cc + 1 < W) { const double d = yold - y_in[G + 1]; q += w0[G] * (d * d); }
-            if (R + 1 < H) {
-                const double d = yold - y_in[G + W];
-                q += w1[G] * (d * d);
-                if (L.ndir == 8) {
-                    if (Cc + 1 < W) { const double d2 = yold - y_in[G + W + 1]; q += w2[G] * (d2 * d2); }
-                    if (Cc > 0) { const double d3 = yold - y_in[G + W - 1]; q += w3[G] * (d3 * d3); }
-                }
-            }
-            e_acc += uu[G] * yold + L.lam * q;
-        }
+        if (want_e && mode == 0 && border) e_acc += e_term;
         const bool ychg = (y != yold);
         if (ychg || (av + (yh - y)) != av) marks |= 1u;
         if (ychg) marks |= 1u << 10;
