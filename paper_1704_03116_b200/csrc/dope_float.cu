@@ -942,7 +942,10 @@ static int launch_k1(const LatF &o, const VarF *v, cudaStream_t s) {
     // 6 fixed sweeps measured best on C2 (K1 10.4 -> 7.8 ms per run vs 1 + levels)
     static const int smin = getenv("DOPE_SWEEPF_MIN") ? atoi(getenv("DOPE_SWEEPF_MIN")) : 6;
     static const int smul = getenv("DOPE_SWEEPF_MUL") ? atoi(getenv("DOPE_SWEEPF_MUL")) : 0;
-    v->kernel<<<o.K, v->nt, v->smem, s>>>(o, smin, smul);
+    // dense rounds (DOPE_SWEEPF_DMIN / _DMUL; 0 / unset: as the sparse rounds)
+    static const int dmin = getenv("DOPE_SWEEPF_DMIN") ? atoi(getenv("DOPE_SWEEPF_DMIN")) : 0;
+    static const int dmul = getenv("DOPE_SWEEPF_DMUL") ? atoi(getenv("DOPE_SWEEPF_DMUL")) : 0;
+    v->kernel<<<o.K, v->nt, v->smem, s>>>(o, smin | (dmin << 16), smul | (dmul << 16));
     return cuda_check(cudaGetLastError(), "launch K1f");
 }
 

@@ -116,7 +116,10 @@ __device__ int mincut_solve(int32_t *g, int32_t *rr, uint16_t *h, uint64_t *mask
         if (!hit) break;
         if (++rounds > (1 << 16)) return -1;
         levels_to_heights<M, NT>(planes, reach, h, levels);   // published by the barriers below
-        const int cap_sweeps = sweep_min + sweep_mul * levels;
+        // sweeps per relabel: min + mul * levels; dense rounds (cold solves) may
+        // carry their own pair in the high halves of the two arguments
+        const int cap_sweeps = (sweep_min & 0xFFFF) + (sweep_mul & 0xFFFF) * levels;
+        const int cap_dense = (sweep_min >> 16) ? (sweep_min >> 16) + (sweep_mul >> 16) * levels : cap_sweeps;
         // Sweeps over candidate bitmasks, as in the integer K1
         // (dope_lattice.cu): C = nodes to push from (reach & active after the
         // BFS), N = nodes to relabel; each warp compacts the set bits of its
@@ -142,7 +145,7 @@ __device__ int mincut_solve(int32_t *g, int32_t *rr, uint16_t *h, uint64_t *mask
         K1F_D(9, += misc[2]);
         if (misc[2] > M / 16) {
             K1F_D(6, += 1);
-            for (int sw = 0; sw < cap_sweeps; ++sw) {
+            for (int sw = 0; sw < cap_dense; ++sw) {
                 K1F_D(5, += 1);
                 for (int i = 0; i < NPT; ++i) {
                     const int v = tid + i * NT;
