@@ -315,7 +315,10 @@ __device__ int bfs_relabel_planes(const uint64_t *__restrict__ masks, uint64_t *
                 if (!(lv & 1)) continue;
 #pragma unroll
                 for (int k = 0; k < WPL; ++k)
-                    if (on && NEW[k]) planes[b * NW + lane * WPL + k] |= NEW[k];
+                    if (on && NEW[k]) {
+                        DOPE_ASSERT(b < 16 && (NEW[k] & R[k]) == NEW[k]);   // planes fit the height array
+                        planes[b * NW + lane * WPL + k] |= NEW[k];
+                    }
             }
         }
     }
@@ -338,6 +341,7 @@ __device__ __forceinline__ void levels_to_heights(const uint64_t *planes, const 
                                                   uint16_t *h, int levels) {
     constexpr int NPT = M / NT, NW = M / 64;
     const int np = 32 - __clz(levels);
+    DOPE_ASSERT(levels > 0 && levels < M && np <= 16);
     uint16_t hv[NPT];
 #pragma unroll
     for (int i = 0; i < NPT; ++i) {

@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
     if (L.warm && tid == 0) {
         // one bulk copy per plane (16-byte loads by the threads took 8 dependent
         // round trips: 9 us of prologue per solve)
+        DOPE_ASSERT((reinterpret_cast<uintptr_t>(gres) & 15) == 0);
         mc_bar_expect(bar, NDIR * M * 4);
 #pragma unroll
         for (int d = 0; d < NDIR; ++d) mc_bulk_load(rr + d * M, gres + d * M, M * 4, bar);

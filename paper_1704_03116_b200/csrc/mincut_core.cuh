@@ -255,6 +255,8 @@ __device__ int mincut_solve(int32_t *g, int32_t *rr, uint16_t *h, uint64_t *mask
                                             const int w = u + OFFS[d];
                                             if (hws[d] != ht) continue;
                                             const int32_t delta = left < rv ? left : rv;
+                                            DOPE_ASSERT(w >= 0 && w < M && delta > 0 && h[w] == ht &&
+                                                        rr[d * M + u] == rv);
                                             rr[d * M + u] = rv - delta;
                                             rr[(d ^ 1) * M + w] += delta;
                                             atomicAdd(&g[w], delta);
