@@ -1,6 +1,13 @@
 """Anatomy of the float path's block solves on C2 (diagnostics, -DK1F_DIAG
 build loaded with DOPE_LIB): per iteration the solved blocks' time split
-(prologue / solve / epilogue), relabel rounds, BFS levels, sweeps."""
+(prologue / solve / epilogue), relabel rounds, BFS levels, sweeps; from
+iteration 12 on also the consensus pass's slowest CTAs (mode, phase stamps).
+
+    nvcc -t 0 -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
+        -Xcompiler -fPIC -shared -cudart static -Iinclude -Ipaper_1704_03116_b200/csrc \
+        -DK1F_DIAG -o paper_1704_03116_b200/libdope_k1fdiag.so paper_1704_03116_b200/csrc/*.cu
+    DOPE_LIB=$PWD/paper_1704_03116_b200/libdope_k1fdiag.so python tools/k1f_diag.py C2 24 3
+"""
 import ctypes as C
 import sys
 from pathlib import Path
