@@ -393,6 +393,15 @@ typedef struct dope_lattice_f {
     int32_t *trace_clamped;
     uint64_t *trace_hash;       /* optional audit digests (labels only), as in
                                    dope_lattice                                */
+    int32_t energy_prepass;     /* 1: the block min-cut kernel also sums the
+                                   energy of the current iterate over the
+                                   interior of every block it re-solves (in
+                                   the warps that wait for a relabel BFS), so
+                                   the consensus pass skips that loop.  Needs
+                                   dirty = 7K words ([6K, 7K): pass of each
+                                   block's interior energy) and part_energy =
+                                   33K doubles ([K, 33K): 32 per-warp sums per
+                                   block).  0: the 6K / K layouts              */
 } dope_lattice_f;
 
 int64_t dope_f_resid_stride(const dope_lattice_f *L);

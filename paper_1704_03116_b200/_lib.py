@@ -126,6 +126,7 @@ class LatticeF(C.Structure):
         ("trace_max_residual", C.c_void_p),
         ("trace_clamped", C.c_void_p),
         ("trace_hash", C.c_void_p),
+        ("energy_prepass", C.c_int32),
     ]
 
 

@@ -18,6 +18,8 @@ path's device kernels with the reference's host-visible state semantics.
 """
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 import math
 from dataclasses import dataclass, field
@@ -234,9 +236,11 @@ class _FloatDeviceState:
         self.resid = torch.zeros(K * stride // 4, dtype=torch.int32, device=dev)
         # [0, K) re-solve flags, [K, 2K) solve epochs, [2K, 5K) y-buffer stamps,
         # [5K, 6K) last change of each block's iterate (clean-block pass)
-        self.dirty = torch.zeros(6 * K, dtype=torch.int32, device=dev)
+        # [6K, 7K) pass of each block's interior energy from K1f (energy_prepass)
+        self.dirty = torch.zeros(7 * K, dtype=torch.int32, device=dev)
         self.dirty[:K] = 1
-        self.pe = torch.zeros(K, dtype=f64, device=dev)
+        self.pe = torch.zeros(33 * K, dtype=f64, device=dev)   # [K, 33K): K1f's per-warp interior energy sums
+        L.energy_prepass = int(os.environ.get("DOPE_F_EPRE", "1"))
         self.pr = torch.zeros(K, dtype=f64, device=dev)
         self.pf = torch.zeros(K, dtype=torch.int32, device=dev)
         self.state = torch.zeros(C.sizeof(_lib.RunState), dtype=torch.uint8, device=dev)

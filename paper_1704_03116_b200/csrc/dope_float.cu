@@ -46,6 +46,7 @@ struct LatF {
     double lam, mu, eps, qs;
     double inv_mu;                // 1/mu when mu is a power of two (x/mu == x*inv_mu exactly), else 0
     int32_t warm, skip_clean, fuse, max_iters, K, boxh, boxw;
+    int32_t epre;                 // dope_lattice_f.energy_prepass
     const double *u, *rdiag;
     const double *w[4];          // E S SE SW, weight of pair (i, i+off) at i
     const int32_t *cq[4];        // quantised lam*w*S, same layout
@@ -82,6 +83,53 @@ __device__ __forceinline__ int64_t pair_low(const LatF &L, int64_t G, int d, int
     }
 }
 
+// Energy of the current iterate over a re-solved block's interior pixels (the
+// term the consensus pass needs of its "previous" iterate, energy.py:187-194):
+// computed inside K1f by the warps that would otherwise wait for warp 0's BFS,
+// a chunk of (NT - 32) pixels per BFS, the rest after the solve (under the
+// residual planes' bulk stores).  Partial
+// sums live in shared memory (no register is held across the solve).
+template <int NT>
+struct EnergyIdle {
+    const LatF &L;
+    double *eacc;          // [NT] per-thread partial sums (shared)
+    const double *y;       // the current iterate
+    int32_t lo_r, lo_c, iw, mi;
+    static constexpr int CH = NT - 32;
+    __device__ __forceinline__ double pixel(int p) const {
+        const int r = p / iw + 1, c = p - (r - 1) * iw + 1;
+        const int64_t W = L.W;
+        const int64_t G = (int64_t)(lo_r + r) * W + lo_c + c;
+        // interior pixels: every forward pair exists (E S [SE SW])
+        const double yo = y[G];
+        const double d0 = yo - y[G + 1], d1 = yo - y[G + W];
+        double q = L.w[0][G] * (d0 * d0);
+        q += L.w[1][G] * (d1 * d1);
+        if (L.ndir == 8) {
+            const double d2 = yo - y[G + W + 1], d3 = yo - y[G + W - 1];
+            q += L.w[2][G] * (d2 * d2);
+            q += L.w[3][G] * (d3 * d3);
+        }
+        return L.u[G] * yo + L.lam * q;
+    }
+    // chunks per BFS (1 and 2 measured alike on C2; with 2 a solve with two
+    // BFS runs leaves nothing for the tail)
+    #ifndef K1F_EPRE_PER_CALL
+#define K1F_EPRE_PER_CALL 2
+#endif
+    static constexpr int PER_CALL = K1F_EPRE_PER_CALL;
+    __device__ __forceinline__ void operator()(int call) const {
+        const int t = (int)threadIdx.x - 32;
+        double e = 0.0;
+#pragma unroll
+        for (int j = 0; j < PER_CALL; ++j) {
+            const int p = (PER_CALL * call + j) * CH + t;
+            if (p < mi) e += pixel(p);
+        }
+        eacc[threadIdx.x] += e;
+    }
+};
+
 // ---------------------------------------------------------------------------
 // K1f: block min cut, quantised float capacities, 4/8 directions
 // ---------------------------------------------------------------------------
@@ -96,8 +144,10 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
     uint64_t *masks = reinterpret_cast<uint64_t *>(smem + Cf::OFF_MASK);
     uint64_t *reach = reinterpret_cast<uint64_t *>(smem + Cf::OFF_REACH);
     int *misc = reinterpret_cast<int *>(smem + Cf::OFF_MISC);
+    double *eacc = reinterpret_cast<double *>(smem + Cf::SMEM);   // [NT], after the core's layout
     const int tid = threadIdx.x;
     const int k = blockIdx.x;
+    const int it0 = L.st->iteration;   // with the stop flag: one round trip
     if (L.st->stop) return;
     if (L.skip_clean && L.dirty[k] == 0) return;
     uint64_t *bar = reinterpret_cast<uint64_t *>(misc + 8);
@@ -105,7 +155,7 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
     __syncthreads();
     if (tid == 0) {
         L.dirty[k] = 0;
-        L.dirty[L.K + k] = (uint32_t)L.st->iteration + 1u;   // solve epoch (K2f's clean-block pass)
+        L.dirty[L.K + k] = (uint32_t)it0 + 1u;   // solve epoch (K2f's clean-block pass)
     }
     const int by = k / L.ax.k, bx = k - by * L.ax.k;
     int32_t lo_r, hr, lo_c, wc;
@@ -244,8 +294,15 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
     }
 
     K1F_D(1, = k1f_now());
+    // interior energy of the current iterate for the consensus pass (run loop,
+    // from the second iteration on): see EnergyIdle
+    const int e_iw = wc - 2, e_ih = hr - 2;
+    const bool e_on = L.fuse && L.epre && it0 >= 1 && e_iw > 0 && e_ih > 0;
+    const EnergyIdle<NT> eidle{L, eacc, y_cur, lo_r, lo_c, e_iw, e_on ? e_iw * e_ih : 0};
+    eacc[tid] = 0.0;
+    int rounds_;
     {
-        const int rounds_ = mincut_solve<BH, BW, NT, NDIR>(g, rr, h, masks, reach, misc, sweep_min, sweep_mul);
+        rounds_ = mincut_solve<BH, BW, NT, NDIR>(g, rr, h, masks, reach, misc, sweep_min, sweep_mul, eidle);
         if (rounds_ < 0 && tid == 0) atomicCAS(&L.st->error, 0, k + 1);
         K1F_D(3, = rounds_);
         K1F_D(2, = k1f_now());
@@ -264,6 +321,21 @@ __global__ void __launch_bounds__(NT) k_block_mincut_f(LatF L, int sweep_min, in
         const int r = v / BW, c = v % BW;
         if (r < hr && c < wc)
             L.yhat[(int64_t)(lo_r + r) * Wg + lo_c + c] = (uint8_t)((reach[v >> 6] >> (v & 63)) & 1ull);
+    }
+    // the interior energy's tail and block sum overlap the bulk stores
+    if (e_on && rounds_ >= 0) {
+        // chunks the BFS waits did not reach (rounds_ + 1 BFS runs)
+        const int done = EnergyIdle<NT>::PER_CALL * (rounds_ + 1) * EnergyIdle<NT>::CH;
+        double e = 0.0;
+#pragma unroll 4
+        for (int p = done + tid; p < eidle.mi; p += NT) e += eidle.pixel(p);   // loads of all chunks in flight
+        e += eacc[tid];
+        // per-warp sums (32 slots per block; absent warps hold 0): the consensus
+        // pass folds them in a fixed order -- no CTA barrier on K1f's tail
+        e = warp_sum(e);
+        if ((tid & 31) == 0) L.pe[L.K + 32 * (size_t)k + (tid >> 5)] = e;
+        if (NT < 1024 && tid < 32 && tid >= NT / 32) L.pe[L.K + 32 * (size_t)k + tid] = 0.0;
+        if (tid == 0) L.dirty[6 * L.K + k] = (uint32_t)it0 + 1u;   // ... of this pass
     }
     if (L.warm && tid == 0) mc_bulk_store_wait();
     if (tid == 0) atomicAdd((unsigned long long *)&L.st->solves, 1ull);
@@ -308,6 +380,7 @@ __global__ void k_init_state_f(LatF L, int64_t n) {
         L.dirty[3 * L.K + i] = 0xFFFFFFFFu;    // ... buffers 1, 2 nothing yet
         L.dirty[4 * L.K + i] = 0xFFFFFFFFu;
         L.dirty[5 * L.K + i] = 0u;             // pass of the last change of the block's iterate
+        if (L.epre) L.dirty[6 * L.K + i] = 0u; // pass of K1f's interior energy sum
         L.pe[i] = 0.0;
         L.pr[i] = 0.0;
         L.pf[i] = 0;
@@ -446,8 +519,10 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
     // buffer; 3 ring only (a neighbour was re-solved), 4 ring only + copy
     __shared__ int mode;
     __shared__ int last;
+    __shared__ int epre;                   // K1f summed this block's interior energy in this pass
     if (tid == 0) {
         nbmark = 0;
+        epre = L.epre && L.dirty[6 * L.K + k] == (uint32_t)(iteration + 1);
         // Clean-block fixed point: a block K1 did not re-solve
         // had y and a unmoved (so y == yhat) in the previous pass, and no
         // border pixel next to it moved either; if none of its 8 neighbours
@@ -623,7 +698,13 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
     // this pass: its own loop, so the loads of several pixels are in flight
     // together (inside pixel() every pixel's loads waited behind the previous
     // pixel's in-place multiplier store).  Same per-thread summation order.
-    if (want_e) {
+    __shared__ double epre_sum;
+    if (want_e && epre && warp == 1) {   // K1f's 32 per-warp interior sums, fixed order
+        double v = L.pe[L.K + 32 * (size_t)k + lane];
+        v = warp_sum(v);
+        if (lane == 0) epre_sum = v;
+    }
+    if (want_e && !epre) {
 #pragma unroll 4
         for (int v = tid; v < mi; v += K2F_NT) {
             const int r = v / iw + 1, c = v % iw + 1;
@@ -715,6 +796,7 @@ __global__ void __launch_bounds__(K2F_NT, 2) k_consensus_f(LatF L) {
         int F = 0;
         for (int w = 0; w < NWARP; ++w) { E += red_e[w]; S += red_s[w]; F |= red_f[w]; }
         if (mode == 0) {
+            if (want_e && epre) E += epre_sum;   // interior part from K1f
             L.pe[k] = E;
             L.pf[k] = F;   // bit 0 any pixel clamped, bit 1 an interior pixel clamped
         } else {           // ring only: the energy partial and the interior clamp memo hold
@@ -830,7 +912,7 @@ struct VarF {
 
 template <int BH, int BW, int NT, int ND>
 static VarF make_varf() {
-    return VarF{BH, BW, NT, ND, K1FCfg<BH, BW, NT, ND>::SMEM, &k_block_mincut_f<BH, BW, NT, ND>};
+    return VarF{BH, BW, NT, ND, K1FCfg<BH, BW, NT, ND>::SMEM + 8 * (size_t)NT, &k_block_mincut_f<BH, BW, NT, ND>};
 }
 
 static const VarF *pick_varf(int conn, int maxh, int maxw, int nblocks) {
@@ -886,6 +968,7 @@ static int build(const dope_lattice_f *L, LatF &o, const VarF **var) {
     o.warm = L->warm_start;
     o.skip_clean = L->skip_clean;
     o.fuse = L->fuse_multipliers;
+    o.epre = L->energy_prepass;
     o.max_iters = L->max_iters;
     o.K = L->kpa[0] * L->kpa[1];
     o.u = L->u;

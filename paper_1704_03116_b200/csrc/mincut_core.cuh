@@ -74,9 +74,16 @@ __device__ __forceinline__ long long k1f_now() {
 #define K1F_D(slot, expr) do { } while (0)
 #endif
 
-template <int BH, int BW, int NT, int NDIR>
+// Work for the warps that wait while warp 0 runs a global-relabel BFS alone:
+// idle(i) is called by every thread of warps 1 .. NT/32 - 1 during the i-th BFS
+// of the solve (i = 0, 1, ...; the same count on every thread).
+struct NoIdle {
+    __device__ __forceinline__ void operator()(int) const {}
+};
+
+template <int BH, int BW, int NT, int NDIR, class Idle = NoIdle>
 __device__ int mincut_solve(int32_t *g, int32_t *rr, uint16_t *h, uint64_t *masks, uint64_t *reach, int *misc,
-                            int sweep_min, int sweep_mul) {
+                            int sweep_min, int sweep_mul, Idle idle = Idle()) {
     using Cf = K1FCfg<BH, BW, NT, NDIR>;
     constexpr int M = Cf::M, NPT = Cf::NPT, NW = Cf::NW;
     uint32_t *masks32 = reinterpret_cast<uint32_t *>(masks);
@@ -108,6 +115,8 @@ __device__ int mincut_solve(int32_t *g, int32_t *rr, uint16_t *h, uint64_t *mask
             int levels = 0;
             const int hit = bfs_relabel_planes<NW, BW, 0, NDIR == 8>(masks, reach, planes, lane, &levels);
             if (lane == 0) { misc[0] = hit; misc[1] = levels; }
+        } else {
+            idle(rounds);
         }
         __syncthreads();
         const int hit = misc[0], levels = misc[1];
