@@ -342,3 +342,26 @@ def test_float_grids_match_oracle_within_tolerance(size, block, iters):
     e = np.array([t.energy for t in state.trace])
     np.testing.assert_allclose(e, ref["energy"], rtol=1e-5)
     assert np.mean(labels != ref["labels"]) <= 1e-4
+
+
+@pytest.mark.parametrize("size,block", [(512, 64), (250, 62)])
+def test_float_energy_prepass_equals_the_consensus_pass_sum(size, block, monkeypatch):
+    """dope_lattice_f.energy_prepass (K1f sums a re-solved block's interior energy
+    while warp 0 runs the relabel BFS) against the consensus pass's own loop:
+    identical labels and iterates, energies equal up to summation order."""
+    from paper_1704_03116_b200 import admm as A
+    wl = W.c2(seed=7, size=size, block=block, iters=16)
+    model, part = _float_model(wl)
+    cfg = dope.AdmmConfig(mu0=wl.rho, mu_fact=1.0, eps=0.0, max_iters=16)
+    runs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("DOPE_F_EPRE", flag)
+        A._forget(A._problems_for(model, part))   # new device state for each setting
+        labels, state = dope.run(model, part, cfg)
+        assert A._problems_for(model, part)._run_dev.L.energy_prepass == int(flag)
+        runs.append((labels, state.labels_global().copy(), np.array(state.y).copy(),
+                     np.array([t.energy for t in state.trace])))
+    assert np.array_equal(runs[0][0], runs[1][0])
+    assert np.array_equal(runs[0][1], runs[1][1])
+    assert np.array_equal(runs[0][2], runs[1][2])
+    np.testing.assert_allclose(runs[0][3], runs[1][3], rtol=1e-12)
