@@ -545,23 +545,39 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
     uint32_t R = 0;
     for (;;) {
         // ---- sink / active rows and initial heights (node-parallel) ----
-        uint32_t ra = 0;
-#pragma unroll 4
-        for (int z = 0; z < B; ++z) {
-            const int v = z * PLANE + tid;
-            const int32_t gv = s3_getg(G2, v);
-            const uint32_t bK = __ballot_sync(FULLMASK, gv < 0);
-            const uint32_t bA = __ballot_sync(FULLMASK, gv > 0);
-            h[v] = gv < 0 ? 0 : HINF;
-            ra |= (bA != 0u ? 1u : 0u) << z;
-            if (lane == 0) {
-                Kb[z * B + warp] = bK;
-                Kb[1024 + z * B + warp] = bA;
+        // eight nodes of a row per thread (one 16-byte load of packed excess, one
+        // 16-byte store of heights; the four lanes of a row OR their mask bytes):
+        // 4 passes instead of 32 ballot passes over the 32768 nodes.  Biased
+        // halves: g < 0 <=> bit 15 clear; g > 0 <=> bit 15 set and low bits != 0.
+        if (tid < 32) { Fp[tid] = 0; Fr[tid] = 0; }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int item = i * NT + tid, rho = item >> 2, qd = item & 3;
+            const int v0 = rho * B + 8 * qd;
+            const uint4 w4 = *reinterpret_cast<const uint4 *>(G2 + (v0 >> 1));
+            const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
+            uint32_t hw[4], neg8 = 0, pos8 = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t w = ws[j];
+                const uint32_t sg = w & 0x80008000u;             // sign bits: g >= 0
+                hw[j] = (sg >> 15) * 0xFFFFu;                    // g < 0 -> 0, else HINF
+                const uint32_t ng = ~w & 0x80008000u;
+                neg8 |= (((ng >> 15) & 1u) | ((ng >> 30) & 2u)) << (2 * j);
+                const uint32_t p0 = ((w >> 15) & 1u) & ((w & 0x7fffu) != 0u ? 1u : 0u);
+                const uint32_t p1 = (w >> 31) & ((w & 0x7fff0000u) != 0u ? 1u : 0u);
+                pos8 |= (p0 | (p1 << 1)) << (2 * j);
             }
-        }
-        if (lane == 0) {
-            Fp[warp] = ra;
-            Fr[warp] = 0;
+            *reinterpret_cast<uint4 *>(h + v0) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            uint32_t bK = neg8 << (8 * qd), bA = pos8 << (8 * qd);
+            bK |= __shfl_xor_sync(FULLMASK, bK, 1);
+            bA |= __shfl_xor_sync(FULLMASK, bA, 1);
+            bK |= __shfl_xor_sync(FULLMASK, bK, 2);
+            bA |= __shfl_xor_sync(FULLMASK, bA, 2);
+            if (qd == 0) {
+                Kb[rho] = bK;            // rho = z * B + y
+                Kb[1024 + rho] = bA;
+            }
         }
         if (tid == 0) { misc[0] = 0; misc[1] = 0; misc[2] = 0; }
         __syncthreads();
@@ -585,6 +601,7 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
         const int64_t t0 = tl ? gtimer() : 0;
         R = Kb[oz * B + oy];
         const uint32_t A = Kb[1024 + oz * B + oy];
+        if (A) atomicOr(&Fp[oy], 1u << oz);   // row (z, y) holds active nodes: push flags of warp y
         const bool have_active = __syncthreads_or(A != 0);
         Rb[oz * B + oy] = R;
         __syncthreads();
