@@ -32,7 +32,8 @@ constexpr size_t OFF_K = OFF_R + 2 * 4 * 1024;             // uint32[2][1024] si
 constexpr size_t OFF_SLOT = OFF_K + 2 * 4 * 1024;           // uint16[32 warps][32] batches
 constexpr size_t OFF_FLAG = OFF_SLOT + 2 * 32 * 32;          // uint32[2][32] row-activity flags
 constexpr size_t OFF_MISC = OFF_FLAG + 2 * 4 * 32;
-constexpr size_t SMEM = OFF_MISC + 64;
+constexpr size_t OFF_CAND = OFF_MISC + 64;                  // uint32[2][1024] push / relabel candidate rows
+constexpr size_t SMEM = OFF_CAND + 2 * 4 * 1024;
 constexpr int UBR = M + 128;                               // int8 u brick: 128-byte header + box
 constexpr int BIAS = 32768;
 constexpr int GMAX = 32000;
@@ -103,13 +104,22 @@ __device__ __forceinline__ int s3_enqueue(uint16_t *slots, uint32_t word, int cn
     return cnt;
 }
 
+// candidate bitmasks of the sweeps: word (y, z) = y * 32 + z holds one bit per x,
+// so warp y reads the words of its 32 rows with one load (lane = z)
+__device__ __forceinline__ void s3_mark(uint32_t *C, int v) {
+    atomicOr(&C[(((v >> 5) & 31) << 5) + (v >> 10)], 1u << (v & 31));
+}
+
 // push the excess of active node v along its admissible arcs (h[w] = h[v]-1),
-// E W S N D U order
+// E W S N D U order; nodes that received excess or kept some become relabel
+// candidates (Cr)
 __device__ __forceinline__ void s3_push(uint32_t *G2, const uint16_t *h, uint32_t *FE, uint32_t *FS,
-                                        uint32_t *FD, uint32_t *Fr, int v, int32_t cap2) {
+                                        uint32_t *FD, uint32_t *Cr, int v, int32_t cap2) {
     using namespace k1s;
     const int32_t e = s3_getg(G2, v);
-    const uint16_t ht = h[v] - 1;
+    const uint16_t hv = h[v];
+    if (e <= 0 || hv == HINF || hv == 0) return;
+    const uint16_t ht = hv - 1;
     const int x = v & (B - 1), y = (v >> 5) & (B - 1), z = v >> 10;
     int32_t left = e;
 #pragma unroll
@@ -132,19 +142,20 @@ __device__ __forceinline__ void s3_push(uint32_t *G2, const uint16_t *h, uint32_
         else if (d == 4) s3_addnib(FD, v, -delta);
         else s3_addnib(FD, w, delta);
         s3_addg(G2, w, delta);
-        atomicOr(&Fr[(w >> 5) & (B - 1)], 1u << (w >> 10));
+        s3_mark(Cr, w);
         left -= delta;
         if (left == 0) break;
     }
     if (left != e) s3_addg(G2, v, -(e - left));
-    if (left) atomicOr(&Fr[y], 1u << z);
+    if (left) s3_mark(Cr, v);
 }
 
 // h[v] = 1 + min height over v's residual arcs (HINF when none or >= M);
 // returns whether v stays below HINF
-__device__ __forceinline__ int s3_relabel(uint16_t *h, const uint32_t *FE, const uint32_t *FS,
-                                          const uint32_t *FD, uint32_t *Fp, int v, int32_t cap2) {
+__device__ __forceinline__ int s3_relabel(const uint32_t *G2, uint16_t *h, const uint32_t *FE, const uint32_t *FS,
+                                          const uint32_t *FD, uint32_t *Cp, int v, int32_t cap2) {
     using namespace k1s;
+    if (s3_getg(G2, v) <= 0 || h[v] == HINF) return 0;   // a candidate without excess (a sink absorbed it)
     const int x = v & (B - 1), y = (v >> 5) & (B - 1), z = v >> 10;
     uint32_t mn = HINF;
     if (s3_nib(FE, v)) mn = min(mn, (uint32_t)h[v + 1]);
@@ -155,7 +166,7 @@ __device__ __forceinline__ int s3_relabel(uint16_t *h, const uint32_t *FE, const
     if (z > 0 && s3_nib(FD, v - PLANE) != cap2) mn = min(mn, (uint32_t)h[v - PLANE]);
     const uint32_t nh = (mn + 1 >= (uint32_t)M) ? HINF : mn + 1;
     if (nh != h[v]) h[v] = (uint16_t)nh;
-    if (nh != HINF) atomicOr(&Fp[y], 1u << z);
+    if (nh != HINF) s3_mark(Cp, v);   // pushes in the next sweep
     return nh != HINF;
 }
 
@@ -186,7 +197,7 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
     uint16_t *slots = reinterpret_cast<uint16_t *>(sm3 + OFF_SLOT) + warp * 32;
     // row-activity flags: word y, bit z <=> row (z, y) may hold a node to push
     // (Fp) / to relabel (Fr); warp w scans the rows of word w
-    uint32_t *Fp = reinterpret_cast<uint32_t *>(sm3 + OFF_FLAG), *Fr = Fp + 32;
+    uint32_t *Cp = reinterpret_cast<uint32_t *>(sm3 + OFF_CAND), *Cr = Cp + 1024;
     int k = blockIdx.x;
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm3 + OFF_MISC + 32);
     if (L.dlist) {   // run loop: CTA i takes entry i of this iteration's dirty-block list
@@ -549,7 +560,6 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
         // 16-byte store of heights; the four lanes of a row OR their mask bytes):
         // 4 passes instead of 32 ballot passes over the 32768 nodes.  Biased
         // halves: g < 0 <=> bit 15 clear; g > 0 <=> bit 15 set and low bits != 0.
-        if (tid < 32) { Fp[tid] = 0; Fr[tid] = 0; }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int item = i * NT + tid, rho = item >> 2, qd = item & 3;
@@ -601,7 +611,6 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
         const int64_t t0 = tl ? gtimer() : 0;
         R = Kb[oz * B + oy];
         const uint32_t A = Kb[1024 + oz * B + oy];
-        if (A) atomicOr(&Fp[oy], 1u << oz);   // row (z, y) holds active nodes: push flags of warp y
         const bool have_active = __syncthreads_or(A != 0);
         Rb[oz * B + oy] = R;
         __syncthreads();
@@ -636,6 +645,9 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
             if (!(f & 1)) break;                  // no growth: BFS complete
             if (have_active && !(f & 2)) break;   // every active node has a height
         }
+        // sweep candidates: C (push from) = the active nodes the BFS reached, N (relabel) empty
+        Cp[oy * B + oz] = A & R;
+        Cr[oy * B + oz] = 0u;
         const int hit = __syncthreads_or((A & R) != 0);
         if (tl) {
             const int64_t t1 = gtimer();
@@ -656,46 +668,41 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
         const int cap_sweeps = T.sweep_min + T.sweep_mul * level;
         for (int sw = 0; sw < cap_sweeps; ++sw) {
             ++sweeps_done;
-            // push: each warp scans its rows (z, warp) and packs the active
-            // nodes into batches of 32, so a lane works on an active node
-            // instead of idling behind one (the active set is sparse after
-            // the first sweeps)
+            // push from C, then relabel N: warp y reads the candidate words of
+            // its 32 rows (lane = z) in one load and packs the set bits into
+            // batches of 32, one node per lane (no per-row scan of h and g)
             int cnt = 0;
-            uint32_t rows = Fp[warp];
-            __syncwarp();
-            if (lane == 0) Fp[warp] = 0;
+            uint32_t cw = Cp[warp * B + lane];
+            if (cw) Cp[warp * B + lane] = 0u;
+            uint32_t rows = __ballot_sync(FULLMASK, cw != 0u);
             while (rows) {
                 const int z = __ffs(rows) - 1;
                 rows &= rows - 1;
-                const int v = z * PLANE + tid;
-                const uint16_t hv = h[v];
-                const bool p = s3_getg(G2, v) > 0 && hv != HINF && hv != 0;
-                cnt = s3_enqueue(slots, __ballot_sync(FULLMASK, p), cnt, lane, v,
-                                 [&](int u) { s3_push(G2, h, FE, FS, FD, Fr, u, cap2); });
+                const uint32_t word = __shfl_sync(FULLMASK, cw, z);
+                cnt = s3_enqueue(slots, word, cnt, lane, z * PLANE + tid,
+                                 [&](int u) { s3_push(G2, h, FE, FS, FD, Cr, u, cap2); });
             }
             if (cnt) {
                 __syncwarp();
-                if (lane < cnt) s3_push(G2, h, FE, FS, FD, Fr, slots[lane], cap2);
+                if (lane < cnt) s3_push(G2, h, FE, FS, FD, Cr, slots[lane], cap2);
                 __syncwarp();
             }
             __syncthreads();
-            // relabel every node that still holds excess
             int act = 0;
             cnt = 0;
-            rows = Fr[warp];
-            __syncwarp();
-            if (lane == 0) Fr[warp] = 0;
+            cw = Cr[warp * B + lane];
+            if (cw) Cr[warp * B + lane] = 0u;
+            rows = __ballot_sync(FULLMASK, cw != 0u);
             while (rows) {
                 const int z = __ffs(rows) - 1;
                 rows &= rows - 1;
-                const int v = z * PLANE + tid;
-                const bool p = s3_getg(G2, v) > 0 && h[v] != HINF;
-                cnt = s3_enqueue(slots, __ballot_sync(FULLMASK, p), cnt, lane, v,
-                                 [&](int u) { act |= s3_relabel(h, FE, FS, FD, Fp, u, cap2); });
+                const uint32_t word = __shfl_sync(FULLMASK, cw, z);
+                cnt = s3_enqueue(slots, word, cnt, lane, z * PLANE + tid,
+                                 [&](int u) { act |= s3_relabel(G2, h, FE, FS, FD, Cp, u, cap2); });
             }
             if (cnt) {
                 __syncwarp();
-                if (lane < cnt) act |= s3_relabel(h, FE, FS, FD, Fp, slots[lane], cap2);
+                if (lane < cnt) act |= s3_relabel(G2, h, FE, FS, FD, Cp, slots[lane], cap2);
                 __syncwarp();
             }
             if (!__syncthreads_or(act)) break;
