@@ -711,11 +711,25 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
     // ---- epilogue: labels (sink side) and the E/S/D residual planes ----
     Rb[oz * B + oy] = R;
     __syncthreads();
+    if (quads && (W & 3) == 0) {
+        // four labels per 32-bit store: thread -> 4 consecutive x of one row,
+        // 128 rows per pass (the quad prologue's mapping)
+        const int x0 = (tid & 7) * 4;
 #pragma unroll 4
-    for (int z = 0; z < B; ++z) {
-        if (!(xin && yin && z < gb.dz)) continue;
-        const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + warp) * W + gb.lo_c + lane;
-        L.yhat[G] = (uint8_t)((Rb[z * B + warp] >> lane) & 1u);
+        for (int p = 0; p < 8; ++p) {
+            const int row = p * 128 + (tid >> 3), z = row >> 5, y = row & 31;
+            if (!(z < gb.dz && y < gb.hr && x0 < gb.wc)) continue;
+            const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + y) * W + gb.lo_c + x0;
+            const uint32_t b = (Rb[z * B + y] >> x0) & 0xFu;
+            *reinterpret_cast<uint32_t *>(L.yhat + G) = (b * 0x00204081u) & 0x01010101u;
+        }
+    } else {
+#pragma unroll 4
+        for (int z = 0; z < B; ++z) {
+            if (!(xin && yin && z < gb.dz)) continue;
+            const int64_t G = ((int64_t)(gb.lo_z + z) * H + gb.lo_r + warp) * W + gb.lo_c + lane;
+            L.yhat[G] = (uint8_t)((Rb[z * B + warp] >> lane) & 1u);
+        }
     }
     if (L.warm && sweeps_done > 0) {   // E/S/D nibble planes back (48 KB; unchanged without a sweep)
 #pragma unroll
