@@ -625,7 +625,9 @@ def main():
         def pstep():
             return dope.run(dope.EnergyModel(u_np, model.weights, wl.lam), part, cfgp)
 
-        for _ in range(max(2, args.warmup)):
+        # the first calls lower the model, capture the graph and register the
+        # host buffers (C5-b16: 1548, 22, 11 ms, then 4.6 ms per call)
+        for _ in range(max(4, args.warmup + 1)):
             pstep()
         torch.cuda.synchronize()
         p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
