@@ -32,8 +32,9 @@ constexpr size_t OFF_K = OFF_R + 2 * 4 * 1024;             // uint32[2][1024] si
 constexpr size_t OFF_SLOT = OFF_K + 2 * 4 * 1024;           // uint16[32 warps][32] batches
 constexpr size_t OFF_FLAG = OFF_SLOT + 2 * 32 * 32;          // uint32[2][32] row-activity flags
 constexpr size_t OFF_MISC = OFF_FLAG + 2 * 4 * 32;
-constexpr size_t OFF_CAND = OFF_MISC + 64;                  // uint32[2][1024] push / relabel candidate rows
-constexpr size_t SMEM = OFF_CAND + 2 * 4 * 1024;
+constexpr size_t OFF_CAND = OFF_MISC + 64;                  // uint32[2][32 * 33] push / relabel candidate rows
+constexpr int CPITCH = 33;                                  // word (y, z) = y * 33 + z: conflict-free by y and by z
+constexpr size_t SMEM = OFF_CAND + 2 * 4 * 32 * CPITCH;
 constexpr int UBR = M + 128;                               // int8 u brick: 128-byte header + box
 constexpr int BIAS = 32768;
 constexpr int GMAX = 32000;
@@ -104,10 +105,11 @@ __device__ __forceinline__ int s3_enqueue(uint16_t *slots, uint32_t word, int cn
     return cnt;
 }
 
-// candidate bitmasks of the sweeps: word (y, z) = y * 32 + z holds one bit per x,
-// so warp y reads the words of its 32 rows with one load (lane = z)
+// candidate bitmasks of the sweeps: word (y, z) = y * CPITCH + z holds one bit per
+// x, so warp y reads the words of its 32 rows with one load (lane = z) and the
+// BFS owners (warp z, lane y) store theirs without bank conflicts
 __device__ __forceinline__ void s3_mark(uint32_t *C, int v) {
-    atomicOr(&C[(((v >> 5) & 31) << 5) + (v >> 10)], 1u << (v & 31));
+    atomicOr(&C[((v >> 5) & 31) * k1s::CPITCH + (v >> 10)], 1u << (v & 31));
 }
 
 // push the excess of active node v along its admissible arcs (h[w] = h[v]-1),
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
     uint16_t *slots = reinterpret_cast<uint16_t *>(sm3 + OFF_SLOT) + warp * 32;
     // row-activity flags: word y, bit z <=> row (z, y) may hold a node to push
     // (Fp) / to relabel (Fr); warp w scans the rows of word w
-    uint32_t *Cp = reinterpret_cast<uint32_t *>(sm3 + OFF_CAND), *Cr = Cp + 1024;
+    uint32_t *Cp = reinterpret_cast<uint32_t *>(sm3 + OFF_CAND), *Cr = Cp + 32 * CPITCH;
     int k = blockIdx.x;
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm3 + OFF_MISC + 32);
     if (L.dlist) {   // run loop: CTA i takes entry i of this iteration's dirty-block list
@@ -646,8 +648,8 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
             if (have_active && !(f & 2)) break;   // every active node has a height
         }
         // sweep candidates: C (push from) = the active nodes the BFS reached, N (relabel) empty
-        Cp[oy * B + oz] = A & R;
-        Cr[oy * B + oz] = 0u;
+        Cp[oy * CPITCH + oz] = A & R;
+        Cr[oy * CPITCH + oz] = 0u;
         const int hit = __syncthreads_or((A & R) != 0);
         if (tl) {
             const int64_t t1 = gtimer();
@@ -672,8 +674,8 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
             // its 32 rows (lane = z) in one load and packs the set bits into
             // batches of 32, one node per lane (no per-row scan of h and g)
             int cnt = 0;
-            uint32_t cw = Cp[warp * B + lane];
-            if (cw) Cp[warp * B + lane] = 0u;
+            uint32_t cw = Cp[warp * CPITCH + lane];
+            if (cw) Cp[warp * CPITCH + lane] = 0u;
             uint32_t rows = __ballot_sync(FULLMASK, cw != 0u);
             while (rows) {
                 const int z = __ffs(rows) - 1;
@@ -690,8 +692,8 @@ __global__ void __launch_bounds__(k1s::NT, 1) k_block_mincut3d_s(Lat2 L, K1Tune 
             __syncthreads();
             int act = 0;
             cnt = 0;
-            cw = Cr[warp * B + lane];
-            if (cw) Cr[warp * B + lane] = 0u;
+            cw = Cr[warp * CPITCH + lane];
+            if (cw) Cr[warp * CPITCH + lane] = 0u;
             rows = __ballot_sync(FULLMASK, cw != 0u);
             while (rows) {
                 const int z = __ffs(rows) - 1;
