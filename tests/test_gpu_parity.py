@@ -365,3 +365,24 @@ def test_float_energy_prepass_equals_the_consensus_pass_sum(size, block, monkeyp
     assert np.array_equal(runs[0][1], runs[1][1])
     assert np.array_equal(runs[0][2], runs[1][2])
     np.testing.assert_allclose(runs[0][3], runs[1][3], rtol=1e-12)
+
+
+def test_float_run_variants_agree_with_energy_prepass():
+    """Float path with the K1f energy prepass: eager vs graph launches, cold vs
+    warm solves and clean-block skipping on / off give the same labels, iterates
+    and (up to summation order) energies."""
+    wl = W.c2(seed=9, size=256, block=64, iters=14)
+    model, part = _float_model(wl)
+    base = None
+    for kw in ({}, {"use_graph": False}, {"warm_start": False}, {"skip_clean": False}):
+        cfg = dope.AdmmConfig(mu0=wl.rho, mu_fact=1.0, eps=0.0, max_iters=14, **kw)
+        labels, state = dope.run(model, part, cfg)
+        got = (labels, state.labels_global().copy(), np.array(state.y).copy(),
+               np.array([t.energy for t in state.trace]))
+        if base is None:
+            base = got
+            continue
+        assert np.array_equal(got[0], base[0]), kw
+        assert np.array_equal(got[1], base[1]), kw
+        assert np.array_equal(got[2], base[2]), kw
+        np.testing.assert_allclose(got[3], base[3], rtol=1e-12, err_msg=str(kw))
